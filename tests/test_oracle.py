@@ -1,0 +1,85 @@
+"""Pin the CPU oracle (oracle/) against the reference-generated golden fixtures.
+
+These are CPU tests: the oracle must reproduce every SimReport (floats
+included), every per-layer decision hash and, where recorded, every decision
+of the reference simulator on the same traces.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from golden_util import COSTS, GOLDEN, case_trace, include_prefill, load, policy_name
+
+
+def _check_case(case, check_decisions=True):
+    header, events = case_trace(case)
+    L, E, K = header
+    for run in case["runs"]:
+        nets = oracle.nets_from_spec(run["nets"], L, E, GOLDEN)
+        pol = policy_name(run["policy"])
+        report, hashes, outs = oracle.simulate(
+            header, events, pol, run["capacity"], COSTS[run["cost"]], run["window"],
+            nets if pol == "ml" else None, include_prefill(run["policy"]),
+            want_outcomes=check_decisions and "decisions" in run)
+        assert report == run["report"], (case["name"], run["policy"], run["capacity"])
+        assert [format(h, "016x") for h in hashes] == run["hashes"], (case["name"], run["policy"])
+        if outs is not None:
+            assert [o.tolist() for o in outs] == run["decisions"]
+
+
+@pytest.mark.parametrize("idx", range(0, 167, 1))
+def test_oracle_small_cases(idx):
+    cases = load("small_cases.json.gz")["cases"]
+    if idx >= len(cases):
+        pytest.skip("fewer cases")
+    _check_case(cases[idx])
+
+
+def test_oracle_zipf_and_dominance_cases():
+    for case in load("zipf_cases.json.gz")["cases"]:
+        _check_case(case, check_decisions=False)
+
+
+def test_oracle_c1_and_mixtral_full_size():
+    if not os.path.exists(os.path.join(GOLDEN, "big_cases.json.gz")):
+        pytest.skip("big fixtures not generated")
+    for case in load("big_cases.json.gz")["cases"]:
+        _check_case(case, check_decisions=False)
+
+
+def test_oracle_efficacy_golden():
+    """Trained net (reference train_eviction_net) on 10 held-out traces:
+    ml 82.90% / lru 81.30% / lfu 79.78% (pkg/test_output.txt:360)."""
+    path = os.path.join(GOLDEN, "efficacy_cases.json.gz")
+    if not os.path.exists(path):
+        pytest.skip("efficacy fixtures not generated")
+    g = load("efficacy_cases.json.gz")
+    rates = {"ml": [], "lru": [], "lfu": []}
+    for case in g["cases"]:
+        _check_case(case, check_decisions=False)
+        for run in case["runs"]:
+            rates[policy_name(run["policy"])].append(run["report"]["hit_rate"])
+    means = {p: round(100 * float(np.mean(v)), 2) for p, v in rates.items()}
+    assert means == {"ml": 82.90, "lru": 81.30, "lfu": 79.78}
+
+
+def test_uniform_batch_matches_simulate():
+    """The multi-threaded decode-only batch driver (CPU baseline) agrees with
+    the per-trace path on the Mixtral-shaped golden trace."""
+    path = os.path.join(GOLDEN, "big_cases.json.gz")
+    if not os.path.exists(path):
+        pytest.skip("big fixtures not generated")
+    case = load("big_cases.json.gz")["cases"][1]
+    from golden_util import big_ids
+    ids, E = big_ids(case)
+    T, L, K = ids.shape
+    chains = np.ascontiguousarray(ids.transpose(1, 0, 2))
+    jobs = [(policy_name(r["policy"]), r["capacity"]) for r in case["runs"]]
+    nets = oracle.nets_from_spec({"kind": "per_layer_seed"}, L, E)
+    cnt, lat, hsh = oracle.replay_uniform(chains, L, E, jobs, COSTS["default"], 5, nets, threads=4)
+    for j, run in enumerate(case["runs"]):
+        rep = oracle.fold_report(jobs[j][0], jobs[j][1], 5, cnt[:, j], lat[:, j], T)
+        assert rep == run["report"]
+        assert [format(int(h), "016x") for h in hsh[:, j]] == run["hashes"]
