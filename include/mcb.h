@@ -1,0 +1,220 @@
+/*
+ * mcb.h -- C ABI of the B200 expert-cache replay engine (libmcb.so).
+ *
+ * The reference (FlashMoE simulation lab, moecache 0.1.0) is pure Python;
+ * its hot path is reached through engine.run_simulation / simulate / sweep
+ * (pkg/src/moecache/engine.py:300-391, 439-465).  The per-access
+ * CachePolicy.access protocol (policies.py:95-113) is far too fine-grained
+ * to cross an FFI, so this ABI sits at run_simulation/sweep granularity: one
+ * call replays a packed trace under a policy list x capacity list and
+ * returns the per-(trace, policy, capacity) counters from which SimReport
+ * (engine.py:95-122) is assembled.  The binding a maintainer would add on the
+ * reference side is a ctypes stub; see INTEGRATION.md.
+ *
+ * Conventions: extern "C", plain pointers and sizes, no exceptions cross the
+ * boundary; every entry point returns an mcb_status and records a message
+ * retrievable with mcb_last_error() (thread-local).  Device entry points take
+ * device pointers and a cudaStream_t passed as void*; they enqueue work and
+ * do not synchronise.  Host entry points take host pointers, copy in, run and
+ * copy out (synchronously).  The caller owns every buffer it passes; the
+ * context owns only its device scratch.
+ *
+ * Supported: num_experts <= 128, top_k <= num_experts, chains of < 2^32
+ * accesses, policies LRU / LFU / Belady / ML (the north star's four).  FIFO,
+ * ARC and LeCaR (policies.py:152-168, 217-395) are rejected with
+ * MCB_ERR_UNSUPPORTED rather than falling back to a CPU path.
+ */
+#ifndef MCB_H_
+#define MCB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCB_ABI_VERSION 1
+
+/* ---- status codes (mapped by the Python shim onto the reference's exceptions) ---- */
+typedef enum {
+    MCB_OK = 0,
+    MCB_ERR_INVALID = 1,       /* InvalidConfigError (trace.py:23) / SimulationError (engine.py:30) */
+    MCB_ERR_CAPACITY = 2,      /* CapacityTooSmallError (engine.py:34, 312-316, 449-453) */
+    MCB_ERR_NO_EVICTABLE = 3,  /* NoEvictableError (policies.py:24, mlpolicy.py:24-25) */
+    MCB_ERR_CUDA = 4,          /* CUDA runtime failure */
+    MCB_ERR_UNSUPPORTED = 5,   /* policy / shape outside the B200 engine */
+    MCB_ERR_NOMEM = 6,
+    MCB_ERR_SHAPE = 7          /* ValueError: net E mismatch (mlpolicy.py:47-50) */
+} mcb_status;
+
+/* ---- policies (engine.py:150 names) ---- */
+typedef enum {
+    MCB_LRU = 0,               /* policies.py:132-149 */
+    MCB_LFU = 1,               /* policies.py:171-197 */
+    MCB_BELADY = 2,            /* policies.py:200-214 */
+    MCB_ML = 3,                /* mlpolicy.py:33-65, include_prefill=True */
+    MCB_ML_NO_PREFILL = 4      /* mlpolicy.py, {"name": "ml", "include_prefill": False} */
+} mcb_policy;
+
+/* ---- per-(trace, policy, capacity) report slots ---- */
+enum {
+    MCB_R_PREFILL_HITS = 0,
+    MCB_R_PREFILL_MISSES = 1,
+    MCB_R_DECODE_HITS = 2,
+    MCB_R_DECODE_MISSES = 3,
+    MCB_R_COMPULSORY = 4,
+    MCB_R_EVICTIONS = 5,
+    MCB_R_REFETCHED = 6,       /* numerator of refetch_within_w (engine.py:266-297) */
+    MCB_R_STATUS = 7,          /* mcb_status of this cell (NO_EVICTABLE possible for ML) */
+    MCB_R_N = 8
+};
+
+/* outcome codes written per access when outcomes are requested */
+#define MCB_OUT_HIT 0xFFFFu
+#define MCB_OUT_MISS 0xFFFEu   /* miss without eviction; otherwise the victim id */
+
+/*
+ * Packed trace.  A trace unrolls into one access stream per layer
+ * (replay.py:44-81); a "chain" is one (trace, layer) stream, chain index
+ * c = trace * num_layers + layer.  Streams are stored chain-major so a chain
+ * is contiguous in HBM.
+ *
+ * uniform = 1: decode-only, one sequence per trace, every chain has
+ *   events_per_chain events of top_k accesses; acc[c][t][k] (uint8).  The
+ *   chain_* / ev_info / routed pointers are ignored.
+ * uniform = 0: general (prefill + several sequences):
+ *   chain_acc_off[c]..[c+1]  accesses of chain c in acc (after prefill
+ *                            load-once dedup, replay.py:54-71)
+ *   chain_ev_off[c]..[c+1]   events of chain c in ev_info
+ *   chain_rt_off[c]..[c+1]   routed ids of chain c in routed (the full stored
+ *                            expert list; feature updates use it)
+ *   ev_info[e] = n_acc | n_routed << 9 | is_decode << 30 | new_sequence << 31
+ */
+typedef struct {
+    int32_t num_layers;
+    int32_t num_experts;
+    int32_t top_k;
+    int32_t num_traces;
+    int32_t uniform;
+    int32_t reserved;
+    int64_t events_per_chain;          /* uniform only */
+    int64_t total_acc;                 /* general only: chain_acc_off[n_chains] */
+    int64_t total_events;              /* general only: chain_ev_off[n_chains] */
+    const uint8_t *acc;                /* readable up to round_up(total, 128) bytes */
+    const int64_t *chain_acc_off;      /* [n_chains + 1] */
+    const int64_t *chain_ev_off;       /* [n_chains + 1] */
+    const int64_t *chain_rt_off;       /* [n_chains + 1] */
+    const uint32_t *ev_info;           /* [n_events] */
+    const uint8_t *routed;             /* [n_routed] */
+} mcb_trace;
+
+/* CostModel (engine.py:38-55) */
+typedef struct {
+    double t_load_s;
+    double t_compute_s;
+    double ml_score_cost_s;
+    int32_t loads_serial;
+    int32_t window;                    /* refetch window w (engine.py:266-297) */
+} mcb_cost;
+
+/*
+ * EvictionNet parameters (net.py:61-86), float64, in .evnet order
+ * (net.py:282-305): per net w1[H][2E] b1[H] w2[H][H] b2[H] w3[E][H] b3[E].
+ * num_nets = 1 (one shared net) or num_layers (net for layer l at index l).
+ */
+typedef struct {
+    int32_t num_experts;
+    int32_t hidden;
+    int32_t num_nets;
+    int32_t reserved;
+    const double *params;
+} mcb_nets;
+
+/*
+ * Outputs.  reports[trace][pol][cap][MCB_R_N] int64 and
+ * latency[trace][pol][cap][2] float64 (decode, prefill) are summed over
+ * layers in layer order exactly like engine.py:330-343 (float64, no FMA).
+ * Optional (NULL to skip): chain_reports[c][pol][cap][MCB_R_N],
+ * hashes[c][pol][cap] (FNV-1a 64 over the u16 outcome codes of the chain),
+ * outcomes[pol][cap][total_acc] u16 (record_decisions, small traces).
+ */
+typedef struct {
+    int64_t *reports;
+    double *latency;
+    int64_t *chain_reports;
+    uint64_t *hashes;
+    uint16_t *outcomes;
+} mcb_outputs;
+
+typedef struct mcb_ctx mcb_ctx;
+
+/* ---- lifecycle / errors ---- */
+int mcb_abi_version(void);
+int mcb_ctx_create(int device, mcb_ctx **out);
+int mcb_ctx_destroy(mcb_ctx *ctx);
+int mcb_last_error(char *buf, size_t n);
+/* Launch statistics of the last mcb_replay on this context: number of kernels
+ * launched, and the uncertain-rank counter of the ML scorer (events whose
+ * float64 scores had two values closer than 1e-12 relative). */
+int mcb_last_stats(mcb_ctx *ctx, int64_t *kernels_launched, int64_t *uncertain_events);
+
+/* ---- host-side trace validation + packing (trace.py:57-141, replay.py:44-81) ----
+ * Input: one trace as flat events in stored order: seq_id, phase (0 prefill,
+ * 1 decode), step, layer, CSR experts.  Validates exactly what
+ * RoutingTrace.validate() checks (MCB_ERR_INVALID + message on failure) and
+ * produces an owned packed trace (uniform layout when the trace is
+ * decode-only with one sequence). */
+typedef struct mcb_packed mcb_packed;
+int mcb_pack_trace(int32_t num_layers, int32_t num_experts, int32_t top_k, int64_t num_events,
+                   const int64_t *seq_id, const uint8_t *phase, const int64_t *step,
+                   const int32_t *layer, const int64_t *expert_off, const int32_t *experts,
+                   mcb_packed **out);
+/* Host view of a packed trace, sizes, and num_decode_steps() (trace.py:139-141). */
+int mcb_packed_view(const mcb_packed *p, mcb_trace *view, int64_t *total_acc, int64_t *total_events,
+                    int64_t *total_routed, int64_t *num_decode_steps);
+/* Per-access (tick, decode_index) of chain c (for EvictionRecord assembly). */
+int mcb_packed_positions(const mcb_packed *p, int64_t chain, int64_t *tick, int64_t *decode_index);
+int mcb_packed_free(mcb_packed *p);
+
+/* ---- the hot path ----
+ * Replays every chain of `trace` under every policy in `policies` and every
+ * capacity in `capacities` (engine.py:439-465 cross product).  Belady
+ * next-use positions (K2) and ML ranks (K3) are computed once per chain and
+ * shared by every capacity.  `nets` may be NULL when no ML policy is listed.
+ * mcb_replay: device pointers, asynchronous on `stream`.
+ * mcb_replay_host: host pointers (pinned or pageable), synchronous; the
+ * host<->device copies are part of the call. */
+int mcb_replay(mcb_ctx *ctx, const mcb_trace *trace, const int32_t *policies, int32_t n_policies,
+               const int32_t *capacities, int32_t n_capacities, const mcb_cost *cost,
+               const mcb_nets *nets, const mcb_outputs *out, void *stream);
+int mcb_replay_host(mcb_ctx *ctx, const mcb_trace *trace, const int32_t *policies,
+                    int32_t n_policies, const int32_t *capacities, int32_t n_capacities,
+                    const mcb_cost *cost, const mcb_nets *nets, const mcb_outputs *out);
+
+/* ---- individual kernels (exposed for tests and benchmarks) ---- */
+/* K2: next_pos[i] = chain-relative position of the next access of the same
+ * expert after access i of its chain, 0xFFFFFFFF if none
+ * (OracleIndex.next_use, policies.py:65-76).  Device pointers. */
+int mcb_next_use(mcb_ctx *ctx, const mcb_trace *trace, uint32_t *next_pos, void *stream);
+/* K3: per event, rank[e] in 0..E of expert e's float64 score
+ * (0 = never selectable: NaN or -inf, mlpolicy.py:15-26); optional float64
+ * scores[event][E].  Device pointers. */
+int mcb_score(mcb_ctx *ctx, const mcb_trace *trace, const mcb_nets *nets, int32_t include_prefill,
+              uint8_t *ranks, double *scores, void *stream);
+
+/* ---- K1: router-logits GEMM + top-k trace generator (tcgen05 / TMA) ----
+ * hidden[T][d] bf16 (shared by all layers), weight[L*E][d] bf16 (router
+ * gate rows of every layer, layer-major).  Writes acc[l][t][k] (uint8,
+ * chain-major uniform layout for trace 0) with the K largest logits of
+ * layer l per token, sorted descending, ties to the lower expert id
+ * (torch.topk semantics used by the HF routers the extractor hooks,
+ * extractor.py:162-183).  Optional fp32 logits[t][L*E].  Device pointers. */
+int mcb_router_topk(mcb_ctx *ctx, const void *hidden_bf16, const void *weight_bf16, int64_t T,
+                    int32_t d, int32_t num_layers, int32_t num_experts, int32_t top_k,
+                    uint8_t *acc, float *logits, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCB_H_ */

@@ -1,0 +1,41 @@
+"""B200-native expert-cache replay engine (FlashMoE, arXiv 2601.17063).
+
+Drop-in for the reference simulator's hot path (moecache: simulate /
+run_simulation / sweep / policy_factory -> SimReport), backed by hand-written
+sm_100a CUDA kernels behind the C ABI of include/mcb.h (libmcb.so).
+"""
+from .engine import (
+    POLICY_NAMES,
+    CapacityTooSmallError,
+    CostModel,
+    EvictionRecord,
+    HardwareBudget,
+    SimReport,
+    SimRun,
+    SimulationError,
+    cache_size_calc,
+    policy_factory,
+    refetch_rate,
+    run_simulation,
+    simulate,
+    step_latency_s,
+    sweep,
+)
+from .net import EvictionNet, NetError, ShapeMismatchError, load_net, save_net
+from .policies import NoEvictableError, PolicyDecision, PolicyError
+from .trace import (
+    AccessEvent,
+    HeaderMismatchError,
+    InsufficientTokensError,
+    InvalidConfigError,
+    PackedTrace,
+    Phase,
+    RoutingTrace,
+    TraceError,
+    TraceHeader,
+    TraceParseError,
+    pack_trace,
+    packed_from_decode_ids,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,389 @@
+// C ABI of libmcb.so (include/mcb.h): context, scratch, orchestration of the
+// K2 -> K3 -> K4 -> K5 pipeline, and the host-buffer entry point.
+//
+// mcb_replay mirrors engine.sweep (pkg/src/moecache/engine.py:439-465) over
+// the policies x capacities cross product for every trace of a packed batch;
+// the per-cell arithmetic is engine.run_simulation (engine.py:300-380).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "mcb_internal.h"
+#include "mcb_kernels.cuh"
+
+// ---------------------------------------------------------------- errors ---
+static thread_local std::string g_err;
+
+int mcb_set_error(int code, const char *msg) {
+    g_err = msg ? msg : "";
+    return code;
+}
+void mcb_clear_error() { g_err.clear(); }
+
+extern "C" int mcb_last_error(char *buf, size_t n) {
+    if (!buf || n == 0) return (int)g_err.size();
+    const size_t k = g_err.size() < n - 1 ? g_err.size() : n - 1;
+    memcpy(buf, g_err.data(), k);
+    buf[k] = 0;
+    return (int)g_err.size();
+}
+
+extern "C" int mcb_abi_version(void) { return MCB_ABI_VERSION; }
+
+#define CUDA_TRY(expr)                                                                             \
+    do {                                                                                           \
+        cudaError_t e_ = (expr);                                                                   \
+        if (e_ != cudaSuccess) {                                                                   \
+            char b_[256];                                                                          \
+            snprintf(b_, sizeof b_, "CUDA error %s at %s:%d: %s", cudaGetErrorName(e_), __FILE__, \
+                     __LINE__, cudaGetErrorString(e_));                                            \
+            return mcb_set_error(MCB_ERR_CUDA, b_);                                                \
+        }                                                                                          \
+    } while (0)
+
+// ---------------------------------------------------------------- context --
+struct DevBuf {
+    void *p = nullptr;
+    size_t n = 0;
+    int ensure(size_t bytes) {
+        if (bytes <= n) return MCB_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        const size_t want = bytes + bytes / 8 + 256;
+        if (cudaMalloc(&p, want) != cudaSuccess) {
+            cudaGetLastError();
+            return mcb_set_error(MCB_ERR_NOMEM, "device scratch allocation failed");
+        }
+        n = want;
+        return MCB_OK;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+struct mcb_ctx {
+    int device = 0;
+    std::mutex mu;
+    DevBuf next_pos, ranks[2], inst_out, inst_lat, wt, snaps, tile_off, stats, pol_caps;
+    // host path staging
+    DevBuf h_acc, h_acc_off, h_ev_off, h_rt_off, h_ev_info, h_routed, h_params, h_reports, h_latency,
+        h_chain_reports, h_hashes, h_outcomes;
+    cudaStream_t stream = nullptr;
+    int64_t last_kernels = 0;
+    int64_t last_uncertain = 0;
+};
+
+extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
+    mcb_clear_error();
+    if (!out) return mcb_set_error(MCB_ERR_INVALID, "out is NULL");
+    int n = 0;
+    CUDA_TRY(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) return mcb_set_error(MCB_ERR_INVALID, "no such CUDA device");
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        return mcb_set_error(MCB_ERR_UNSUPPORTED, "libmcb is built for sm_100a (B200); device is older");
+    auto *c = new (std::nothrow) mcb_ctx();
+    if (!c) return mcb_set_error(MCB_ERR_NOMEM, "out of host memory");
+    c->device = device;
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return mcb_set_error(MCB_ERR_CUDA, "stream creation failed");
+    }
+    *out = c;
+    return MCB_OK;
+}
+
+extern "C" int mcb_ctx_destroy(mcb_ctx *c) {
+    if (!c) return MCB_OK;
+    cudaSetDevice(c->device);
+    DevBuf *all[] = {&c->next_pos, &c->ranks[0], &c->ranks[1], &c->inst_out, &c->inst_lat, &c->wt, &c->snaps,
+                     &c->tile_off, &c->stats, &c->pol_caps, &c->h_acc, &c->h_acc_off, &c->h_ev_off,
+                     &c->h_rt_off, &c->h_ev_info, &c->h_routed, &c->h_params, &c->h_reports, &c->h_latency,
+                     &c->h_chain_reports, &c->h_hashes, &c->h_outcomes};
+    for (DevBuf *b : all) b->release();
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return MCB_OK;
+}
+
+extern "C" int mcb_last_stats(mcb_ctx *c, int64_t *kernels, int64_t *uncertain) {
+    if (!c) return mcb_set_error(MCB_ERR_INVALID, "ctx is NULL");
+    if (kernels) *kernels = c->last_kernels;
+    if (uncertain) *uncertain = c->last_uncertain;
+    return MCB_OK;
+}
+
+// ------------------------------------------------------------ validation --
+static int check_trace(const mcb_trace *t) {
+    if (!t) return mcb_set_error(MCB_ERR_INVALID, "trace is NULL");
+    if (t->num_layers < 1 || t->num_experts < 1 || t->top_k < 1 || t->top_k > t->num_experts ||
+        t->num_traces < 0)
+        return mcb_set_error(MCB_ERR_INVALID, "invalid trace header");
+    if (t->num_experts > MCB_MAX_EXPERTS)
+        return mcb_set_error(MCB_ERR_UNSUPPORTED, "num_experts > 128 is not supported by the B200 engine");
+    if (!t->acc) return mcb_set_error(MCB_ERR_INVALID, "trace.acc is NULL");
+    if (!t->uniform && (!t->chain_acc_off || !t->chain_ev_off || !t->chain_rt_off || !t->ev_info || !t->routed))
+        return mcb_set_error(MCB_ERR_INVALID, "general-mode trace needs chain offsets, ev_info and routed");
+    if (t->uniform && t->events_per_chain < 0) return mcb_set_error(MCB_ERR_INVALID, "events_per_chain < 0");
+    return MCB_OK;
+}
+
+static DevTrace make_dev_trace(const mcb_trace *t) {
+    DevTrace d;
+    d.L = t->num_layers;
+    d.E = t->num_experts;
+    d.K = t->top_k;
+    d.uniform = t->uniform;
+    d.T = t->events_per_chain;
+    d.n_chains = (int64_t)t->num_layers * t->num_traces;
+    d.total_acc = t->uniform ? d.n_chains * d.T * d.K : t->total_acc;
+    d.total_events = t->uniform ? d.n_chains * d.T : t->total_events;
+    d.acc = t->acc;
+    d.acc_off = t->chain_acc_off;
+    d.ev_off = t->chain_ev_off;
+    d.rt_off = t->chain_rt_off;
+    d.ev_info = t->ev_info;
+    d.routed = t->routed;
+    return d;
+}
+
+static int64_t max_score_tiles(const DevTrace &d) {
+    if (d.uniform) return d.n_chains * ((d.T + MCB_TILE_EV - 1) / MCB_TILE_EV);
+    return d.total_events / MCB_TILE_EV + d.n_chains;  // upper bound of sum(ceil(n_c / TILE))
+}
+
+static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int include_prefill, uint8_t *ranks,
+                     double *scores, cudaStream_t s, int64_t *launched) {
+    const int E = d.E, H = nets->hidden;
+    if (nets->num_experts != E) return mcb_set_error(MCB_ERR_SHAPE, "net num_experts does not match the trace");
+    if (H < 1 || H > 256) return mcb_set_error(MCB_ERR_UNSUPPORTED, "net hidden size must be in [1, 256]");
+    if (nets->num_nets != 1 && nets->num_nets != d.L)
+        return mcb_set_error(MCB_ERR_INVALID, "num_nets must be 1 or num_layers");
+    if (!nets->params) return mcb_set_error(MCB_ERR_INVALID, "nets.params is NULL");
+    const size_t per = prepared_net_doubles(E, H);
+    if (int rc = c->wt.ensure(per * nets->num_nets * sizeof(double))) return rc;
+    *launched += launch_prepare_nets(nets->params, E, H, nets->num_nets, (double *)c->wt.p, s);
+    const int64_t tiles = max_score_tiles(d);
+    if (int rc = c->snaps.ensure((size_t)(tiles + 1) * (2 * E + 4) * sizeof(int32_t))) return rc;
+    if (int rc = c->tile_off.ensure((size_t)(d.n_chains + 1) * sizeof(int64_t))) return rc;
+    const int n = launch_score(d, (const double *)c->wt.p, H, nets->num_nets, include_prefill, ranks, scores,
+                               (int32_t *)c->snaps.p, (int64_t *)c->tile_off.p, tiles,
+                               (unsigned long long *)c->stats.p, s);
+    *launched += n;
+    return MCB_OK;
+}
+
+extern "C" int mcb_next_use(mcb_ctx *c, const mcb_trace *t, uint32_t *next_pos, void *stream) {
+    mcb_clear_error();
+    if (!c) return mcb_set_error(MCB_ERR_INVALID, "ctx is NULL");
+    if (int rc = check_trace(t)) return rc;
+    if (!next_pos) return mcb_set_error(MCB_ERR_INVALID, "next_pos is NULL");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CUDA_TRY(cudaSetDevice(c->device));
+    const DevTrace d = make_dev_trace(t);
+    launch_next_use(d, next_pos, (cudaStream_t)stream);
+    CUDA_TRY(cudaGetLastError());
+    return MCB_OK;
+}
+
+extern "C" int mcb_score(mcb_ctx *c, const mcb_trace *t, const mcb_nets *nets, int32_t include_prefill,
+                         uint8_t *ranks, double *scores, void *stream) {
+    mcb_clear_error();
+    if (!c) return mcb_set_error(MCB_ERR_INVALID, "ctx is NULL");
+    if (int rc = check_trace(t)) return rc;
+    if (!nets || !ranks) return mcb_set_error(MCB_ERR_INVALID, "nets / ranks is NULL");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (int rc = c->stats.ensure(64)) return rc;
+    CUDA_TRY(cudaMemsetAsync(c->stats.p, 0, 64, s));
+    const DevTrace d = make_dev_trace(t);
+    int64_t launched = 0;
+    if (int rc = run_score(c, d, nets, include_prefill, ranks, scores, s, &launched)) return rc;
+    CUDA_TRY(cudaGetLastError());
+    return MCB_OK;
+}
+
+static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, int32_t n_pol, const int32_t *caps,
+                         int32_t n_cap, const mcb_cost *cost, const mcb_nets *nets, const mcb_outputs *out,
+                         cudaStream_t s) {
+    if (int rc = check_trace(t)) return rc;
+    if (!pols || !caps || !cost || !out || !out->reports || !out->latency)
+        return mcb_set_error(MCB_ERR_INVALID, "NULL policies / capacities / cost / outputs");
+    if (n_pol < 1 || n_pol > MCB_MAX_POL) return mcb_set_error(MCB_ERR_UNSUPPORTED, "1..8 policies per call");
+    if (n_cap < 1 || n_cap > MCB_MAX_CAP) return mcb_set_error(MCB_ERR_UNSUPPORTED, "1..64 capacities per call");
+    // CostModel.validate (engine.py:51-55)
+    if (!(cost->t_load_s > 0) || !(cost->t_compute_s > 0))
+        return mcb_set_error(MCB_ERR_INVALID, "cost durations must be positive");
+    if (!(cost->ml_score_cost_s >= 0)) return mcb_set_error(MCB_ERR_INVALID, "ml_score_cost_s must be >= 0");
+    // capacity >= top_k (engine.py:312-316, 449-453)
+    for (int i = 0; i < n_cap; ++i)
+        if (caps[i] < t->top_k) {
+            char b[128];
+            snprintf(b, sizeof b, "capacity %d < top_k %d: a decode event cannot fit in the cache", caps[i], t->top_k);
+            return mcb_set_error(MCB_ERR_CAPACITY, b);
+        }
+    bool need_next = false, need_ml[2] = {false, false};
+    for (int i = 0; i < n_pol; ++i) {
+        switch (pols[i]) {
+            case MCB_LRU: case MCB_LFU: break;
+            case MCB_BELADY: need_next = true; break;
+            case MCB_ML: need_ml[0] = true; break;
+            case MCB_ML_NO_PREFILL: need_ml[1] = true; break;
+            default: return mcb_set_error(MCB_ERR_UNSUPPORTED, "policy not supported by the B200 engine");
+        }
+    }
+    if ((need_ml[0] || need_ml[1]) && (!nets || !nets->params))
+        return mcb_set_error(MCB_ERR_INVALID, "ml policy requires trained eviction nets");
+
+    const DevTrace d = make_dev_trace(t);
+    int64_t launched = 0;
+    if (int rc = c->stats.ensure(64)) return rc;
+    CUDA_TRY(cudaMemsetAsync(c->stats.p, 0, 64, s));
+
+    ReplayParams P;
+    memset(&P, 0, sizeof P);
+    P.tr = d;
+    P.n_pol = n_pol;
+    P.n_cap = n_cap;
+    for (int i = 0; i < n_pol; ++i) P.pol[i] = pols[i];
+    for (int i = 0; i < n_cap; ++i) P.cap[i] = caps[i];
+    P.t_load = cost->t_load_s;
+    P.t_compute = cost->t_compute_s;
+    P.ml_cost = cost->ml_score_cost_s;
+    P.loads_serial = cost->loads_serial;
+    P.window = cost->window;
+
+    if (need_next) {
+        if (int rc = c->next_pos.ensure((size_t)(d.total_acc + 64) * sizeof(uint32_t))) return rc;
+        launched += launch_next_use(d, (uint32_t *)c->next_pos.p, s);
+        P.next_pos = (const uint32_t *)c->next_pos.p;
+    }
+    for (int v = 0; v < 2; ++v) {
+        if (!need_ml[v]) continue;
+        if (int rc = c->ranks[v].ensure((size_t)d.total_events * d.E + 64)) return rc;
+        if (int rc = run_score(c, d, nets, v == 0 ? 1 : 0, (uint8_t *)c->ranks[v].p, nullptr, s, &launched))
+            return rc;
+        P.rank[v] = (const uint8_t *)c->ranks[v].p;
+    }
+    const int64_t n_inst = d.n_chains * n_pol * n_cap;
+    if (out->chain_reports) {
+        P.inst_out = out->chain_reports;
+    } else {
+        if (int rc = c->inst_out.ensure((size_t)(n_inst + 1) * MCB_R_N * sizeof(int64_t))) return rc;
+        P.inst_out = (int64_t *)c->inst_out.p;
+    }
+    if (int rc = c->inst_lat.ensure((size_t)(n_inst + 1) * 2 * sizeof(double))) return rc;
+    P.inst_lat = (double *)c->inst_lat.p;
+    P.hashes = out->hashes;
+    P.outcomes = out->outcomes;
+    launched += launch_replay(P, s);
+    launched += launch_fold(P, t->num_traces, out->reports, out->latency, s);
+    CUDA_TRY(cudaGetLastError());
+    c->last_kernels = launched;
+    return MCB_OK;
+}
+
+extern "C" int mcb_replay(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, int32_t n_pol, const int32_t *caps,
+                          int32_t n_cap, const mcb_cost *cost, const mcb_nets *nets, const mcb_outputs *out,
+                          void *stream) {
+    mcb_clear_error();
+    if (!c) return mcb_set_error(MCB_ERR_INVALID, "ctx is NULL");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CUDA_TRY(cudaSetDevice(c->device));
+    return replay_locked(c, t, pols, n_pol, caps, n_cap, cost, nets, out, (cudaStream_t)stream);
+}
+
+template <typename T>
+static int upload(DevBuf &b, const T *src, size_t count, size_t pad_bytes, cudaStream_t s, const T **dst) {
+    const size_t bytes = count * sizeof(T);
+    if (int rc = b.ensure(bytes + pad_bytes)) return rc;
+    if (bytes) CUDA_TRY(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, s));
+    if (pad_bytes) CUDA_TRY(cudaMemsetAsync((char *)b.p + bytes, 0, pad_bytes, s));
+    *dst = (const T *)b.p;
+    return MCB_OK;
+}
+
+extern "C" int mcb_replay_host(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, int32_t n_pol,
+                               const int32_t *caps, int32_t n_cap, const mcb_cost *cost, const mcb_nets *nets,
+                               const mcb_outputs *out) {
+    mcb_clear_error();
+    if (!c) return mcb_set_error(MCB_ERR_INVALID, "ctx is NULL");
+    if (int rc = check_trace(t)) return rc;
+    if (!out || !out->reports || !out->latency) return mcb_set_error(MCB_ERR_INVALID, "outputs are NULL");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    mcb_trace dt = *t;
+    const DevTrace d = make_dev_trace(t);
+    const int64_t n_chains = d.n_chains;
+    if (int rc = upload(c->h_acc, t->acc, (size_t)d.total_acc, 256, s, &dt.acc)) return rc;
+    if (!t->uniform) {
+        int64_t total_rt = 0;
+        if (n_chains > 0) total_rt = t->chain_rt_off[n_chains];
+        if (int rc = upload(c->h_acc_off, t->chain_acc_off, (size_t)n_chains + 1, 0, s, &dt.chain_acc_off)) return rc;
+        if (int rc = upload(c->h_ev_off, t->chain_ev_off, (size_t)n_chains + 1, 0, s, &dt.chain_ev_off)) return rc;
+        if (int rc = upload(c->h_rt_off, t->chain_rt_off, (size_t)n_chains + 1, 0, s, &dt.chain_rt_off)) return rc;
+        if (int rc = upload(c->h_ev_info, t->ev_info, (size_t)d.total_events, 64, s, &dt.ev_info)) return rc;
+        if (int rc = upload(c->h_routed, t->routed, (size_t)total_rt, 64, s, &dt.routed)) return rc;
+    }
+    mcb_nets dn;
+    const mcb_nets *np = nullptr;
+    if (nets && nets->params) {
+        dn = *nets;
+        const size_t cnt = prepared_net_doubles(nets->num_experts, nets->hidden) * (size_t)nets->num_nets;
+        if (int rc = upload(c->h_params, nets->params, cnt, 0, s, &dn.params)) return rc;
+        np = &dn;
+    }
+    const int64_t n_cells = (int64_t)t->num_traces * n_pol * n_cap;
+    const int64_t n_inst = n_chains * n_pol * n_cap;
+    mcb_outputs dout;
+    memset(&dout, 0, sizeof dout);
+    if (int rc = c->h_reports.ensure((size_t)(n_cells + 1) * MCB_R_N * sizeof(int64_t))) return rc;
+    if (int rc = c->h_latency.ensure((size_t)(n_cells + 1) * 2 * sizeof(double))) return rc;
+    dout.reports = (int64_t *)c->h_reports.p;
+    dout.latency = (double *)c->h_latency.p;
+    if (out->chain_reports) {
+        if (int rc = c->h_chain_reports.ensure((size_t)(n_inst + 1) * MCB_R_N * sizeof(int64_t))) return rc;
+        dout.chain_reports = (int64_t *)c->h_chain_reports.p;
+    }
+    if (out->hashes) {
+        if (int rc = c->h_hashes.ensure((size_t)(n_inst + 1) * sizeof(uint64_t))) return rc;
+        dout.hashes = (uint64_t *)c->h_hashes.p;
+    }
+    if (out->outcomes) {
+        if (int rc = c->h_outcomes.ensure((size_t)(n_pol * n_cap * d.total_acc + 1) * sizeof(uint16_t))) return rc;
+        dout.outcomes = (uint16_t *)c->h_outcomes.p;
+    }
+    if (int rc = replay_locked(c, &dt, pols, n_pol, caps, n_cap, cost, np, &dout, s)) {
+        cudaStreamSynchronize(s);
+        return rc;
+    }
+    CUDA_TRY(cudaMemcpyAsync(out->reports, dout.reports, (size_t)n_cells * MCB_R_N * sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(out->latency, dout.latency, (size_t)n_cells * 2 * sizeof(double),
+                             cudaMemcpyDeviceToHost, s));
+    if (out->chain_reports)
+        CUDA_TRY(cudaMemcpyAsync(out->chain_reports, dout.chain_reports, (size_t)n_inst * MCB_R_N * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, s));
+    if (out->hashes)
+        CUDA_TRY(cudaMemcpyAsync(out->hashes, dout.hashes, (size_t)n_inst * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    if (out->outcomes)
+        CUDA_TRY(cudaMemcpyAsync(out->outcomes, dout.outcomes, (size_t)n_pol * n_cap * d.total_acc * sizeof(uint16_t),
+                                 cudaMemcpyDeviceToHost, s));
+    unsigned long long unc = 0;
+    CUDA_TRY(cudaMemcpyAsync(&unc, c->stats.p, sizeof unc, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    c->last_uncertain = (int64_t)unc;
+    return MCB_OK;
+}

@@ -1,0 +1,722 @@
+// sm_100a kernels of the expert-cache replay engine.
+//
+//   K2  k_next_use      reverse segmented next-use scan (Belady oracle)
+//   K3  k_feat_snap     per-chain recency/frequency scan, tile snapshots
+//       k_score_tile    feature rebuild + float64 scorer MLP + per-event ranks
+//   K4  k_replay        lane-group-per-instance cache replay (LRU/LFU/Belady/ML)
+//   K5  k_fold          per-(trace, policy, capacity) layer-order fold
+//
+// Reference semantics: pkg/src/moecache/engine.py:205-263 (_replay_layer),
+// policies.py:95-214, mlpolicy.py:15-62, features.py:34-52, net.py:43-105,
+// replay.py:44-89; normative restatement in SURVEY.md Appendix A.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "mcb_kernels.cuh"
+
+#define FULL_MASK 0xFFFFFFFFu
+
+// ===========================================================================
+// K2: next-use positions.  One warp per chain walks its stream backwards in
+// windows of 32 positions.  Inside a window __match_any_sync groups equal
+// experts: a lane's next use is the next higher lane of its group, or, for
+// the last occurrence in the window, the first occurrence after the window
+// (per-expert table in shared memory, E <= 128 entries per warp).  The lowest
+// lane of each group then publishes its position as the new first occurrence.
+// Integer only, so bit-exact with OracleIndex.next_use (policies.py:65-76):
+// next_use(e, p) = next_pos[p] - p, inf when next_pos == 0xFFFFFFFF.
+// ===========================================================================
+__global__ void __launch_bounds__(128) k_next_use(DevTrace tr, uint32_t *__restrict__ next_pos) {
+    __shared__ uint32_t table[4][MCB_MAX_EXPERTS];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t c = (int64_t)blockIdx.x * 4 + w;
+    if (c >= tr.n_chains) return;
+    uint32_t *tbl = table[w];
+    for (int e = lane; e < MCB_MAX_EXPERTS; e += 32) tbl[e] = MCB_NEXT_INF;
+    __syncwarp();
+    const int64_t a0 = tr.acc_begin(c);
+    const int64_t n = tr.acc_end(c) - a0;
+    const uint8_t *acc = tr.acc + a0;
+    uint32_t *out = next_pos + a0;
+    int64_t nwin = (n + 31) >> 5;
+    // software pipeline: the load of window w-1 is in flight while w is processed
+    uint32_t x_next = 0;
+    if (nwin > 0) {
+        const int64_t p = ((nwin - 1) << 5) + lane;
+        x_next = p < n ? (uint32_t)__ldg(acc + p) : 256u + lane;
+    }
+    for (int64_t win = nwin - 1; win >= 0; --win) {
+        const int64_t p = (win << 5) + lane;
+        const bool valid = p < n;
+        const uint32_t x = x_next;
+        if (win > 0) x_next = (uint32_t)__ldg(acc + p - 32);
+        const uint32_t m = __match_any_sync(FULL_MASK, x);
+        const uint32_t higher = m & ~((2u << lane) - 1u);
+        uint32_t r;
+        if (higher) r = (uint32_t)((win << 5) + __ffs(higher) - 1);
+        else r = valid ? tbl[x] : 0u;
+        __syncwarp();
+        if (valid && (m & ((1u << lane) - 1u)) == 0u) tbl[x] = (uint32_t)p;
+        __syncwarp();
+        if (valid) out[p] = r;
+    }
+}
+
+int launch_next_use(const DevTrace &tr, uint32_t *next_pos, cudaStream_t s) {
+    if (tr.n_chains == 0) return 0;
+    const int64_t blocks = (tr.n_chains + 3) / 4;
+    k_next_use<<<(unsigned)blocks, 128, 0, s>>>(tr, next_pos);
+    return 1;
+}
+
+// ===========================================================================
+// K4: replay.  One lane group of G lanes replays one cache instance
+// (chain, policy, capacity).  Expert e lives in lane e / EPL, slot e % EPL.
+// Per lane: resident / pinned / seen bits, the policy key of each of its
+// experts for ALL experts (LRU last position, LFU in-sequence count, Belady
+// bitwise-not of the next-use position, ML 256 - score rank), and the
+// pending-refetch decode index of experts it evicted.  Every policy's victim
+// is the argmin of (key, expert id) over resident \ pinned:
+// a lane-local scan in slot order, a redux.sync min over the group, and a
+// ballot that picks the lowest lane among equal keys, i.e. the lowest id.
+// ===========================================================================
+enum { POL_LRU = 0, POL_LFU = 1, POL_BELADY = 2, POL_ML = 3 };
+
+#define KEY_SENT 0xFFFFFFFFu
+
+template <int G>
+struct U32Stream {
+    // 4*G-byte (or G-word) chunks of a stream held one u32 per lane, next
+    // chunk prefetched while the current one is consumed.
+    const uint32_t *base;
+    int64_t limit_words;  // words readable
+    int64_t chunk;        // index of the chunk held in `cur`
+    uint32_t cur, nxt;
+    __device__ __forceinline__ uint32_t load(int64_t ch, int glane) const {
+        const int64_t wi = ch * G + glane;
+        return wi < limit_words ? __ldg(base + wi) : 0u;
+    }
+    __device__ __forceinline__ void init(const void *p, int64_t words, int64_t first_word, int glane) {
+        base = (const uint32_t *)p;
+        limit_words = words;
+        chunk = first_word / G;
+        cur = load(chunk, glane);
+        nxt = load(chunk + 1, glane);
+    }
+    // word index -> value (must be called by the whole group, monotone words)
+    __device__ __forceinline__ uint32_t get(int64_t word, int glane, int gbase, unsigned gmask) {
+        const int64_t ch = word / G;
+        if (ch != chunk) {
+            if (ch == chunk + 1) {
+                cur = nxt;
+            } else {
+                cur = load(ch, glane);
+            }
+            chunk = ch;
+            nxt = load(ch + 1, glane);
+        }
+        return __shfl_sync(gmask, cur, gbase + (int)(word - ch * G));
+    }
+};
+
+template <int EPL>
+__device__ __forceinline__ void set_slot(uint32_t (&a)[EPL], int slot, uint32_t v) {
+#pragma unroll
+    for (int s = 0; s < EPL; ++s)
+        if (s == slot) a[s] = v;
+}
+template <int EPL>
+__device__ __forceinline__ uint32_t get_slot(const uint32_t (&a)[EPL], int slot) {
+    uint32_t v = a[0];
+#pragma unroll
+    for (int s = 1; s < EPL; ++s)
+        if (s == slot) v = a[s];
+    return v;
+}
+
+__device__ __forceinline__ uint64_t fnv16(uint64_t h, uint32_t code) {
+    h ^= (uint64_t)(code & 0xFFu);
+    h *= MCB_FNV_PRIME;
+    h ^= (uint64_t)((code >> 8) & 0xFFu);
+    h *= MCB_FNV_PRIME;
+    return h;
+}
+
+template <int G, int EPL, int POL, bool UNIFORM>
+__device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t chain, int pol_i, int cap_i,
+                                                int64_t inst, int ml_variant) {
+    const DevTrace &tr = P.tr;
+    const int lane = threadIdx.x & 31;
+    const int glane = lane % G;
+    const int gbase = lane - glane;
+    const unsigned gmask = (G == 32) ? FULL_MASK : (((1u << G) - 1u) << gbase);
+    const uint32_t C = (uint32_t)P.cap[cap_i];
+    const int E = tr.E;
+
+    uint32_t res = 0, pin = 0, seen = 0;
+    uint32_t key[EPL], pend[EPL];
+#pragma unroll
+    for (int s = 0; s < EPL; ++s) { key[s] = 0; pend[s] = 0; }
+    uint32_t count = 0, ph = 0, pm = 0, dh = 0, dm = 0, nev = 0, comp = 0, refc = 0;
+    double dlat = 0.0, plat = 0.0;
+    uint64_t h = MCB_FNV_OFF;
+    int status = MCB_OK;
+
+    const int64_t a0 = tr.acc_begin(chain);
+    const int64_t e0 = tr.ev_begin(chain);
+    const int64_t n_ev = tr.ev_end(chain) - e0;
+    const int64_t acc_words = (tr.total_acc + 3) >> 2;
+
+    U32Stream<G> ids;   // access ids, 4 per word
+    ids.init(tr.acc, acc_words, a0 >> 2, glane);
+    U32Stream<G> nx;    // Belady next-use positions, 1 per word
+    if (POL == POL_BELADY) nx.init(P.next_pos, tr.total_acc, a0, glane);
+    const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
+    uint16_t *outc = P.outcomes ? P.outcomes + ((int64_t)pol_i * P.n_cap + cap_i) * tr.total_acc : nullptr;
+
+    uint32_t pos = 0, dec = 0;
+    for (int64_t ev = 0; ev < n_ev; ++ev) {
+        const uint32_t info = UNIFORM ? mcb_ev_pack((uint32_t)tr.K, (uint32_t)tr.K, true, ev == 0)
+                                      : __ldg(tr.ev_info + e0 + ev);
+        const uint32_t nacc = mcb_ev_nacc(info);
+        const bool decode = mcb_ev_decode(info);
+        if (POL == POL_LFU && mcb_ev_newseq(info)) {
+            // start_sequence: LFU counts reset (policies.py:184-185)
+#pragma unroll
+            for (int s = 0; s < EPL; ++s) key[s] = 0;
+        }
+        if (POL == POL_ML) {
+            // per-event score ranks (mlpolicy.py:59-62): argmax score == argmin (256 - rank)
+            const uint8_t *row = rank + (e0 + ev) * E;
+#pragma unroll
+            for (int s = 0; s < EPL; ++s) {
+                const int e = glane * EPL + s;
+                const uint32_t r = e < E ? (uint32_t)__ldg(row + e) : 0u;
+                key[s] = r ? 256u - r : KEY_SENT;
+            }
+        }
+        pin = 0;
+        uint32_t step_miss = 0;
+        for (uint32_t j = 0; j < nacc; ++j, ++pos) {
+            const int64_t A = a0 + pos;
+            const uint32_t word = ids.get(A >> 2, glane, gbase, gmask);
+            const uint32_t x = (word >> (8 * (uint32_t)(A & 3))) & 0xFFu;
+            const int owner = (int)(x / EPL);
+            const int slot = (int)(x % EPL);
+            const bool mine = glane == owner;
+            const uint32_t bit = 1u << slot;
+            const bool hit = (__ballot_sync(gmask, mine && (res & bit)) & gmask) != 0u;
+            if (POL == POL_BELADY) {
+                const uint32_t np = nx.get(A, glane, gbase, gmask);
+                if (mine) set_slot<EPL>(key, slot, ~np);
+            }
+            if (POL == POL_LRU && mine) set_slot<EPL>(key, slot, pos);
+            if (POL == POL_LFU && mine) set_slot<EPL>(key, slot, get_slot<EPL>(key, slot) + 1u);
+            uint32_t code = MCB_OUT_HIT;
+            if (hit) {
+                if (decode) ++dh; else ++ph;
+            } else {
+                if (decode) ++dm; else ++pm;
+                ++step_miss;
+                if (count >= C) {
+                    const uint32_t cand = res & ~pin;
+                    uint32_t lk = KEY_SENT;
+                    int ls = 0;
+#pragma unroll
+                    for (int s = 0; s < EPL; ++s)
+                        if (((cand >> s) & 1u) && key[s] < lk) { lk = key[s]; ls = s; }
+                    const uint32_t m = __reduce_min_sync(gmask, lk);
+                    if (m == KEY_SENT) { status = MCB_ERR_NO_EVICTABLE; break; }
+                    const unsigned b = __ballot_sync(gmask, lk == m) & gmask;
+                    const int wl = __ffs(b) - 1;
+                    const int vs = __shfl_sync(gmask, ls, wl);
+                    const int vlane = wl - gbase;
+                    if (glane == vlane) {
+                        res &= ~(1u << vs);
+                        set_slot<EPL>(pend, vs, dec + 1u);
+                    }
+                    code = (uint32_t)(vlane * EPL + vs);
+                    ++nev;
+                } else {
+                    ++count;
+                    code = MCB_OUT_MISS;
+                }
+                if (mine) {
+                    // compulsory (engine.py:248-250) and refetch of an earlier
+                    // victim (engine.py:289-296): its first access after the
+                    // eviction is necessarily this miss
+                    if (!(seen & bit)) {
+                        ++comp;
+                    } else {
+                        const uint32_t pe = get_slot<EPL>(pend, slot);
+                        if (pe && (int64_t)dec - (int64_t)(pe - 1u) <= (int64_t)P.window) ++refc;
+                    }
+                    set_slot<EPL>(pend, slot, 0u);
+                    seen |= bit;
+                    res |= bit;
+                }
+            }
+            if (decode && mine) pin |= bit;
+            if (outc) {
+                h = fnv16(h, code);
+                if (glane == 0) outc[A] = (uint16_t)code;
+            } else if (P.hashes) {
+                h = fnv16(h, code);
+            }
+        }
+        if (status != MCB_OK) break;
+        // step_latency_s (engine.py:58-62) accumulated in event order (engine.py:258-262)
+        double lat;
+        if (step_miss > 0)
+            lat = __dmul_rn((double)(P.loads_serial ? step_miss : 1u), P.t_load);
+        else
+            lat = __dmul_rn((double)nacc, P.t_compute);
+        if (decode) dlat = __dadd_rn(dlat, __dadd_rn(lat, POL == POL_ML ? P.ml_cost : 0.0));
+        else plat = __dadd_rn(plat, lat);
+        if (decode) ++dec;
+    }
+    comp = __reduce_add_sync(gmask, comp);
+    refc = __reduce_add_sync(gmask, refc);
+    if (glane == 0) {
+        int64_t *o = P.inst_out + inst * MCB_R_N;
+        o[MCB_R_PREFILL_HITS] = ph;
+        o[MCB_R_PREFILL_MISSES] = pm;
+        o[MCB_R_DECODE_HITS] = dh;
+        o[MCB_R_DECODE_MISSES] = dm;
+        o[MCB_R_COMPULSORY] = comp;
+        o[MCB_R_EVICTIONS] = nev;
+        o[MCB_R_REFETCHED] = refc;
+        o[MCB_R_STATUS] = status;
+        P.inst_lat[inst * 2 + 0] = dlat;
+        P.inst_lat[inst * 2 + 1] = plat;
+        if (P.hashes) P.hashes[inst] = h;
+    }
+}
+
+template <int G, int EPL, bool UNIFORM>
+__global__ void __launch_bounds__(128) k_replay(const __grid_constant__ ReplayParams P) {
+    const int64_t inst = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const int64_t n_inst = P.tr.n_chains * P.n_pol * P.n_cap;
+    if (inst >= n_inst) return;
+    const int cap_i = (int)(inst % P.n_cap);
+    const int pol_i = (int)((inst / P.n_cap) % P.n_pol);
+    const int64_t chain = inst / ((int64_t)P.n_cap * P.n_pol);
+    switch (P.pol[pol_i]) {
+        case MCB_LRU: replay_instance<G, EPL, POL_LRU, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
+        case MCB_LFU: replay_instance<G, EPL, POL_LFU, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
+        case MCB_BELADY: replay_instance<G, EPL, POL_BELADY, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
+        case MCB_ML: replay_instance<G, EPL, POL_ML, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
+        default: replay_instance<G, EPL, POL_ML, UNIFORM>(P, chain, pol_i, cap_i, inst, 1); break;
+    }
+}
+
+template <int G, int EPL>
+static void launch_replay_t(const ReplayParams &p, cudaStream_t s) {
+    const int64_t n_inst = p.tr.n_chains * p.n_pol * p.n_cap;
+    const int per_block = 128 / G;
+    const unsigned blocks = (unsigned)((n_inst + per_block - 1) / per_block);
+    if (p.tr.uniform) k_replay<G, EPL, true><<<blocks, 128, 0, s>>>(p);
+    else k_replay<G, EPL, false><<<blocks, 128, 0, s>>>(p);
+}
+
+int launch_replay(const ReplayParams &p, cudaStream_t s) {
+    if (p.tr.n_chains * p.n_pol * p.n_cap == 0) return 0;
+    const int E = p.tr.E;
+    if (E <= 8) launch_replay_t<8, 1>(p, s);
+    else if (E <= 16) launch_replay_t<16, 1>(p, s);
+    else if (E <= 32) launch_replay_t<32, 1>(p, s);
+    else if (E <= 64) launch_replay_t<32, 2>(p, s);
+    else launch_replay_t<32, 4>(p, s);
+    return 1;
+}
+
+// ===========================================================================
+// K5: fold chains -> (trace, policy, capacity) in layer order (engine.py:330-343)
+// ===========================================================================
+__global__ void k_fold(const __grid_constant__ ReplayParams P, int num_traces, int64_t *__restrict__ reports,
+                       double *__restrict__ latency) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = (int64_t)num_traces * P.n_pol * P.n_cap;
+    if (i >= n) return;
+    const int cap_i = (int)(i % P.n_cap);
+    const int pol_i = (int)((i / P.n_cap) % P.n_pol);
+    const int64_t trace = i / ((int64_t)P.n_cap * P.n_pol);
+    int64_t acc[MCB_R_N] = {0, 0, 0, 0, 0, 0, 0, 0};
+    double dl = 0.0, pl = 0.0;
+    for (int l = 0; l < P.tr.L; ++l) {
+        const int64_t chain = trace * P.tr.L + l;
+        const int64_t inst = (chain * P.n_pol + pol_i) * P.n_cap + cap_i;
+        const int64_t *o = P.inst_out + inst * MCB_R_N;
+#pragma unroll
+        for (int k = 0; k < MCB_R_STATUS; ++k) acc[k] += o[k];
+        if (acc[MCB_R_STATUS] == 0 && o[MCB_R_STATUS] != 0) acc[MCB_R_STATUS] = o[MCB_R_STATUS];
+        dl = __dadd_rn(dl, P.inst_lat[inst * 2 + 0]);
+        pl = __dadd_rn(pl, P.inst_lat[inst * 2 + 1]);
+    }
+#pragma unroll
+    for (int k = 0; k < MCB_R_N; ++k) reports[i * MCB_R_N + k] = acc[k];
+    latency[i * 2 + 0] = dl;
+    latency[i * 2 + 1] = pl;
+}
+
+int launch_fold(const ReplayParams &p, int num_traces, int64_t *reports, double *latency, cudaStream_t s) {
+    const int64_t n = (int64_t)num_traces * p.n_pol * p.n_cap;
+    if (n == 0) return 0;
+    k_fold<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(p, num_traces, reports, latency);
+    return 1;
+}
+
+// ===========================================================================
+// K3: ML scorer.
+// ===========================================================================
+// Prepared (transposed) weights per net: Wt1[D][H] b1[H] Wt2[H][H] b2[H] Wt3[H][E] b3[E]
+__host__ __device__ size_t prepared_net_doubles(int E, int H) {
+    const size_t D = 2 * (size_t)E;
+    return D * H + H + (size_t)H * H + H + (size_t)H * E + E;
+}
+
+__global__ void k_prepare_nets(const double *__restrict__ params, int E, int H, int num_nets,
+                               double *__restrict__ wt) {
+    const int D = 2 * E;
+    const size_t per = prepared_net_doubles(E, H);
+    const int64_t total = (int64_t)per * num_nets;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t net = i / per;
+        int64_t r = i % per;
+        const double *src = params + net * per;  // same total size, .evnet order
+        double v;
+        // source offsets (.evnet): w1[H][D] b1 w2[H][H] b2 w3[E][H] b3
+        const int64_t s_w1 = 0, s_b1 = (int64_t)H * D, s_w2 = s_b1 + H, s_b2 = s_w2 + (int64_t)H * H,
+                      s_w3 = s_b2 + H, s_b3 = s_w3 + (int64_t)E * H;
+        if (r < (int64_t)D * H) {                 // Wt1[k][h] = w1[h][k]
+            const int64_t k = r / H, hh = r % H;
+            v = src[s_w1 + hh * D + k];
+        } else if ((r -= (int64_t)D * H) < H) {
+            v = src[s_b1 + r];
+        } else if ((r -= H) < (int64_t)H * H) {   // Wt2[k][h] = w2[h][k]
+            const int64_t k = r / H, hh = r % H;
+            v = src[s_w2 + hh * H + k];
+        } else if ((r -= (int64_t)H * H) < H) {
+            v = src[s_b2 + r];
+        } else if ((r -= H) < (int64_t)H * E) {   // Wt3[k][e] = w3[e][k]
+            const int64_t k = r / E, e = r % E;
+            v = src[s_w3 + e * H + k];
+        } else {
+            r -= (int64_t)H * E;
+            v = src[s_b3 + r];
+        }
+        wt[i] = v;
+    }
+}
+
+int launch_prepare_nets(const double *params, int E, int H, int num_nets, double *wt, cudaStream_t s) {
+    const int64_t total = (int64_t)prepared_net_doubles(E, H) * num_nets;
+    const unsigned blocks = (unsigned)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+    k_prepare_nets<<<blocks, 256, 0, s>>>(params, E, H, num_nets, wt);
+    return 1;
+}
+
+// Snapshot record per tile: last[E] (update index of the last routing, -1 =
+// never), freq[E], u (updates since the sequence start), rt_lo, rt_hi
+// (routed-list offset of the tile's first event within the chain).
+__host__ __device__ __forceinline__ int snap_stride(int E) { return 2 * E + 4; }
+
+__global__ void k_tile_offsets(DevTrace tr, int64_t *__restrict__ tile_off) {
+    // single block exclusive scan of ceil(n_ev / TILE) over chains
+    __shared__ int64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < tr.n_chains; base += blockDim.x) {
+        const int64_t c = base + threadIdx.x;
+        int64_t v = 0;
+        if (c < tr.n_chains) v = (tr.ev_end(c) - tr.ev_begin(c) + MCB_TILE_EV - 1) / MCB_TILE_EV;
+        // block inclusive scan (Hillis-Steele in shared memory)
+        __shared__ int64_t buf[1024];
+        buf[threadIdx.x] = v;
+        __syncthreads();
+        for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+            const int64_t add = threadIdx.x >= (unsigned)o ? buf[threadIdx.x - o] : 0;
+            __syncthreads();
+            buf[threadIdx.x] += add;
+            __syncthreads();
+        }
+        if (c < tr.n_chains) tile_off[c] = carry + buf[threadIdx.x] - v;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry += buf[threadIdx.x];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) tile_off[tr.n_chains] = carry;
+}
+
+__device__ __forceinline__ int64_t chain_tile_begin(const DevTrace &tr, const int64_t *tile_off, int64_t c) {
+    if (tr.uniform) return c * ((tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV);
+    return tile_off[c];
+}
+
+// One warp per chain: sequential FeatureTracker scan (features.py:34-39),
+// reset at sequence boundaries (mlpolicy.py:56-57), updates only for decode
+// events unless include_prefill (mlpolicy.py:59-61).
+__global__ void __launch_bounds__(128) k_feat_snap(DevTrace tr, int include_prefill, const int64_t *tile_off,
+                                                   int32_t *__restrict__ snaps) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (c >= tr.n_chains) return;
+    const int E = tr.E;
+    const int SN = snap_stride(E);
+    int32_t last[4], f[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { last[j] = -1; f[j] = 0; }
+    int32_t u = 0;
+    const int64_t e0 = tr.ev_begin(c), n_ev = tr.ev_end(c) - e0;
+    const uint8_t *routed = tr.routed_ptr() + tr.rt_begin(c);
+    int64_t rt = 0;
+    int64_t tile = chain_tile_begin(tr, tile_off, c);
+    for (int64_t ev = 0; ev < n_ev; ++ev) {
+        const uint32_t info = tr.info(c, e0 + ev);
+        if (ev % MCB_TILE_EV == 0) {
+            int32_t *sp = snaps + tile * SN;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int e = lane + 32 * j;
+                if (e < E) { sp[e] = last[j]; sp[E + e] = f[j]; }
+            }
+            if (lane == 0) { sp[2 * E] = u; sp[2 * E + 1] = (int32_t)(rt & 0xFFFFFFFF); sp[2 * E + 2] = (int32_t)(rt >> 32); }
+            ++tile;
+        }
+        if (mcb_ev_newseq(info)) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) { last[j] = -1; f[j] = 0; }
+            u = 0;
+        }
+        const uint32_t nrt = mcb_ev_nrt(info);
+        if (mcb_ev_decode(info) || include_prefill) {
+            ++u;
+            for (uint32_t r = 0; r < nrt; ++r) {
+                const int x = __ldg(routed + rt + r);
+                if ((x & 31) == lane) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if ((x >> 5) == j) { last[j] = u; ++f[j]; }
+                }
+            }
+        }
+        rt += nrt;
+    }
+}
+
+__device__ __forceinline__ double sigmoid_ref(double z) {
+    // sign-split logistic (net.py:43-49)
+    if (z >= 0.0) return 1.0 / (1.0 + exp(-z));
+    const double ez = exp(z);
+    return ez / (1.0 + ez);
+}
+
+// Out[i][col] = act(sum_k A[i][k] * Wt[k][col] + b[col]) for the tile's 32
+// events; warp w owns events 4w..4w+3, lane owns columns lane + 32 j.
+// Fixed summation order: k ascending, fma, then + bias.
+template <int NJ>
+__device__ __forceinline__ void mlp_layer(const double *A, int lda, int Din, const double *__restrict__ Wt,
+                                          const double *__restrict__ bias, int Dout, double *Out, int ldo,
+                                          bool act) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double accu[4][NJ];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) accu[i][j] = 0.0;
+    for (int k = 0; k < Din; ++k) {
+        double a[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = A[(w * 4 + i) * lda + k];
+        double wv[NJ];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int col = lane + 32 * j;
+            wv[j] = col < Dout ? __ldg(Wt + (int64_t)k * Dout + col) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) accu[i][j] = fma(a[i], wv[j], accu[i][j]);
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const int col = lane + 32 * j;
+        if (col < Dout) {
+            const double b = __ldg(bias + col);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const double z = __dadd_rn(accu[i][j], b);
+                Out[(w * 4 + i) * ldo + col] = act ? __dmul_rn(z, sigmoid_ref(z)) : z;
+            }
+        }
+    }
+}
+
+__device__ void mlp_layer_any(const double *A, int lda, int Din, const double *Wt, const double *bias, int Dout,
+                              double *Out, int ldo, bool act) {
+    if (Dout <= 32) mlp_layer<1>(A, lda, Din, Wt, bias, Dout, Out, ldo, act);
+    else if (Dout <= 64) mlp_layer<2>(A, lda, Din, Wt, bias, Dout, Out, ldo, act);
+    else if (Dout <= 128) mlp_layer<4>(A, lda, Din, Wt, bias, Dout, Out, ldo, act);
+    else mlp_layer<8>(A, lda, Din, Wt, bias, Dout, Out, ldo, act);
+}
+
+// One block (256 threads) per (chain, tile of 32 events): rebuild the
+// features of each event from the tile snapshot, run the float64 MLP
+// (EvictionNet.forward, net.py:88-105), and rank every expert's score within
+// its event: rank = 1 + #{selectable j : s_j < s_e} for selectable e (s > -inf),
+// 0 otherwise (NaN / -inf are never evicted, mlpolicy.py:15-26).  Argmax of
+// score with lowest-id ties == argmax of rank with lowest-id ties.
+__global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *__restrict__ wt_all, int H,
+                                                     int num_nets, int include_prefill,
+                                                     const int64_t *__restrict__ tile_off,
+                                                     const int32_t *__restrict__ snaps, int64_t n_tiles,
+                                                     uint8_t *__restrict__ ranks, double *__restrict__ scores,
+                                                     unsigned long long *uncertain) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int E = tr.E, D = 2 * E;
+    const int lda = D > H ? D : H;
+    const int ldb = H > E ? H : E;
+    double *bufA = (double *)smem_raw;                       // [TILE][lda]
+    double *bufB = bufA + MCB_TILE_EV * lda;                 // [TILE][ldb]
+    int32_t *s_last = (int32_t *)(bufB + MCB_TILE_EV * ldb); // [E]
+    int32_t *s_f = s_last + MCB_MAX_EXPERTS;                 // [E]
+    int32_t *s_flag = s_f + MCB_MAX_EXPERTS;                 // [TILE]
+
+    const int64_t tile = blockIdx.x;
+    if (tile >= n_tiles) return;
+    // locate the chain
+    int64_t c, tile_in_chain;
+    if (tr.uniform) {
+        const int64_t tpc = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
+        c = tile / tpc;
+        tile_in_chain = tile % tpc;
+    } else {
+        if (tile >= tile_off[tr.n_chains]) return;  // grid is an upper bound in general mode
+        int64_t lo = 0, hi = tr.n_chains;  // largest c with tile_off[c] <= tile
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) / 2;
+            if (tile_off[mid] <= tile) lo = mid; else hi = mid;
+        }
+        c = lo;
+        tile_in_chain = tile - tile_off[c];
+    }
+    const int64_t e0 = tr.ev_begin(c);
+    const int64_t ev0 = tile_in_chain * MCB_TILE_EV;
+    const int64_t n_ev_chain = tr.ev_end(c) - e0;
+    const int nev = (int)min((int64_t)MCB_TILE_EV, n_ev_chain - ev0);
+    const int SN = snap_stride(E);
+    const int32_t *sp = snaps + tile * SN;
+    const int tid = threadIdx.x;
+    for (int e = tid; e < E; e += blockDim.x) { s_last[e] = sp[e]; s_f[e] = sp[E + e]; }
+    int32_t u = sp[2 * E];
+    int64_t rt = (int64_t)(uint32_t)sp[2 * E + 1] | ((int64_t)sp[2 * E + 2] << 32);
+    const uint8_t *routed = tr.routed_ptr() + tr.rt_begin(c);
+    __syncthreads();
+    // max frequency at the tile start
+    int32_t maxf = 0;
+    for (int e = 0; e < E; ++e) maxf = max(maxf, s_f[e]);
+
+    for (int i = 0; i < MCB_TILE_EV; ++i) {
+        if (i < nev) {
+            const uint32_t info = tr.info(c, e0 + ev0 + i);
+            const uint32_t nrt = mcb_ev_nrt(info);
+            const bool newseq = mcb_ev_newseq(info);
+            const bool upd = mcb_ev_decode(info) || include_prefill;
+            if (newseq) { u = 0; maxf = 0; }
+            if (upd) ++u;
+            for (int e = tid; e < E; e += blockDim.x) {
+                int32_t l = newseq ? -1 : s_last[e];
+                int32_t fe = newseq ? 0 : s_f[e];
+                if (upd) {
+                    for (uint32_t r = 0; r < nrt; ++r)
+                        if (__ldg(routed + rt + r) == e) { l = u; ++fe; }
+                }
+                s_last[e] = l;
+                s_f[e] = fe;
+            }
+            __syncthreads();
+            if (upd)
+                for (uint32_t r = 0; r < nrt; ++r) maxf = max(maxf, s_f[__ldg(routed + rt + r)]);
+            rt += nrt;
+            // features (features.py:44-52): [1/r || f / max_f]
+            for (int k = tid; k < D; k += blockDim.x) {
+                double v;
+                if (k < E) {
+                    const int32_t l = s_last[k];
+                    v = l < 0 ? 0.0 : 1.0 / (double)(u - l + 1);
+                } else {
+                    v = maxf > 0 ? (double)s_f[k - E] / (double)maxf : 0.0;
+                }
+                bufA[i * lda + k] = v;
+            }
+            __syncthreads();
+        } else {
+            for (int k = tid; k < D; k += blockDim.x) bufA[i * lda + k] = 0.0;
+        }
+    }
+    __syncthreads();
+    const int64_t layer = c % tr.L;
+    const double *wt = wt_all + (num_nets == 1 ? 0 : layer) * (int64_t)prepared_net_doubles(E, H);
+    const double *Wt1 = wt, *b1 = Wt1 + (int64_t)D * H, *Wt2 = b1 + H, *b2 = Wt2 + (int64_t)H * H,
+                 *Wt3 = b2 + H, *b3 = Wt3 + (int64_t)H * E;
+    mlp_layer_any(bufA, lda, D, Wt1, b1, H, bufB, ldb, true);   // h1 -> B
+    __syncthreads();
+    mlp_layer_any(bufB, ldb, H, Wt2, b2, H, bufA, lda, true);   // h2 -> A
+    __syncthreads();
+    mlp_layer_any(bufA, lda, H, Wt3, b3, E, bufB, ldb, false);  // scores -> B
+    __syncthreads();
+    for (int i = tid; i < MCB_TILE_EV; i += blockDim.x) s_flag[i] = 0;
+    __syncthreads();
+    for (int q = tid; q < nev * E; q += blockDim.x) {
+        const int i = q / E, e = q % E;
+        const double s = bufB[i * ldb + e];
+        uint32_t r = 0;
+        bool near = false;
+        if (s > -INFINITY) {
+            r = 1;
+            for (int j = 0; j < E; ++j) {
+                const double sj = bufB[i * ldb + j];
+                if (sj > -INFINITY) {
+                    if (sj < s) ++r;
+                    if (sj != s && fabs(sj - s) <= 1e-12 * fmax(fabs(s), fabs(sj))) near = true;
+                }
+            }
+        }
+        const int64_t g = (e0 + ev0 + i) * E + e;
+        ranks[g] = (uint8_t)r;
+        if (scores) scores[g] = s;
+        if (near) s_flag[i] = 1;
+    }
+    __syncthreads();
+    if (tid == 0 && uncertain) {
+        unsigned long long cnt = 0;
+        for (int i = 0; i < nev; ++i) cnt += s_flag[i];
+        if (cnt) atomicAdd(uncertain, cnt);
+    }
+}
+
+int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill, uint8_t *ranks,
+                 double *scores, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,
+                 unsigned long long *uncertain, cudaStream_t s) {
+    if (tr.n_chains == 0) return 0;
+    int launched = 0;
+    if (!tr.uniform) {
+        k_tile_offsets<<<1, 1024, 0, s>>>(tr, tile_off);
+        ++launched;
+    }
+    k_feat_snap<<<(unsigned)((tr.n_chains + 3) / 4), 128, 0, s>>>(tr, include_prefill, tile_off, snaps);
+    ++launched;
+    const int E = tr.E, D = 2 * E;
+    const int lda = D > H ? D : H, ldb = H > E ? H : E;
+    const size_t smem = (size_t)MCB_TILE_EV * (lda + ldb) * sizeof(double) +
+                        (2 * MCB_MAX_EXPERTS + MCB_TILE_EV) * sizeof(int32_t);
+    cudaFuncSetAttribute(k_score_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (max_tiles > 0) {
+        k_score_tile<<<(unsigned)max_tiles, 256, smem, s>>>(tr, wt, H, num_nets, include_prefill, tile_off, snaps,
+                                                            max_tiles, ranks, scores, uncertain);
+        ++launched;
+    }
+    return launched;
+}

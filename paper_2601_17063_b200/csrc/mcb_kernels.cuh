@@ -1,0 +1,62 @@
+// Device-side views and kernel launch declarations (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mcb_internal.h"
+
+#define MCB_MAX_POL 8
+#define MCB_MAX_CAP 64
+#define MCB_TILE_EV 32          // events per scorer tile (K3)
+#define MCB_FNV_OFF 0xCBF29CE484222325ull
+#define MCB_FNV_PRIME 0x100000001B3ull
+
+// Chain-major trace view usable on the device (mcb.h mcb_trace, device pointers).
+struct DevTrace {
+    int L, E, K;
+    int uniform;
+    int64_t T;                  // uniform: events per chain
+    int64_t n_chains;
+    int64_t total_acc, total_events;
+    const uint8_t *acc;
+    const int64_t *acc_off, *ev_off, *rt_off;
+    const uint32_t *ev_info;
+    const uint8_t *routed;
+
+    __device__ __forceinline__ int64_t acc_begin(int64_t c) const { return uniform ? c * T * K : acc_off[c]; }
+    __device__ __forceinline__ int64_t acc_end(int64_t c) const { return uniform ? (c + 1) * T * K : acc_off[c + 1]; }
+    __device__ __forceinline__ int64_t ev_begin(int64_t c) const { return uniform ? c * T : ev_off[c]; }
+    __device__ __forceinline__ int64_t ev_end(int64_t c) const { return uniform ? (c + 1) * T : ev_off[c + 1]; }
+    __device__ __forceinline__ int64_t rt_begin(int64_t c) const { return uniform ? c * T * K : rt_off[c]; }
+    __device__ __forceinline__ const uint8_t *routed_ptr() const { return uniform ? acc : routed; }
+    __device__ __forceinline__ uint32_t info(int64_t c, int64_t global_ev) const {
+        return uniform ? mcb_ev_pack((uint32_t)K, (uint32_t)K, true, global_ev == c * T) : ev_info[global_ev];
+    }
+};
+
+struct ReplayParams {
+    DevTrace tr;
+    int n_pol, n_cap;
+    int32_t pol[MCB_MAX_POL];
+    int32_t cap[MCB_MAX_CAP];
+    const uint32_t *next_pos;           // K2 output (Belady)
+    const uint8_t *rank[2];             // K3 output: [0] include_prefill, [1] decode-only features
+    double t_load, t_compute, ml_cost;
+    int loads_serial, window;
+    int64_t *inst_out;                  // [chain][pol][cap][MCB_R_N]
+    double *inst_lat;                   // [chain][pol][cap][2]
+    uint64_t *hashes;                   // optional [chain][pol][cap]
+    uint16_t *outcomes;                 // optional [pol][cap][total_acc]
+};
+
+// launchers (mcb_kernels.cu); return the number of kernels launched or <0 on error
+int launch_next_use(const DevTrace &tr, uint32_t *next_pos, cudaStream_t s);
+int launch_replay(const ReplayParams &p, cudaStream_t s);
+int launch_fold(const ReplayParams &p, int num_traces, int64_t *reports, double *latency, cudaStream_t s);
+int launch_prepare_nets(const double *params, int E, int H, int num_nets, double *wt, cudaStream_t s);
+__host__ __device__ size_t prepared_net_doubles(int E, int H);
+// K3: snapshot scan + tile scorer. snaps scratch: n_tiles_total * (2E+1) int32; tile_off: n_chains+1 int64
+int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill,
+                 uint8_t *ranks, double *scores, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,
+                 unsigned long long *uncertain, cudaStream_t s);
