@@ -158,6 +158,12 @@ int mcb_last_error(char *buf, size_t n);
  * launched, and the uncertain-rank counter of the ML scorer (events whose
  * float64 scores had two values closer than 1e-12 relative). */
 int mcb_last_stats(mcb_ctx *ctx, int64_t *kernels_launched, int64_t *uncertain_events);
+/* Stage timing: when enabled, mcb_replay records CUDA events on its stream
+ * around each stage; mcb_last_timings returns the stage durations in ms of
+ * the last call (after the stream has been synchronised):
+ * [0] K2 next-use scan, [1] K3 scorer, [2] K4 replay, [3] K5 fold. */
+int mcb_set_timing(mcb_ctx *ctx, int32_t enable);
+int mcb_last_timings(mcb_ctx *ctx, float *ms, int32_t n);
 
 /* ---- host-side trace validation + packing (trace.py:57-141, replay.py:44-81) ----
  * Input: one trace as flat events in stored order: seq_id, phase (0 prefill,
@@ -190,7 +196,8 @@ int mcb_replay(mcb_ctx *ctx, const mcb_trace *trace, const int32_t *policies, in
                const mcb_nets *nets, const mcb_outputs *out, void *stream);
 int mcb_replay_host(mcb_ctx *ctx, const mcb_trace *trace, const int32_t *policies,
                     int32_t n_policies, const int32_t *capacities, int32_t n_capacities,
-                    const mcb_cost *cost, const mcb_nets *nets, const mcb_outputs *out);
+                    const mcb_cost *cost, const mcb_nets *nets, const mcb_outputs *out,
+                    void *stream /* NULL: the context's own stream */);
 
 /* ---- individual kernels (exposed for tests and benchmarks) ---- */
 /* K2: next_pos[i] = chain-relative position of the next access of the same

@@ -30,6 +30,7 @@ OUT_HIT, OUT_MISS = 0xFFFF, 0xFFFE
 
 EXPORTED_SYMBOLS = (
     "mcb_abi_version", "mcb_ctx_create", "mcb_ctx_destroy", "mcb_last_error", "mcb_last_stats",
+    "mcb_set_timing", "mcb_last_timings",
     "mcb_pack_trace", "mcb_packed_view", "mcb_packed_positions", "mcb_packed_free",
     "mcb_replay", "mcb_replay_host", "mcb_next_use", "mcb_score", "mcb_router_topk",
 )
@@ -115,10 +116,12 @@ def load_library():
             "mcb_packed_positions": ([P, i64, P, P], ctypes.c_int),
             "mcb_packed_free": ([P], ctypes.c_int),
             "mcb_replay": ([P, P, P, i32, P, i32, P, P, P, P], ctypes.c_int),
-            "mcb_replay_host": ([P, P, P, i32, P, i32, P, P, P], ctypes.c_int),
+            "mcb_replay_host": ([P, P, P, i32, P, i32, P, P, P, P], ctypes.c_int),
+            "mcb_set_timing": ([P, i32], ctypes.c_int),
+            "mcb_last_timings": ([P, P, i32], ctypes.c_int),
             "mcb_next_use": ([P, P, P, P], ctypes.c_int),
             "mcb_score": ([P, P, P, i32, P, P, P], ctypes.c_int),
-            "mcb_router_topk": ([P, P, P, i64, i32, i32, i32, i32, P, P, P, P], ctypes.c_int),
+            "mcb_router_topk": ([P, P, P, i64, i32, i32, i32, i32, P, P, P], ctypes.c_int),
         }
         for name, (argt, rest) in sig.items():
             fn = getattr(lib, name)

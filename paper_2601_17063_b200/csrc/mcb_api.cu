@@ -79,7 +79,32 @@ struct mcb_ctx {
     cudaStream_t stream = nullptr;
     int64_t last_kernels = 0;
     int64_t last_uncertain = 0;
+    bool timing = false;
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 };
+
+static void mark(mcb_ctx *c, int i, cudaStream_t s) {
+    if (c->timing) cudaEventRecord(c->ev[i], s);
+}
+
+extern "C" int mcb_set_timing(mcb_ctx *c, int32_t enable) {
+    mcb_clear_error();
+    if (!c) return mcb_set_error(MCB_ERR_INVALID, "ctx is NULL");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (enable && !c->ev[0])
+        for (auto &e : c->ev) CUDA_TRY(cudaEventCreate(&e));
+    c->timing = enable != 0;
+    return MCB_OK;
+}
+
+extern "C" int mcb_last_timings(mcb_ctx *c, float *ms, int32_t n) {
+    mcb_clear_error();
+    if (!c || !ms) return mcb_set_error(MCB_ERR_INVALID, "ctx / ms is NULL");
+    if (!c->timing) return mcb_set_error(MCB_ERR_INVALID, "timing is not enabled");
+    for (int i = 0; i < n && i < 4; ++i) CUDA_TRY(cudaEventElapsedTime(&ms[i], c->ev[i], c->ev[i + 1]));
+    return MCB_OK;
+}
 
 extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     mcb_clear_error();
@@ -112,6 +137,8 @@ extern "C" int mcb_ctx_destroy(mcb_ctx *c) {
                      &c->h_chain_reports, &c->h_hashes, &c->h_outcomes};
     for (DevBuf *b : all) b->release();
     if (c->stream) cudaStreamDestroy(c->stream);
+    for (auto &e : c->ev)
+        if (e) cudaEventDestroy(e);
     delete c;
     return MCB_OK;
 }
@@ -174,7 +201,7 @@ static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int in
     if (int rc = c->wt.ensure(per * nets->num_nets * sizeof(double))) return rc;
     *launched += launch_prepare_nets(nets->params, E, H, nets->num_nets, (double *)c->wt.p, s);
     const int64_t tiles = max_score_tiles(d);
-    if (int rc = c->snaps.ensure((size_t)(tiles + 1) * (2 * E + 4) * sizeof(int32_t))) return rc;
+    if (int rc = c->snaps.ensure((size_t)(tiles + 1) * (4 * E + 8) * sizeof(int32_t))) return rc;
     if (int rc = c->tile_off.ensure((size_t)(d.n_chains + 1) * sizeof(int64_t))) return rc;
     const int n = launch_score(d, (const double *)c->wt.p, H, nets->num_nets, include_prefill, ranks, scores,
                                (int32_t *)c->snaps.p, (int64_t *)c->tile_off.p, tiles,
@@ -264,11 +291,13 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     P.loads_serial = cost->loads_serial;
     P.window = cost->window;
 
+    mark(c, 0, s);
     if (need_next) {
         if (int rc = c->next_pos.ensure((size_t)(d.total_acc + 64) * sizeof(uint32_t))) return rc;
         launched += launch_next_use(d, (uint32_t *)c->next_pos.p, s);
         P.next_pos = (const uint32_t *)c->next_pos.p;
     }
+    mark(c, 1, s);
     for (int v = 0; v < 2; ++v) {
         if (!need_ml[v]) continue;
         if (int rc = c->ranks[v].ensure((size_t)d.total_events * d.E + 64)) return rc;
@@ -287,8 +316,11 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     P.inst_lat = (double *)c->inst_lat.p;
     P.hashes = out->hashes;
     P.outcomes = out->outcomes;
+    mark(c, 2, s);
     launched += launch_replay(P, s);
+    mark(c, 3, s);
     launched += launch_fold(P, t->num_traces, out->reports, out->latency, s);
+    mark(c, 4, s);
     CUDA_TRY(cudaGetLastError());
     c->last_kernels = launched;
     return MCB_OK;
@@ -316,14 +348,14 @@ static int upload(DevBuf &b, const T *src, size_t count, size_t pad_bytes, cudaS
 
 extern "C" int mcb_replay_host(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, int32_t n_pol,
                                const int32_t *caps, int32_t n_cap, const mcb_cost *cost, const mcb_nets *nets,
-                               const mcb_outputs *out) {
+                               const mcb_outputs *out, void *stream) {
     mcb_clear_error();
     if (!c) return mcb_set_error(MCB_ERR_INVALID, "ctx is NULL");
     if (int rc = check_trace(t)) return rc;
     if (!out || !out->reports || !out->latency) return mcb_set_error(MCB_ERR_INVALID, "outputs are NULL");
     std::lock_guard<std::mutex> lk(c->mu);
     CUDA_TRY(cudaSetDevice(c->device));
-    cudaStream_t s = c->stream;
+    cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
     mcb_trace dt = *t;
     const DevTrace d = make_dev_trace(t);
     const int64_t n_chains = d.n_chains;

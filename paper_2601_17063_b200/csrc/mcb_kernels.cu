@@ -175,6 +175,12 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
     const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
     uint16_t *outc = P.outcomes ? P.outcomes + ((int64_t)pol_i * P.n_cap + cap_i) * tr.total_acc : nullptr;
 
+    uint32_t nrow[EPL];
+#pragma unroll
+    for (int s = 0; s < EPL; ++s) {
+        const int e = glane * EPL + s;
+        nrow[s] = (POL == POL_ML && n_ev > 0 && e < E) ? (uint32_t)__ldg(rank + e0 * E + e) : 0u;
+    }
     uint32_t pos = 0, dec = 0;
     for (int64_t ev = 0; ev < n_ev; ++ev) {
         const uint32_t info = UNIFORM ? mcb_ev_pack((uint32_t)tr.K, (uint32_t)tr.K, true, ev == 0)
@@ -187,13 +193,13 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
             for (int s = 0; s < EPL; ++s) key[s] = 0;
         }
         if (POL == POL_ML) {
-            // per-event score ranks (mlpolicy.py:59-62): argmax score == argmin (256 - rank)
-            const uint8_t *row = rank + (e0 + ev) * E;
+            // per-event score ranks (mlpolicy.py:59-62): argmax score == argmin (256 - rank);
+            // the next event's row is already in flight (prefetched one event ahead)
 #pragma unroll
             for (int s = 0; s < EPL; ++s) {
+                key[s] = nrow[s] ? 256u - nrow[s] : KEY_SENT;
                 const int e = glane * EPL + s;
-                const uint32_t r = e < E ? (uint32_t)__ldg(row + e) : 0u;
-                key[s] = r ? 256u - r : KEY_SENT;
+                nrow[s] = (ev + 1 < n_ev && e < E) ? (uint32_t)__ldg(rank + (e0 + ev + 1) * E + e) : 0u;
             }
         }
         pin = 0;
@@ -311,6 +317,238 @@ __global__ void __launch_bounds__(128) k_replay(const __grid_constant__ ReplayPa
     }
 }
 
+// ---------------------------------------------------------------------------
+// K4-solo: one THREAD per cache instance, for num_experts <= 16.  All state
+// (resident / pinned / seen bitmasks, the EM per-expert keys and pending
+// refetch marks, counters) lives in registers, so an access costs no
+// cross-lane traffic; the victim is a register min-tree over packed
+// (key << 8 | expert) values, i.e. argmin of (key, id) over resident \ pinned.
+// blockIdx.y selects the policy, so a warp never diverges on policy; the
+// threads of a warp share chains (consecutive capacities of one chain), so
+// their id / next-use / rank loads coalesce into broadcasts.
+// ---------------------------------------------------------------------------
+template <int EM>
+__device__ __forceinline__ uint64_t min_tree(const uint64_t (&k)[EM]) {
+    uint64_t t[EM];
+#pragma unroll
+    for (int s = 0; s < EM; ++s) t[s] = k[s];
+#pragma unroll
+    for (int w = EM / 2; w >= 1; w /= 2)
+#pragma unroll
+        for (int s = 0; s < w; ++s) t[s] = t[s] < t[s + w] ? t[s] : t[s + w];
+    return t[0];
+}
+
+__device__ __forceinline__ uint32_t sel4(const uint4 &v, uint32_t i) {
+    uint32_t r = v.x;
+    r = i == 1 ? v.y : r;
+    r = i == 2 ? v.z : r;
+    r = i == 3 ? v.w : r;
+    return r;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+template <int EM>
+struct Solo {
+    static constexpr int SH = EM == 8 ? 3 : 4;                 // id bits in a packed key
+    static constexpr uint32_t KMAX = (1u << (32 - SH)) - 1u;   // keys must stay below this
+};
+
+template <int EM, int POL, bool UNIFORM>
+__device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t chain, int pol_i, int cap_i, int ml_variant,
+                                              uint32_t *s_pk, uint32_t *s_pend) {
+    constexpr int SH = Solo<EM>::SH;
+    constexpr uint32_t KMAX = Solo<EM>::KMAX;
+    const DevTrace &tr = P.tr;
+    const int tid = threadIdx.x;
+    const uint32_t C = (uint32_t)P.cap[cap_i];
+    const int E = tr.E;
+    const int64_t inst = (chain * P.n_pol + pol_i) * P.n_cap + cap_i;
+    // per-thread columns of packed keys (key << SH | id) and pending-refetch marks
+    uint32_t *pk = s_pk + tid;      // pk[s * 128]
+    uint32_t *pd = s_pend + tid;    // pd[s * 128]
+#pragma unroll
+    for (int s = 0; s < EM; ++s) { pk[s * 128] = (uint32_t)s; pd[s * 128] = 0u; }
+
+    uint32_t res = 0, pin = 0, seen = 0, valid = (1u << E) - 1u;
+    uint32_t mlk[EM];
+#pragma unroll
+    for (int s = 0; s < EM; ++s) mlk[s] = ~0u;
+    uint32_t count = 0, ph = 0, pm = 0, dh = 0, dm = 0, nev = 0, comp = 0, refc = 0;
+    double dlat = 0.0, plat = 0.0;
+    uint64_t h = MCB_FNV_OFF;
+    int status = MCB_OK;
+
+    const int64_t a0 = tr.acc_begin(chain);
+    const int64_t e0 = tr.ev_begin(chain);
+    const int64_t n_ev = tr.ev_end(chain) - e0;
+    const int64_t a_end = tr.acc_end(chain);
+    const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
+    uint16_t *outc = P.outcomes ? P.outcomes + ((int64_t)pol_i * P.n_cap + cap_i) * tr.total_acc : nullptr;
+
+    // id stream: 16-byte chunks, current + next in registers, L2 prefetch 512 B ahead
+    const uint4 *ids16 = (const uint4 *)tr.acc;
+    int64_t ich = a0 >> 4;
+    uint4 icur = __ldg(ids16 + ich), inxt = __ldg(ids16 + ich + 1);
+    // Belady next-use stream: 4 positions per chunk
+    const uint4 *np16 = (const uint4 *)P.next_pos;
+    int64_t nch = a0 >> 2;
+    uint4 ncur = make_uint4(0, 0, 0, 0), nnxt = make_uint4(0, 0, 0, 0);
+    if (POL == POL_BELADY) { ncur = __ldg(np16 + nch); nnxt = __ldg(np16 + nch + 1); }
+    // ML rank rows, one event ahead
+    uint32_t rrow[EM];
+#pragma unroll
+    for (int s = 0; s < EM; ++s) rrow[s] = (POL == POL_ML && n_ev > 0 && s < E) ? __ldg(rank + e0 * E + s) : 0u;
+    uint32_t info_next = (!UNIFORM && n_ev > 0) ? __ldg(tr.ev_info + e0) : 0u;
+
+    int64_t A = a0;
+    uint32_t pos = 0, dec = 0;
+    for (int64_t ev = 0; ev < n_ev; ++ev) {
+        uint32_t info;
+        if (UNIFORM) {
+            info = mcb_ev_pack((uint32_t)tr.K, (uint32_t)tr.K, true, ev == 0);
+        } else {
+            info = info_next;
+            info_next = ev + 1 < n_ev ? __ldg(tr.ev_info + e0 + ev + 1) : 0u;
+        }
+        const uint32_t nacc = mcb_ev_nacc(info);
+        const bool decode = UNIFORM ? true : mcb_ev_decode(info);
+        if (POL == POL_LFU && !UNIFORM && mcb_ev_newseq(info)) {
+#pragma unroll
+            for (int s = 0; s < EM; ++s) pk[s * 128] = (uint32_t)s;   // start_sequence (policies.py:184-185)
+        }
+        if (POL == POL_ML) {
+            valid = 0;
+#pragma unroll
+            for (int s = 0; s < EM; ++s) {
+                mlk[s] = ((256u - rrow[s]) << SH) | (uint32_t)s;
+                valid |= (rrow[s] != 0u ? 1u : 0u) << s;
+                rrow[s] = (ev + 1 < n_ev && s < E) ? __ldg(rank + (e0 + ev + 1) * E + s) : 0u;
+            }
+        }
+        pin = 0;
+        uint32_t step_miss = 0;
+        for (uint32_t j = 0; j < nacc; ++j, ++pos, ++A) {
+            if ((A >> 4) != ich) {
+                ++ich;
+                icur = inxt;
+                inxt = __ldg(ids16 + ich + 1);
+                if ((ich & 7) == 0 && ((ich + 32) << 4) < a_end) prefetch_l2(ids16 + ich + 32);
+            }
+            const uint32_t x = (sel4(icur, (uint32_t)(A >> 2) & 3u) >> (8u * (uint32_t)(A & 3))) & 0xFFu;
+            const uint32_t bit = 1u << x;
+            const bool hit = (res & bit) != 0u;
+            if (POL == POL_BELADY) {
+                if ((A >> 2) != nch) {
+                    ++nch;
+                    ncur = nnxt;
+                    nnxt = __ldg(np16 + nch + 1);
+                    if ((nch & 7) == 0 && ((nch + 64) << 2) < a_end) prefetch_l2(np16 + nch + 64);
+                }
+                const uint32_t np = sel4(ncur, (uint32_t)A & 3u);
+                // farthest next use first: key = KMAX - next_pos, never used again -> 0
+                pk[x * 128] = ((np == MCB_NEXT_INF ? 0u : KMAX - np) << SH) | x;
+            }
+            if (POL == POL_LRU) pk[x * 128] = (pos << SH) | x;
+            if (POL == POL_LFU) pk[x * 128] += 1u << SH;
+            uint32_t code = MCB_OUT_HIT;
+            if (hit) {
+                if (decode) ++dh; else ++ph;
+            } else {
+                if (decode) ++dm; else ++pm;
+                ++step_miss;
+                if (count >= C) {
+                    const uint32_t cand = res & ~pin & valid;
+                    uint32_t t[EM];
+#pragma unroll
+                    for (int s = 0; s < EM; ++s) {
+                        const uint32_t k = (POL == POL_ML) ? mlk[s] : pk[s * 128];
+                        t[s] = ((cand >> s) & 1u) ? k : ~0u;
+                    }
+#pragma unroll
+                    for (int w = EM / 2; w >= 1; w /= 2)
+#pragma unroll
+                        for (int s = 0; s < w; ++s) t[s] = min(t[s], t[s + w]);
+                    if (t[0] == ~0u) { status = MCB_ERR_NO_EVICTABLE; break; }
+                    const uint32_t v = t[0] & (uint32_t)(EM - 1);
+                    res &= ~(1u << v);
+                    pd[v * 128] = dec + 1u;
+                    code = v;
+                    ++nev;
+                } else {
+                    ++count;
+                    code = MCB_OUT_MISS;
+                }
+                if (!(seen & bit)) {
+                    ++comp;
+                } else {
+                    const uint32_t pe = pd[x * 128];
+                    if (pe && (int64_t)dec - (int64_t)(pe - 1u) <= (int64_t)P.window) ++refc;
+                }
+                pd[x * 128] = 0u;
+                seen |= bit;
+                res |= bit;
+            }
+            if (decode) pin |= bit;
+            if (outc) {
+                h = fnv16(h, code);
+                outc[A] = (uint16_t)code;
+            } else if (P.hashes) {
+                h = fnv16(h, code);
+            }
+        }
+        if (status != MCB_OK) break;
+        double lat;
+        if (step_miss > 0)
+            lat = __dmul_rn((double)(P.loads_serial ? step_miss : 1u), P.t_load);
+        else
+            lat = __dmul_rn((double)nacc, P.t_compute);
+        if (decode) dlat = __dadd_rn(dlat, __dadd_rn(lat, POL == POL_ML ? P.ml_cost : 0.0));
+        else plat = __dadd_rn(plat, lat);
+        if (decode) ++dec;
+    }
+    int64_t *o = P.inst_out + inst * MCB_R_N;
+    o[MCB_R_PREFILL_HITS] = ph;
+    o[MCB_R_PREFILL_MISSES] = pm;
+    o[MCB_R_DECODE_HITS] = dh;
+    o[MCB_R_DECODE_MISSES] = dm;
+    o[MCB_R_COMPULSORY] = comp;
+    o[MCB_R_EVICTIONS] = nev;
+    o[MCB_R_REFETCHED] = refc;
+    o[MCB_R_STATUS] = status;
+    P.inst_lat[inst * 2 + 0] = dlat;
+    P.inst_lat[inst * 2 + 1] = plat;
+    if (P.hashes) P.hashes[inst] = h;
+}
+
+template <int EM, bool UNIFORM>
+__global__ void __launch_bounds__(128) k_replay_solo(const __grid_constant__ ReplayParams P) {
+    __shared__ uint32_t s_pk[EM * 128], s_pend[EM * 128];
+    const int pol_i = blockIdx.y;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= P.tr.n_chains * P.n_cap) return;
+    const int cap_i = (int)(t % P.n_cap);
+    const int64_t chain = t / P.n_cap;
+    switch (P.pol[pol_i]) {
+        case MCB_LRU: solo_instance<EM, POL_LRU, UNIFORM>(P, chain, pol_i, cap_i, 0, s_pk, s_pend); break;
+        case MCB_LFU: solo_instance<EM, POL_LFU, UNIFORM>(P, chain, pol_i, cap_i, 0, s_pk, s_pend); break;
+        case MCB_BELADY: solo_instance<EM, POL_BELADY, UNIFORM>(P, chain, pol_i, cap_i, 0, s_pk, s_pend); break;
+        case MCB_ML: solo_instance<EM, POL_ML, UNIFORM>(P, chain, pol_i, cap_i, 0, s_pk, s_pend); break;
+        default: solo_instance<EM, POL_ML, UNIFORM>(P, chain, pol_i, cap_i, 1, s_pk, s_pend); break;
+    }
+}
+
+template <int EM>
+static void launch_solo_t(const ReplayParams &p, cudaStream_t s) {
+    const int64_t n = p.tr.n_chains * p.n_cap;
+    const dim3 grid((unsigned)((n + 127) / 128), (unsigned)p.n_pol);
+    if (p.tr.uniform) k_replay_solo<EM, true><<<grid, 128, 0, s>>>(p);
+    else k_replay_solo<EM, false><<<grid, 128, 0, s>>>(p);
+}
+
 template <int G, int EPL>
 static void launch_replay_t(const ReplayParams &p, cudaStream_t s) {
     const int64_t n_inst = p.tr.n_chains * p.n_pol * p.n_cap;
@@ -323,7 +561,11 @@ static void launch_replay_t(const ReplayParams &p, cudaStream_t s) {
 int launch_replay(const ReplayParams &p, cudaStream_t s) {
     if (p.tr.n_chains * p.n_pol * p.n_cap == 0) return 0;
     const int E = p.tr.E;
-    if (E <= 8) launch_replay_t<8, 1>(p, s);
+    // solo kernels pack (key << 3|4 | id) into 32 bits: chains must stay below 2^28 accesses
+    const bool solo_ok = p.tr.total_acc < (1ll << 27);
+    if (E <= 8 && solo_ok) launch_solo_t<8>(p, s);
+    else if (E <= 16 && solo_ok) launch_solo_t<16>(p, s);
+    else if (E <= 8) launch_replay_t<8, 1>(p, s);
     else if (E <= 16) launch_replay_t<16, 1>(p, s);
     else if (E <= 32) launch_replay_t<32, 1>(p, s);
     else if (E <= 64) launch_replay_t<32, 2>(p, s);
@@ -497,7 +739,7 @@ __global__ void __launch_bounds__(128) k_feat_snap(DevTrace tr, int include_pref
                 if ((x & 31) == lane) {
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
-                        if ((x >> 5) == j) { last[j] = u; ++f[j]; }
+                        { const bool hit_j = (x >> 5) == j; last[j] = hit_j ? u : last[j]; f[j] += hit_j ? 1 : 0; }
                 }
             }
         }
@@ -512,62 +754,151 @@ __device__ __forceinline__ double sigmoid_ref(double z) {
     return ez / (1.0 + ez);
 }
 
-// Out[i][col] = act(sum_k A[i][k] * Wt[k][col] + b[col]) for the tile's 32
-// events; warp w owns events 4w..4w+3, lane owns columns lane + 32 j.
-// Fixed summation order: k ascending, fma, then + bias.
-template <int NJ>
-__device__ __forceinline__ void mlp_layer(const double *A, int lda, int Din, const double *__restrict__ Wt,
-                                          const double *__restrict__ bias, int Dout, double *Out, int ldo,
-                                          bool act) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    double accu[4][NJ];
+// Uniform traces (decode-only, one sequence per chain): the tracker state at
+// a tile start is a prefix over earlier tiles, computed in two parallel
+// passes instead of one sequential walk per chain:
+//   k_tile_summary  one warp per tile: per-expert routing count in the tile
+//                   and the 1-based index of its last routing in the tile
+//   k_snap_scan     one warp per chain: exclusive scan over its tiles ->
+//                   snapshot (last update index, count, u) at every tile start
+__global__ void __launch_bounds__(128) k_tile_summary(DevTrace tr, int32_t *__restrict__ summ) {
+    const int lane = threadIdx.x & 31;
+    const int64_t tile = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int64_t tpc = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
+    if (tile >= tr.n_chains * tpc) return;
+    const int64_t c = tile / tpc, ev0 = (tile % tpc) * MCB_TILE_EV;
+    const int nev = (int)min((int64_t)MCB_TILE_EV, tr.T - ev0);
+    const int E = tr.E, K = tr.K;
+    int32_t cnt[4] = {0, 0, 0, 0}, last[4] = {0, 0, 0, 0};
+    const uint8_t *ids = tr.acc + (c * tr.T + ev0) * K;
+    for (int i = 0; i < nev; ++i) {
+        for (int k = 0; k < K; ++k) {
+            const int x = __ldg(ids + i * K + k);
+            if ((x & 31) == lane) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+                for (int j = 0; j < 4; ++j)
+                    { const bool hit_j = (x >> 5) == j; cnt[j] += hit_j ? 1 : 0; last[j] = hit_j ? i + 1 : last[j]; }
+            }
+        }
+    }
+    int32_t *o = summ + tile * 2 * E;
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) accu[i][j] = 0.0;
-    for (int k = 0; k < Din; ++k) {
-        double a[4];
+    for (int j = 0; j < 4; ++j) {
+        const int e = lane + 32 * j;
+        if (e < E) { o[e] = cnt[j]; o[E + e] = last[j]; }
+    }
+}
+
+__global__ void __launch_bounds__(128) k_snap_scan(DevTrace tr, const int32_t *__restrict__ summ,
+                                                   int32_t *__restrict__ snaps) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (c >= tr.n_chains) return;
+    const int E = tr.E, SN = 2 * E + 4;
+    const int64_t tpc = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
+    int32_t last[4] = {-1, -1, -1, -1}, f[4] = {0, 0, 0, 0};
+    int32_t u = 0;
+    for (int64_t t = 0; t < tpc; ++t) {
+        const int64_t tile = c * tpc + t;
+        int32_t *sp = snaps + tile * SN;
+        const int32_t *sm = summ + tile * 2 * E;
+        int32_t sc[4], sl[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = A[(w * 4 + i) * lda + k];
-        double wv[NJ];
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-            const int col = lane + 32 * j;
-            wv[j] = col < Dout ? __ldg(Wt + (int64_t)k * Dout + col) : 0.0;
+        for (int j = 0; j < 4; ++j) {
+            const int e = lane + 32 * j;
+            sc[j] = e < E ? __ldg(sm + e) : 0;
+            sl[j] = e < E ? __ldg(sm + E + e) : 0;
+            if (e < E) { sp[e] = last[j]; sp[E + e] = f[j]; }
+        }
+        if (lane == 0) {
+            const int64_t rt = t * MCB_TILE_EV * (int64_t)tr.K;
+            sp[2 * E] = u; sp[2 * E + 1] = (int32_t)(rt & 0xFFFFFFFF); sp[2 * E + 2] = (int32_t)(rt >> 32);
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < NJ; ++j) accu[i][j] = fma(a[i], wv[j], accu[i][j]);
+        for (int j = 0; j < 4; ++j) {
+            f[j] += sc[j];
+            if (sl[j] > 0) last[j] = u + sl[j];
+        }
+        u += (int32_t)min((int64_t)MCB_TILE_EV, tr.T - t * MCB_TILE_EV);
     }
+}
+
+// Out^T[col][i] = act(sum_k A^T[k][i] * Wt[k][col] + b[col]) for the tile's
+// 64 events.  256 threads = NG = 64/EVT event groups x (256/NG) column
+// slots; a thread owns EVT consecutive events x CT consecutive columns per
+// pass (EVT*CT independent float64 FMA chains).  The shape is chosen per
+// layer so every thread has work even for narrow layers (E = 8 outputs).
+// Fixed summation order per output: k ascending (fma), then + bias --
+// identical for every event, so identical inputs give identical scores.
+template <int EVT, int CT>
+__device__ __forceinline__ void mlp_layer_tt(const double *At, int Din, const double *__restrict__ Wt,
+                                             const double *__restrict__ bias, int Dout, double *Ot, bool act) {
+    constexpr int NG = MCB_TILE_EV / EVT;
+    constexpr int NSLOT = 256 / NG;
+    const int eg = threadIdx.x % NG, cs = threadIdx.x / NG;
+    for (int p0 = 0; p0 < Dout; p0 += NSLOT * CT) {
+        const int c0 = p0 + cs * CT;
+        if (c0 >= Dout) continue;
+        double acc[EVT][CT];
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-        const int col = lane + 32 * j;
-        if (col < Dout) {
-            const double b = __ldg(bias + col);
+        for (int i = 0; i < EVT; ++i)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const double z = __dadd_rn(accu[i][j], b);
-                Out[(w * 4 + i) * ldo + col] = act ? __dmul_rn(z, sigmoid_ref(z)) : z;
+            for (int j = 0; j < CT; ++j) acc[i][j] = 0.0;
+        const bool full = c0 + CT - 1 < Dout;
+        for (int k = 0; k < Din; ++k) {
+            const double2 *arow = (const double2 *)(At + k * MCB_TILE_EV + eg * EVT);
+            double a[EVT];
+#pragma unroll
+            for (int q = 0; q < EVT / 2; ++q) {
+                const double2 v = arow[q];
+                a[2 * q] = v.x;
+                a[2 * q + 1] = v.y;
+            }
+            const double *wr = Wt + (int64_t)k * Dout + c0;
+            double wv[CT];
+#pragma unroll
+            for (int j = 0; j < CT; ++j) wv[j] = (full || c0 + j < Dout) ? __ldg(wr + j) : 0.0;
+#pragma unroll
+            for (int i = 0; i < EVT; ++i)
+#pragma unroll
+                for (int j = 0; j < CT; ++j) acc[i][j] = fma(a[i], wv[j], acc[i][j]);
+        }
+#pragma unroll
+        for (int j = 0; j < CT; ++j) {
+            const int col = c0 + j;
+            if (col < Dout) {
+                const double b = __ldg(bias + col);
+                double2 *orow = (double2 *)(Ot + col * MCB_TILE_EV + eg * EVT);
+#pragma unroll
+                for (int q = 0; q < EVT / 2; ++q) {
+                    const double z0 = __dadd_rn(acc[2 * q][j], b), z1 = __dadd_rn(acc[2 * q + 1][j], b);
+                    double2 v;
+                    v.x = act ? __dmul_rn(z0, sigmoid_ref(z0)) : z0;
+                    v.y = act ? __dmul_rn(z1, sigmoid_ref(z1)) : z1;
+                    orow[q] = v;
+                }
             }
         }
     }
 }
 
-__device__ void mlp_layer_any(const double *A, int lda, int Din, const double *Wt, const double *bias, int Dout,
-                              double *Out, int ldo, bool act) {
-    if (Dout <= 32) mlp_layer<1>(A, lda, Din, Wt, bias, Dout, Out, ldo, act);
-    else if (Dout <= 64) mlp_layer<2>(A, lda, Din, Wt, bias, Dout, Out, ldo, act);
-    else if (Dout <= 128) mlp_layer<4>(A, lda, Din, Wt, bias, Dout, Out, ldo, act);
-    else mlp_layer<8>(A, lda, Din, Wt, bias, Dout, Out, ldo, act);
+__device__ __forceinline__ void mlp_layer_t(const double *At, int Din, const double *Wt, const double *bias, int Dout,
+                                            double *Ot, bool act) {
+    if (Dout >= 128) mlp_layer_tt<8, 4>(At, Din, Wt, bias, Dout, Ot, act);
+    else if (Dout >= 64) mlp_layer_tt<8, 2>(At, Din, Wt, bias, Dout, Ot, act);
+    else if (Dout >= 32) mlp_layer_tt<4, 2>(At, Din, Wt, bias, Dout, Ot, act);
+    else if (Dout >= 16) mlp_layer_tt<4, 1>(At, Din, Wt, bias, Dout, Ot, act);
+    else mlp_layer_tt<2, 1>(At, Din, Wt, bias, Dout, Ot, act);
 }
 
-// One block (256 threads) per (chain, tile of 32 events): rebuild the
-// features of each event from the tile snapshot, run the float64 MLP
-// (EvictionNet.forward, net.py:88-105), and rank every expert's score within
-// its event: rank = 1 + #{selectable j : s_j < s_e} for selectable e (s > -inf),
-// 0 otherwise (NaN / -inf are never evicted, mlpolicy.py:15-26).  Argmax of
-// score with lowest-id ties == argmax of rank with lowest-id ties.
+// One block (256 threads) per (chain, tile of 64 events): warp 0 rebuilds
+// the features of each event from the tile snapshot (features.py:34-52:
+// [1/r || f / max_f]), the block runs the float64 MLP (EvictionNet.forward,
+// net.py:88-105) in the transposed layout above, and ranks every expert's
+// score within its event: rank = 1 + #{selectable j : s_j < s_e} for
+// selectable e (s > -inf), 0 otherwise (NaN / -inf are never evicted,
+// mlpolicy.py:15-26).  argmax score with lowest-id ties == argmax rank with
+// lowest-id ties.
 __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *__restrict__ wt_all, int H,
                                                      int num_nets, int include_prefill,
                                                      const int64_t *__restrict__ tile_off,
@@ -576,17 +907,15 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
                                                      unsigned long long *uncertain) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int E = tr.E, D = 2 * E;
-    const int lda = D > H ? D : H;
-    const int ldb = H > E ? H : E;
-    double *bufA = (double *)smem_raw;                       // [TILE][lda]
-    double *bufB = bufA + MCB_TILE_EV * lda;                 // [TILE][ldb]
-    int32_t *s_last = (int32_t *)(bufB + MCB_TILE_EV * ldb); // [E]
-    int32_t *s_f = s_last + MCB_MAX_EXPERTS;                 // [E]
-    int32_t *s_flag = s_f + MCB_MAX_EXPERTS;                 // [TILE]
+    const int ra = D > H ? D : H;
+    const int rb = H > E ? H : E;
+    double *bufA = (double *)smem_raw;                    // [ra][TILE]
+    double *bufB = bufA + ra * MCB_TILE_EV;               // [rb][TILE]
+    uint8_t *s_rank = (uint8_t *)(bufB + rb * MCB_TILE_EV);  // [TILE][E]
+    int32_t *s_flag = (int32_t *)(s_rank + MCB_TILE_EV * MCB_MAX_EXPERTS);  // [TILE]
 
     const int64_t tile = blockIdx.x;
     if (tile >= n_tiles) return;
-    // locate the chain
     int64_t c, tile_in_chain;
     if (tr.uniform) {
         const int64_t tpc = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
@@ -594,7 +923,7 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
         tile_in_chain = tile % tpc;
     } else {
         if (tile >= tile_off[tr.n_chains]) return;  // grid is an upper bound in general mode
-        int64_t lo = 0, hi = tr.n_chains;  // largest c with tile_off[c] <= tile
+        int64_t lo = 0, hi = tr.n_chains;          // largest c with tile_off[c] <= tile
         while (hi - lo > 1) {
             const int64_t mid = (lo + hi) / 2;
             if (tile_off[mid] <= tile) lo = mid; else hi = mid;
@@ -604,56 +933,113 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
     }
     const int64_t e0 = tr.ev_begin(c);
     const int64_t ev0 = tile_in_chain * MCB_TILE_EV;
-    const int64_t n_ev_chain = tr.ev_end(c) - e0;
-    const int nev = (int)min((int64_t)MCB_TILE_EV, n_ev_chain - ev0);
-    const int SN = snap_stride(E);
-    const int32_t *sp = snaps + tile * SN;
-    const int tid = threadIdx.x;
-    for (int e = tid; e < E; e += blockDim.x) { s_last[e] = sp[e]; s_f[e] = sp[E + e]; }
-    int32_t u = sp[2 * E];
-    int64_t rt = (int64_t)(uint32_t)sp[2 * E + 1] | ((int64_t)sp[2 * E + 2] << 32);
-    const uint8_t *routed = tr.routed_ptr() + tr.rt_begin(c);
-    __syncthreads();
-    // max frequency at the tile start
-    int32_t maxf = 0;
-    for (int e = 0; e < E; ++e) maxf = max(maxf, s_f[e]);
+    const int nev = (int)min((int64_t)MCB_TILE_EV, tr.ev_end(c) - e0 - ev0);
+    const int tid = threadIdx.x, lane = tid & 31;
 
-    for (int i = 0; i < MCB_TILE_EV; ++i) {
-        if (i < nev) {
-            const uint32_t info = tr.info(c, e0 + ev0 + i);
-            const uint32_t nrt = mcb_ev_nrt(info);
-            const bool newseq = mcb_ev_newseq(info);
-            const bool upd = mcb_ev_decode(info) || include_prefill;
-            if (newseq) { u = 0; maxf = 0; }
-            if (upd) ++u;
-            for (int e = tid; e < E; e += blockDim.x) {
-                int32_t l = newseq ? -1 : s_last[e];
-                int32_t fe = newseq ? 0 : s_f[e];
-                if (upd) {
-                    for (uint32_t r = 0; r < nrt; ++r)
-                        if (__ldg(routed + rt + r) == e) { l = u; ++fe; }
+    if (tr.uniform) {
+        // decode-only single sequence: every event updates, no resets, so the
+        // tracker state at event i is the snapshot plus in-tile prefix counts
+        // (features.py:34-39): thread i sets bit i of occ[e] for its routed e.
+        unsigned long long *occ = (unsigned long long *)s_rank;   // [E] (s_rank reused before ranking)
+        int32_t *pmax = s_flag;                                    // [TILE]
+        const int32_t *sp = snaps + tile * (2 * E + 4);
+        const int32_t u0 = sp[2 * E];
+        for (int e = tid; e < E; e += blockDim.x) occ[e] = 0ull;
+        __syncthreads();
+        const uint8_t *ids = tr.acc + (c * tr.T + ev0) * tr.K;
+        if (tid < nev)
+            for (int k = 0; k < tr.K; ++k) atomicOr(&occ[__ldg(ids + tid * tr.K + k)], 1ull << tid);
+        __syncthreads();
+        if (tid < MCB_TILE_EV) {
+            int32_t m = 0;
+            if (tid < nev) {
+                const unsigned long long upto = tid == 63 ? ~0ull : ((2ull << tid) - 1ull);
+                for (int k = 0; k < tr.K; ++k) {
+                    const int x = __ldg(ids + tid * tr.K + k);
+                    m = max(m, sp[E + x] + __popcll(occ[x] & upto));
                 }
-                s_last[e] = l;
-                s_f[e] = fe;
             }
-            __syncthreads();
-            if (upd)
-                for (uint32_t r = 0; r < nrt; ++r) maxf = max(maxf, s_f[__ldg(routed + rt + r)]);
-            rt += nrt;
-            // features (features.py:44-52): [1/r || f / max_f]
-            for (int k = tid; k < D; k += blockDim.x) {
-                double v;
-                if (k < E) {
-                    const int32_t l = s_last[k];
-                    v = l < 0 ? 0.0 : 1.0 / (double)(u - l + 1);
-                } else {
-                    v = maxf > 0 ? (double)s_f[k - E] / (double)maxf : 0.0;
+            pmax[tid] = m;
+        }
+        __syncthreads();
+        if (tid < 32) {   // inclusive prefix max over the 64 events, then max with the snapshot max_f
+            int32_t a = pmax[2 * tid], b = max(a, pmax[2 * tid + 1]);
+            int32_t m0 = 0;
+            for (int e = 0; e < E; ++e) m0 = max(m0, sp[E + e]);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t t = __shfl_up_sync(FULL_MASK, b, o);
+                if (tid >= o) { a = max(a, t); b = max(b, t); }
+            }
+            pmax[2 * tid] = max(a, m0);
+            pmax[2 * tid + 1] = max(b, m0);
+        }
+        __syncthreads();
+        for (int q = tid; q < MCB_TILE_EV * E; q += blockDim.x) {
+            const int i = q % MCB_TILE_EV, e = q / MCB_TILE_EV;
+            double rv = 0.0, fv = 0.0;
+            if (i < nev) {
+                const unsigned long long seen = occ[e] & (i == 63 ? ~0ull : ((2ull << i) - 1ull));
+                const int32_t f = sp[E + e] + __popcll(seen);
+                const int32_t lastu = seen ? u0 + (63 - __clzll(seen)) + 1 : sp[e];
+                const int32_t u = u0 + i + 1;
+                rv = lastu < 0 ? 0.0 : 1.0 / (double)(u - lastu + 1);
+                const int32_t mf = pmax[i];
+                fv = mf > 0 ? (double)f / (double)mf : 0.0;
+            }
+            bufA[e * MCB_TILE_EV + i] = rv;
+            bufA[(E + e) * MCB_TILE_EV + i] = fv;
+        }
+    } else if (tid < 32) {
+        const int32_t *sp = snaps + tile * (2 * E + 4);
+        int32_t last[4], f[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int e = lane + 32 * j;
+            last[j] = e < E ? sp[e] : -1;
+            f[j] = e < E ? sp[E + e] : 0;
+        }
+        int32_t u = sp[2 * E];
+        int64_t rt = (int64_t)(uint32_t)sp[2 * E + 1] | ((int64_t)sp[2 * E + 2] << 32);
+        int32_t maxf = __reduce_max_sync(FULL_MASK, max(max(f[0], f[1]), max(f[2], f[3])));
+        const uint8_t *routed = tr.routed_ptr() + tr.rt_begin(c);
+        for (int i = 0; i < MCB_TILE_EV; ++i) {
+            if (i < nev) {
+                const uint32_t info = tr.info(c, e0 + ev0 + i);
+                const uint32_t nrt = mcb_ev_nrt(info);
+                if (mcb_ev_newseq(info)) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) { last[j] = -1; f[j] = 0; }
+                    u = 0;
+                    maxf = 0;
                 }
-                bufA[i * lda + k] = v;
+                if (mcb_ev_decode(info) || include_prefill) {
+                    ++u;
+                    for (uint32_t r = 0; r < nrt; ++r) {
+                        const int x = __ldg(routed + rt + r);
+                        if ((x & 31) == lane) {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                { const bool hit_j = (x >> 5) == j; last[j] = hit_j ? u : last[j]; f[j] += hit_j ? 1 : 0; }
+                        }
+                    }
+                    maxf = __reduce_max_sync(FULL_MASK, max(max(f[0], f[1]), max(f[2], f[3])));
+                }
+                rt += nrt;
             }
-            __syncthreads();
-        } else {
-            for (int k = tid; k < D; k += blockDim.x) bufA[i * lda + k] = 0.0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int e = lane + 32 * j;
+                if (e < E) {
+                    double rv = 0.0, fv = 0.0;
+                    if (i < nev) {
+                        rv = last[j] < 0 ? 0.0 : 1.0 / (double)(u - last[j] + 1);
+                        fv = maxf > 0 ? (double)f[j] / (double)maxf : 0.0;
+                    }
+                    bufA[e * MCB_TILE_EV + i] = rv;
+                    bufA[(E + e) * MCB_TILE_EV + i] = fv;
+                }
+            }
         }
     }
     __syncthreads();
@@ -661,35 +1047,37 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
     const double *wt = wt_all + (num_nets == 1 ? 0 : layer) * (int64_t)prepared_net_doubles(E, H);
     const double *Wt1 = wt, *b1 = Wt1 + (int64_t)D * H, *Wt2 = b1 + H, *b2 = Wt2 + (int64_t)H * H,
                  *Wt3 = b2 + H, *b3 = Wt3 + (int64_t)H * E;
-    mlp_layer_any(bufA, lda, D, Wt1, b1, H, bufB, ldb, true);   // h1 -> B
+    mlp_layer_t(bufA, D, Wt1, b1, H, bufB, true);    // h1^T -> B
     __syncthreads();
-    mlp_layer_any(bufB, ldb, H, Wt2, b2, H, bufA, lda, true);   // h2 -> A
+    mlp_layer_t(bufB, H, Wt2, b2, H, bufA, true);    // h2^T -> A
     __syncthreads();
-    mlp_layer_any(bufA, lda, H, Wt3, b3, E, bufB, ldb, false);  // scores -> B
+    mlp_layer_t(bufA, H, Wt3, b3, E, bufB, false);   // scores^T -> B
     __syncthreads();
     for (int i = tid; i < MCB_TILE_EV; i += blockDim.x) s_flag[i] = 0;
     __syncthreads();
-    for (int q = tid; q < nev * E; q += blockDim.x) {
-        const int i = q / E, e = q % E;
-        const double s = bufB[i * ldb + e];
+    for (int q = tid; q < MCB_TILE_EV * E; q += blockDim.x) {
+        const int i = q % MCB_TILE_EV, e = q / MCB_TILE_EV;
+        if (i >= nev) continue;
+        const double s = bufB[e * MCB_TILE_EV + i];
         uint32_t r = 0;
         bool near = false;
         if (s > -INFINITY) {
             r = 1;
             for (int j = 0; j < E; ++j) {
-                const double sj = bufB[i * ldb + j];
+                const double sj = bufB[j * MCB_TILE_EV + i];
                 if (sj > -INFINITY) {
                     if (sj < s) ++r;
                     if (sj != s && fabs(sj - s) <= 1e-12 * fmax(fabs(s), fabs(sj))) near = true;
                 }
             }
         }
-        const int64_t g = (e0 + ev0 + i) * E + e;
-        ranks[g] = (uint8_t)r;
-        if (scores) scores[g] = s;
+        s_rank[i * E + e] = (uint8_t)r;
+        if (scores) scores[(e0 + ev0 + i) * E + e] = s;
         if (near) s_flag[i] = 1;
     }
     __syncthreads();
+    uint8_t *dst = ranks + (e0 + ev0) * E;
+    for (int q = tid; q < nev * E; q += blockDim.x) dst[q] = s_rank[q];
     if (tid == 0 && uncertain) {
         unsigned long long cnt = 0;
         for (int i = 0; i < nev; ++i) cnt += s_flag[i];
@@ -702,16 +1090,21 @@ int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int 
                  unsigned long long *uncertain, cudaStream_t s) {
     if (tr.n_chains == 0) return 0;
     int launched = 0;
-    if (!tr.uniform) {
+    if (tr.uniform) {
+        // snaps scratch holds [summaries | snapshots]
+        int32_t *summ = snaps + max_tiles * (2 * tr.E + 4);
+        k_tile_summary<<<(unsigned)((max_tiles + 3) / 4), 128, 0, s>>>(tr, summ);
+        k_snap_scan<<<(unsigned)((tr.n_chains + 3) / 4), 128, 0, s>>>(tr, summ, snaps);
+        launched += 2;
+    } else {
         k_tile_offsets<<<1, 1024, 0, s>>>(tr, tile_off);
-        ++launched;
+        k_feat_snap<<<(unsigned)((tr.n_chains + 3) / 4), 128, 0, s>>>(tr, include_prefill, tile_off, snaps);
+        launched += 2;
     }
-    k_feat_snap<<<(unsigned)((tr.n_chains + 3) / 4), 128, 0, s>>>(tr, include_prefill, tile_off, snaps);
-    ++launched;
     const int E = tr.E, D = 2 * E;
-    const int lda = D > H ? D : H, ldb = H > E ? H : E;
-    const size_t smem = (size_t)MCB_TILE_EV * (lda + ldb) * sizeof(double) +
-                        (2 * MCB_MAX_EXPERTS + MCB_TILE_EV) * sizeof(int32_t);
+    const int ra = D > H ? D : H, rb = H > E ? H : E;
+    const size_t smem = (size_t)MCB_TILE_EV * (ra + rb) * sizeof(double) + MCB_TILE_EV * MCB_MAX_EXPERTS +
+                        MCB_TILE_EV * sizeof(int32_t);
     cudaFuncSetAttribute(k_score_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (max_tiles > 0) {
         k_score_tile<<<(unsigned)max_tiles, 256, smem, s>>>(tr, wt, H, num_nets, include_prefill, tile_off, snaps,

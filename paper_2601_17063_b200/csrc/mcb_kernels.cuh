@@ -8,7 +8,7 @@
 
 #define MCB_MAX_POL 8
 #define MCB_MAX_CAP 64
-#define MCB_TILE_EV 32          // events per scorer tile (K3)
+#define MCB_TILE_EV 64          // events per scorer tile (K3)
 #define MCB_FNV_OFF 0xCBF29CE484222325ull
 #define MCB_FNV_PRIME 0x100000001B3ull
 

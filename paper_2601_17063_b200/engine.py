@@ -216,7 +216,7 @@ def _cost_struct(cost: CostModel, window: int) -> _lib.MCBCost:
 
 def replay_host(packed: PackedTrace, codes: Sequence[int], capacities: Sequence[int], cost: CostModel,
                 window: int, nets=None, *, want_outcomes=False, want_hashes=False, want_chain=False,
-                device: int = 0) -> dict:
+                device: int = 0, stream=None) -> dict:
     """One native call: every trace of ``packed`` x codes x capacities.
 
     Returns numpy arrays: reports [trace][pol][cap][8] int64, latency
@@ -257,7 +257,7 @@ def replay_host(packed: PackedTrace, codes: Sequence[int], capacities: Sequence[
     view = packed.view()
     cs = _cost_struct(cost, window)
     rc = lib.mcb_replay_host(ctx, ctypes.byref(view), pols, n_pol, caps, n_cap, ctypes.byref(cs), netsp,
-                             ctypes.byref(out))
+                             ctypes.byref(out), stream)
     _lib.check(rc)
     del keep
     return res
