@@ -196,10 +196,12 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--policies", default="lru,lfu,belady,ml", help="comma list (diagnostics only)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = dict(WORKLOADS[args.workload])
     rank, world, local = dist_env()
+    POLICIES[:] = args.policies.split(",")
 
     if args.impl == "reference":
         run_reference(args, wl, rank)

@@ -163,6 +163,11 @@ int mcb_last_stats(mcb_ctx *ctx, int64_t *kernels_launched, int64_t *uncertain_e
  * the last call (after the stream has been synchronised):
  * [0] K2 next-use scan, [1] K3 scorer, [2] K4 replay, [3] K5 fold. */
 int mcb_set_timing(mcb_ctx *ctx, int32_t enable);
+/* Tuning knobs (results never depend on them):
+ * MCB_TUNE_SOLO_MIN: minimum instance count for the thread-per-instance
+ * replay kernel (num_experts <= 16); below it one warp replays one instance. */
+#define MCB_TUNE_SOLO_MIN 0
+int mcb_set_tuning(mcb_ctx *ctx, int32_t knob, int64_t value);
 int mcb_last_timings(mcb_ctx *ctx, float *ms, int32_t n);
 
 /* ---- host-side trace validation + packing (trace.py:57-141, replay.py:44-81) ----

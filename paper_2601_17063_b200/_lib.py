@@ -24,13 +24,14 @@ MCB_ERR_NOMEM = 6
 MCB_ERR_SHAPE = 7
 
 MCB_LRU, MCB_LFU, MCB_BELADY, MCB_ML, MCB_ML_NO_PREFILL = range(5)
+MCB_TUNE_SOLO_MIN = 0
 R_PH, R_PM, R_DH, R_DM, R_COMP, R_EVICT, R_REFETCH, R_STATUS = range(8)
 R_N = 8
 OUT_HIT, OUT_MISS = 0xFFFF, 0xFFFE
 
 EXPORTED_SYMBOLS = (
     "mcb_abi_version", "mcb_ctx_create", "mcb_ctx_destroy", "mcb_last_error", "mcb_last_stats",
-    "mcb_set_timing", "mcb_last_timings",
+    "mcb_set_timing", "mcb_last_timings", "mcb_set_tuning",
     "mcb_pack_trace", "mcb_packed_view", "mcb_packed_positions", "mcb_packed_free",
     "mcb_replay", "mcb_replay_host", "mcb_next_use", "mcb_score", "mcb_router_topk",
 )
@@ -119,6 +120,7 @@ def load_library():
             "mcb_replay_host": ([P, P, P, i32, P, i32, P, P, P, P], ctypes.c_int),
             "mcb_set_timing": ([P, i32], ctypes.c_int),
             "mcb_last_timings": ([P, P, i32], ctypes.c_int),
+            "mcb_set_tuning": ([P, i32, i64], ctypes.c_int),
             "mcb_next_use": ([P, P, P, P], ctypes.c_int),
             "mcb_score": ([P, P, P, i32, P, P, P], ctypes.c_int),
             "mcb_router_topk": ([P, P, P, i64, i32, i32, i32, i32, P, P, P], ctypes.c_int),
@@ -160,6 +162,10 @@ def context(device: int = 0) -> ctypes.c_void_p:
     with _lock:
         _contexts[device] = h
     return h
+
+
+def set_tuning(knob: int, value: int, device: int = 0):
+    check(load_library().mcb_set_tuning(context(device), knob, value))
 
 
 def check(rc: int, errors: dict | None = None):

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -80,6 +81,7 @@ struct mcb_ctx {
     int64_t last_kernels = 0;
     int64_t last_uncertain = 0;
     bool timing = false;
+    int64_t solo_min_instances = 16384;   // overridable with MCB_SOLO_MIN (tuning / tests)
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 };
 
@@ -96,6 +98,17 @@ extern "C" int mcb_set_timing(mcb_ctx *c, int32_t enable) {
         for (auto &e : c->ev) CUDA_TRY(cudaEventCreate(&e));
     c->timing = enable != 0;
     return MCB_OK;
+}
+
+extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
+    mcb_clear_error();
+    if (!c) return mcb_set_error(MCB_ERR_INVALID, "ctx is NULL");
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (knob == MCB_TUNE_SOLO_MIN) {
+        c->solo_min_instances = value;
+        return MCB_OK;
+    }
+    return mcb_set_error(MCB_ERR_INVALID, "unknown tuning knob");
 }
 
 extern "C" int mcb_last_timings(mcb_ctx *c, float *ms, int32_t n) {
@@ -120,6 +133,7 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     auto *c = new (std::nothrow) mcb_ctx();
     if (!c) return mcb_set_error(MCB_ERR_NOMEM, "out of host memory");
     c->device = device;
+    if (const char *env = getenv("MCB_SOLO_MIN")) c->solo_min_instances = atoll(env);
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
         delete c;
         return mcb_set_error(MCB_ERR_CUDA, "stream creation failed");
@@ -290,6 +304,7 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     P.ml_cost = cost->ml_score_cost_s;
     P.loads_serial = cost->loads_serial;
     P.window = cost->window;
+    P.solo_min_instances = c->solo_min_instances;
 
     mark(c, 0, s);
     if (need_next) {

@@ -360,6 +360,10 @@ struct Solo {
 template <int EM, int POL, bool UNIFORM>
 __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t chain, int pol_i, int cap_i, int ml_variant,
                                               uint32_t *s_pk, uint32_t *s_pend) {
+    // Branch-free per access: every access computes the would-be victim
+    // (register min-tree over packed keys) and applies it under a predicate,
+    // so the warp runs one straight-line instruction stream regardless of
+    // which of its instances hit or miss (no divergence, no reconvergence).
     constexpr int SH = Solo<EM>::SH;
     constexpr uint32_t KMAX = Solo<EM>::KMAX;
     const DevTrace &tr = P.tr;
@@ -367,20 +371,19 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
     const uint32_t C = (uint32_t)P.cap[cap_i];
     const int E = tr.E;
     const int64_t inst = (chain * P.n_pol + pol_i) * P.n_cap + cap_i;
-    // per-thread columns of packed keys (key << SH | id) and pending-refetch marks
-    uint32_t *pk = s_pk + tid;      // pk[s * 128]
-    uint32_t *pd = s_pend + tid;    // pd[s * 128]
+    uint32_t *pd = s_pend + tid;    // pending-refetch marks pd[s * 128] (off the critical path)
 #pragma unroll
-    for (int s = 0; s < EM; ++s) { pk[s * 128] = (uint32_t)s; pd[s * 128] = 0u; }
+    for (int s = 0; s < EM; ++s) pd[s * 128] = 0u;
+    (void)s_pk;
 
-    uint32_t res = 0, pin = 0, seen = 0, valid = (1u << E) - 1u;
-    uint32_t mlk[EM];
+    uint32_t pk[EM];                // packed keys (key << SH | id), all experts
 #pragma unroll
-    for (int s = 0; s < EM; ++s) mlk[s] = ~0u;
+    for (int s = 0; s < EM; ++s) pk[s] = (uint32_t)s;
+    uint32_t res = 0, pin = 0, seen = 0, valid = (1u << E) - 1u;
     uint32_t count = 0, ph = 0, pm = 0, dh = 0, dm = 0, nev = 0, comp = 0, refc = 0;
     double dlat = 0.0, plat = 0.0;
     uint64_t h = MCB_FNV_OFF;
-    int status = MCB_OK;
+    bool stuck = false;
 
     const int64_t a0 = tr.acc_begin(chain);
     const int64_t e0 = tr.ev_begin(chain);
@@ -388,17 +391,15 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
     const int64_t a_end = tr.acc_end(chain);
     const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
     uint16_t *outc = P.outcomes ? P.outcomes + ((int64_t)pol_i * P.n_cap + cap_i) * tr.total_acc : nullptr;
+    const bool track = outc != nullptr || P.hashes != nullptr;
 
-    // id stream: 16-byte chunks, current + next in registers, L2 prefetch 512 B ahead
     const uint4 *ids16 = (const uint4 *)tr.acc;
     int64_t ich = a0 >> 4;
     uint4 icur = __ldg(ids16 + ich), inxt = __ldg(ids16 + ich + 1);
-    // Belady next-use stream: 4 positions per chunk
     const uint4 *np16 = (const uint4 *)P.next_pos;
     int64_t nch = a0 >> 2;
     uint4 ncur = make_uint4(0, 0, 0, 0), nnxt = make_uint4(0, 0, 0, 0);
     if (POL == POL_BELADY) { ncur = __ldg(np16 + nch); nnxt = __ldg(np16 + nch + 1); }
-    // ML rank rows, one event ahead
     uint32_t rrow[EM];
 #pragma unroll
     for (int s = 0; s < EM; ++s) rrow[s] = (POL == POL_ML && n_ev > 0 && s < E) ? __ldg(rank + e0 * E + s) : 0u;
@@ -418,13 +419,13 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
         const bool decode = UNIFORM ? true : mcb_ev_decode(info);
         if (POL == POL_LFU && !UNIFORM && mcb_ev_newseq(info)) {
 #pragma unroll
-            for (int s = 0; s < EM; ++s) pk[s * 128] = (uint32_t)s;   // start_sequence (policies.py:184-185)
+            for (int s = 0; s < EM; ++s) pk[s] = (uint32_t)s;   // start_sequence (policies.py:184-185)
         }
         if (POL == POL_ML) {
             valid = 0;
 #pragma unroll
             for (int s = 0; s < EM; ++s) {
-                mlk[s] = ((256u - rrow[s]) << SH) | (uint32_t)s;
+                pk[s] = ((256u - rrow[s]) << SH) | (uint32_t)s;
                 valid |= (rrow[s] != 0u ? 1u : 0u) << s;
                 rrow[s] = (ev + 1 < n_ev && s < E) ? __ldg(rank + (e0 + ev + 1) * E + s) : 0u;
             }
@@ -441,6 +442,15 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
             const uint32_t x = (sel4(icur, (uint32_t)(A >> 2) & 3u) >> (8u * (uint32_t)(A & 3))) & 0xFFu;
             const uint32_t bit = 1u << x;
             const bool hit = (res & bit) != 0u;
+            // policy key of x (capacity-independent)
+            uint32_t nk = 0;
+            if (POL == POL_LRU) nk = (pos << SH) | x;
+            if (POL == POL_LFU) {
+                uint32_t cur = 0;
+#pragma unroll
+                for (int s = 0; s < EM; ++s) cur = ((bit >> s) & 1u) ? pk[s] : cur;
+                nk = cur + (1u << SH);
+            }
             if (POL == POL_BELADY) {
                 if ((A >> 2) != nch) {
                     ++nch;
@@ -449,58 +459,50 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
                     if ((nch & 7) == 0 && ((nch + 64) << 2) < a_end) prefetch_l2(np16 + nch + 64);
                 }
                 const uint32_t np = sel4(ncur, (uint32_t)A & 3u);
-                // farthest next use first: key = KMAX - next_pos, never used again -> 0
-                pk[x * 128] = ((np == MCB_NEXT_INF ? 0u : KMAX - np) << SH) | x;
+                nk = ((np == MCB_NEXT_INF ? 0u : KMAX - np) << SH) | x;   // farthest next use = smallest key
             }
-            if (POL == POL_LRU) pk[x * 128] = (pos << SH) | x;
-            if (POL == POL_LFU) pk[x * 128] += 1u << SH;
-            uint32_t code = MCB_OUT_HIT;
-            if (hit) {
-                if (decode) ++dh; else ++ph;
-            } else {
-                if (decode) ++dm; else ++pm;
-                ++step_miss;
-                if (count >= C) {
-                    const uint32_t cand = res & ~pin & valid;
-                    uint32_t t[EM];
+            if (POL != POL_ML) {
 #pragma unroll
-                    for (int s = 0; s < EM; ++s) {
-                        const uint32_t k = (POL == POL_ML) ? mlk[s] : pk[s * 128];
-                        t[s] = ((cand >> s) & 1u) ? k : ~0u;
-                    }
+                for (int s = 0; s < EM; ++s) pk[s] = ((bit >> s) & 1u) ? nk : pk[s];
+            }
+            // would-be victim: argmin packed key over resident \ pinned
+            const uint32_t cand = res & ~pin & valid;
+            uint32_t t[EM];
 #pragma unroll
-                    for (int w = EM / 2; w >= 1; w /= 2)
+            for (int s = 0; s < EM; ++s) t[s] = ((cand >> s) & 1u) ? pk[s] : ~0u;
 #pragma unroll
-                        for (int s = 0; s < w; ++s) t[s] = min(t[s], t[s + w]);
-                    if (t[0] == ~0u) { status = MCB_ERR_NO_EVICTABLE; break; }
-                    const uint32_t v = t[0] & (uint32_t)(EM - 1);
-                    res &= ~(1u << v);
-                    pd[v * 128] = dec + 1u;
-                    code = v;
-                    ++nev;
-                } else {
-                    ++count;
-                    code = MCB_OUT_MISS;
-                }
-                if (!(seen & bit)) {
-                    ++comp;
-                } else {
-                    const uint32_t pe = pd[x * 128];
-                    if (pe && (int64_t)dec - (int64_t)(pe - 1u) <= (int64_t)P.window) ++refc;
-                }
+            for (int w = EM / 2; w >= 1; w /= 2)
+#pragma unroll
+                for (int s = 0; s < w; ++s) t[s] = min(t[s], t[s + w]);
+            const bool miss = !hit;
+            const bool full = count >= C;
+            const bool evict = miss && full;
+            stuck |= evict && t[0] == ~0u;
+            const uint32_t v = t[0] & (uint32_t)(EM - 1);
+            const uint32_t vbit = evict ? (1u << v) : 0u;
+            res = (res & ~vbit) | bit;
+            count += (miss && !full) ? 1u : 0u;
+            nev += evict ? 1u : 0u;
+            step_miss += miss ? 1u : 0u;
+            if (decode) { dh += hit ? 1u : 0u; dm += miss ? 1u : 0u; }
+            else { ph += hit ? 1u : 0u; pm += miss ? 1u : 0u; }
+            // compulsory (engine.py:248-250) and refetch of an earlier victim (engine.py:289-296)
+            const bool first = (seen & bit) == 0u;
+            comp += (miss && first) ? 1u : 0u;
+            if (miss && !first) {
+                const uint32_t pe = pd[x * 128];
+                if (pe && (int64_t)dec - (int64_t)(pe - 1u) <= (int64_t)P.window) ++refc;
                 pd[x * 128] = 0u;
-                seen |= bit;
-                res |= bit;
             }
-            if (decode) pin |= bit;
-            if (outc) {
+            if (evict) pd[v * 128] = dec + 1u;
+            seen |= bit;
+            pin |= decode ? bit : 0u;
+            if (track) {
+                const uint32_t code = hit ? MCB_OUT_HIT : (evict ? v : MCB_OUT_MISS);
                 h = fnv16(h, code);
-                outc[A] = (uint16_t)code;
-            } else if (P.hashes) {
-                h = fnv16(h, code);
+                if (outc) outc[A] = (uint16_t)code;
             }
         }
-        if (status != MCB_OK) break;
         double lat;
         if (step_miss > 0)
             lat = __dmul_rn((double)(P.loads_serial ? step_miss : 1u), P.t_load);
@@ -518,7 +520,7 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
     o[MCB_R_COMPULSORY] = comp;
     o[MCB_R_EVICTIONS] = nev;
     o[MCB_R_REFETCHED] = refc;
-    o[MCB_R_STATUS] = status;
+    o[MCB_R_STATUS] = stuck ? MCB_ERR_NO_EVICTABLE : MCB_OK;
     P.inst_lat[inst * 2 + 0] = dlat;
     P.inst_lat[inst * 2 + 1] = plat;
     if (P.hashes) P.hashes[inst] = h;
@@ -526,7 +528,8 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
 
 template <int EM, bool UNIFORM>
 __global__ void __launch_bounds__(128) k_replay_solo(const __grid_constant__ ReplayParams P) {
-    __shared__ uint32_t s_pk[EM * 128], s_pend[EM * 128];
+    __shared__ uint32_t s_pend[EM * 128];
+    uint32_t *s_pk = nullptr;
     const int pol_i = blockIdx.y;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= P.tr.n_chains * P.n_cap) return;
@@ -561,12 +564,15 @@ static void launch_replay_t(const ReplayParams &p, cudaStream_t s) {
 int launch_replay(const ReplayParams &p, cudaStream_t s) {
     if (p.tr.n_chains * p.n_pol * p.n_cap == 0) return 0;
     const int E = p.tr.E;
-    // solo kernels pack (key << 3|4 | id) into 32 bits: chains must stay below 2^28 accesses
-    const bool solo_ok = p.tr.total_acc < (1ll << 27);
+    // solo kernels pack (key << 3|4 | id) into 32 bits: chains must stay below 2^28 accesses.
+    // Thread-per-instance only pays off when there are enough instances to
+    // fill the machine; few long chains (e.g. one Mixtral trace) are
+    // latency-bound, and a whole warp per instance has the shorter per-access
+    // critical path (lane-parallel victim search, no divergence).
+    const int64_t n_inst = p.tr.n_chains * p.n_pol * p.n_cap;
+    const bool solo_ok = p.tr.total_acc < (1ll << 27) && n_inst >= p.solo_min_instances;
     if (E <= 8 && solo_ok) launch_solo_t<8>(p, s);
     else if (E <= 16 && solo_ok) launch_solo_t<16>(p, s);
-    else if (E <= 8) launch_replay_t<8, 1>(p, s);
-    else if (E <= 16) launch_replay_t<16, 1>(p, s);
     else if (E <= 32) launch_replay_t<32, 1>(p, s);
     else if (E <= 64) launch_replay_t<32, 2>(p, s);
     else launch_replay_t<32, 4>(p, s);
@@ -846,13 +852,17 @@ __device__ __forceinline__ void mlp_layer_tt(const double *At, int Din, const do
             for (int j = 0; j < CT; ++j) acc[i][j] = 0.0;
         const bool full = c0 + CT - 1 < Dout;
         for (int k = 0; k < Din; ++k) {
-            const double2 *arow = (const double2 *)(At + k * MCB_TILE_EV + eg * EVT);
             double a[EVT];
+            if constexpr (EVT == 1) {
+                a[0] = At[k * MCB_TILE_EV + eg];
+            } else {
+                const double2 *arow = (const double2 *)(At + k * MCB_TILE_EV + eg * EVT);
 #pragma unroll
-            for (int q = 0; q < EVT / 2; ++q) {
-                const double2 v = arow[q];
-                a[2 * q] = v.x;
-                a[2 * q + 1] = v.y;
+                for (int q = 0; q < EVT / 2; ++q) {
+                    const double2 v = arow[q];
+                    a[2 * q] = v.x;
+                    a[2 * q + 1] = v.y;
+                }
             }
             const double *wr = Wt + (int64_t)k * Dout + c0;
             double wv[CT];
@@ -868,14 +878,19 @@ __device__ __forceinline__ void mlp_layer_tt(const double *At, int Din, const do
             const int col = c0 + j;
             if (col < Dout) {
                 const double b = __ldg(bias + col);
-                double2 *orow = (double2 *)(Ot + col * MCB_TILE_EV + eg * EVT);
+                if constexpr (EVT == 1) {
+                    const double z = __dadd_rn(acc[0][j], b);
+                    Ot[col * MCB_TILE_EV + eg] = act ? __dmul_rn(z, sigmoid_ref(z)) : z;
+                } else {
+                    double2 *orow = (double2 *)(Ot + col * MCB_TILE_EV + eg * EVT);
 #pragma unroll
-                for (int q = 0; q < EVT / 2; ++q) {
-                    const double z0 = __dadd_rn(acc[2 * q][j], b), z1 = __dadd_rn(acc[2 * q + 1][j], b);
-                    double2 v;
-                    v.x = act ? __dmul_rn(z0, sigmoid_ref(z0)) : z0;
-                    v.y = act ? __dmul_rn(z1, sigmoid_ref(z1)) : z1;
-                    orow[q] = v;
+                    for (int q = 0; q < EVT / 2; ++q) {
+                        const double z0 = __dadd_rn(acc[2 * q][j], b), z1 = __dadd_rn(acc[2 * q + 1][j], b);
+                        double2 v;
+                        v.x = act ? __dmul_rn(z0, sigmoid_ref(z0)) : z0;
+                        v.y = act ? __dmul_rn(z1, sigmoid_ref(z1)) : z1;
+                        orow[q] = v;
+                    }
                 }
             }
         }
@@ -884,11 +899,13 @@ __device__ __forceinline__ void mlp_layer_tt(const double *At, int Din, const do
 
 __device__ __forceinline__ void mlp_layer_t(const double *At, int Din, const double *Wt, const double *bias, int Dout,
                                             double *Ot, bool act) {
-    if (Dout >= 128) mlp_layer_tt<8, 4>(At, Din, Wt, bias, Dout, Ot, act);
-    else if (Dout >= 64) mlp_layer_tt<8, 2>(At, Din, Wt, bias, Dout, Ot, act);
-    else if (Dout >= 32) mlp_layer_tt<4, 2>(At, Din, Wt, bias, Dout, Ot, act);
-    else if (Dout >= 16) mlp_layer_tt<4, 1>(At, Din, Wt, bias, Dout, Ot, act);
-    else mlp_layer_tt<2, 1>(At, Din, Wt, bias, Dout, Ot, act);
+    // 256 threads over a 32-event tile: (events per thread, columns per thread)
+    static_assert(MCB_TILE_EV == 32, "thread shapes below assume 32-event tiles");
+    if (Dout >= 128) mlp_layer_tt<4, 4>(At, Din, Wt, bias, Dout, Ot, act);
+    else if (Dout >= 64) mlp_layer_tt<4, 2>(At, Din, Wt, bias, Dout, Ot, act);
+    else if (Dout >= 32) mlp_layer_tt<2, 2>(At, Din, Wt, bias, Dout, Ot, act);
+    else if (Dout >= 16) mlp_layer_tt<2, 1>(At, Din, Wt, bias, Dout, Ot, act);
+    else mlp_layer_tt<1, 1>(At, Din, Wt, bias, Dout, Ot, act);
 }
 
 // One block (256 threads) per (chain, tile of 64 events): warp 0 rebuilds
@@ -962,8 +979,9 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
             pmax[tid] = m;
         }
         __syncthreads();
-        if (tid < 32) {   // inclusive prefix max over the 64 events, then max with the snapshot max_f
-            int32_t a = pmax[2 * tid], b = max(a, pmax[2 * tid + 1]);
+        if (tid < 32) {   // inclusive prefix max over the tile's events, then max with the snapshot max_f
+            int32_t a = 2 * tid < MCB_TILE_EV ? pmax[2 * tid] : 0;
+            int32_t b = max(a, 2 * tid + 1 < MCB_TILE_EV ? pmax[2 * tid + 1] : 0);
             int32_t m0 = 0;
             for (int e = 0; e < E; ++e) m0 = max(m0, sp[E + e]);
 #pragma unroll
@@ -971,8 +989,8 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
                 const int32_t t = __shfl_up_sync(FULL_MASK, b, o);
                 if (tid >= o) { a = max(a, t); b = max(b, t); }
             }
-            pmax[2 * tid] = max(a, m0);
-            pmax[2 * tid + 1] = max(b, m0);
+            if (2 * tid < MCB_TILE_EV) pmax[2 * tid] = max(a, m0);
+            if (2 * tid + 1 < MCB_TILE_EV) pmax[2 * tid + 1] = max(b, m0);
         }
         __syncthreads();
         for (int q = tid; q < MCB_TILE_EV * E; q += blockDim.x) {

@@ -8,7 +8,7 @@
 
 #define MCB_MAX_POL 8
 #define MCB_MAX_CAP 64
-#define MCB_TILE_EV 64          // events per scorer tile (K3)
+#define MCB_TILE_EV 32          // events per scorer tile (K3)
 #define MCB_FNV_OFF 0xCBF29CE484222325ull
 #define MCB_FNV_PRIME 0x100000001B3ull
 
@@ -48,6 +48,7 @@ struct ReplayParams {
     double *inst_lat;                   // [chain][pol][cap][2]
     uint64_t *hashes;                   // optional [chain][pol][cap]
     uint16_t *outcomes;                 // optional [pol][cap][total_acc]
+    int64_t solo_min_instances;         // thread-per-instance kernel threshold (E <= 16)
 };
 
 // launchers (mcb_kernels.cu); return the number of kernels launched or <0 on error

@@ -77,26 +77,38 @@ def ar1_hidden(tokens: int, d: int, rho: float, seed: int, device="cuda", chunk:
     return out
 
 
+def padded_experts(E: int) -> int:
+    """Gate rows per layer in the weight layout: E rounded up to a power of
+    two >= 8 (a divisor of the kernel's 256-column tile); padding rows are
+    never selected."""
+    ep = 8
+    while ep < E:
+        ep *= 2
+    return ep
+
+
 def router_weights(w: RouterWorkload, device="cuda") -> torch.Tensor:
-    """bf16 [L*E, d_pad] gate rows of all layers (layer-major), N(0, 1/d),
-    column d = the per-layer Zipf bias."""
+    """bf16 [L*Ep, d_pad] gate rows of all layers (layer-major), N(0, 1/d),
+    column d = the per-layer Zipf bias; rows E..Ep-1 of each layer are zero."""
     L, E, d = w.num_layers, w.num_experts, w.hidden_dim
+    Ep = padded_experts(E)
     d_pad = (d + 1 + 63) // 64 * 64
     g = _gen(w.seed * 1000003 + 1, device)
-    W = torch.zeros((L * E, d_pad), dtype=torch.float32, device=device)
-    W[:, :d] = torch.randn((L * E, d), generator=g, device=device) / math.sqrt(d)
+    W = torch.zeros((L, Ep, d_pad), dtype=torch.float32, device=device)
+    W[:, :E, :d] = torch.randn((L, E, d), generator=g, device=device) / math.sqrt(d)
     gc = torch.Generator()
     gc.manual_seed(w.seed * 7919 + 3)
     for layer in range(L):
         rank = torch.randperm(E, generator=gc)
-        W[layer * E:(layer + 1) * E, d] = (-w.zipf_s * torch.log1p(rank.double())).float().to(device)
-    return W.to(torch.bfloat16)
+        W[layer, :E, d] = (-w.zipf_s * torch.log1p(rank.double())).float().to(device)
+    return W.reshape(L * Ep, d_pad).to(torch.bfloat16)
 
 
 def route_topk_torch(hidden: torch.Tensor, weight: torch.Tensor, L: int, E: int, K: int,
                      chunk: int = 16384) -> torch.Tensor:
     """Reference: ids[l][t][:] = topk(hidden.float() @ weight.float().T)[.., l*E:(l+1)*E], sorted."""
     T = hidden.shape[0]
+    Ep = weight.shape[0] // L
     out = torch.empty((L, T, K), dtype=torch.uint8, device=hidden.device)
     prev = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = False
@@ -104,7 +116,7 @@ def route_topk_torch(hidden: torch.Tensor, weight: torch.Tensor, L: int, E: int,
         Wf = weight.float()
         for t0 in range(0, T, chunk):
             lg = hidden[t0:t0 + chunk].float() @ Wf.T
-            lg = lg.view(lg.shape[0], L, E)
+            lg = lg.view(lg.shape[0], L, Ep)[:, :, :E]
             idx = torch.topk(lg, K, dim=-1, sorted=True).indices
             out[:, t0:t0 + lg.shape[0]] = idx.permute(1, 0, 2).to(torch.uint8)
     finally:

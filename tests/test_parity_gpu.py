@@ -58,14 +58,23 @@ def check_case(case, decisions=True):
             assert got == run["decisions"], (case["name"], run["policy"])
 
 
+@pytest.fixture(params=["warp", "solo"])
+def kernel_variant(request):
+    """Run each parity case through both replay kernels: one warp per
+    instance, and one thread per instance (num_experts <= 16)."""
+    _lib.set_tuning(_lib.MCB_TUNE_SOLO_MIN, 0 if request.param == "solo" else 1 << 62)
+    yield request.param
+    _lib.set_tuning(_lib.MCB_TUNE_SOLO_MIN, 16384)
+
+
 @pytest.mark.parametrize("part", range(4))
-def test_small_cases(part):
+def test_small_cases(part, kernel_variant):
     cases = load("small_cases.json.gz")["cases"]
     for case in cases[part::4]:
         check_case(case)
 
 
-def test_zipf_and_dominance_cases():
+def test_zipf_and_dominance_cases(kernel_variant):
     for case in load("zipf_cases.json.gz")["cases"]:
         check_case(case, decisions=False)
 
@@ -82,7 +91,7 @@ def test_efficacy_golden_means():
 
 
 @pytest.mark.parametrize("which", [0, 1])
-def test_full_size_c1_and_mixtral(which):
+def test_full_size_c1_and_mixtral(which, kernel_variant):
     """C1 (Qwen3-shaped L48/E128/K8, 2048 tokens) and the Mixtral-shaped trace
     at full size: one engine call per trace for all policies x capacities."""
     case = load("big_cases.json.gz")["cases"][which]
