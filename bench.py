@@ -65,12 +65,14 @@ def dist_env():
 
 
 def measured_peaks():
+    """(HBM GB/s, bf16 dense TFLOP/s burst, source) from MEASURED_PEAKS.json,
+    else the fallback of /opt/skills/guides/B200_PROFILING.md."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as fh:
             d = json.load(fh)
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops", 1590.0)), "measured"
+    return 6650.0, 1590.0, "fallback"
 
 
 class ClockSampler:
@@ -114,15 +116,42 @@ class ClockSampler:
 
 
 def make_trace_ids(wl, seed: int, gen: str, device):
-    """uint8 [n_traces][L][T][K] ids from the router-GEMM generator."""
+    """uint8 [n_traces][L][T][K] ids from the router-GEMM generator (K1).
+
+    Also times K1 itself (CUDA events, after one warm-up launch) on the first
+    trace: returns (ids, generator report)."""
     import torch
 
     from paper_2601_17063_b200 import generator
     outs = []
+    gen_report = None
     for i in range(wl["n_traces_local"]):
         w = generator.RouterWorkload(wl["L"], wl["E"], wl["K"], wl["T"], wl["d"], seed=seed + i)
-        outs.append(generator.synthetic_ids(w, impl=gen, device=device))
-    return torch.stack(outs)
+        H = generator.ar1_hidden(w.tokens, w.hidden_dim, w.rho, w.seed * 2 + 11, device)
+        W = generator.router_weights(w, device)
+        if gen == "torch":
+            ids = generator.route_topk_torch(H, W, w.num_layers, w.num_experts, w.top_k)
+        else:
+            ids = generator.route_topk(H, W, w.num_layers, w.num_experts, w.top_k)
+            if gen_report is None:
+                s = torch.cuda.current_stream(device)
+                reps = 5
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                for _ in range(reps):
+                    generator.route_topk(H, W, w.num_layers, w.num_experts, w.top_k, out=ids)
+                b.record(s)
+                b.synchronize()
+                ms = a.elapsed_time(b) / reps
+                Ep = generator.padded_experts(w.num_experts)
+                flops = 2.0 * w.tokens * H.shape[1] * w.num_layers * Ep
+                hbm = H.numel() * 2 + W.numel() * 2 + ids.numel()
+                gen_report = {"kernel": "router_topk_kernel (K1, tcgen05.mma kind::f16 + TMA, fused top-k)",
+                              "ms": ms, "tflops": flops / ms / 1e9, "gbs": hbm / ms / 1e6,
+                              "tokens": w.tokens, "gemm": f"{w.tokens}x{H.shape[1]}x{w.num_layers * Ep}"}
+        outs.append(ids)
+        del H, W
+    return torch.stack(outs), gen_report
 
 
 def nets_for(L: int, E: int):
@@ -192,7 +221,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--gen", default="torch", choices=["torch", "tcgen05"])
+    ap.add_argument("--gen", default="tcgen05", choices=["torch", "tcgen05"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -228,7 +257,7 @@ def main():
     L, E, K, T = wl["L"], wl["E"], wl["K"], wl["T"]
     codes = [{"lru": _lib.MCB_LRU, "lfu": _lib.MCB_LFU, "belady": _lib.MCB_BELADY, "ml": _lib.MCB_ML}[p]
              for p in POLICIES]
-    ids = make_trace_ids(wl, args.seed + 1000 * rank, args.gen, dev)
+    ids, gen_report = make_trace_ids(wl, args.seed + 1000 * rank, args.gen, dev)
     torch.cuda.synchronize()
     dtrace = DeviceTrace.from_decode_ids(ids, E)
     hidden, n_nets, flat = nets_for(L, E)
@@ -245,7 +274,7 @@ def main():
     clocks = ClockSampler(local)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    stage = np.zeros(4)
+    stage = np.zeros(5)
     launches = 0
     if world > 1:
         dist.barrier()
@@ -279,12 +308,16 @@ def main():
     value = acc_all * args.steps / (total_ms / 1e3)
     ms_per_step = total_ms / args.steps
 
-    # roofline of the dominant kernel (K4 replay) from the in-run stage events
-    replay_ms = stage[2] / args.steps
+    # roofline of the dominant kernel (K4 replay) from the in-run per-launch
+    # events: algorithmic bytes of both K4 launches (non-ML, ML) / their time
+    replay_ms = (stage[2] + stage[3]) / args.steps
     n_acc_cell = dtrace.total_acc
     alg_bytes = sum(bytes_per_access(p, E, K) * n_acc_cell * len(wl["caps"]) for p in POLICIES)
     achieved = alg_bytes / (replay_ms / 1e3) / 1e9
-    peak, peak_kind = measured_peaks()
+    peak, bf16_peak, peak_kind = measured_peaks()
+    if gen_report:
+        gen_report["frac_of_bf16_peak"] = gen_report["tflops"] / bf16_peak
+        gen_report["frac_of_hbm"] = gen_report["gbs"] / peak
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.workload}.json")
     if os.path.exists(prof):
@@ -349,7 +382,10 @@ def main():
                        "capacities": wl["caps"], "policies": POLICIES, "parallelism": f"shard{world}",
                        "l2": "flushed before every timed step (256 MiB write)",
                        "stage_ms_per_step": {"k2_next_use": stage[0] / args.steps, "k3_scorer": stage[1] / args.steps,
-                                             "k4_replay": stage[2] / args.steps, "k5_fold": stage[3] / args.steps}},
+                                             "k4_replay_non_ml": stage[2] / args.steps,
+                                             "k4_replay_ml": stage[3] / args.steps, "k5_fold": stage[4] / args.steps,
+                                             "note": "K2 + K4(non-ML) run on a side stream concurrently "
+                                                     "with K3 -> K4(ML)"}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "k_replay (K4)",
                          "peak_source": peak_kind,
@@ -358,6 +394,7 @@ def main():
             "e2e": e2e,
             "clocks": clk,
             "gpu_launches": launches,
+            "generator": gen_report,
             "hit_rates": hit_rates,
         }
         print(json.dumps(line), flush=True)

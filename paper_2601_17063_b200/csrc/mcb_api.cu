@@ -47,6 +47,7 @@ extern "C" int mcb_abi_version(void) { return MCB_ABI_VERSION; }
     } while (0)
 
 // ---------------------------------------------------------------- context --
+int mcb_router_preload();   // mcb_router.cu
 struct DevBuf {
     void *p = nullptr;
     size_t n = 0;
@@ -81,13 +82,21 @@ struct mcb_ctx {
     int64_t last_kernels = 0;
     int64_t last_uncertain = 0;
     bool timing = false;
-    int64_t solo_min_instances = 16384;   // overridable with MCB_SOLO_MIN (tuning / tests)
-    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t side = nullptr;       // non-ML replay runs here concurrently with K3
+    cudaStream_t side2 = nullptr;      // pipelined ML replay (waits on K3's per-tile flags)
+    cudaEvent_t join2 = nullptr;
+    DevBuf ready[2];                   // per-(chain, tile) "ranks published" flags
+    int32_t epoch = 0;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    int64_t solo_min_instances = 0;   // thread-per-instance whenever E <= 16 (MCB_SOLO_MIN overrides)
+    cudaEvent_t ev[10] = {};          // start/stop per stage: K2, K3, K4 non-ML, K4 ML, K5
+    bool ran[5] = {};
 };
 
 static void mark(mcb_ctx *c, int i, cudaStream_t s) {
     if (c->timing) cudaEventRecord(c->ev[i], s);
 }
+static const int N_STAGES = 5;
 
 extern "C" int mcb_set_timing(mcb_ctx *c, int32_t enable) {
     mcb_clear_error();
@@ -115,7 +124,10 @@ extern "C" int mcb_last_timings(mcb_ctx *c, float *ms, int32_t n) {
     mcb_clear_error();
     if (!c || !ms) return mcb_set_error(MCB_ERR_INVALID, "ctx / ms is NULL");
     if (!c->timing) return mcb_set_error(MCB_ERR_INVALID, "timing is not enabled");
-    for (int i = 0; i < n && i < 4; ++i) CUDA_TRY(cudaEventElapsedTime(&ms[i], c->ev[i], c->ev[i + 1]));
+    for (int i = 0; i < n && i < N_STAGES; ++i) {
+        ms[i] = 0.f;
+        if (c->ran[i]) CUDA_TRY(cudaEventElapsedTime(&ms[i], c->ev[2 * i], c->ev[2 * i + 1]));
+    }
     return MCB_OK;
 }
 
@@ -130,11 +142,20 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     CUDA_TRY(cudaGetDeviceProperties(&prop, device));
     if (prop.major < 10)
         return mcb_set_error(MCB_ERR_UNSUPPORTED, "libmcb is built for sm_100a (B200); device is older");
+    if (preload_kernels() != 0) return mcb_set_error(MCB_ERR_CUDA, "failed to load the replay kernels");
+    if (int rc = mcb_router_preload()) return rc;
     auto *c = new (std::nothrow) mcb_ctx();
     if (!c) return mcb_set_error(MCB_ERR_NOMEM, "out of host memory");
     c->device = device;
     if (const char *env = getenv("MCB_SOLO_MIN")) c->solo_min_instances = atoll(env);
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);   // replay warps dispatch ahead of K3 blocks
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c->side2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->join2, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess) {
         delete c;
         return mcb_set_error(MCB_ERR_CUDA, "stream creation failed");
     }
@@ -151,6 +172,13 @@ extern "C" int mcb_ctx_destroy(mcb_ctx *c) {
                      &c->h_chain_reports, &c->h_hashes, &c->h_outcomes};
     for (DevBuf *b : all) b->release();
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->side2) cudaStreamDestroy(c->side2);
+    if (c->join2) cudaEventDestroy(c->join2);
+    c->ready[0].release();
+    c->ready[1].release();
+    if (c->fork) cudaEventDestroy(c->fork);
+    if (c->join) cudaEventDestroy(c->join);
     for (auto &e : c->ev)
         if (e) cudaEventDestroy(e);
     delete c;
@@ -203,23 +231,36 @@ static int64_t max_score_tiles(const DevTrace &d) {
     return d.total_events / MCB_TILE_EV + d.n_chains;  // upper bound of sum(ceil(n_c / TILE))
 }
 
+// All device allocations of K3 happen here, before anything is launched:
+// cudaMalloc may synchronise the device, which must never happen while a
+// pipelined replay kernel is already waiting on K3's flags.
+static int ensure_score_buffers(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets) {
+    const int E = d.E, H = nets->hidden;
+    const size_t per = prepared_net_doubles(E, H);
+    if (int rc = c->wt.ensure(per * nets->num_nets * sizeof(double))) return rc;
+    const int64_t tiles = max_score_tiles(d);
+    if (int rc = c->snaps.ensure((size_t)(tiles + 1) * (4 * E + 8) * sizeof(int32_t))) return rc;
+    if (int rc = c->tile_off.ensure((size_t)(d.n_chains + 1) * sizeof(int64_t))) return rc;
+    return MCB_OK;
+}
+
 static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int include_prefill, uint8_t *ranks,
-                     double *scores, cudaStream_t s, int64_t *launched) {
+                     double *scores, cudaStream_t s, int64_t *launched, int32_t *ready = nullptr,
+                     int32_t epoch = 0) {
     const int E = d.E, H = nets->hidden;
     if (nets->num_experts != E) return mcb_set_error(MCB_ERR_SHAPE, "net num_experts does not match the trace");
     if (H < 1 || H > 256) return mcb_set_error(MCB_ERR_UNSUPPORTED, "net hidden size must be in [1, 256]");
     if (nets->num_nets != 1 && nets->num_nets != d.L)
         return mcb_set_error(MCB_ERR_INVALID, "num_nets must be 1 or num_layers");
     if (!nets->params) return mcb_set_error(MCB_ERR_INVALID, "nets.params is NULL");
+    if (int rc = ensure_score_buffers(c, d, nets)) return rc;
     const size_t per = prepared_net_doubles(E, H);
-    if (int rc = c->wt.ensure(per * nets->num_nets * sizeof(double))) return rc;
+    (void)per;
     *launched += launch_prepare_nets(nets->params, E, H, nets->num_nets, (double *)c->wt.p, s);
     const int64_t tiles = max_score_tiles(d);
-    if (int rc = c->snaps.ensure((size_t)(tiles + 1) * (4 * E + 8) * sizeof(int32_t))) return rc;
-    if (int rc = c->tile_off.ensure((size_t)(d.n_chains + 1) * sizeof(int64_t))) return rc;
     const int n = launch_score(d, (const double *)c->wt.p, H, nets->num_nets, include_prefill, ranks, scores,
                                (int32_t *)c->snaps.p, (int64_t *)c->tile_off.p, tiles,
-                               (unsigned long long *)c->stats.p, s);
+                               (unsigned long long *)c->stats.p, ready, epoch, s);
     *launched += n;
     return MCB_OK;
 }
@@ -306,20 +347,11 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     P.window = cost->window;
     P.solo_min_instances = c->solo_min_instances;
 
-    mark(c, 0, s);
-    if (need_next) {
-        if (int rc = c->next_pos.ensure((size_t)(d.total_acc + 64) * sizeof(uint32_t))) return rc;
-        launched += launch_next_use(d, (uint32_t *)c->next_pos.p, s);
-        P.next_pos = (const uint32_t *)c->next_pos.p;
-    }
-    mark(c, 1, s);
-    for (int v = 0; v < 2; ++v) {
-        if (!need_ml[v]) continue;
-        if (int rc = c->ranks[v].ensure((size_t)d.total_events * d.E + 64)) return rc;
-        if (int rc = run_score(c, d, nets, v == 0 ? 1 : 0, (uint8_t *)c->ranks[v].p, nullptr, s, &launched))
-            return rc;
-        P.rank[v] = (const uint8_t *)c->ranks[v].p;
-    }
+    // Orchestration.  K3 (ML scores) is only needed by ML instances, so when
+    // both kinds are present the non-ML replay runs on a high-priority side
+    // stream concurrently with K3, and the ML replay follows K3:
+    //     s:    K2 --+-- K3 ........ K4(ml) --+-- K5
+    //     side:      +-- K4(lru/lfu/belady) --+
     const int64_t n_inst = d.n_chains * n_pol * n_cap;
     if (out->chain_reports) {
         P.inst_out = out->chain_reports;
@@ -331,11 +363,103 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     P.inst_lat = (double *)c->inst_lat.p;
     P.hashes = out->hashes;
     P.outcomes = out->outcomes;
-    mark(c, 2, s);
-    launched += launch_replay(P, s);
-    mark(c, 3, s);
+    ReplayParams Pn = P, Pm = P;   // non-ML and ML launches
+    Pn.n_pol_launch = Pm.n_pol_launch = 0;
+    for (int i = 0; i < n_pol; ++i) {
+        if (pols[i] == MCB_ML || pols[i] == MCB_ML_NO_PREFILL) Pm.pol_map[Pm.n_pol_launch++] = i;
+        else Pn.pol_map[Pn.n_pol_launch++] = i;
+    }
+    const bool split = Pn.n_pol_launch > 0 && Pm.n_pol_launch > 0;
+    cudaStream_t sn = split ? c->side : s;
+    for (bool &r : c->ran) r = false;
+    if (need_next) {
+        if (int rc = c->next_pos.ensure((size_t)(d.total_acc + 64) * sizeof(uint32_t))) return rc;
+        Pn.next_pos = Pm.next_pos = (const uint32_t *)c->next_pos.p;
+        mark(c, 0, s);
+        launched += launch_next_use(d, (uint32_t *)c->next_pos.p, s);
+        mark(c, 1, s);
+        c->ran[0] = true;
+    }
+    if (split) {
+        CUDA_TRY(cudaEventRecord(c->fork, s));
+        CUDA_TRY(cudaStreamWaitEvent(c->side, c->fork, 0));
+    }
+    if (Pn.n_pol_launch > 0) {
+        mark(c, 4, sn);
+        launched += launch_replay(Pn, sn);
+        mark(c, 5, sn);
+        c->ran[2] = true;
+    }
+    // Pipelined ML replay (uniform traces, small ML grid): the ML K4 runs on
+    // its own high-priority stream concurrently with K3 and waits per tile on
+    // K3's release flags, so scoring and replay overlap event by event.  The
+    // ML grid is kept far below the SM count, so K3 always has SMs to finish
+    // (no deadlock) while the replay warps spin-sleep.
+    const bool pipe = Pm.n_pol_launch > 0 && d.uniform && replay_blocks(Pm) <= 64;
+    if (Pm.n_pol_launch > 0) {
+        if (int rc = ensure_score_buffers(c, d, nets)) return rc;
+        for (int v = 0; v < 2; ++v)
+            if (need_ml[v])
+                if (int rc = c->ranks[v].ensure((size_t)d.total_events * d.E + 64)) return rc;
+        prepare_launch_attributes(d, nets->hidden);
+        int32_t *ready[2] = {nullptr, nullptr};
+        int32_t epoch = 0;
+        if (pipe) {
+            const int64_t tiles = max_score_tiles(d);
+            epoch = ++c->epoch;
+            for (int v = 0; v < 2; ++v) {
+                if (!need_ml[v]) continue;
+                const size_t bytes = (size_t)(tiles + 1) * sizeof(int32_t);
+                if (c->ready[v].n < bytes) {
+                    if (int rc = c->ready[v].ensure(bytes)) return rc;
+                    CUDA_TRY(cudaMemsetAsync(c->ready[v].p, 0, c->ready[v].n, s));
+                }
+                ready[v] = (int32_t *)c->ready[v].p;
+                Pm.ready[v] = ready[v];
+            }
+            Pm.epoch = epoch;
+            for (int v = 0; v < 2; ++v)
+                if (need_ml[v]) {
+                    if (int rc = c->ranks[v].ensure((size_t)d.total_events * d.E + 64)) return rc;
+                    Pm.rank[v] = (const uint8_t *)c->ranks[v].p;
+                }
+            CUDA_TRY(cudaEventRecord(c->fork, s));
+            CUDA_TRY(cudaStreamWaitEvent(c->side2, c->fork, 0));
+            mark(c, 6, c->side2);
+            launched += launch_replay(Pm, c->side2);
+            mark(c, 7, c->side2);
+            c->ran[3] = true;
+        }
+        mark(c, 2, s);
+        for (int v = 0; v < 2; ++v) {
+            if (!need_ml[v]) continue;
+            if (int rc = c->ranks[v].ensure((size_t)d.total_events * d.E + 64)) return rc;
+            if (int rc = run_score(c, d, nets, v == 0 ? 1 : 0, (uint8_t *)c->ranks[v].p, nullptr, s, &launched,
+                                   ready[v], epoch))
+                return rc;
+            Pm.rank[v] = (const uint8_t *)c->ranks[v].p;
+        }
+        mark(c, 3, s);
+        c->ran[1] = true;
+        if (!pipe) {
+            mark(c, 6, s);
+            launched += launch_replay(Pm, s);
+            mark(c, 7, s);
+            c->ran[3] = true;
+        }
+    }
+    if (split) {
+        CUDA_TRY(cudaEventRecord(c->join, c->side));
+        CUDA_TRY(cudaStreamWaitEvent(s, c->join, 0));
+    }
+    if (pipe) {
+        CUDA_TRY(cudaEventRecord(c->join2, c->side2));
+        CUDA_TRY(cudaStreamWaitEvent(s, c->join2, 0));
+    }
+    mark(c, 8, s);
     launched += launch_fold(P, t->num_traces, out->reports, out->latency, s);
-    mark(c, 4, s);
+    mark(c, 9, s);
+    c->ran[4] = true;
     CUDA_TRY(cudaGetLastError());
     c->last_kernels = launched;
     return MCB_OK;

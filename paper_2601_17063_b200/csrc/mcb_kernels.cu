@@ -175,11 +175,13 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
     const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
     uint16_t *outc = P.outcomes ? P.outcomes + ((int64_t)pol_i * P.n_cap + cap_i) * tr.total_acc : nullptr;
 
+    const int64_t rank_tile0 = chain * ((tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV);   // uniform traces only
+    if (POL == POL_ML && n_ev > 0) wait_rank_tile(P, ml_variant, rank_tile0);
     uint32_t nrow[EPL];
 #pragma unroll
     for (int s = 0; s < EPL; ++s) {
         const int e = glane * EPL + s;
-        nrow[s] = (POL == POL_ML && n_ev > 0 && e < E) ? (uint32_t)__ldg(rank + e0 * E + e) : 0u;
+        nrow[s] = (POL == POL_ML && n_ev > 0 && e < E) ? (uint32_t)__ldcg(rank + e0 * E + e) : 0u;
     }
     uint32_t pos = 0, dec = 0;
     for (int64_t ev = 0; ev < n_ev; ++ev) {
@@ -195,11 +197,12 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
         if (POL == POL_ML) {
             // per-event score ranks (mlpolicy.py:59-62): argmax score == argmin (256 - rank);
             // the next event's row is already in flight (prefetched one event ahead)
+            if ((ev + 1) % MCB_TILE_EV == 0 && ev + 1 < n_ev) wait_rank_tile(P, ml_variant, rank_tile0 + (ev + 1) / MCB_TILE_EV);
 #pragma unroll
             for (int s = 0; s < EPL; ++s) {
                 key[s] = nrow[s] ? 256u - nrow[s] : KEY_SENT;
                 const int e = glane * EPL + s;
-                nrow[s] = (ev + 1 < n_ev && e < E) ? (uint32_t)__ldg(rank + (e0 + ev + 1) * E + e) : 0u;
+                nrow[s] = (ev + 1 < n_ev && e < E) ? (uint32_t)__ldcg(rank + (e0 + ev + 1) * E + e) : 0u;
             }
         }
         pin = 0;
@@ -302,12 +305,13 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
 
 template <int G, int EPL, bool UNIFORM>
 __global__ void __launch_bounds__(128) k_replay(const __grid_constant__ ReplayParams P) {
-    const int64_t inst = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-    const int64_t n_inst = P.tr.n_chains * P.n_pol * P.n_cap;
-    if (inst >= n_inst) return;
-    const int cap_i = (int)(inst % P.n_cap);
-    const int pol_i = (int)((inst / P.n_cap) % P.n_pol);
-    const int64_t chain = inst / ((int64_t)P.n_cap * P.n_pol);
+    const int64_t li = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;   // instance of this launch
+    const int64_t n_inst = P.tr.n_chains * P.n_pol_launch * P.n_cap;
+    if (li >= n_inst) return;
+    const int cap_i = (int)(li % P.n_cap);
+    const int pol_i = P.pol_map[(li / P.n_cap) % P.n_pol_launch];
+    const int64_t chain = li / ((int64_t)P.n_cap * P.n_pol_launch);
+    const int64_t inst = (chain * P.n_pol + pol_i) * P.n_cap + cap_i;
     switch (P.pol[pol_i]) {
         case MCB_LRU: replay_instance<G, EPL, POL_LRU, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
         case MCB_LFU: replay_instance<G, EPL, POL_LFU, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
@@ -357,9 +361,14 @@ struct Solo {
     static constexpr uint32_t KMAX = (1u << (32 - SH)) - 1u;   // keys must stay below this
 };
 
-template <int EM, int POL, bool UNIFORM>
-__device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t chain, int pol_i, int cap_i, int ml_variant,
-                                              uint32_t *s_pk, uint32_t *s_pend) {
+// Refetch without per-expert bookkeeping: ring[i] holds the experts evicted
+// at decode index dec - i (i = 0..window).  A victim's first access after its
+// eviction is a miss (it is not resident), so at a miss of x, x was evicted
+// within the window iff its bit is set in some ring slot; the bits of x are
+// cleared at that miss, and the ring shifts when the decode index advances.
+// Equivalent to _refetch_rate's next-access test (engine.py:266-297).
+template <int EM, int POL, bool UNIFORM, int WMAX>
+__device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t chain, int pol_i, int cap_i, int ml_variant) {
     // Branch-free per access: every access computes the would-be victim
     // (register min-tree over packed keys) and applies it under a predicate,
     // so the warp runs one straight-line instruction stream regardless of
@@ -367,18 +376,18 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
     constexpr int SH = Solo<EM>::SH;
     constexpr uint32_t KMAX = Solo<EM>::KMAX;
     const DevTrace &tr = P.tr;
-    const int tid = threadIdx.x;
     const uint32_t C = (uint32_t)P.cap[cap_i];
     const int E = tr.E;
+    const int W = P.window;          // 0 <= W <= WMAX (checked at launch)
     const int64_t inst = (chain * P.n_pol + pol_i) * P.n_cap + cap_i;
-    uint32_t *pd = s_pend + tid;    // pending-refetch marks pd[s * 128] (off the critical path)
-#pragma unroll
-    for (int s = 0; s < EM; ++s) pd[s * 128] = 0u;
-    (void)s_pk;
 
-    uint32_t pk[EM];                // packed keys (key << SH | id), all experts
+    uint32_t pk[EM];                 // packed keys (key << SH | id), all experts
 #pragma unroll
     for (int s = 0; s < EM; ++s) pk[s] = (uint32_t)s;
+    uint32_t ring[WMAX + 1];
+#pragma unroll
+    for (int s = 0; s <= WMAX; ++s) ring[s] = 0u;
+    uint32_t ring_or = 0u;
     uint32_t res = 0, pin = 0, seen = 0, valid = (1u << E) - 1u;
     uint32_t count = 0, ph = 0, pm = 0, dh = 0, dm = 0, nev = 0, comp = 0, refc = 0;
     double dlat = 0.0, plat = 0.0;
@@ -400,13 +409,15 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
     int64_t nch = a0 >> 2;
     uint4 ncur = make_uint4(0, 0, 0, 0), nnxt = make_uint4(0, 0, 0, 0);
     if (POL == POL_BELADY) { ncur = __ldg(np16 + nch); nnxt = __ldg(np16 + nch + 1); }
+    const int64_t rank_tile0 = chain * ((tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV);   // uniform traces only
+    if (POL == POL_ML && n_ev > 0) wait_rank_tile(P, ml_variant, rank_tile0);
     uint32_t rrow[EM];
 #pragma unroll
-    for (int s = 0; s < EM; ++s) rrow[s] = (POL == POL_ML && n_ev > 0 && s < E) ? __ldg(rank + e0 * E + s) : 0u;
+    for (int s = 0; s < EM; ++s) rrow[s] = (POL == POL_ML && n_ev > 0 && s < E) ? __ldcg(rank + e0 * E + s) : 0u;
     uint32_t info_next = (!UNIFORM && n_ev > 0) ? __ldg(tr.ev_info + e0) : 0u;
 
     int64_t A = a0;
-    uint32_t pos = 0, dec = 0;
+    uint32_t pos = 0;
     for (int64_t ev = 0; ev < n_ev; ++ev) {
         uint32_t info;
         if (UNIFORM) {
@@ -423,11 +434,12 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
         }
         if (POL == POL_ML) {
             valid = 0;
+            if ((ev + 1) % MCB_TILE_EV == 0 && ev + 1 < n_ev) wait_rank_tile(P, ml_variant, rank_tile0 + (ev + 1) / MCB_TILE_EV);
 #pragma unroll
             for (int s = 0; s < EM; ++s) {
                 pk[s] = ((256u - rrow[s]) << SH) | (uint32_t)s;
                 valid |= (rrow[s] != 0u ? 1u : 0u) << s;
-                rrow[s] = (ev + 1 < n_ev && s < E) ? __ldg(rank + (e0 + ev + 1) * E + s) : 0u;
+                rrow[s] = (ev + 1 < n_ev && s < E) ? __ldcg(rank + (e0 + ev + 1) * E + s) : 0u;
             }
         }
         pin = 0;
@@ -448,7 +460,7 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
             if (POL == POL_LFU) {
                 uint32_t cur = 0;
 #pragma unroll
-                for (int s = 0; s < EM; ++s) cur = ((bit >> s) & 1u) ? pk[s] : cur;
+                for (int s = 0; s < EM; ++s) cur |= ((bit >> s) & 1u) ? pk[s] : 0u;
                 nk = cur + (1u << SH);
             }
             if (POL == POL_BELADY) {
@@ -486,15 +498,14 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
             step_miss += miss ? 1u : 0u;
             if (decode) { dh += hit ? 1u : 0u; dm += miss ? 1u : 0u; }
             else { ph += hit ? 1u : 0u; pm += miss ? 1u : 0u; }
-            // compulsory (engine.py:248-250) and refetch of an earlier victim (engine.py:289-296)
-            const bool first = (seen & bit) == 0u;
-            comp += (miss && first) ? 1u : 0u;
-            if (miss && !first) {
-                const uint32_t pe = pd[x * 128];
-                if (pe && (int64_t)dec - (int64_t)(pe - 1u) <= (int64_t)P.window) ++refc;
-                pd[x * 128] = 0u;
-            }
-            if (evict) pd[v * 128] = dec + 1u;
+            // compulsory (engine.py:248-250) and refetch of a recent victim (ring above)
+            const uint32_t mbit = miss ? bit : 0u;
+            comp += (mbit & ~seen) ? 1u : 0u;
+            refc += (mbit & ring_or) ? 1u : 0u;
+            ring_or = (ring_or & ~mbit) | vbit;
+#pragma unroll
+            for (int s = 0; s <= WMAX; ++s) ring[s] &= ~mbit;
+            ring[0] |= vbit;
             seen |= bit;
             pin |= decode ? bit : 0u;
             if (track) {
@@ -508,9 +519,19 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
             lat = __dmul_rn((double)(P.loads_serial ? step_miss : 1u), P.t_load);
         else
             lat = __dmul_rn((double)nacc, P.t_compute);
-        if (decode) dlat = __dadd_rn(dlat, __dadd_rn(lat, POL == POL_ML ? P.ml_cost : 0.0));
-        else plat = __dadd_rn(plat, lat);
-        if (decode) ++dec;
+        if (decode) {
+            dlat = __dadd_rn(dlat, __dadd_rn(lat, POL == POL_ML ? P.ml_cost : 0.0));
+            // decode index advances: slot i now holds evictions from dec - i
+#pragma unroll
+            for (int s = WMAX; s >= 1; --s) ring[s] = ring[s - 1];
+            ring[0] = 0u;
+            uint32_t o = 0u;
+#pragma unroll
+            for (int s = 0; s <= WMAX; ++s) o |= (s <= W) ? ring[s] : 0u;
+            ring_or = o;
+        } else {
+            plat = __dadd_rn(plat, lat);
+        }
     }
     int64_t *o = P.inst_out + inst * MCB_R_N;
     o[MCB_R_PREFILL_HITS] = ph;
@@ -526,51 +547,77 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
     if (P.hashes) P.hashes[inst] = h;
 }
 
+#define SOLO_WMAX 7
+
 template <int EM, bool UNIFORM>
 __global__ void __launch_bounds__(128) k_replay_solo(const __grid_constant__ ReplayParams P) {
-    __shared__ uint32_t s_pend[EM * 128];
-    uint32_t *s_pk = nullptr;
-    const int pol_i = blockIdx.y;
+    const int pol_i = P.pol_map[blockIdx.y];
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= P.tr.n_chains * P.n_cap) return;
     const int cap_i = (int)(t % P.n_cap);
     const int64_t chain = t / P.n_cap;
     switch (P.pol[pol_i]) {
-        case MCB_LRU: solo_instance<EM, POL_LRU, UNIFORM>(P, chain, pol_i, cap_i, 0, s_pk, s_pend); break;
-        case MCB_LFU: solo_instance<EM, POL_LFU, UNIFORM>(P, chain, pol_i, cap_i, 0, s_pk, s_pend); break;
-        case MCB_BELADY: solo_instance<EM, POL_BELADY, UNIFORM>(P, chain, pol_i, cap_i, 0, s_pk, s_pend); break;
-        case MCB_ML: solo_instance<EM, POL_ML, UNIFORM>(P, chain, pol_i, cap_i, 0, s_pk, s_pend); break;
-        default: solo_instance<EM, POL_ML, UNIFORM>(P, chain, pol_i, cap_i, 1, s_pk, s_pend); break;
+        case MCB_LRU: solo_instance<EM, POL_LRU, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
+        case MCB_LFU: solo_instance<EM, POL_LFU, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
+        case MCB_BELADY: solo_instance<EM, POL_BELADY, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
+        case MCB_ML: solo_instance<EM, POL_ML, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
+        default: solo_instance<EM, POL_ML, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 1); break;
     }
 }
 
 template <int EM>
 static void launch_solo_t(const ReplayParams &p, cudaStream_t s) {
     const int64_t n = p.tr.n_chains * p.n_cap;
-    const dim3 grid((unsigned)((n + 127) / 128), (unsigned)p.n_pol);
-    if (p.tr.uniform) k_replay_solo<EM, true><<<grid, 128, 0, s>>>(p);
-    else k_replay_solo<EM, false><<<grid, 128, 0, s>>>(p);
+    // Few instances (latency-bound chains, e.g. one Mixtral trace): one warp
+    // per block, with a shared-memory reservation that keeps other kernels'
+    // blocks (the concurrently running K3) off its SM, so each replay warp
+    // issues alone.  Many instances: ordinary 128-thread blocks.
+    const int64_t warps = (n + 31) / 32 * p.n_pol_launch;
+    const bool exclusive = warps <= 64;
+    const int bs = exclusive ? 32 : 128;
+    const size_t smem = exclusive ? (size_t)160 * 1024 : 0;
+    const dim3 grid((unsigned)((n + bs - 1) / bs), (unsigned)p.n_pol_launch);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_replay_solo<EM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(k_replay_solo<EM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        attr_set = true;
+    }
+    if (p.tr.uniform) k_replay_solo<EM, true><<<grid, bs, smem, s>>>(p);
+    else k_replay_solo<EM, false><<<grid, bs, smem, s>>>(p);
 }
 
 template <int G, int EPL>
 static void launch_replay_t(const ReplayParams &p, cudaStream_t s) {
-    const int64_t n_inst = p.tr.n_chains * p.n_pol * p.n_cap;
+    const int64_t n_inst = p.tr.n_chains * p.n_pol_launch * p.n_cap;
     const int per_block = 128 / G;
     const unsigned blocks = (unsigned)((n_inst + per_block - 1) / per_block);
     if (p.tr.uniform) k_replay<G, EPL, true><<<blocks, 128, 0, s>>>(p);
     else k_replay<G, EPL, false><<<blocks, 128, 0, s>>>(p);
 }
 
+int64_t replay_blocks(const ReplayParams &p) {
+    const int64_t n = p.tr.n_chains * p.n_cap;
+    const bool solo = p.tr.E <= 16 && p.tr.total_acc < (1ll << 27) &&
+                      n * p.n_pol_launch >= p.solo_min_instances && p.window >= 0 && p.window <= SOLO_WMAX;
+    if (solo) {
+        const int64_t warps = (n + 31) / 32 * p.n_pol_launch;
+        return warps <= 64 ? warps : (n + 127) / 128 * p.n_pol_launch;
+    }
+    return (n * p.n_pol_launch + 3) / 4;
+}
+
 int launch_replay(const ReplayParams &p, cudaStream_t s) {
-    if (p.tr.n_chains * p.n_pol * p.n_cap == 0) return 0;
+    if (p.tr.n_chains * p.n_pol_launch * p.n_cap == 0) return 0;
     const int E = p.tr.E;
     // solo kernels pack (key << 3|4 | id) into 32 bits: chains must stay below 2^28 accesses.
     // Thread-per-instance only pays off when there are enough instances to
     // fill the machine; few long chains (e.g. one Mixtral trace) are
     // latency-bound, and a whole warp per instance has the shorter per-access
     // critical path (lane-parallel victim search, no divergence).
-    const int64_t n_inst = p.tr.n_chains * p.n_pol * p.n_cap;
-    const bool solo_ok = p.tr.total_acc < (1ll << 27) && n_inst >= p.solo_min_instances;
+    const int64_t n_inst = p.tr.n_chains * p.n_pol_launch * p.n_cap;
+    const bool solo_ok = p.tr.total_acc < (1ll << 27) && n_inst >= p.solo_min_instances && p.window >= 0 &&
+                         p.window <= SOLO_WMAX;
     if (E <= 8 && solo_ok) launch_solo_t<8>(p, s);
     else if (E <= 16 && solo_ok) launch_solo_t<16>(p, s);
     else if (E <= 32) launch_replay_t<32, 1>(p, s);
@@ -921,7 +968,8 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
                                                      const int64_t *__restrict__ tile_off,
                                                      const int32_t *__restrict__ snaps, int64_t n_tiles,
                                                      uint8_t *__restrict__ ranks, double *__restrict__ scores,
-                                                     unsigned long long *uncertain) {
+                                                     unsigned long long *uncertain, int32_t *ready,
+                                                     int32_t epoch) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int E = tr.E, D = 2 * E;
     const int ra = D > H ? D : H;
@@ -931,13 +979,16 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
     uint8_t *s_rank = (uint8_t *)(bufB + rb * MCB_TILE_EV);  // [TILE][E]
     int32_t *s_flag = (int32_t *)(s_rank + MCB_TILE_EV * MCB_MAX_EXPERTS);  // [TILE]
 
-    const int64_t tile = blockIdx.x;
+    int64_t tile = blockIdx.x;
     if (tile >= n_tiles) return;
     int64_t c, tile_in_chain;
     if (tr.uniform) {
+        // blocks sweep tile-in-chain major so early events of every chain are
+        // scored first (the pipelined ML replay consumes them in event order)
         const int64_t tpc = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
-        c = tile / tpc;
-        tile_in_chain = tile % tpc;
+        c = tile % tr.n_chains;
+        tile_in_chain = tile / tr.n_chains;
+        tile = c * tpc + tile_in_chain;
     } else {
         if (tile >= tile_off[tr.n_chains]) return;  // grid is an upper bound in general mode
         int64_t lo = 0, hi = tr.n_chains;          // largest c with tile_off[c] <= tile
@@ -1096,6 +1147,13 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
     __syncthreads();
     uint8_t *dst = ranks + (e0 + ev0) * E;
     for (int q = tid; q < nev * E; q += blockDim.x) dst[q] = s_rank[q];
+    if (ready != nullptr) {
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ready + tile), "r"(epoch) : "memory");
+        }
+    }
     if (tid == 0 && uncertain) {
         unsigned long long cnt = 0;
         for (int i = 0; i < nev; ++i) cnt += s_flag[i];
@@ -1103,9 +1161,25 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
     }
 }
 
+static size_t score_smem(int E, int H) {
+    const int D = 2 * E, ra = D > H ? D : H, rb = H > E ? H : E;
+    return (size_t)MCB_TILE_EV * (ra + rb) * sizeof(double) + MCB_TILE_EV * MCB_MAX_EXPERTS +
+           MCB_TILE_EV * sizeof(int32_t);
+}
+
+// Function attributes are set once per shape, outside any pipelined section.
+void prepare_launch_attributes(const DevTrace &tr, int H) {
+    static size_t done = 0;
+    const size_t smem = score_smem(tr.E, H);
+    if (smem > done) {
+        cudaFuncSetAttribute(k_score_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        done = smem;
+    }
+}
+
 int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill, uint8_t *ranks,
                  double *scores, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,
-                 unsigned long long *uncertain, cudaStream_t s) {
+                 unsigned long long *uncertain, int32_t *ready, int32_t epoch, cudaStream_t s) {
     if (tr.n_chains == 0) return 0;
     int launched = 0;
     if (tr.uniform) {
@@ -1119,15 +1193,38 @@ int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int 
         k_feat_snap<<<(unsigned)((tr.n_chains + 3) / 4), 128, 0, s>>>(tr, include_prefill, tile_off, snaps);
         launched += 2;
     }
-    const int E = tr.E, D = 2 * E;
-    const int ra = D > H ? D : H, rb = H > E ? H : E;
-    const size_t smem = (size_t)MCB_TILE_EV * (ra + rb) * sizeof(double) + MCB_TILE_EV * MCB_MAX_EXPERTS +
-                        MCB_TILE_EV * sizeof(int32_t);
-    cudaFuncSetAttribute(k_score_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    prepare_launch_attributes(tr, H);
+    const size_t smem = score_smem(tr.E, H);
     if (max_tiles > 0) {
         k_score_tile<<<(unsigned)max_tiles, 256, smem, s>>>(tr, wt, H, num_nets, include_prefill, tile_off, snaps,
-                                                            max_tiles, ranks, scores, uncertain);
+                                                            max_tiles, ranks, scores, uncertain,
+                                                            tr.uniform ? ready : nullptr, epoch);
         ++launched;
     }
     return launched;
+}
+
+// Force-load every kernel of the library at context creation.  With CUDA 12
+// lazy module loading the first launch of a kernel may wait for the device
+// to go idle, which would deadlock the pipelined ML replay (it spins on K3's
+// flags while K3 itself would be waiting to be loaded).
+int preload_kernels() {
+    cudaFuncAttributes a;
+    const void *fns[] = {
+        (const void *)k_next_use, (const void *)k_fold, (const void *)k_prepare_nets, (const void *)k_tile_offsets,
+        (const void *)k_feat_snap, (const void *)k_tile_summary, (const void *)k_snap_scan, (const void *)k_score_tile,
+        (const void *)k_replay<32, 1, true>, (const void *)k_replay<32, 1, false>,
+        (const void *)k_replay<32, 2, true>, (const void *)k_replay<32, 2, false>,
+        (const void *)k_replay<32, 4, true>, (const void *)k_replay<32, 4, false>,
+        (const void *)k_replay_solo<8, true>, (const void *)k_replay_solo<8, false>,
+        (const void *)k_replay_solo<16, true>, (const void *)k_replay_solo<16, false>,
+    };
+    for (const void *f : fns)
+        if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
+    cudaFuncSetAttribute(k_replay_solo<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_replay_solo<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_replay_solo<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_replay_solo<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_score_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    return 0;
 }

@@ -37,7 +37,9 @@ struct DevTrace {
 
 struct ReplayParams {
     DevTrace tr;
-    int n_pol, n_cap;
+    int n_pol, n_cap;                   // totals (output indexing)
+    int n_pol_launch;                   // policies replayed by this launch ...
+    int32_t pol_map[MCB_MAX_POL];       // ... and their indices in pol[]
     int32_t pol[MCB_MAX_POL];
     int32_t cap[MCB_MAX_CAP];
     const uint32_t *next_pos;           // K2 output (Belady)
@@ -49,15 +51,34 @@ struct ReplayParams {
     uint64_t *hashes;                   // optional [chain][pol][cap]
     uint16_t *outcomes;                 // optional [pol][cap][total_acc]
     int64_t solo_min_instances;         // thread-per-instance kernel threshold (E <= 16)
+    // K3 -> K4(ML) pipelining (uniform traces): K3 publishes ready[v][tile] = epoch
+    // once a tile's rank rows are in HBM; the ML replay waits on it per tile.
+    const int32_t *ready[2];
+    int32_t epoch;
 };
+
+// wait until the rank rows of chain-tile `tile` of variant `v` are published
+__device__ __forceinline__ void wait_rank_tile(const ReplayParams &P, int v, int64_t tile) {
+    const int32_t *f = P.ready[v];
+    if (f == nullptr) return;
+    for (;;) {
+        int32_t x;
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(x) : "l"(f + tile) : "memory");
+        if (x == P.epoch) break;
+        __nanosleep(256);
+    }
+}
 
 // launchers (mcb_kernels.cu); return the number of kernels launched or <0 on error
 int launch_next_use(const DevTrace &tr, uint32_t *next_pos, cudaStream_t s);
 int launch_replay(const ReplayParams &p, cudaStream_t s);
+int64_t replay_blocks(const ReplayParams &p);   // blocks launch_replay would use
+void prepare_launch_attributes(const DevTrace &tr, int H);
+int preload_kernels();   // force module loading + smem attributes (call at context creation)
 int launch_fold(const ReplayParams &p, int num_traces, int64_t *reports, double *latency, cudaStream_t s);
 int launch_prepare_nets(const double *params, int E, int H, int num_nets, double *wt, cudaStream_t s);
 __host__ __device__ size_t prepared_net_doubles(int E, int H);
 // K3: snapshot scan + tile scorer. snaps scratch: n_tiles_total * (2E+1) int32; tile_off: n_chains+1 int64
 int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill,
                  uint8_t *ranks, double *scores, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,
-                 unsigned long long *uncertain, cudaStream_t s);
+                 unsigned long long *uncertain, int32_t *ready, int32_t epoch, cudaStream_t s);

@@ -264,6 +264,15 @@ int make_map(CUtensorMap *map, const void *base, uint64_t rows, uint64_t cols, u
 
 }  // namespace k1
 
+int mcb_router_preload() {
+    cudaFuncAttributes a;
+    if (cudaFuncGetAttributes(&a, (const void *)k1::router_topk_kernel) != cudaSuccess)
+        return mcb_set_error(MCB_ERR_CUDA, "failed to load the router kernel");
+    const size_t smem = (size_t)k1::STAGES * k1::STAGE_BYTES + 1024 + 256;
+    cudaFuncSetAttribute(k1::router_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return MCB_OK;
+}
+
 // hidden: bf16 [T][d] (d a multiple of 64, 16-B aligned rows); weight: bf16
 // [L*Ep][d] with Ep = num_experts rounded up to a divisor of 256 (rows of
 // padding experts are ignored); acc: uint8 [L][T][K].

@@ -114,8 +114,9 @@ class DeviceReplay:
         _lib.check(self.lib.mcb_set_timing(self.ctx, int(enable)))
 
     def stage_ms(self):
-        ms = (ctypes.c_float * 4)()
-        _lib.check(self.lib.mcb_last_timings(self.ctx, ms, 4))
+        """[K2 next-use, K3 scorer, K4 replay (non-ML launch), K4 replay (ML launch), K5 fold] in ms."""
+        ms = (ctypes.c_float * 5)()
+        _lib.check(self.lib.mcb_last_timings(self.ctx, ms, 5))
         return list(ms)
 
     def kernels_launched(self) -> int:

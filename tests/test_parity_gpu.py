@@ -64,7 +64,7 @@ def kernel_variant(request):
     instance, and one thread per instance (num_experts <= 16)."""
     _lib.set_tuning(_lib.MCB_TUNE_SOLO_MIN, 0 if request.param == "solo" else 1 << 62)
     yield request.param
-    _lib.set_tuning(_lib.MCB_TUNE_SOLO_MIN, 16384)
+    _lib.set_tuning(_lib.MCB_TUNE_SOLO_MIN, 0)
 
 
 @pytest.mark.parametrize("part", range(4))
