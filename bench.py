@@ -384,8 +384,9 @@ def main():
                        "stage_ms_per_step": {"k2_next_use": stage[0] / args.steps, "k3_scorer": stage[1] / args.steps,
                                              "k4_replay_non_ml": stage[2] / args.steps,
                                              "k4_replay_ml": stage[3] / args.steps, "k5_fold": stage[4] / args.steps,
-                                             "note": "K2 + K4(non-ML) run on a side stream concurrently "
-                                                     "with K3 -> K4(ML)"}},
+                                             "note": "K4(non-ML) runs on a side stream concurrently with "
+                                                     "K3 -> K4(ML); K4 stages include the segmented "
+                                                     "spec + finish kernels when used"}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "k_replay (K4)",
                          "peak_source": peak_kind,

@@ -167,6 +167,10 @@ int mcb_set_timing(mcb_ctx *ctx, int32_t enable);
  * MCB_TUNE_SOLO_MIN: minimum instance count for the thread-per-instance
  * replay kernel (num_experts <= 16); below it one warp replays one instance. */
 #define MCB_TUNE_SOLO_MIN 0
+/* MCB_TUNE_SEG_EV: segmented speculative replay of uniform traces with
+ * num_experts <= 16 (mcb_segment.cu): 0 = automatic (used when the instances
+ * are too few to fill the GPU), < 0 = off, > 0 = events per segment. */
+#define MCB_TUNE_SEG_EV 1
 int mcb_set_tuning(mcb_ctx *ctx, int32_t knob, int64_t value);
 int mcb_last_timings(mcb_ctx *ctx, float *ms, int32_t n);
 

@@ -274,11 +274,16 @@ static inline uint64_t fnv16(uint64_t h, uint16_t c) {
     return h;
 }
 
+/* Spliceable decision hash used by the CUDA engine: h = h * P + (code + 1)
+ * mod 2^64 over the per-access outcome codes, so h(AB) = h(A) * P^|B| + h(B).
+ * (FNV-1a above is the hash stored in the reference-made fixtures.) */
+static inline uint64_t poly16(uint64_t h, uint16_t c) { return h * FNV_PRIME + (uint64_t)c + 1u; }
+
 /* evictions list for _refetch_rate (engine.py:266-297) */
 typedef struct { int64_t pos, decode_index; int victim; } evrec;
 
 static int replay_layer(const orc_layer *ly, const orc_cfg *cfg, int64_t *cnt, double *lat,
-                        uint16_t *outcomes, uint64_t *hash) {
+                        uint16_t *outcomes, uint64_t *hash /* [2]: fnv, poly */) {
     const int E = cfg->E, C = cfg->capacity;
     int rc = ORC_OK;
     uint8_t *res = (uint8_t *)calloc((size_t)E, 1);
@@ -304,7 +309,7 @@ static int replay_layer(const orc_layer *ly, const orc_cfg *cfg, int64_t *cnt, d
     for (int e = 0; e < E; ++e) rec[e] = INFINITY;
 
     int n_res = 0;
-    uint64_t h = FNV_OFF;
+    uint64_t h = FNV_OFF, hp = 0;
     double dlat = 0.0, plat = 0.0;
     for (int k = 0; k < C_N; ++k) cnt[k] = 0;
 
@@ -405,6 +410,7 @@ static int replay_layer(const orc_layer *ly, const orc_cfg *cfg, int64_t *cnt, d
             }
             if (outcomes) outcomes[pos] = code;
             h = fnv16(h, code);
+            hp = poly16(hp, code);
             if (decode) pinned[xe] = 1;
         }
         /* step_latency_s (engine.py:58-62) and accumulation (engine.py:258-262) */
@@ -428,7 +434,7 @@ static int replay_layer(const orc_layer *ly, const orc_cfg *cfg, int64_t *cnt, d
     }
     lat[0] = dlat;
     lat[1] = plat;
-    if (hash) *hash = h;
+    if (hash) { hash[0] = h; hash[1] = hp; }
 done:
     if (have_ix) index_free(&ix);
     free(res); free(pinned); free(seen); free(stamp); free(freq); free(rec); free(fr);
@@ -443,7 +449,7 @@ done:
 /*
  * Simulate one trace under one (policy, capacity).  The trace is flat:
  * events in stored order with seq/phase/layer and CSR experts.
- * Outputs per layer: cnt[L][C_N], lat[L][2] (decode, prefill), hashes[L];
+ * Outputs per layer: cnt[L][C_N], lat[L][2] (decode, prefill), hashes[L][2] (fnv, poly);
  * outcomes (optional) are written at outcome_off[l] + position.
  * The caller folds layers in layer order (engine.py:330-343).
  */
@@ -463,7 +469,7 @@ int orc_simulate(int L, int E, int64_t n_events, const int64_t *seq, const uint8
         if (policy == ORC_ML) cfg.net = nets + (n_nets == 1 ? 0 : (size_t)l * np);
         if (layer_len) layer_len[l] = ls[l].n_acc;
         rc = replay_layer(&ls[l], &cfg, cnt + (size_t)l * C_N, lat + 2 * l,
-                          outcomes ? outcomes + outcome_off[l] : NULL, hashes ? hashes + l : NULL);
+                          outcomes ? outcomes + outcome_off[l] : NULL, hashes ? hashes + 2 * l : NULL);
     }
     free_layers(ls, L);
     return rc;
@@ -503,7 +509,7 @@ typedef struct {
     int loads_serial, window;
     int64_t *cnt;     /* [chain][job][C_N] */
     double *lat;      /* [chain][job][2] */
-    uint64_t *hash;   /* [chain][job] */
+    uint64_t *hash;   /* [chain][job][2] (fnv, poly) */
     int64_t next;     /* work counter */
     pthread_mutex_t mu;
     int rc;
@@ -544,7 +550,7 @@ static void *batch_worker(void *arg) {
                        b->nets ? b->nets + (size_t)(layer % b->n_nets) * np : NULL};
         int rc = replay_layer(&ly, &cfg, b->cnt + ((size_t)c * b->n_jobs + j) * C_N,
                               b->lat + ((size_t)c * b->n_jobs + j) * 2, NULL,
-                              b->hash + (size_t)c * b->n_jobs + j);
+                              b->hash + ((size_t)c * b->n_jobs + j) * 2);
         if (rc) b->rc = rc;
     }
 out:

@@ -83,12 +83,10 @@ struct mcb_ctx {
     int64_t last_uncertain = 0;
     bool timing = false;
     cudaStream_t side = nullptr;       // non-ML replay runs here concurrently with K3
-    cudaStream_t side2 = nullptr;      // pipelined ML replay (waits on K3's per-tile flags)
-    cudaEvent_t join2 = nullptr;
-    DevBuf ready[2];                   // per-(chain, tile) "ranks published" flags
-    int32_t epoch = 0;
     cudaEvent_t fork = nullptr, join = nullptr;
     int64_t solo_min_instances = 0;   // thread-per-instance whenever E <= 16 (MCB_SOLO_MIN overrides)
+    int64_t seg_ev = 0;               // segmented replay: 0 auto, <0 off, >0 events per segment (MCB_SEG_EV)
+    DevBuf seg_snap, seg_summ, seg_out, seg_codes;
     cudaEvent_t ev[10] = {};          // start/stop per stage: K2, K3, K4 non-ML, K4 ML, K5
     bool ran[5] = {};
 };
@@ -117,6 +115,10 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
         c->solo_min_instances = value;
         return MCB_OK;
     }
+    if (knob == MCB_TUNE_SEG_EV) {
+        c->seg_ev = value;
+        return MCB_OK;
+    }
     return mcb_set_error(MCB_ERR_INVALID, "unknown tuning knob");
 }
 
@@ -142,18 +144,18 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     CUDA_TRY(cudaGetDeviceProperties(&prop, device));
     if (prop.major < 10)
         return mcb_set_error(MCB_ERR_UNSUPPORTED, "libmcb is built for sm_100a (B200); device is older");
-    if (preload_kernels() != 0) return mcb_set_error(MCB_ERR_CUDA, "failed to load the replay kernels");
+    if (preload_kernels() != 0 || preload_segment_kernels() != 0)
+        return mcb_set_error(MCB_ERR_CUDA, "failed to load the replay kernels");
     if (int rc = mcb_router_preload()) return rc;
     auto *c = new (std::nothrow) mcb_ctx();
     if (!c) return mcb_set_error(MCB_ERR_NOMEM, "out of host memory");
     c->device = device;
     if (const char *env = getenv("MCB_SOLO_MIN")) c->solo_min_instances = atoll(env);
+    if (const char *env = getenv("MCB_SEG_EV")) c->seg_ev = atoll(env);
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);   // replay warps dispatch ahead of K3 blocks
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&c->side2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->join2, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess) {
         delete c;
@@ -169,14 +171,11 @@ extern "C" int mcb_ctx_destroy(mcb_ctx *c) {
     DevBuf *all[] = {&c->next_pos, &c->ranks[0], &c->ranks[1], &c->inst_out, &c->inst_lat, &c->wt, &c->snaps,
                      &c->tile_off, &c->stats, &c->pol_caps, &c->h_acc, &c->h_acc_off, &c->h_ev_off,
                      &c->h_rt_off, &c->h_ev_info, &c->h_routed, &c->h_params, &c->h_reports, &c->h_latency,
-                     &c->h_chain_reports, &c->h_hashes, &c->h_outcomes};
+                     &c->h_chain_reports, &c->h_hashes, &c->h_outcomes, &c->seg_snap, &c->seg_summ,
+                     &c->seg_out, &c->seg_codes};
     for (DevBuf *b : all) b->release();
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->side) cudaStreamDestroy(c->side);
-    if (c->side2) cudaStreamDestroy(c->side2);
-    if (c->join2) cudaEventDestroy(c->join2);
-    c->ready[0].release();
-    c->ready[1].release();
     if (c->fork) cudaEventDestroy(c->fork);
     if (c->join) cudaEventDestroy(c->join);
     for (auto &e : c->ev)
@@ -231,9 +230,7 @@ static int64_t max_score_tiles(const DevTrace &d) {
     return d.total_events / MCB_TILE_EV + d.n_chains;  // upper bound of sum(ceil(n_c / TILE))
 }
 
-// All device allocations of K3 happen here, before anything is launched:
-// cudaMalloc may synchronise the device, which must never happen while a
-// pipelined replay kernel is already waiting on K3's flags.
+// All device allocations of K3 happen here, before anything is launched.
 static int ensure_score_buffers(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets) {
     const int E = d.E, H = nets->hidden;
     const size_t per = prepared_net_doubles(E, H);
@@ -245,8 +242,7 @@ static int ensure_score_buffers(mcb_ctx *c, const DevTrace &d, const mcb_nets *n
 }
 
 static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int include_prefill, uint8_t *ranks,
-                     double *scores, cudaStream_t s, int64_t *launched, int32_t *ready = nullptr,
-                     int32_t epoch = 0) {
+                     double *scores, cudaStream_t s, int64_t *launched) {
     const int E = d.E, H = nets->hidden;
     if (nets->num_experts != E) return mcb_set_error(MCB_ERR_SHAPE, "net num_experts does not match the trace");
     if (H < 1 || H > 256) return mcb_set_error(MCB_ERR_UNSUPPORTED, "net hidden size must be in [1, 256]");
@@ -260,7 +256,7 @@ static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int in
     const int64_t tiles = max_score_tiles(d);
     const int n = launch_score(d, (const double *)c->wt.p, H, nets->num_nets, include_prefill, ranks, scores,
                                (int32_t *)c->snaps.p, (int64_t *)c->tile_off.p, tiles,
-                               (unsigned long long *)c->stats.p, ready, epoch, s);
+                               (unsigned long long *)c->stats.p, s);
     *launched += n;
     return MCB_OK;
 }
@@ -350,8 +346,8 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     // Orchestration.  K3 (ML scores) is only needed by ML instances, so when
     // both kinds are present the non-ML replay runs on a high-priority side
     // stream concurrently with K3, and the ML replay follows K3:
-    //     s:    K2 --+-- K3 ........ K4(ml) --+-- K5
-    //     side:      +-- K4(lru/lfu/belady) --+
+    //     s:    K2 -- snapshot --+-- K3 -- K4(ml) --+-- K5
+    //     side:                  +-- K4(lru/lfu/belady) --+
     const int64_t n_inst = d.n_chains * n_pol * n_cap;
     if (out->chain_reports) {
         P.inst_out = out->chain_reports;
@@ -372,6 +368,38 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     const bool split = Pn.n_pol_launch > 0 && Pm.n_pol_launch > 0;
     cudaStream_t sn = split ? c->side : s;
     for (bool &r : c->ran) r = false;
+
+    // Segmented speculative replay (mcb_segment.cu) when the instances are
+    // too few to fill the GPU; every buffer is sized here, before any launch.
+    {
+        const int64_t n_launch = d.n_chains * n_cap * (Pn.n_pol_launch > Pm.n_pol_launch ? Pn.n_pol_launch
+                                                                                         : Pm.n_pol_launch);
+        ReplayParams probe = P;
+        probe.seg.n_seg = 2;
+        const bool solo_ok = n_launch >= c->solo_min_instances;
+        const int se = (c->seg_ev >= 0 && solo_ok && d.uniform) ? seg_events_per_segment(d.T, n_launch, c->seg_ev) : 0;
+        if (se > 0 && seg_eligible(probe)) {
+            P.seg.SE = se;
+            P.seg.n_seg = (int)((d.T + se - 1) / se);
+            P.seg.Tpad = (d.T + 15) / 16 * 16;
+            if (int rc = c->seg_snap.ensure(seg_snap_bytes(d.n_chains, P.seg.n_seg))) return rc;
+            if (int rc = c->seg_summ.ensure(seg_snap_bytes(d.n_chains, P.seg.n_seg))) return rc;
+            if (int rc = c->seg_out.ensure(seg_out_bytes(n_inst, P.seg.n_seg))) return rc;
+            if (int rc = c->seg_codes.ensure(seg_codes_bytes(n_inst, P.seg.Tpad))) return rc;
+            P.seg.snap = (int2 *)c->seg_snap.p;
+            P.seg.summ = (int2 *)c->seg_summ.p;
+            P.seg.out = (SegOut *)c->seg_out.p;
+            P.seg.codes = (uint8_t *)c->seg_codes.p;
+            Pn.seg = Pm.seg = P.seg;
+        }
+    }
+    if (Pm.n_pol_launch > 0) {
+        if (int rc = ensure_score_buffers(c, d, nets)) return rc;
+        for (int v = 0; v < 2; ++v)
+            if (need_ml[v])
+                if (int rc = c->ranks[v].ensure((size_t)d.total_events * d.E + 64)) return rc;
+        prepare_launch_attributes(d, nets->hidden);
+    }
     if (need_next) {
         if (int rc = c->next_pos.ensure((size_t)(d.total_acc + 64) * sizeof(uint32_t))) return rc;
         Pn.next_pos = Pm.next_pos = (const uint32_t *)c->next_pos.p;
@@ -380,81 +408,35 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         mark(c, 1, s);
         c->ran[0] = true;
     }
+    if (P.seg.n_seg > 1) launched += launch_seg_snapshot(P, s);
     if (split) {
         CUDA_TRY(cudaEventRecord(c->fork, s));
         CUDA_TRY(cudaStreamWaitEvent(c->side, c->fork, 0));
     }
     if (Pn.n_pol_launch > 0) {
         mark(c, 4, sn);
-        launched += launch_replay(Pn, sn);
+        launched += seg_eligible(Pn) ? launch_replay_segmented(Pn, sn) : launch_replay(Pn, sn);
         mark(c, 5, sn);
         c->ran[2] = true;
     }
-    // Pipelined ML replay (uniform traces, small ML grid): the ML K4 runs on
-    // its own high-priority stream concurrently with K3 and waits per tile on
-    // K3's release flags, so scoring and replay overlap event by event.  The
-    // ML grid is kept far below the SM count, so K3 always has SMs to finish
-    // (no deadlock) while the replay warps spin-sleep.
-    const bool pipe = Pm.n_pol_launch > 0 && d.uniform && replay_blocks(Pm) <= 64;
     if (Pm.n_pol_launch > 0) {
-        if (int rc = ensure_score_buffers(c, d, nets)) return rc;
-        for (int v = 0; v < 2; ++v)
-            if (need_ml[v])
-                if (int rc = c->ranks[v].ensure((size_t)d.total_events * d.E + 64)) return rc;
-        prepare_launch_attributes(d, nets->hidden);
-        int32_t *ready[2] = {nullptr, nullptr};
-        int32_t epoch = 0;
-        if (pipe) {
-            const int64_t tiles = max_score_tiles(d);
-            epoch = ++c->epoch;
-            for (int v = 0; v < 2; ++v) {
-                if (!need_ml[v]) continue;
-                const size_t bytes = (size_t)(tiles + 1) * sizeof(int32_t);
-                if (c->ready[v].n < bytes) {
-                    if (int rc = c->ready[v].ensure(bytes)) return rc;
-                    CUDA_TRY(cudaMemsetAsync(c->ready[v].p, 0, c->ready[v].n, s));
-                }
-                ready[v] = (int32_t *)c->ready[v].p;
-                Pm.ready[v] = ready[v];
-            }
-            Pm.epoch = epoch;
-            for (int v = 0; v < 2; ++v)
-                if (need_ml[v]) {
-                    if (int rc = c->ranks[v].ensure((size_t)d.total_events * d.E + 64)) return rc;
-                    Pm.rank[v] = (const uint8_t *)c->ranks[v].p;
-                }
-            CUDA_TRY(cudaEventRecord(c->fork, s));
-            CUDA_TRY(cudaStreamWaitEvent(c->side2, c->fork, 0));
-            mark(c, 6, c->side2);
-            launched += launch_replay(Pm, c->side2);
-            mark(c, 7, c->side2);
-            c->ran[3] = true;
-        }
         mark(c, 2, s);
         for (int v = 0; v < 2; ++v) {
             if (!need_ml[v]) continue;
-            if (int rc = c->ranks[v].ensure((size_t)d.total_events * d.E + 64)) return rc;
-            if (int rc = run_score(c, d, nets, v == 0 ? 1 : 0, (uint8_t *)c->ranks[v].p, nullptr, s, &launched,
-                                   ready[v], epoch))
+            if (int rc = run_score(c, d, nets, v == 0 ? 1 : 0, (uint8_t *)c->ranks[v].p, nullptr, s, &launched))
                 return rc;
             Pm.rank[v] = (const uint8_t *)c->ranks[v].p;
         }
         mark(c, 3, s);
         c->ran[1] = true;
-        if (!pipe) {
-            mark(c, 6, s);
-            launched += launch_replay(Pm, s);
-            mark(c, 7, s);
-            c->ran[3] = true;
-        }
+        mark(c, 6, s);
+        launched += seg_eligible(Pm) ? launch_replay_segmented(Pm, s) : launch_replay(Pm, s);
+        mark(c, 7, s);
+        c->ran[3] = true;
     }
     if (split) {
         CUDA_TRY(cudaEventRecord(c->join, c->side));
         CUDA_TRY(cudaStreamWaitEvent(s, c->join, 0));
-    }
-    if (pipe) {
-        CUDA_TRY(cudaEventRecord(c->join2, c->side2));
-        CUDA_TRY(cudaStreamWaitEvent(s, c->join2, 0));
     }
     mark(c, 8, s);
     launched += launch_fold(P, t->num_traces, out->reports, out->latency, s);

@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include "mcb_kernels.cuh"
+#include "mcb_solo.cuh"
 
 #define FULL_MASK 0xFFFFFFFFu
 
@@ -81,8 +82,6 @@ int launch_next_use(const DevTrace &tr, uint32_t *next_pos, cudaStream_t s) {
 // a lane-local scan in slot order, a redux.sync min over the group, and a
 // ballot that picks the lowest lane among equal keys, i.e. the lowest id.
 // ===========================================================================
-enum { POL_LRU = 0, POL_LFU = 1, POL_BELADY = 2, POL_ML = 3 };
-
 #define KEY_SENT 0xFFFFFFFFu
 
 template <int G>
@@ -135,14 +134,6 @@ __device__ __forceinline__ uint32_t get_slot(const uint32_t (&a)[EPL], int slot)
     return v;
 }
 
-__device__ __forceinline__ uint64_t fnv16(uint64_t h, uint32_t code) {
-    h ^= (uint64_t)(code & 0xFFu);
-    h *= MCB_FNV_PRIME;
-    h ^= (uint64_t)((code >> 8) & 0xFFu);
-    h *= MCB_FNV_PRIME;
-    return h;
-}
-
 template <int G, int EPL, int POL, bool UNIFORM>
 __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t chain, int pol_i, int cap_i,
                                                 int64_t inst, int ml_variant) {
@@ -160,7 +151,7 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
     for (int s = 0; s < EPL; ++s) { key[s] = 0; pend[s] = 0; }
     uint32_t count = 0, ph = 0, pm = 0, dh = 0, dm = 0, nev = 0, comp = 0, refc = 0;
     double dlat = 0.0, plat = 0.0;
-    uint64_t h = MCB_FNV_OFF;
+    uint64_t h = 0;
     int status = MCB_OK;
 
     const int64_t a0 = tr.acc_begin(chain);
@@ -175,8 +166,6 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
     const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
     uint16_t *outc = P.outcomes ? P.outcomes + ((int64_t)pol_i * P.n_cap + cap_i) * tr.total_acc : nullptr;
 
-    const int64_t rank_tile0 = chain * ((tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV);   // uniform traces only
-    if (POL == POL_ML && n_ev > 0) wait_rank_tile(P, ml_variant, rank_tile0);
     uint32_t nrow[EPL];
 #pragma unroll
     for (int s = 0; s < EPL; ++s) {
@@ -197,7 +186,6 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
         if (POL == POL_ML) {
             // per-event score ranks (mlpolicy.py:59-62): argmax score == argmin (256 - rank);
             // the next event's row is already in flight (prefetched one event ahead)
-            if ((ev + 1) % MCB_TILE_EV == 0 && ev + 1 < n_ev) wait_rank_tile(P, ml_variant, rank_tile0 + (ev + 1) / MCB_TILE_EV);
 #pragma unroll
             for (int s = 0; s < EPL; ++s) {
                 key[s] = nrow[s] ? 256u - nrow[s] : KEY_SENT;
@@ -268,10 +256,10 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
             }
             if (decode && mine) pin |= bit;
             if (outc) {
-                h = fnv16(h, code);
+                h = poly16(h, code);
                 if (glane == 0) outc[A] = (uint16_t)code;
             } else if (P.hashes) {
-                h = fnv16(h, code);
+                h = poly16(h, code);
             }
         }
         if (status != MCB_OK) break;
@@ -323,58 +311,16 @@ __global__ void __launch_bounds__(128) k_replay(const __grid_constant__ ReplayPa
 
 // ---------------------------------------------------------------------------
 // K4-solo: one THREAD per cache instance, for num_experts <= 16.  All state
-// (resident / pinned / seen bitmasks, the EM per-expert keys and pending
-// refetch marks, counters) lives in registers, so an access costs no
-// cross-lane traffic; the victim is a register min-tree over packed
-// (key << 8 | expert) values, i.e. argmin of (key, id) over resident \ pinned.
-// blockIdx.y selects the policy, so a warp never diverges on policy; the
-// threads of a warp share chains (consecutive capacities of one chain), so
-// their id / next-use / rank loads coalesce into broadcasts.
+// (resident mask, refetch ring, the packed per-expert keys, counters) lives
+// in registers, so an access costs no cross-lane traffic; the per-access step
+// is sstep() (mcb_solo.cuh), shared with the segmented replay.  blockIdx.y
+// selects the policy, so a warp never diverges on policy; the threads of a
+// warp share chains (consecutive capacities of one chain), so their id /
+// next-use / rank loads coalesce into broadcasts.
 // ---------------------------------------------------------------------------
-template <int EM>
-__device__ __forceinline__ uint64_t min_tree(const uint64_t (&k)[EM]) {
-    uint64_t t[EM];
-#pragma unroll
-    for (int s = 0; s < EM; ++s) t[s] = k[s];
-#pragma unroll
-    for (int w = EM / 2; w >= 1; w /= 2)
-#pragma unroll
-        for (int s = 0; s < w; ++s) t[s] = t[s] < t[s + w] ? t[s] : t[s + w];
-    return t[0];
-}
-
-__device__ __forceinline__ uint32_t sel4(const uint4 &v, uint32_t i) {
-    uint32_t r = v.x;
-    r = i == 1 ? v.y : r;
-    r = i == 2 ? v.z : r;
-    r = i == 3 ? v.w : r;
-    return r;
-}
-
-__device__ __forceinline__ void prefetch_l2(const void *p) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
-template <int EM>
-struct Solo {
-    static constexpr int SH = EM == 8 ? 3 : 4;                 // id bits in a packed key
-    static constexpr uint32_t KMAX = (1u << (32 - SH)) - 1u;   // keys must stay below this
-};
-
-// Refetch without per-expert bookkeeping: ring[i] holds the experts evicted
-// at decode index dec - i (i = 0..window).  A victim's first access after its
-// eviction is a miss (it is not resident), so at a miss of x, x was evicted
-// within the window iff its bit is set in some ring slot; the bits of x are
-// cleared at that miss, and the ring shifts when the decode index advances.
-// Equivalent to _refetch_rate's next-access test (engine.py:266-297).
 template <int EM, int POL, bool UNIFORM, int WMAX>
 __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t chain, int pol_i, int cap_i, int ml_variant) {
-    // Branch-free per access: every access computes the would-be victim
-    // (register min-tree over packed keys) and applies it under a predicate,
-    // so the warp runs one straight-line instruction stream regardless of
-    // which of its instances hit or miss (no divergence, no reconvergence).
     constexpr int SH = Solo<EM>::SH;
-    constexpr uint32_t KMAX = Solo<EM>::KMAX;
     const DevTrace &tr = P.tr;
     const uint32_t C = (uint32_t)P.cap[cap_i];
     const int E = tr.E;
@@ -384,14 +330,13 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
     uint32_t pk[EM];                 // packed keys (key << SH | id), all experts
 #pragma unroll
     for (int s = 0; s < EM; ++s) pk[s] = (uint32_t)s;
-    uint32_t ring[WMAX + 1];
-#pragma unroll
-    for (int s = 0; s <= WMAX; ++s) ring[s] = 0u;
-    uint32_t ring_or = 0u;
-    uint32_t res = 0, pin = 0, seen = 0, valid = (1u << E) - 1u;
-    uint32_t count = 0, ph = 0, pm = 0, dh = 0, dm = 0, nev = 0, comp = 0, refc = 0;
+    SState<WMAX> S;
+    sstate_clear(S);
+    uint32_t pin = 0, seen = 0, valid = (1u << E) - 1u;
+    uint32_t ph = 0, pm = 0, dh = 0, dm = 0, comp = 0;
+    SCount n = {0u, 0u, 0u};
     double dlat = 0.0, plat = 0.0;
-    uint64_t h = MCB_FNV_OFF;
+    uint64_t h = 0;
     bool stuck = false;
 
     const int64_t a0 = tr.acc_begin(chain);
@@ -402,18 +347,12 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
     uint16_t *outc = P.outcomes ? P.outcomes + ((int64_t)pol_i * P.n_cap + cap_i) * tr.total_acc : nullptr;
     const bool track = outc != nullptr || P.hashes != nullptr;
 
-    const uint4 *ids16 = (const uint4 *)tr.acc;
-    int64_t ich = a0 >> 4;
-    uint4 icur = __ldg(ids16 + ich), inxt = __ldg(ids16 + ich + 1);
-    const uint4 *np16 = (const uint4 *)P.next_pos;
-    int64_t nch = a0 >> 2;
-    uint4 ncur = make_uint4(0, 0, 0, 0), nnxt = make_uint4(0, 0, 0, 0);
-    if (POL == POL_BELADY) { ncur = __ldg(np16 + nch); nnxt = __ldg(np16 + nch + 1); }
-    const int64_t rank_tile0 = chain * ((tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV);   // uniform traces only
-    if (POL == POL_ML && n_ev > 0) wait_rank_tile(P, ml_variant, rank_tile0);
+    IdReader ids;
+    ids.init(tr.acc, a0, a_end);
+    NextReader nx;
+    if (POL == POL_BELADY) nx.init(P.next_pos, a0, a_end);
     uint32_t rrow[EM];
-#pragma unroll
-    for (int s = 0; s < EM; ++s) rrow[s] = (POL == POL_ML && n_ev > 0 && s < E) ? __ldcg(rank + e0 * E + s) : 0u;
+    if (POL == POL_ML && n_ev > 0) load_rank_row<EM>(rrow, rank + e0 * E, E);
     uint32_t info_next = (!UNIFORM && n_ev > 0) ? __ldg(tr.ev_info + e0) : 0u;
 
     int64_t A = a0;
@@ -433,84 +372,26 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
             for (int s = 0; s < EM; ++s) pk[s] = (uint32_t)s;   // start_sequence (policies.py:184-185)
         }
         if (POL == POL_ML) {
-            valid = 0;
-            if ((ev + 1) % MCB_TILE_EV == 0 && ev + 1 < n_ev) wait_rank_tile(P, ml_variant, rank_tile0 + (ev + 1) / MCB_TILE_EV);
-#pragma unroll
-            for (int s = 0; s < EM; ++s) {
-                pk[s] = ((256u - rrow[s]) << SH) | (uint32_t)s;
-                valid |= (rrow[s] != 0u ? 1u : 0u) << s;
-                rrow[s] = (ev + 1 < n_ev && s < E) ? __ldcg(rank + (e0 + ev + 1) * E + s) : 0u;
-            }
+            solo_ml_keys<EM>(pk, valid, rrow);   // this event's rank row (mlpolicy.py:59-62)
+            if (ev + 1 < n_ev) load_rank_row<EM>(rrow, rank + (e0 + ev + 1) * E, E);
         }
         pin = 0;
         uint32_t step_miss = 0;
         for (uint32_t j = 0; j < nacc; ++j, ++pos, ++A) {
-            if ((A >> 4) != ich) {
-                ++ich;
-                icur = inxt;
-                inxt = __ldg(ids16 + ich + 1);
-                if ((ich & 7) == 0 && ((ich + 32) << 4) < a_end) prefetch_l2(ids16 + ich + 32);
-            }
-            const uint32_t x = (sel4(icur, (uint32_t)(A >> 2) & 3u) >> (8u * (uint32_t)(A & 3))) & 0xFFu;
+            const uint32_t x = ids.get(A);
             const uint32_t bit = 1u << x;
-            const bool hit = (res & bit) != 0u;
-            // policy key of x (capacity-independent)
-            uint32_t nk = 0;
-            if (POL == POL_LRU) nk = (pos << SH) | x;
-            if (POL == POL_LFU) {
-                uint32_t cur = 0;
-#pragma unroll
-                for (int s = 0; s < EM; ++s) cur |= ((bit >> s) & 1u) ? pk[s] : 0u;
-                nk = cur + (1u << SH);
-            }
-            if (POL == POL_BELADY) {
-                if ((A >> 2) != nch) {
-                    ++nch;
-                    ncur = nnxt;
-                    nnxt = __ldg(np16 + nch + 1);
-                    if ((nch & 7) == 0 && ((nch + 64) << 2) < a_end) prefetch_l2(np16 + nch + 64);
-                }
-                const uint32_t np = sel4(ncur, (uint32_t)A & 3u);
-                nk = ((np == MCB_NEXT_INF ? 0u : KMAX - np) << SH) | x;   // farthest next use = smallest key
-            }
-            if (POL != POL_ML) {
-#pragma unroll
-                for (int s = 0; s < EM; ++s) pk[s] = ((bit >> s) & 1u) ? nk : pk[s];
-            }
-            // would-be victim: argmin packed key over resident \ pinned
-            const uint32_t cand = res & ~pin & valid;
-            uint32_t t[EM];
-#pragma unroll
-            for (int s = 0; s < EM; ++s) t[s] = ((cand >> s) & 1u) ? pk[s] : ~0u;
-#pragma unroll
-            for (int w = EM / 2; w >= 1; w /= 2)
-#pragma unroll
-                for (int s = 0; s < w; ++s) t[s] = min(t[s], t[s + w]);
-            const bool miss = !hit;
-            const bool full = count >= C;
-            const bool evict = miss && full;
-            stuck |= evict && t[0] == ~0u;
-            const uint32_t v = t[0] & (uint32_t)(EM - 1);
-            const uint32_t vbit = evict ? (1u << v) : 0u;
-            res = (res & ~vbit) | bit;
-            count += (miss && !full) ? 1u : 0u;
-            nev += evict ? 1u : 0u;
-            step_miss += miss ? 1u : 0u;
-            if (decode) { dh += hit ? 1u : 0u; dm += miss ? 1u : 0u; }
-            else { ph += hit ? 1u : 0u; pm += miss ? 1u : 0u; }
-            // compulsory (engine.py:248-250) and refetch of a recent victim (ring above)
-            const uint32_t mbit = miss ? bit : 0u;
-            comp += (mbit & ~seen) ? 1u : 0u;
-            refc += (mbit & ring_or) ? 1u : 0u;
-            ring_or = (ring_or & ~mbit) | vbit;
-#pragma unroll
-            for (int s = 0; s <= WMAX; ++s) ring[s] &= ~mbit;
-            ring[0] |= vbit;
+            const uint32_t np = (POL == POL_BELADY) ? nx.get(A) : 0u;
+            solo_key_update<EM, POL>(pk, x, bit, pos, np);
+            uint32_t miss;
+            const uint32_t code = sstep<EM, WMAX>(S, pk, bit, pin, valid, C, n, stuck, miss);
+            step_miss += miss;
+            if (decode) { dh += 1u - miss; dm += miss; }
+            else { ph += 1u - miss; pm += miss; }
+            comp += (miss && !(seen & bit)) ? 1u : 0u;   // compulsory (engine.py:248-250)
             seen |= bit;
             pin |= decode ? bit : 0u;
             if (track) {
-                const uint32_t code = hit ? MCB_OUT_HIT : (evict ? v : MCB_OUT_MISS);
-                h = fnv16(h, code);
+                h = poly16(h, code);
                 if (outc) outc[A] = (uint16_t)code;
             }
         }
@@ -521,33 +402,25 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
             lat = __dmul_rn((double)nacc, P.t_compute);
         if (decode) {
             dlat = __dadd_rn(dlat, __dadd_rn(lat, POL == POL_ML ? P.ml_cost : 0.0));
-            // decode index advances: slot i now holds evictions from dec - i
-#pragma unroll
-            for (int s = WMAX; s >= 1; --s) ring[s] = ring[s - 1];
-            ring[0] = 0u;
-            uint32_t o = 0u;
-#pragma unroll
-            for (int s = 0; s <= WMAX; ++s) o |= (s <= W) ? ring[s] : 0u;
-            ring_or = o;
+            sstate_next_decode<WMAX>(S, W);
         } else {
             plat = __dadd_rn(plat, lat);
         }
     }
+    (void)SH;
     int64_t *o = P.inst_out + inst * MCB_R_N;
     o[MCB_R_PREFILL_HITS] = ph;
     o[MCB_R_PREFILL_MISSES] = pm;
     o[MCB_R_DECODE_HITS] = dh;
     o[MCB_R_DECODE_MISSES] = dm;
     o[MCB_R_COMPULSORY] = comp;
-    o[MCB_R_EVICTIONS] = nev;
-    o[MCB_R_REFETCHED] = refc;
+    o[MCB_R_EVICTIONS] = n.nev;
+    o[MCB_R_REFETCHED] = n.refc;
     o[MCB_R_STATUS] = stuck ? MCB_ERR_NO_EVICTABLE : MCB_OK;
     P.inst_lat[inst * 2 + 0] = dlat;
     P.inst_lat[inst * 2 + 1] = plat;
     if (P.hashes) P.hashes[inst] = h;
 }
-
-#define SOLO_WMAX 7
 
 template <int EM, bool UNIFORM>
 __global__ void __launch_bounds__(128) k_replay_solo(const __grid_constant__ ReplayParams P) {
@@ -594,17 +467,6 @@ static void launch_replay_t(const ReplayParams &p, cudaStream_t s) {
     const unsigned blocks = (unsigned)((n_inst + per_block - 1) / per_block);
     if (p.tr.uniform) k_replay<G, EPL, true><<<blocks, 128, 0, s>>>(p);
     else k_replay<G, EPL, false><<<blocks, 128, 0, s>>>(p);
-}
-
-int64_t replay_blocks(const ReplayParams &p) {
-    const int64_t n = p.tr.n_chains * p.n_cap;
-    const bool solo = p.tr.E <= 16 && p.tr.total_acc < (1ll << 27) &&
-                      n * p.n_pol_launch >= p.solo_min_instances && p.window >= 0 && p.window <= SOLO_WMAX;
-    if (solo) {
-        const int64_t warps = (n + 31) / 32 * p.n_pol_launch;
-        return warps <= 64 ? warps : (n + 127) / 128 * p.n_pol_launch;
-    }
-    return (n * p.n_pol_launch + 3) / 4;
 }
 
 int launch_replay(const ReplayParams &p, cudaStream_t s) {
@@ -968,8 +830,7 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
                                                      const int64_t *__restrict__ tile_off,
                                                      const int32_t *__restrict__ snaps, int64_t n_tiles,
                                                      uint8_t *__restrict__ ranks, double *__restrict__ scores,
-                                                     unsigned long long *uncertain, int32_t *ready,
-                                                     int32_t epoch) {
+                                                     unsigned long long *uncertain) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int E = tr.E, D = 2 * E;
     const int ra = D > H ? D : H;
@@ -983,8 +844,6 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
     if (tile >= n_tiles) return;
     int64_t c, tile_in_chain;
     if (tr.uniform) {
-        // blocks sweep tile-in-chain major so early events of every chain are
-        // scored first (the pipelined ML replay consumes them in event order)
         const int64_t tpc = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
         c = tile % tr.n_chains;
         tile_in_chain = tile / tr.n_chains;
@@ -1147,13 +1006,6 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
     __syncthreads();
     uint8_t *dst = ranks + (e0 + ev0) * E;
     for (int q = tid; q < nev * E; q += blockDim.x) dst[q] = s_rank[q];
-    if (ready != nullptr) {
-        __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ready + tile), "r"(epoch) : "memory");
-        }
-    }
     if (tid == 0 && uncertain) {
         unsigned long long cnt = 0;
         for (int i = 0; i < nev; ++i) cnt += s_flag[i];
@@ -1179,7 +1031,7 @@ void prepare_launch_attributes(const DevTrace &tr, int H) {
 
 int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill, uint8_t *ranks,
                  double *scores, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,
-                 unsigned long long *uncertain, int32_t *ready, int32_t epoch, cudaStream_t s) {
+                 unsigned long long *uncertain, cudaStream_t s) {
     if (tr.n_chains == 0) return 0;
     int launched = 0;
     if (tr.uniform) {
@@ -1197,8 +1049,7 @@ int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int 
     const size_t smem = score_smem(tr.E, H);
     if (max_tiles > 0) {
         k_score_tile<<<(unsigned)max_tiles, 256, smem, s>>>(tr, wt, H, num_nets, include_prefill, tile_off, snaps,
-                                                            max_tiles, ranks, scores, uncertain,
-                                                            tr.uniform ? ready : nullptr, epoch);
+                                                            max_tiles, ranks, scores, uncertain);
         ++launched;
     }
     return launched;

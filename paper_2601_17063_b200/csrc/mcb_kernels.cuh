@@ -9,8 +9,6 @@
 #define MCB_MAX_POL 8
 #define MCB_MAX_CAP 64
 #define MCB_TILE_EV 32          // events per scorer tile (K3)
-#define MCB_FNV_OFF 0xCBF29CE484222325ull
-#define MCB_FNV_PRIME 0x100000001B3ull
 
 // Chain-major trace view usable on the device (mcb.h mcb_trace, device pointers).
 struct DevTrace {
@@ -51,34 +49,47 @@ struct ReplayParams {
     uint64_t *hashes;                   // optional [chain][pol][cap]
     uint16_t *outcomes;                 // optional [pol][cap][total_acc]
     int64_t solo_min_instances;         // thread-per-instance kernel threshold (E <= 16)
-    // K3 -> K4(ML) pipelining (uniform traces): K3 publishes ready[v][tile] = epoch
-    // once a tile's rank rows are in HBM; the ML replay waits on it per tile.
-    const int32_t *ready[2];
-    int32_t epoch;
+    // segmented speculative replay (mcb_segment.cu); seg.n_seg == 0: whole-chain kernels
+    struct Seg {
+        int SE;                         // events per segment (multiple of 16)
+        int n_seg;                      // segments per chain
+        int64_t Tpad;                   // row stride of codes (events, multiple of 16)
+        int2 *snap;                     // [chain][seg][16] (last position before, count before)
+        int2 *summ;                     // scratch [chain][seg][16]
+        struct SegOut *out;             // [inst][seg]
+        uint8_t *codes;                 // [inst][Tpad] per-event miss counts
+    } seg;
 };
 
-// wait until the rank rows of chain-tile `tile` of variant `v` are published
-__device__ __forceinline__ void wait_rank_tile(const ReplayParams &P, int v, int64_t tile) {
-    const int32_t *f = P.ready[v];
-    if (f == nullptr) return;
-    for (;;) {
-        int32_t x;
-        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(x) : "l"(f + tile) : "memory");
-        if (x == P.epoch) break;
-        __nanosleep(256);
-    }
-}
+// Per (instance, segment) result of the speculative pass (mcb_segment.cu).
+struct SegOut {
+    uint32_t misses, nev, refc, comp;
+    uint32_t res;
+    int32_t stuck_ev;                   // first event (chain-relative) with no evictable expert, -1 none
+    uint32_t pad0, pad1;
+    uint64_t hash;                      // poly hash of the segment's outcome codes (from 0)
+    uint64_t pad2;
+    uint32_t ring[8];
+};
 
 // launchers (mcb_kernels.cu); return the number of kernels launched or <0 on error
 int launch_next_use(const DevTrace &tr, uint32_t *next_pos, cudaStream_t s);
 int launch_replay(const ReplayParams &p, cudaStream_t s);
-int64_t replay_blocks(const ReplayParams &p);   // blocks launch_replay would use
 void prepare_launch_attributes(const DevTrace &tr, int H);
 int preload_kernels();   // force module loading + smem attributes (call at context creation)
+// segmented replay (uniform traces, num_experts <= 16); seg_* are host helpers
+bool seg_eligible(const ReplayParams &p);
+int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se);
+size_t seg_snap_bytes(int64_t n_chains, int n_seg);
+size_t seg_out_bytes(int64_t n_inst, int n_seg);
+size_t seg_codes_bytes(int64_t n_inst, int64_t Tpad);
+int launch_seg_snapshot(const ReplayParams &p, cudaStream_t s);
+int launch_replay_segmented(const ReplayParams &p, cudaStream_t s);
+int preload_segment_kernels();
 int launch_fold(const ReplayParams &p, int num_traces, int64_t *reports, double *latency, cudaStream_t s);
 int launch_prepare_nets(const double *params, int E, int H, int num_nets, double *wt, cudaStream_t s);
 __host__ __device__ size_t prepared_net_doubles(int E, int H);
 // K3: snapshot scan + tile scorer. snaps scratch: n_tiles_total * (2E+1) int32; tile_off: n_chains+1 int64
 int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill,
                  uint8_t *ranks, double *scores, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,
-                 unsigned long long *uncertain, int32_t *ready, int32_t epoch, cudaStream_t s);
+                 unsigned long long *uncertain, cudaStream_t s);

@@ -1,0 +1,229 @@
+// Register-resident replay step for caches of num_experts <= 16 (one thread
+// per cache instance).  Shared by the whole-chain kernel (k_replay_solo) and
+// the segmented speculative replay (mcb_segment.cu) so both execute the
+// identical per-access arithmetic.
+//
+// Semantics: SURVEY.md Appendix A (S7, S9, S11) / policies.py:95-214,
+// mlpolicy.py:15-26, engine.py:229-257 (pinning), engine.py:266-297
+// (refetch).  Every policy's victim is the argmin over resident \ pinned of
+// a packed (key << SH | expert id) word; the keys depend on
+// the trace only, so two cache states replaying the same stretch of trace
+// share them.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mcb_kernels.cuh"
+
+enum { POL_LRU = 0, POL_LFU = 1, POL_BELADY = 2, POL_ML = 3 };
+
+#define SOLO_WMAX 7                       // largest refetch window of the solo kernels
+#define MCB_HASH_MUL 0x100000001B3ull     // poly hash: h = h * MUL + code + 1 (mod 2^64)
+
+__device__ __forceinline__ uint64_t poly16(uint64_t h, uint32_t code) {
+    return h * MCB_HASH_MUL + (uint64_t)code + 1ull;
+}
+
+__device__ __forceinline__ uint64_t pow_mul(uint64_t e) {   // MCB_HASH_MUL^e mod 2^64
+    uint64_t r = 1ull, b = MCB_HASH_MUL;
+    while (e) {
+        if (e & 1ull) r *= b;
+        b *= b;
+        e >>= 1;
+    }
+    return r;
+}
+
+__device__ __forceinline__ uint32_t sel4(const uint4 &v, uint32_t i) {
+    uint32_t r = v.x;
+    r = i == 1 ? v.y : r;
+    r = i == 2 ? v.z : r;
+    r = i == 3 ? v.w : r;
+    return r;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+template <int EM>
+struct Solo {
+    static constexpr int SH = EM == 8 ? 3 : 4;                 // id bits in a packed key
+    static constexpr uint32_t KMAX = (1u << (32 - SH)) - 1u;   // keys must stay below this
+};
+
+// Per-instance cache state.  The resident count is popc(res) (a miss that
+// does not evict adds one expert, an eviction swaps one for one).  Refetch
+// without per-expert bookkeeping: ring[i] holds the experts evicted at decode
+// index dec - i (i = 0..W); a victim's first access after its eviction is a
+// miss, so at a miss of x, x was evicted within the window iff its bit is in
+// some ring slot; its bits are cleared at that miss and the ring shifts when
+// the decode index advances (== _refetch_rate's next-access test).
+template <int WMAX>
+struct SState {
+    uint32_t res;
+    uint32_t ring_or;
+    uint32_t ring[WMAX + 1];
+};
+
+template <int WMAX>
+__device__ __forceinline__ void sstate_clear(SState<WMAX> &S) {
+    S.res = 0u;
+    S.ring_or = 0u;
+#pragma unroll
+    for (int s = 0; s <= WMAX; ++s) S.ring[s] = 0u;
+}
+
+struct SCount {
+    uint32_t misses, nev, refc;
+};
+
+// One access of expert x (bit = 1 << x) against state S.  pk[] are the packed
+// keys after this access's key update, pin the experts already accessed in
+// this decode event, valid the selectable experts (ML: rank != 0).
+// Branch-free: the would-be victim is always computed (register min-tree)
+// and applied under a predicate.  Returns the outcome code (MCB_OUT_HIT,
+// MCB_OUT_MISS or the victim id); *miss is set for the event's miss count.
+template <int EM, int WMAX>
+__device__ __forceinline__ uint32_t sstep(SState<WMAX> &S, const uint32_t (&pk)[EM], uint32_t bit, uint32_t pin,
+                                          uint32_t valid, uint32_t C, SCount &n, bool &stuck, uint32_t &miss_out) {
+    const uint32_t cand = S.res & ~pin & valid;
+    uint32_t t[EM];
+#pragma unroll
+    for (int s = 0; s < EM; ++s) t[s] = ((cand >> s) & 1u) ? pk[s] : ~0u;
+#pragma unroll
+    for (int w = EM / 2; w >= 1; w /= 2)
+#pragma unroll
+        for (int s = 0; s < w; ++s) t[s] = min(t[s], t[s + w]);
+    const bool hit = (S.res & bit) != 0u;
+    const bool miss = !hit;
+    const bool full = (uint32_t)__popc(S.res) >= C;
+    const bool evict = miss && full;
+    stuck |= evict && t[0] == ~0u;
+    const uint32_t v = t[0] & (uint32_t)(EM - 1);
+    const uint32_t vbit = evict ? (1u << v) : 0u;
+    S.res = (S.res & ~vbit) | bit;
+    n.misses += miss ? 1u : 0u;
+    n.nev += evict ? 1u : 0u;
+    const uint32_t mbit = miss ? bit : 0u;
+    n.refc += (mbit & S.ring_or) ? 1u : 0u;
+    S.ring_or = (S.ring_or & ~mbit) | vbit;
+#pragma unroll
+    for (int s = 0; s <= WMAX; ++s) S.ring[s] &= ~mbit;
+    S.ring[0] |= vbit;
+    miss_out = miss ? 1u : 0u;
+    return hit ? MCB_OUT_HIT : (evict ? v : MCB_OUT_MISS);
+}
+
+// decode index advances: slot i now holds evictions from dec - i
+template <int WMAX>
+__device__ __forceinline__ void sstate_next_decode(SState<WMAX> &S, int W) {
+#pragma unroll
+    for (int s = WMAX; s >= 1; --s) S.ring[s] = S.ring[s - 1];
+    S.ring[0] = 0u;
+    uint32_t o = 0u;
+#pragma unroll
+    for (int s = 0; s <= WMAX; ++s) o |= (s <= W) ? S.ring[s] : 0u;
+    S.ring_or = o;
+}
+
+// state equality as far as the future is concerned (ring slots > W are dead)
+template <int WMAX>
+__device__ __forceinline__ bool sstate_equal(const SState<WMAX> &A, const SState<WMAX> &B, int W) {
+    uint32_t d = A.res ^ B.res;
+#pragma unroll
+    for (int s = 0; s <= WMAX; ++s) d |= (s <= W) ? (A.ring[s] ^ B.ring[s]) : 0u;
+    return d == 0u;
+}
+
+// Sequential reader of a chain's uint8 id stream, 16 ids per vector load
+// with the next vector in flight and an L2 prefetch 512 B ahead.
+struct IdReader {
+    const uint4 *p;
+    int64_t ch;
+    int64_t end;   // absolute access index bound (for prefetch)
+    uint4 cur, nxt;
+    __device__ __forceinline__ void init(const uint8_t *acc, int64_t a, int64_t a_end) {
+        p = (const uint4 *)acc;
+        ch = a >> 4;
+        end = a_end;
+        cur = __ldg(p + ch);
+        nxt = __ldg(p + ch + 1);
+    }
+    __device__ __forceinline__ uint32_t get(int64_t a) {
+        if ((a >> 4) != ch) {
+            ++ch;
+            cur = nxt;
+            nxt = __ldg(p + ch + 1);
+            if ((ch & 7) == 0 && ((ch + 32) << 4) < end) prefetch_l2(p + ch + 32);
+        }
+        return (sel4(cur, (uint32_t)(a >> 2) & 3u) >> (8u * (uint32_t)(a & 3))) & 0xFFu;
+    }
+};
+
+// Sequential reader of next_pos (4 per vector load).
+struct NextReader {
+    const uint4 *p;
+    int64_t ch;
+    int64_t end;
+    uint4 cur, nxt;
+    __device__ __forceinline__ void init(const uint32_t *np, int64_t a, int64_t a_end) {
+        p = (const uint4 *)np;
+        ch = a >> 2;
+        end = a_end;
+        cur = __ldg(p + ch);
+        nxt = __ldg(p + ch + 1);
+    }
+    __device__ __forceinline__ uint32_t get(int64_t a) {
+        if ((a >> 2) != ch) {
+            ++ch;
+            cur = nxt;
+            nxt = __ldg(p + ch + 1);
+            if ((ch & 7) == 0 && ((ch + 64) << 2) < end) prefetch_l2(p + ch + 64);
+        }
+        return sel4(cur, (uint32_t)a & 3u);
+    }
+};
+
+// The trace-determined key of the accessed expert x at chain position pos
+// (absolute access index a), applied to the packed key array.  LFU counts
+// are carried in pk itself.
+template <int EM, int POL>
+__device__ __forceinline__ void solo_key_update(uint32_t (&pk)[EM], uint32_t x, uint32_t bit, uint32_t pos,
+                                                uint32_t np) {
+    constexpr int SH = Solo<EM>::SH;
+    constexpr uint32_t KMAX = Solo<EM>::KMAX;
+    uint32_t nk = 0;
+    if (POL == POL_LRU) nk = (pos << SH) | x;
+    if (POL == POL_LFU) {
+        uint32_t cur = 0;
+#pragma unroll
+        for (int s = 0; s < EM; ++s) cur |= ((bit >> s) & 1u) ? pk[s] : 0u;
+        nk = cur + (1u << SH);
+    }
+    if (POL == POL_BELADY) nk = ((np == MCB_NEXT_INF ? 0u : KMAX - np) << SH) | x;   // farthest next use first
+    if (POL != POL_ML) {
+#pragma unroll
+        for (int s = 0; s < EM; ++s) pk[s] = ((bit >> s) & 1u) ? nk : pk[s];
+    }
+}
+
+// ML: packed keys and the selectable mask from one event's rank row
+// (argmax score == argmin (256 - rank); rank 0 = NaN / -inf, never selected).
+template <int EM>
+__device__ __forceinline__ void solo_ml_keys(uint32_t (&pk)[EM], uint32_t &valid, const uint32_t (&rrow)[EM]) {
+    constexpr int SH = Solo<EM>::SH;
+    valid = 0u;
+#pragma unroll
+    for (int s = 0; s < EM; ++s) {
+        pk[s] = ((256u - rrow[s]) << SH) | (uint32_t)s;
+        valid |= (rrow[s] != 0u ? 1u : 0u) << s;
+    }
+}
+
+template <int EM>
+__device__ __forceinline__ void load_rank_row(uint32_t (&rrow)[EM], const uint8_t *row, int E) {
+#pragma unroll
+    for (int s = 0; s < EM; ++s) rrow[s] = s < E ? (uint32_t)__ldcg(row + s) : 0u;
+}

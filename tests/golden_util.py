@@ -46,3 +46,56 @@ def policy_name(spec):
 
 def include_prefill(spec):
     return True if isinstance(spec, str) else spec.get("include_prefill", True)
+
+
+M64 = (1 << 64) - 1
+HASH_MUL = 0x100000001B3
+FNV_OFF = 0xCBF29CE484222325
+
+
+def poly_hash(codes) -> int:
+    """The CUDA engine's spliceable decision hash: h = h * P + code + 1 mod 2^64."""
+    h = 0
+    for c in codes:
+        h = (h * HASH_MUL + int(c) + 1) & M64
+    return h
+
+
+def fnv_hash(codes) -> int:
+    """FNV-1a 64 over the u16 outcome codes (the fixtures' hash, make_golden.py)."""
+    h = FNV_OFF
+    for c in codes:
+        for b in (int(c) & 0xFF, int(c) >> 8):
+            h = ((h ^ b) * HASH_MUL) & M64
+    return h
+
+
+_POLY_CACHE: dict = {}
+
+
+def expected_poly_hashes(case, run_index: int) -> list:
+    """Per-layer poly hashes of the reference's decisions for one golden run.
+
+    From the recorded decisions when the fixture has them (checked against the
+    fixture's FNV hashes first); otherwise from the C oracle, whose FNV hashes
+    must equal the fixture's (the oracle is the reference's restatement)."""
+    key = (case["name"], run_index)
+    if key in _POLY_CACHE:
+        return _POLY_CACHE[key]
+    import oracle
+    run = case["runs"][run_index]
+    if "decisions" in run:
+        assert [format(fnv_hash(d), "016x") for d in run["decisions"]] == run["hashes"]
+        out = [poly_hash(d) for d in run["decisions"]]
+    else:
+        header, events = case_trace(case)
+        L, E, _ = header
+        name = policy_name(run["policy"])
+        nets = oracle.nets_from_spec(run["nets"], L, E, GOLDEN) if name == "ml" else None
+        kw = dict(cost=COSTS[run["cost"]], window=run["window"], nets=nets,
+                  include_prefill=include_prefill(run["policy"]))
+        _, fnv, _ = oracle.simulate(header, events, name, run["capacity"], **kw)
+        assert [format(h, "016x") for h in fnv] == run["hashes"]
+        _, out, _ = oracle.simulate(header, events, name, run["capacity"], hash_kind="poly", **kw)
+    _POLY_CACHE[key] = out
+    return out

@@ -83,3 +83,20 @@ def test_uniform_batch_matches_simulate():
         rep = oracle.fold_report(jobs[j][0], jobs[j][1], 5, cnt[:, j], lat[:, j], T)
         assert rep == run["report"]
         assert [format(int(h), "016x") for h in hsh[:, j]] == run["hashes"]
+
+
+def test_oracle_poly_hash_matches_recorded_decisions():
+    """The spliceable hash the CUDA engine reports (poly) is a function of the
+    same per-access outcome codes as the fixtures' FNV hash."""
+    from golden_util import poly_hash
+    for case in load("small_cases.json.gz")["cases"][::5]:
+        header, events = case_trace(case)
+        L, E, K = header
+        for run in case["runs"]:
+            if "decisions" not in run:
+                continue
+            name = policy_name(run["policy"])
+            nets = oracle.nets_from_spec(run["nets"], L, E, GOLDEN) if name == "ml" else None
+            _, hp, _ = oracle.simulate(header, events, name, run["capacity"], COSTS[run["cost"]], run["window"],
+                                       nets, include_prefill(run["policy"]), hash_kind="poly")
+            assert hp == [poly_hash(d) for d in run["decisions"]], case["name"]

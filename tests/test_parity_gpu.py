@@ -8,7 +8,8 @@ import numpy as np
 import pytest
 
 import oracle
-from golden_util import COSTS, GOLDEN, big_ids, case_trace, include_prefill, load, policy_name
+from golden_util import (COSTS, GOLDEN, big_ids, case_trace, expected_poly_hashes, include_prefill, load,
+                         policy_name)
 
 pytestmark = pytest.mark.gpu
 
@@ -39,7 +40,7 @@ def check_case(case, decisions=True):
     header, events = case_trace(case)
     L, E, K = header
     packed = mcb.pack_trace(to_trace(header, events))
-    for run in case["runs"]:
+    for ri, run in enumerate(case["runs"]):
         nets = oracle.nets_from_spec(run["nets"], L, E, GOLDEN) if policy_name(run["policy"]) == "ml" else None
         want_dec = decisions and "decisions" in run
         res = engine.replay_host(packed, [code_of(run["policy"])], [run["capacity"]], cost_of(run["cost"]),
@@ -48,7 +49,7 @@ def check_case(case, decisions=True):
                                      res["reports"][0, 0, 0], res["latency"][0, 0, 0], packed.decode_steps[0])
         assert int(res["reports"][0, 0, 0, _lib.R_STATUS]) == 0
         assert rep.to_dict() == run["report"], (case["name"], run["policy"], run["capacity"])
-        assert [format(int(h), "016x") for h in res["hashes"][:, 0, 0]] == run["hashes"], case["name"]
+        assert [int(h) for h in res["hashes"][:, 0, 0]] == expected_poly_hashes(case, ri), case["name"]
         if want_dec:
             got = []
             for l in range(L):
@@ -58,13 +59,17 @@ def check_case(case, decisions=True):
             assert got == run["decisions"], (case["name"], run["policy"])
 
 
-@pytest.fixture(params=["warp", "solo"])
+@pytest.fixture(params=["warp", "solo", "seg"])
 def kernel_variant(request):
-    """Run each parity case through both replay kernels: one warp per
-    instance, and one thread per instance (num_experts <= 16)."""
-    _lib.set_tuning(_lib.MCB_TUNE_SOLO_MIN, 0 if request.param == "solo" else 1 << 62)
+    """Run each parity case through every replay kernel: one warp per
+    instance, one thread per instance (num_experts <= 16), and the segmented
+    speculative replay (uniform traces, num_experts <= 16) with short
+    segments so the stitching is exercised."""
+    _lib.set_tuning(_lib.MCB_TUNE_SOLO_MIN, 1 << 62 if request.param == "warp" else 0)
+    _lib.set_tuning(_lib.MCB_TUNE_SEG_EV, {"warp": -1, "solo": -1, "seg": 32}[request.param])
     yield request.param
     _lib.set_tuning(_lib.MCB_TUNE_SOLO_MIN, 0)
+    _lib.set_tuning(_lib.MCB_TUNE_SEG_EV, 0)
 
 
 @pytest.mark.parametrize("part", range(4))
@@ -103,11 +108,11 @@ def test_full_size_c1_and_mixtral(which, kernel_variant):
     caps = list(dict.fromkeys(r["capacity"] for r in runs))
     nets = oracle.nets_from_spec({"kind": "per_layer_seed"}, L, E)
     res = engine.replay_host(packed, [code_of(p) for p in pols], caps, mcb.CostModel(), 5, nets, want_hashes=True)
-    for r in runs:
+    for ri, r in enumerate(runs):
         i, j = pols.index(policy_name(r["policy"])), caps.index(r["capacity"])
         rep = engine.assemble_report(pols[i], caps[j], 5, res["reports"][0, i, j], res["latency"][0, i, j], T)
         assert rep.to_dict() == r["report"], (case["name"], r["policy"], r["capacity"])
-        assert [format(int(h), "016x") for h in res["hashes"][:, i, j]] == r["hashes"]
+        assert [int(h) for h in res["hashes"][:, i, j]] == expected_poly_hashes(case, ri)
 
 
 def test_public_api_matches_reports():
