@@ -163,6 +163,11 @@ int mcb_last_stats(mcb_ctx *ctx, int64_t *kernels_launched, int64_t *uncertain_e
  * the last call (after the stream has been synchronised):
  * [0] K2 next-use scan, [1] K3 scorer, [2] K4 replay, [3] K5 fold. */
 int mcb_set_timing(mcb_ctx *ctx, int32_t enable);
+/* Device-side counters of the last mcb_replay (synchronises the device):
+ * [0] uncertain scorer events, [1] segmented replay: events replayed by the
+ * fix-up walk, [2] segments whose speculative state never converged,
+ * [3] segments walked. */
+int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
 /* Tuning knobs (results never depend on them):
  * MCB_TUNE_SOLO_MIN: minimum instance count for the thread-per-instance
  * replay kernel (num_experts <= 16); below it one warp replays one instance. */

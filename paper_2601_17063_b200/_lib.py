@@ -32,7 +32,7 @@ OUT_HIT, OUT_MISS = 0xFFFF, 0xFFFE
 
 EXPORTED_SYMBOLS = (
     "mcb_abi_version", "mcb_ctx_create", "mcb_ctx_destroy", "mcb_last_error", "mcb_last_stats",
-    "mcb_set_timing", "mcb_last_timings", "mcb_set_tuning",
+    "mcb_set_timing", "mcb_last_timings", "mcb_set_tuning", "mcb_read_stats",
     "mcb_pack_trace", "mcb_packed_view", "mcb_packed_positions", "mcb_packed_free",
     "mcb_replay", "mcb_replay_host", "mcb_next_use", "mcb_score", "mcb_router_topk",
 )
@@ -122,6 +122,7 @@ def load_library():
             "mcb_set_timing": ([P, i32], ctypes.c_int),
             "mcb_last_timings": ([P, P, i32], ctypes.c_int),
             "mcb_set_tuning": ([P, i32, i64], ctypes.c_int),
+            "mcb_read_stats": ([P, P, i32], ctypes.c_int),
             "mcb_next_use": ([P, P, P, P], ctypes.c_int),
             "mcb_score": ([P, P, P, i32, P, P, P], ctypes.c_int),
             "mcb_router_topk": ([P, P, P, i64, i32, i32, i32, i32, P, P, P], ctypes.c_int),
@@ -163,6 +164,14 @@ def context(device: int = 0) -> ctypes.c_void_p:
     with _lock:
         _contexts[device] = h
     return h
+
+
+def read_stats(device: int = 0) -> list:
+    """Device counters of the last replay: [uncertain scorer events, segmented
+    fix-up events, unconverged segments, segments walked, ...]."""
+    out = (ctypes.c_int64 * 8)()
+    check(load_library().mcb_read_stats(context(device), out, 8))
+    return list(out)
 
 
 def set_tuning(knob: int, value: int, device: int = 0):

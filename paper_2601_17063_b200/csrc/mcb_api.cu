@@ -184,6 +184,19 @@ extern "C" int mcb_ctx_destroy(mcb_ctx *c) {
     return MCB_OK;
 }
 
+extern "C" int mcb_read_stats(mcb_ctx *c, int64_t *out, int32_t n) {
+    mcb_clear_error();
+    if (!c || !out) return mcb_set_error(MCB_ERR_INVALID, "ctx / out is NULL");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (int rc = c->stats.ensure(64)) return rc;
+    unsigned long long v[8];
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(v, c->stats.p, sizeof v, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n && i < 8; ++i) out[i] = (int64_t)v[i];
+    return MCB_OK;
+}
+
 extern "C" int mcb_last_stats(mcb_ctx *c, int64_t *kernels, int64_t *uncertain) {
     if (!c) return mcb_set_error(MCB_ERR_INVALID, "ctx is NULL");
     if (kernels) *kernels = c->last_kernels;
@@ -342,6 +355,7 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     P.loads_serial = cost->loads_serial;
     P.window = cost->window;
     P.solo_min_instances = c->solo_min_instances;
+    P.stats = (unsigned long long *)c->stats.p;
 
     // Orchestration.  K3 (ML scores) is only needed by ML instances, so when
     // both kinds are present the non-ML replay runs on a high-priority side
@@ -381,14 +395,17 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         if (se > 0 && seg_eligible(probe)) {
             P.seg.SE = se;
             P.seg.n_seg = (int)((d.T + se - 1) / se);
+            P.seg.NW = seg_warmup_events(se);
+            P.seg.n_snap = (int)((d.T + MCB_SNAP_EV - 1) / MCB_SNAP_EV);
             P.seg.Tpad = (d.T + 15) / 16 * 16;
-            if (int rc = c->seg_snap.ensure(seg_snap_bytes(d.n_chains, P.seg.n_seg))) return rc;
-            if (int rc = c->seg_summ.ensure(seg_snap_bytes(d.n_chains, P.seg.n_seg))) return rc;
-            if (int rc = c->seg_out.ensure(seg_out_bytes(n_inst, P.seg.n_seg))) return rc;
+            if (int rc = c->seg_snap.ensure(seg_snap_bytes(d.n_chains, P.seg.n_snap))) return rc;
+            if (int rc = c->seg_summ.ensure(seg_snap_bytes(d.n_chains, P.seg.n_snap))) return rc;
+            if (int rc = c->seg_out.ensure(2 * seg_out_bytes(n_inst, P.seg.n_seg))) return rc;
             if (int rc = c->seg_codes.ensure(seg_codes_bytes(n_inst, P.seg.Tpad))) return rc;
             P.seg.snap = (int2 *)c->seg_snap.p;
             P.seg.summ = (int2 *)c->seg_summ.p;
-            P.seg.out = (SegOut *)c->seg_out.p;
+            P.seg.out[0] = (SegOut *)c->seg_out.p;
+            P.seg.out[1] = P.seg.out[0] + n_inst * P.seg.n_seg;
             P.seg.codes = (uint8_t *)c->seg_codes.p;
             Pn.seg = Pm.seg = P.seg;
         }

@@ -51,25 +51,36 @@ struct ReplayParams {
     int64_t solo_min_instances;         // thread-per-instance kernel threshold (E <= 16)
     // segmented speculative replay (mcb_segment.cu); seg.n_seg == 0: whole-chain kernels
     struct Seg {
-        int SE;                         // events per segment (multiple of 16)
+        int SE;                         // events per segment (multiple of MCB_SNAP_EV)
         int n_seg;                      // segments per chain
+        int NW;                         // warm-up events before each segment (multiple of MCB_SNAP_EV)
+        int n_snap;                     // snapshots per chain (every MCB_SNAP_EV events)
         int64_t Tpad;                   // row stride of codes (events, multiple of 16)
-        int2 *snap;                     // [chain][seg][16] (last position before, count before)
-        int2 *summ;                     // scratch [chain][seg][16]
-        struct SegOut *out;             // [inst][seg]
+        int2 *snap;                     // [chain][n_snap][16] (last position before, count before)
+        int2 *summ;                     // scratch [chain][n_snap][16]
+        struct SegOut *out[2];          // [inst][seg] of speculation pass 0 and pass 1
         uint8_t *codes;                 // [inst][Tpad] per-event miss counts
     } seg;
+    unsigned long long *stats;          // device counters (mcb_read_stats): [1] fix-up events,
+                                        // [2] unconverged segments, [3] segments walked
 };
+
+#define MCB_SNAP_EV 32           // key-snapshot granularity of the segmented replay (events)
+#define MCB_SEG_BINS 18          // miss-count histogram bins (K <= 16 -> 17 used)
 
 // Per (instance, segment) result of the speculative pass (mcb_segment.cu).
 struct SegOut {
-    uint32_t misses, nev, refc, comp;
-    uint32_t res;
+    uint32_t misses, nev, refc, comp;   // counters of the segment (speculative run)
+    uint32_t res_end;                   // state at the segment end ...
     int32_t stuck_ev;                   // first event (chain-relative) with no evictable expert, -1 none
-    uint32_t pad0, pad1;
+    uint32_t res_start;                 // ... and at the segment start (after the warm-up)
+    uint32_t pad0;
     uint64_t hash;                      // poly hash of the segment's outcome codes (from 0)
-    uint64_t pad2;
-    uint32_t ring[8];
+    uint32_t ring_end[4];               // refetch rings, 8 x 16-bit slots
+    uint32_t ring_start[4];
+    uint32_t pk_start[16];              // packed policy keys at the segment start (non-ML)
+    uint16_t hist[MCB_SEG_BINS];        // events per miss count
+    uint32_t pad1[5];                   // 192 bytes
 };
 
 // launchers (mcb_kernels.cu); return the number of kernels launched or <0 on error
@@ -80,7 +91,8 @@ int preload_kernels();   // force module loading + smem attributes (call at cont
 // segmented replay (uniform traces, num_experts <= 16); seg_* are host helpers
 bool seg_eligible(const ReplayParams &p);
 int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se);
-size_t seg_snap_bytes(int64_t n_chains, int n_seg);
+size_t seg_snap_bytes(int64_t n_chains, int n_snap);
+int seg_warmup_events(int se);
 size_t seg_out_bytes(int64_t n_inst, int n_seg);
 size_t seg_codes_bytes(int64_t n_inst, int64_t Tpad);
 int launch_seg_snapshot(const ReplayParams &p, cudaStream_t s);

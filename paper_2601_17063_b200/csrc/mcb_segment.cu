@@ -5,32 +5,45 @@
 // the cache state after access i depends on every earlier access.  A single
 // Mixtral-shaped trace has only 32 chains x policies x capacities = 768
 // instances of 131,072 accesses each -- far too few threads for 148 SMs.
-// But the policy keys depend on the trace alone (F1), and the cache state is
-// small (resident mask + refetch ring), so a chain can be cut into S segments
-// replayed in parallel and stitched exactly:
+// But the policy keys depend on the trace alone (F1) and the cache state is
+// small (resident mask + refetch ring), so a chain is cut into segments that
+// are replayed in parallel and stitched exactly:
 //
-//   snapshot  per (chain, segment): each expert's last access position and
-//             access count before the segment (two-pass scan) -> the exact
-//             policy keys at the segment start
-//   spec      one thread per (instance, segment): replay the segment from a
-//             GUESSED cache state (the min(C, #seen) experts with the best
-//             keys, empty refetch ring; exact for segment 0) and record the
-//             counters, the end state, the poly hash of its outcome codes and
-//             the per-event miss counts
-//   finish    one thread per instance walks its segments in order carrying the
-//             TRUE state: it replays segment k from the true state (A) and
-//             from the guess (B) in lockstep until the two states coincide --
-//             from there on the speculative run is the true run, so its
-//             counters / hash / end state are spliced in with the prefix
-//             corrected (counters by difference, hash via h(AB) = h(A) P^|B| +
-//             h(B)); if they never coincide, A's results are used and A's end
-//             state carries on.  It also folds the float64 latency over every
-//             event in order (engine.py:258-262), reading the per-event miss
-//             counts, so SimReport floats stay bit-identical.
+//   snapshot  every MCB_SNAP_EV events of every chain: each expert's last
+//             access position and access count so far (two-pass scan), i.e.
+//             the exact policy keys at that point
+//   spec      one thread per (instance, segment): start NW events before the
+//             segment from a guessed cache state (the min(C, #seen) experts
+//             the policy would evict last, empty refetch ring), replay the
+//             warm-up without counting -- states started apart coalesce --
+//             record the state at the segment start, then replay the segment
+//             and record its counters, end state, poly hash of the outcome
+//             codes, per-event miss counts and their histogram
+//   spec 2    (not for LRU, whose guess is already the exact resident set)
+//             every segment is replayed again from pass 1's END state of the
+//             previous segment -- the true state whenever that segment's
+//             speculation had coalesced -- so only segments behind a long
+//             non-coalescing stretch still differ from the true run
+//   finish    one warp per instance walks its segments in order carrying the
+//             TRUE state A.  If A equals the segment's recorded start state,
+//             the speculative run IS the true run and is spliced in whole.
+//             Otherwise A and the recorded start state B are replayed in
+//             lockstep until they coincide; from there on the speculative run
+//             is the true run, so its results are spliced in with the prefix
+//             corrected (counters by difference, hash via h(XY) = h(X) P^|Y| +
+//             h(Y)); if they never coincide, A's own results are used and A
+//             carries on.
 //
-// Results are identical to the whole-chain kernel by construction; the
-// states typically coincide within a few events (LRU: the guess is the exact
-// resident set, only the refetch ring differs for W+1 decode steps).
+// float64 latency (engine.py:258-262) is a sequential sum over events of
+// values from a (K+1)-entry table.  Inside one binade [2^(e-1), 2^e) of the
+// running sum, RN(S + v) = S + q(v) ulp with q(v) = v / ulp rounded to
+// nearest -- independent of S unless v / ulp is a tie -- so a whole segment
+// is folded from its miss-count histogram with integer arithmetic whenever it
+// stays in one binade and hits no tie, and event by event otherwise.  Both
+// paths give the reference's bits exactly.
+//
+// Results are identical to the whole-chain kernel by construction
+// (tests/test_segment_gpu.py checks them against the oracle).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -38,16 +51,18 @@
 #include "mcb_solo.cuh"
 
 #define SEG_MAX_E 16
+#define SEG_DEFAULT_NW 64
 
 bool seg_eligible(const ReplayParams &p) {
-    return p.seg.n_seg > 1 && p.tr.uniform && p.tr.E <= SEG_MAX_E && p.outcomes == nullptr && p.window >= 0 &&
-           p.window <= SOLO_WMAX && p.tr.total_acc < (1ll << 27) && p.tr.T * p.tr.K < (1ll << 27);
+    return p.seg.n_seg > 1 && p.tr.uniform && p.tr.E <= SEG_MAX_E && p.tr.K + 1 <= MCB_SEG_BINS &&
+           p.outcomes == nullptr && p.window >= 0 && p.window <= SOLO_WMAX && p.tr.total_acc < (1ll << 27) &&
+           p.tr.T * p.tr.K < (1ll << 27);
 }
 
 int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se) {
-    // enough (instance, segment) threads to fill every SM several times over,
-    // segments long enough that the fix-up walk stays a small fraction
-    const int64_t target_threads = 148ll * 768;
+    // enough (instance, segment) threads to fill every SM several times over;
+    // segments at least 2 warm-ups long so the warm-up stays a minor cost
+    const int64_t target_threads = 148ll * 1024;
     int64_t se;
     if (override_se > 0) {
         se = override_se;
@@ -55,62 +70,82 @@ int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se
         const int64_t n_seg = n_inst_launch > 0 ? target_threads / n_inst_launch : 1;
         if (n_seg <= 2) return 0;
         se = (T + n_seg - 1) / n_seg;
-        if (se < 64) se = 64;
+        if (se < 2 * SEG_DEFAULT_NW) se = 2 * SEG_DEFAULT_NW;
     }
-    se = (se + 15) / 16 * 16;
+    se = (se + MCB_SNAP_EV - 1) / MCB_SNAP_EV * MCB_SNAP_EV;
     if (se >= T) return 0;
     return (int)se;
 }
 
-size_t seg_snap_bytes(int64_t n_chains, int n_seg) { return (size_t)n_chains * n_seg * SEG_MAX_E * sizeof(int2); }
+int seg_warmup_events(int se) {
+    int nw = SEG_DEFAULT_NW < se ? SEG_DEFAULT_NW : se;
+    return nw / MCB_SNAP_EV * MCB_SNAP_EV;
+}
+
+size_t seg_snap_bytes(int64_t n_chains, int n_snap) { return (size_t)n_chains * n_snap * SEG_MAX_E * sizeof(int2); }
 size_t seg_out_bytes(int64_t n_inst, int n_seg) { return (size_t)n_inst * n_seg * sizeof(SegOut); }
 size_t seg_codes_bytes(int64_t n_inst, int64_t Tpad) { return (size_t)n_inst * Tpad + 64; }
 
 // ---------------------------------------------------------------- snapshot --
+// one thread per (chain, block of MCB_SNAP_EV events): last position / count
 __global__ void __launch_bounds__(128) k_seg_summary(const __grid_constant__ ReplayParams P) {
-    __shared__ int32_t s_cnt[128][SEG_MAX_E + 1];
-    __shared__ int32_t s_last[128][SEG_MAX_E + 1];
+    __shared__ int32_t s_cnt[SEG_MAX_E][128];
+    __shared__ int32_t s_last[SEG_MAX_E][128];
     const DevTrace &tr = P.tr;
-    const int n_seg = P.seg.n_seg, SE = P.seg.SE;
+    const int n_snap = P.seg.n_snap;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= tr.n_chains * n_seg) return;
-    const int64_t chain = t / n_seg;
-    const int seg = (int)(t % n_seg);
-    int32_t *cnt = s_cnt[threadIdx.x], *last = s_last[threadIdx.x];
-    for (int e = 0; e < SEG_MAX_E; ++e) { cnt[e] = 0; last[e] = -1; }
+    if (t >= tr.n_chains * n_snap) return;
+    const int64_t chain = t / n_snap;
+    const int b = (int)(t % n_snap);
+    const int tid = threadIdx.x;
+    for (int e = 0; e < SEG_MAX_E; ++e) { s_cnt[e][tid] = 0; s_last[e][tid] = -1; }
     const int K = tr.K;
     const int64_t a0 = tr.acc_begin(chain);
-    const int64_t p0 = (int64_t)seg * SE * K;
-    const int64_t p1 = min((int64_t)(seg + 1) * SE, tr.T) * K;
+    const int64_t p0 = (int64_t)b * MCB_SNAP_EV * K;
+    const int64_t p1 = min((int64_t)(b + 1) * MCB_SNAP_EV, tr.T) * K;
     IdReader ids;
     ids.init(tr.acc, a0 + p0, a0 + p1);
     for (int64_t p = p0; p < p1; ++p) {
         const uint32_t x = ids.get(a0 + p);
-        cnt[x] += 1;
-        last[x] = (int32_t)p;
+        s_cnt[x][tid] += 1;
+        s_last[x][tid] = (int32_t)p;
     }
     int2 *o = P.seg.summ + t * SEG_MAX_E;
-    for (int e = 0; e < SEG_MAX_E; ++e) o[e] = make_int2(last[e], cnt[e]);
+    for (int e = 0; e < SEG_MAX_E; ++e) o[e] = make_int2(s_last[e][tid], s_cnt[e][tid]);
 }
 
+// one thread per (chain, expert): exclusive scan over the chain's blocks
 __global__ void k_seg_scan(const __grid_constant__ ReplayParams P) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= P.tr.n_chains * SEG_MAX_E) return;
     const int64_t chain = t / SEG_MAX_E;
     const int e = (int)(t % SEG_MAX_E);
-    const int n_seg = P.seg.n_seg;
+    const int n = P.seg.n_snap;
+    const int2 *in = P.seg.summ + chain * n * SEG_MAX_E + e;
+    int2 *out = P.seg.snap + chain * n * SEG_MAX_E + e;
     int32_t last = -1, cnt = 0;
-    for (int seg = 0; seg < n_seg; ++seg) {
-        const int64_t i = (chain * n_seg + seg) * SEG_MAX_E + e;
-        const int2 s = P.seg.summ[i];
-        P.seg.snap[i] = make_int2(last, cnt);
+    int b = 0;
+    for (; b + 8 <= n; b += 8) {
+        int2 s[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s[i] = __ldg(in + (int64_t)(b + i) * SEG_MAX_E);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            out[(int64_t)(b + i) * SEG_MAX_E] = make_int2(last, cnt);
+            if (s[i].x >= 0) last = s[i].x;
+            cnt += s[i].y;
+        }
+    }
+    for (; b < n; ++b) {
+        const int2 s = __ldg(in + (int64_t)b * SEG_MAX_E);
+        out[(int64_t)b * SEG_MAX_E] = make_int2(last, cnt);
         if (s.x >= 0) last = s.x;
         cnt += s.y;
     }
 }
 
 int launch_seg_snapshot(const ReplayParams &p, cudaStream_t s) {
-    const int64_t n = p.tr.n_chains * p.seg.n_seg;
+    const int64_t n = p.tr.n_chains * p.seg.n_snap;
     k_seg_summary<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(p);
     const int64_t m = p.tr.n_chains * SEG_MAX_E;
     k_seg_scan<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(p);
@@ -118,23 +153,41 @@ int launch_seg_snapshot(const ReplayParams &p, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------ shared parts --
-// Exact policy keys at the start of segment `seg` of `chain` (all experts),
-// the seen mask, and the guessed resident set: the min(C, #seen) seen experts
-// with the LARGEST packed keys (the ones the policy would evict last).  For
-// LRU this is the true resident set (a stack algorithm over recency).
+template <int WMAX>
+__device__ __forceinline__ void pack_ring(const SState<WMAX> &S, uint32_t (&o)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        o[i] = (2 * i <= WMAX ? (S.ring[2 * i] & 0xFFFFu) : 0u) |
+               (2 * i + 1 <= WMAX ? (S.ring[2 * i + 1] << 16) : 0u);
+}
+
+template <int WMAX>
+__device__ __forceinline__ void unpack_state(SState<WMAX> &S, uint32_t res, const uint32_t *r, int W) {
+    S.res = res;
+    uint32_t o = 0u;
+#pragma unroll
+    for (int s = 0; s <= WMAX; ++s) {
+        S.ring[s] = (r[s >> 1] >> (16 * (s & 1))) & 0xFFFFu;
+        o |= (s <= W) ? S.ring[s] : 0u;
+    }
+    S.ring_or = o;
+}
+
+// Exact policy keys at event `ev` of `chain` (a snapshot point), the seen
+// mask, and the guessed resident set: the min(C, #seen) seen experts with the
+// LARGEST packed keys, i.e. the ones the policy would evict last.
 template <int EM, int POL>
-__device__ __forceinline__ void seg_start(const ReplayParams &P, int64_t chain, int seg, uint32_t C, int ml_variant,
-                                          uint32_t (&pk)[EM], uint32_t &seen, uint32_t &guess) {
+__device__ __forceinline__ void keys_at(const ReplayParams &P, int64_t chain, int64_t ev, uint32_t C, int ml_variant,
+                                        uint32_t (&pk)[EM], uint32_t &seen, uint32_t &guess) {
     constexpr int SH = Solo<EM>::SH;
     constexpr uint32_t KMAX = Solo<EM>::KMAX;
     const DevTrace &tr = P.tr;
     const int E = tr.E;
-    const int2 *sn = P.seg.snap + (chain * P.seg.n_seg + seg) * SEG_MAX_E;
+    const int2 *sn = P.seg.snap + (chain * P.seg.n_snap + ev / MCB_SNAP_EV) * SEG_MAX_E;
     const int64_t a0 = tr.acc_begin(chain);
-    const int64_t ev0 = (int64_t)seg * P.seg.SE;
     uint32_t rrow[EM];
     if (POL == POL_ML) {
-        if (ev0 > 0) load_rank_row<EM>(rrow, P.rank[ml_variant] + (tr.ev_begin(chain) + ev0 - 1) * E, E);
+        if (ev > 0) load_rank_row<EM>(rrow, P.rank[ml_variant] + (tr.ev_begin(chain) + ev - 1) * E, E);
         else
 #pragma unroll
             for (int s = 0; s < EM; ++s) rrow[s] = 0u;
@@ -142,7 +195,7 @@ __device__ __forceinline__ void seg_start(const ReplayParams &P, int64_t chain, 
     seen = 0u;
 #pragma unroll
     for (int s = 0; s < EM; ++s) {
-        const int2 v = s < E ? sn[s] : make_int2(-1, 0);
+        const int2 v = s < E ? __ldg(sn + s) : make_int2(-1, 0);
         seen |= (v.x >= 0 ? 1u : 0u) << s;
         uint32_t k = (uint32_t)s;
         if (POL == POL_LRU) k = v.x >= 0 ? (((uint32_t)v.x << SH) | (uint32_t)s) : (uint32_t)s;
@@ -168,40 +221,65 @@ __device__ __forceinline__ void seg_start(const ReplayParams &P, int64_t chain, 
 // ------------------------------------------------------------------- spec --
 template <int EM, int POL>
 __device__ __forceinline__ void seg_spec(const ReplayParams &P, int64_t chain, int seg, int pol_i, int cap_i,
-                                         int ml_variant) {
+                                         int ml_variant, uint16_t (*s_hist)[128], int pass) {
     constexpr int WMAX = SOLO_WMAX;
     const DevTrace &tr = P.tr;
     const int E = tr.E, K = tr.K, W = P.window;
+    const int tid = threadIdx.x;
     const uint32_t C = (uint32_t)P.cap[cap_i];
     const int64_t inst = (chain * P.n_pol + pol_i) * P.n_cap + cap_i;
     const int64_t ev0 = (int64_t)seg * P.seg.SE;
     const int64_t ev1 = min(ev0 + P.seg.SE, tr.T);
+    // pass 0: warm-up start (a snapshot point); pass 1: no warm-up
+    const int64_t ws = (pass == 0 && ev0 > P.seg.NW) ? ev0 - P.seg.NW : ev0;
     const int64_t a0 = tr.acc_begin(chain);
     const int64_t e0 = tr.ev_begin(chain);
     const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
 
     uint32_t pk[EM], seen, guess;
-    seg_start<EM, POL>(P, chain, seg, C, ml_variant, pk, seen, guess);
+    keys_at<EM, POL>(P, chain, ws, C, ml_variant, pk, seen, guess);
     SState<WMAX> S;
     sstate_clear(S);
     S.res = guess;
+    if (pass == 1 && seg > 0) {   // start from pass 0's end state of the previous segment
+        const SegOut &q = P.seg.out[0][inst * P.seg.n_seg + seg - 1];
+        uint32_t r[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) r[i] = q.ring_end[i];
+        unpack_state<WMAX>(S, q.res_end, r, W);
+    }
     uint32_t valid = (1u << E) - 1u, comp = 0;
     SCount n = {0u, 0u, 0u};
     bool stuck = false;
     int32_t stuck_ev = -1;
     uint64_t h = 0;
     const bool track = P.hashes != nullptr;
+    for (int b = 0; b <= K; ++b) s_hist[b][tid] = 0;
 
     IdReader ids;
-    ids.init(tr.acc, a0 + ev0 * K, a0 + ev1 * K);
+    ids.init(tr.acc, a0 + ws * K, a0 + ev1 * K);
     NextReader nx;
-    if (POL == POL_BELADY) nx.init(P.next_pos, a0 + ev0 * K, a0 + ev1 * K);
+    if (POL == POL_BELADY) nx.init(P.next_pos, a0 + ws * K, a0 + ev1 * K);
     uint32_t rrow[EM];
-    if (POL == POL_ML) load_rank_row<EM>(rrow, rank + (e0 + ev0) * E, E);
+    if (POL == POL_ML) load_rank_row<EM>(rrow, rank + (e0 + ws) * E, E);
     uint32_t *codes = (uint32_t *)(P.seg.codes + inst * P.seg.Tpad);
     uint32_t word = 0;
+    SegOut &o = P.seg.out[pass][inst * P.seg.n_seg + seg];
 
-    for (int64_t ev = ev0; ev < ev1; ++ev) {
+    for (int64_t ev = ws; ev < ev1; ++ev) {
+        if (ev == ev0) {   // end of the warm-up: the speculative start state
+            o.res_start = S.res;
+            uint32_t r[4];
+            pack_ring<WMAX>(S, r);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) o.ring_start[i] = r[i];
+            if (POL != POL_ML)
+#pragma unroll
+                for (int s = 0; s < 16; ++s) o.pk_start[s] = s < EM ? pk[s] : 0u;
+            n.misses = n.nev = n.refc = 0u;
+            comp = 0u;
+            stuck = false;
+        }
         if (POL == POL_ML) {
             solo_ml_keys<EM>(pk, valid, rrow);
             if (ev + 1 < ev1) load_rank_row<EM>(rrow, rank + (e0 + ev + 1) * E, E);
@@ -220,30 +298,37 @@ __device__ __forceinline__ void seg_spec(const ReplayParams &P, int64_t chain, i
             comp += (miss && !(seen & bit)) ? 1u : 0u;
             seen |= bit;
             pin |= bit;
-            if (track) h = poly16(h, code);
+            if (track && ev >= ev0) h = poly16(h, code);
         }
-        if (stuck && stuck_ev < 0) stuck_ev = (int32_t)ev;
-        word |= sm << (8 * (uint32_t)(ev & 3));
-        if ((ev & 3) == 3) { codes[ev >> 2] = word; word = 0; }
+        if (ev >= ev0) {
+            if (stuck && stuck_ev < 0) stuck_ev = (int32_t)ev;
+            s_hist[sm][tid] += 1;
+            word |= sm << (8 * (uint32_t)(ev & 3));
+            if ((ev & 3) == 3) { codes[ev >> 2] = word; word = 0; }
+        }
         sstate_next_decode<WMAX>(S, W);
     }
-    if (ev1 & 3) codes[ev1 >> 2] = word;   // tail word (segment ends mid-word only at the chain end)
+    if (ev1 & 3) codes[ev1 >> 2] = word;   // a segment ends mid-word only at the chain end
 
-    SegOut &o = P.seg.out[inst * P.seg.n_seg + seg];
     o.misses = n.misses;
     o.nev = n.nev;
     o.refc = n.refc;
     o.comp = comp;
-    o.res = S.res;
+    o.res_end = S.res;
     o.stuck_ev = stuck_ev;
     o.hash = h;
+    uint32_t r[4];
+    pack_ring<WMAX>(S, r);
 #pragma unroll
-    for (int s = 0; s <= WMAX; ++s) o.ring[s] = S.ring[s];
+    for (int i = 0; i < 4; ++i) o.ring_end[i] = r[i];
+    for (int b = 0; b < MCB_SEG_BINS; ++b) o.hist[b] = b <= K ? s_hist[b][tid] : (uint16_t)0;
 }
 
 template <int EM>
-__global__ void __launch_bounds__(128) k_seg_spec(const __grid_constant__ ReplayParams P) {
+__global__ void __launch_bounds__(128) k_seg_spec(const __grid_constant__ ReplayParams P, int pass) {
+    __shared__ uint16_t s_hist[MCB_SEG_BINS][128];
     const int pol_i = P.pol_map[blockIdx.y];
+    if (pass == 1 && P.pol[pol_i] == MCB_LRU) return;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int n_seg = P.seg.n_seg;
     if (t >= P.tr.n_chains * n_seg * P.n_cap) return;
@@ -252,42 +337,79 @@ __global__ void __launch_bounds__(128) k_seg_spec(const __grid_constant__ Replay
     const int seg = (int)(r % n_seg);
     const int64_t chain = r / n_seg;
     switch (P.pol[pol_i]) {
-        case MCB_LRU: seg_spec<EM, POL_LRU>(P, chain, seg, pol_i, cap_i, 0); break;
-        case MCB_LFU: seg_spec<EM, POL_LFU>(P, chain, seg, pol_i, cap_i, 0); break;
-        case MCB_BELADY: seg_spec<EM, POL_BELADY>(P, chain, seg, pol_i, cap_i, 0); break;
-        case MCB_ML: seg_spec<EM, POL_ML>(P, chain, seg, pol_i, cap_i, 0); break;
-        default: seg_spec<EM, POL_ML>(P, chain, seg, pol_i, cap_i, 1); break;
+        case MCB_LRU: seg_spec<EM, POL_LRU>(P, chain, seg, pol_i, cap_i, 0, s_hist, pass); break;
+        case MCB_LFU: seg_spec<EM, POL_LFU>(P, chain, seg, pol_i, cap_i, 0, s_hist, pass); break;
+        case MCB_BELADY: seg_spec<EM, POL_BELADY>(P, chain, seg, pol_i, cap_i, 0, s_hist, pass); break;
+        case MCB_ML: seg_spec<EM, POL_ML>(P, chain, seg, pol_i, cap_i, 0, s_hist, pass); break;
+        default: seg_spec<EM, POL_ML>(P, chain, seg, pol_i, cap_i, 1, s_hist, pass); break;
     }
 }
 
 // ----------------------------------------------------------------- finish --
-// float64 latency of events [ev, ev1) from the stored miss counts, in order
+// Exact fold of cnt[m] additions of lut[m] (any order within the run) onto S
+// when the running sum provably stays in S's binade and no addend is a
+// rounding tie there; false = use the sequential fold.
+__device__ __forceinline__ bool fold_hist_fast(double &S, const uint32_t *cnt, int nb, const double *lut) {
+    if (!(S > 0.0)) return false;
+    int ex;
+    frexp(S, &ex);                                             // S in [2^(ex-1), 2^ex), ulp 2^(ex-53)
+    const uint64_t two52 = 1ull << 52, two53 = 1ull << 53;
+    const uint64_t s_int = (uint64_t)scalbn(S, 53 - ex);       // in [2^52, 2^53)
+    uint64_t tot = 0;
+    for (int m = 0; m < nb; ++m) {
+        const uint64_t c = cnt[m];
+        if (!c) continue;
+        const double qf = scalbn(lut[m], 53 - ex);             // exact (power-of-two scaling)
+        if (!(qf < (double)two52)) return false;
+        const double fl = floor(qf);
+        const double fr = qf - fl;
+        if (fr == 0.5) return false;                           // tie: depends on the running sum's parity
+        const uint64_t q = (uint64_t)fl + (fr > 0.5 ? 1ull : 0ull);
+        if (__umul64hi(c, q)) return false;
+        const uint64_t p = c * q;
+        if (p >= two52) return false;
+        tot += p;
+        if (tot >= two52) return false;
+    }
+    if (s_int + tot >= two53) return false;                    // would reach the next binade
+    S = scalbn((double)(s_int + tot), ex - 53);
+    return true;
+}
+
+// sequential float64 fold of events [ev, ev1) from the stored miss counts
 __device__ __forceinline__ double fold_codes(double dlat, const uint8_t *codes, int64_t ev, int64_t ev1,
                                              const double *lut) {
     while (ev < ev1 && (ev & 15)) dlat = __dadd_rn(dlat, lut[__ldg(codes + ev++)]);
     const uint4 *v = (const uint4 *)(codes + ev);
     const int64_t nv = (ev1 - ev) >> 4;
-    uint4 cur = nv > 0 ? __ldg(v) : make_uint4(0, 0, 0, 0);
     for (int64_t i = 0; i < nv; ++i) {
-        const uint4 nxt = i + 1 < nv ? __ldg(v + i + 1) : make_uint4(0, 0, 0, 0);
+        const uint4 cur = __ldg(v + i);
         const uint32_t w[4] = {cur.x, cur.y, cur.z, cur.w};
+        double a[16];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) dlat = __dadd_rn(dlat, lut[(w[q] >> (8 * b)) & 0xFFu]);
-        cur = nxt;
+            for (int b = 0; b < 4; ++b) a[4 * q + b] = lut[(w[q] >> (8 * b)) & 0xFFu];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) dlat = __dadd_rn(dlat, a[q]);
     }
     ev += nv << 4;
     while (ev < ev1) dlat = __dadd_rn(dlat, lut[__ldg(codes + ev++)]);
     return dlat;
 }
 
+// word offsets in SegOut (192 bytes = 48 u32) of the fields the walk reads
+enum { SO_MISSES = 0, SO_NEV = 1, SO_REFC = 2, SO_COMP = 3, SO_RES_END = 4, SO_STUCK = 5, SO_RES_START = 6,
+       SO_HASH = 8, SO_RING_END = 10, SO_RING_START = 14, SO_PK = 18, SO_HIST = 34 };
+static_assert(sizeof(SegOut) == 192, "SegOut layout");
+
 template <int EM, int POL>
 __device__ __forceinline__ void seg_finish(const ReplayParams &P, int64_t chain, int pol_i, int cap_i, int ml_variant,
-                                           const double *lut) {
+                                           const double *lut, uint16_t (*s_hb)[32]) {
     constexpr int WMAX = SOLO_WMAX;
     const DevTrace &tr = P.tr;
     const int E = tr.E, K = tr.K, W = P.window;
+    const int lane = threadIdx.x & 31;
     const uint32_t C = (uint32_t)P.cap[cap_i];
     const int n_seg = P.seg.n_seg, SE = P.seg.SE;
     const int64_t inst = (chain * P.n_pol + pol_i) * P.n_cap + cap_i;
@@ -295,95 +417,141 @@ __device__ __forceinline__ void seg_finish(const ReplayParams &P, int64_t chain,
     const int64_t e0 = tr.ev_begin(chain);
     const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
     const uint8_t *codes = P.seg.codes + inst * P.seg.Tpad;
-    const SegOut *so = P.seg.out + inst * n_seg;
+    const SegOut *so = P.seg.out[POL == POL_LRU ? 0 : 1] + inst * n_seg;
     const bool track = P.hashes != nullptr;
-
-    // segment 0 starts from the true (empty) state: its speculative run is exact
-    SState<WMAX> A;
-    A.res = so[0].res;
-#pragma unroll
-    for (int s = 0; s <= WMAX; ++s) A.ring[s] = so[0].ring[s];
-    uint32_t misses = so[0].misses, nev = so[0].nev, refc = so[0].refc, comp = so[0].comp;
-    bool stuck = so[0].stuck_ev >= 0;
-    uint64_t h = so[0].hash;
-    double dlat = fold_codes(0.0, codes, 0, min((int64_t)SE, tr.T), lut);
     const uint64_t pow_full = track ? pow_mul((uint64_t)SE * K) : 0ull;
 
-    for (int seg = 1; seg < n_seg; ++seg) {
-        const int64_t ev0 = (int64_t)seg * SE;
-        const int64_t ev1 = min(ev0 + SE, tr.T);
-        {   // ring_or of the carried state
-            uint32_t o = 0u;
+    // Every lane of the warp walks the same instance redundantly (uniform
+    // control flow, no divergence); lane j prefetches the record of segment
+    // base + j so a batch of 32 records costs one memory round trip.
+    SState<WMAX> A;                    // the true state, carried across segments
+    sstate_clear(A);
+    uint32_t misses = 0, nev = 0, refc = 0, comp = 0, fix_events = 0, unconverged = 0, slow = 0;
+    bool stuck = false;
+    uint64_t h = 0;
+    double dlat = 0.0;
+
+    for (int base = 0; base < n_seg; base += 32) {
+        uint4 rv[8];
+        {
+            const int sj = base + lane;
+            const uint4 *rp = (const uint4 *)(so + (sj < n_seg ? sj : 0));
 #pragma unroll
-            for (int s = 0; s <= WMAX; ++s) o |= (s <= W) ? A.ring[s] : 0u;
-            A.ring_or = o;
+            for (int i = 0; i < 5; ++i) rv[i] = __ldg(rp + i);            // words 0..19
+#pragma unroll
+            for (int i = 0; i < 3; ++i) rv[5 + i] = __ldg(rp + 8 + i);    // words 32..43
         }
-        uint32_t pk[EM], seen, guess;
-        seg_start<EM, POL>(P, chain, seg, C, ml_variant, pk, seen, guess);
-        SState<WMAX> B;
-        sstate_clear(B);
-        B.res = guess;
-        SCount ca = {0u, 0u, 0u}, cb = {0u, 0u, 0u};
-        uint64_t ha = 0, hb = 0;
-        bool stuck_a = false, stuck_b = false;
-        uint32_t valid = (1u << E) - 1u;
-        int64_t ev = ev0;
-        bool conv = sstate_equal<WMAX>(A, B, W);
-        if (!conv) {
-            IdReader ids;
-            ids.init(tr.acc, a0 + ev0 * K, a0 + ev1 * K);
-            NextReader nx;
-            if (POL == POL_BELADY) nx.init(P.next_pos, a0 + ev0 * K, a0 + ev1 * K);
-            while (!conv && ev < ev1) {
-                if (POL == POL_ML) {
-                    uint32_t rrow[EM];
-                    load_rank_row<EM>(rrow, rank + (e0 + ev) * E, E);
-                    solo_ml_keys<EM>(pk, valid, rrow);
-                }
-                uint32_t pin = 0, sma = 0;
-                for (int j = 0; j < K; ++j) {
-                    const int64_t Aa = a0 + ev * K + j;
-                    const uint32_t x = ids.get(Aa);
-                    const uint32_t bit = 1u << x;
-                    const uint32_t np = (POL == POL_BELADY) ? nx.get(Aa) : 0u;
-                    solo_key_update<EM, POL>(pk, x, bit, (uint32_t)(ev * K + j), np);
-                    uint32_t ma, mb;
-                    const uint32_t codea = sstep<EM, WMAX>(A, pk, bit, pin, valid, C, ca, stuck_a, ma);
-                    const uint32_t codeb = sstep<EM, WMAX>(B, pk, bit, pin, valid, C, cb, stuck_b, mb);
-                    sma += ma;
-                    pin |= bit;
-                    if (track) { ha = poly16(ha, codea); hb = poly16(hb, codeb); }
-                }
-                dlat = __dadd_rn(dlat, lut[sma]);
-                sstate_next_decode<WMAX>(A, W);
-                sstate_next_decode<WMAX>(B, W);
-                ++ev;
-                conv = sstate_equal<WMAX>(A, B, W);
+        const int nb = min(32, n_seg - base);
+        for (int i = 0; i < nb; ++i) {
+            uint32_t wd[44];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                wd[4 * q + 0] = __shfl_sync(0xFFFFFFFFu, rv[q].x, i);
+                wd[4 * q + 1] = __shfl_sync(0xFFFFFFFFu, rv[q].y, i);
+                wd[4 * q + 2] = __shfl_sync(0xFFFFFFFFu, rv[q].z, i);
+                wd[4 * q + 3] = __shfl_sync(0xFFFFFFFFu, rv[q].w, i);
             }
-        }
-        const SegOut &o = so[seg];
-        uint64_t hseg;
-        if (conv) {
-            // from event ev on, the speculative run (which started from B's
-            // state) is the true run: splice it in, correcting the prefix
-            misses += ca.misses + o.misses - cb.misses;
-            nev += ca.nev + o.nev - cb.nev;
-            refc += ca.refc + o.refc - cb.refc;
-            stuck = stuck || stuck_a || (o.stuck_ev >= 0 && o.stuck_ev >= ev);
-            hseg = track ? o.hash + (ha - hb) * pow_mul((uint64_t)(ev1 - ev) * K) : 0ull;
-            A.res = o.res;
 #pragma unroll
-            for (int s = 0; s <= WMAX; ++s) A.ring[s] = o.ring[s];
-            dlat = fold_codes(dlat, codes, ev, ev1, lut);
-        } else {
-            misses += ca.misses;
-            nev += ca.nev;
-            refc += ca.refc;
-            stuck = stuck || stuck_a;
-            hseg = ha;
+            for (int q = 0; q < 3; ++q) {
+                wd[32 + 4 * q + 0] = __shfl_sync(0xFFFFFFFFu, rv[5 + q].x, i);
+                wd[32 + 4 * q + 1] = __shfl_sync(0xFFFFFFFFu, rv[5 + q].y, i);
+                wd[32 + 4 * q + 2] = __shfl_sync(0xFFFFFFFFu, rv[5 + q].z, i);
+                wd[32 + 4 * q + 3] = __shfl_sync(0xFFFFFFFFu, rv[5 + q].w, i);
+            }
+            const int seg = base + i;
+            const int64_t ev0 = (int64_t)seg * SE;
+            const int64_t ev1 = min(ev0 + (int64_t)SE, tr.T);
+            SState<WMAX> B;
+            unpack_state<WMAX>(B, wd[SO_RES_START], wd + SO_RING_START, W);
+            bool conv = sstate_equal<WMAX>(A, B, W);
+            int64_t ev = ev0;
+            SCount ca = {0u, 0u, 0u}, cb = {0u, 0u, 0u};
+            uint64_t ha = 0, hb = 0;
+            bool stuck_a = false, stuck_b = false;
+            if (!conv) {
+                // lockstep replay of the true state A and the speculative start B
+                for (int b = 0; b <= K; ++b) s_hb[b][lane] = 0;
+                uint32_t pk[EM];
+                if (POL != POL_ML)
+#pragma unroll
+                    for (int s = 0; s < EM; ++s) pk[s] = __ldg((const uint32_t *)(so + seg) + SO_PK + s);
+                uint32_t valid = (1u << E) - 1u;
+                IdReader ids;
+                ids.init(tr.acc, a0 + ev0 * K, a0 + ev1 * K);
+                NextReader nx;
+                if (POL == POL_BELADY) nx.init(P.next_pos, a0 + ev0 * K, a0 + ev1 * K);
+                while (!conv && ev < ev1) {
+                    if (POL == POL_ML) {
+                        uint32_t rrow[EM];
+                        load_rank_row<EM>(rrow, rank + (e0 + ev) * E, E);
+                        solo_ml_keys<EM>(pk, valid, rrow);
+                    }
+                    uint32_t pin = 0, sma = 0, smb = 0;
+                    for (int j = 0; j < K; ++j) {
+                        const int64_t Aa = a0 + ev * K + j;
+                        const uint32_t x = ids.get(Aa);
+                        const uint32_t bit = 1u << x;
+                        const uint32_t np = (POL == POL_BELADY) ? nx.get(Aa) : 0u;
+                        solo_key_update<EM, POL>(pk, x, bit, (uint32_t)(ev * K + j), np);
+                        uint32_t ma, mb;
+                        const uint32_t codea = sstep<EM, WMAX>(A, pk, bit, pin, valid, C, ca, stuck_a, ma);
+                        const uint32_t codeb = sstep<EM, WMAX>(B, pk, bit, pin, valid, C, cb, stuck_b, mb);
+                        sma += ma;
+                        smb += mb;
+                        pin |= bit;
+                        if (track) { ha = poly16(ha, codea); hb = poly16(hb, codeb); }
+                    }
+                    dlat = __dadd_rn(dlat, lut[sma]);
+                    s_hb[smb][lane] += 1;
+                    sstate_next_decode<WMAX>(A, W);
+                    sstate_next_decode<WMAX>(B, W);
+                    ++ev;
+                    conv = sstate_equal<WMAX>(A, B, W);
+                }
+                fix_events += (uint32_t)(ev - ev0);
+            }
+            uint64_t hseg;
+            if (conv) {
+                // from event ev on the speculative run (started from B) is the
+                // true run: splice it in, correcting for the prefix replayed above
+                misses += ca.misses + wd[SO_MISSES] - cb.misses;
+                nev += ca.nev + wd[SO_NEV] - cb.nev;
+                refc += ca.refc + wd[SO_REFC] - cb.refc;
+                const int32_t sev = (int32_t)wd[SO_STUCK];
+                stuck = stuck || stuck_a || (sev >= 0 && sev >= ev);
+                const uint64_t oh = (uint64_t)wd[SO_HASH] | ((uint64_t)wd[SO_HASH + 1] << 32);
+                hseg = track ? oh + (ha - hb) * pow_mul((uint64_t)(ev1 - ev) * K) : 0ull;
+                unpack_state<WMAX>(A, wd[SO_RES_END], wd + SO_RING_END, W);
+                // latency of the remaining events [ev, ev1): histogram minus B's prefix
+                uint32_t cnt[MCB_SEG_BINS];
+                const bool prefix = ev > ev0;
+#pragma unroll
+                for (int b = 0; b < MCB_SEG_BINS; ++b) {
+                    const uint32_t hv = (wd[SO_HIST + (b >> 1)] >> (16 * (b & 1))) & 0xFFFFu;
+                    cnt[b] = b <= K ? hv - (prefix ? (uint32_t)s_hb[b][lane] : 0u) : 0u;
+                }
+                if (!fold_hist_fast(dlat, cnt, K + 1, lut)) {
+                    dlat = fold_codes(dlat, codes, ev, ev1, lut);
+                    ++slow;
+                }
+            } else {
+                misses += ca.misses;
+                nev += ca.nev;
+                refc += ca.refc;
+                stuck = stuck || stuck_a;
+                hseg = ha;
+                ++unconverged;
+            }
+            comp += wd[SO_COMP];
+            if (track) h = h * (ev1 - ev0 == SE ? pow_full : pow_mul((uint64_t)(ev1 - ev0) * K)) + hseg;
         }
-        comp += o.comp;
-        if (track) h = h * (ev1 - ev0 == SE ? pow_full : pow_mul((uint64_t)(ev1 - ev0) * K)) + hseg;
+    }
+    if (lane != 0) return;
+    if (P.stats) {
+        atomicAdd(P.stats + 1, (unsigned long long)fix_events);
+        atomicAdd(P.stats + 2, (unsigned long long)unconverged);
+        atomicAdd(P.stats + 3, (unsigned long long)n_seg);
+        atomicAdd(P.stats + 4, (unsigned long long)slow);
     }
     const uint32_t total = (uint32_t)(tr.T * K);
     int64_t *out = P.inst_out + inst * MCB_R_N;
@@ -400,9 +568,11 @@ __device__ __forceinline__ void seg_finish(const ReplayParams &P, int64_t chain,
     if (track) P.hashes[inst] = h;
 }
 
+// one warp per instance (blockDim 32, blockIdx.x = instance of the policy blockIdx.y)
 template <int EM>
-__global__ void __launch_bounds__(128) k_seg_finish(const __grid_constant__ ReplayParams P) {
-    __shared__ double lut[SEG_MAX_E + 1];
+__global__ void __launch_bounds__(32) k_seg_finish(const __grid_constant__ ReplayParams P) {
+    __shared__ double lut[MCB_SEG_BINS];
+    __shared__ uint16_t s_hb[MCB_SEG_BINS][32];
     const int pol_i = P.pol_map[blockIdx.y];
     const int pol = P.pol[pol_i];
     const int K = P.tr.K;
@@ -413,33 +583,35 @@ __global__ void __launch_bounds__(128) k_seg_finish(const __grid_constant__ Repl
                                  : __dmul_rn((double)K, P.t_compute);
         lut[m] = __dadd_rn(lat, (pol == MCB_ML || pol == MCB_ML_NO_PREFILL) ? P.ml_cost : 0.0);
     }
-    __syncthreads();
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    __syncwarp();
+    const int64_t t = blockIdx.x;
     if (t >= P.tr.n_chains * P.n_cap) return;
     const int cap_i = (int)(t % P.n_cap);
     const int64_t chain = t / P.n_cap;
     switch (pol) {
-        case MCB_LRU: seg_finish<EM, POL_LRU>(P, chain, pol_i, cap_i, 0, lut); break;
-        case MCB_LFU: seg_finish<EM, POL_LFU>(P, chain, pol_i, cap_i, 0, lut); break;
-        case MCB_BELADY: seg_finish<EM, POL_BELADY>(P, chain, pol_i, cap_i, 0, lut); break;
-        case MCB_ML: seg_finish<EM, POL_ML>(P, chain, pol_i, cap_i, 0, lut); break;
-        default: seg_finish<EM, POL_ML>(P, chain, pol_i, cap_i, 1, lut); break;
+        case MCB_LRU: seg_finish<EM, POL_LRU>(P, chain, pol_i, cap_i, 0, lut, s_hb); break;
+        case MCB_LFU: seg_finish<EM, POL_LFU>(P, chain, pol_i, cap_i, 0, lut, s_hb); break;
+        case MCB_BELADY: seg_finish<EM, POL_BELADY>(P, chain, pol_i, cap_i, 0, lut, s_hb); break;
+        case MCB_ML: seg_finish<EM, POL_ML>(P, chain, pol_i, cap_i, 0, lut, s_hb); break;
+        default: seg_finish<EM, POL_ML>(P, chain, pol_i, cap_i, 1, lut, s_hb); break;
     }
 }
 
 template <int EM>
 static void launch_seg_t(const ReplayParams &p, cudaStream_t s) {
     const int64_t n_spec = p.tr.n_chains * p.seg.n_seg * p.n_cap;
-    k_seg_spec<EM><<<dim3((unsigned)((n_spec + 127) / 128), (unsigned)p.n_pol_launch), 128, 0, s>>>(p);
+    const dim3 g((unsigned)((n_spec + 127) / 128), (unsigned)p.n_pol_launch);
+    k_seg_spec<EM><<<g, 128, 0, s>>>(p, 0);
+    k_seg_spec<EM><<<g, 128, 0, s>>>(p, 1);
     const int64_t n_fin = p.tr.n_chains * p.n_cap;
-    k_seg_finish<EM><<<dim3((unsigned)((n_fin + 127) / 128), (unsigned)p.n_pol_launch), 128, 0, s>>>(p);
+    k_seg_finish<EM><<<dim3((unsigned)n_fin, (unsigned)p.n_pol_launch), 32, 0, s>>>(p);
 }
 
 int launch_replay_segmented(const ReplayParams &p, cudaStream_t s) {
     if (p.tr.n_chains * p.n_pol_launch * p.n_cap == 0) return 0;
     if (p.tr.E <= 8) launch_seg_t<8>(p, s);
     else launch_seg_t<16>(p, s);
-    return 2;
+    return 3;
 }
 
 int preload_segment_kernels() {
