@@ -292,6 +292,7 @@ def main():
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    dev_stats = _lib.read_stats(local)   # last step: [uncertain scorer events, seg fix-up events, ...]
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = float(sum(step_ms))
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -395,6 +396,9 @@ def main():
             "e2e": e2e,
             "clocks": clk,
             "gpu_launches": launches,
+            "scorer_uncertain_events": dev_stats[0],
+            "segmented_replay": {"fixup_events": dev_stats[1], "unconverged_segments": dev_stats[2],
+                                 "segments": dev_stats[3], "slow_latency_folds": dev_stats[4]},
             "generator": gen_report,
             "hit_rates": hit_rates,
         }

@@ -511,7 +511,7 @@ extern "C" int mcb_replay_host(mcb_ctx *c, const mcb_trace *t, const int32_t *po
     const mcb_nets *np = nullptr;
     if (nets && nets->params) {
         dn = *nets;
-        const size_t cnt = prepared_net_doubles(nets->num_experts, nets->hidden) * (size_t)nets->num_nets;
+        const size_t cnt = net_param_doubles(nets->num_experts, nets->hidden) * (size_t)nets->num_nets;
         if (int rc = upload(c->h_params, nets->params, cnt, 0, s, &dn.params)) return rc;
         np = &dn;
     }

@@ -101,6 +101,7 @@ int preload_segment_kernels();
 int launch_fold(const ReplayParams &p, int num_traces, int64_t *reports, double *latency, cudaStream_t s);
 int launch_prepare_nets(const double *params, int E, int H, int num_nets, double *wt, cudaStream_t s);
 __host__ __device__ size_t prepared_net_doubles(int E, int H);
+__host__ __device__ size_t net_param_doubles(int E, int H);
 // K3: snapshot scan + tile scorer. snaps scratch: n_tiles_total * (2E+1) int32; tile_off: n_chains+1 int64
 int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill,
                  uint8_t *ranks, double *scores, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,

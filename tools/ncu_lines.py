@@ -1,0 +1,48 @@
+"""Per-source-line instruction / stall breakdown of an .ncu-rep (sass joined to cuda lines)."""
+import collections
+import csv
+import subprocess
+import sys
+
+rep = sys.argv[1]
+top = int(sys.argv[2]) if len(sys.argv) > 2 else 15
+a = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                   capture_output=True, text=True).stdout.splitlines()
+b = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                   capture_output=True, text=True).stdout.splitlines()
+addr2line, cur, curfile = {}, None, None
+for r in csv.reader(a):
+    if r and r[0] == "File Path":
+        curfile = r[1].split("/")[-1]
+    elif len(r) >= 4 and r[0] and r[0] not in ("Line No", "Function Name"):
+        cur = (curfile, int(r[0]), r[1].strip()[:80])
+    elif len(r) >= 4 and r[2].startswith("0x"):
+        addr2line[r[2]] = cur
+rows = list(csv.reader(b))
+h = rows[1]
+ia, ie, iw = h.index("Address"), h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)")
+L, W, ops = collections.Counter(), collections.Counter(), collections.Counter()
+tot = tw = 0
+for r in rows[2:]:
+    if len(r) <= ie:
+        continue
+    try:
+        n, w = int(r[ie]), int(r[iw])
+    except ValueError:
+        continue
+    k = addr2line.get(r[ia])
+    L[k] += n
+    W[k] += w
+    tot += n
+    tw += w
+    t = r[h.index("Source")].split()
+    op = (t[1] if t and t[0].startswith("@") else (t[0] if t else "")).split(".")[0]
+    ops[op] += n
+print(f"total warp instructions {tot}")
+print("ops:", ", ".join(f"{o} {n / tot * 100:.1f}%" for o, n in ops.most_common(12)))
+print("-- by instructions")
+for k, n in L.most_common(top):
+    print(f"{n / tot * 100:5.1f}% inst {W[k] / tw * 100:5.1f}% stall  {k}")
+print("-- by stall samples")
+for k, n in W.most_common(top):
+    print(f"{L[k] / tot * 100:5.1f}% inst {n / tw * 100:5.1f}% stall  {k}")
