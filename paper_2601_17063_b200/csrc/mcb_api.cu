@@ -86,7 +86,7 @@ struct mcb_ctx {
     cudaEvent_t fork = nullptr, join = nullptr;
     int64_t solo_min_instances = 0;   // thread-per-instance whenever E <= 16 (MCB_SOLO_MIN overrides)
     int64_t seg_ev = 0;               // segmented replay: 0 auto, <0 off, >0 events per segment (MCB_SEG_EV)
-    DevBuf seg_snap, seg_summ, seg_out, seg_codes;
+    DevBuf seg_snap, seg_summ, seg_out, seg_codes, nu_scratch;
     cudaEvent_t ev[10] = {};          // start/stop per stage: K2, K3, K4 non-ML, K4 ML, K5
     bool ran[5] = {};
 };
@@ -172,7 +172,7 @@ extern "C" int mcb_ctx_destroy(mcb_ctx *c) {
                      &c->tile_off, &c->stats, &c->pol_caps, &c->h_acc, &c->h_acc_off, &c->h_ev_off,
                      &c->h_rt_off, &c->h_ev_info, &c->h_routed, &c->h_params, &c->h_reports, &c->h_latency,
                      &c->h_chain_reports, &c->h_hashes, &c->h_outcomes, &c->seg_snap, &c->seg_summ,
-                     &c->seg_out, &c->seg_codes};
+                     &c->seg_out, &c->seg_codes, &c->nu_scratch};
     for (DevBuf *b : all) b->release();
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->side) cudaStreamDestroy(c->side);
@@ -282,7 +282,10 @@ extern "C" int mcb_next_use(mcb_ctx *c, const mcb_trace *t, uint32_t *next_pos, 
     std::lock_guard<std::mutex> lk(c->mu);
     CUDA_TRY(cudaSetDevice(c->device));
     const DevTrace d = make_dev_trace(t);
-    launch_next_use(d, next_pos, (cudaStream_t)stream);
+    const size_t sw = next_use_scratch_words(d);
+    if (sw)
+        if (int rc = c->nu_scratch.ensure(sw * sizeof(uint32_t))) return rc;
+    launch_next_use(d, next_pos, sw ? (uint32_t *)c->nu_scratch.p : nullptr, (cudaStream_t)stream);
     CUDA_TRY(cudaGetLastError());
     return MCB_OK;
 }
@@ -417,11 +420,14 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
                 if (int rc = c->ranks[v].ensure((size_t)d.total_events * d.E + 64)) return rc;
         prepare_launch_attributes(d, nets->hidden);
     }
+    const size_t nu_sw = need_next ? next_use_scratch_words(d) : 0;
+    if (nu_sw)
+        if (int rc = c->nu_scratch.ensure(nu_sw * sizeof(uint32_t))) return rc;
     if (need_next) {
         if (int rc = c->next_pos.ensure((size_t)(d.total_acc + 64) * sizeof(uint32_t))) return rc;
         Pn.next_pos = Pm.next_pos = (const uint32_t *)c->next_pos.p;
         mark(c, 0, s);
-        launched += launch_next_use(d, (uint32_t *)c->next_pos.p, s);
+        launched += launch_next_use(d, (uint32_t *)c->next_pos.p, nu_sw ? (uint32_t *)c->nu_scratch.p : nullptr, s);
         mark(c, 1, s);
         c->ran[0] = true;
     }

@@ -10,6 +10,8 @@
 // policies.py:95-214, mlpolicy.py:15-62, features.py:34-52, net.py:43-105,
 // replay.py:44-89; normative restatement in SURVEY.md Appendix A.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <math.h>
 #include <stdint.h>
 
@@ -28,30 +30,47 @@
 // Integer only, so bit-exact with OracleIndex.next_use (policies.py:65-76):
 // next_use(e, p) = next_pos[p] - p, inf when next_pos == 0xFFFFFFFF.
 // ===========================================================================
-__global__ void __launch_bounds__(128) k_next_use(DevTrace tr, uint32_t *__restrict__ next_pos) {
+//
+// Long chains (few of them, e.g. one Mixtral trace: 32 chains of 131K
+// accesses) are cut into blocks so every SM has warps: pass 1 scans each
+// block backwards from an empty table and records the block's per-expert
+// first occurrence; a reverse scan over blocks turns those into "first
+// occurrence after block b"; pass 2 re-scans each block from that table and
+// writes the positions.  Same integer results as the single-block walk.
+// ===========================================================================
+template <bool WRITE>
+__global__ void __launch_bounds__(128) k_next_use(DevTrace tr, int64_t blk_acc, int64_t n_blk,
+                                                  const uint32_t *__restrict__ tab_in, uint32_t *__restrict__ tab_out,
+                                                  uint32_t *__restrict__ next_pos) {
     __shared__ uint32_t table[4][MCB_MAX_EXPERTS];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t c = (int64_t)blockIdx.x * 4 + w;
+    const int64_t id = (int64_t)blockIdx.x * 4 + w;
+    const int64_t c = id / n_blk, blk = id % n_blk;
     if (c >= tr.n_chains) return;
+    const int E = tr.E;
     uint32_t *tbl = table[w];
-    for (int e = lane; e < MCB_MAX_EXPERTS; e += 32) tbl[e] = MCB_NEXT_INF;
+    const uint32_t *tin = tab_in ? tab_in + id * E : nullptr;
+    for (int e = lane; e < MCB_MAX_EXPERTS; e += 32) tbl[e] = (tin && e < E) ? tin[e] : MCB_NEXT_INF;
     __syncwarp();
     const int64_t a0 = tr.acc_begin(c);
-    const int64_t n = tr.acc_end(c) - a0;
+    const int64_t n_chain = tr.acc_end(c) - a0;
+    const int64_t p0 = blk * blk_acc;                       // multiple of 32
+    const int64_t n = min(n_chain, p0 + blk_acc);           // block = [p0, n)
     const uint8_t *acc = tr.acc + a0;
     uint32_t *out = next_pos + a0;
-    int64_t nwin = (n + 31) >> 5;
+    const int64_t w0 = p0 >> 5;
+    const int64_t nwin = (n + 31) >> 5;
     // software pipeline: the load of window w-1 is in flight while w is processed
     uint32_t x_next = 0;
-    if (nwin > 0) {
+    if (nwin > w0) {
         const int64_t p = ((nwin - 1) << 5) + lane;
         x_next = p < n ? (uint32_t)__ldg(acc + p) : 256u + lane;
     }
-    for (int64_t win = nwin - 1; win >= 0; --win) {
+    for (int64_t win = nwin - 1; win >= w0; --win) {
         const int64_t p = (win << 5) + lane;
         const bool valid = p < n;
         const uint32_t x = x_next;
-        if (win > 0) x_next = (uint32_t)__ldg(acc + p - 32);
+        if (win > w0) x_next = (uint32_t)__ldg(acc + p - 32);
         const uint32_t m = __match_any_sync(FULL_MASK, x);
         const uint32_t higher = m & ~((2u << lane) - 1u);
         uint32_t r;
@@ -60,15 +79,63 @@ __global__ void __launch_bounds__(128) k_next_use(DevTrace tr, uint32_t *__restr
         __syncwarp();
         if (valid && (m & ((1u << lane) - 1u)) == 0u) tbl[x] = (uint32_t)p;
         __syncwarp();
-        if (valid) out[p] = r;
+        if (WRITE && valid) out[p] = r;
+    }
+    if (tab_out)
+        for (int e = lane; e < E; e += 32) tab_out[id * E + e] = tbl[e];
+}
+
+// firsts[c][b][e] (first occurrence in block b) -> after[c][b][e] (first
+// occurrence in any later block), one thread per (chain, expert)
+__global__ void k_next_use_blocks(int64_t n_chains, int E, int64_t n_blk, const uint32_t *__restrict__ firsts,
+                                  uint32_t *__restrict__ after) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_chains * E) return;
+    const int64_t c = t / E;
+    const int e = (int)(t % E);
+    uint32_t nf = MCB_NEXT_INF;
+    for (int64_t b = n_blk - 1; b >= 0; --b) {
+        const int64_t i = (c * n_blk + b) * E + e;
+        after[i] = nf;
+        const uint32_t f = firsts[i];
+        if (f != MCB_NEXT_INF) nf = f;
     }
 }
 
-int launch_next_use(const DevTrace &tr, uint32_t *next_pos, cudaStream_t s) {
+// blocks per chain for the blocked walk (1 = single walk per chain)
+int64_t next_use_blocks(const DevTrace &tr) {
+    if (!tr.uniform || tr.n_chains == 0) return 1;
+    const int64_t len = tr.T * tr.K;
+    const int64_t target_warps = 148ll * 16;
+    int64_t nb = (target_warps + tr.n_chains - 1) / tr.n_chains;
+    const int64_t cap = len / 2048;                        // blocks of at least 2048 accesses
+    if (nb > cap) nb = cap;
+    return nb > 1 ? nb : 1;
+}
+
+size_t next_use_scratch_words(const DevTrace &tr) {
+    const int64_t nb = next_use_blocks(tr);
+    return nb > 1 ? (size_t)(2 * tr.n_chains * nb * tr.E) : 0;
+}
+
+int launch_next_use(const DevTrace &tr, uint32_t *next_pos, uint32_t *scratch, cudaStream_t s) {
     if (tr.n_chains == 0) return 0;
-    const int64_t blocks = (tr.n_chains + 3) / 4;
-    k_next_use<<<(unsigned)blocks, 128, 0, s>>>(tr, next_pos);
-    return 1;
+    const int64_t nb = scratch ? next_use_blocks(tr) : 1;
+    if (nb <= 1) {
+        const int64_t blocks = (tr.n_chains + 3) / 4;
+        k_next_use<true><<<(unsigned)blocks, 128, 0, s>>>(tr, (int64_t)1 << 40, 1, nullptr, nullptr, next_pos);
+        return 1;
+    }
+    const int64_t len = tr.T * tr.K;
+    const int64_t blk_acc = ((len + nb - 1) / nb + 31) / 32 * 32;
+    const int64_t n_blk = (len + blk_acc - 1) / blk_acc;
+    uint32_t *firsts = scratch, *after = scratch + tr.n_chains * n_blk * tr.E;
+    const unsigned g = (unsigned)((tr.n_chains * n_blk + 3) / 4);
+    k_next_use<false><<<g, 128, 0, s>>>(tr, blk_acc, n_blk, nullptr, firsts, next_pos);
+    k_next_use_blocks<<<(unsigned)((tr.n_chains * tr.E + 127) / 128), 128, 0, s>>>(tr.n_chains, tr.E, n_blk, firsts,
+                                                                                     after);
+    k_next_use<true><<<g, 128, 0, s>>>(tr, blk_acc, n_blk, after, nullptr, next_pos);
+    return 3;
 }
 
 // ===========================================================================
@@ -681,7 +748,7 @@ __global__ void __launch_bounds__(128) k_feat_snap(DevTrace tr, int include_pref
 // degree-6 Taylor polynomial (truncation < 2^-58).  x < -708 flushes to 0 (the
 // logistic of such an input is below 1e-307; its SiLU contribution vanishes).
 // Within a few ulp of the correctly rounded exp.
-__constant__ double c_exp2_32[32] = {
+__device__ double g_exp2_32[32] = {
     1.0, 1.0218971486541166, 1.0442737824274138, 1.0671404006768237, 1.0905077326652577, 1.1143867425958924,
     1.1387886347566916, 1.1637248587775775, 1.189207115002721, 1.215247359980469, 1.241857812073484,
     1.2690509571917332, 1.2968395546510096, 1.3252366431597413, 1.3542555469368927, 1.383909881963832,
@@ -777,28 +844,41 @@ __global__ void __launch_bounds__(128) k_snap_scan(DevTrace tr, const int32_t *_
     const int64_t tpc = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
     int32_t last[4] = {-1, -1, -1, -1}, f[4] = {0, 0, 0, 0};
     int32_t u = 0;
-    for (int64_t t = 0; t < tpc; ++t) {
-        const int64_t tile = c * tpc + t;
-        int32_t *sp = snaps + tile * SN;
-        const int32_t *sm = summ + tile * 2 * E;
-        int32_t sc[4], sl[4];
+    constexpr int B = 8;   // tiles whose summaries are loaded together (loads off the carried chain)
+    for (int64_t t0 = 0; t0 < tpc; t0 += B) {
+        int32_t sc[B][4], sl[B][4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int e = lane + 32 * j;
-            sc[j] = e < E ? __ldg(sm + e) : 0;
-            sl[j] = e < E ? __ldg(sm + E + e) : 0;
-            if (e < E) { sp[e] = last[j]; sp[E + e] = f[j]; }
-        }
-        if (lane == 0) {
-            const int64_t rt = t * MCB_TILE_EV * (int64_t)tr.K;
-            sp[2 * E] = u; sp[2 * E + 1] = (int32_t)(rt & 0xFFFFFFFF); sp[2 * E + 2] = (int32_t)(rt >> 32);
+        for (int b = 0; b < B; ++b) {
+            const int32_t *sm = summ + (c * tpc + t0 + b) * 2 * E;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int e = lane + 32 * j;
+                const bool ok = t0 + b < tpc && e < E;
+                sc[b][j] = ok ? __ldg(sm + e) : 0;
+                sl[b][j] = ok ? __ldg(sm + E + e) : 0;
+            }
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            f[j] += sc[j];
-            if (sl[j] > 0) last[j] = u + sl[j];
+        for (int b = 0; b < B; ++b) {
+            const int64_t t = t0 + b;
+            if (t >= tpc) break;
+            int32_t *sp = snaps + (c * tpc + t) * SN;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int e = lane + 32 * j;
+                if (e < E) { sp[e] = last[j]; sp[E + e] = f[j]; }
+            }
+            if (lane == 0) {
+                const int64_t rt = t * MCB_TILE_EV * (int64_t)tr.K;
+                sp[2 * E] = u; sp[2 * E + 1] = (int32_t)(rt & 0xFFFFFFFF); sp[2 * E + 2] = (int32_t)(rt >> 32);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                f[j] += sc[b][j];
+                if (sl[b][j] > 0) last[j] = u + sl[b][j];
+            }
+            u += (int32_t)min((int64_t)MCB_TILE_EV, tr.T - t * MCB_TILE_EV);
         }
-        u += (int32_t)min((int64_t)MCB_TILE_EV, tr.T - t * MCB_TILE_EV);
     }
 }
 
@@ -944,9 +1024,10 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
     int32_t *s_flag = (int32_t *)(s_rank + MCB_TILE_EV * MCB_MAX_EXPERTS);  // [TILE]
 
     __shared__ double s_exp2[32];
-    if (threadIdx.x < 32) s_exp2[threadIdx.x] = c_exp2_32[threadIdx.x];   // visible after the first barrier
-    int64_t tile = blockIdx.x;
-    if (tile >= n_tiles) return;
+    if (threadIdx.x < 32) s_exp2[threadIdx.x] = g_exp2_32[threadIdx.x];   // visible after the first barrier
+    // persistent: each CTA walks tiles blockIdx.x, blockIdx.x + gridDim.x, ...
+    for (int64_t tile_it = blockIdx.x; tile_it < n_tiles; tile_it += gridDim.x) {
+    int64_t tile = tile_it;
     int64_t c, tile_in_chain;
     if (tr.uniform) {
         const int64_t tpc = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
@@ -954,7 +1035,7 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
         tile_in_chain = tile / tr.n_chains;
         tile = c * tpc + tile_in_chain;
     } else {
-        if (tile >= tile_off[tr.n_chains]) return;  // grid is an upper bound in general mode
+        if (tile >= tile_off[tr.n_chains]) break;   // n_tiles is an upper bound in general mode
         int64_t lo = 0, hi = tr.n_chains;          // largest c with tile_off[c] <= tile
         while (hi - lo > 1) {
             const int64_t mid = (lo + hi) / 2;
@@ -1119,6 +1200,8 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
         for (int i = 0; i < nev; ++i) cnt += s_flag[i];
         if (cnt) atomicAdd(uncertain, cnt);
     }
+    __syncthreads();   // shared buffers are reused by the next tile
+    }
 }
 
 static size_t score_smem(int E, int H) {
@@ -1168,8 +1251,14 @@ int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int 
     }
     const size_t smem = score_smem(tr.E, H);
     if (max_tiles > 0) {
-        score_kernel(tr.E, H)<<<(unsigned)max_tiles, 256, smem, s>>>(tr, wt, H, num_nets, include_prefill, tile_off,
-                                                                     snaps, max_tiles, ranks, scores, uncertain);
+        const score_fn fn = score_kernel(tr.E, H);
+        int dev = 0, n_sm = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)fn, 256, smem);
+        const int64_t grid = std::min<int64_t>(max_tiles, (int64_t)n_sm * (per_sm > 0 ? per_sm : 1));
+        fn<<<(unsigned)grid, 256, smem, s>>>(tr, wt, H, num_nets, include_prefill, tile_off, snaps, max_tiles, ranks,
+                                             scores, uncertain);
         ++launched;
     }
     return launched;
@@ -1181,7 +1270,8 @@ int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int 
 int preload_kernels() {
     cudaFuncAttributes a;
     const void *fns[] = {
-        (const void *)k_next_use, (const void *)k_fold, (const void *)k_prepare_nets, (const void *)k_tile_offsets,
+        (const void *)k_next_use<true>, (const void *)k_next_use<false>, (const void *)k_next_use_blocks,
+        (const void *)k_fold, (const void *)k_prepare_nets, (const void *)k_tile_offsets,
         (const void *)k_feat_snap, (const void *)k_tile_summary, (const void *)k_snap_scan,
         (const void *)k_score_tile<0, 0>, (const void *)k_score_tile<8, 128>, (const void *)k_score_tile<16, 128>,
         (const void *)k_score_tile<64, 128>, (const void *)k_score_tile<128, 128>,

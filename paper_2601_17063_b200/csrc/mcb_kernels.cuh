@@ -84,7 +84,8 @@ struct SegOut {
 };
 
 // launchers (mcb_kernels.cu); return the number of kernels launched or <0 on error
-int launch_next_use(const DevTrace &tr, uint32_t *next_pos, cudaStream_t s);
+int launch_next_use(const DevTrace &tr, uint32_t *next_pos, uint32_t *scratch, cudaStream_t s);
+size_t next_use_scratch_words(const DevTrace &tr);   // scratch for the blocked walk (0: not used)
 int launch_replay(const ReplayParams &p, cudaStream_t s);
 void prepare_launch_attributes(const DevTrace &tr, int H);
 int preload_kernels();   // force module loading + smem attributes (call at context creation)

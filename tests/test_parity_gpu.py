@@ -154,7 +154,8 @@ def test_eviction_records_match_reference():
 def test_next_use_kernel_matches_numpy():
     import torch
     rng = np.random.default_rng(0)
-    for E, n_chains, T, K in ((8, 5, 1000, 2), (128, 3, 777, 8), (64, 7, 33, 6)):
+    # the last two shapes run the blocked walk (several blocks per chain)
+    for E, n_chains, T, K in ((8, 5, 1000, 2), (64, 7, 33, 6), (128, 3, 777, 8), (8, 2, 40000, 2)):
         ids = np.stack([np.stack([rng.choice(E, K, replace=False) for _ in range(T)]) for _ in range(n_chains)])
         packed = mcb.packed_from_decode_ids(ids[None].astype(np.uint8), E)
         dev_acc = torch.from_numpy(packed.acc).cuda()
