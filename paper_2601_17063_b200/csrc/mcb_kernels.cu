@@ -835,50 +835,50 @@ __global__ void __launch_bounds__(128) k_tile_summary(DevTrace tr, int32_t *__re
     }
 }
 
+// One warp per (chain, expert): 32 tiles at a time, lane j = tile t0 + j,
+// warp-wide exclusive prefix sum of the routing counts and prefix max of the
+// last-routing update index (u at a tile start is t * TILE for decode-only
+// single-sequence chains), carried across chunks.
 __global__ void __launch_bounds__(128) k_snap_scan(DevTrace tr, const int32_t *__restrict__ summ,
                                                    int32_t *__restrict__ snaps) {
     const int lane = threadIdx.x & 31;
-    const int64_t c = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-    if (c >= tr.n_chains) return;
+    const int64_t wid = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
     const int E = tr.E, SN = 2 * E + 4;
+    const int64_t c = wid / E;
+    const int e = (int)(wid % E);
+    if (c >= tr.n_chains) return;
     const int64_t tpc = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
-    int32_t last[4] = {-1, -1, -1, -1}, f[4] = {0, 0, 0, 0};
-    int32_t u = 0;
-    constexpr int B = 8;   // tiles whose summaries are loaded together (loads off the carried chain)
-    for (int64_t t0 = 0; t0 < tpc; t0 += B) {
-        int32_t sc[B][4], sl[B][4];
+    int32_t carry_f = 0, carry_last = -1;
+    for (int64_t t0 = 0; t0 < tpc; t0 += 32) {
+        const int64_t t = t0 + lane;
+        const bool ok = t < tpc;
+        const int32_t *sm = summ + (c * tpc + (ok ? t : 0)) * 2 * E;
+        const int32_t cnt = ok ? __ldg(sm + e) : 0;
+        const int32_t l = ok ? __ldg(sm + E + e) : 0;
+        const int32_t la = l > 0 ? (int32_t)(t * MCB_TILE_EV) + l : -1;
+        int32_t incl_f = cnt, incl_l = la;
 #pragma unroll
-        for (int b = 0; b < B; ++b) {
-            const int32_t *sm = summ + (c * tpc + t0 + b) * 2 * E;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int e = lane + 32 * j;
-                const bool ok = t0 + b < tpc && e < E;
-                sc[b][j] = ok ? __ldg(sm + e) : 0;
-                sl[b][j] = ok ? __ldg(sm + E + e) : 0;
-            }
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t vf = __shfl_up_sync(FULL_MASK, incl_f, o);
+            const int32_t vl = __shfl_up_sync(FULL_MASK, incl_l, o);
+            if (lane >= o) { incl_f += vf; incl_l = max(incl_l, vl); }
         }
-#pragma unroll
-        for (int b = 0; b < B; ++b) {
-            const int64_t t = t0 + b;
-            if (t >= tpc) break;
+        const int32_t ex_f = __shfl_up_sync(FULL_MASK, incl_f, 1), ex_l = __shfl_up_sync(FULL_MASK, incl_l, 1);
+        const int32_t f_before = carry_f + (lane ? ex_f : 0);
+        const int32_t l_before = max(carry_last, lane ? ex_l : -1);
+        if (ok) {
             int32_t *sp = snaps + (c * tpc + t) * SN;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int e = lane + 32 * j;
-                if (e < E) { sp[e] = last[j]; sp[E + e] = f[j]; }
-            }
-            if (lane == 0) {
+            sp[e] = l_before;
+            sp[E + e] = f_before;
+            if (e == 0) {
                 const int64_t rt = t * MCB_TILE_EV * (int64_t)tr.K;
-                sp[2 * E] = u; sp[2 * E + 1] = (int32_t)(rt & 0xFFFFFFFF); sp[2 * E + 2] = (int32_t)(rt >> 32);
+                sp[2 * E] = (int32_t)(t * MCB_TILE_EV);
+                sp[2 * E + 1] = (int32_t)(rt & 0xFFFFFFFF);
+                sp[2 * E + 2] = (int32_t)(rt >> 32);
             }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                f[j] += sc[b][j];
-                if (sl[b][j] > 0) last[j] = u + sl[b][j];
-            }
-            u += (int32_t)min((int64_t)MCB_TILE_EV, tr.T - t * MCB_TILE_EV);
         }
+        carry_f += __shfl_sync(FULL_MASK, incl_f, 31);
+        carry_last = max(carry_last, __shfl_sync(FULL_MASK, incl_l, 31));
     }
 }
 
@@ -1242,7 +1242,7 @@ int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int 
         // snaps scratch holds [summaries | snapshots]
         int32_t *summ = snaps + max_tiles * (2 * tr.E + 4);
         k_tile_summary<<<(unsigned)((max_tiles + 3) / 4), 128, 0, s>>>(tr, summ);
-        k_snap_scan<<<(unsigned)((tr.n_chains + 3) / 4), 128, 0, s>>>(tr, summ, snaps);
+        k_snap_scan<<<(unsigned)((tr.n_chains * tr.E + 3) / 4), 128, 0, s>>>(tr, summ, snaps);
         launched += 2;
     } else {
         k_tile_offsets<<<1, 1024, 0, s>>>(tr, tile_off);

@@ -114,41 +114,39 @@ __global__ void __launch_bounds__(128) k_seg_summary(const __grid_constant__ Rep
     for (int e = 0; e < SEG_MAX_E; ++e) o[e] = make_int2(s_last[e][tid], s_cnt[e][tid]);
 }
 
-// one thread per (chain, expert): exclusive scan over the chain's blocks
-__global__ void k_seg_scan(const __grid_constant__ ReplayParams P) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= P.tr.n_chains * SEG_MAX_E) return;
-    const int64_t chain = t / SEG_MAX_E;
-    const int e = (int)(t % SEG_MAX_E);
+// one warp per (chain, expert): exclusive prefix (max of last position, sum
+// of counts) over the chain's blocks, 32 blocks per step, carried across steps
+__global__ void __launch_bounds__(128) k_seg_scan(const __grid_constant__ ReplayParams P) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int64_t chain = wid / SEG_MAX_E;
+    const int e = (int)(wid % SEG_MAX_E);
+    if (chain >= P.tr.n_chains) return;
     const int n = P.seg.n_snap;
     const int2 *in = P.seg.summ + chain * n * SEG_MAX_E + e;
     int2 *out = P.seg.snap + chain * n * SEG_MAX_E + e;
-    int32_t last = -1, cnt = 0;
-    int b = 0;
-    for (; b + 8 <= n; b += 8) {
-        int2 s[8];
+    int32_t carry_last = -1, carry_cnt = 0;
+    for (int b0 = 0; b0 < n; b0 += 32) {
+        const int b = b0 + lane;
+        const int2 v = b < n ? __ldg(in + (int64_t)b * SEG_MAX_E) : make_int2(-1, 0);
+        int32_t il = v.x, ic = v.y;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) s[i] = __ldg(in + (int64_t)(b + i) * SEG_MAX_E);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            out[(int64_t)(b + i) * SEG_MAX_E] = make_int2(last, cnt);
-            if (s[i].x >= 0) last = s[i].x;
-            cnt += s[i].y;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t tl = __shfl_up_sync(0xFFFFFFFFu, il, o), tc = __shfl_up_sync(0xFFFFFFFFu, ic, o);
+            if (lane >= o) { il = max(il, tl); ic += tc; }
         }
-    }
-    for (; b < n; ++b) {
-        const int2 s = __ldg(in + (int64_t)b * SEG_MAX_E);
-        out[(int64_t)b * SEG_MAX_E] = make_int2(last, cnt);
-        if (s.x >= 0) last = s.x;
-        cnt += s.y;
+        const int32_t el = __shfl_up_sync(0xFFFFFFFFu, il, 1), ec = __shfl_up_sync(0xFFFFFFFFu, ic, 1);
+        if (b < n) out[(int64_t)b * SEG_MAX_E] = make_int2(max(carry_last, lane ? el : -1), carry_cnt + (lane ? ec : 0));
+        carry_last = max(carry_last, __shfl_sync(0xFFFFFFFFu, il, 31));
+        carry_cnt += __shfl_sync(0xFFFFFFFFu, ic, 31);
     }
 }
 
 int launch_seg_snapshot(const ReplayParams &p, cudaStream_t s) {
     const int64_t n = p.tr.n_chains * p.seg.n_snap;
     k_seg_summary<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(p);
-    const int64_t m = p.tr.n_chains * SEG_MAX_E;
-    k_seg_scan<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(p);
+    const int64_t m = p.tr.n_chains * SEG_MAX_E;   // warps
+    k_seg_scan<<<(unsigned)((m + 3) / 4), 128, 0, s>>>(p);
     return 2;
 }
 

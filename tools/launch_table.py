@@ -6,8 +6,11 @@ import sys
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
 h = rows[0]
 ki, vi, gi, bi = h.index("Kernel Name"), h.index("Metric Value"), h.index("Grid Size"), h.index("Block Size")
+mi = h.index("Metric Name")
 agg = collections.defaultdict(lambda: [0, 0.0, ""])
 for r in rows[1:]:
+    if r[mi] != "gpu__time_duration.sum":
+        continue
     try:
         v = float(r[vi].replace(",", ""))
     except ValueError:
