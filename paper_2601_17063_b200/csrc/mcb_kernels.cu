@@ -885,7 +885,8 @@ __global__ void __launch_bounds__(128) k_snap_scan(DevTrace tr, const int32_t *_
 // fp64 tensor-core MLP layer (DMMA.8x8x4 via mma.sync m8n8k4 f64):
 //   O[i][n] = act(sum_k A[i][k] * Wt[k][n] + b[n]),  i < 32 events of the tile
 // A and O row-major in shared memory (leading dims = 4 mod 16 doubles, which
-// makes the 8x4 A-fragment loads bank-conflict free); Wt streamed from
+// makes the 8x4 A-fragment loads bank-conflict free; O may alias A: all warps
+// finish reading A before the epilogue writes); Wt streamed from
 // L1/L2.  Warp w owns n-tiles w, w+8, ... (NTW of them) x all four 8-row
 // m-tiles: per k-step 4 A + NTW B fragments feed 4*NTW DMMAs.  Fragments:
 // A(row=lane/4, k=lane%4), B(k=lane%4, col=lane/4), C(row=lane/4,
@@ -903,7 +904,7 @@ __device__ __forceinline__ void mma_layer(const double *A, int lda, int K, const
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, q = lane & 3;
     const int NT = N >> 3;
-    if (warp >= NT) return;
+    const bool idle = warp >= NT;
     double acc[4][NTW][2];
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt)
@@ -916,6 +917,7 @@ __device__ __forceinline__ void mma_layer(const double *A, int lda, int K, const
         have[j] = warp + 8 * j < NT;
         col[j] = (warp + 8 * j) * 8;
     }
+    if (!idle) {
     const double *arow = A + g * lda + q;
     const double *wcol = Wt + (int64_t)q * N + g;
     // fragments of k-step k0 + 4 are in flight while k-step k0 multiplies
@@ -941,6 +943,10 @@ __device__ __forceinline__ void mma_layer(const double *A, int lda, int K, const
 #pragma unroll
         for (int j = 0; j < NTW; ++j) b[j] = bn[j];
     }
+    }
+    // every warp has consumed A before anyone overwrites it (O may alias A)
+    __syncthreads();
+    if (idle) return;
 #pragma unroll
     for (int j = 0; j < NTW; ++j) {
         if (!have[j]) continue;
@@ -1008,7 +1014,7 @@ __host__ __device__ __forceinline__ int mlp_ld(int cols) { return (cols + 15) / 
 // mlpolicy.py:15-26).  argmax score with lowest-id ties == argmax rank with
 // lowest-id ties.
 template <int TE, int TH>   // (num_experts, hidden) specialisation, 0 = runtime
-__global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *__restrict__ wt_all, int H_rt,
+__global__ void __launch_bounds__(256, TE ? 4 : 1) k_score_tile(DevTrace tr, const double *__restrict__ wt_all, int H_rt,
                                                      int num_nets, int include_prefill,
                                                      const int64_t *__restrict__ tile_off,
                                                      const int32_t *__restrict__ snaps, int64_t n_tiles,
@@ -1017,9 +1023,9 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int E = TE ? TE : tr.E, D = 2 * E, H = TH ? TH : H_rt;
     const int Hp = mlp_hp(H), Kp1 = mlp_kp1(E), Ep = mlp_ep(E);
-    const int ldA = mlp_ld(Kp1 > Hp ? Kp1 : Hp), ldB = mlp_ld(Hp > Ep ? Hp : Ep);
-    double *bufA = (double *)smem_raw;                    // [TILE][ldA]: features, then h2
-    double *bufB = bufA + ldA * MCB_TILE_EV;              // [TILE][ldB]: h1, then scores
+    const int ldA = mlp_ld(Kp1 > Ep ? Kp1 : Ep), ldB = mlp_ld(Hp);
+    double *bufA = (double *)smem_raw;                    // [TILE][ldA]: features, then scores
+    double *bufB = bufA + ldA * MCB_TILE_EV;              // [TILE][ldB]: h1, then h2 (in place)
     uint8_t *s_rank = (uint8_t *)(bufB + ldB * MCB_TILE_EV);  // [TILE][E]
     int32_t *s_flag = (int32_t *)(s_rank + MCB_TILE_EV * MCB_MAX_EXPERTS);  // [TILE]
 
@@ -1165,23 +1171,23 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
                  *Wt3 = b2 + Hp, *b3 = Wt3 + (int64_t)Hp * Ep;
     mma_layer_any(bufA, ldA, Kp1, Wt1, b1, Hp, bufB, ldB, true, s_exp2);    // h1 -> B
     __syncthreads();
-    mma_layer_any(bufB, ldB, Hp, Wt2, b2, Hp, bufA, ldA, true, s_exp2);     // h2 -> A
+    mma_layer_any(bufB, ldB, Hp, Wt2, b2, Hp, bufB, ldB, true, s_exp2);     // h2 -> B (in place)
     __syncthreads();
-    mma_layer_any(bufA, ldA, Hp, Wt3, b3, Ep, bufB, ldB, false, s_exp2);    // scores -> B
+    mma_layer_any(bufB, ldB, Hp, Wt3, b3, Ep, bufA, ldA, false, s_exp2);    // scores -> A
     __syncthreads();
     for (int i = tid; i < MCB_TILE_EV; i += blockDim.x) s_flag[i] = 0;
     __syncthreads();
     for (int q = tid; q < MCB_TILE_EV * E; q += blockDim.x) {
         const int i = q % MCB_TILE_EV, e = q / MCB_TILE_EV;
         if (i >= nev) continue;
-        const double s = bufB[i * ldB + e];
+        const double s = bufA[i * ldA + e];
         uint32_t r = 0;
         bool near = false;
         if (s > -INFINITY) {
             r = 1;
 #pragma unroll 8
             for (int j = 0; j < E; ++j) {
-                const double sj = bufB[i * ldB + j];
+                const double sj = bufA[i * ldA + j];
                 if (sj > -INFINITY) {
                     if (sj < s) ++r;
                     if (sj != s && fabs(sj - s) <= 1e-12 * fmax(fabs(s), fabs(sj))) near = true;
@@ -1206,7 +1212,7 @@ __global__ void __launch_bounds__(256) k_score_tile(DevTrace tr, const double *_
 
 static size_t score_smem(int E, int H) {
     const int Hp = mlp_hp(H), Kp1 = mlp_kp1(E), Ep = mlp_ep(E);
-    const int ldA = mlp_ld(Kp1 > Hp ? Kp1 : Hp), ldB = mlp_ld(Hp > Ep ? Hp : Ep);
+    const int ldA = mlp_ld(Kp1 > Ep ? Kp1 : Ep), ldB = mlp_ld(Hp);
     return (size_t)MCB_TILE_EV * (ldA + ldB) * sizeof(double) + MCB_TILE_EV * MCB_MAX_EXPERTS +
            MCB_TILE_EV * sizeof(int32_t);
 }
