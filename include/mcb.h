@@ -176,6 +176,9 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
  * num_experts <= 16 (mcb_segment.cu): 0 = automatic (used when the instances
  * are too few to fill the GPU), < 0 = off, > 0 = events per segment. */
 #define MCB_TUNE_SEG_EV 1
+/* MCB_TUNE_SEG_NW: warm-up events replayed before each speculative segment
+ * (0 = automatic). */
+#define MCB_TUNE_SEG_NW 2
 int mcb_set_tuning(mcb_ctx *ctx, int32_t knob, int64_t value);
 int mcb_last_timings(mcb_ctx *ctx, float *ms, int32_t n);
 

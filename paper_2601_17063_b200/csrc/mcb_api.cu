@@ -6,6 +6,8 @@
 // the per-cell arithmetic is engine.run_simulation (engine.py:300-380).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -86,6 +88,7 @@ struct mcb_ctx {
     cudaEvent_t fork = nullptr, join = nullptr;
     int64_t solo_min_instances = 0;   // thread-per-instance whenever E <= 16 (MCB_SOLO_MIN overrides)
     int64_t seg_ev = 0;               // segmented replay: 0 auto, <0 off, >0 events per segment (MCB_SEG_EV)
+    int64_t seg_nw = 0;               // warm-up events before each segment: 0 auto (MCB_SEG_NW)
     DevBuf seg_snap, seg_summ, seg_out, seg_codes, nu_scratch;
     cudaEvent_t ev[10] = {};          // start/stop per stage: K2, K3, K4 non-ML, K4 ML, K5
     bool ran[5] = {};
@@ -117,6 +120,10 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
     }
     if (knob == MCB_TUNE_SEG_EV) {
         c->seg_ev = value;
+        return MCB_OK;
+    }
+    if (knob == MCB_TUNE_SEG_NW) {
+        c->seg_nw = value;
         return MCB_OK;
     }
     return mcb_set_error(MCB_ERR_INVALID, "unknown tuning knob");
@@ -152,15 +159,18 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     c->device = device;
     if (const char *env = getenv("MCB_SOLO_MIN")) c->solo_min_instances = atoll(env);
     if (const char *env = getenv("MCB_SEG_EV")) c->seg_ev = atoll(env);
+    if (const char *env = getenv("MCB_SEG_NW")) c->seg_nw = atoll(env);
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);   // replay warps dispatch ahead of K3 blocks
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+
         cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess) {
         delete c;
         return mcb_set_error(MCB_ERR_CUDA, "stream creation failed");
     }
+
     *out = c;
     return MCB_OK;
 }
@@ -176,6 +186,7 @@ extern "C" int mcb_ctx_destroy(mcb_ctx *c) {
     for (DevBuf *b : all) b->release();
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->side) cudaStreamDestroy(c->side);
+
     if (c->fork) cudaEventDestroy(c->fork);
     if (c->join) cudaEventDestroy(c->join);
     for (auto &e : c->ev)
@@ -254,14 +265,20 @@ static int ensure_score_buffers(mcb_ctx *c, const DevTrace &d, const mcb_nets *n
     return MCB_OK;
 }
 
-static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int include_prefill, uint8_t *ranks,
-                     double *scores, cudaStream_t s, int64_t *launched) {
-    const int E = d.E, H = nets->hidden;
-    if (nets->num_experts != E) return mcb_set_error(MCB_ERR_SHAPE, "net num_experts does not match the trace");
+static int check_nets(const DevTrace &d, const mcb_nets *nets) {
+    const int H = nets->hidden;
+    if (nets->num_experts != d.E) return mcb_set_error(MCB_ERR_SHAPE, "net num_experts does not match the trace");
     if (H < 1 || H > 256) return mcb_set_error(MCB_ERR_UNSUPPORTED, "net hidden size must be in [1, 256]");
     if (nets->num_nets != 1 && nets->num_nets != d.L)
         return mcb_set_error(MCB_ERR_INVALID, "num_nets must be 1 or num_layers");
     if (!nets->params) return mcb_set_error(MCB_ERR_INVALID, "nets.params is NULL");
+    return MCB_OK;
+}
+
+static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int include_prefill, uint8_t *ranks,
+                     double *scores, cudaStream_t s, int64_t *launched) {
+    const int E = d.E, H = nets->hidden;
+    if (int rc = check_nets(d, nets)) return rc;
     if (int rc = ensure_score_buffers(c, d, nets)) return rc;
     const size_t per = prepared_net_doubles(E, H);
     (void)per;
@@ -359,6 +376,8 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     P.window = cost->window;
     P.solo_min_instances = c->solo_min_instances;
     P.stats = (unsigned long long *)c->stats.p;
+    P.chain_lo = 0;
+    P.chain_hi = d.n_chains;
 
     // Orchestration.  K3 (ML scores) is only needed by ML instances, so when
     // both kinds are present the non-ML replay runs on a high-priority side
@@ -398,7 +417,7 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         if (se > 0 && seg_eligible(probe)) {
             P.seg.SE = se;
             P.seg.n_seg = (int)((d.T + se - 1) / se);
-            P.seg.NW = seg_warmup_events(se);
+            P.seg.NW = seg_warmup_events(se, c->seg_nw);
             P.seg.n_snap = (int)((d.T + MCB_SNAP_EV - 1) / MCB_SNAP_EV);
             P.seg.Tpad = (d.T + 15) / 16 * 16;
             if (int rc = c->seg_snap.ensure(seg_snap_bytes(d.n_chains, P.seg.n_snap))) return rc;
@@ -443,6 +462,10 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         c->ran[2] = true;
     }
     if (Pm.n_pol_launch > 0) {
+        // The ML replay needs K3's ranks; it follows K3 on the same stream.
+        // (Pipelining K3 chunks with per-chunk ML replays was measured slower:
+        // the replay's finish walk is latency-bound per instance, so every
+        // chunk pays it again.)
         mark(c, 2, s);
         for (int v = 0; v < 2; ++v) {
             if (!need_ml[v]) continue;
@@ -451,10 +474,10 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
             Pm.rank[v] = (const uint8_t *)c->ranks[v].p;
         }
         mark(c, 3, s);
-        c->ran[1] = true;
         mark(c, 6, s);
         launched += seg_eligible(Pm) ? launch_replay_segmented(Pm, s) : launch_replay(Pm, s);
         mark(c, 7, s);
+        c->ran[1] = true;
         c->ran[3] = true;
     }
     if (split) {

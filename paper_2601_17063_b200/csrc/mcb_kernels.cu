@@ -361,11 +361,11 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
 template <int G, int EPL, bool UNIFORM>
 __global__ void __launch_bounds__(128) k_replay(const __grid_constant__ ReplayParams P) {
     const int64_t li = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;   // instance of this launch
-    const int64_t n_inst = P.tr.n_chains * P.n_pol_launch * P.n_cap;
+    const int64_t n_inst = (P.chain_hi - P.chain_lo) * P.n_pol_launch * P.n_cap;
     if (li >= n_inst) return;
     const int cap_i = (int)(li % P.n_cap);
     const int pol_i = P.pol_map[(li / P.n_cap) % P.n_pol_launch];
-    const int64_t chain = li / ((int64_t)P.n_cap * P.n_pol_launch);
+    const int64_t chain = P.chain_lo + li / ((int64_t)P.n_cap * P.n_pol_launch);
     const int64_t inst = (chain * P.n_pol + pol_i) * P.n_cap + cap_i;
     switch (P.pol[pol_i]) {
         case MCB_LRU: replay_instance<G, EPL, POL_LRU, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
@@ -493,9 +493,9 @@ template <int EM, bool UNIFORM>
 __global__ void __launch_bounds__(128) k_replay_solo(const __grid_constant__ ReplayParams P) {
     const int pol_i = P.pol_map[blockIdx.y];
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= P.tr.n_chains * P.n_cap) return;
+    if (t >= (P.chain_hi - P.chain_lo) * P.n_cap) return;
     const int cap_i = (int)(t % P.n_cap);
-    const int64_t chain = t / P.n_cap;
+    const int64_t chain = P.chain_lo + t / P.n_cap;
     switch (P.pol[pol_i]) {
         case MCB_LRU: solo_instance<EM, POL_LRU, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
         case MCB_LFU: solo_instance<EM, POL_LFU, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(128) k_replay_solo(const __grid_constant__ Rep
 
 template <int EM>
 static void launch_solo_t(const ReplayParams &p, cudaStream_t s) {
-    const int64_t n = p.tr.n_chains * p.n_cap;
+    const int64_t n = (p.chain_hi - p.chain_lo) * p.n_cap;
     // Few instances (latency-bound chains, e.g. one Mixtral trace): one warp
     // per block, with a shared-memory reservation that keeps other kernels'
     // blocks (the concurrently running K3) off its SM, so each replay warp
@@ -529,7 +529,7 @@ static void launch_solo_t(const ReplayParams &p, cudaStream_t s) {
 
 template <int G, int EPL>
 static void launch_replay_t(const ReplayParams &p, cudaStream_t s) {
-    const int64_t n_inst = p.tr.n_chains * p.n_pol_launch * p.n_cap;
+    const int64_t n_inst = (p.chain_hi - p.chain_lo) * p.n_pol_launch * p.n_cap;
     const int per_block = 128 / G;
     const unsigned blocks = (unsigned)((n_inst + per_block - 1) / per_block);
     if (p.tr.uniform) k_replay<G, EPL, true><<<blocks, 128, 0, s>>>(p);
@@ -537,14 +537,14 @@ static void launch_replay_t(const ReplayParams &p, cudaStream_t s) {
 }
 
 int launch_replay(const ReplayParams &p, cudaStream_t s) {
-    if (p.tr.n_chains * p.n_pol_launch * p.n_cap == 0) return 0;
+    if ((p.chain_hi - p.chain_lo) * p.n_pol_launch * p.n_cap == 0) return 0;
     const int E = p.tr.E;
     // solo kernels pack (key << 3|4 | id) into 32 bits: chains must stay below 2^28 accesses.
     // Thread-per-instance only pays off when there are enough instances to
     // fill the machine; few long chains (e.g. one Mixtral trace) are
     // latency-bound, and a whole warp per instance has the shorter per-access
     // critical path (lane-parallel victim search, no divergence).
-    const int64_t n_inst = p.tr.n_chains * p.n_pol_launch * p.n_cap;
+    const int64_t n_inst = (p.chain_hi - p.chain_lo) * p.n_pol_launch * p.n_cap;
     const bool solo_ok = p.tr.total_acc < (1ll << 27) && n_inst >= p.solo_min_instances && p.window >= 0 &&
                          p.window <= SOLO_WMAX;
     if (E <= 8 && solo_ok) launch_solo_t<8>(p, s);
@@ -1017,7 +1017,8 @@ template <int TE, int TH>   // (num_experts, hidden) specialisation, 0 = runtime
 __global__ void __launch_bounds__(256, TE ? 4 : 1) k_score_tile(DevTrace tr, const double *__restrict__ wt_all, int H_rt,
                                                      int num_nets, int include_prefill,
                                                      const int64_t *__restrict__ tile_off,
-                                                     const int32_t *__restrict__ snaps, int64_t n_tiles,
+                                                     const int32_t *__restrict__ snaps, int64_t tile_lo,
+                                                     int64_t tile_hi,
                                                      uint8_t *__restrict__ ranks, double *__restrict__ scores,
                                                      unsigned long long *uncertain) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1032,14 +1033,16 @@ __global__ void __launch_bounds__(256, TE ? 4 : 1) k_score_tile(DevTrace tr, con
     __shared__ double s_exp2[32];
     if (threadIdx.x < 32) s_exp2[threadIdx.x] = g_exp2_32[threadIdx.x];   // visible after the first barrier
     // persistent: each CTA walks tiles blockIdx.x, blockIdx.x + gridDim.x, ...
-    for (int64_t tile_it = blockIdx.x; tile_it < n_tiles; tile_it += gridDim.x) {
+    for (int64_t tile_it = tile_lo + blockIdx.x; tile_it < tile_hi; tile_it += gridDim.x) {
     int64_t tile = tile_it;
     int64_t c, tile_in_chain;
     if (tr.uniform) {
+        // chain-major: the CTAs in flight (a window of consecutive tiles) work
+        // on the same chain, i.e. the same layer net, so its weights stay hot
+        // in L1 / L2 instead of every SM streaming several nets
         const int64_t tpc = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
-        c = tile % tr.n_chains;
-        tile_in_chain = tile / tr.n_chains;
-        tile = c * tpc + tile_in_chain;
+        c = tile / tpc;
+        tile_in_chain = tile % tpc;
     } else {
         if (tile >= tile_off[tr.n_chains]) break;   // n_tiles is an upper bound in general mode
         int64_t lo = 0, hi = tr.n_chains;          // largest c with tile_off[c] <= tile
@@ -1222,7 +1225,7 @@ static size_t score_smem(int E, int H) {
 // EvictionNet's default, net.py:64); anything else runs the runtime-shape
 // instantiation <0, 0>.
 typedef void (*score_fn)(DevTrace, const double *, int, int, int, const int64_t *, const int32_t *, int64_t,
-                         uint8_t *, double *, unsigned long long *);
+                         int64_t, uint8_t *, double *, unsigned long long *);
 static score_fn score_kernel(int E, int H) {
     if (H == 128) {
         if (E == 8) return k_score_tile<8, 128>;
@@ -1239,34 +1242,47 @@ void prepare_launch_attributes(const DevTrace &tr, int H) {
     (void)H;
 }
 
-int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill, uint8_t *ranks,
-                 double *scores, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,
-                 unsigned long long *uncertain, cudaStream_t s) {
+// K3 part 1: tile snapshots of the feature tracker (all chains)
+int launch_score_prep(const DevTrace &tr, int include_prefill, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,
+                      cudaStream_t s) {
     if (tr.n_chains == 0) return 0;
-    int launched = 0;
     if (tr.uniform) {
         // snaps scratch holds [summaries | snapshots]
         int32_t *summ = snaps + max_tiles * (2 * tr.E + 4);
         k_tile_summary<<<(unsigned)((max_tiles + 3) / 4), 128, 0, s>>>(tr, summ);
         k_snap_scan<<<(unsigned)((tr.n_chains * tr.E + 3) / 4), 128, 0, s>>>(tr, summ, snaps);
-        launched += 2;
     } else {
         k_tile_offsets<<<1, 1024, 0, s>>>(tr, tile_off);
         k_feat_snap<<<(unsigned)((tr.n_chains + 3) / 4), 128, 0, s>>>(tr, include_prefill, tile_off, snaps);
-        launched += 2;
     }
+    return 2;
+}
+
+// K3 part 2: score tiles [tile_lo, tile_hi) (persistent CTAs).  Uniform
+// traces number tiles chain-major, so a chain range maps to a tile range.
+int launch_score_tiles(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill,
+                       uint8_t *ranks, double *scores, const int32_t *snaps, const int64_t *tile_off,
+                       int64_t tile_lo, int64_t tile_hi, unsigned long long *uncertain, cudaStream_t s) {
+    if (tile_hi <= tile_lo) return 0;
     const size_t smem = score_smem(tr.E, H);
-    if (max_tiles > 0) {
-        const score_fn fn = score_kernel(tr.E, H);
-        int dev = 0, n_sm = 148, per_sm = 1;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)fn, 256, smem);
-        const int64_t grid = std::min<int64_t>(max_tiles, (int64_t)n_sm * (per_sm > 0 ? per_sm : 1));
-        fn<<<(unsigned)grid, 256, smem, s>>>(tr, wt, H, num_nets, include_prefill, tile_off, snaps, max_tiles, ranks,
-                                             scores, uncertain);
-        ++launched;
-    }
+    const score_fn fn = score_kernel(tr.E, H);
+    int dev = 0, n_sm = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)fn, 256, smem);
+    const int64_t grid = std::min<int64_t>(tile_hi - tile_lo, (int64_t)n_sm * (per_sm > 0 ? per_sm : 1));
+    fn<<<(unsigned)grid, 256, smem, s>>>(tr, wt, H, num_nets, include_prefill, tile_off, snaps, tile_lo, tile_hi,
+                                         ranks, scores, uncertain);
+    return 1;
+}
+
+int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill, uint8_t *ranks,
+                 double *scores, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,
+                 unsigned long long *uncertain, cudaStream_t s) {
+    if (tr.n_chains == 0) return 0;
+    int launched = launch_score_prep(tr, include_prefill, snaps, tile_off, max_tiles, s);
+    launched += launch_score_tiles(tr, wt, H, num_nets, include_prefill, ranks, scores, snaps, tile_off, 0,
+                                   max_tiles, uncertain, s);
     return launched;
 }
 

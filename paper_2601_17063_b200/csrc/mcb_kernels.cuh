@@ -49,6 +49,7 @@ struct ReplayParams {
     uint64_t *hashes;                   // optional [chain][pol][cap]
     uint16_t *outcomes;                 // optional [pol][cap][total_acc]
     int64_t solo_min_instances;         // thread-per-instance kernel threshold (E <= 16)
+    int64_t chain_lo, chain_hi;         // chains [lo, hi) replayed by this launch (outputs stay global)
     // segmented speculative replay (mcb_segment.cu); seg.n_seg == 0: whole-chain kernels
     struct Seg {
         int SE;                         // events per segment (multiple of MCB_SNAP_EV)
@@ -93,7 +94,7 @@ int preload_kernels();   // force module loading + smem attributes (call at cont
 bool seg_eligible(const ReplayParams &p);
 int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se);
 size_t seg_snap_bytes(int64_t n_chains, int n_snap);
-int seg_warmup_events(int se);
+int seg_warmup_events(int se, int64_t override_nw);
 size_t seg_out_bytes(int64_t n_inst, int n_seg);
 size_t seg_codes_bytes(int64_t n_inst, int64_t Tpad);
 int launch_seg_snapshot(const ReplayParams &p, cudaStream_t s);
@@ -104,6 +105,11 @@ int launch_prepare_nets(const double *params, int E, int H, int num_nets, double
 __host__ __device__ size_t prepared_net_doubles(int E, int H);
 __host__ __device__ size_t net_param_doubles(int E, int H);
 // K3: snapshot scan + tile scorer. snaps scratch: n_tiles_total * (2E+1) int32; tile_off: n_chains+1 int64
+int launch_score_prep(const DevTrace &tr, int include_prefill, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,
+                      cudaStream_t s);
+int launch_score_tiles(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill,
+                       uint8_t *ranks, double *scores, const int32_t *snaps, const int64_t *tile_off,
+                       int64_t tile_lo, int64_t tile_hi, unsigned long long *uncertain, cudaStream_t s);
 int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill,
                  uint8_t *ranks, double *scores, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,
                  unsigned long long *uncertain, cudaStream_t s);

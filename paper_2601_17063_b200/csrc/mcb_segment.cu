@@ -51,7 +51,7 @@
 #include "mcb_solo.cuh"
 
 #define SEG_MAX_E 16
-#define SEG_DEFAULT_NW 64
+#define SEG_DEFAULT_NW 256
 
 bool seg_eligible(const ReplayParams &p) {
     return p.seg.n_seg > 1 && p.tr.uniform && p.tr.E <= SEG_MAX_E && p.tr.K + 1 <= MCB_SEG_BINS &&
@@ -77,9 +77,10 @@ int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se
     return (int)se;
 }
 
-int seg_warmup_events(int se) {
-    int nw = SEG_DEFAULT_NW < se ? SEG_DEFAULT_NW : se;
-    return nw / MCB_SNAP_EV * MCB_SNAP_EV;
+int seg_warmup_events(int se, int64_t override_nw) {
+    int64_t nw = override_nw > 0 ? override_nw : SEG_DEFAULT_NW;
+    if (nw > se) nw = se;
+    return (int)(nw / MCB_SNAP_EV * MCB_SNAP_EV);
 }
 
 size_t seg_snap_bytes(int64_t n_chains, int n_snap) { return (size_t)n_chains * n_snap * SEG_MAX_E * sizeof(int2); }
@@ -329,11 +330,11 @@ __global__ void __launch_bounds__(128) k_seg_spec(const __grid_constant__ Replay
     if (pass == 1 && P.pol[pol_i] == MCB_LRU) return;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int n_seg = P.seg.n_seg;
-    if (t >= P.tr.n_chains * n_seg * P.n_cap) return;
+    if (t >= (P.chain_hi - P.chain_lo) * n_seg * P.n_cap) return;
     const int cap_i = (int)(t % P.n_cap);
     const int64_t r = t / P.n_cap;
     const int seg = (int)(r % n_seg);
-    const int64_t chain = r / n_seg;
+    const int64_t chain = P.chain_lo + r / n_seg;
     switch (P.pol[pol_i]) {
         case MCB_LRU: seg_spec<EM, POL_LRU>(P, chain, seg, pol_i, cap_i, 0, s_hist, pass); break;
         case MCB_LFU: seg_spec<EM, POL_LFU>(P, chain, seg, pol_i, cap_i, 0, s_hist, pass); break;
@@ -401,6 +402,132 @@ enum { SO_MISSES = 0, SO_NEV = 1, SO_REFC = 2, SO_COMP = 3, SO_RES_END = 4, SO_S
        SO_HASH = 8, SO_RING_END = 10, SO_RING_START = 14, SO_PK = 18, SO_HIST = 34 };
 static_assert(sizeof(SegOut) == 192, "SegOut layout");
 
+__device__ __forceinline__ uint32_t rv_word(const uint4 (&rv)[8], int w) {   // word w of the lane's record
+    const int q = w < 20 ? w / 4 : 5 + (w - 32) / 4;
+    const uint4 v = rv[q];
+    const int c = w & 3;
+    return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    return v;
+}
+
+// Warp-parallel walk of 32 segments (lane j = segment base + j): when every
+// segment's recorded start state equals its predecessor's recorded end state
+// (lane 0: the carried true state A), the speculative runs ARE the true run
+// for the whole batch, so counters are warp sums, the hash a warp sum of
+// h_j * P^(length after j), and the float64 latency an exact integer sum of
+// histogram increments while the running sum stays in one binade (else the
+// segments are folded one by one).  Returns false (nothing consumed) when
+// some segment needs the lockstep fix-up.
+template <int WMAX>
+__device__ __forceinline__ bool batch_splice(const ReplayParams &P, const uint4 (&rv)[8], int nb, int base, int lane,
+                                             int W, int K, int SE, bool track, const uint8_t *codes,
+                                             const double *lut, SState<WMAX> &A, uint32_t &misses, uint32_t &nev,
+                                             uint32_t &refc, uint32_t &comp, bool &stuck, uint64_t &h, double &dlat,
+                                             uint32_t &slow) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const bool valid = lane < nb;
+    // predecessor end state: previous lane's record, lane 0 the carried A
+    uint32_t a_ring[4];
+    pack_ring<WMAX>(A, a_ring);
+    uint32_t pe_res = __shfl_up_sync(FULL, rv_word(rv, SO_RES_END), 1);
+    uint32_t pe_ring[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) pe_ring[i] = __shfl_up_sync(FULL, rv_word(rv, SO_RING_END + i), 1);
+    if (lane == 0) {
+        pe_res = A.res;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) pe_ring[i] = a_ring[i];
+    }
+    bool match = rv_word(rv, SO_RES_START) == pe_res;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t m = (2 * i <= W ? 0xFFFFu : 0u) | (2 * i + 1 <= W ? 0xFFFF0000u : 0u);
+        match = match && ((rv_word(rv, SO_RING_START + i) ^ pe_ring[i]) & m) == 0u;
+    }
+    if (!__all_sync(FULL, match || !valid)) return false;
+
+    misses += __reduce_add_sync(FULL, valid ? rv_word(rv, SO_MISSES) : 0u);
+    nev += __reduce_add_sync(FULL, valid ? rv_word(rv, SO_NEV) : 0u);
+    refc += __reduce_add_sync(FULL, valid ? rv_word(rv, SO_REFC) : 0u);
+    comp += __reduce_add_sync(FULL, valid ? rv_word(rv, SO_COMP) : 0u);
+    stuck = stuck || __any_sync(FULL, valid && (int32_t)rv_word(rv, SO_STUCK) >= 0);
+    const int seg = base + lane;
+    const int64_t ev0 = (int64_t)seg * SE;
+    const int64_t ev1 = valid ? min(ev0 + (int64_t)SE, P.tr.T) : ev0;
+    if (track) {
+        const uint64_t len = (uint64_t)(ev1 - ev0) * K;
+        uint64_t incl = len;   // inclusive suffix sum of the segment lengths over lanes >= lane
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t v = __shfl_down_sync(FULL, incl, o);
+            if (lane + o < 32) incl += v;
+        }
+        const uint64_t after = incl - len;   // accesses of later segments in the batch
+        const uint64_t hj = (uint64_t)rv_word(rv, SO_HASH) | ((uint64_t)rv_word(rv, SO_HASH + 1) << 32);
+        const uint64_t term = valid ? hj * pow_mul(after) : 0ull;
+        const uint64_t total = __shfl_sync(FULL, incl, 0);
+        h = h * pow_mul(total) + warp_sum_u64(term);
+    }
+    // float64 latency: all lanes share S, its binade and the per-bin increments
+    bool done = false;
+    if (dlat > 0.0) {
+        int ex;
+        frexp(dlat, &ex);
+        const uint64_t two52 = 1ull << 52, two53 = 1ull << 53;
+        const uint64_t s_int = (uint64_t)scalbn(dlat, 53 - ex);
+        bool bad = false;
+        uint64_t tot = 0;
+#pragma unroll
+        for (int m = 0; m < MCB_SEG_BINS; ++m) {
+            if (m > K) break;
+            const uint32_t word = rv_word(rv, SO_HIST + (m >> 1));
+            const uint64_t c = valid ? (word >> (16 * (m & 1))) & 0xFFFFu : 0u;
+            const double qf = scalbn(lut[m], 53 - ex);
+            const double fl = floor(qf);
+            const double fr = qf - fl;
+            if (!(qf < (double)two52) || fr == 0.5) { bad = true; break; }
+            const uint64_t q = (uint64_t)fl + (fr > 0.5 ? 1ull : 0ull);
+            if (__umul64hi(c, q) || c * q >= two52) { bad = true; break; }
+            tot += c * q;
+            if (tot >= two52) { bad = true; break; }
+        }
+        bad = __any_sync(FULL, bad);
+        if (!bad) {
+            const uint64_t all = warp_sum_u64(tot);
+            if (all < two52 && s_int + all < two53) {
+                dlat = scalbn((double)(s_int + all), ex - 53);
+                done = true;
+            }
+        }
+    }
+    if (!done) {
+        for (int i = 0; i < nb; ++i) {   // one segment at a time (binade crossing, tie, or S == 0)
+            uint32_t cnt[MCB_SEG_BINS];
+#pragma unroll
+            for (int b = 0; b < MCB_SEG_BINS; ++b) {
+                const uint32_t w = __shfl_sync(FULL, rv_word(rv, SO_HIST + (b >> 1)), i);
+                cnt[b] = b <= K ? (w >> (16 * (b & 1))) & 0xFFFFu : 0u;
+            }
+            if (!fold_hist_fast(dlat, cnt, K + 1, lut)) {
+                const int64_t e0 = (int64_t)(base + i) * SE;
+                dlat = fold_codes(dlat, codes, e0, min(e0 + (int64_t)SE, P.tr.T), lut);
+                ++slow;
+            }
+        }
+    }
+    // the batch's last segment's end state is the true state
+    uint32_t er[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) er[i] = __shfl_sync(FULL, rv_word(rv, SO_RING_END + i), nb - 1);
+    unpack_state<WMAX>(A, __shfl_sync(FULL, rv_word(rv, SO_RES_END), nb - 1), er, W);
+    return true;
+}
+
 template <int EM, int POL>
 __device__ __forceinline__ void seg_finish(const ReplayParams &P, int64_t chain, int pol_i, int cap_i, int ml_variant,
                                            const double *lut, uint16_t (*s_hb)[32]) {
@@ -440,6 +567,9 @@ __device__ __forceinline__ void seg_finish(const ReplayParams &P, int64_t chain,
             for (int i = 0; i < 3; ++i) rv[5 + i] = __ldg(rp + 8 + i);    // words 32..43
         }
         const int nb = min(32, n_seg - base);
+        if (batch_splice<WMAX>(P, rv, nb, base, lane, W, K, SE, track, codes, lut, A, misses, nev, refc, comp,
+                               stuck, h, dlat, slow))
+            continue;   // every segment of the batch started from its predecessor's end state
         for (int i = 0; i < nb; ++i) {
             uint32_t wd[44];
 #pragma unroll
@@ -583,9 +713,9 @@ __global__ void __launch_bounds__(32) k_seg_finish(const __grid_constant__ Repla
     }
     __syncwarp();
     const int64_t t = blockIdx.x;
-    if (t >= P.tr.n_chains * P.n_cap) return;
+    if (t >= (P.chain_hi - P.chain_lo) * P.n_cap) return;
     const int cap_i = (int)(t % P.n_cap);
-    const int64_t chain = t / P.n_cap;
+    const int64_t chain = P.chain_lo + t / P.n_cap;
     switch (pol) {
         case MCB_LRU: seg_finish<EM, POL_LRU>(P, chain, pol_i, cap_i, 0, lut, s_hb); break;
         case MCB_LFU: seg_finish<EM, POL_LFU>(P, chain, pol_i, cap_i, 0, lut, s_hb); break;
@@ -597,16 +727,16 @@ __global__ void __launch_bounds__(32) k_seg_finish(const __grid_constant__ Repla
 
 template <int EM>
 static void launch_seg_t(const ReplayParams &p, cudaStream_t s) {
-    const int64_t n_spec = p.tr.n_chains * p.seg.n_seg * p.n_cap;
+    const int64_t n_spec = (p.chain_hi - p.chain_lo) * p.seg.n_seg * p.n_cap;
     const dim3 g((unsigned)((n_spec + 127) / 128), (unsigned)p.n_pol_launch);
     k_seg_spec<EM><<<g, 128, 0, s>>>(p, 0);
     k_seg_spec<EM><<<g, 128, 0, s>>>(p, 1);
-    const int64_t n_fin = p.tr.n_chains * p.n_cap;
+    const int64_t n_fin = (p.chain_hi - p.chain_lo) * p.n_cap;
     k_seg_finish<EM><<<dim3((unsigned)n_fin, (unsigned)p.n_pol_launch), 32, 0, s>>>(p);
 }
 
 int launch_replay_segmented(const ReplayParams &p, cudaStream_t s) {
-    if (p.tr.n_chains * p.n_pol_launch * p.n_cap == 0) return 0;
+    if ((p.chain_hi - p.chain_lo) * p.n_pol_launch * p.n_cap == 0) return 0;
     if (p.tr.E <= 8) launch_seg_t<8>(p, s);
     else launch_seg_t<16>(p, s);
     return 3;
