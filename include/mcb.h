@@ -179,6 +179,10 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
 /* MCB_TUNE_SEG_NW: warm-up events replayed before each speculative segment
  * (0 = automatic). */
 #define MCB_TUNE_SEG_NW 2
+/* MCB_TUNE_SEG_PASSES: speculation passes of the segmented replay (1 or 2;
+ * the second restarts every segment from the first pass's end state of its
+ * predecessor). */
+#define MCB_TUNE_SEG_PASSES 3
 int mcb_set_tuning(mcb_ctx *ctx, int32_t knob, int64_t value);
 int mcb_last_timings(mcb_ctx *ctx, float *ms, int32_t n);
 

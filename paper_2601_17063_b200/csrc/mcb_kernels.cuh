@@ -55,6 +55,7 @@ struct ReplayParams {
         int SE;                         // events per segment (multiple of MCB_SNAP_EV)
         int n_seg;                      // segments per chain
         int NW;                         // warm-up events before each segment (multiple of MCB_SNAP_EV)
+        int passes;                     // speculation passes (1 or 2; LRU always 1)
         int n_snap;                     // snapshots per chain (every MCB_SNAP_EV events)
         int64_t Tpad;                   // row stride of codes (events, multiple of 16)
         int2 *snap;                     // [chain][n_snap][16] (last position before, count before)

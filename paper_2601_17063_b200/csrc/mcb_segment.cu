@@ -229,8 +229,10 @@ __device__ __forceinline__ void seg_spec(const ReplayParams &P, int64_t chain, i
     const int64_t inst = (chain * P.n_pol + pol_i) * P.n_cap + cap_i;
     const int64_t ev0 = (int64_t)seg * P.seg.SE;
     const int64_t ev1 = min(ev0 + P.seg.SE, tr.T);
-    // pass 0: warm-up start (a snapshot point); pass 1: no warm-up
-    const int64_t ws = (pass == 0 && ev0 > P.seg.NW) ? ev0 - P.seg.NW : ev0;
+    // pass 0: warm-up start (a snapshot point); pass 1: no warm-up.  LRU's
+    // guess is the exact resident set, so it only warms the refetch ring.
+    const int64_t nw = POL == POL_LRU ? (P.seg.NW < MCB_SNAP_EV ? P.seg.NW : MCB_SNAP_EV) : P.seg.NW;
+    const int64_t ws = pass == 0 ? (ev0 > nw ? ev0 - nw : 0) : ev0;
     const int64_t a0 = tr.acc_begin(chain);
     const int64_t e0 = tr.ev_begin(chain);
     const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
@@ -542,7 +544,7 @@ __device__ __forceinline__ void seg_finish(const ReplayParams &P, int64_t chain,
     const int64_t e0 = tr.ev_begin(chain);
     const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
     const uint8_t *codes = P.seg.codes + inst * P.seg.Tpad;
-    const SegOut *so = P.seg.out[POL == POL_LRU ? 0 : 1] + inst * n_seg;
+    const SegOut *so = P.seg.out[(POL == POL_LRU || P.seg.passes < 2) ? 0 : 1] + inst * n_seg;
     const bool track = P.hashes != nullptr;
     const uint64_t pow_full = track ? pow_mul((uint64_t)SE * K) : 0ull;
 
@@ -730,7 +732,7 @@ static void launch_seg_t(const ReplayParams &p, cudaStream_t s) {
     const int64_t n_spec = (p.chain_hi - p.chain_lo) * p.seg.n_seg * p.n_cap;
     const dim3 g((unsigned)((n_spec + 127) / 128), (unsigned)p.n_pol_launch);
     k_seg_spec<EM><<<g, 128, 0, s>>>(p, 0);
-    k_seg_spec<EM><<<g, 128, 0, s>>>(p, 1);
+    if (p.seg.passes > 1) k_seg_spec<EM><<<g, 128, 0, s>>>(p, 1);
     const int64_t n_fin = (p.chain_hi - p.chain_lo) * p.n_cap;
     k_seg_finish<EM><<<dim3((unsigned)n_fin, (unsigned)p.n_pol_launch), 32, 0, s>>>(p);
 }

@@ -43,17 +43,21 @@ def random_ids(rng, n_chains, T, E, K, locality):
     return out
 
 
-def run_case(ids, L, E, caps, window, cost, seg_ev, pols=("lru", "lfu", "belady", "ml")):
+def run_case(ids, L, E, caps, window, cost, seg_ev, pols=("lru", "lfu", "belady", "ml"), passes=1, nw=0):
     n_chains, T, K = ids.shape
     n_traces = n_chains // L
     nets = oracle.nets_from_spec({"kind": "per_layer_seed"}, L, E)
     packed = mcb.packed_from_decode_ids(ids.reshape(n_traces, L, T, K), E)
     _lib.set_tuning(_lib.MCB_TUNE_SEG_EV, seg_ev)
+    _lib.set_tuning(_lib.MCB_TUNE_SEG_PASSES, passes)
+    _lib.set_tuning(_lib.MCB_TUNE_SEG_NW, nw)
     try:
         res = engine.replay_host(packed, [CODES[p] for p in pols], caps, cost, window, nets,
                                  want_hashes=True, want_chain=True)
     finally:
         _lib.set_tuning(_lib.MCB_TUNE_SEG_EV, 0)
+        _lib.set_tuning(_lib.MCB_TUNE_SEG_PASSES, 1)
+        _lib.set_tuning(_lib.MCB_TUNE_SEG_NW, 0)
     jobs = [(p, c) for p in pols for c in caps]
     cdict = {"t_load_s": cost.t_load_s, "t_compute_s": cost.t_compute_s, "loads_serial": cost.loads_serial,
              "ml_score_cost_s": cost.ml_score_cost_s}
@@ -73,12 +77,12 @@ def run_case(ids, L, E, caps, window, cost, seg_ev, pols=("lru", "lfu", "belady"
 
 @pytest.mark.parametrize("E,K,caps", [(8, 2, [2, 3, 5, 7]), (16, 4, [4, 9, 15]), (12, 3, [3, 6, 11]),
                                       (4, 1, [1, 2, 3])])
-@pytest.mark.parametrize("seg_ev", [16, 48, 0])
-def test_segmented_matches_oracle(E, K, caps, seg_ev):
+@pytest.mark.parametrize("seg_ev,passes,nw", [(32, 1, 32), (64, 2, 32), (96, 1, 64), (0, 1, 0), (0, 2, 0)])
+def test_segmented_matches_oracle(E, K, caps, seg_ev, passes, nw):
     rng = np.random.default_rng(E * 100 + K + seg_ev)
     L, T = 3, 1000
     ids = random_ids(rng, 2 * L, T, E, K, locality=0.6)
-    run_case(ids, L, E, caps, 5, mcb.CostModel(), seg_ev)
+    run_case(ids, L, E, caps, 5, mcb.CostModel(), seg_ev, passes=passes, nw=nw)
 
 
 @pytest.mark.parametrize("window", [0, 1, 7])
@@ -87,7 +91,7 @@ def test_segmented_windows_and_costs(window):
     L, E, K, T = 2, 8, 2, 777       # T not a multiple of the segment length
     ids = random_ids(rng, L, T, E, K, locality=0.3)
     cost = mcb.CostModel(t_load_s=2.5e-3, t_compute_s=1.7e-4, loads_serial=False, ml_score_cost_s=1e-4)
-    run_case(ids, L, E, [2, 4, 6], window, cost, 32)
+    run_case(ids, L, E, [2, 4, 6], window, cost, 32, nw=32)
 
 
 def test_segmented_low_locality_long_fixups():
@@ -96,4 +100,5 @@ def test_segmented_low_locality_long_fixups():
     rng = np.random.default_rng(11)
     L, E, K, T = 2, 16, 2, 600
     ids = np.stack([np.stack([rng.choice(E, K, replace=False) for _ in range(T)]) for _ in range(L)]).astype(np.uint8)
-    run_case(ids, L, E, [2, 5, 8, 12], 5, mcb.CostModel(), 16)
+    run_case(ids, L, E, [2, 5, 8, 12], 5, mcb.CostModel(), 32, nw=32)
+    run_case(ids, L, E, [2, 5, 8, 12], 5, mcb.CostModel(), 64, passes=2, nw=32)
