@@ -249,12 +249,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--gen", default="tcgen05", choices=["torch", "tcgen05"])
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--traces", type=int, default=None, help="override the workload's trace count (diagnostics)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--policies", default="lru,lfu,belady,ml", help="comma list (diagnostics only)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = dict(WORKLOADS[args.workload])
+    if args.traces:
+        wl["traces"] = args.traces
     rank, world, local = dist_env()
     POLICIES[:] = args.policies.split(",")
 

@@ -183,6 +183,9 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
  * the second restarts every segment from the first pass's end state of its
  * predecessor). */
 #define MCB_TUNE_SEG_PASSES 3
+/* MCB_TUNE_GROUP_LANES: lanes per cache instance of the num_experts > 16
+ * replay (0 = automatic, 8, 16 or 32). */
+#define MCB_TUNE_GROUP_LANES 4
 int mcb_set_tuning(mcb_ctx *ctx, int32_t knob, int64_t value);
 int mcb_last_timings(mcb_ctx *ctx, float *ms, int32_t n);
 

@@ -90,6 +90,7 @@ struct mcb_ctx {
     int64_t seg_ev = 0;               // segmented replay: 0 auto, <0 off, >0 events per segment (MCB_SEG_EV)
     int64_t seg_nw = 0;               // warm-up events before each segment: 0 auto (MCB_SEG_NW)
     int64_t seg_passes = 1;           // speculation passes (MCB_SEG_PASSES)
+    int64_t group_lanes = 0;          // lanes per instance of the E > 16 replay: 0 auto, 8 / 16 / 32
     DevBuf seg_snap, seg_summ, seg_out, seg_codes, nu_scratch;
     cudaEvent_t ev[10] = {};          // start/stop per stage: K2, K3, K4 non-ML, K4 ML, K5
     bool ran[5] = {};
@@ -125,6 +126,12 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
     }
     if (knob == MCB_TUNE_SEG_NW) {
         c->seg_nw = value;
+        return MCB_OK;
+    }
+    if (knob == MCB_TUNE_GROUP_LANES) {
+        if (value != 0 && value != 8 && value != 16 && value != 32)
+            return mcb_set_error(MCB_ERR_INVALID, "lane group must be 0, 8, 16 or 32");
+        c->group_lanes = value;
         return MCB_OK;
     }
     if (knob == MCB_TUNE_SEG_PASSES) {
@@ -167,6 +174,7 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     if (const char *env = getenv("MCB_SEG_EV")) c->seg_ev = atoll(env);
     if (const char *env = getenv("MCB_SEG_NW")) c->seg_nw = atoll(env);
     if (const char *env = getenv("MCB_SEG_PASSES")) c->seg_passes = atoll(env) == 1 ? 1 : 2;
+    if (const char *env = getenv("MCB_GROUP_LANES")) c->group_lanes = atoll(env);
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);   // replay warps dispatch ahead of K3 blocks
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -385,6 +393,7 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     P.stats = (unsigned long long *)c->stats.p;
     P.chain_lo = 0;
     P.chain_hi = d.n_chains;
+    P.group_lanes = (int)c->group_lanes;
 
     // Orchestration.  K3 (ML scores) is only needed by ML instances, so when
     // both kinds are present the non-ML replay runs on a high-priority side

@@ -548,11 +548,28 @@ int launch_replay(const ReplayParams &p, cudaStream_t s) {
     const int64_t n_inst = (p.chain_hi - p.chain_lo) * p.n_pol_launch * p.n_cap;
     const bool solo_ok = p.tr.total_acc < (1ll << 27) && n_inst >= p.solo_min_instances && p.window >= 0 &&
                          p.window <= SOLO_WMAX;
-    if (E <= 8 && solo_ok) launch_solo_t<8>(p, s);
-    else if (E <= 16 && solo_ok) launch_solo_t<16>(p, s);
-    else if (E <= 32) launch_replay_t<32, 1>(p, s);
-    else if (E <= 64) launch_replay_t<32, 2>(p, s);
-    else launch_replay_t<32, 4>(p, s);
+    if (E <= 8 && solo_ok) { launch_solo_t<8>(p, s); return 1; }
+    if (E <= 16 && solo_ok) { launch_solo_t<16>(p, s); return 1; }
+    // Lane-group size: one whole warp per instance by default.  Groups of 8 /
+    // 16 lanes (4 / 2 instances per warp) are available through
+    // MCB_TUNE_GROUP_LANES but measured slower even with many instances
+    // (c4-shaped, 20K instances: 32 lanes 11.8e9, 16 lanes 8.5e9, 8 lanes
+    // 7.8e9 accesses/s): the groups of a warp diverge on hit / miss.
+    int G = p.group_lanes > 0 ? p.group_lanes : 32;
+    const int gmin = E <= 64 ? 8 : 16;   // at most 8 experts per lane
+    if (G < gmin) G = gmin;
+    if (E <= 32) {
+        if (G == 8) launch_replay_t<8, 4>(p, s);
+        else if (G == 16) launch_replay_t<16, 2>(p, s);
+        else launch_replay_t<32, 1>(p, s);
+    } else if (E <= 64) {
+        if (G == 8) launch_replay_t<8, 8>(p, s);
+        else if (G == 16) launch_replay_t<16, 4>(p, s);
+        else launch_replay_t<32, 2>(p, s);
+    } else {
+        if (G == 16) launch_replay_t<16, 8>(p, s);
+        else launch_replay_t<32, 4>(p, s);
+    }
     return 1;
 }
 
@@ -1301,6 +1318,11 @@ int preload_kernels() {
         (const void *)k_replay<32, 1, true>, (const void *)k_replay<32, 1, false>,
         (const void *)k_replay<32, 2, true>, (const void *)k_replay<32, 2, false>,
         (const void *)k_replay<32, 4, true>, (const void *)k_replay<32, 4, false>,
+        (const void *)k_replay<8, 4, true>, (const void *)k_replay<8, 4, false>,
+        (const void *)k_replay<16, 2, true>, (const void *)k_replay<16, 2, false>,
+        (const void *)k_replay<8, 8, true>, (const void *)k_replay<8, 8, false>,
+        (const void *)k_replay<16, 4, true>, (const void *)k_replay<16, 4, false>,
+        (const void *)k_replay<16, 8, true>, (const void *)k_replay<16, 8, false>,
         (const void *)k_replay_solo<8, true>, (const void *)k_replay_solo<8, false>,
         (const void *)k_replay_solo<16, true>, (const void *)k_replay_solo<16, false>,
     };

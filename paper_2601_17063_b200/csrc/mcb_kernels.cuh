@@ -50,6 +50,7 @@ struct ReplayParams {
     uint16_t *outcomes;                 // optional [pol][cap][total_acc]
     int64_t solo_min_instances;         // thread-per-instance kernel threshold (E <= 16)
     int64_t chain_lo, chain_hi;         // chains [lo, hi) replayed by this launch (outputs stay global)
+    int group_lanes;                    // lane-group size of k_replay (0 = automatic)
     // segmented speculative replay (mcb_segment.cu); seg.n_seg == 0: whole-chain kernels
     struct Seg {
         int SE;                         // events per segment (multiple of MCB_SNAP_EV)

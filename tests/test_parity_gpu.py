@@ -59,16 +59,20 @@ def check_case(case, decisions=True):
             assert got == run["decisions"], (case["name"], run["policy"])
 
 
-@pytest.fixture(params=["warp", "solo", "seg"])
+@pytest.fixture(params=["warp", "group8", "solo", "seg"])
 def kernel_variant(request):
     """Run each parity case through every replay kernel: one warp per
-    instance, one thread per instance (num_experts <= 16), and the segmented
+    instance, 8-lane groups (16 for num_experts > 64: 4 / 2 instances per
+    warp), one thread per instance (num_experts <= 16), and the segmented
     speculative replay (uniform traces, num_experts <= 16) with short
     segments so the stitching is exercised."""
-    _lib.set_tuning(_lib.MCB_TUNE_SOLO_MIN, 1 << 62 if request.param == "warp" else 0)
-    _lib.set_tuning(_lib.MCB_TUNE_SEG_EV, {"warp": -1, "solo": -1, "seg": 32}[request.param])
-    yield request.param
+    v = request.param
+    _lib.set_tuning(_lib.MCB_TUNE_SOLO_MIN, 1 << 62 if v in ("warp", "group8") else 0)
+    _lib.set_tuning(_lib.MCB_TUNE_GROUP_LANES, {"warp": 32, "group8": 8}.get(v, 0))
+    _lib.set_tuning(_lib.MCB_TUNE_SEG_EV, 32 if v == "seg" else -1)
+    yield v
     _lib.set_tuning(_lib.MCB_TUNE_SOLO_MIN, 0)
+    _lib.set_tuning(_lib.MCB_TUNE_GROUP_LANES, 0)
     _lib.set_tuning(_lib.MCB_TUNE_SEG_EV, 0)
 
 
