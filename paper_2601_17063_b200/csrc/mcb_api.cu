@@ -164,7 +164,7 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     CUDA_TRY(cudaGetDeviceProperties(&prop, device));
     if (prop.major < 10)
         return mcb_set_error(MCB_ERR_UNSUPPORTED, "libmcb is built for sm_100a (B200); device is older");
-    if (preload_kernels() != 0 || preload_segment_kernels() != 0)
+    if (preload_kernels() != 0 || preload_segment_kernels() != 0 || preload_segment_warp_kernels() != 0)
         return mcb_set_error(MCB_ERR_CUDA, "failed to load the replay kernels");
     if (int rc = mcb_router_preload()) return rc;
     auto *c = new (std::nothrow) mcb_ctx();
@@ -429,7 +429,7 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         ReplayParams probe = P;
         probe.seg.n_seg = 2;
         const bool solo_ok = n_launch >= c->solo_min_instances;
-        const int se = (c->seg_ev >= 0 && solo_ok && d.uniform) ? seg_events_per_segment(d.T, n_launch, c->seg_ev) : 0;
+        const int se = (c->seg_ev >= 0 && solo_ok && d.uniform) ? seg_events_per_segment(d.T, n_launch, c->seg_ev, d.E) : 0;
         if (se > 0 && seg_eligible(probe)) {
             P.seg.SE = se;
             P.seg.n_seg = (int)((d.T + se - 1) / se);
@@ -437,14 +437,15 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
             P.seg.passes = (int)c->seg_passes;
             P.seg.n_snap = (int)((d.T + MCB_SNAP_EV - 1) / MCB_SNAP_EV);
             P.seg.Tpad = (d.T + 15) / 16 * 16;
-            if (int rc = c->seg_snap.ensure(seg_snap_bytes(d.n_chains, P.seg.n_snap))) return rc;
-            if (int rc = c->seg_summ.ensure(seg_snap_bytes(d.n_chains, P.seg.n_snap))) return rc;
-            if (int rc = c->seg_out.ensure(2 * seg_out_bytes(n_inst, P.seg.n_seg))) return rc;
+            P.seg.snap_e = seg_snap_stride(d.E);
+            if (int rc = c->seg_snap.ensure(seg_snap_bytes(d.n_chains, P.seg.n_snap, d.E))) return rc;
+            if (int rc = c->seg_summ.ensure(seg_snap_bytes(d.n_chains, P.seg.n_snap, d.E))) return rc;
+            if (int rc = c->seg_out.ensure(2 * seg_out_bytes(n_inst, P.seg.n_seg, d.E))) return rc;
             if (int rc = c->seg_codes.ensure(seg_codes_bytes(n_inst, P.seg.Tpad))) return rc;
             P.seg.snap = (int2 *)c->seg_snap.p;
             P.seg.summ = (int2 *)c->seg_summ.p;
             P.seg.out[0] = (SegOut *)c->seg_out.p;
-            P.seg.out[1] = P.seg.out[0] + n_inst * P.seg.n_seg;
+            P.seg.out[1] = (SegOut *)((char *)c->seg_out.p + seg_out_bytes(n_inst, P.seg.n_seg, d.E));
             P.seg.codes = (uint8_t *)c->seg_codes.p;
             Pn.seg = Pm.seg = P.seg;
         }

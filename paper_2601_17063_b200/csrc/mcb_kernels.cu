@@ -152,41 +152,6 @@ int launch_next_use(const DevTrace &tr, uint32_t *next_pos, uint32_t *scratch, c
 // ===========================================================================
 #define KEY_SENT 0xFFFFFFFFu
 
-template <int G>
-struct U32Stream {
-    // 4*G-byte (or G-word) chunks of a stream held one u32 per lane, next
-    // chunk prefetched while the current one is consumed.
-    const uint32_t *base;
-    int64_t limit_words;  // words readable
-    int64_t chunk;        // index of the chunk held in `cur`
-    uint32_t cur, nxt;
-    __device__ __forceinline__ uint32_t load(int64_t ch, int glane) const {
-        const int64_t wi = ch * G + glane;
-        return wi < limit_words ? __ldg(base + wi) : 0u;
-    }
-    __device__ __forceinline__ void init(const void *p, int64_t words, int64_t first_word, int glane) {
-        base = (const uint32_t *)p;
-        limit_words = words;
-        chunk = first_word / G;
-        cur = load(chunk, glane);
-        nxt = load(chunk + 1, glane);
-    }
-    // word index -> value (must be called by the whole group, monotone words)
-    __device__ __forceinline__ uint32_t get(int64_t word, int glane, int gbase, unsigned gmask) {
-        const int64_t ch = word / G;
-        if (ch != chunk) {
-            if (ch == chunk + 1) {
-                cur = nxt;
-            } else {
-                cur = load(ch, glane);
-            }
-            chunk = ch;
-            nxt = load(ch + 1, glane);
-        }
-        return __shfl_sync(gmask, cur, gbase + (int)(word - ch * G));
-    }
-};
-
 template <int EPL>
 __device__ __forceinline__ void set_slot(uint32_t (&a)[EPL], int slot, uint32_t v) {
 #pragma unroll

@@ -58,6 +58,7 @@ struct ReplayParams {
         int NW;                         // warm-up events before each segment (multiple of MCB_SNAP_EV)
         int passes;                     // speculation passes (1 or 2; LRU always 1)
         int n_snap;                     // snapshots per chain (every MCB_SNAP_EV events)
+        int snap_e;                     // experts per snapshot record (16, or E rounded up to 32)
         int64_t Tpad;                   // row stride of codes (events, multiple of 16)
         int2 *snap;                     // [chain][n_snap][16] (last position before, count before)
         int2 *summ;                     // scratch [chain][n_snap][16]
@@ -94,10 +95,12 @@ void prepare_launch_attributes(const DevTrace &tr, int H);
 int preload_kernels();   // force module loading + smem attributes (call at context creation)
 // segmented replay (uniform traces, num_experts <= 16); seg_* are host helpers
 bool seg_eligible(const ReplayParams &p);
-int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se);
-size_t seg_snap_bytes(int64_t n_chains, int n_snap);
+int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se, int E);
+size_t seg_snap_bytes(int64_t n_chains, int n_snap, int E);
+int seg_snap_stride(int E);
+int preload_segment_warp_kernels();
 int seg_warmup_events(int se, int64_t override_nw);
-size_t seg_out_bytes(int64_t n_inst, int n_seg);
+size_t seg_out_bytes(int64_t n_inst, int n_seg, int E);
 size_t seg_codes_bytes(int64_t n_inst, int64_t Tpad);
 int launch_seg_snapshot(const ReplayParams &p, cudaStream_t s);
 int launch_replay_segmented(const ReplayParams &p, cudaStream_t s);

@@ -54,23 +54,28 @@
 #define SEG_DEFAULT_NW 256
 
 bool seg_eligible(const ReplayParams &p) {
-    return p.seg.n_seg > 1 && p.tr.uniform && p.tr.E <= SEG_MAX_E && p.tr.K + 1 <= MCB_SEG_BINS &&
+    return p.seg.n_seg > 1 && p.tr.uniform && p.tr.E <= MCB_MAX_EXPERTS && p.tr.K + 1 <= MCB_SEG_BINS &&
            p.outcomes == nullptr && p.window >= 0 && p.window <= SOLO_WMAX && p.tr.total_acc < (1ll << 27) &&
            p.tr.T * p.tr.K < (1ll << 27);
 }
 
-int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se) {
-    // enough (instance, segment) threads to fill every SM several times over;
-    // segments at least 2 warm-ups long so the warm-up stays a minor cost
-    const int64_t target_threads = 148ll * 1024;
+int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se, int E) {
+    // enough (instance, segment) workers to fill every SM several times over:
+    // threads for the thread-per-instance replay (E <= 16), warps for the
+    // warp-per-instance one.  Thread segments are at least 2 default warm-ups
+    // long (measured best on C2); warp segments may be short (one warp per
+    // segment is plenty of parallel work), down to 64 events.
+    const bool warp = E > SEG_MAX_E;
+    const int64_t target = warp ? 148ll * 32 : 148ll * 1024;
+    const int64_t min_se = warp ? 2 * MCB_SNAP_EV : 2 * SEG_DEFAULT_NW;
     int64_t se;
     if (override_se > 0) {
         se = override_se;
     } else {
-        const int64_t n_seg = n_inst_launch > 0 ? target_threads / n_inst_launch : 1;
+        const int64_t n_seg = n_inst_launch > 0 ? target / n_inst_launch : 1;
         if (n_seg <= 2) return 0;
         se = (T + n_seg - 1) / n_seg;
-        if (se < 2 * SEG_DEFAULT_NW) se = 2 * SEG_DEFAULT_NW;
+        if (se < min_se) se = min_se;
     }
     se = (se + MCB_SNAP_EV - 1) / MCB_SNAP_EV * MCB_SNAP_EV;
     if (se >= T) return 0;
@@ -79,12 +84,20 @@ int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se
 
 int seg_warmup_events(int se, int64_t override_nw) {
     int64_t nw = override_nw > 0 ? override_nw : SEG_DEFAULT_NW;
+    if (override_nw <= 0 && nw > se / 2) nw = se / 2;   // automatic: at most half a segment
     if (nw > se) nw = se;
-    return (int)(nw / MCB_SNAP_EV * MCB_SNAP_EV);
+    nw = nw / MCB_SNAP_EV * MCB_SNAP_EV;
+    return (int)(nw > 0 ? nw : MCB_SNAP_EV);
 }
 
-size_t seg_snap_bytes(int64_t n_chains, int n_snap) { return (size_t)n_chains * n_snap * SEG_MAX_E * sizeof(int2); }
-size_t seg_out_bytes(int64_t n_inst, int n_seg) { return (size_t)n_inst * n_seg * sizeof(SegOut); }
+int seg_snap_stride(int E) { return E <= SEG_MAX_E ? SEG_MAX_E : (E + 31) / 32 * 32; }
+size_t seg_snap_bytes(int64_t n_chains, int n_snap, int E) {
+    return (size_t)n_chains * n_snap * seg_snap_stride(E) * sizeof(int2);
+}
+size_t wseg_out_bytes(int64_t n_inst, int n_seg);   // mcb_segment_warp.cu
+size_t seg_out_bytes(int64_t n_inst, int n_seg, int E) {
+    return E <= SEG_MAX_E ? (size_t)n_inst * n_seg * sizeof(SegOut) : wseg_out_bytes(n_inst, n_seg);
+}
 size_t seg_codes_bytes(int64_t n_inst, int64_t Tpad) { return (size_t)n_inst * Tpad + 64; }
 
 // ---------------------------------------------------------------- snapshot --
@@ -111,7 +124,7 @@ __global__ void __launch_bounds__(128) k_seg_summary(const __grid_constant__ Rep
         s_cnt[x][tid] += 1;
         s_last[x][tid] = (int32_t)p;
     }
-    int2 *o = P.seg.summ + t * SEG_MAX_E;
+    int2 *o = P.seg.summ + t * P.seg.snap_e;
     for (int e = 0; e < SEG_MAX_E; ++e) o[e] = make_int2(s_last[e][tid], s_cnt[e][tid]);
 }
 
@@ -120,16 +133,17 @@ __global__ void __launch_bounds__(128) k_seg_summary(const __grid_constant__ Rep
 __global__ void __launch_bounds__(128) k_seg_scan(const __grid_constant__ ReplayParams P) {
     const int lane = threadIdx.x & 31;
     const int64_t wid = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-    const int64_t chain = wid / SEG_MAX_E;
-    const int e = (int)(wid % SEG_MAX_E);
+    const int SN = P.seg.snap_e;
+    const int64_t chain = wid / SN;
+    const int e = (int)(wid % SN);
     if (chain >= P.tr.n_chains) return;
     const int n = P.seg.n_snap;
-    const int2 *in = P.seg.summ + chain * n * SEG_MAX_E + e;
-    int2 *out = P.seg.snap + chain * n * SEG_MAX_E + e;
+    const int2 *in = P.seg.summ + chain * n * SN + e;
+    int2 *out = P.seg.snap + chain * n * SN + e;
     int32_t carry_last = -1, carry_cnt = 0;
     for (int b0 = 0; b0 < n; b0 += 32) {
         const int b = b0 + lane;
-        const int2 v = b < n ? __ldg(in + (int64_t)b * SEG_MAX_E) : make_int2(-1, 0);
+        const int2 v = b < n ? __ldg(in + (int64_t)b * SN) : make_int2(-1, 0);
         int32_t il = v.x, ic = v.y;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -137,16 +151,18 @@ __global__ void __launch_bounds__(128) k_seg_scan(const __grid_constant__ Replay
             if (lane >= o) { il = max(il, tl); ic += tc; }
         }
         const int32_t el = __shfl_up_sync(0xFFFFFFFFu, il, 1), ec = __shfl_up_sync(0xFFFFFFFFu, ic, 1);
-        if (b < n) out[(int64_t)b * SEG_MAX_E] = make_int2(max(carry_last, lane ? el : -1), carry_cnt + (lane ? ec : 0));
+        if (b < n) out[(int64_t)b * SN] = make_int2(max(carry_last, lane ? el : -1), carry_cnt + (lane ? ec : 0));
         carry_last = max(carry_last, __shfl_sync(0xFFFFFFFFu, il, 31));
         carry_cnt += __shfl_sync(0xFFFFFFFFu, ic, 31);
     }
 }
 
+int launch_seg_snapshot_warp(const ReplayParams &p, cudaStream_t s);   // mcb_segment_warp.cu
 int launch_seg_snapshot(const ReplayParams &p, cudaStream_t s) {
     const int64_t n = p.tr.n_chains * p.seg.n_snap;
-    k_seg_summary<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(p);
-    const int64_t m = p.tr.n_chains * SEG_MAX_E;   // warps
+    if (p.tr.E <= SEG_MAX_E) k_seg_summary<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(p);
+    else launch_seg_snapshot_warp(p, s);
+    const int64_t m = p.tr.n_chains * p.seg.snap_e;   // warps
     k_seg_scan<<<(unsigned)((m + 3) / 4), 128, 0, s>>>(p);
     return 2;
 }
@@ -182,7 +198,7 @@ __device__ __forceinline__ void keys_at(const ReplayParams &P, int64_t chain, in
     constexpr uint32_t KMAX = Solo<EM>::KMAX;
     const DevTrace &tr = P.tr;
     const int E = tr.E;
-    const int2 *sn = P.seg.snap + (chain * P.seg.n_snap + ev / MCB_SNAP_EV) * SEG_MAX_E;
+    const int2 *sn = P.seg.snap + (chain * P.seg.n_snap + ev / MCB_SNAP_EV) * P.seg.snap_e;
     const int64_t a0 = tr.acc_begin(chain);
     uint32_t rrow[EM];
     if (POL == POL_ML) {
@@ -347,58 +363,6 @@ __global__ void __launch_bounds__(128) k_seg_spec(const __grid_constant__ Replay
 }
 
 // ----------------------------------------------------------------- finish --
-// Exact fold of cnt[m] additions of lut[m] (any order within the run) onto S
-// when the running sum provably stays in S's binade and no addend is a
-// rounding tie there; false = use the sequential fold.
-__device__ __forceinline__ bool fold_hist_fast(double &S, const uint32_t *cnt, int nb, const double *lut) {
-    if (!(S > 0.0)) return false;
-    int ex;
-    frexp(S, &ex);                                             // S in [2^(ex-1), 2^ex), ulp 2^(ex-53)
-    const uint64_t two52 = 1ull << 52, two53 = 1ull << 53;
-    const uint64_t s_int = (uint64_t)scalbn(S, 53 - ex);       // in [2^52, 2^53)
-    uint64_t tot = 0;
-    for (int m = 0; m < nb; ++m) {
-        const uint64_t c = cnt[m];
-        if (!c) continue;
-        const double qf = scalbn(lut[m], 53 - ex);             // exact (power-of-two scaling)
-        if (!(qf < (double)two52)) return false;
-        const double fl = floor(qf);
-        const double fr = qf - fl;
-        if (fr == 0.5) return false;                           // tie: depends on the running sum's parity
-        const uint64_t q = (uint64_t)fl + (fr > 0.5 ? 1ull : 0ull);
-        if (__umul64hi(c, q)) return false;
-        const uint64_t p = c * q;
-        if (p >= two52) return false;
-        tot += p;
-        if (tot >= two52) return false;
-    }
-    if (s_int + tot >= two53) return false;                    // would reach the next binade
-    S = scalbn((double)(s_int + tot), ex - 53);
-    return true;
-}
-
-// sequential float64 fold of events [ev, ev1) from the stored miss counts
-__device__ __forceinline__ double fold_codes(double dlat, const uint8_t *codes, int64_t ev, int64_t ev1,
-                                             const double *lut) {
-    while (ev < ev1 && (ev & 15)) dlat = __dadd_rn(dlat, lut[__ldg(codes + ev++)]);
-    const uint4 *v = (const uint4 *)(codes + ev);
-    const int64_t nv = (ev1 - ev) >> 4;
-    for (int64_t i = 0; i < nv; ++i) {
-        const uint4 cur = __ldg(v + i);
-        const uint32_t w[4] = {cur.x, cur.y, cur.z, cur.w};
-        double a[16];
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) a[4 * q + b] = lut[(w[q] >> (8 * b)) & 0xFFu];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) dlat = __dadd_rn(dlat, a[q]);
-    }
-    ev += nv << 4;
-    while (ev < ev1) dlat = __dadd_rn(dlat, lut[__ldg(codes + ev++)]);
-    return dlat;
-}
-
 // word offsets in SegOut (192 bytes = 48 u32) of the fields the walk reads
 enum { SO_MISSES = 0, SO_NEV = 1, SO_REFC = 2, SO_COMP = 3, SO_RES_END = 4, SO_STUCK = 5, SO_RES_START = 6,
        SO_HASH = 8, SO_RING_END = 10, SO_RING_START = 14, SO_PK = 18, SO_HIST = 34 };
@@ -737,8 +701,10 @@ static void launch_seg_t(const ReplayParams &p, cudaStream_t s) {
     k_seg_finish<EM><<<dim3((unsigned)n_fin, (unsigned)p.n_pol_launch), 32, 0, s>>>(p);
 }
 
+int launch_replay_segmented_warp(const ReplayParams &p, cudaStream_t s);   // mcb_segment_warp.cu
 int launch_replay_segmented(const ReplayParams &p, cudaStream_t s) {
     if ((p.chain_hi - p.chain_lo) * p.n_pol_launch * p.n_cap == 0) return 0;
+    if (p.tr.E > SEG_MAX_E) return launch_replay_segmented_warp(p, s);
     if (p.tr.E <= 8) launch_seg_t<8>(p, s);
     else launch_seg_t<16>(p, s);
     return 3;

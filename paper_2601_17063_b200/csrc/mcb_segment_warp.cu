@@ -1,0 +1,583 @@
+// Segmented speculative replay for 16 < num_experts <= 128 (one warp per
+// cache instance), the counterpart of mcb_segment.cu's thread-per-instance
+// version.  Same scheme (see mcb_segment.cu): key snapshots every
+// MCB_SNAP_EV events, one warp per (instance, segment) replays the segment
+// from a guessed state after a warm-up and records start / end state,
+// counters, the poly hash and the miss-count histogram; one warp per
+// instance then walks the segments carrying the true state, splicing a
+// segment whole when the recorded start state equals the true one and
+// replaying true and speculative states in lockstep until they coincide
+// otherwise.  Results are identical to k_replay's by construction.
+//
+// Warp state: expert e lives in lane e / EPL, slot e % EPL (as in k_replay);
+// per lane the resident bits, refetch ring (evictions of the last W decode
+// steps, engine.py:266-297) and the policy keys of its EPL experts.  The
+// victim is the lane-local argmin + redux.sync min + ballot for the lowest
+// id among equal keys (policies.py:148-214, mlpolicy.py:15-26).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mcb_kernels.cuh"
+#include "mcb_solo.cuh"
+
+#define WKEY_SENT 0xFFFFFFFFu
+
+template <int EPL>
+struct WState {
+    uint32_t res;                        // this lane's resident slots
+    uint32_t ring[SOLO_WMAX + 1];        // this lane's slots evicted at decode index dec - i
+    uint32_t ring_or;
+    uint32_t count;                      // resident experts (warp-uniform)
+};
+
+template <int EPL>
+__device__ __forceinline__ void wstate_clear(WState<EPL> &S) {
+    S.res = 0u;
+    S.ring_or = 0u;
+    S.count = 0u;
+#pragma unroll
+    for (int s = 0; s <= SOLO_WMAX; ++s) S.ring[s] = 0u;
+}
+
+// One access of expert x = owner * EPL + slot.  Warp-uniform control flow
+// (hit / miss / evict are ballots or uniform counts).  n.misses / n.nev are
+// warp-uniform, n.refc counts on the owner lane only.
+template <int EPL>
+__device__ __forceinline__ uint32_t wstep(WState<EPL> &S, const uint32_t (&key)[EPL], int owner, uint32_t bit,
+                                          uint32_t pin, uint32_t valid, uint32_t C, int lane, SCount &n, bool &stuck,
+                                          uint32_t &miss_out) {
+    const bool mine = lane == owner;
+    const bool hit = __ballot_sync(FULL_MASK_W, mine && (S.res & bit)) != 0u;
+    miss_out = hit ? 0u : 1u;
+    if (hit) return MCB_OUT_HIT;
+    uint32_t code = MCB_OUT_MISS, vbit = 0u;
+    if (S.count >= C) {
+        const uint32_t cand = S.res & ~pin & valid;
+        uint32_t lk = WKEY_SENT;
+        int ls = 0;
+#pragma unroll
+        for (int s = 0; s < EPL; ++s)
+            if (((cand >> s) & 1u) && key[s] < lk) { lk = key[s]; ls = s; }
+        const uint32_t m = __reduce_min_sync(FULL_MASK_W, lk);
+        stuck |= m == WKEY_SENT;
+        const unsigned b = __ballot_sync(FULL_MASK_W, lk == m);
+        const int wl = __ffs(b) - 1;
+        const int vs = __shfl_sync(FULL_MASK_W, ls, wl);
+        if (lane == wl) {
+            vbit = 1u << vs;
+            S.res &= ~vbit;
+        }
+        code = (uint32_t)(wl * EPL + vs);
+        ++n.nev;
+    } else {
+        ++S.count;
+    }
+    ++n.misses;
+    if (mine) {
+        n.refc += (S.ring_or & bit) ? 1u : 0u;
+#pragma unroll
+        for (int s = 0; s <= SOLO_WMAX; ++s) S.ring[s] &= ~bit;
+        S.ring_or &= ~bit;
+        S.res |= bit;
+    }
+    S.ring[0] |= vbit;
+    S.ring_or |= vbit;
+    return code;
+}
+
+template <int EPL>
+__device__ __forceinline__ void wstate_next_decode(WState<EPL> &S, int W) {
+#pragma unroll
+    for (int s = SOLO_WMAX; s >= 1; --s) S.ring[s] = S.ring[s - 1];
+    S.ring[0] = 0u;
+    uint32_t o = 0u;
+#pragma unroll
+    for (int s = 0; s <= SOLO_WMAX; ++s) o |= (s <= W) ? S.ring[s] : 0u;
+    S.ring_or = o;
+}
+
+template <int EPL>
+__device__ __forceinline__ bool wstate_equal(const WState<EPL> &A, const WState<EPL> &B, int W) {
+    uint32_t d = A.res ^ B.res;
+#pragma unroll
+    for (int s = 0; s <= SOLO_WMAX; ++s) d |= (s <= W) ? (A.ring[s] ^ B.ring[s]) : 0u;
+    return __all_sync(FULL_MASK_W, d == 0u);
+}
+
+// Per (instance, segment) record of the warp version (384 bytes).
+struct WSegOut {
+    uint32_t misses, nev, refc, comp;
+    int32_t stuck_ev;
+    uint32_t pad0;
+    uint64_t hash;
+    uint32_t res_start[4], res_end[4];           // expert masks (bit e % 32 of word e / 32)
+    uint32_t ring_start[SOLO_WMAX + 1][4];
+    uint32_t ring_end[SOLO_WMAX + 1][4];
+    uint16_t hist[MCB_SEG_BINS];
+    uint32_t pad1[7];
+};
+static_assert(sizeof(WSegOut) == 384, "WSegOut layout");
+
+// lane bits (EPL slots) <-> 128-bit expert masks
+template <int EPL>
+__device__ __forceinline__ uint32_t pack_word(uint32_t bits, int lane, int w) {
+    const int e0 = lane * EPL;
+    return __reduce_or_sync(FULL_MASK_W, (e0 >> 5) == w ? (bits << (e0 & 31)) : 0u);
+}
+template <int EPL>
+__device__ __forceinline__ uint32_t unpack_bits(const uint32_t *words, int lane) {
+    const int e0 = lane * EPL;
+    return (words[e0 >> 5] >> (e0 & 31)) & ((1u << EPL) - 1u);
+}
+
+template <int EPL>
+__device__ __forceinline__ void store_state(const WState<EPL> &S, uint32_t *res4, uint32_t (*ring4)[4], int lane) {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        const uint32_t v = pack_word<EPL>(S.res, lane, w);
+        if (lane == w) res4[w] = v;
+    }
+#pragma unroll
+    for (int s = 0; s <= SOLO_WMAX; ++s)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const uint32_t v = pack_word<EPL>(S.ring[s], lane, w);
+            if (lane == w) ring4[s][w] = v;
+        }
+}
+
+template <int EPL>
+__device__ __forceinline__ void load_state(WState<EPL> &S, const uint32_t *res4, const uint32_t (*ring4)[4], int lane,
+                                           int W) {
+    S.res = unpack_bits<EPL>(res4, lane);
+    uint32_t o = 0u;
+#pragma unroll
+    for (int s = 0; s <= SOLO_WMAX; ++s) {
+        S.ring[s] = unpack_bits<EPL>(ring4[s], lane);
+        o |= (s <= W) ? S.ring[s] : 0u;
+    }
+    S.ring_or = o;
+    S.count = __reduce_add_sync(FULL_MASK_W, (uint32_t)__popc(S.res));
+}
+
+// ------------------------------------------------------------------ snapshot --
+// one warp per (chain, block of MCB_SNAP_EV events), lanes over experts
+__global__ void __launch_bounds__(128) k_wseg_summary(const __grid_constant__ ReplayParams P) {
+    const DevTrace &tr = P.tr;
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int n_snap = P.seg.n_snap, SN = P.seg.snap_e;
+    if (wid >= tr.n_chains * n_snap) return;
+    const int64_t chain = wid / n_snap;
+    const int b = (int)(wid % n_snap);
+    int32_t cnt[4] = {0, 0, 0, 0}, last[4] = {-1, -1, -1, -1};
+    const int K = tr.K;
+    const int64_t a0 = tr.acc_begin(chain);
+    const int64_t p0 = (int64_t)b * MCB_SNAP_EV * K;
+    const int64_t p1 = min((int64_t)(b + 1) * MCB_SNAP_EV, tr.T) * K;
+    U32Stream<32> ids;
+    ids.init(tr.acc, (tr.total_acc + 3) >> 2, (a0 + p0) >> 2, lane);
+    for (int64_t p = p0; p < p1; ++p) {
+        const int64_t A = a0 + p;
+        const uint32_t word = ids.get(A >> 2, lane, 0, FULL_MASK_W);
+        const uint32_t x = (word >> (8 * (uint32_t)(A & 3))) & 0xFFu;
+        if ((int)(x & 31) == lane) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if ((int)(x >> 5) == j) { cnt[j] += 1; last[j] = (int32_t)p; }
+        }
+    }
+    int2 *o = P.seg.summ + wid * SN;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int e = lane + 32 * j;
+        if (e < SN) o[e] = make_int2(last[j], cnt[j]);
+    }
+}
+
+// ------------------------------------------------------------------- keys --
+// Exact keys of this lane's experts at event ev (a snapshot point), their
+// seen mask, and (optionally) the guessed resident set: the min(C, #seen)
+// seen experts the policy would evict last (largest keys, then largest ids).
+template <int EPL, int POL>
+__device__ __forceinline__ void wkeys_at(const ReplayParams &P, int64_t chain, int64_t ev, int lane, int ml_variant,
+                                         uint32_t (&key)[EPL], uint32_t &seen) {
+    const DevTrace &tr = P.tr;
+    const int E = tr.E;
+    const int2 *sn = P.seg.snap + (chain * P.seg.n_snap + ev / MCB_SNAP_EV) * P.seg.snap_e;
+    const int64_t a0 = tr.acc_begin(chain);
+    seen = 0u;
+#pragma unroll
+    for (int s = 0; s < EPL; ++s) {
+        const int e = lane * EPL + s;
+        const int2 v = e < E ? __ldg(sn + e) : make_int2(-1, 0);
+        seen |= (v.x >= 0 ? 1u : 0u) << s;
+        uint32_t k = 0u;
+        if (POL == POL_LRU) k = v.x >= 0 ? (uint32_t)v.x : 0u;
+        if (POL == POL_LFU) k = (uint32_t)v.y;
+        if (POL == POL_BELADY) k = ~(v.x >= 0 ? __ldg(P.next_pos + a0 + v.x) : MCB_NEXT_INF);
+        if (POL == POL_ML) {
+            const uint32_t r = (ev > 0 && e < E) ? (uint32_t)__ldcg(P.rank[ml_variant] + (tr.ev_begin(chain) + ev - 1) * E + e) : 0u;
+            k = r ? 256u - r : WKEY_SENT;
+        }
+        key[s] = k;
+    }
+}
+
+template <int EPL>
+__device__ __forceinline__ uint32_t wguess(const uint32_t (&key)[EPL], uint32_t seen, uint32_t C, int lane) {
+    const uint32_t n_seen = __reduce_add_sync(FULL_MASK_W, (uint32_t)__popc(seen));
+    const uint32_t n_res = min(C, n_seen);
+    uint32_t chosen = 0u;
+    for (uint32_t r = 0; r < n_res; ++r) {
+        // largest key among the unchosen seen experts, ties to the largest id
+        uint32_t lk = 0u;
+        int ls = -1;
+#pragma unroll
+        for (int s = 0; s < EPL; ++s)
+            if (((seen & ~chosen) >> s) & 1u) {
+                const uint32_t k = key[s] == WKEY_SENT ? 0u : key[s] + 1u;
+                if (ls < 0 || k >= lk) { lk = k; ls = s; }
+            }
+        const uint32_t m = __reduce_max_sync(FULL_MASK_W, ls >= 0 ? lk : 0u);
+        const unsigned b = __ballot_sync(FULL_MASK_W, ls >= 0 && lk == m);
+        const int wl = 31 - __clz(b);
+        if (lane == wl) chosen |= 1u << ls;
+    }
+    return chosen;
+}
+
+// ---------------------------------------------------------------- replay --
+template <int EPL, int POL>
+struct WReplay {
+    // access stream of one chain from access index a
+    U32Stream<32> ids;
+    U32Stream<32> nx;
+    __device__ __forceinline__ void init(const ReplayParams &P, int64_t a, int lane) {
+        ids.init(P.tr.acc, (P.tr.total_acc + 3) >> 2, a >> 2, lane);
+        if (POL == POL_BELADY) nx.init(P.next_pos, P.tr.total_acc, a, lane);
+    }
+    __device__ __forceinline__ uint32_t id(int64_t A, int lane) {
+        const uint32_t word = ids.get(A >> 2, lane, 0, FULL_MASK_W);
+        return (word >> (8 * (uint32_t)(A & 3))) & 0xFFu;
+    }
+    __device__ __forceinline__ uint32_t next(int64_t A, int lane) { return nx.get(A, lane, 0, FULL_MASK_W); }
+};
+
+template <int EPL, int POL>
+__device__ __forceinline__ void wkey_update(uint32_t (&key)[EPL], bool mine, int slot, uint32_t pos, uint32_t np) {
+    if (!mine) return;
+#pragma unroll
+    for (int s = 0; s < EPL; ++s) {
+        if (s != slot) continue;
+        if (POL == POL_LRU) key[s] = pos;
+        if (POL == POL_LFU) key[s] += 1u;
+        if (POL == POL_BELADY) key[s] = ~np;
+    }
+}
+
+template <int EPL>
+__device__ __forceinline__ void wml_keys(uint32_t (&key)[EPL], uint32_t &valid, const uint8_t *row, int lane, int E) {
+    valid = 0u;
+#pragma unroll
+    for (int s = 0; s < EPL; ++s) {
+        const int e = lane * EPL + s;
+        const uint32_t r = e < E ? (uint32_t)__ldcg(row + e) : 0u;
+        key[s] = r ? 256u - r : WKEY_SENT;
+        valid |= (r ? 1u : 0u) << s;
+    }
+}
+
+template <int EPL, int POL>
+__device__ __forceinline__ void wseg_spec(const ReplayParams &P, int64_t chain, int seg, int pol_i, int cap_i,
+                                          int ml_variant, int lane) {
+    const DevTrace &tr = P.tr;
+    const int E = tr.E, K = tr.K, W = P.window;
+    const uint32_t C = (uint32_t)P.cap[cap_i];
+    const int64_t inst = (chain * P.n_pol + pol_i) * P.n_cap + cap_i;
+    const int64_t ev0 = (int64_t)seg * P.seg.SE;
+    const int64_t ev1 = min(ev0 + P.seg.SE, tr.T);
+    const int64_t nw = POL == POL_LRU ? (P.seg.NW < MCB_SNAP_EV ? P.seg.NW : MCB_SNAP_EV) : P.seg.NW;
+    const int64_t ws = ev0 > nw ? ev0 - nw : 0;
+    const int64_t a0 = tr.acc_begin(chain);
+    const int64_t e0 = tr.ev_begin(chain);
+    const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
+
+    uint32_t key[EPL], seen;
+    wkeys_at<EPL, POL>(P, chain, ws, lane, ml_variant, key, seen);
+    WState<EPL> S;
+    wstate_clear(S);
+    S.res = wguess<EPL>(key, seen, C, lane);
+    S.count = __reduce_add_sync(FULL_MASK_W, (uint32_t)__popc(S.res));
+    uint32_t valid = 0u;
+#pragma unroll
+    for (int s = 0; s < EPL; ++s) valid |= (lane * EPL + s < E ? 1u : 0u) << s;
+    uint32_t comp = 0, hist = 0;
+    SCount n = {0u, 0u, 0u};
+    bool stuck = false;
+    int32_t stuck_ev = -1;
+    uint64_t h = 0;
+    const bool track = P.hashes != nullptr;
+    WSegOut &o = ((WSegOut *)P.seg.out[0])[inst * P.seg.n_seg + seg];
+    uint32_t *codes = (uint32_t *)(P.seg.codes + inst * P.seg.Tpad);
+    uint32_t word = 0;
+    WReplay<EPL, POL> rp;
+    rp.init(P, a0 + ws * K, lane);
+
+    for (int64_t ev = ws; ev < ev1; ++ev) {
+        if (ev == ev0) {
+            store_state<EPL>(S, o.res_start, o.ring_start, lane);
+            n.misses = n.nev = n.refc = 0u;
+            comp = 0u;
+            stuck = false;
+        }
+        if (POL == POL_ML) wml_keys<EPL>(key, valid, rank + (e0 + ev) * E, lane, E);
+        uint32_t pin = 0, sm = 0;
+        for (int j = 0; j < K; ++j) {
+            const int64_t A = a0 + ev * K + j;
+            const uint32_t x = rp.id(A, lane);
+            const int owner = (int)(x / EPL), slot = (int)(x % EPL);
+            const uint32_t bit = 1u << slot;
+            const bool mine = lane == owner;
+            const uint32_t np = POL == POL_BELADY ? rp.next(A, lane) : 0u;
+            wkey_update<EPL, POL>(key, mine, slot, (uint32_t)(ev * K + j), np);
+            uint32_t miss;
+            const uint32_t code = wstep<EPL>(S, key, owner, bit, pin, valid, C, lane, n, stuck, miss);
+            sm += miss;
+            if (mine && miss && !(seen & bit)) ++comp;
+            if (mine) { seen |= bit; pin |= bit; }
+            if (track && ev >= ev0) h = poly16(h, code);
+        }
+        if (ev >= ev0) {
+            if (stuck && stuck_ev < 0) stuck_ev = (int32_t)ev;
+            hist += (sm == (uint32_t)lane) ? 1u : 0u;
+            word |= sm << (8 * (uint32_t)(ev & 3));
+            if ((ev & 3) == 3) {
+                if (lane == 0) codes[ev >> 2] = word;
+                word = 0;
+            }
+        }
+        wstate_next_decode<EPL>(S, W);
+    }
+    if ((ev1 & 3) && lane == 0) codes[ev1 >> 2] = word;
+    const uint32_t refc = __reduce_add_sync(FULL_MASK_W, n.refc);
+    comp = __reduce_add_sync(FULL_MASK_W, comp);
+    store_state<EPL>(S, o.res_end, o.ring_end, lane);
+    if (lane < MCB_SEG_BINS) o.hist[lane] = lane <= K ? (uint16_t)hist : (uint16_t)0;
+    if (lane == 0) {
+        o.misses = n.misses;
+        o.nev = n.nev;
+        o.refc = refc;
+        o.comp = comp;
+        o.stuck_ev = stuck_ev;
+        o.hash = h;
+    }
+}
+
+template <int EPL>
+__global__ void __launch_bounds__(128) k_wseg_spec(const __grid_constant__ ReplayParams P) {
+    const int pol_i = P.pol_map[blockIdx.y];
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int n_seg = P.seg.n_seg;
+    if (w >= (P.chain_hi - P.chain_lo) * n_seg * P.n_cap) return;
+    const int cap_i = (int)(w % P.n_cap);
+    const int64_t r = w / P.n_cap;
+    const int seg = (int)(r % n_seg);
+    const int64_t chain = P.chain_lo + r / n_seg;
+    switch (P.pol[pol_i]) {
+        case MCB_LRU: wseg_spec<EPL, POL_LRU>(P, chain, seg, pol_i, cap_i, 0, lane); break;
+        case MCB_LFU: wseg_spec<EPL, POL_LFU>(P, chain, seg, pol_i, cap_i, 0, lane); break;
+        case MCB_BELADY: wseg_spec<EPL, POL_BELADY>(P, chain, seg, pol_i, cap_i, 0, lane); break;
+        case MCB_ML: wseg_spec<EPL, POL_ML>(P, chain, seg, pol_i, cap_i, 0, lane); break;
+        default: wseg_spec<EPL, POL_ML>(P, chain, seg, pol_i, cap_i, 1, lane); break;
+    }
+}
+
+// ----------------------------------------------------------------- finish --
+
+template <int EPL, int POL>
+__device__ __forceinline__ void wseg_finish(const ReplayParams &P, int64_t chain, int pol_i, int cap_i, int ml_variant,
+                                            const double *lut, int lane) {
+    const DevTrace &tr = P.tr;
+    const int E = tr.E, K = tr.K, W = P.window;
+    const uint32_t C = (uint32_t)P.cap[cap_i];
+    const int n_seg = P.seg.n_seg, SE = P.seg.SE;
+    const int64_t inst = (chain * P.n_pol + pol_i) * P.n_cap + cap_i;
+    const int64_t a0 = tr.acc_begin(chain);
+    const int64_t e0 = tr.ev_begin(chain);
+    const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
+    const uint8_t *codes = P.seg.codes + inst * P.seg.Tpad;
+    const WSegOut *so = (const WSegOut *)P.seg.out[0] + inst * n_seg;
+    const bool track = P.hashes != nullptr;
+
+    WState<EPL> A;                         // the true state, carried across segments
+    wstate_clear(A);
+    uint32_t misses = 0, nev = 0, refc = 0, comp = 0, fix_events = 0, unconverged = 0, slow = 0;
+    bool stuck = false;
+    uint64_t h = 0;
+    double dlat = 0.0;
+    uint32_t valid0 = 0u;
+#pragma unroll
+    for (int s = 0; s < EPL; ++s) valid0 |= (lane * EPL + s < E ? 1u : 0u) << s;
+
+    for (int seg = 0; seg < n_seg; ++seg) {
+        const int64_t ev0 = (int64_t)seg * SE;
+        const int64_t ev1 = min(ev0 + (int64_t)SE, tr.T);
+        const WSegOut &o = so[seg];
+        WState<EPL> B;
+        load_state<EPL>(B, o.res_start, o.ring_start, lane, W);
+        bool conv = wstate_equal<EPL>(A, B, W);
+        int64_t ev = ev0;
+        SCount ca = {0u, 0u, 0u}, cb = {0u, 0u, 0u};
+        uint64_t ha = 0, hb = 0;
+        bool stuck_a = false, stuck_b = false;
+        uint32_t hb_lane = 0;               // B's prefix miss-count histogram (bin = lane)
+        if (!conv) {
+            uint32_t key[EPL], seen;
+            wkeys_at<EPL, POL>(P, chain, ev0, lane, ml_variant, key, seen);
+            uint32_t valid = valid0;
+            WReplay<EPL, POL> rp;
+            rp.init(P, a0 + ev0 * K, lane);
+            while (!conv && ev < ev1) {
+                if (POL == POL_ML) wml_keys<EPL>(key, valid, rank + (e0 + ev) * E, lane, E);
+                uint32_t pin = 0, sma = 0, smb = 0;
+                for (int j = 0; j < K; ++j) {
+                    const int64_t Aa = a0 + ev * K + j;
+                    const uint32_t x = rp.id(Aa, lane);
+                    const int owner = (int)(x / EPL), slot = (int)(x % EPL);
+                    const uint32_t bit = 1u << slot;
+                    const bool mine = lane == owner;
+                    const uint32_t np = POL == POL_BELADY ? rp.next(Aa, lane) : 0u;
+                    wkey_update<EPL, POL>(key, mine, slot, (uint32_t)(ev * K + j), np);
+                    uint32_t ma, mb;
+                    const uint32_t codea = wstep<EPL>(A, key, owner, bit, pin, valid, C, lane, ca, stuck_a, ma);
+                    const uint32_t codeb = wstep<EPL>(B, key, owner, bit, pin, valid, C, lane, cb, stuck_b, mb);
+                    sma += ma;
+                    smb += mb;
+                    if (mine) pin |= bit;
+                    if (track) { ha = poly16(ha, codea); hb = poly16(hb, codeb); }
+                }
+                dlat = __dadd_rn(dlat, lut[sma]);
+                hb_lane += (smb == (uint32_t)lane) ? 1u : 0u;
+                wstate_next_decode<EPL>(A, W);
+                wstate_next_decode<EPL>(B, W);
+                ++ev;
+                conv = wstate_equal<EPL>(A, B, W);
+            }
+            fix_events += (uint32_t)(ev - ev0);
+        }
+        const uint32_t refa = __reduce_add_sync(FULL_MASK_W, ca.refc);
+        const uint32_t refb = __reduce_add_sync(FULL_MASK_W, cb.refc);
+        uint64_t hseg;
+        if (conv) {
+            misses += ca.misses + o.misses - cb.misses;
+            nev += ca.nev + o.nev - cb.nev;
+            refc += refa + o.refc - refb;
+            stuck = stuck || stuck_a || (o.stuck_ev >= 0 && o.stuck_ev >= ev);
+            hseg = track ? o.hash + (ha - hb) * pow_mul((uint64_t)(ev1 - ev) * K) : 0ull;
+            load_state<EPL>(A, o.res_end, o.ring_end, lane, W);
+            uint32_t cnt[MCB_SEG_BINS];
+#pragma unroll
+            for (int b = 0; b < MCB_SEG_BINS; ++b) {
+                const uint32_t hbv = __shfl_sync(FULL_MASK_W, hb_lane, b);
+                cnt[b] = b <= K ? (uint32_t)o.hist[b] - hbv : 0u;
+            }
+            if (!fold_hist_fast(dlat, cnt, K + 1, lut)) {
+                dlat = fold_codes(dlat, codes, ev, ev1, lut);
+                ++slow;
+            }
+        } else {
+            misses += ca.misses;
+            nev += ca.nev;
+            refc += refa;
+            stuck = stuck || stuck_a;
+            hseg = ha;
+            ++unconverged;
+        }
+        comp += o.comp;
+        if (track) h = h * pow_mul((uint64_t)(ev1 - ev0) * K) + hseg;
+    }
+    if (lane != 0) return;
+    if (P.stats) {
+        atomicAdd(P.stats + 1, (unsigned long long)fix_events);
+        atomicAdd(P.stats + 2, (unsigned long long)unconverged);
+        atomicAdd(P.stats + 3, (unsigned long long)n_seg);
+        atomicAdd(P.stats + 4, (unsigned long long)slow);
+    }
+    const uint32_t total = (uint32_t)(tr.T * K);
+    int64_t *out = P.inst_out + inst * MCB_R_N;
+    out[MCB_R_PREFILL_HITS] = 0;
+    out[MCB_R_PREFILL_MISSES] = 0;
+    out[MCB_R_DECODE_HITS] = total - misses;
+    out[MCB_R_DECODE_MISSES] = misses;
+    out[MCB_R_COMPULSORY] = comp;
+    out[MCB_R_EVICTIONS] = nev;
+    out[MCB_R_REFETCHED] = refc;
+    out[MCB_R_STATUS] = stuck ? MCB_ERR_NO_EVICTABLE : MCB_OK;
+    P.inst_lat[inst * 2 + 0] = dlat;
+    P.inst_lat[inst * 2 + 1] = 0.0;
+    if (track) P.hashes[inst] = h;
+}
+
+template <int EPL>
+__global__ void __launch_bounds__(32) k_wseg_finish(const __grid_constant__ ReplayParams P) {
+    __shared__ double lut[MCB_SEG_BINS];
+    const int pol_i = P.pol_map[blockIdx.y];
+    const int pol = P.pol[pol_i];
+    const int K = P.tr.K;
+    const int lane = threadIdx.x & 31;
+    if (lane <= K) {
+        // step_latency_s (engine.py:58-62) per miss count, + ml_score_cost_s for ML decode steps
+        const uint32_t m = lane;
+        const double lat = m > 0 ? __dmul_rn((double)(P.loads_serial ? m : 1u), P.t_load)
+                                 : __dmul_rn((double)K, P.t_compute);
+        lut[m] = __dadd_rn(lat, (pol == MCB_ML || pol == MCB_ML_NO_PREFILL) ? P.ml_cost : 0.0);
+    }
+    __syncwarp();
+    const int64_t t = blockIdx.x;
+    if (t >= (P.chain_hi - P.chain_lo) * P.n_cap) return;
+    const int cap_i = (int)(t % P.n_cap);
+    const int64_t chain = P.chain_lo + t / P.n_cap;
+    switch (pol) {
+        case MCB_LRU: wseg_finish<EPL, POL_LRU>(P, chain, pol_i, cap_i, 0, lut, lane); break;
+        case MCB_LFU: wseg_finish<EPL, POL_LFU>(P, chain, pol_i, cap_i, 0, lut, lane); break;
+        case MCB_BELADY: wseg_finish<EPL, POL_BELADY>(P, chain, pol_i, cap_i, 0, lut, lane); break;
+        case MCB_ML: wseg_finish<EPL, POL_ML>(P, chain, pol_i, cap_i, 0, lut, lane); break;
+        default: wseg_finish<EPL, POL_ML>(P, chain, pol_i, cap_i, 1, lut, lane); break;
+    }
+}
+
+template <int EPL>
+static void launch_wseg_t(const ReplayParams &p, cudaStream_t s) {
+    const int64_t n_spec = (p.chain_hi - p.chain_lo) * p.seg.n_seg * p.n_cap;   // warps
+    k_wseg_spec<EPL><<<dim3((unsigned)((n_spec + 3) / 4), (unsigned)p.n_pol_launch), 128, 0, s>>>(p);
+    const int64_t n_fin = (p.chain_hi - p.chain_lo) * p.n_cap;
+    k_wseg_finish<EPL><<<dim3((unsigned)n_fin, (unsigned)p.n_pol_launch), 32, 0, s>>>(p);
+}
+
+int launch_replay_segmented_warp(const ReplayParams &p, cudaStream_t s) {
+    if ((p.chain_hi - p.chain_lo) * p.n_pol_launch * p.n_cap == 0) return 0;
+    if (p.tr.E <= 32) launch_wseg_t<1>(p, s);
+    else if (p.tr.E <= 64) launch_wseg_t<2>(p, s);
+    else launch_wseg_t<4>(p, s);
+    return 2;
+}
+
+int launch_seg_snapshot_warp(const ReplayParams &p, cudaStream_t s) {
+    const int64_t n = p.tr.n_chains * p.seg.n_snap;   // warps
+    k_wseg_summary<<<(unsigned)((n + 3) / 4), 128, 0, s>>>(p);
+    return 1;
+}
+
+size_t wseg_out_bytes(int64_t n_inst, int n_seg) { return (size_t)n_inst * n_seg * sizeof(WSegOut); }
+
+int preload_segment_warp_kernels() {
+    cudaFuncAttributes a;
+    const void *fns[] = {(const void *)k_wseg_summary, (const void *)k_wseg_spec<1>, (const void *)k_wseg_spec<2>,
+                         (const void *)k_wseg_spec<4>, (const void *)k_wseg_finish<1>,
+                         (const void *)k_wseg_finish<2>, (const void *)k_wseg_finish<4>};
+    for (const void *f : fns)
+        if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
+    return 0;
+}

@@ -19,6 +19,7 @@
 enum { POL_LRU = 0, POL_LFU = 1, POL_BELADY = 2, POL_ML = 3 };
 
 #define SOLO_WMAX 7                       // largest refetch window of the solo kernels
+#define FULL_MASK_W 0xFFFFFFFFu
 #define MCB_HASH_MUL 0x100000001B3ull     // poly hash: h = h * MUL + code + 1 (mod 2^64)
 
 __device__ __forceinline__ uint64_t poly16(uint64_t h, uint32_t code) {
@@ -137,6 +138,44 @@ __device__ __forceinline__ bool sstate_equal(const SState<WMAX> &A, const SState
     return d == 0u;
 }
 
+// Lane-cooperative stream reader for a group of G lanes: the group holds a
+// chunk of G consecutive 32-bit words (one per lane) and the next chunk in
+// flight; get() broadcasts a word by shuffle (whole group, monotone words).
+template <int G>
+struct U32Stream {
+    // 4*G-byte (or G-word) chunks of a stream held one u32 per lane, next
+    // chunk prefetched while the current one is consumed.
+    const uint32_t *base;
+    int64_t limit_words;  // words readable
+    int64_t chunk;        // index of the chunk held in `cur`
+    uint32_t cur, nxt;
+    __device__ __forceinline__ uint32_t load(int64_t ch, int glane) const {
+        const int64_t wi = ch * G + glane;
+        return wi < limit_words ? __ldg(base + wi) : 0u;
+    }
+    __device__ __forceinline__ void init(const void *p, int64_t words, int64_t first_word, int glane) {
+        base = (const uint32_t *)p;
+        limit_words = words;
+        chunk = first_word / G;
+        cur = load(chunk, glane);
+        nxt = load(chunk + 1, glane);
+    }
+    // word index -> value (must be called by the whole group, monotone words)
+    __device__ __forceinline__ uint32_t get(int64_t word, int glane, int gbase, unsigned gmask) {
+        const int64_t ch = word / G;
+        if (ch != chunk) {
+            if (ch == chunk + 1) {
+                cur = nxt;
+            } else {
+                cur = load(ch, glane);
+            }
+            chunk = ch;
+            nxt = load(ch + 1, glane);
+        }
+        return __shfl_sync(gmask, cur, gbase + (int)(word - ch * G));
+    }
+};
+
 // Sequential reader of a chain's uint8 id stream, 16 ids per vector load
 // with the next vector in flight and an L2 prefetch 512 B ahead.
 struct IdReader {
@@ -226,4 +265,56 @@ template <int EM>
 __device__ __forceinline__ void load_rank_row(uint32_t (&rrow)[EM], const uint8_t *row, int E) {
 #pragma unroll
     for (int s = 0; s < EM; ++s) rrow[s] = s < E ? (uint32_t)__ldcg(row + s) : 0u;
+}
+
+// Exact fold of cnt[m] additions of lut[m] (any order within the run) onto S
+// when the running sum provably stays in S's binade and no addend is a
+// rounding tie there; false = use the sequential fold.
+__device__ __forceinline__ bool fold_hist_fast(double &S, const uint32_t *cnt, int nb, const double *lut) {
+    if (!(S > 0.0)) return false;
+    int ex;
+    frexp(S, &ex);                                             // S in [2^(ex-1), 2^ex), ulp 2^(ex-53)
+    const uint64_t two52 = 1ull << 52, two53 = 1ull << 53;
+    const uint64_t s_int = (uint64_t)scalbn(S, 53 - ex);       // in [2^52, 2^53)
+    uint64_t tot = 0;
+    for (int m = 0; m < nb; ++m) {
+        const uint64_t c = cnt[m];
+        if (!c) continue;
+        const double qf = scalbn(lut[m], 53 - ex);             // exact (power-of-two scaling)
+        if (!(qf < (double)two52)) return false;
+        const double fl = floor(qf);
+        const double fr = qf - fl;
+        if (fr == 0.5) return false;                           // tie: depends on the running sum's parity
+        const uint64_t q = (uint64_t)fl + (fr > 0.5 ? 1ull : 0ull);
+        if (__umul64hi(c, q)) return false;
+        const uint64_t p = c * q;
+        if (p >= two52) return false;
+        tot += p;
+        if (tot >= two52) return false;
+    }
+    if (s_int + tot >= two53) return false;                    // would reach the next binade
+    S = scalbn((double)(s_int + tot), ex - 53);
+    return true;
+}
+
+// sequential float64 fold of events [ev, ev1) from the stored miss counts
+__device__ __forceinline__ double fold_codes(double dlat, const uint8_t *codes, int64_t ev, int64_t ev1,
+                                             const double *lut) {
+    while (ev < ev1 && (ev & 15)) dlat = __dadd_rn(dlat, lut[__ldg(codes + ev++)]);
+    const uint4 *v = (const uint4 *)(codes + ev);
+    const int64_t nv = (ev1 - ev) >> 4;
+    for (int64_t i = 0; i < nv; ++i) {
+        const uint4 cur = __ldg(v + i);
+        const uint32_t w[4] = {cur.x, cur.y, cur.z, cur.w};
+        double a[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) a[4 * q + b] = lut[(w[q] >> (8 * b)) & 0xFFu];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) dlat = __dadd_rn(dlat, a[q]);
+    }
+    ev += nv << 4;
+    while (ev < ev1) dlat = __dadd_rn(dlat, lut[__ldg(codes + ev++)]);
+    return dlat;
 }

@@ -85,6 +85,17 @@ def test_segmented_matches_oracle(E, K, caps, seg_ev, passes, nw):
     run_case(ids, L, E, caps, 5, mcb.CostModel(), seg_ev, passes=passes, nw=nw)
 
 
+@pytest.mark.parametrize("E,K,caps", [(32, 4, [4, 10, 31]), (64, 6, [6, 16, 40]), (128, 8, [8, 32, 100]),
+                                      (48, 3, [3, 20])])
+@pytest.mark.parametrize("seg_ev,nw", [(32, 32), (64, 32), (0, 0)])
+def test_warp_segmented_matches_oracle(E, K, caps, seg_ev, nw):
+    """num_experts > 16: one warp per (instance, segment) (mcb_segment_warp.cu)."""
+    rng = np.random.default_rng(E * 10 + K + seg_ev)
+    L, T = 2, 640
+    ids = random_ids(rng, 2 * L, T, E, K, locality=0.5)
+    run_case(ids, L, E, caps, 5, mcb.CostModel(), seg_ev, nw=nw)
+
+
 @pytest.mark.parametrize("window", [0, 1, 7])
 def test_segmented_windows_and_costs(window):
     rng = np.random.default_rng(window)
