@@ -89,7 +89,7 @@ struct mcb_ctx {
     int64_t solo_min_instances = 0;   // thread-per-instance whenever E <= 16 (MCB_SOLO_MIN overrides)
     int64_t seg_ev = 0;               // segmented replay: 0 auto, <0 off, >0 events per segment (MCB_SEG_EV)
     int64_t seg_nw = 0;               // warm-up events before each segment: 0 auto (MCB_SEG_NW)
-    int64_t seg_passes = 1;           // speculation passes (MCB_SEG_PASSES)
+    int64_t seg_passes = 0;           // speculation passes (MCB_SEG_PASSES): 0 auto, 1 or 2
     int64_t group_lanes = 0;          // lanes per instance of the E > 16 replay: 0 auto, 8 / 16 / 32
     DevBuf seg_snap, seg_summ, seg_out, seg_codes, nu_scratch;
     cudaEvent_t ev[10] = {};          // start/stop per stage: K2, K3, K4 non-ML, K4 ML, K5
@@ -135,7 +135,7 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
         return MCB_OK;
     }
     if (knob == MCB_TUNE_SEG_PASSES) {
-        if (value < 1 || value > 2) return mcb_set_error(MCB_ERR_INVALID, "speculation passes must be 1 or 2");
+        if (value < 0 || value > 2) return mcb_set_error(MCB_ERR_INVALID, "speculation passes must be 0 (auto), 1 or 2");
         c->seg_passes = value;
         return MCB_OK;
     }
@@ -173,7 +173,7 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     if (const char *env = getenv("MCB_SOLO_MIN")) c->solo_min_instances = atoll(env);
     if (const char *env = getenv("MCB_SEG_EV")) c->seg_ev = atoll(env);
     if (const char *env = getenv("MCB_SEG_NW")) c->seg_nw = atoll(env);
-    if (const char *env = getenv("MCB_SEG_PASSES")) c->seg_passes = atoll(env) == 1 ? 1 : 2;
+    if (const char *env = getenv("MCB_SEG_PASSES")) c->seg_passes = atoll(env);
     if (const char *env = getenv("MCB_GROUP_LANES")) c->group_lanes = atoll(env);
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);   // replay warps dispatch ahead of K3 blocks
@@ -433,8 +433,10 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         if (se > 0 && seg_eligible(probe)) {
             P.seg.SE = se;
             P.seg.n_seg = (int)((d.T + se - 1) / se);
-            P.seg.NW = seg_warmup_events(se, c->seg_nw);
-            P.seg.passes = (int)c->seg_passes;
+            P.seg.NW = seg_warmup_events(se, c->seg_nw, d.E);
+            // one pass for the thread-per-instance replay (measured best on C2); two for
+            // the warp version, whose states (E > 16) coalesce more slowly
+            P.seg.passes = c->seg_passes > 0 ? (int)c->seg_passes : (d.E <= 16 ? 1 : 2);
             P.seg.n_snap = (int)((d.T + MCB_SNAP_EV - 1) / MCB_SNAP_EV);
             P.seg.Tpad = (d.T + 15) / 16 * 16;
             P.seg.snap_e = seg_snap_stride(d.E);

@@ -99,7 +99,7 @@ int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se
 size_t seg_snap_bytes(int64_t n_chains, int n_snap, int E);
 int seg_snap_stride(int E);
 int preload_segment_warp_kernels();
-int seg_warmup_events(int se, int64_t override_nw);
+int seg_warmup_events(int se, int64_t override_nw, int E);
 size_t seg_out_bytes(int64_t n_inst, int n_seg, int E);
 size_t seg_codes_bytes(int64_t n_inst, int64_t Tpad);
 int launch_seg_snapshot(const ReplayParams &p, cudaStream_t s);

@@ -63,11 +63,11 @@ int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se
     // enough (instance, segment) workers to fill every SM several times over:
     // threads for the thread-per-instance replay (E <= 16), warps for the
     // warp-per-instance one.  Thread segments are at least 2 default warm-ups
-    // long (measured best on C2); warp segments may be short (one warp per
-    // segment is plenty of parallel work), down to 64 events.
+    // long (measured best on C2); warp segments at least 256 events (C1,
+    // E = 128: shorter segments coalesce too rarely and the fix-ups dominate).
     const bool warp = E > SEG_MAX_E;
     const int64_t target = warp ? 148ll * 32 : 148ll * 1024;
-    const int64_t min_se = warp ? 2 * MCB_SNAP_EV : 2 * SEG_DEFAULT_NW;
+    const int64_t min_se = warp ? 8 * MCB_SNAP_EV : 2 * SEG_DEFAULT_NW;
     int64_t se;
     if (override_se > 0) {
         se = override_se;
@@ -82,9 +82,11 @@ int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se
     return (int)se;
 }
 
-int seg_warmup_events(int se, int64_t override_nw) {
+int seg_warmup_events(int se, int64_t override_nw, int E) {
     int64_t nw = override_nw > 0 ? override_nw : SEG_DEFAULT_NW;
-    if (override_nw <= 0 && nw > se / 2) nw = se / 2;   // automatic: at most half a segment
+    // automatic: at most half a segment (thread version), a quarter (warp version)
+    const int64_t cap = E > SEG_MAX_E ? se / 4 : se / 2;
+    if (override_nw <= 0 && nw > cap) nw = cap;
     if (nw > se) nw = se;
     nw = nw / MCB_SNAP_EV * MCB_SNAP_EV;
     return (int)(nw > 0 ? nw : MCB_SNAP_EV);

@@ -290,15 +290,17 @@ __device__ __forceinline__ void wml_keys(uint32_t (&key)[EPL], uint32_t &valid, 
 
 template <int EPL, int POL>
 __device__ __forceinline__ void wseg_spec(const ReplayParams &P, int64_t chain, int seg, int pol_i, int cap_i,
-                                          int ml_variant, int lane) {
+                                          int ml_variant, int lane, int pass) {
     const DevTrace &tr = P.tr;
     const int E = tr.E, K = tr.K, W = P.window;
     const uint32_t C = (uint32_t)P.cap[cap_i];
     const int64_t inst = (chain * P.n_pol + pol_i) * P.n_cap + cap_i;
     const int64_t ev0 = (int64_t)seg * P.seg.SE;
     const int64_t ev1 = min(ev0 + P.seg.SE, tr.T);
+    // pass 0: warm-up from a guess; pass 1: start at the segment from pass 0's
+    // end state of the previous segment (no warm-up)
     const int64_t nw = POL == POL_LRU ? (P.seg.NW < MCB_SNAP_EV ? P.seg.NW : MCB_SNAP_EV) : P.seg.NW;
-    const int64_t ws = ev0 > nw ? ev0 - nw : 0;
+    const int64_t ws = pass == 0 ? (ev0 > nw ? ev0 - nw : 0) : ev0;
     const int64_t a0 = tr.acc_begin(chain);
     const int64_t e0 = tr.ev_begin(chain);
     const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
@@ -307,8 +309,13 @@ __device__ __forceinline__ void wseg_spec(const ReplayParams &P, int64_t chain, 
     wkeys_at<EPL, POL>(P, chain, ws, lane, ml_variant, key, seen);
     WState<EPL> S;
     wstate_clear(S);
-    S.res = wguess<EPL>(key, seen, C, lane);
-    S.count = __reduce_add_sync(FULL_MASK_W, (uint32_t)__popc(S.res));
+    if (pass == 1 && seg > 0) {
+        const WSegOut &q = ((const WSegOut *)P.seg.out[0])[inst * P.seg.n_seg + seg - 1];
+        load_state<EPL>(S, q.res_end, q.ring_end, lane, W);
+    } else {
+        S.res = wguess<EPL>(key, seen, C, lane);
+        S.count = __reduce_add_sync(FULL_MASK_W, (uint32_t)__popc(S.res));
+    }
     uint32_t valid = 0u;
 #pragma unroll
     for (int s = 0; s < EPL; ++s) valid |= (lane * EPL + s < E ? 1u : 0u) << s;
@@ -318,7 +325,7 @@ __device__ __forceinline__ void wseg_spec(const ReplayParams &P, int64_t chain, 
     int32_t stuck_ev = -1;
     uint64_t h = 0;
     const bool track = P.hashes != nullptr;
-    WSegOut &o = ((WSegOut *)P.seg.out[0])[inst * P.seg.n_seg + seg];
+    WSegOut &o = ((WSegOut *)P.seg.out[pass])[inst * P.seg.n_seg + seg];
     uint32_t *codes = (uint32_t *)(P.seg.codes + inst * P.seg.Tpad);
     uint32_t word = 0;
     WReplay<EPL, POL> rp;
@@ -375,8 +382,9 @@ __device__ __forceinline__ void wseg_spec(const ReplayParams &P, int64_t chain, 
 }
 
 template <int EPL>
-__global__ void __launch_bounds__(128) k_wseg_spec(const __grid_constant__ ReplayParams P) {
+__global__ void __launch_bounds__(128) k_wseg_spec(const __grid_constant__ ReplayParams P, int pass) {
     const int pol_i = P.pol_map[blockIdx.y];
+    if (pass == 1 && P.pol[pol_i] == MCB_LRU) return;   // LRU's guess is exact
     const int lane = threadIdx.x & 31;
     const int64_t w = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
     const int n_seg = P.seg.n_seg;
@@ -386,11 +394,11 @@ __global__ void __launch_bounds__(128) k_wseg_spec(const __grid_constant__ Repla
     const int seg = (int)(r % n_seg);
     const int64_t chain = P.chain_lo + r / n_seg;
     switch (P.pol[pol_i]) {
-        case MCB_LRU: wseg_spec<EPL, POL_LRU>(P, chain, seg, pol_i, cap_i, 0, lane); break;
-        case MCB_LFU: wseg_spec<EPL, POL_LFU>(P, chain, seg, pol_i, cap_i, 0, lane); break;
-        case MCB_BELADY: wseg_spec<EPL, POL_BELADY>(P, chain, seg, pol_i, cap_i, 0, lane); break;
-        case MCB_ML: wseg_spec<EPL, POL_ML>(P, chain, seg, pol_i, cap_i, 0, lane); break;
-        default: wseg_spec<EPL, POL_ML>(P, chain, seg, pol_i, cap_i, 1, lane); break;
+        case MCB_LRU: wseg_spec<EPL, POL_LRU>(P, chain, seg, pol_i, cap_i, 0, lane, pass); break;
+        case MCB_LFU: wseg_spec<EPL, POL_LFU>(P, chain, seg, pol_i, cap_i, 0, lane, pass); break;
+        case MCB_BELADY: wseg_spec<EPL, POL_BELADY>(P, chain, seg, pol_i, cap_i, 0, lane, pass); break;
+        case MCB_ML: wseg_spec<EPL, POL_ML>(P, chain, seg, pol_i, cap_i, 0, lane, pass); break;
+        default: wseg_spec<EPL, POL_ML>(P, chain, seg, pol_i, cap_i, 1, lane, pass); break;
     }
 }
 
@@ -408,7 +416,7 @@ __device__ __forceinline__ void wseg_finish(const ReplayParams &P, int64_t chain
     const int64_t e0 = tr.ev_begin(chain);
     const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
     const uint8_t *codes = P.seg.codes + inst * P.seg.Tpad;
-    const WSegOut *so = (const WSegOut *)P.seg.out[0] + inst * n_seg;
+    const WSegOut *so = (const WSegOut *)P.seg.out[(POL == POL_LRU || P.seg.passes < 2) ? 0 : 1] + inst * n_seg;
     const bool track = P.hashes != nullptr;
 
     WState<EPL> A;                         // the true state, carried across segments
@@ -551,7 +559,9 @@ __global__ void __launch_bounds__(32) k_wseg_finish(const __grid_constant__ Repl
 template <int EPL>
 static void launch_wseg_t(const ReplayParams &p, cudaStream_t s) {
     const int64_t n_spec = (p.chain_hi - p.chain_lo) * p.seg.n_seg * p.n_cap;   // warps
-    k_wseg_spec<EPL><<<dim3((unsigned)((n_spec + 3) / 4), (unsigned)p.n_pol_launch), 128, 0, s>>>(p);
+    const dim3 g((unsigned)((n_spec + 3) / 4), (unsigned)p.n_pol_launch);
+    k_wseg_spec<EPL><<<g, 128, 0, s>>>(p, 0);
+    if (p.seg.passes > 1) k_wseg_spec<EPL><<<g, 128, 0, s>>>(p, 1);
     const int64_t n_fin = (p.chain_hi - p.chain_lo) * p.n_cap;
     k_wseg_finish<EPL><<<dim3((unsigned)n_fin, (unsigned)p.n_pol_launch), 32, 0, s>>>(p);
 }

@@ -43,7 +43,7 @@ def random_ids(rng, n_chains, T, E, K, locality):
     return out
 
 
-def run_case(ids, L, E, caps, window, cost, seg_ev, pols=("lru", "lfu", "belady", "ml"), passes=1, nw=0):
+def run_case(ids, L, E, caps, window, cost, seg_ev, pols=("lru", "lfu", "belady", "ml"), passes=0, nw=0):
     n_chains, T, K = ids.shape
     n_traces = n_chains // L
     nets = oracle.nets_from_spec({"kind": "per_layer_seed"}, L, E)
@@ -56,7 +56,7 @@ def run_case(ids, L, E, caps, window, cost, seg_ev, pols=("lru", "lfu", "belady"
                                  want_hashes=True, want_chain=True)
     finally:
         _lib.set_tuning(_lib.MCB_TUNE_SEG_EV, 0)
-        _lib.set_tuning(_lib.MCB_TUNE_SEG_PASSES, 1)
+        _lib.set_tuning(_lib.MCB_TUNE_SEG_PASSES, 0)
         _lib.set_tuning(_lib.MCB_TUNE_SEG_NW, 0)
     jobs = [(p, c) for p in pols for c in caps]
     cdict = {"t_load_s": cost.t_load_s, "t_compute_s": cost.t_compute_s, "loads_serial": cost.loads_serial,
@@ -87,13 +87,13 @@ def test_segmented_matches_oracle(E, K, caps, seg_ev, passes, nw):
 
 @pytest.mark.parametrize("E,K,caps", [(32, 4, [4, 10, 31]), (64, 6, [6, 16, 40]), (128, 8, [8, 32, 100]),
                                       (48, 3, [3, 20])])
-@pytest.mark.parametrize("seg_ev,nw", [(32, 32), (64, 32), (0, 0)])
-def test_warp_segmented_matches_oracle(E, K, caps, seg_ev, nw):
+@pytest.mark.parametrize("seg_ev,nw,passes", [(32, 32, 1), (64, 32, 2), (0, 0, 0)])
+def test_warp_segmented_matches_oracle(E, K, caps, seg_ev, nw, passes):
     """num_experts > 16: one warp per (instance, segment) (mcb_segment_warp.cu)."""
     rng = np.random.default_rng(E * 10 + K + seg_ev)
     L, T = 2, 640
     ids = random_ids(rng, 2 * L, T, E, K, locality=0.5)
-    run_case(ids, L, E, caps, 5, mcb.CostModel(), seg_ev, nw=nw)
+    run_case(ids, L, E, caps, 5, mcb.CostModel(), seg_ev, nw=nw, passes=passes)
 
 
 @pytest.mark.parametrize("window", [0, 1, 7])
