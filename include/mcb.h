@@ -186,6 +186,9 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
 /* MCB_TUNE_GROUP_LANES: lanes per cache instance of the num_experts > 16
  * replay (0 = automatic, 8, 16 or 32). */
 #define MCB_TUNE_GROUP_LANES 4
+/* MCB_TUNE_SERIAL: 1 = run every stage on the caller's stream (no concurrent
+ * side stream), so mcb_last_timings attributes time to each stage alone. */
+#define MCB_TUNE_SERIAL 5
 int mcb_set_tuning(mcb_ctx *ctx, int32_t knob, int64_t value);
 int mcb_last_timings(mcb_ctx *ctx, float *ms, int32_t n);
 

@@ -91,6 +91,7 @@ struct mcb_ctx {
     int64_t seg_nw = 0;               // warm-up events before each segment: 0 auto (MCB_SEG_NW)
     int64_t seg_passes = 0;           // speculation passes (MCB_SEG_PASSES): 0 auto, 1 or 2
     int64_t group_lanes = 0;          // lanes per instance of the E > 16 replay: 0 auto, 8 / 16 / 32
+    bool serial = false;              // one stream for every stage (per-stage attribution timing)
     DevBuf seg_snap, seg_summ, seg_out, seg_codes, nu_scratch;
     cudaEvent_t ev[10] = {};          // start/stop per stage: K2, K3, K4 non-ML, K4 ML, K5
     bool ran[5] = {};
@@ -126,6 +127,10 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
     }
     if (knob == MCB_TUNE_SEG_NW) {
         c->seg_nw = value;
+        return MCB_OK;
+    }
+    if (knob == MCB_TUNE_SERIAL) {
+        c->serial = value != 0;
         return MCB_OK;
     }
     if (knob == MCB_TUNE_GROUP_LANES) {
@@ -417,7 +422,7 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         if (pols[i] == MCB_ML || pols[i] == MCB_ML_NO_PREFILL) Pm.pol_map[Pm.n_pol_launch++] = i;
         else Pn.pol_map[Pn.n_pol_launch++] = i;
     }
-    const bool split = Pn.n_pol_launch > 0 && Pm.n_pol_launch > 0;
+    const bool split = Pn.n_pol_launch > 0 && Pm.n_pol_launch > 0 && !c->serial;
     cudaStream_t sn = split ? c->side : s;
     for (bool &r : c->ran) r = false;
 
