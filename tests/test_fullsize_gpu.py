@@ -1,0 +1,84 @@
+"""BASELINE-size parity (C2: Mixtral-shaped L=32, E=8, K=2, 65,536 tokens,
+capacities 2..7, all four policies; C1: Qwen3-shaped L=48, E=128, K=8) on a
+trace from the router-GEMM generator (K1):
+
+* every chain of every cell is replayed twice -- by the segmented
+  speculative replay and by the whole-chain kernel -- and the per-chain
+  counters and per-access decision hashes must be identical;
+* sampled chains are checked cell by cell against the C oracle (counters,
+  float64 latency, decision hashes);
+* size-independent properties of the reference semantics hold on every
+  chain: evictions = max(0, misses - C), compulsory misses =
+  distinct experts (the same for every cell), hit counts non-decreasing in C
+  (inclusion property), and Belady's hits >= LRU's / LFU's
+  (optimality of the clairvoyant victim)."""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+import torch  # noqa: E402
+
+import paper_2601_17063_b200 as mcb  # noqa: E402
+from paper_2601_17063_b200 import _lib, engine, generator  # noqa: E402
+
+POLS = ["lru", "lfu", "belady", "ml"]
+CODES = [_lib.MCB_LRU, _lib.MCB_LFU, _lib.MCB_BELADY, _lib.MCB_ML]
+
+
+def make_ids(L, E, K, T, d, seed):
+    w = generator.RouterWorkload(L, E, K, T, d, seed=seed)
+    return generator.synthetic_ids(w, device="cuda").cpu().numpy()   # [L][T][K]
+
+
+def replay(packed, caps, nets, seg):
+    _lib.set_tuning(_lib.MCB_TUNE_SEG_EV, 0 if seg else -1)
+    try:
+        return engine.replay_host(packed, CODES, caps, mcb.CostModel(), 5, nets, want_hashes=True, want_chain=True)
+    finally:
+        _lib.set_tuning(_lib.MCB_TUNE_SEG_EV, 0)
+
+
+@pytest.mark.parametrize("shape", ["c2", "c1"])
+def test_full_size_properties_and_kernel_agreement(shape):
+    if shape == "c2":
+        L, E, K, T, d, caps = 32, 8, 2, 65536, 4096, [2, 3, 4, 5, 6, 7]
+    else:
+        L, E, K, T, d, caps = 48, 128, 8, 2048, 2048, [16, 32, 64]
+    ids = make_ids(L, E, K, T, d, seed=3)
+    packed = mcb.packed_from_decode_ids(ids, E)
+    nets = oracle.nets_from_spec({"kind": "per_layer_seed"}, L, E)
+    seg = replay(packed, caps, nets, True)
+    whole = replay(packed, caps, nets, False)
+    cr = seg["chain_reports"]                                   # [chain][pol][cap][8]
+    assert np.all(cr[..., _lib.R_STATUS] == 0)
+    assert np.array_equal(cr, whole["chain_reports"])
+    assert np.array_equal(seg["hashes"], whole["hashes"])
+    assert np.array_equal(seg["latency"], whole["latency"])
+
+    misses = cr[..., _lib.R_DM]
+    hits = cr[..., _lib.R_DH]
+    ev = cr[..., _lib.R_EVICT]
+    cap = np.array(caps)[None, None, :]
+    assert np.array_equal(ev, np.maximum(0, misses - cap))
+    distinct = np.array([len(np.unique(ids[c])) for c in range(L)])
+    assert np.all(cr[..., _lib.R_COMP] == distinct[:, None, None])
+    assert np.all(np.diff(hits, axis=2) >= 0), "hits must not decrease with capacity"
+    bel = hits[:, POLS.index("belady")]
+    for p in ("lru", "lfu"):
+        assert np.all(bel >= hits[:, POLS.index(p)]), p
+
+    # sampled chains against the oracle, every cell
+    rng = np.random.default_rng(0)
+    sample = sorted(rng.choice(L, 2, replace=False).tolist())
+    sub = np.ascontiguousarray(ids[sample])
+    jobs = [(p, c) for p in POLS for c in caps]
+    sub_nets = (nets[0], len(sample), np.concatenate(
+        [nets[2][l * len(nets[2]) // L:(l + 1) * len(nets[2]) // L] for l in sample]))
+    cnt, lat, hsh = oracle.replay_uniform(sub, len(sample), E, jobs, None, 5, sub_nets, hash_kind="poly")
+    for i, c in enumerate(sample):
+        got = cr[c].reshape(len(jobs), _lib.R_N)[:, :7]
+        assert np.array_equal(got, cnt[i]), c
+        assert np.array_equal(seg["hashes"][c].reshape(len(jobs)), hsh[i]), c
