@@ -100,3 +100,13 @@ def test_oracle_poly_hash_matches_recorded_decisions():
             _, hp, _ = oracle.simulate(header, events, name, run["capacity"], COSTS[run["cost"]], run["window"],
                                        nets, include_prefill(run["policy"]), hash_kind="poly")
             assert hp == [poly_hash(d) for d in run["decisions"]], case["name"]
+
+
+def test_oracle_generator_matches_reference_fixtures():
+    """oracle.generate_experts (numpy restatement of trace.py:186-287) against
+    traces made by the reference generator (tests/golden/make_gen_golden.py)."""
+    import json
+    z = np.load(os.path.join(GOLDEN, "gen_cases.npz"))
+    for m in json.loads(str(z["meta"])):
+        got = oracle.generate_experts(tuple(m["header"]), m["config"])
+        assert np.array_equal(got, z[m["name"]]), m["name"]
