@@ -253,9 +253,10 @@ int mcb_router_topk(mcb_ctx *ctx, const void *hidden_bf16, const void *weight_bf
  * the same routing as the reference's numpy generator, bit for bit.  The
  * host supplies the per-layer popularity (trace.py:186-202, float64 [L][E])
  * and the initial PCG64 state of default_rng([rng_seed, 1]) as
- * {state_hi, state_lo, inc_hi, inc_lo}.  Writes experts[seq][token][layer][K]
- * (tokens: prefill then decode; the reference's event order).  Device
- * pointers, asynchronous on `stream`. */
+ * {state_hi, state_lo, inc_hi, inc_lo} (a HOST array of 4).  Writes
+ * experts[seq][token][layer][K] (tokens: prefill then decode; the
+ * reference's event order).  popularity / experts are device pointers; the
+ * call is asynchronous on `stream`. */
 int mcb_gen_reference(mcb_ctx *ctx, int32_t num_layers, int32_t num_experts, int32_t top_k, int64_t num_seqs,
                       int64_t prefill_tokens, int64_t decode_steps, int32_t w_hot, double recency_boost,
                       const double *popularity, const uint64_t *pcg_state, uint8_t *experts, void *stream);

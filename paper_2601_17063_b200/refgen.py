@@ -84,13 +84,13 @@ def generate_experts(header: TraceHeader, cfg: SyntheticWorkloadConfig, device: 
     toks = cfg.prefill_tokens + cfg.decode_steps
     dev = torch.device("cuda", device)
     pop = torch.from_numpy(layer_popularity(header, cfg)).to(dev)
-    st = torch.from_numpy(stream_state(cfg).view(np.int64)).to(dev)
+    st = np.ascontiguousarray(stream_state(cfg))          # host array (read by the host entry point)
     out = torch.empty((cfg.num_seqs, toks, L, K), dtype=torch.uint8, device=dev)
     s = torch.cuda.current_stream(dev)
     lib = _lib.load_library()
     _lib.check(lib.mcb_gen_reference(_lib.context(device), L, E, K, cfg.num_seqs, cfg.prefill_tokens,
                                      cfg.decode_steps, cfg.w_hot, float(cfg.recency_boost), pop.data_ptr(),
-                                     st.data_ptr(), out.data_ptr(), ctypes.c_void_p(s.cuda_stream)))
+                                     st.ctypes.data, out.data_ptr(), ctypes.c_void_p(s.cuda_stream)))
     return out
 
 
