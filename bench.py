@@ -151,6 +151,30 @@ def make_trace_ids(wl, seed: int, gen: str, device):
     from paper_2601_17063_b200 import generator
     outs = []
     gen_report = None
+    if gen == "reference":
+        # the reference's own Zipf + recency generator, reproduced bit-exactly on the GPU
+        from paper_2601_17063_b200 import refgen
+        from paper_2601_17063_b200.trace import TraceHeader
+        hdr = TraceHeader("bench", wl["L"], wl["E"], wl["K"])
+        for i in range(wl["n_traces_local"]):
+            cfg = refgen.SyntheticWorkloadConfig(num_seqs=1, decode_steps=wl["T"], prefill_tokens=0, zipf_s=1.0,
+                                                 recency_boost=0.3, w_hot=4, rng_seed=seed + i)
+            if gen_report is None:
+                refgen.generate_decode_ids(hdr, cfg, device.index or 0)
+                s = torch.cuda.current_stream(device)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                ids = refgen.generate_decode_ids(hdr, cfg, device.index or 0)
+                b.record(s)
+                b.synchronize()
+                ms = a.elapsed_time(b)
+                gen_report = {"kernel": "k_refgen (bit-exact reference generator, trace.py:212-287)", "ms": ms,
+                              "draws_per_s": wl["L"] * wl["T"] * wl["K"] / ms * 1e3,
+                              "config": "zipf_s=1.0, recency_boost=0.3, w_hot=4 (SURVEY.md 8d)"}
+            else:
+                ids = refgen.generate_decode_ids(hdr, cfg, device.index or 0)
+            outs.append(ids)
+        return torch.stack(outs), gen_report
     for i in range(wl["n_traces_local"]):
         w = generator.RouterWorkload(wl["L"], wl["E"], wl["K"], wl["T"], wl["d"], seed=seed + i)
         H = generator.ar1_hidden(w.tokens, w.hidden_dim, w.rho, w.seed * 2 + 11, device)
@@ -247,7 +271,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--gen", default="tcgen05", choices=["torch", "tcgen05"])
+    ap.add_argument("--gen", default="tcgen05", choices=["torch", "tcgen05", "reference"],
+                    help="trace source: K1 router-GEMM generator (tcgen05 / torch) or the reference's "
+                         "Zipf + recency generator reproduced bit-exactly on the GPU")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--traces", type=int, default=None, help="override the workload's trace count (diagnostics)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -360,7 +386,7 @@ def main():
     n_acc_cell = dtrace.total_acc
     alg_bytes = sum(bytes_per_access(p, E, K) * n_acc_cell * len(wl["caps"]) for p in POLICIES)
     peak, bf16_peak, peak_kind = measured_peaks()
-    if gen_report:
+    if gen_report and "tflops" in gen_report:
         gen_report["frac_of_bf16_peak"] = gen_report["tflops"] / bf16_peak
         gen_report["frac_of_hbm"] = gen_report["gbs"] / peak
     traffic = ncu_traffic(args.workload)
@@ -436,7 +462,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": wl["scaling"], "vs_baseline": None, "dtype": "u8/u32 (scorer f64)",
-            "data": f"synthetic (router-GEMM trace via {args.gen}; random-init EvictionNet(E, seed=layer))",
+            "data": ("synthetic (reference Zipf+recency generator, bit-exact on GPU" if args.gen == "reference"
+                     else f"synthetic (router-GEMM trace via {args.gen}") + "; random-init EvictionNet(E, seed=layer))",
             "config": {"workload": wl["name"], "layers": L, "experts": E, "top_k": K, "tokens": T,
                        "traces_total": wl["traces"] if wl["scaling"] == "strong" else wl["traces"] * world,
                        "capacities": wl["caps"], "policies": POLICIES, "parallelism": f"shard{world}",
