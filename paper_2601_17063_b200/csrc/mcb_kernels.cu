@@ -791,30 +791,31 @@ __device__ __forceinline__ double sigmoid_ref(double z, const double *tab) {
 //   k_snap_scan     one warp per chain: exclusive scan over its tiles ->
 //                   snapshot (last update index, count, u) at every tile start
 __global__ void __launch_bounds__(128) k_tile_summary(DevTrace tr, int32_t *__restrict__ summ) {
-    const int lane = threadIdx.x & 31;
-    const int64_t tile = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    // one warp per 32-event tile: lane i marks bit i of occ[e] for each
+    // expert e its event routes to; then per expert count = popc(occ),
+    // last routing (1-based) = 32 - clz(occ)
+    static_assert(MCB_TILE_EV == 32, "one lane per event of a tile");
+    __shared__ uint32_t occ_s[4][MCB_MAX_EXPERTS];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t tile = (int64_t)blockIdx.x * 4 + w;
     const int64_t tpc = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
     if (tile >= tr.n_chains * tpc) return;
     const int64_t c = tile / tpc, ev0 = (tile % tpc) * MCB_TILE_EV;
     const int nev = (int)min((int64_t)MCB_TILE_EV, tr.T - ev0);
     const int E = tr.E, K = tr.K;
-    int32_t cnt[4] = {0, 0, 0, 0}, last[4] = {0, 0, 0, 0};
-    const uint8_t *ids = tr.acc + (c * tr.T + ev0) * K;
-    for (int i = 0; i < nev; ++i) {
-        for (int k = 0; k < K; ++k) {
-            const int x = __ldg(ids + i * K + k);
-            if ((x & 31) == lane) {
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    { const bool hit_j = (x >> 5) == j; cnt[j] += hit_j ? 1 : 0; last[j] = hit_j ? i + 1 : last[j]; }
-            }
-        }
+    uint32_t *occ = occ_s[w];
+    for (int e = lane; e < E; e += 32) occ[e] = 0u;
+    __syncwarp();
+    if (lane < nev) {
+        const uint8_t *ids = tr.acc + (c * tr.T + ev0 + lane) * K;
+        for (int k = 0; k < K; ++k) atomicOr(&occ[__ldg(ids + k)], 1u << lane);
     }
+    __syncwarp();
     int32_t *o = summ + tile * 2 * E;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int e = lane + 32 * j;
-        if (e < E) { o[e] = cnt[j]; o[E + e] = last[j]; }
+    for (int e = lane; e < E; e += 32) {
+        const uint32_t m = occ[e];
+        o[e] = __popc(m);
+        o[E + e] = m ? 32 - __clz(m) : 0;
     }
 }
 
