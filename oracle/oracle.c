@@ -43,7 +43,7 @@
 #define ORC_ERR_NO_EVICTABLE 3
 #define ORC_ERR_NOMEM 6
 
-enum { ORC_LRU = 0, ORC_LFU = 1, ORC_BELADY = 2, ORC_ML = 3 };
+enum { ORC_LRU = 0, ORC_LFU = 1, ORC_BELADY = 2, ORC_ML = 3, ORC_FIFO = 4 };   /* FIFO: policies.py:152-168 */
 
 #define OUT_HIT 0xFFFFu
 #define OUT_MISS 0xFFFEu
@@ -309,6 +309,7 @@ static int replay_layer(const orc_layer *ly, const orc_cfg *cfg, int64_t *cnt, d
     for (int e = 0; e < E; ++e) rec[e] = INFINITY;
 
     int n_res = 0;
+    int64_t fifo_clock = 0;
     uint64_t h = FNV_OFF, hp = 0;
     double dlat = 0.0, plat = 0.0;
     for (int k = 0; k < C_N; ++k) cnt[k] = 0;
@@ -350,11 +351,13 @@ static int replay_layer(const orc_layer *ly, const orc_cfg *cfg, int64_t *cnt, d
             } else {
                 if (cfg->policy == ORC_LFU) freq[xe] += 1;   /* _on_miss */
                 if (n_res >= C) {
-                    if (cfg->policy == ORC_LRU || cfg->policy == ORC_LFU) {
+                    if (cfg->policy == ORC_LRU || cfg->policy == ORC_LFU || cfg->policy == ORC_FIFO) {
                         int64_t bk = 0;
                         for (int e = 0; e < E; ++e) {
                             if (!res[e] || (decode && pinned[e])) continue;
-                            int64_t kk = cfg->policy == ORC_LRU ? stamp[e] : freq[e];
+                            /* FIFO: min (arrival clock, id) (policies.py:168); arrival
+                             * is kept in stamp[] (written at insertion only) */
+                            int64_t kk = (cfg->policy == ORC_LRU || cfg->policy == ORC_FIFO) ? stamp[e] : freq[e];
                             if (victim < 0 || kk < bk) { victim = e; bk = kk; }
                         }
                     } else if (cfg->policy == ORC_BELADY) {
@@ -385,6 +388,7 @@ static int replay_layer(const orc_layer *ly, const orc_cfg *cfg, int64_t *cnt, d
                 res[xe] = 1;
                 n_res++;
                 if (cfg->policy == ORC_LRU) stamp[xe] = pos;   /* _on_insert */
+                if (cfg->policy == ORC_FIFO) stamp[xe] = fifo_clock++;   /* FIFOPolicy._on_insert */
             }
             /* engine-side accounting (engine.py:243-257) */
             if (hit) {

@@ -285,6 +285,7 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
                     set_slot<EPL>(pend, slot, 0u);
                     seen |= bit;
                     res |= bit;
+                    if (POL == POL_FIFO) set_slot<EPL>(key, slot, pos);   // arrival (policies.py:159-161)
                 }
             }
             if (decode && mine) pin |= bit;
@@ -338,6 +339,7 @@ __global__ void __launch_bounds__(128) k_replay(const __grid_constant__ ReplayPa
         case MCB_LFU: replay_instance<G, EPL, POL_LFU, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
         case MCB_BELADY: replay_instance<G, EPL, POL_BELADY, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
         case MCB_ML: replay_instance<G, EPL, POL_ML, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
+        case MCB_FIFO: replay_instance<G, EPL, POL_FIFO, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
         default: replay_instance<G, EPL, POL_ML, UNIFORM>(P, chain, pol_i, cap_i, inst, 1); break;
     }
 }
@@ -417,6 +419,7 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
             solo_key_update<EM, POL>(pk, x, bit, pos, np);
             uint32_t miss;
             const uint32_t code = sstep<EM, WMAX>(S, pk, bit, pin, valid, C, n, stuck, miss);
+            if (POL == POL_FIFO) solo_fifo_insert<EM>(pk, x, bit, pos, miss);
             step_miss += miss;
             if (decode) { dh += 1u - miss; dm += miss; }
             else { ph += 1u - miss; pm += miss; }
@@ -467,6 +470,7 @@ __global__ void __launch_bounds__(128) k_replay_solo(const __grid_constant__ Rep
         case MCB_LFU: solo_instance<EM, POL_LFU, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
         case MCB_BELADY: solo_instance<EM, POL_BELADY, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
         case MCB_ML: solo_instance<EM, POL_ML, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
+        case MCB_FIFO: solo_instance<EM, POL_FIFO, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
         default: solo_instance<EM, POL_ML, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 1); break;
     }
 }

@@ -16,7 +16,7 @@
 
 #include "mcb_kernels.cuh"
 
-enum { POL_LRU = 0, POL_LFU = 1, POL_BELADY = 2, POL_ML = 3 };
+enum { POL_LRU = 0, POL_LFU = 1, POL_BELADY = 2, POL_ML = 3, POL_FIFO = 4 };
 
 #define SOLO_WMAX 7                       // largest refetch window of the solo kernels
 #define FULL_MASK_W 0xFFFFFFFFu
@@ -242,10 +242,23 @@ __device__ __forceinline__ void solo_key_update(uint32_t (&pk)[EM], uint32_t x, 
         nk = cur + (1u << SH);
     }
     if (POL == POL_BELADY) nk = ((np == MCB_NEXT_INF ? 0u : KMAX - np) << SH) | x;   // farthest next use first
+    if (POL == POL_FIFO) return;   // FIFO keys change at insertion only (solo_fifo_insert)
     if (POL != POL_ML) {
 #pragma unroll
         for (int s = 0; s < EM; ++s) pk[s] = ((bit >> s) & 1u) ? nk : pk[s];
     }
+}
+
+// FIFO (policies.py:152-168): the key is the arrival order, set when x is
+// inserted (a miss); positions grow with the arrival clock, so (pos, id)
+// orders like the reference's (arrival, id).  State-dependent, so FIFO runs
+// in the whole-chain kernels only.
+template <int EM>
+__device__ __forceinline__ void solo_fifo_insert(uint32_t (&pk)[EM], uint32_t x, uint32_t bit, uint32_t pos,
+                                                 uint32_t miss) {
+    const uint32_t nk = (pos << Solo<EM>::SH) | x;
+#pragma unroll
+    for (int s = 0; s < EM; ++s) pk[s] = (miss && ((bit >> s) & 1u)) ? nk : pk[s];
 }
 
 // ML: packed keys and the selectable mask from one event's rank row

@@ -96,6 +96,7 @@ def test_uniform_layout_for_decode_only_single_sequence():
 
 def test_policy_factory_and_errors_without_gpu():
     assert mcb.policy_factory("lru")[0] == "lru"
+    assert mcb.policy_factory("fifo")[1].code == _lib.MCB_FIFO      # FIFO runs on the GPU too
     with pytest.raises(mcb.SimulationError):
         mcb.policy_factory("nope")
     with pytest.raises(mcb.SimulationError):

@@ -110,3 +110,9 @@ def test_oracle_generator_matches_reference_fixtures():
     for m in json.loads(str(z["meta"])):
         got = oracle.generate_experts(tuple(m["header"]), m["config"])
         assert np.array_equal(got, z[m["name"]]), m["name"]
+
+
+def test_oracle_fifo_cases():
+    """FIFO (policies.py:152-168) on reference-made fixtures (make_fifo_golden.py)."""
+    for case in load("fifo_cases.json.gz")["cases"]:
+        _check_case(case)
