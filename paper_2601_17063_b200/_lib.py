@@ -39,6 +39,7 @@ EXPORTED_SYMBOLS = (
     "mcb_set_timing", "mcb_last_timings", "mcb_set_tuning", "mcb_read_stats",
     "mcb_pack_trace", "mcb_packed_view", "mcb_packed_positions", "mcb_packed_free",
     "mcb_replay", "mcb_replay_host", "mcb_next_use", "mcb_score", "mcb_router_topk", "mcb_gen_reference",
+    "mcb_training_data",
 )
 
 
@@ -130,6 +131,7 @@ def load_library():
             "mcb_next_use": ([P, P, P, P], ctypes.c_int),
             "mcb_score": ([P, P, P, i32, P, P, P], ctypes.c_int),
             "mcb_router_topk": ([P, P, P, i64, i32, i32, i32, i32, P, P, P], ctypes.c_int),
+            "mcb_training_data": ([P, P, i32, i32, P, P, P, P], ctypes.c_int),
             "mcb_gen_reference": ([P, i32, i32, i32, i64, i64, i64, i32, ctypes.c_double, P, P, P, P],
                                   ctypes.c_int),
         }

@@ -520,6 +520,60 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     return MCB_OK;
 }
 
+// Belady-labelled training data (dataset.py:35-96) for decode-only
+// single-sequence traces: features [chain][T][2E] (float64), targets
+// [chain][T][E] (float64) and masks [chain][T][E] (0/1 bytes).  Device
+// pointers, asynchronous on `stream`.
+extern "C" int mcb_training_data(mcb_ctx *c, const mcb_trace *t, int32_t capacity, int32_t distance_cap,
+                                 double *features, double *targets, uint8_t *masks, void *stream) {
+    mcb_clear_error();
+    if (!c) return mcb_set_error(MCB_ERR_INVALID, "ctx is NULL");
+    if (int rc = check_trace(t)) return rc;
+    if (!t->uniform)
+        return mcb_set_error(MCB_ERR_UNSUPPORTED, "training data on the GPU needs a decode-only single-sequence trace");
+    if (capacity < t->top_k) return mcb_set_error(MCB_ERR_CAPACITY, "capacity is below top_k");
+    if (distance_cap < 1) return mcb_set_error(MCB_ERR_INVALID, "distance_cap must be >= 1");
+    if (!features || !targets || !masks) return mcb_set_error(MCB_ERR_INVALID, "NULL output");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const DevTrace d = make_dev_trace(t);
+    // Belady residency at the label capacity (whole-chain replay, masks at every event start)
+    const size_t nu_sw = next_use_scratch_words(d);
+    if (nu_sw)
+        if (int rc = c->nu_scratch.ensure(nu_sw * sizeof(uint32_t))) return rc;
+    if (int rc = c->next_pos.ensure((size_t)(d.total_acc + 64) * sizeof(uint32_t))) return rc;
+    if (int rc = c->inst_out.ensure((size_t)(d.n_chains + 1) * MCB_R_N * sizeof(int64_t))) return rc;
+    if (int rc = c->inst_lat.ensure((size_t)(d.n_chains + 1) * 2 * sizeof(double))) return rc;
+    const int64_t tiles = max_score_tiles(d);
+    if (int rc = c->snaps.ensure((size_t)(tiles + 1) * (4 * d.E + 8) * sizeof(int32_t))) return rc;
+    launch_next_use(d, (uint32_t *)c->next_pos.p, nu_sw ? (uint32_t *)c->nu_scratch.p : nullptr, s);
+    ReplayParams P;
+    memset(&P, 0, sizeof P);
+    P.tr = d;
+    P.n_pol = 1;
+    P.n_cap = 1;
+    P.n_pol_launch = 1;
+    P.pol[0] = MCB_BELADY;
+    P.cap[0] = capacity;
+    P.t_load = 1.0;
+    P.t_compute = 1.0;
+    P.window = 5;
+    P.inst_out = (int64_t *)c->inst_out.p;
+    P.inst_lat = (double *)c->inst_lat.p;
+    P.next_pos = (const uint32_t *)c->next_pos.p;
+    P.chain_lo = 0;
+    P.chain_hi = d.n_chains;
+    P.res_masks = masks;
+    launch_replay(P, s);
+    // features and targets
+    launch_score_prep(d, 1, (int32_t *)c->snaps.p, (int64_t *)c->tile_off.p, tiles, s);
+    launch_train_features(d, (const int32_t *)c->snaps.p, tiles, features, s);
+    launch_train_targets(d, distance_cap, targets, s);
+    CUDA_TRY(cudaGetLastError());
+    return MCB_OK;
+}
+
 extern "C" int mcb_replay(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, int32_t n_pol, const int32_t *caps,
                           int32_t n_cap, const mcb_cost *cost, const mcb_nets *nets, const mcb_outputs *out,
                           void *stream) {

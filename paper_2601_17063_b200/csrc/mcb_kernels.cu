@@ -211,6 +211,14 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
                                       : __ldg(tr.ev_info + e0 + ev);
         const uint32_t nacc = mcb_ev_nacc(info);
         const bool decode = mcb_ev_decode(info);
+        if (UNIFORM && P.res_masks) {   // resident set before the event (dataset.py:61-63)
+            uint8_t *m = P.res_masks + (chain * tr.T + ev) * E;
+#pragma unroll
+            for (int s = 0; s < EPL; ++s) {
+                const int e = glane * EPL + s;
+                if (e < E) m[e] = (uint8_t)((res >> s) & 1u);
+            }
+        }
         if (POL == POL_LFU && mcb_ev_newseq(info)) {
             // start_sequence: LFU counts reset (policies.py:184-185)
 #pragma unroll
@@ -405,6 +413,10 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
         if (POL == POL_LFU && !UNIFORM && mcb_ev_newseq(info)) {
 #pragma unroll
             for (int s = 0; s < EM; ++s) pk[s] = (uint32_t)s;   // start_sequence (policies.py:184-185)
+        }
+        if (UNIFORM && P.res_masks) {   // resident set before the event (dataset.py:61-63)
+            uint8_t *m = P.res_masks + (chain * tr.T + ev) * E;
+            for (int e = 0; e < E; ++e) m[e] = (uint8_t)((S.res >> e) & 1u);
         }
         if (POL == POL_ML) {
             solo_ml_keys<EM>(pk, valid, rrow);   // this event's rank row (mlpolicy.py:59-62)
@@ -1001,6 +1013,136 @@ __host__ __device__ __forceinline__ int mlp_ld(int cols) { return (cols + 15) / 
 // selectable e (s > -inf), 0 otherwise (NaN / -inf are never evicted,
 // mlpolicy.py:15-26).  argmax score with lowest-id ties == argmax rank with
 // lowest-id ties.
+// Feature vectors [1/r || f / max_f] (features.py:44-52, float64) of the
+// events [ev0, ev0 + nev) of chain c (one 32-event tile of a decode-only
+// single-sequence trace) from the tile's tracker snapshot: thread i sets bit
+// i of occ[e] for each expert its event routes to (features.py:34-39), so
+// recency and counts at event i are the snapshot plus in-tile prefix bits.
+// Rows go to out[i * ld + ...]; all_rows also zero-fills rows i >= nev.
+// Shared scratch: occ[E] (u64), pmax[32].  Every thread of the block calls it.
+__device__ __forceinline__ void tile_features_uniform(const DevTrace &tr, const int32_t *__restrict__ snaps,
+                                                      int64_t tile, int64_t c, int64_t ev0, int nev, int E,
+                                                      unsigned long long *occ, int32_t *pmax, double *out, int ld,
+                                                      bool all_rows) {
+    const int tid = threadIdx.x;
+    const int32_t *sp = snaps + tile * (2 * E + 4);
+    const int32_t u0 = sp[2 * E];
+    for (int e = tid; e < E; e += blockDim.x) occ[e] = 0ull;
+    __syncthreads();
+    const uint8_t *ids = tr.acc + (c * tr.T + ev0) * tr.K;
+    if (tid < nev)
+        for (int k = 0; k < tr.K; ++k) atomicOr(&occ[__ldg(ids + tid * tr.K + k)], 1ull << tid);
+    __syncthreads();
+    if (tid < MCB_TILE_EV) {
+        int32_t m = 0;
+        if (tid < nev) {
+            const unsigned long long upto = tid == 63 ? ~0ull : ((2ull << tid) - 1ull);
+            for (int k = 0; k < tr.K; ++k) {
+                const int x = __ldg(ids + tid * tr.K + k);
+                m = max(m, sp[E + x] + __popcll(occ[x] & upto));
+            }
+        }
+        pmax[tid] = m;
+    }
+    __syncthreads();
+    if (tid < 32) {   // inclusive prefix max over the tile's events, then max with the snapshot max_f
+        int32_t a = 2 * tid < MCB_TILE_EV ? pmax[2 * tid] : 0;
+        int32_t b = max(a, 2 * tid + 1 < MCB_TILE_EV ? pmax[2 * tid + 1] : 0);
+        int32_t m0 = 0;
+        for (int e = 0; e < E; ++e) m0 = max(m0, sp[E + e]);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t t = __shfl_up_sync(FULL_MASK, b, o);
+            if (tid >= o) { a = max(a, t); b = max(b, t); }
+        }
+        if (2 * tid < MCB_TILE_EV) pmax[2 * tid] = max(a, m0);
+        if (2 * tid + 1 < MCB_TILE_EV) pmax[2 * tid + 1] = max(b, m0);
+    }
+    __syncthreads();
+    for (int q = tid; q < MCB_TILE_EV * E; q += blockDim.x) {
+        const int i = q % MCB_TILE_EV, e = q / MCB_TILE_EV;
+        double rv = 0.0, fv = 0.0;
+        if (i < nev) {
+            const unsigned long long seen = occ[e] & (i == 63 ? ~0ull : ((2ull << i) - 1ull));
+            const int32_t f = sp[E + e] + __popcll(seen);
+            const int32_t lastu = seen ? u0 + (63 - __clzll(seen)) + 1 : sp[e];
+            const int32_t u = u0 + i + 1;
+            rv = lastu < 0 ? 0.0 : 1.0 / (double)(u - lastu + 1);
+            const int32_t mf = pmax[i];
+            fv = mf > 0 ? (double)f / (double)mf : 0.0;
+        }
+        if (i < nev || all_rows) {
+            out[i * ld + e] = rv;
+            out[i * ld + E + e] = fv;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Training data (dataset.py:35-96, decode-only single-sequence traces):
+// features of every decode step (the K3 feature rows) and capped next-use
+// distance targets; the Belady residency masks come from the replay kernels
+// (ReplayParams::res_masks).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_train_features(DevTrace tr, const int32_t *__restrict__ snaps,
+                                                        double *__restrict__ features) {
+    __shared__ unsigned long long occ[MCB_MAX_EXPERTS];
+    __shared__ int32_t pmax[MCB_TILE_EV];
+    const int64_t tile = blockIdx.x;
+    const int64_t tpc = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
+    if (tile >= tr.n_chains * tpc) return;
+    const int64_t c = tile / tpc, ev0 = (tile % tpc) * MCB_TILE_EV;
+    const int nev = (int)min((int64_t)MCB_TILE_EV, tr.T - ev0);
+    const int E = tr.E;
+    tile_features_uniform(tr, snaps, tile, c, ev0, nev, E, occ, pmax, features + (c * tr.T + ev0) * 2 * E, 2 * E,
+                          false);
+}
+
+// targets[c][t][e] = min(d, cap) / cap with d the events until e is next
+// routed strictly after t (StepNextUse.distance, replay.py:92-109; never
+// again -> 1.0).  One warp per chain walks its events backwards, lanes over
+// experts.
+__global__ void __launch_bounds__(128) k_train_targets(DevTrace tr, int cap, double *__restrict__ targets) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (c >= tr.n_chains) return;
+    const int E = tr.E, K = tr.K;
+    int64_t next[4] = {-1, -1, -1, -1};
+    const double dcap = (double)cap;
+    const uint8_t *ids = tr.acc + c * tr.T * K;
+    for (int64_t t = tr.T - 1; t >= 0; --t) {
+        double *row = targets + (c * tr.T + t) * E;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int e = lane + 32 * j;
+            if (e < E) {
+                const int64_t d = next[j] < 0 ? (int64_t)cap : min(next[j] - t, (int64_t)cap);
+                row[e] = __ddiv_rn((double)d, dcap);
+            }
+        }
+        for (int k = 0; k < K; ++k) {
+            const int x = __ldg(ids + t * K + k);
+            if ((x & 31) == lane)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if ((x >> 5) == j) next[j] = t;
+        }
+    }
+}
+
+int launch_train_features(const DevTrace &tr, const int32_t *snaps, int64_t max_tiles, double *features,
+                          cudaStream_t s) {
+    if (max_tiles <= 0) return 0;
+    k_train_features<<<(unsigned)max_tiles, 128, 0, s>>>(tr, snaps, features);
+    return 1;
+}
+
+int launch_train_targets(const DevTrace &tr, int distance_cap, double *targets, cudaStream_t s) {
+    if (tr.n_chains == 0) return 0;
+    k_train_targets<<<(unsigned)((tr.n_chains + 3) / 4), 128, 0, s>>>(tr, distance_cap, targets);
+    return 1;
+}
+
 // Ranks of one event's E scores by a warp-wide bitonic sort of (score, id)
 // (P elements per lane, N = 32 P >= E; padding sorts last as +inf):
 // rank = 1 + #{selectable j : s_j < s_e} = 1 + (first sorted position of
@@ -1134,57 +1276,8 @@ __global__ void __launch_bounds__(256, TE ? 4 : 1) k_score_tile(DevTrace tr, con
         // decode-only single sequence: every event updates, no resets, so the
         // tracker state at event i is the snapshot plus in-tile prefix counts
         // (features.py:34-39): thread i sets bit i of occ[e] for its routed e.
-        unsigned long long *occ = (unsigned long long *)s_rank;   // [E] (s_rank reused before ranking)
-        int32_t *pmax = s_flag;                                    // [TILE]
-        const int32_t *sp = snaps + tile * (2 * E + 4);
-        const int32_t u0 = sp[2 * E];
-        for (int e = tid; e < E; e += blockDim.x) occ[e] = 0ull;
-        __syncthreads();
-        const uint8_t *ids = tr.acc + (c * tr.T + ev0) * tr.K;
-        if (tid < nev)
-            for (int k = 0; k < tr.K; ++k) atomicOr(&occ[__ldg(ids + tid * tr.K + k)], 1ull << tid);
-        __syncthreads();
-        if (tid < MCB_TILE_EV) {
-            int32_t m = 0;
-            if (tid < nev) {
-                const unsigned long long upto = tid == 63 ? ~0ull : ((2ull << tid) - 1ull);
-                for (int k = 0; k < tr.K; ++k) {
-                    const int x = __ldg(ids + tid * tr.K + k);
-                    m = max(m, sp[E + x] + __popcll(occ[x] & upto));
-                }
-            }
-            pmax[tid] = m;
-        }
-        __syncthreads();
-        if (tid < 32) {   // inclusive prefix max over the tile's events, then max with the snapshot max_f
-            int32_t a = 2 * tid < MCB_TILE_EV ? pmax[2 * tid] : 0;
-            int32_t b = max(a, 2 * tid + 1 < MCB_TILE_EV ? pmax[2 * tid + 1] : 0);
-            int32_t m0 = 0;
-            for (int e = 0; e < E; ++e) m0 = max(m0, sp[E + e]);
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int32_t t = __shfl_up_sync(FULL_MASK, b, o);
-                if (tid >= o) { a = max(a, t); b = max(b, t); }
-            }
-            if (2 * tid < MCB_TILE_EV) pmax[2 * tid] = max(a, m0);
-            if (2 * tid + 1 < MCB_TILE_EV) pmax[2 * tid + 1] = max(b, m0);
-        }
-        __syncthreads();
-        for (int q = tid; q < MCB_TILE_EV * E; q += blockDim.x) {
-            const int i = q % MCB_TILE_EV, e = q / MCB_TILE_EV;
-            double rv = 0.0, fv = 0.0;
-            if (i < nev) {
-                const unsigned long long seen = occ[e] & (i == 63 ? ~0ull : ((2ull << i) - 1ull));
-                const int32_t f = sp[E + e] + __popcll(seen);
-                const int32_t lastu = seen ? u0 + (63 - __clzll(seen)) + 1 : sp[e];
-                const int32_t u = u0 + i + 1;
-                rv = lastu < 0 ? 0.0 : 1.0 / (double)(u - lastu + 1);
-                const int32_t mf = pmax[i];
-                fv = mf > 0 ? (double)f / (double)mf : 0.0;
-            }
-            bufA[i * ldA + e] = rv;
-            bufA[i * ldA + E + e] = fv;
-        }
+        tile_features_uniform(tr, snaps, tile, c, ev0, nev, E, (unsigned long long *)s_rank, s_flag, bufA, ldA,
+                              true);
     } else if (tid < 32) {
         const int32_t *sp = snaps + tile * (2 * E + 4);
         int32_t last[4], f[4];
@@ -1378,7 +1471,7 @@ int preload_kernels() {
     cudaFuncAttributes a;
     const void *fns[] = {
         (const void *)k_next_use<true>, (const void *)k_next_use<false>, (const void *)k_next_use_blocks,
-        (const void *)k_fold, (const void *)k_prepare_nets, (const void *)k_tile_offsets,
+        (const void *)k_fold, (const void *)k_train_features, (const void *)k_train_targets, (const void *)k_prepare_nets, (const void *)k_tile_offsets,
         (const void *)k_feat_snap, (const void *)k_tile_summary, (const void *)k_snap_scan,
         (const void *)k_score_tile<0, 0>, (const void *)k_score_tile<8, 128>, (const void *)k_score_tile<16, 128>,
         (const void *)k_score_tile<64, 128>, (const void *)k_score_tile<128, 128>,

@@ -51,6 +51,8 @@ struct ReplayParams {
     int64_t solo_min_instances;         // thread-per-instance kernel threshold (E <= 16)
     int64_t chain_lo, chain_hi;         // chains [lo, hi) replayed by this launch (outputs stay global)
     int group_lanes;                    // lane-group size of k_replay (0 = automatic)
+    uint8_t *res_masks;                 // optional [chain][T][E]: resident set at each event start
+                                        // (uniform traces, one policy x capacity; dataset.py masks)
     // segmented speculative replay (mcb_segment.cu); seg.n_seg == 0: whole-chain kernels
     struct Seg {
         int SE;                         // events per segment (multiple of MCB_SNAP_EV)
@@ -115,6 +117,9 @@ int launch_score_prep(const DevTrace &tr, int include_prefill, int32_t *snaps, i
 int launch_score_tiles(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill,
                        uint8_t *ranks, double *scores, const int32_t *snaps, const int64_t *tile_off,
                        int64_t tile_lo, int64_t tile_hi, unsigned long long *uncertain, cudaStream_t s);
+int launch_train_features(const DevTrace &tr, const int32_t *snaps, int64_t max_tiles, double *features,
+                          cudaStream_t s);
+int launch_train_targets(const DevTrace &tr, int distance_cap, double *targets, cudaStream_t s);
 int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill,
                  uint8_t *ranks, double *scores, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,
                  unsigned long long *uncertain, cudaStream_t s);
