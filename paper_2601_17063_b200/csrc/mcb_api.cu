@@ -490,9 +490,10 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     }
     if (Pm.n_pol_launch > 0) {
         // The ML replay needs K3's ranks; it follows K3 on the same stream.
-        // (Pipelining K3 chunks with per-chunk ML replays was measured slower:
-        // the replay's finish walk is latency-bound per instance, so every
-        // chunk pays it again.)
+        // (Pipelining K3 chunks with per-chunk ML replays -- whole replays, or
+        // only the speculation with one finish walk -- was measured slower: the
+        // speculation and the walk are latency-bound per thread / instance, so
+        // every chunk pays their latency again.)
         mark(c, 2, s);
         for (int v = 0; v < 2; ++v) {
             if (!need_ml[v]) continue;

@@ -105,7 +105,8 @@ int seg_warmup_events(int se, int64_t override_nw, int E);
 size_t seg_out_bytes(int64_t n_inst, int n_seg, int E);
 size_t seg_codes_bytes(int64_t n_inst, int64_t Tpad);
 int launch_seg_snapshot(const ReplayParams &p, cudaStream_t s);
-int launch_replay_segmented(const ReplayParams &p, cudaStream_t s);
+enum { SEG_ALL = 0, SEG_SPEC = 1, SEG_FINISH = 2 };   // launch_replay_segmented phases
+int launch_replay_segmented(const ReplayParams &p, cudaStream_t s, int phase = SEG_ALL);
 int preload_segment_kernels();
 int launch_fold(const ReplayParams &p, int num_traces, int64_t *reports, double *latency, cudaStream_t s);
 int launch_prepare_nets(const double *params, int E, int H, int num_nets, double *wt, cudaStream_t s);

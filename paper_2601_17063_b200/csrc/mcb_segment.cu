@@ -694,22 +694,31 @@ __global__ void __launch_bounds__(32) k_seg_finish(const __grid_constant__ Repla
 }
 
 template <int EM>
-static void launch_seg_t(const ReplayParams &p, cudaStream_t s) {
-    const int64_t n_spec = (p.chain_hi - p.chain_lo) * p.seg.n_seg * p.n_cap;
-    const dim3 g((unsigned)((n_spec + 127) / 128), (unsigned)p.n_pol_launch);
-    k_seg_spec<EM><<<g, 128, 0, s>>>(p, 0);
-    if (p.seg.passes > 1) k_seg_spec<EM><<<g, 128, 0, s>>>(p, 1);
-    const int64_t n_fin = (p.chain_hi - p.chain_lo) * p.n_cap;
-    k_seg_finish<EM><<<dim3((unsigned)n_fin, (unsigned)p.n_pol_launch), 32, 0, s>>>(p);
+static int launch_seg_t(const ReplayParams &p, cudaStream_t s, int phase) {
+    int n = 0;
+    if (phase != SEG_FINISH) {
+        const int64_t n_spec = (p.chain_hi - p.chain_lo) * p.seg.n_seg * p.n_cap;
+        const dim3 g((unsigned)((n_spec + 127) / 128), (unsigned)p.n_pol_launch);
+        k_seg_spec<EM><<<g, 128, 0, s>>>(p, 0);
+        ++n;
+        if (p.seg.passes > 1) {
+            k_seg_spec<EM><<<g, 128, 0, s>>>(p, 1);
+            ++n;
+        }
+    }
+    if (phase != SEG_SPEC) {
+        const int64_t n_fin = (p.chain_hi - p.chain_lo) * p.n_cap;
+        k_seg_finish<EM><<<dim3((unsigned)n_fin, (unsigned)p.n_pol_launch), 32, 0, s>>>(p);
+        ++n;
+    }
+    return n;
 }
 
-int launch_replay_segmented_warp(const ReplayParams &p, cudaStream_t s);   // mcb_segment_warp.cu
-int launch_replay_segmented(const ReplayParams &p, cudaStream_t s) {
+int launch_replay_segmented_warp(const ReplayParams &p, cudaStream_t s, int phase);   // mcb_segment_warp.cu
+int launch_replay_segmented(const ReplayParams &p, cudaStream_t s, int phase) {
     if ((p.chain_hi - p.chain_lo) * p.n_pol_launch * p.n_cap == 0) return 0;
-    if (p.tr.E > SEG_MAX_E) return launch_replay_segmented_warp(p, s);
-    if (p.tr.E <= 8) launch_seg_t<8>(p, s);
-    else launch_seg_t<16>(p, s);
-    return 3;
+    if (p.tr.E > SEG_MAX_E) return launch_replay_segmented_warp(p, s, phase);
+    return p.tr.E <= 8 ? launch_seg_t<8>(p, s, phase) : launch_seg_t<16>(p, s, phase);
 }
 
 int preload_segment_kernels() {

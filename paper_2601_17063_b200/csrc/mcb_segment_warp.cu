@@ -557,21 +557,31 @@ __global__ void __launch_bounds__(32) k_wseg_finish(const __grid_constant__ Repl
 }
 
 template <int EPL>
-static void launch_wseg_t(const ReplayParams &p, cudaStream_t s) {
-    const int64_t n_spec = (p.chain_hi - p.chain_lo) * p.seg.n_seg * p.n_cap;   // warps
-    const dim3 g((unsigned)((n_spec + 3) / 4), (unsigned)p.n_pol_launch);
-    k_wseg_spec<EPL><<<g, 128, 0, s>>>(p, 0);
-    if (p.seg.passes > 1) k_wseg_spec<EPL><<<g, 128, 0, s>>>(p, 1);
-    const int64_t n_fin = (p.chain_hi - p.chain_lo) * p.n_cap;
-    k_wseg_finish<EPL><<<dim3((unsigned)n_fin, (unsigned)p.n_pol_launch), 32, 0, s>>>(p);
+static int launch_wseg_t(const ReplayParams &p, cudaStream_t s, int phase) {
+    int n = 0;
+    if (phase != SEG_FINISH) {
+        const int64_t n_spec = (p.chain_hi - p.chain_lo) * p.seg.n_seg * p.n_cap;   // warps
+        const dim3 g((unsigned)((n_spec + 3) / 4), (unsigned)p.n_pol_launch);
+        k_wseg_spec<EPL><<<g, 128, 0, s>>>(p, 0);
+        ++n;
+        if (p.seg.passes > 1) {
+            k_wseg_spec<EPL><<<g, 128, 0, s>>>(p, 1);
+            ++n;
+        }
+    }
+    if (phase != SEG_SPEC) {
+        const int64_t n_fin = (p.chain_hi - p.chain_lo) * p.n_cap;
+        k_wseg_finish<EPL><<<dim3((unsigned)n_fin, (unsigned)p.n_pol_launch), 32, 0, s>>>(p);
+        ++n;
+    }
+    return n;
 }
 
-int launch_replay_segmented_warp(const ReplayParams &p, cudaStream_t s) {
+int launch_replay_segmented_warp(const ReplayParams &p, cudaStream_t s, int phase) {
     if ((p.chain_hi - p.chain_lo) * p.n_pol_launch * p.n_cap == 0) return 0;
-    if (p.tr.E <= 32) launch_wseg_t<1>(p, s);
-    else if (p.tr.E <= 64) launch_wseg_t<2>(p, s);
-    else launch_wseg_t<4>(p, s);
-    return 2;
+    if (p.tr.E <= 32) return launch_wseg_t<1>(p, s, phase);
+    if (p.tr.E <= 64) return launch_wseg_t<2>(p, s, phase);
+    return launch_wseg_t<4>(p, s, phase);
 }
 
 int launch_seg_snapshot_warp(const ReplayParams &p, cudaStream_t s) {
