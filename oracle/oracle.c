@@ -43,7 +43,8 @@
 #define ORC_ERR_NO_EVICTABLE 3
 #define ORC_ERR_NOMEM 6
 
-enum { ORC_LRU = 0, ORC_LFU = 1, ORC_BELADY = 2, ORC_ML = 3, ORC_FIFO = 4 };   /* FIFO: policies.py:152-168 */
+enum { ORC_LRU = 0, ORC_LFU = 1, ORC_BELADY = 2, ORC_ML = 3, ORC_FIFO = 4, ORC_ARC = 5 };
+/* FIFO: policies.py:152-168; ARC: policies.py:217-302 */
 
 #define OUT_HIT 0xFFFFu
 #define OUT_MISS 0xFFFEu
@@ -282,6 +283,98 @@ static inline uint64_t poly16(uint64_t h, uint16_t c) { return h * FNV_PRIME + (
 /* evictions list for _refetch_rate (engine.py:266-297) */
 typedef struct { int64_t pos, decode_index; int victim; } evrec;
 
+/* ---- ARC (policies.py:217-302): T1/T2 resident, B1/B2 ghosts, each an LRU-
+ * ordered list; list membership per expert plus an insertion clock gives the
+ * OrderedDict order (LRU end = smallest clock). */
+enum { ARC_NONE = 0, ARC_T1 = 1, ARC_T2 = 2, ARC_B1 = 3, ARC_B2 = 4 };
+typedef struct {
+    int E, C;
+    uint8_t *lst;
+    int64_t *ord;
+    int64_t clock;
+    int n[5];
+    double p;
+} arc_state;
+
+static void arc_put(arc_state *a, int e, int l) {   /* append at the MRU end of list l */
+    if (a->lst[e]) a->n[a->lst[e]]--;
+    a->lst[e] = (uint8_t)l;
+    a->ord[e] = a->clock++;
+    a->n[l]++;
+}
+static void arc_del(arc_state *a, int e) {
+    if (a->lst[e]) a->n[a->lst[e]]--;
+    a->lst[e] = ARC_NONE;
+}
+/* LRU end of list l, skipping pinned experts when pinned != NULL; -1 if none */
+static int arc_lru(const arc_state *a, int l, const uint8_t *pinned) {
+    int best = -1;
+    for (int e = 0; e < a->E; ++e)
+        if (a->lst[e] == l && !(pinned && pinned[e]) && (best < 0 || a->ord[e] < a->ord[best])) best = e;
+    return best;
+}
+/* _replace (policies.py:236-254): returns the victim or -1 (NoEvictableError) */
+static int arc_replace(arc_state *a, int in_b2, const uint8_t *pinned) {
+    const int use_t1 = a->n[ARC_T1] >= 1 &&
+                       ((double)a->n[ARC_T1] > a->p || (in_b2 && (double)a->n[ARC_T1] == a->p));
+    const int src[2] = {use_t1 ? ARC_T1 : ARC_T2, use_t1 ? ARC_T2 : ARC_T1};
+    for (int i = 0; i < 2; ++i) {
+        const int v = arc_lru(a, src[i], pinned);
+        if (v >= 0) {
+            arc_put(a, v, src[i] == ARC_T1 ? ARC_B1 : ARC_B2);
+            return v;
+        }
+    }
+    return -1;
+}
+/* ARCPolicy.access (policies.py:256-302): *victim = evicted expert or -1;
+ * returns 0, or -1 for NoEvictableError */
+static int arc_access(arc_state *a, int x, const uint8_t *pinned, int *victim) {
+    *victim = -1;
+    if (a->lst[x] == ARC_T1 || a->lst[x] == ARC_T2) {
+        arc_put(a, x, ARC_T2);
+        return 0;
+    }
+    const int c = a->C;
+    const int full = a->n[ARC_T1] + a->n[ARC_T2] >= c;
+    if (a->lst[x] == ARC_B1) {
+        double q = (double)a->n[ARC_B2] / (double)a->n[ARC_B1];
+        if (q < 1.0) q = 1.0;
+        const double np = a->p + q;
+        a->p = (double)c <= np ? (double)c : np;
+        if (full && (*victim = arc_replace(a, 0, pinned)) < 0) return -1;
+        arc_put(a, x, ARC_T2);
+    } else if (a->lst[x] == ARC_B2) {
+        double q = (double)a->n[ARC_B1] / (double)a->n[ARC_B2];
+        if (q < 1.0) q = 1.0;
+        const double np = a->p - q;
+        a->p = 0.0 >= np ? 0.0 : np;
+        if (full && (*victim = arc_replace(a, 1, pinned)) < 0) return -1;
+        arc_put(a, x, ARC_T2);
+    } else {
+        const int l1 = a->n[ARC_T1] + a->n[ARC_B1];
+        if (l1 == c) {
+            if (a->n[ARC_T1] < c) {
+                arc_del(a, arc_lru(a, ARC_B1, NULL));
+                if (a->n[ARC_T1] + a->n[ARC_T2] >= c && (*victim = arc_replace(a, 0, pinned)) < 0) return -1;
+            } else {
+                const int v = arc_lru(a, ARC_T1, pinned);   /* T1's LRU, no ghost entry */
+                if (v < 0) return -1;
+                arc_del(a, v);
+                *victim = v;
+            }
+        } else if (l1 < c) {
+            const int total = l1 + a->n[ARC_T2] + a->n[ARC_B2];
+            if (total >= c) {
+                if (total == 2 * c) arc_del(a, arc_lru(a, ARC_B2, NULL));
+                if (a->n[ARC_T1] + a->n[ARC_T2] >= c && (*victim = arc_replace(a, 0, pinned)) < 0) return -1;
+            }
+        }
+        arc_put(a, x, ARC_T1);
+    }
+    return 0;
+}
+
 static int replay_layer(const orc_layer *ly, const orc_cfg *cfg, int64_t *cnt, double *lat,
                         uint16_t *outcomes, uint64_t *hash /* [2]: fnv, poly */) {
     const int E = cfg->E, C = cfg->capacity;
@@ -301,6 +394,7 @@ static int replay_layer(const orc_layer *ly, const orc_cfg *cfg, int64_t *cnt, d
     evrec *evs = (evrec *)malloc((size_t)ev_cap * sizeof(evrec));
     orc_index ix = {0};
     int have_ix = 0;
+    arc_state arc = {E, C, NULL, NULL, 0, {0, 0, 0, 0, 0}, 0.0};
     if (!res || !pinned || !seen || !stamp || !freq || !rec || !fr || !x || !scores || !h1 || !h2 || !evs) {
         rc = ORC_ERR_NOMEM; goto done;
     }
@@ -310,6 +404,11 @@ static int replay_layer(const orc_layer *ly, const orc_cfg *cfg, int64_t *cnt, d
 
     int n_res = 0;
     int64_t fifo_clock = 0;
+    if (cfg->policy == ORC_ARC) {
+        arc.lst = (uint8_t *)calloc((size_t)E, 1);
+        arc.ord = (int64_t *)calloc((size_t)E, sizeof(int64_t));
+        if (!arc.lst || !arc.ord) { rc = ORC_ERR_NOMEM; goto done; }
+    }
     uint64_t h = FNV_OFF, hp = 0;
     double dlat = 0.0, plat = 0.0;
     for (int k = 0; k < C_N; ++k) cnt[k] = 0;
@@ -345,7 +444,15 @@ static int replay_layer(const orc_layer *ly, const orc_cfg *cfg, int64_t *cnt, d
             const int xe = st->acc[j];
             int hit = res[xe];
             int victim = -1;
-            if (hit) {
+            if (cfg->policy == ORC_ARC) {
+                /* ARC overrides access() entirely; the resident set is T1 u T2 */
+                if (arc_access(&arc, xe, decode ? pinned : NULL, &victim) != 0) { rc = ORC_ERR_NO_EVICTABLE; goto done; }
+                if (!hit) {
+                    if (victim >= 0) { res[victim] = 0; n_res--; }
+                    res[xe] = 1;
+                    n_res++;
+                }
+            } else if (hit) {
                 if (cfg->policy == ORC_LRU) stamp[xe] = pos;
                 if (cfg->policy == ORC_LFU) freq[xe] += 1;
             } else {
@@ -443,6 +550,7 @@ done:
     if (have_ix) index_free(&ix);
     free(res); free(pinned); free(seen); free(stamp); free(freq); free(rec); free(fr);
     free(x); free(scores); free(h1); free(h2); free(evs);
+    free(arc.lst); free(arc.ord);
     return rc;
 }
 

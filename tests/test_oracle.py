@@ -116,3 +116,9 @@ def test_oracle_fifo_cases():
     """FIFO (policies.py:152-168) on reference-made fixtures (make_fifo_golden.py)."""
     for case in load("fifo_cases.json.gz")["cases"]:
         _check_case(case)
+
+
+def test_oracle_arc_cases():
+    """ARC (policies.py:217-302) on reference-made fixtures (make_arc_golden.py)."""
+    for case in load("arc_cases.json.gz")["cases"]:
+        _check_case(case)
