@@ -20,9 +20,9 @@
  * context owns only its device scratch.
  *
  * Supported: num_experts <= 128, top_k <= num_experts, chains of < 2^32
- * accesses, policies LRU / LFU / Belady / ML (the north star's four) and FIFO.
- * ARC and LeCaR (policies.py:217-395) are rejected with MCB_ERR_UNSUPPORTED
- * rather than falling back to a CPU path.
+ * accesses, policies LRU / LFU / Belady / ML (the north star's four), FIFO
+ * and ARC.  LeCaR (policies.py:305-395) is rejected with
+ * MCB_ERR_UNSUPPORTED rather than falling back to a CPU path.
  */
 #ifndef MCB_H_
 #define MCB_H_
@@ -55,7 +55,8 @@ typedef enum {
     MCB_BELADY = 2,            /* policies.py:200-214 */
     MCB_ML = 3,                /* mlpolicy.py:33-65, include_prefill=True */
     MCB_ML_NO_PREFILL = 4,     /* mlpolicy.py, {"name": "ml", "include_prefill": False} */
-    MCB_FIFO = 5               /* policies.py:152-168 (whole-chain replay kernels only) */
+    MCB_FIFO = 5,              /* policies.py:152-168 (whole-chain replay kernels only) */
+    MCB_ARC = 6                /* policies.py:217-302 (whole-chain replay kernels only) */
 } mcb_policy;
 
 /* ---- per-(trace, policy, capacity) report slots ---- */

@@ -23,7 +23,7 @@ MCB_ERR_UNSUPPORTED = 5
 MCB_ERR_NOMEM = 6
 MCB_ERR_SHAPE = 7
 
-MCB_LRU, MCB_LFU, MCB_BELADY, MCB_ML, MCB_ML_NO_PREFILL, MCB_FIFO = range(6)
+MCB_LRU, MCB_LFU, MCB_BELADY, MCB_ML, MCB_ML_NO_PREFILL, MCB_FIFO, MCB_ARC = range(7)
 MCB_TUNE_SOLO_MIN = 0
 MCB_TUNE_SEG_EV = 1
 MCB_TUNE_SEG_NW = 2

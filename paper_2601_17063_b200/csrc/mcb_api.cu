@@ -367,7 +367,7 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     bool need_next = false, need_ml[2] = {false, false};
     for (int i = 0; i < n_pol; ++i) {
         switch (pols[i]) {
-            case MCB_LRU: case MCB_LFU: case MCB_FIFO: break;
+            case MCB_LRU: case MCB_LFU: case MCB_FIFO: case MCB_ARC: break;
             case MCB_BELADY: need_next = true; break;
             case MCB_ML: need_ml[0] = true; break;
             case MCB_ML_NO_PREFILL: need_ml[1] = true; break;
@@ -481,7 +481,8 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         CUDA_TRY(cudaStreamWaitEvent(c->side, c->fork, 0));
     }
     for (int i = 0; i < Pn.n_pol_launch; ++i)
-        if (pols[Pn.pol_map[i]] == MCB_FIFO) Pn.seg.n_seg = 0;   // arrival keys depend on the cache state
+        if (pols[Pn.pol_map[i]] == MCB_FIFO || pols[Pn.pol_map[i]] == MCB_ARC)
+            Pn.seg.n_seg = 0;   // their eviction order depends on the cache state
     if (Pn.n_pol_launch > 0) {
         mark(c, 4, sn);
         launched += seg_eligible(Pn) ? launch_replay_segmented(Pn, sn) : launch_replay(Pn, sn);

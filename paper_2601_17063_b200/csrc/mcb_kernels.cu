@@ -167,6 +167,137 @@ __device__ __forceinline__ uint32_t get_slot(const uint32_t (&a)[EPL], int slot)
     return v;
 }
 
+// ARC (policies.py:217-302) for the lane-group replay: per lane the T1 / T2 /
+// B1 / B2 membership of its EPL experts and their insertion clocks; list
+// sizes, the clock and the adaptation target p are group-uniform.  A list's
+// LRU end is the smallest clock (redux.sync min + ballot; clocks are unique).
+template <int EPL>
+struct WArc {
+    uint32_t t1, t2, b1, b2;
+    uint32_t ord[EPL];
+    uint32_t clock;
+    int n1, n2, nb1, nb2;
+    double p;
+};
+
+template <int EPL>
+__device__ __forceinline__ void warc_lru(const WArc<EPL> &a, uint32_t mask, unsigned gmask, int gbase, int &vlane,
+                                         int &vs) {
+    uint32_t lk = KEY_SENT;
+    int ls = 0;
+#pragma unroll
+    for (int s = 0; s < EPL; ++s)
+        if (((mask >> s) & 1u) && a.ord[s] < lk) { lk = a.ord[s]; ls = s; }
+    const uint32_t m = __reduce_min_sync(gmask, lk);
+    if (m == KEY_SENT) { vlane = -1; vs = 0; return; }
+    const unsigned b = __ballot_sync(gmask, lk == m) & gmask;
+    const int wl = __ffs(b) - 1;
+    vs = __shfl_sync(gmask, ls, wl);
+    vlane = wl - gbase;
+}
+
+// move expert (vlane, vs) to list which (0 T1, 1 T2, 2 B1, 3 B2, 4 remove)
+template <int EPL>
+__device__ __forceinline__ void warc_put(WArc<EPL> &a, int vlane, int vs, int which, unsigned gmask, int gbase,
+                                         int glane) {
+    int old = 0;
+    if (glane == vlane) {
+        const uint32_t b = 1u << vs;
+        old = (a.t1 & b) ? 1 : (a.t2 & b) ? 2 : (a.b1 & b) ? 3 : (a.b2 & b) ? 4 : 0;
+        a.t1 &= ~b;
+        a.t2 &= ~b;
+        a.b1 &= ~b;
+        a.b2 &= ~b;
+        if (which == 0) a.t1 |= b;
+        if (which == 1) a.t2 |= b;
+        if (which == 2) a.b1 |= b;
+        if (which == 3) a.b2 |= b;
+        if (which != 4) set_slot<EPL>(a.ord, vs, a.clock);
+    }
+    old = __shfl_sync(gmask, old, gbase + vlane);
+    a.n1 -= old == 1; a.n2 -= old == 2; a.nb1 -= old == 3; a.nb2 -= old == 4;
+    a.n1 += which == 0; a.n2 += which == 1; a.nb1 += which == 2; a.nb2 += which == 3;
+    if (which != 4) ++a.clock;
+}
+
+template <int EPL>
+__device__ __forceinline__ void warc_replace(WArc<EPL> &a, bool in_b2, uint32_t pin, unsigned gmask, int gbase,
+                                             int glane, int &vl, int &vs) {
+    const bool use_t1 = a.n1 >= 1 && ((double)a.n1 > a.p || (in_b2 && (double)a.n1 == a.p));
+    warc_lru<EPL>(a, (use_t1 ? a.t1 : a.t2) & ~pin, gmask, gbase, vl, vs);
+    bool from_t1 = use_t1;
+    if (vl < 0) {
+        warc_lru<EPL>(a, (use_t1 ? a.t2 : a.t1) & ~pin, gmask, gbase, vl, vs);
+        from_t1 = !use_t1;
+    }
+    if (vl >= 0) warc_put<EPL>(a, vl, vs, from_t1 ? 2 : 3, gmask, gbase, glane);
+}
+
+// miss path of ARCPolicy.access (policies.py:264-302): victim (vl, vs) or
+// vl = -1; none_left when every candidate is pinned
+template <int EPL>
+__device__ __forceinline__ void warc_miss(WArc<EPL> &a, int owner, int slot, uint32_t pin, uint32_t C,
+                                          unsigned gmask, int gbase, int glane, int &vl, int &vs, bool &none_left) {
+    const uint32_t bit = 1u << slot;
+    const bool mine = glane == owner;
+    const bool in_b1 = (__ballot_sync(gmask, mine && (a.b1 & bit)) & gmask) != 0u;
+    const bool in_b2 = (__ballot_sync(gmask, mine && (a.b2 & bit)) & gmask) != 0u;
+    const int c = (int)C;
+    const bool full = a.n1 + a.n2 >= c;
+    vl = -1;
+    vs = 0;
+    none_left = false;
+    if (in_b1 || in_b2) {
+        if (in_b1) {
+            double q = (double)a.nb2 / (double)a.nb1;
+            q = q < 1.0 ? 1.0 : q;
+            const double np = a.p + q;
+            a.p = (double)c <= np ? (double)c : np;
+        } else {
+            double q = (double)a.nb1 / (double)a.nb2;
+            q = q < 1.0 ? 1.0 : q;
+            const double np = a.p - q;
+            a.p = 0.0 >= np ? 0.0 : np;
+        }
+        if (full) {
+            warc_replace<EPL>(a, in_b2, pin, gmask, gbase, glane, vl, vs);
+            none_left = vl < 0;
+        }
+        warc_put<EPL>(a, owner, slot, 1, gmask, gbase, glane);
+        return;
+    }
+    const int l1 = a.n1 + a.nb1;
+    if (l1 == c) {
+        if (a.n1 < c) {
+            int bl, bs;
+            warc_lru<EPL>(a, a.b1, gmask, gbase, bl, bs);
+            warc_put<EPL>(a, bl, bs, 4, gmask, gbase, glane);
+            if (a.n1 + a.n2 >= c) {
+                warc_replace<EPL>(a, false, pin, gmask, gbase, glane, vl, vs);
+                none_left = vl < 0;
+            }
+        } else {   // B1 empty, T1 full: drop T1's LRU without a ghost entry
+            warc_lru<EPL>(a, a.t1 & ~pin, gmask, gbase, vl, vs);
+            none_left = vl < 0;
+            if (vl >= 0) warc_put<EPL>(a, vl, vs, 4, gmask, gbase, glane);
+        }
+    } else if (l1 < c) {
+        const int total = l1 + a.n2 + a.nb2;
+        if (total >= c) {
+            if (total == 2 * c) {
+                int bl, bs;
+                warc_lru<EPL>(a, a.b2, gmask, gbase, bl, bs);
+                warc_put<EPL>(a, bl, bs, 4, gmask, gbase, glane);
+            }
+            if (a.n1 + a.n2 >= c) {
+                warc_replace<EPL>(a, false, pin, gmask, gbase, glane, vl, vs);
+                none_left = vl < 0;
+            }
+        }
+    }
+    warc_put<EPL>(a, owner, slot, 0, gmask, gbase, glane);
+}
+
 template <int G, int EPL, int POL, bool UNIFORM>
 __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t chain, int pol_i, int cap_i,
                                                 int64_t inst, int ml_variant) {
@@ -180,6 +311,15 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
 
     uint32_t res = 0, pin = 0, seen = 0;
     uint32_t key[EPL], pend[EPL];
+    WArc<EPL> arc;
+    if (POL == POL_ARC) {
+        arc.t1 = arc.t2 = arc.b1 = arc.b2 = 0u;
+#pragma unroll
+        for (int s = 0; s < EPL; ++s) arc.ord[s] = 0u;
+        arc.clock = 0u;
+        arc.n1 = arc.n2 = arc.nb1 = arc.nb2 = 0;
+        arc.p = 0.0;
+    }
 #pragma unroll
     for (int s = 0; s < EPL; ++s) { key[s] = 0; pend[s] = 0; }
     uint32_t count = 0, ph = 0, pm = 0, dh = 0, dm = 0, nev = 0, comp = 0, refc = 0;
@@ -254,10 +394,25 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
             uint32_t code = MCB_OUT_HIT;
             if (hit) {
                 if (decode) ++dh; else ++ph;
+                if (POL == POL_ARC) warc_put<EPL>(arc, owner, slot, 1, gmask, gbase, glane);   // to T2's MRU end
             } else {
                 if (decode) ++dm; else ++pm;
                 ++step_miss;
-                if (count >= C) {
+                if (POL == POL_ARC) {
+                    int vl, vs;
+                    bool none_left;
+                    warc_miss<EPL>(arc, owner, slot, pin, C, gmask, gbase, glane, vl, vs, none_left);
+                    if (none_left) { status = MCB_ERR_NO_EVICTABLE; break; }
+                    res = arc.t1 | arc.t2;
+                    count = (uint32_t)(arc.n1 + arc.n2);
+                    if (vl >= 0) {
+                        if (glane == vl) set_slot<EPL>(pend, vs, dec + 1u);
+                        code = (uint32_t)(vl * EPL + vs);
+                        ++nev;
+                    } else {
+                        code = MCB_OUT_MISS;
+                    }
+                } else if (count >= C) {
                     const uint32_t cand = res & ~pin;
                     uint32_t lk = KEY_SENT;
                     int ls = 0;
@@ -348,6 +503,7 @@ __global__ void __launch_bounds__(128) k_replay(const __grid_constant__ ReplayPa
         case MCB_BELADY: replay_instance<G, EPL, POL_BELADY, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
         case MCB_ML: replay_instance<G, EPL, POL_ML, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
         case MCB_FIFO: replay_instance<G, EPL, POL_FIFO, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
+        case MCB_ARC: replay_instance<G, EPL, POL_ARC, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
         default: replay_instance<G, EPL, POL_ML, UNIFORM>(P, chain, pol_i, cap_i, inst, 1); break;
     }
 }
@@ -375,6 +531,8 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
     for (int s = 0; s < EM; ++s) pk[s] = (uint32_t)s;
     SState<WMAX> S;
     sstate_clear(S);
+    ArcState<EM> arc;
+    if (POL == POL_ARC) arc_clear<EM>(arc);
     uint32_t pin = 0, seen = 0, valid = (1u << E) - 1u;
     uint32_t ph = 0, pm = 0, dh = 0, dm = 0, comp = 0;
     SCount n = {0u, 0u, 0u};
@@ -430,8 +588,13 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
             const uint32_t np = (POL == POL_BELADY) ? nx.get(A) : 0u;
             solo_key_update<EM, POL>(pk, x, bit, pos, np);
             uint32_t miss;
-            const uint32_t code = sstep<EM, WMAX>(S, pk, bit, pin, valid, C, n, stuck, miss);
-            if (POL == POL_FIFO) solo_fifo_insert<EM>(pk, x, bit, pos, miss);
+            uint32_t code;
+            if (POL == POL_ARC) {
+                code = sstep_arc<EM, WMAX>(S, arc, x, bit, decode ? pin : 0u, C, n, stuck, miss);
+            } else {
+                code = sstep<EM, WMAX>(S, pk, bit, pin, valid, C, n, stuck, miss);
+                if (POL == POL_FIFO) solo_fifo_insert<EM>(pk, x, bit, pos, miss);
+            }
             step_miss += miss;
             if (decode) { dh += 1u - miss; dm += miss; }
             else { ph += 1u - miss; pm += miss; }
@@ -483,6 +646,7 @@ __global__ void __launch_bounds__(128) k_replay_solo(const __grid_constant__ Rep
         case MCB_BELADY: solo_instance<EM, POL_BELADY, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
         case MCB_ML: solo_instance<EM, POL_ML, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
         case MCB_FIFO: solo_instance<EM, POL_FIFO, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
+        case MCB_ARC: solo_instance<EM, POL_ARC, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
         default: solo_instance<EM, POL_ML, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 1); break;
     }
 }

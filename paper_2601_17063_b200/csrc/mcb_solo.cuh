@@ -16,7 +16,7 @@
 
 #include "mcb_kernels.cuh"
 
-enum { POL_LRU = 0, POL_LFU = 1, POL_BELADY = 2, POL_ML = 3, POL_FIFO = 4 };
+enum { POL_LRU = 0, POL_LFU = 1, POL_BELADY = 2, POL_ML = 3, POL_FIFO = 4, POL_ARC = 5 };
 
 #define SOLO_WMAX 7                       // largest refetch window of the solo kernels
 #define FULL_MASK_W 0xFFFFFFFFu
@@ -242,7 +242,7 @@ __device__ __forceinline__ void solo_key_update(uint32_t (&pk)[EM], uint32_t x, 
         nk = cur + (1u << SH);
     }
     if (POL == POL_BELADY) nk = ((np == MCB_NEXT_INF ? 0u : KMAX - np) << SH) | x;   // farthest next use first
-    if (POL == POL_FIFO) return;   // FIFO keys change at insertion only (solo_fifo_insert)
+    if (POL == POL_FIFO || POL == POL_ARC) return;   // state-dependent order (solo_fifo_insert / ArcState)
     if (POL != POL_ML) {
 #pragma unroll
         for (int s = 0; s < EM; ++s) pk[s] = ((bit >> s) & 1u) ? nk : pk[s];
@@ -259,6 +259,133 @@ __device__ __forceinline__ void solo_fifo_insert(uint32_t (&pk)[EM], uint32_t x,
     const uint32_t nk = (pos << Solo<EM>::SH) | x;
 #pragma unroll
     for (int s = 0; s < EM; ++s) pk[s] = (miss && ((bit >> s) & 1u)) ? nk : pk[s];
+}
+
+// ARC (policies.py:217-302) for num_experts <= 16: the four OrderedDicts as
+// expert masks (T1, T2 resident; B1, B2 ghosts) plus each expert's insertion
+// clock, so a list's LRU end is its smallest clock; the adaptation target p
+// is a float64 updated with the reference's operations.
+template <int EM>
+struct ArcState {
+    uint32_t t1, t2, b1, b2;
+    uint32_t ord[EM];
+    uint32_t clock;
+    double p;
+};
+
+template <int EM>
+__device__ __forceinline__ void arc_clear(ArcState<EM> &a) {
+    a.t1 = a.t2 = a.b1 = a.b2 = 0u;
+#pragma unroll
+    for (int s = 0; s < EM; ++s) a.ord[s] = 0u;
+    a.clock = 0u;
+    a.p = 0.0;
+}
+
+// LRU end (smallest clock) of the experts in mask; EM if empty
+template <int EM>
+__device__ __forceinline__ uint32_t arc_lru(const ArcState<EM> &a, uint32_t mask) {
+    constexpr int SH = Solo<EM>::SH;
+    uint32_t t = ~0u;
+#pragma unroll
+    for (int s = 0; s < EM; ++s) t = ((mask >> s) & 1u) ? min(t, (a.ord[s] << SH) | (uint32_t)s) : t;
+    return t == ~0u ? (uint32_t)EM : (t & (uint32_t)(EM - 1));
+}
+
+// move expert v to the MRU end of the list `which` (0 T1, 1 T2, 2 B1, 3 B2); 4 = remove
+template <int EM>
+__device__ __forceinline__ void arc_put(ArcState<EM> &a, uint32_t v, int which) {
+    const uint32_t b = 1u << v;
+    a.t1 &= ~b;
+    a.t2 &= ~b;
+    a.b1 &= ~b;
+    a.b2 &= ~b;
+    if (which == 0) a.t1 |= b;
+    if (which == 1) a.t2 |= b;
+    if (which == 2) a.b1 |= b;
+    if (which == 3) a.b2 |= b;
+    if (which == 4) return;   // removal: no new position
+#pragma unroll
+    for (int s = 0; s < EM; ++s) a.ord[s] = (s == (int)v) ? a.clock : a.ord[s];
+    ++a.clock;
+}
+
+// _replace (policies.py:236-254): victim, or EM when every resident is pinned
+template <int EM>
+__device__ __forceinline__ uint32_t arc_replace(ArcState<EM> &a, bool in_b2, uint32_t pin) {
+    const int n1 = __popc(a.t1);
+    const bool use_t1 = n1 >= 1 && ((double)n1 > a.p || (in_b2 && (double)n1 == a.p));
+    uint32_t v = arc_lru<EM>(a, (use_t1 ? a.t1 : a.t2) & ~pin);
+    bool from_t1 = use_t1;
+    if (v == (uint32_t)EM) {
+        v = arc_lru<EM>(a, (use_t1 ? a.t2 : a.t1) & ~pin);
+        from_t1 = !use_t1;
+    }
+    if (v != (uint32_t)EM) arc_put<EM>(a, v, from_t1 ? 2 : 3);
+    return v;
+}
+
+// ARCPolicy.access (policies.py:256-302) + the engine's accounting on S
+// (resident mask, refetch ring) exactly as sstep: returns the outcome code.
+template <int EM, int WMAX>
+__device__ __forceinline__ uint32_t sstep_arc(SState<WMAX> &S, ArcState<EM> &a, uint32_t x, uint32_t bit,
+                                              uint32_t pin, uint32_t C, SCount &n, bool &stuck, uint32_t &miss_out) {
+    const bool hit = ((a.t1 | a.t2) & bit) != 0u;
+    miss_out = hit ? 0u : 1u;
+    if (hit) {
+        arc_put<EM>(a, x, 1);
+        return MCB_OUT_HIT;
+    }
+    uint32_t v = (uint32_t)EM;   // victim (EM: none)
+    bool none_left = false;
+    const bool full = (uint32_t)__popc(a.t1 | a.t2) >= C;
+    if (a.b1 & bit) {
+        double q = (double)__popc(a.b2) / (double)__popc(a.b1);
+        q = q < 1.0 ? 1.0 : q;
+        const double np = a.p + q;
+        a.p = (double)C <= np ? (double)C : np;
+        if (full) { v = arc_replace<EM>(a, false, pin); none_left = v == (uint32_t)EM; }
+        arc_put<EM>(a, x, 1);
+    } else if (a.b2 & bit) {
+        double q = (double)__popc(a.b1) / (double)__popc(a.b2);
+        q = q < 1.0 ? 1.0 : q;
+        const double np = a.p - q;
+        a.p = 0.0 >= np ? 0.0 : np;
+        if (full) { v = arc_replace<EM>(a, true, pin); none_left = v == (uint32_t)EM; }
+        arc_put<EM>(a, x, 1);
+    } else {
+        const uint32_t n1 = (uint32_t)__popc(a.t1);
+        const uint32_t l1 = n1 + (uint32_t)__popc(a.b1);
+        if (l1 == C) {
+            if (n1 < C) {
+                arc_put<EM>(a, arc_lru<EM>(a, a.b1), 4);
+                if ((uint32_t)__popc(a.t1 | a.t2) >= C) { v = arc_replace<EM>(a, false, pin); none_left = v == (uint32_t)EM; }
+            } else {   // B1 empty, T1 full: drop T1's LRU without a ghost entry
+                v = arc_lru<EM>(a, a.t1 & ~pin);
+                none_left = v == (uint32_t)EM;
+                if (!none_left) arc_put<EM>(a, v, 4);
+            }
+        } else if (l1 < C) {
+            const uint32_t total = l1 + (uint32_t)__popc(a.t2) + (uint32_t)__popc(a.b2);
+            if (total >= C) {
+                if (total == 2 * C) arc_put<EM>(a, arc_lru<EM>(a, a.b2), 4);
+                if ((uint32_t)__popc(a.t1 | a.t2) >= C) { v = arc_replace<EM>(a, false, pin); none_left = v == (uint32_t)EM; }
+            }
+        }
+        arc_put<EM>(a, x, 0);
+    }
+    stuck |= none_left;
+    const bool evict = v != (uint32_t)EM;
+    const uint32_t vbit = evict ? (1u << v) : 0u;
+    S.res = a.t1 | a.t2;
+    ++n.misses;
+    n.nev += evict ? 1u : 0u;
+    n.refc += (bit & S.ring_or) ? 1u : 0u;
+    S.ring_or = (S.ring_or & ~bit) | vbit;
+#pragma unroll
+    for (int s = 0; s <= WMAX; ++s) S.ring[s] &= ~bit;
+    S.ring[0] |= vbit;
+    return evict ? v : MCB_OUT_MISS;
 }
 
 // ML: packed keys and the selectable mask from one event's rank row

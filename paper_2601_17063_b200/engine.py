@@ -124,7 +124,8 @@ class SimRun:
 
 
 POLICY_NAMES = ("lru", "lfu", "fifo", "arc", "lecar", "belady", "ml")
-_CODES = {"lru": _lib.MCB_LRU, "lfu": _lib.MCB_LFU, "belady": _lib.MCB_BELADY, "fifo": _lib.MCB_FIFO}
+_CODES = {"lru": _lib.MCB_LRU, "lfu": _lib.MCB_LFU, "belady": _lib.MCB_BELADY, "fifo": _lib.MCB_FIFO,
+          "arc": _lib.MCB_ARC}
 
 
 class EnginePolicy:
@@ -149,9 +150,9 @@ def policy_factory(spec: Union[str, dict], nets=None):
     name = params.pop("name", None)
     if name not in POLICY_NAMES:
         raise SimulationError(f"unknown policy {name!r}; expected one of {POLICY_NAMES}")
-    if name in ("arc", "lecar"):
+    if name == "lecar":
         raise SimulationError(f"policy {name!r} is unsupported by the B200 engine "
-                              "(the engine replays lru, lfu, belady, ml and fifo)")
+                              "(the engine replays lru, lfu, belady, ml, fifo and arc)")
     if name == "ml":
         if nets is None:
             raise SimulationError("ml policy requires trained eviction nets")

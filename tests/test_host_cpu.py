@@ -101,8 +101,9 @@ def test_policy_factory_and_errors_without_gpu():
         mcb.policy_factory("nope")
     with pytest.raises(mcb.SimulationError):
         mcb.policy_factory("ml")                       # needs nets (engine.py:184-185)
+    assert mcb.policy_factory("arc")[1].code == _lib.MCB_ARC
     with pytest.raises(mcb.SimulationError):
-        mcb.policy_factory("arc")                      # outside the B200 engine, no CPU fallback
+        mcb.policy_factory("lecar")                    # outside the B200 engine, no CPU fallback
     name, ep = mcb.policy_factory({"name": "ml", "include_prefill": False}, nets=mcb.EvictionNet(4))
     assert name == "ml" and ep.code == _lib.MCB_ML_NO_PREFILL
     t = tr([AccessEvent(0, D, 0, 0, (0, 1))])

@@ -33,7 +33,8 @@ def code_of(spec):
     name = policy_name(spec)
     if name == "ml":
         return _lib.MCB_ML if include_prefill(spec) else _lib.MCB_ML_NO_PREFILL
-    return {"lru": _lib.MCB_LRU, "lfu": _lib.MCB_LFU, "belady": _lib.MCB_BELADY, "fifo": _lib.MCB_FIFO}[name]
+    return {"lru": _lib.MCB_LRU, "lfu": _lib.MCB_LFU, "belady": _lib.MCB_BELADY, "fifo": _lib.MCB_FIFO,
+            "arc": _lib.MCB_ARC}[name]
 
 
 def check_case(case, decisions=True):
@@ -87,6 +88,13 @@ def test_small_cases(part, kernel_variant):
 def test_fifo_cases(part, kernel_variant):
     """FIFO (policies.py:152-168) against reference-made fixtures, decisions included."""
     for case in load("fifo_cases.json.gz")["cases"][part::2]:
+        check_case(case)
+
+
+@pytest.mark.parametrize("part", range(2))
+def test_arc_cases(part, kernel_variant):
+    """ARC (policies.py:217-302) against reference-made fixtures, decisions included."""
+    for case in load("arc_cases.json.gz")["cases"][part::2]:
         check_case(case)
 
 
