@@ -56,7 +56,8 @@ typedef enum {
     MCB_ML = 3,                /* mlpolicy.py:33-65, include_prefill=True */
     MCB_ML_NO_PREFILL = 4,     /* mlpolicy.py, {"name": "ml", "include_prefill": False} */
     MCB_FIFO = 5,              /* policies.py:152-168 (whole-chain replay kernels only) */
-    MCB_ARC = 6                /* policies.py:217-302 (whole-chain replay kernels only) */
+    MCB_ARC = 6,               /* policies.py:217-302 (whole-chain replay kernels only) */
+    MCB_LECAR = 7              /* policies.py:305-395, parameters from mcb_set_lecar (whole-chain kernels only) */
 } mcb_policy;
 
 /* ---- per-(trace, policy, capacity) report slots ---- */
@@ -192,6 +193,19 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
  * side stream), so mcb_last_timings attributes time to each stage alone. */
 #define MCB_TUNE_SERIAL 5
 int mcb_set_tuning(mcb_ctx *ctx, int32_t knob, int64_t value);
+/* LeCaR parameters used by the MCB_LECAR cells of later mcb_replay calls on
+ * this context (LeCaRPolicy.__init__, policies.py:333-349; defaults 0.45,
+ * 0.005, 0).  Every per-layer policy object of the reference seeds its own
+ * random.Random(seed), so each cache instance consumes the same stream of
+ * random() draws, one per eviction; the engine materialises that stream
+ * (CPython's MT19937 seeding and genrand_res53) and the per-capacity
+ * regret factors exp(learning_rate * discount**elapsed) with the host libm,
+ * so the device only multiplies, adds and divides.  seed >= 0 (an int seed;
+ * negative values seed like their absolute value in CPython). */
+int mcb_set_lecar(mcb_ctx *ctx, double learning_rate, double discount_base, int64_t seed);
+/* Host-only: the first n values of CPython's random.Random(seed).random()
+ * (the stream mcb_set_lecar's seed selects), into out[n]. */
+int mcb_lecar_random(int64_t seed, int64_t n, double *out);
 int mcb_last_timings(mcb_ctx *ctx, float *ms, int32_t n);
 
 /* ---- host-side trace validation + packing (trace.py:57-141, replay.py:44-81) ----

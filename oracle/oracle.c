@@ -13,6 +13,7 @@
  *                                                positions + bisect_right)
  *   CachePolicy.access       policies.py:95-107
  *   LRU / LFU / Belady       policies.py:132-149, 171-214
+ *   FIFO / ARC / LeCaR       policies.py:152-168, 217-302, 305-395
  *   FeatureTracker           features.py:34-52
  *   EvictionNet.forward      net.py:43-53, 88-105 (float64)
  *   ml_policy_evict          mlpolicy.py:15-26
@@ -43,8 +44,23 @@
 #define ORC_ERR_NO_EVICTABLE 3
 #define ORC_ERR_NOMEM 6
 
-enum { ORC_LRU = 0, ORC_LFU = 1, ORC_BELADY = 2, ORC_ML = 3, ORC_FIFO = 4, ORC_ARC = 5 };
-/* FIFO: policies.py:152-168; ARC: policies.py:217-302 */
+enum { ORC_LRU = 0, ORC_LFU = 1, ORC_BELADY = 2, ORC_ML = 3, ORC_FIFO = 4, ORC_ARC = 5, ORC_LECAR = 6 };
+/* FIFO: policies.py:152-168; ARC: policies.py:217-302; LeCaR: policies.py:305-395 */
+
+/* LeCaR parameters (LeCaRPolicy.__init__, policies.py:333-349) and the
+ * random.Random(seed).random() stream every per-layer instance draws from
+ * (one draw per eviction; produced by the caller with Python's own random
+ * module).  Set with orc_set_lecar before a replay. */
+static double g_lecar_lr = 0.45, g_lecar_base = 0.005;
+static const double *g_lecar_u = NULL;
+static int64_t g_lecar_n = 0;
+
+void orc_set_lecar(double learning_rate, double discount_base, const double *u, int64_t n) {
+    g_lecar_lr = learning_rate;
+    g_lecar_base = discount_base;
+    g_lecar_u = u;
+    g_lecar_n = n;
+}
 
 #define OUT_HIT 0xFFFFu
 #define OUT_MISS 0xFFFEu
@@ -395,7 +411,10 @@ static int replay_layer(const orc_layer *ly, const orc_cfg *cfg, int64_t *cnt, d
     orc_index ix = {0};
     int have_ix = 0;
     arc_state arc = {E, C, NULL, NULL, 0, {0, 0, 0, 0, 0}, 0.0};
-    if (!res || !pinned || !seen || !stamp || !freq || !rec || !fr || !x || !scores || !h1 || !h2 || !evs) {
+    uint8_t *ghost = (uint8_t *)calloc((size_t)E, 1);
+    int64_t *gpos = (int64_t *)calloc((size_t)E, sizeof(int64_t));
+    if (!res || !pinned || !seen || !stamp || !freq || !rec || !fr || !x || !scores || !h1 || !h2 || !evs || !ghost ||
+        !gpos) {
         rc = ORC_ERR_NOMEM; goto done;
     }
     if (index_build(&ix, ly, E) != 0) { rc = ORC_ERR_NOMEM; goto done; }
@@ -404,6 +423,11 @@ static int replay_layer(const orc_layer *ly, const orc_cfg *cfg, int64_t *cnt, d
 
     int n_res = 0;
     int64_t fifo_clock = 0;
+    /* LeCaR: ghost membership (1 lru, 2 lfu) + eviction position, weights, draws */
+    int n_ghost[3] = {0, 0, 0};
+    double w_lru = 0.5, w_lfu = 0.5;
+    const double discount = pow(g_lecar_base, 1.0 / (double)C);   /* discount_base ** (1.0 / capacity) */
+    int64_t n_draw = 0;
     if (cfg->policy == ORC_ARC) {
         arc.lst = (uint8_t *)calloc((size_t)E, 1);
         arc.ord = (int64_t *)calloc((size_t)E, sizeof(int64_t));
@@ -417,7 +441,7 @@ static int replay_layer(const orc_layer *ly, const orc_cfg *cfg, int64_t *cnt, d
         const orc_step *st = &ly->steps[s];
         if (st->new_seq) {
             /* start_sequence: LFU counts (policies.py:184-185), ML tracker (mlpolicy.py:56-57) */
-            if (cfg->policy == ORC_LFU) memset(freq, 0, (size_t)E * sizeof(int64_t));
+            if (cfg->policy == ORC_LFU || cfg->policy == ORC_LECAR) memset(freq, 0, (size_t)E * sizeof(int64_t));
             if (cfg->policy == ORC_ML) {
                 for (int e = 0; e < E; ++e) { rec[e] = INFINITY; fr[e] = 0; }
             }
@@ -453,11 +477,47 @@ static int replay_layer(const orc_layer *ly, const orc_cfg *cfg, int64_t *cnt, d
                     n_res++;
                 }
             } else if (hit) {
-                if (cfg->policy == ORC_LRU) stamp[xe] = pos;
-                if (cfg->policy == ORC_LFU) freq[xe] += 1;
+                if (cfg->policy == ORC_LRU || cfg->policy == ORC_LECAR) stamp[xe] = pos;
+                if (cfg->policy == ORC_LFU || cfg->policy == ORC_LECAR) freq[xe] += 1;
             } else {
-                if (cfg->policy == ORC_LFU) freq[xe] += 1;   /* _on_miss */
-                if (n_res >= C) {
+                if (cfg->policy == ORC_LFU || cfg->policy == ORC_LECAR) freq[xe] += 1;   /* _on_miss */
+                if (cfg->policy == ORC_LECAR && ghost[xe]) {
+                    /* ghost hit: lecar_update (policies.py:305-327, 358-367) */
+                    const double reward = pow(discount, (double)(pos - gpos[xe]));
+                    if (ghost[xe] == 1) w_lfu *= exp(g_lecar_lr * reward);
+                    else w_lru *= exp(g_lecar_lr * reward);
+                    const double total = w_lru + w_lfu;
+                    w_lru = w_lru / total;
+                    w_lfu = w_lfu / total;
+                    n_ghost[ghost[xe]]--;
+                    ghost[xe] = 0;
+                }
+                if (n_res >= C && cfg->policy == ORC_LECAR) {
+                    /* _choose_victim (policies.py:379-395) */
+                    int any = 0;
+                    for (int e = 0; e < E; ++e) any |= res[e] && !(decode && pinned[e]);
+                    if (!any) { rc = ORC_ERR_NO_EVICTABLE; goto done; }
+                    if (n_draw >= g_lecar_n) { rc = ORC_ERR_INVALID; goto done; }
+                    const int use_lru = g_lecar_u[n_draw++] < w_lru;
+                    int64_t bk = 0;
+                    for (int e = 0; e < E; ++e) {
+                        if (!res[e] || (decode && pinned[e])) continue;
+                        const int64_t kk = use_lru ? stamp[e] : freq[e];
+                        if (victim < 0 || kk < bk) { victim = e; bk = kk; }
+                    }
+                    const int g = use_lru ? 1 : 2;
+                    ghost[victim] = (uint8_t)g;
+                    gpos[victim] = pos;
+                    if (++n_ghost[g] > C) {   /* popitem(last=False): the oldest entry */
+                        int o = -1;
+                        for (int e = 0; e < E; ++e)
+                            if (ghost[e] == g && (o < 0 || gpos[e] < gpos[o])) o = e;
+                        ghost[o] = 0;
+                        n_ghost[g]--;
+                    }
+                    res[victim] = 0;
+                    n_res--;
+                } else if (n_res >= C) {
                     if (cfg->policy == ORC_LRU || cfg->policy == ORC_LFU || cfg->policy == ORC_FIFO) {
                         int64_t bk = 0;
                         for (int e = 0; e < E; ++e) {
@@ -494,7 +554,7 @@ static int replay_layer(const orc_layer *ly, const orc_cfg *cfg, int64_t *cnt, d
                 }
                 res[xe] = 1;
                 n_res++;
-                if (cfg->policy == ORC_LRU) stamp[xe] = pos;   /* _on_insert */
+                if (cfg->policy == ORC_LRU || cfg->policy == ORC_LECAR) stamp[xe] = pos;   /* _on_insert */
                 if (cfg->policy == ORC_FIFO) stamp[xe] = fifo_clock++;   /* FIFOPolicy._on_insert */
             }
             /* engine-side accounting (engine.py:243-257) */
@@ -550,7 +610,7 @@ done:
     if (have_ix) index_free(&ix);
     free(res); free(pinned); free(seen); free(stamp); free(freq); free(rec); free(fr);
     free(x); free(scores); free(h1); free(h2); free(evs);
-    free(arc.lst); free(arc.ord);
+    free(arc.lst); free(arc.ord); free(ghost); free(gpos);
     return rc;
 }
 

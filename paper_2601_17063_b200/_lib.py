@@ -23,7 +23,8 @@ MCB_ERR_UNSUPPORTED = 5
 MCB_ERR_NOMEM = 6
 MCB_ERR_SHAPE = 7
 
-MCB_LRU, MCB_LFU, MCB_BELADY, MCB_ML, MCB_ML_NO_PREFILL, MCB_FIFO, MCB_ARC = range(7)
+MCB_LRU, MCB_LFU, MCB_BELADY, MCB_ML, MCB_ML_NO_PREFILL, MCB_FIFO, MCB_ARC, MCB_LECAR = range(8)
+ML_CODES = (MCB_ML, MCB_ML_NO_PREFILL)
 MCB_TUNE_SOLO_MIN = 0
 MCB_TUNE_SEG_EV = 1
 MCB_TUNE_SEG_NW = 2
@@ -39,7 +40,7 @@ EXPORTED_SYMBOLS = (
     "mcb_set_timing", "mcb_last_timings", "mcb_set_tuning", "mcb_read_stats",
     "mcb_pack_trace", "mcb_packed_view", "mcb_packed_positions", "mcb_packed_free",
     "mcb_replay", "mcb_replay_host", "mcb_next_use", "mcb_score", "mcb_router_topk", "mcb_gen_reference",
-    "mcb_training_data",
+    "mcb_training_data", "mcb_set_lecar", "mcb_lecar_random",
 )
 
 
@@ -132,6 +133,8 @@ def load_library():
             "mcb_score": ([P, P, P, i32, P, P, P], ctypes.c_int),
             "mcb_router_topk": ([P, P, P, i64, i32, i32, i32, i32, P, P, P], ctypes.c_int),
             "mcb_training_data": ([P, P, i32, i32, P, P, P, P], ctypes.c_int),
+            "mcb_set_lecar": ([P, ctypes.c_double, ctypes.c_double, i64], ctypes.c_int),
+            "mcb_lecar_random": ([i64, i64, P], ctypes.c_int),
             "mcb_gen_reference": ([P, i32, i32, i32, i64, i64, i64, i32, ctypes.c_double, P, P, P, P],
                                   ctypes.c_int),
         }
@@ -180,6 +183,19 @@ def read_stats(device: int = 0) -> list:
     out = (ctypes.c_int64 * 8)()
     check(load_library().mcb_read_stats(context(device), out, 8))
     return list(out)
+
+
+def set_lecar(learning_rate: float, discount_base: float, seed: int, device: int = 0):
+    """LeCaR parameters for the MCB_LECAR cells of the following replays."""
+    check(load_library().mcb_set_lecar(context(device), float(learning_rate), float(discount_base), int(seed)))
+
+
+def lecar_random(seed: int, n: int):
+    """CPython random.Random(seed).random() x n, as the engine materialises it (host only)."""
+    import numpy as np
+    out = np.zeros(max(int(n), 1), dtype=np.float64)
+    check(load_library().mcb_lecar_random(int(seed), int(n), out.ctypes.data))
+    return out[:n]
 
 
 def set_tuning(knob: int, value: int, device: int = 0):

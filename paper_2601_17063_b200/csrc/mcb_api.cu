@@ -14,6 +14,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "mcb_internal.h"
 #include "mcb_kernels.cuh"
@@ -93,6 +94,12 @@ struct mcb_ctx {
     int64_t group_lanes = 0;          // lanes per instance of the E > 16 replay: 0 auto, 8 / 16 / 32
     bool serial = false;              // one stream for every stage (per-stage attribution timing)
     DevBuf seg_snap, seg_summ, seg_out, seg_codes, nu_scratch;
+    // LeCaR (mcb_set_lecar): parameters, the shared random() stream (cached
+    // per seed, grown on demand) and the per-call regret factor table
+    double lecar_lr = 0.45, lecar_base = 0.005;
+    int64_t lecar_seed = 0, lecar_u_seed = -1, lecar_u_n = 0;
+    DevBuf lecar_u, lecar_f;
+    std::vector<double> lecar_host;
     cudaEvent_t ev[10] = {};          // start/stop per stage: K2, K3, K4 non-ML, K4 ML, K5
     bool ran[5] = {};
 };
@@ -110,6 +117,55 @@ extern "C" int mcb_set_timing(mcb_ctx *c, int32_t enable) {
     if (enable && !c->ev[0])
         for (auto &e : c->ev) CUDA_TRY(cudaEventCreate(&e));
     c->timing = enable != 0;
+    return MCB_OK;
+}
+
+extern "C" int mcb_set_lecar(mcb_ctx *c, double learning_rate, double discount_base, int64_t seed) {
+    mcb_clear_error();
+    if (!c) return mcb_set_error(MCB_ERR_INVALID, "ctx is NULL");
+    if (!(discount_base >= 0.0))
+        return mcb_set_error(MCB_ERR_UNSUPPORTED, "LeCaR discount_base must be >= 0");
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->lecar_lr = learning_rate;
+    c->lecar_base = discount_base;
+    c->lecar_seed = seed < 0 ? -seed : seed;   // random.seed(int) uses abs(n)
+    return MCB_OK;
+}
+
+// LeCaR inputs for one call: the random() stream (at least one draw per
+// access of the longest chain) and the regret factors of these capacities.
+static int lecar_prepare(mcb_ctx *c, const DevTrace &d, const int32_t *caps, int n_cap, ReplayParams &P,
+                         cudaStream_t s) {
+    int64_t maxlen = 0;
+    if (d.uniform) {
+        maxlen = d.T * d.K;
+    } else {
+        std::vector<int64_t> off((size_t)d.n_chains + 1);
+        CUDA_TRY(cudaMemcpyAsync(off.data(), d.acc_off, off.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        for (int64_t i = 0; i < d.n_chains; ++i) maxlen = std::max(maxlen, off[i + 1] - off[i]);
+    }
+    maxlen = std::max<int64_t>(maxlen, 1);
+    if (c->lecar_u_seed != c->lecar_seed || c->lecar_u_n < maxlen) {
+        const int64_t n = std::max(maxlen, c->lecar_u_seed == c->lecar_seed ? 2 * c->lecar_u_n : 0);
+        c->lecar_host.resize((size_t)n);
+        mcb_lecar_stream(c->lecar_seed, n, c->lecar_host.data());
+        if (int rc = c->lecar_u.ensure((size_t)n * sizeof(double))) return rc;
+        CUDA_TRY(cudaMemcpyAsync(c->lecar_u.p, c->lecar_host.data(), (size_t)n * sizeof(double),
+                                 cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        c->lecar_u_seed = c->lecar_seed;
+        c->lecar_u_n = n;
+    }
+    const int64_t tlen = mcb_lecar_factor_len(caps, n_cap, c->lecar_lr, c->lecar_base, maxlen);
+    std::vector<double> f((size_t)(n_cap * tlen));
+    mcb_lecar_factors(caps, n_cap, c->lecar_lr, c->lecar_base, tlen, f.data());
+    if (int rc = c->lecar_f.ensure(f.size() * sizeof(double))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c->lecar_f.p, f.data(), f.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    P.lecar_u = (const double *)c->lecar_u.p;
+    P.lecar_f = (const double *)c->lecar_f.p;
+    P.lecar_tlen = tlen;
     return MCB_OK;
 }
 
@@ -364,10 +420,11 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
             snprintf(b, sizeof b, "capacity %d < top_k %d: a decode event cannot fit in the cache", caps[i], t->top_k);
             return mcb_set_error(MCB_ERR_CAPACITY, b);
         }
-    bool need_next = false, need_ml[2] = {false, false};
+    bool need_next = false, need_lecar = false, need_ml[2] = {false, false};
     for (int i = 0; i < n_pol; ++i) {
         switch (pols[i]) {
             case MCB_LRU: case MCB_LFU: case MCB_FIFO: case MCB_ARC: break;
+            case MCB_LECAR: need_lecar = true; break;
             case MCB_BELADY: need_next = true; break;
             case MCB_ML: need_ml[0] = true; break;
             case MCB_ML_NO_PREFILL: need_ml[1] = true; break;
@@ -399,6 +456,8 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     P.chain_lo = 0;
     P.chain_hi = d.n_chains;
     P.group_lanes = (int)c->group_lanes;
+    if (need_lecar)
+        if (int rc = lecar_prepare(c, d, caps, n_cap, P, s)) return rc;
 
     // Orchestration.  K3 (ML scores) is only needed by ML instances, so when
     // both kinds are present the non-ML replay runs on a high-priority side
@@ -481,7 +540,7 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         CUDA_TRY(cudaStreamWaitEvent(c->side, c->fork, 0));
     }
     for (int i = 0; i < Pn.n_pol_launch; ++i)
-        if (pols[Pn.pol_map[i]] == MCB_FIFO || pols[Pn.pol_map[i]] == MCB_ARC)
+        if (pols[Pn.pol_map[i]] == MCB_FIFO || pols[Pn.pol_map[i]] == MCB_ARC || pols[Pn.pol_map[i]] == MCB_LECAR)
             Pn.seg.n_seg = 0;   // their eviction order depends on the cache state
     if (Pn.n_pol_launch > 0) {
         mark(c, 4, sn);

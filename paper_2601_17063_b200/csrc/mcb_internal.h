@@ -24,3 +24,8 @@ MCB_HD bool mcb_ev_newseq(uint32_t info) { return (info >> 31) & 1u; }
 
 int mcb_set_error(int code, const char *msg);
 void mcb_clear_error();
+
+// LeCaR host inputs (mcb_lecar.cpp)
+void mcb_lecar_stream(int64_t seed, int64_t n, double *out);
+int64_t mcb_lecar_factor_len(const int32_t *caps, int n_cap, double lr, double base, int64_t max_elapsed);
+void mcb_lecar_factors(const int32_t *caps, int n_cap, double lr, double base, int64_t tlen, double *f);

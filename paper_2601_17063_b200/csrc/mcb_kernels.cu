@@ -320,8 +320,14 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
         arc.n1 = arc.n2 = arc.nb1 = arc.nb2 = 0;
         arc.p = 0.0;
     }
+    // LeCaR (policies.py:330-395): key[] holds the stamps, kf[] the counts;
+    // per lane the ghost-list membership of its experts and their eviction
+    // positions; list sizes, weights and the draw counter are group-uniform.
+    uint32_t kf[EPL], gpos[EPL], gl = 0u, gf = 0u, n_draw = 0u;
+    int ngl = 0, ngf = 0;
+    double wl = 0.5, wf = 0.5;
 #pragma unroll
-    for (int s = 0; s < EPL; ++s) { key[s] = 0; pend[s] = 0; }
+    for (int s = 0; s < EPL; ++s) { key[s] = 0; pend[s] = 0; kf[s] = 0; gpos[s] = 0; }
     uint32_t count = 0, ph = 0, pm = 0, dh = 0, dm = 0, nev = 0, comp = 0, refc = 0;
     double dlat = 0.0, plat = 0.0;
     uint64_t h = 0;
@@ -364,6 +370,10 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
 #pragma unroll
             for (int s = 0; s < EPL; ++s) key[s] = 0;
         }
+        if (POL == POL_LECAR && mcb_ev_newseq(info)) {
+#pragma unroll
+            for (int s = 0; s < EPL; ++s) kf[s] = 0;   // start_sequence (policies.py:351-352)
+        }
         if (POL == POL_ML) {
             // per-event score ranks (mlpolicy.py:59-62): argmax score == argmin (256 - rank);
             // the next event's row is already in flight (prefetched one event ahead)
@@ -389,7 +399,8 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
                 const uint32_t np = nx.get(A, glane, gbase, gmask);
                 if (mine) set_slot<EPL>(key, slot, ~np);
             }
-            if (POL == POL_LRU && mine) set_slot<EPL>(key, slot, pos);
+            if ((POL == POL_LRU || POL == POL_LECAR) && mine) set_slot<EPL>(key, slot, pos);
+            if (POL == POL_LECAR && mine) set_slot<EPL>(kf, slot, get_slot<EPL>(kf, slot) + 1u);
             if (POL == POL_LFU && mine) set_slot<EPL>(key, slot, get_slot<EPL>(key, slot) + 1u);
             uint32_t code = MCB_OUT_HIT;
             if (hit) {
@@ -398,6 +409,17 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
             } else {
                 if (decode) ++dm; else ++pm;
                 ++step_miss;
+                if (POL == POL_LECAR) {   // _on_miss ghost hit: regret update (policies.py:358-367)
+                    const bool in_gl = (__ballot_sync(gmask, mine && (gl & bit)) & gmask) != 0u;
+                    const bool in_gf = (__ballot_sync(gmask, mine && (gf & bit)) & gmask) != 0u;
+                    if (in_gl || in_gf) {
+                        const uint32_t gp = __shfl_sync(gmask, get_slot<EPL>(gpos, slot), gbase + owner);
+                        lecar_reward(wl, wf, in_gl, lecar_factor(P, cap_i, pos - gp));
+                        if (mine) { gl &= ~bit; gf &= ~bit; }
+                        if (in_gl) --ngl;
+                        else --ngf;
+                    }
+                }
                 if (POL == POL_ARC) {
                     int vl, vs;
                     bool none_left;
@@ -414,11 +436,18 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
                     }
                 } else if (count >= C) {
                     const uint32_t cand = res & ~pin;
+                    bool use_lru = true;
+                    if (POL == POL_LECAR) {   // _choose_victim (policies.py:379-395)
+                        use_lru = __ldg(P.lecar_u + n_draw) < wl;
+                        ++n_draw;
+                    }
                     uint32_t lk = KEY_SENT;
                     int ls = 0;
 #pragma unroll
-                    for (int s = 0; s < EPL; ++s)
-                        if (((cand >> s) & 1u) && key[s] < lk) { lk = key[s]; ls = s; }
+                    for (int s = 0; s < EPL; ++s) {
+                        const uint32_t ks = (POL == POL_LECAR && !use_lru) ? kf[s] : key[s];
+                        if (((cand >> s) & 1u) && ks < lk) { lk = ks; ls = s; }
+                    }
                     const uint32_t m = __reduce_min_sync(gmask, lk);
                     if (m == KEY_SENT) { status = MCB_ERR_NO_EVICTABLE; break; }
                     const unsigned b = __ballot_sync(gmask, lk == m) & gmask;
@@ -431,6 +460,29 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
                     }
                     code = (uint32_t)(vlane * EPL + vs);
                     ++nev;
+                    if (POL == POL_LECAR) {   // ghost[victim] = position; trim to capacity
+                        if (glane == vlane) {
+                            set_slot<EPL>(gpos, vs, pos);
+                            if (use_lru) gl |= 1u << vs;
+                            else gf |= 1u << vs;
+                        }
+                        int &ng = use_lru ? ngl : ngf;
+                        if (++ng > (int)C) {
+                            const uint32_t g = use_lru ? gl : gf;
+                            uint32_t ok = KEY_SENT;
+                            int os = 0;
+#pragma unroll
+                            for (int s = 0; s < EPL; ++s)
+                                if (((g >> s) & 1u) && gpos[s] < ok) { ok = gpos[s]; os = s; }
+                            const uint32_t om = __reduce_min_sync(gmask, ok);
+                            const int ol = __ffs(__ballot_sync(gmask, ok == om) & gmask) - 1;
+                            if (lane == ol) {
+                                gl &= ~(1u << os);
+                                gf &= ~(1u << os);
+                            }
+                            --ng;
+                        }
+                    }
                 } else {
                     ++count;
                     code = MCB_OUT_MISS;
@@ -504,6 +556,7 @@ __global__ void __launch_bounds__(128) k_replay(const __grid_constant__ ReplayPa
         case MCB_ML: replay_instance<G, EPL, POL_ML, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
         case MCB_FIFO: replay_instance<G, EPL, POL_FIFO, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
         case MCB_ARC: replay_instance<G, EPL, POL_ARC, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
+        case MCB_LECAR: replay_instance<G, EPL, POL_LECAR, UNIFORM>(P, chain, pol_i, cap_i, inst, 0); break;
         default: replay_instance<G, EPL, POL_ML, UNIFORM>(P, chain, pol_i, cap_i, inst, 1); break;
     }
 }
@@ -533,6 +586,8 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
     sstate_clear(S);
     ArcState<EM> arc;
     if (POL == POL_ARC) arc_clear<EM>(arc);
+    LecarState<EM> lec;
+    if (POL == POL_LECAR) lecar_clear<EM>(lec);
     uint32_t pin = 0, seen = 0, valid = (1u << E) - 1u;
     uint32_t ph = 0, pm = 0, dh = 0, dm = 0, comp = 0;
     SCount n = {0u, 0u, 0u};
@@ -572,6 +627,7 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
 #pragma unroll
             for (int s = 0; s < EM; ++s) pk[s] = (uint32_t)s;   // start_sequence (policies.py:184-185)
         }
+        if (POL == POL_LECAR && !UNIFORM && mcb_ev_newseq(info)) lecar_new_sequence<EM>(lec);
         if (UNIFORM && P.res_masks) {   // resident set before the event (dataset.py:61-63)
             uint8_t *m = P.res_masks + (chain * tr.T + ev) * E;
             for (int e = 0; e < E; ++e) m[e] = (uint8_t)((S.res >> e) & 1u);
@@ -591,6 +647,8 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
             uint32_t code;
             if (POL == POL_ARC) {
                 code = sstep_arc<EM, WMAX>(S, arc, x, bit, decode ? pin : 0u, C, n, stuck, miss);
+            } else if (POL == POL_LECAR) {
+                code = sstep_lecar<EM, WMAX>(S, lec, P, cap_i, x, bit, pos, pin, C, n, stuck, miss);
             } else {
                 code = sstep<EM, WMAX>(S, pk, bit, pin, valid, C, n, stuck, miss);
                 if (POL == POL_FIFO) solo_fifo_insert<EM>(pk, x, bit, pos, miss);
@@ -647,6 +705,7 @@ __global__ void __launch_bounds__(128) k_replay_solo(const __grid_constant__ Rep
         case MCB_ML: solo_instance<EM, POL_ML, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
         case MCB_FIFO: solo_instance<EM, POL_FIFO, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
         case MCB_ARC: solo_instance<EM, POL_ARC, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
+        case MCB_LECAR: solo_instance<EM, POL_LECAR, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0); break;
         default: solo_instance<EM, POL_ML, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 1); break;
     }
 }

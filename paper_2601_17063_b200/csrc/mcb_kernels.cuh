@@ -52,6 +52,9 @@ struct ReplayParams {
     int64_t chain_lo, chain_hi;         // chains [lo, hi) replayed by this launch (outputs stay global)
     int group_lanes;                    // lane-group size of k_replay (0 = automatic)
     uint8_t *res_masks;                 // optional [chain][T][E]: resident set at each event start
+    const double *lecar_u;              // LeCaR: random() stream, one draw per eviction (policies.py:381)
+    const double *lecar_f;              // LeCaR: [cap][lecar_tlen] regret factors exp(lr * discount**elapsed)
+    int64_t lecar_tlen;                 //   elapsed >= lecar_tlen has factor 1.0
                                         // (uniform traces, one policy x capacity; dataset.py masks)
     // segmented speculative replay (mcb_segment.cu); seg.n_seg == 0: whole-chain kernels
     struct Seg {

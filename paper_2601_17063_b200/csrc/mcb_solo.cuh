@@ -16,7 +16,7 @@
 
 #include "mcb_kernels.cuh"
 
-enum { POL_LRU = 0, POL_LFU = 1, POL_BELADY = 2, POL_ML = 3, POL_FIFO = 4, POL_ARC = 5 };
+enum { POL_LRU = 0, POL_LFU = 1, POL_BELADY = 2, POL_ML = 3, POL_FIFO = 4, POL_ARC = 5, POL_LECAR = 6 };
 
 #define SOLO_WMAX 7                       // largest refetch window of the solo kernels
 #define FULL_MASK_W 0xFFFFFFFFu
@@ -242,7 +242,7 @@ __device__ __forceinline__ void solo_key_update(uint32_t (&pk)[EM], uint32_t x, 
         nk = cur + (1u << SH);
     }
     if (POL == POL_BELADY) nk = ((np == MCB_NEXT_INF ? 0u : KMAX - np) << SH) | x;   // farthest next use first
-    if (POL == POL_FIFO || POL == POL_ARC) return;   // state-dependent order (solo_fifo_insert / ArcState)
+    if (POL == POL_FIFO || POL == POL_ARC || POL == POL_LECAR) return;   // state-dependent (own step functions)
     if (POL != POL_ML) {
 #pragma unroll
         for (int s = 0; s < EM; ++s) pk[s] = ((bit >> s) & 1u) ? nk : pk[s];
@@ -378,6 +378,118 @@ __device__ __forceinline__ uint32_t sstep_arc(SState<WMAX> &S, ArcState<EM> &a, 
     const bool evict = v != (uint32_t)EM;
     const uint32_t vbit = evict ? (1u << v) : 0u;
     S.res = a.t1 | a.t2;
+    ++n.misses;
+    n.nev += evict ? 1u : 0u;
+    n.refc += (bit & S.ring_or) ? 1u : 0u;
+    S.ring_or = (S.ring_or & ~bit) | vbit;
+#pragma unroll
+    for (int s = 0; s <= WMAX; ++s) S.ring[s] &= ~bit;
+    S.ring[0] |= vbit;
+    return evict ? v : MCB_OUT_MISS;
+}
+
+// LeCaR (policies.py:305-395) for num_experts <= 16: the LRU stamps and LFU
+// counts as packed (key << SH | id) words, the two ghost lists as masks plus
+// each ghost's eviction position (positions grow, so a list's oldest entry
+// is its smallest position), the weights as float64 and the instance's
+// eviction count, which indexes the shared random() stream.
+template <int EM>
+struct LecarState {
+    uint32_t pl[EM];    // (stamp << SH) | id   (_stamp, set at every access)
+    uint32_t pf[EM];    // (freq << SH) | id    (_freq, reset at start_sequence)
+    uint32_t gpos[EM];  // eviction position of a ghost entry
+    uint32_t gl, gf;    // _ghost_lru / _ghost_lfu membership
+    uint32_t k;         // evictions so far = random() draws consumed
+    double wl, wf;      // weights (w_lru, w_lfu)
+};
+
+template <int EM>
+__device__ __forceinline__ void lecar_clear(LecarState<EM> &a) {
+#pragma unroll
+    for (int s = 0; s < EM; ++s) { a.pl[s] = (uint32_t)s; a.pf[s] = (uint32_t)s; a.gpos[s] = 0u; }
+    a.gl = a.gf = 0u;
+    a.k = 0u;
+    a.wl = 0.5;
+    a.wf = 0.5;
+}
+
+template <int EM>
+__device__ __forceinline__ void lecar_new_sequence(LecarState<EM> &a) {   // start_sequence (policies.py:351-352)
+#pragma unroll
+    for (int s = 0; s < EM; ++s) a.pf[s] = (uint32_t)s;
+}
+
+// lecar_update (policies.py:305-327) with the host-made factor
+// f = exp(learning_rate * discount**elapsed); no contraction into FMAs.
+__device__ __forceinline__ void lecar_reward(double &wl, double &wf, bool ghost_lru, double f) {
+    if (ghost_lru) wf = __dmul_rn(wf, f);
+    else wl = __dmul_rn(wl, f);
+    const double total = __dadd_rn(wl, wf);
+    wl = __ddiv_rn(wl, total);
+    wf = __ddiv_rn(wf, total);
+}
+
+__device__ __forceinline__ double lecar_factor(const ReplayParams &P, int cap_i, uint32_t elapsed) {
+    return (int64_t)elapsed < P.lecar_tlen ? __ldg(P.lecar_f + (int64_t)cap_i * P.lecar_tlen + elapsed) : 1.0;
+}
+
+// LeCaRPolicy access (CachePolicy.access, policies.py:95-107, with the LeCaR
+// hooks) + the engine's accounting on S exactly as sstep: the outcome code.
+template <int EM, int WMAX>
+__device__ __forceinline__ uint32_t sstep_lecar(SState<WMAX> &S, LecarState<EM> &a, const ReplayParams &P,
+                                                int cap_i, uint32_t x, uint32_t bit, uint32_t pos, uint32_t pin,
+                                                uint32_t C, SCount &n, bool &stuck, uint32_t &miss_out) {
+    constexpr int SH = Solo<EM>::SH;
+    const bool hit = (S.res & bit) != 0u;
+    // _on_hit / _on_miss: freq += 1; _on_hit / _on_insert: stamp = position
+    // (x is never a victim candidate of its own miss, so both apply up front)
+#pragma unroll
+    for (int s = 0; s < EM; ++s) {
+        const bool me = (bit >> s) & 1u;
+        a.pf[s] = me ? a.pf[s] + (1u << SH) : a.pf[s];
+        a.pl[s] = me ? ((pos << SH) | (uint32_t)s) : a.pl[s];
+    }
+    miss_out = hit ? 0u : 1u;
+    if (hit) return MCB_OUT_HIT;
+    if ((a.gl | a.gf) & bit) {   // ghost hit: regret update (policies.py:358-367)
+        uint32_t gp = 0u;
+#pragma unroll
+        for (int s = 0; s < EM; ++s) gp |= ((bit >> s) & 1u) ? a.gpos[s] : 0u;
+        lecar_reward(a.wl, a.wf, (a.gl & bit) != 0u, lecar_factor(P, cap_i, pos - gp));
+        a.gl &= ~bit;
+        a.gf &= ~bit;
+    }
+    uint32_t v = (uint32_t)EM;
+    if ((uint32_t)__popc(S.res) >= C) {
+        const uint32_t cand = S.res & ~pin;
+        if (!cand) {
+            stuck = true;
+        } else {
+            // _choose_victim (policies.py:379-395)
+            const double u = __ldg(P.lecar_u + a.k);
+            ++a.k;
+            const bool use_lru = u < a.wl;
+            uint32_t t = ~0u;
+#pragma unroll
+            for (int s = 0; s < EM; ++s) t = ((cand >> s) & 1u) ? min(t, use_lru ? a.pl[s] : a.pf[s]) : t;
+            v = t & (uint32_t)(EM - 1);
+            const uint32_t vb = 1u << v;
+#pragma unroll
+            for (int s = 0; s < EM; ++s) a.gpos[s] = s == (int)v ? pos : a.gpos[s];
+            uint32_t g = (use_lru ? a.gl : a.gf) | vb;
+            if ((uint32_t)__popc(g) > C) {   // drop the oldest ghost (popitem(last=False))
+                uint32_t o = ~0u;
+#pragma unroll
+                for (int s = 0; s < EM; ++s) o = ((g >> s) & 1u) ? min(o, (a.gpos[s] << SH) | (uint32_t)s) : o;
+                g &= ~(1u << (o & (uint32_t)(EM - 1)));
+            }
+            if (use_lru) a.gl = g;
+            else a.gf = g;
+        }
+    }
+    const bool evict = v != (uint32_t)EM;
+    const uint32_t vbit = evict ? (1u << v) : 0u;
+    S.res = (S.res & ~vbit) | bit;
     ++n.misses;
     n.nev += evict ? 1u : 0u;
     n.refc += (bit & S.ring_or) ? 1u : 0u;

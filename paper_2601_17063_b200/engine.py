@@ -125,7 +125,8 @@ class SimRun:
 
 POLICY_NAMES = ("lru", "lfu", "fifo", "arc", "lecar", "belady", "ml")
 _CODES = {"lru": _lib.MCB_LRU, "lfu": _lib.MCB_LFU, "belady": _lib.MCB_BELADY, "fifo": _lib.MCB_FIFO,
-          "arc": _lib.MCB_ARC}
+          "arc": _lib.MCB_ARC, "lecar": _lib.MCB_LECAR}
+_LECAR_DEFAULTS = (0.45, 0.005, 0)   # LeCaRPolicy.__init__ (policies.py:333-341)
 
 
 class EnginePolicy:
@@ -134,10 +135,15 @@ class EnginePolicy:
     (make(layer, capacity, header, oracle)) is not supported -- the engine has
     no per-access policy objects."""
 
-    def __init__(self, name: str, code: int, nets=None):
+    def __init__(self, name: str, code: int, nets=None, lecar=None):
         self.name = name
         self.code = code
         self.nets = nets
+        self.lecar = lecar   # (learning_rate, discount_base, seed) for lecar
+
+    @property
+    def is_ml(self) -> bool:
+        return self.code in _lib.ML_CODES
 
     def __call__(self, layer, capacity, header, oracle):
         raise SimulationError("per-access CachePolicy objects are not provided by the B200 engine; "
@@ -151,8 +157,16 @@ def policy_factory(spec: Union[str, dict], nets=None):
     if name not in POLICY_NAMES:
         raise SimulationError(f"unknown policy {name!r}; expected one of {POLICY_NAMES}")
     if name == "lecar":
-        raise SimulationError(f"policy {name!r} is unsupported by the B200 engine "
-                              "(the engine replays lru, lfu, belady, ml, fifo and arc)")
+        lr = params.pop("learning_rate", _LECAR_DEFAULTS[0])
+        base = params.pop("discount_base", _LECAR_DEFAULTS[1])
+        seed = params.pop("seed", _LECAR_DEFAULTS[2])
+        if params:
+            raise TypeError(f"unexpected lecar policy parameters {sorted(params)}")
+        if not isinstance(seed, int) or isinstance(seed, bool):
+            raise SimulationError("lecar: only integer seeds are supported by the B200 engine")
+        if not float(base) >= 0.0:
+            raise SimulationError("lecar: discount_base must be >= 0")
+        return name, EnginePolicy(name, _lib.MCB_LECAR, lecar=(float(lr), float(base), int(seed)))
     if name == "ml":
         if nets is None:
             raise SimulationError("ml policy requires trained eviction nets")
@@ -217,7 +231,7 @@ def _cost_struct(cost: CostModel, window: int) -> _lib.MCBCost:
 
 def replay_host(packed: PackedTrace, codes: Sequence[int], capacities: Sequence[int], cost: CostModel,
                 window: int, nets=None, *, want_outcomes=False, want_hashes=False, want_chain=False,
-                device: int = 0, stream=None) -> dict:
+                device: int = 0, stream=None, lecar=None) -> dict:
     """One native call: every trace of ``packed`` x codes x capacities.
 
     Returns numpy arrays: reports [trace][pol][cap][8] int64, latency
@@ -255,6 +269,8 @@ def replay_host(packed: PackedTrace, codes: Sequence[int], capacities: Sequence[
         ns.num_experts, ns.hidden, ns.num_nets = packed.num_experts, hidden, n_nets
         ns.params = keep.ctypes.data
         netsp = ctypes.byref(ns)
+    if _lib.MCB_LECAR in codes:
+        _lib.set_lecar(*(lecar or _LECAR_DEFAULTS), device=device)
     view = packed.view()
     cs = _cost_struct(cost, window)
     rc = lib.mcb_replay_host(ctx, ctypes.byref(view), pols, n_pol, caps, n_cap, ctypes.byref(cs), netsp,
@@ -316,8 +332,8 @@ def run_simulation(trace, policy, capacity: int, cost: CostModel = CostModel(), 
     """Replay the trace through per-layer caches and assemble a full report (engine.py:300-380)."""
     packed = _prepare(trace, cost, [capacity])
     name, ep = _resolve(policy, nets)
-    netp = _net_params(ep.nets, packed.num_layers, packed.num_experts) if ep.code >= _lib.MCB_ML else None
-    res = replay_host(packed, [ep.code], [capacity], cost, window, netp, want_outcomes=True)
+    netp = _net_params(ep.nets, packed.num_layers, packed.num_experts) if ep.is_ml else None
+    res = replay_host(packed, [ep.code], [capacity], cost, window, netp, want_outcomes=True, lecar=ep.lecar)
     _raise_cell_status(int(res["reports"][0, 0, 0, _lib.R_STATUS]))
     report = assemble_report(name, capacity, window, res["reports"][0, 0, 0], res["latency"][0, 0, 0],
                              packed.decode_steps[0])
@@ -350,8 +366,8 @@ def simulate(trace, policy, capacity: int, cost: CostModel = CostModel(), window
     """engine.py:383-391, without materialising the eviction log."""
     packed = _prepare(trace, cost, [capacity])
     name, ep = _resolve(policy, nets)
-    netp = _net_params(ep.nets, packed.num_layers, packed.num_experts) if ep.code >= _lib.MCB_ML else None
-    res = replay_host(packed, [ep.code], [capacity], cost, window, netp)
+    netp = _net_params(ep.nets, packed.num_layers, packed.num_experts) if ep.is_ml else None
+    res = replay_host(packed, [ep.code], [capacity], cost, window, netp, lecar=ep.lecar)
     _raise_cell_status(int(res["reports"][0, 0, 0, _lib.R_STATUS]))
     return assemble_report(name, capacity, window, res["reports"][0, 0, 0], res["latency"][0, 0, 0],
                            packed.decode_steps[0])
@@ -377,20 +393,32 @@ def sweep(trace, policies: Sequence, capacities: Sequence[int], cost: CostModel 
     packed = _prepare(trace, cost, capacities)
     resolved = [_resolve(p, nets) for p in policies]
     netp = None
-    if any(ep.code >= _lib.MCB_ML for _, ep in resolved):
-        netp = _net_params(next(ep.nets for _, ep in resolved if ep.code >= _lib.MCB_ML),
+    if any(ep.is_ml for _, ep in resolved):
+        netp = _net_params(next(ep.nets for _, ep in resolved if ep.is_ml),
                            packed.num_layers, packed.num_experts)
     reports = []
     caps = list(capacities)
-    for p0 in range(0, len(resolved), _MAX_POL):
-        chunk = resolved[p0:p0 + _MAX_POL]
+    # one engine call per group of <= 8 policies; LeCaR parameters are per
+    # call, so LeCaR specs with different parameters go to different calls
+    groups: list[list[int]] = []
+    for i, (_, ep) in enumerate(resolved):
+        for g in groups:
+            params = {resolved[k][1].lecar for k in g if resolved[k][1].lecar is not None}
+            if len(g) < _MAX_POL and (ep.lecar is None or not params or params == {ep.lecar}):
+                g.append(i)
+                break
+        else:
+            groups.append([i])
+    for g in groups:
+        chunk = [resolved[i] for i in g]
+        lecar = next((ep.lecar for _, ep in chunk if ep.lecar is not None), None)
         for c0 in range(0, len(caps), _MAX_CAP):
             cchunk = caps[c0:c0 + _MAX_CAP]
-            res = replay_host(packed, [ep.code for _, ep in chunk], cchunk, cost, window, netp)
+            res = replay_host(packed, [ep.code for _, ep in chunk], cchunk, cost, window, netp, lecar=lecar)
             for i, (name, _) in enumerate(chunk):
                 for j, cap in enumerate(cchunk):
                     _raise_cell_status(int(res["reports"][0, i, j, _lib.R_STATUS]))
-                    reports.append((p0 + i, c0 + j, assemble_report(
+                    reports.append((g[i], c0 + j, assemble_report(
                         name, cap, window, res["reports"][0, i, j], res["latency"][0, i, j],
                         packed.decode_steps[0])))
     reports.sort(key=lambda t: (t[0], t[1]))   # policy-major cell order, as the reference builds it

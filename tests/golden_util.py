@@ -48,6 +48,13 @@ def include_prefill(spec):
     return True if isinstance(spec, str) else spec.get("include_prefill", True)
 
 
+def lecar_params(spec):
+    """LeCaR keyword parameters of a policy spec (policies.py:333-341)."""
+    if isinstance(spec, str):
+        return {}
+    return {k: spec[k] for k in ("learning_rate", "discount_base", "seed") if k in spec}
+
+
 M64 = (1 << 64) - 1
 HASH_MUL = 0x100000001B3
 FNV_OFF = 0xCBF29CE484222325

@@ -82,3 +82,35 @@ def test_full_size_properties_and_kernel_agreement(shape):
         got = cr[c].reshape(len(jobs), _lib.R_N)[:, :7]
         assert np.array_equal(got, cnt[i]), c
         assert np.array_equal(seg["hashes"][c].reshape(len(jobs)), hsh[i]), c
+
+
+@pytest.mark.parametrize("shape", ["c2", "c1"])
+def test_full_size_state_dependent_policies(shape):
+    """FIFO, ARC and LeCaR (state-dependent eviction orders, whole-chain
+    kernels) at BASELINE size: engine properties on every chain and sampled
+    chains cell by cell against the C oracle."""
+    if shape == "c2":
+        L, E, K, T, d, caps = 32, 8, 2, 65536, 4096, [2, 3, 4, 5, 6, 7]
+    else:
+        L, E, K, T, d, caps = 48, 128, 8, 2048, 2048, [16, 32, 64]
+    ids = make_ids(L, E, K, T, d, seed=5)
+    packed = mcb.packed_from_decode_ids(ids, E)
+    pols = ["fifo", "arc", "lecar"]
+    lecar = (0.45, 0.005, 11)
+    res = engine.replay_host(packed, [_lib.MCB_FIFO, _lib.MCB_ARC, _lib.MCB_LECAR], caps, mcb.CostModel(), 5,
+                             None, want_hashes=True, want_chain=True, lecar=lecar)
+    cr = res["chain_reports"]
+    assert np.all(cr[..., _lib.R_STATUS] == 0)
+    misses = cr[..., _lib.R_DM]
+    cap = np.array(caps)[None, None, :]
+    assert np.array_equal(cr[..., _lib.R_EVICT], np.maximum(0, misses - cap))
+    distinct = np.array([len(np.unique(ids[c])) for c in range(L)])
+    assert np.all(cr[..., _lib.R_COMP] == distinct[:, None, None])
+    sample = [0, L - 1]
+    sub = np.ascontiguousarray(ids[sample])
+    jobs = [(p, c) for p in pols for c in caps]
+    cnt, lat, hsh = oracle.replay_uniform(sub, len(sample), E, jobs, None, 5, None, hash_kind="poly",
+                                          lecar=dict(learning_rate=lecar[0], discount_base=lecar[1], seed=lecar[2]))
+    for i, c in enumerate(sample):
+        assert np.array_equal(cr[c].reshape(len(jobs), _lib.R_N)[:, :7], cnt[i]), c
+        assert np.array_equal(res["hashes"][c].reshape(len(jobs)), hsh[i]), c

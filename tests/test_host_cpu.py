@@ -102,8 +102,16 @@ def test_policy_factory_and_errors_without_gpu():
     with pytest.raises(mcb.SimulationError):
         mcb.policy_factory("ml")                       # needs nets (engine.py:184-185)
     assert mcb.policy_factory("arc")[1].code == _lib.MCB_ARC
+    name, ep = mcb.policy_factory("lecar")
+    assert ep.code == _lib.MCB_LECAR and ep.lecar == (0.45, 0.005, 0)   # policies.py:333-341 defaults
+    _, ep = mcb.policy_factory({"name": "lecar", "seed": 5, "learning_rate": 0.1})
+    assert ep.lecar == (0.1, 0.005, 5)
+    with pytest.raises(TypeError):
+        mcb.policy_factory({"name": "lecar", "alpha": 1})
     with pytest.raises(mcb.SimulationError):
-        mcb.policy_factory("lecar")                    # outside the B200 engine, no CPU fallback
+        mcb.policy_factory({"name": "lecar", "seed": "abc"})     # only integer seeds on the engine
+    with pytest.raises(TypeError):
+        mcb.policy_factory({"name": "lru", "seed": 1})
     name, ep = mcb.policy_factory({"name": "ml", "include_prefill": False}, nets=mcb.EvictionNet(4))
     assert name == "ml" and ep.code == _lib.MCB_ML_NO_PREFILL
     t = tr([AccessEvent(0, D, 0, 0, (0, 1))])
@@ -149,3 +157,14 @@ def test_cost_and_cache_size_helpers():
     assert mcb.step_latency_s(3, 8, mcb.CostModel(loads_serial=False)) == 3e-3
     b = mcb.HardwareBudget(vram_bytes=10, nonexpert_bytes=2, all_experts_bytes=16, experts_per_layer=8)
     assert mcb.cache_size_calc(b) == 4
+
+
+def test_lecar_random_stream_matches_python():
+    """The engine's host-side MT19937 (mcb_lecar_random) reproduces CPython's
+    random.Random(seed).random(), the stream LeCaRPolicy draws from
+    (policies.py:347, 381)."""
+    import random
+    for seed in (0, 1, 7, 2**32 + 5, 12345678901, -3):
+        r = random.Random(seed)
+        want = np.array([r.random() for _ in range(2000)])
+        assert np.array_equal(_lib.lecar_random(seed, 2000), want), seed

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import oracle
-from golden_util import COSTS, GOLDEN, case_trace, include_prefill, load, policy_name
+from golden_util import COSTS, GOLDEN, case_trace, include_prefill, lecar_params, load, policy_name
 
 
 def _check_case(case, check_decisions=True):
@@ -22,7 +22,7 @@ def _check_case(case, check_decisions=True):
         report, hashes, outs = oracle.simulate(
             header, events, pol, run["capacity"], COSTS[run["cost"]], run["window"],
             nets if pol == "ml" else None, include_prefill(run["policy"]),
-            want_outcomes=check_decisions and "decisions" in run)
+            want_outcomes=check_decisions and "decisions" in run, lecar=lecar_params(run["policy"]))
         assert report == run["report"], (case["name"], run["policy"], run["capacity"])
         assert [format(h, "016x") for h in hashes] == run["hashes"], (case["name"], run["policy"])
         if outs is not None:
@@ -121,4 +121,13 @@ def test_oracle_fifo_cases():
 def test_oracle_arc_cases():
     """ARC (policies.py:217-302) on reference-made fixtures (make_arc_golden.py)."""
     for case in load("arc_cases.json.gz")["cases"]:
+        _check_case(case)
+
+
+def test_oracle_lecar_cases():
+    """LeCaR (policies.py:305-395) on reference-made fixtures (make_lecar_golden.py):
+    default and explicit learning_rate / discount_base / seed specs."""
+    cases = load("lecar_cases.json.gz")["cases"]
+    assert sum(r["n_evictions"] for c in cases for r in c["runs"]) > 1000
+    for case in cases:
         _check_case(case)

@@ -8,8 +8,8 @@ import numpy as np
 import pytest
 
 import oracle
-from golden_util import (COSTS, GOLDEN, big_ids, case_trace, expected_poly_hashes, include_prefill, load,
-                         policy_name)
+from golden_util import (COSTS, GOLDEN, big_ids, case_trace, expected_poly_hashes, include_prefill,
+                         lecar_params, load, policy_name)
 
 pytestmark = pytest.mark.gpu
 
@@ -34,7 +34,14 @@ def code_of(spec):
     if name == "ml":
         return _lib.MCB_ML if include_prefill(spec) else _lib.MCB_ML_NO_PREFILL
     return {"lru": _lib.MCB_LRU, "lfu": _lib.MCB_LFU, "belady": _lib.MCB_BELADY, "fifo": _lib.MCB_FIFO,
-            "arc": _lib.MCB_ARC}[name]
+            "arc": _lib.MCB_ARC, "lecar": _lib.MCB_LECAR}[name]
+
+
+def lecar_of(spec):
+    if policy_name(spec) != "lecar":
+        return None
+    p = lecar_params(spec)
+    return (p.get("learning_rate", 0.45), p.get("discount_base", 0.005), p.get("seed", 0))
 
 
 def check_case(case, decisions=True):
@@ -45,7 +52,8 @@ def check_case(case, decisions=True):
         nets = oracle.nets_from_spec(run["nets"], L, E, GOLDEN) if policy_name(run["policy"]) == "ml" else None
         want_dec = decisions and "decisions" in run
         res = engine.replay_host(packed, [code_of(run["policy"])], [run["capacity"]], cost_of(run["cost"]),
-                                 run["window"], nets, want_hashes=True, want_outcomes=want_dec)
+                                 run["window"], nets, want_hashes=True, want_outcomes=want_dec,
+                                 lecar=lecar_of(run["policy"]))
         rep = engine.assemble_report(policy_name(run["policy"]), run["capacity"], run["window"],
                                      res["reports"][0, 0, 0], res["latency"][0, 0, 0], packed.decode_steps[0])
         assert int(res["reports"][0, 0, 0, _lib.R_STATUS]) == 0
@@ -96,6 +104,34 @@ def test_arc_cases(part, kernel_variant):
     """ARC (policies.py:217-302) against reference-made fixtures, decisions included."""
     for case in load("arc_cases.json.gz")["cases"][part::2]:
         check_case(case)
+
+
+@pytest.mark.parametrize("part", range(2))
+def test_lecar_cases(part, kernel_variant):
+    """LeCaR (policies.py:305-395) against reference-made fixtures, decisions
+    included: default and explicit learning_rate / discount_base / seed."""
+    for case in load("lecar_cases.json.gz")["cases"][part::2]:
+        check_case(case)
+
+
+def test_lecar_public_api_and_sweep_grouping():
+    """run_simulation / sweep with LeCaR specs of different parameters in one
+    sweep (one engine call per parameter set) reproduce the fixtures."""
+    cases = load("lecar_cases.json.gz")["cases"]
+    for case in cases[:12]:
+        header, events = case_trace(case)
+        trace = to_trace(header, events)
+        for run in case["runs"]:
+            rep = mcb.run_simulation(trace, run["policy"], run["capacity"], cost_of(run["cost"]),
+                                     run["window"]).report
+            assert rep.to_dict() == run["report"], case["name"]
+    header, events = case_trace(cases[0])
+    trace = to_trace(header, events)
+    specs = ["lecar", {"name": "lecar", "seed": 9}, "lru", {"name": "lecar", "learning_rate": 1.5}]
+    cap = max(header[2], 3)
+    rows = mcb.sweep(trace, specs, [cap])
+    singles = sorted([mcb.simulate(trace, s, cap) for s in specs], key=lambda r: (r.policy, r.capacity))
+    assert [r.to_dict() for r in rows] == [r.to_dict() for r in singles]
 
 
 def test_zipf_and_dominance_cases(kernel_variant):
