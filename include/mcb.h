@@ -208,6 +208,20 @@ int mcb_set_lecar(mcb_ctx *ctx, double learning_rate, double discount_base, int6
 int mcb_lecar_random(int64_t seed, int64_t n, double *out);
 int mcb_last_timings(mcb_ctx *ctx, float *ms, int32_t n);
 
+/* ---- K7: GPU validate + pack of a decode-only batch (batch-kind .mcbt) ----
+ * ids: device uint8 [num_traces][decode_steps][num_layers][top_k] in the
+ * reference's event order (trace.py:121-127, one sequence per trace).
+ * acc: device uint8, >= num_traces * num_layers * decode_steps * top_k bytes:
+ * the chain-major uniform layout of mcb_trace.  first_bad: device int64,
+ * receives the event-order index (trace * T + step) * L + layer of the first
+ * event AccessEvent.validate rejects (trace.py:80-106: expert outside
+ * [0, num_experts) or a duplicate), or -1.  Asynchronous on `stream`.
+ * Replaces parse_trace / RoutingTrace.validate + layer_schedules for this
+ * layout (trace.py:350-412, replay.py:44-81). */
+int mcb_pack_decode_ids(mcb_ctx *ctx, const uint8_t *ids, int64_t num_traces, int64_t decode_steps,
+                        int32_t num_layers, int32_t top_k, int32_t num_experts, uint8_t *acc, int64_t *first_bad,
+                        void *stream);
+
 /* ---- host-side trace validation + packing (trace.py:57-141, replay.py:44-81) ----
  * Input: one trace as flat events in stored order: seq_id, phase (0 prefill,
  * 1 decode), step, layer, CSR experts.  Validates exactly what

@@ -38,4 +38,15 @@ from .trace import (
     packed_from_decode_ids,
 )
 
+from .tracefile import (
+    load_packed,
+    parse_trace,
+    read_trace,
+    read_trace_binary,
+    trace_to_text,
+    write_batch_binary,
+    write_trace,
+    write_trace_binary,
+)
+
 __version__ = "0.1.0"

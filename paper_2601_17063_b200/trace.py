@@ -211,6 +211,12 @@ def pack_trace(trace) -> PackedTrace:
                             _ptr(phase), _ptr(step), _ptr(layer), _ptr(off), _ptr(experts),
                             ctypes.byref(handle))
     _lib.check(rc)
+    return _from_handle(handle)
+
+
+def _from_handle(handle) -> PackedTrace:
+    """PackedTrace over the arrays of a native mcb_packed handle."""
+    lib = _lib.load_library()
     v = _lib.MCBTrace()
     tot_acc, tot_ev, tot_rt, dsteps = (ctypes.c_int64() for _ in range(4))
     _lib.check(lib.mcb_packed_view(handle, ctypes.byref(v), ctypes.byref(tot_acc), ctypes.byref(tot_ev),
