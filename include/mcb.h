@@ -208,6 +208,16 @@ int mcb_set_lecar(mcb_ctx *ctx, double learning_rate, double discount_base, int6
 int mcb_lecar_random(int64_t seed, int64_t n, double *out);
 int mcb_last_timings(mcb_ctx *ctx, float *ms, int32_t n);
 
+/* ---- K8: eviction_quality_duel (engine.py:404-436) ----
+ * outcomes_a / outcomes_b: two policies' per-access outcome codes of the
+ * same trace and capacity (mcb_outputs.outcomes rows: victim id,
+ * MCB_OUT_HIT, MCB_OUT_MISS), next_pos: K2's output for the trace.  At every
+ * access where both evict, the victim with the strictly larger next use
+ * wins.  wins: device int64[2] = {A wins, B wins}; the reference's result is
+ * A / (A + B), or 0.5 when both are 0.  Device pointers, asynchronous. */
+int mcb_eviction_duel(mcb_ctx *ctx, const mcb_trace *trace, const uint16_t *outcomes_a,
+                      const uint16_t *outcomes_b, const uint32_t *next_pos, int64_t *wins, void *stream);
+
 /* ---- K7: GPU validate + pack of a decode-only batch (batch-kind .mcbt) ----
  * ids: device uint8 [num_traces][decode_steps][num_layers][top_k] in the
  * reference's event order (trace.py:121-127, one sequence per trace).

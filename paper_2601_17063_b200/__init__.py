@@ -14,6 +14,7 @@ from .engine import (
     SimRun,
     SimulationError,
     cache_size_calc,
+    eviction_quality_duel,
     policy_factory,
     refetch_rate,
     run_simulation,

@@ -41,6 +41,7 @@ EXPORTED_SYMBOLS = (
     "mcb_pack_trace", "mcb_packed_view", "mcb_packed_positions", "mcb_packed_free",
     "mcb_replay", "mcb_replay_host", "mcb_next_use", "mcb_score", "mcb_router_topk", "mcb_gen_reference",
     "mcb_training_data", "mcb_set_lecar", "mcb_lecar_random", "mcb_pack_decode_ids",
+    "mcb_eviction_duel",
 )
 
 
@@ -136,6 +137,7 @@ def load_library():
             "mcb_set_lecar": ([P, ctypes.c_double, ctypes.c_double, i64], ctypes.c_int),
             "mcb_lecar_random": ([i64, i64, P], ctypes.c_int),
             "mcb_pack_decode_ids": ([P, P, i64, i64, i32, i32, i32, P, P, P], ctypes.c_int),
+            "mcb_eviction_duel": ([P, P, P, P, P, P, P], ctypes.c_int),
             "mcb_gen_reference": ([P, i32, i32, i32, i64, i64, i64, i32, ctypes.c_double, P, P, P, P],
                                   ctypes.c_int),
         }

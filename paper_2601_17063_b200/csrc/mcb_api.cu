@@ -99,6 +99,7 @@ struct mcb_ctx {
     double lecar_lr = 0.45, lecar_base = 0.005;
     int64_t lecar_seed = 0, lecar_u_seed = -1, lecar_u_n = 0;
     DevBuf lecar_u, lecar_f;
+    DevBuf diag;                       // K8 duel tables
     std::vector<double> lecar_host;
     cudaEvent_t ev[10] = {};          // start/stop per stage: K2, K3, K4 non-ML, K4 ML, K5
     bool ran[5] = {};
@@ -398,6 +399,16 @@ extern "C" int mcb_score(mcb_ctx *c, const mcb_trace *t, const mcb_nets *nets, i
     int64_t launched = 0;
     if (int rc = run_score(c, d, nets, include_prefill, ranks, scores, s, &launched)) return rc;
     CUDA_TRY(cudaGetLastError());
+    return MCB_OK;
+}
+
+// shared with the other translation units (mcb_diag.cu)
+DevTrace mcb_dev_trace(const mcb_trace *t) { return make_dev_trace(t); }
+int mcb_check_trace(const mcb_trace *t) { return check_trace(t); }
+int mcb_ctx_scratch(mcb_ctx *c, size_t bytes, void **p) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (int rc = c->diag.ensure(bytes)) return rc;
+    *p = c->diag.p;
     return MCB_OK;
 }
 

@@ -377,6 +377,40 @@ def refetch_rate(trace, policy, capacity: int, window: int = 5, nets=None) -> fl
     return simulate(trace, policy, capacity, window=window, nets=nets).refetch_within_w
 
 
+def eviction_quality_duel(trace, policy_a, policy_b, capacity: int, nets=None) -> float:
+    """Victim quality of policy A against policy B (engine.py:404-436).
+
+    Both policies replay on the GPU (default cost and window, as the
+    reference's run_simulation calls); K8 (mcb_eviction_duel) compares the
+    victims' next uses (K2) at every access where both evict.  Returns the
+    fraction of strict wins that are A's, or 0.5 without a strict winner."""
+    import torch
+    from .device import DeviceTrace
+    cost = CostModel()
+    packed = _prepare(trace, cost, [capacity])
+    codes = []
+    for policy in (policy_a, policy_b):
+        name, ep = _resolve(policy, nets)
+        netp = _net_params(ep.nets, packed.num_layers, packed.num_experts) if ep.is_ml else None
+        res = replay_host(packed, [ep.code], [capacity], cost, 5, netp, want_outcomes=True, lecar=ep.lecar)
+        _raise_cell_status(int(res["reports"][0, 0, 0, _lib.R_STATUS]))
+        codes.append(res["outcomes"][0, 0])
+    lib = _lib.load_library()
+    ctx = _lib.context(0)
+    dt = DeviceTrace.from_packed(packed)
+    view = dt.view()
+    stream = torch.cuda.current_stream(0)
+    n = max(packed.total_acc, 1)
+    next_pos = torch.empty(n + 64, dtype=torch.int32, device="cuda")
+    outs = [torch.from_numpy(np.ascontiguousarray(c[:n]).view(np.int16)).to("cuda") for c in codes]
+    wins = torch.zeros(2, dtype=torch.int64, device="cuda")
+    _lib.check(lib.mcb_next_use(ctx, ctypes.byref(view), next_pos.data_ptr(), ctypes.c_void_p(stream.cuda_stream)))
+    _lib.check(lib.mcb_eviction_duel(ctx, ctypes.byref(view), outs[0].data_ptr(), outs[1].data_ptr(),
+                                     next_pos.data_ptr(), wins.data_ptr(), ctypes.c_void_p(stream.cuda_stream)))
+    a, b = (int(v) for v in wins.cpu().tolist())
+    return 0.5 if a + b == 0 else a / (a + b)
+
+
 def sweep(trace, policies: Sequence, capacities: Sequence[int], cost: CostModel = CostModel(), window: int = 5,
           nets=None, jobs: int = 1) -> list:
     """Cross-product evaluation, rows ordered by (policy, capacity) (engine.py:439-465).
@@ -432,5 +466,6 @@ __all__ = [
     "CapacityTooSmallError", "CostModel", "EvictionRecord", "HardwareBudget", "SimReport", "SimRun",
     "SimulationError", "cache_size_calc", "policy_factory", "refetch_rate",
     "run_simulation", "simulate", "step_latency_s", "sweep", "POLICY_NAMES", "replay_host",
+    "eviction_quality_duel",
     "assemble_report", "Phase",
 ]

@@ -131,3 +131,16 @@ def test_oracle_lecar_cases():
     assert sum(r["n_evictions"] for c in cases for r in c["runs"]) > 1000
     for case in cases:
         _check_case(case)
+
+
+def test_oracle_duel_cases():
+    """eviction_quality_duel (engine.py:404-436) restated on the oracle's
+    outcomes, against reference-made fixtures (make_duel_golden.py)."""
+    for case in load("duel_cases.json.gz")["cases"]:
+        header, events = case_trace(case)
+        L, E, K = header
+        for d in case["duels"]:
+            nets = oracle.nets_from_spec(d["nets"], L, E, GOLDEN)
+            got = oracle.eviction_duel(header, events, policy_name(d["a"]), policy_name(d["b"]), d["capacity"],
+                                       nets, lecar_params(d["a"]), lecar_params(d["b"]))
+            assert got == d["value"], (case["name"], d)
