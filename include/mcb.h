@@ -208,6 +208,38 @@ int mcb_set_lecar(mcb_ctx *ctx, double learning_rate, double discount_base, int6
 int mcb_lecar_random(int64_t seed, int64_t n, double *out);
 int mcb_last_timings(mcb_ctx *ctx, float *ms, int32_t n);
 
+/* ---- K10: EvictionNet training (net.py:107-279) ----
+ * All nets of one call train together (the reference trains one net per
+ * layer, cli.py:253-283).  Device pointers, asynchronous on `stream`.
+ * params / adam_m / adam_v: float64 [num_nets][P] in .evnet order (w1, b1,
+ * w2, b2, w3, b3; P = H*2E + H + H*H + H + E*H + E). */
+typedef struct {
+    int32_t num_nets, num_experts, hidden, reserved;
+    int64_t num_samples;          /* rows per net */
+    const double *features;       /* [net][num_samples][2E] */
+    const double *targets;        /* [net][num_samples][E] */
+    const uint8_t *masks;         /* [net][num_samples][E] (0 / 1) */
+} mcb_train_data;
+typedef struct {
+    double learning_rate, weight_decay, beta1, beta2, eps;   /* AdamW (net.py:159-170) */
+    int64_t batch_size;
+    int64_t n_train;              /* the first n_train rows train (net.py:219-226) */
+} mcb_train_cfg;
+/* One epoch (net.py:245-256): mini-batches of rows order[start : start + batch]
+ * (order: device int32 [n_train], the epoch's permutation), forward, masked
+ * MSE gradient, backward, AdamW step (optimizer step count before the epoch =
+ * step0).  bad: device float64 [num_nets][4] = {flag, loss, batch offset, epoch}
+ * of the first non-finite batch loss (NonFiniteLossError, net.py:250-254);
+ * zero it before the first epoch. */
+int mcb_train_epoch(mcb_ctx *ctx, const mcb_train_data *data, const mcb_train_cfg *cfg, double *params,
+                    double *adam_m, double *adam_v, int64_t step0, int64_t epoch, const int32_t *order, double *bad,
+                    void *stream);
+/* Masked-MSE sums over rows [row0, row0 + rows) of every net (evaluate,
+ * net.py:236-239): sums: device float64 [num_nets][2] = {sum m (pred - y)^2,
+ * sum m}. */
+int mcb_train_eval(mcb_ctx *ctx, const mcb_train_data *data, const double *params, int64_t row0, int64_t rows,
+                   double *sums, void *stream);
+
 /* ---- K8: eviction_quality_duel (engine.py:404-436) ----
  * outcomes_a / outcomes_b: two policies' per-access outcome codes of the
  * same trace and capacity (mcb_outputs.outcomes rows: victim id,

@@ -39,6 +39,14 @@ from .trace import (
     packed_from_decode_ids,
 )
 
+from .train import (
+    EmptyDatasetError,
+    NonFiniteLossError,
+    TrainConfig,
+    TrainResult,
+    train_eviction_net,
+    train_eviction_nets,
+)
 from .tracefile import (
     load_packed,
     parse_trace,

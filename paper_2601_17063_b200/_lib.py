@@ -41,12 +41,24 @@ EXPORTED_SYMBOLS = (
     "mcb_pack_trace", "mcb_packed_view", "mcb_packed_positions", "mcb_packed_free",
     "mcb_replay", "mcb_replay_host", "mcb_next_use", "mcb_score", "mcb_router_topk", "mcb_gen_reference",
     "mcb_training_data", "mcb_set_lecar", "mcb_lecar_random", "mcb_pack_decode_ids",
-    "mcb_eviction_duel",
+    "mcb_eviction_duel", "mcb_train_epoch", "mcb_train_eval",
 )
 
 
 class EngineUnavailableError(RuntimeError):
     """libmcb.so or a CUDA device is missing; the engine has no CPU fallback."""
+
+
+class MCBTrainData(ctypes.Structure):
+    _fields_ = [("num_nets", ctypes.c_int32), ("num_experts", ctypes.c_int32), ("hidden", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("num_samples", ctypes.c_int64), ("features", ctypes.c_void_p),
+                ("targets", ctypes.c_void_p), ("masks", ctypes.c_void_p)]
+
+
+class MCBTrainCfg(ctypes.Structure):
+    _fields_ = [("learning_rate", ctypes.c_double), ("weight_decay", ctypes.c_double),
+                ("beta1", ctypes.c_double), ("beta2", ctypes.c_double), ("eps", ctypes.c_double),
+                ("batch_size", ctypes.c_int64), ("n_train", ctypes.c_int64)]
 
 
 class MCBTrace(ctypes.Structure):
@@ -138,6 +150,8 @@ def load_library():
             "mcb_lecar_random": ([i64, i64, P], ctypes.c_int),
             "mcb_pack_decode_ids": ([P, P, i64, i64, i32, i32, i32, P, P, P], ctypes.c_int),
             "mcb_eviction_duel": ([P, P, P, P, P, P, P], ctypes.c_int),
+            "mcb_train_epoch": ([P, P, P, P, P, P, i64, i64, P, P, P], ctypes.c_int),
+            "mcb_train_eval": ([P, P, P, i64, i64, P, P], ctypes.c_int),
             "mcb_gen_reference": ([P, i32, i32, i32, i64, i64, i64, i32, ctypes.c_double, P, P, P, P],
                                   ctypes.c_int),
         }

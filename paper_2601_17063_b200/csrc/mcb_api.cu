@@ -4,6 +4,7 @@
 // mcb_replay mirrors engine.sweep (pkg/src/moecache/engine.py:439-465) over
 // the policies x capacities cross product for every trace of a packed batch;
 // the per-cell arithmetic is engine.run_simulation (engine.py:300-380).
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -100,6 +101,8 @@ struct mcb_ctx {
     int64_t lecar_seed = 0, lecar_u_seed = -1, lecar_u_n = 0;
     DevBuf lecar_u, lecar_f;
     DevBuf diag;                       // K8 duel tables
+    DevBuf train_ws[2];                // K10 training / evaluation workspaces
+    cublasHandle_t cublas = nullptr;   // K10 batched DGEMMs
     std::vector<double> lecar_host;
     cudaEvent_t ev[10] = {};          // start/stop per stage: K2, K3, K4 non-ML, K4 ML, K5
     bool ran[5] = {};
@@ -259,8 +262,10 @@ extern "C" int mcb_ctx_destroy(mcb_ctx *c) {
                      &c->tile_off, &c->stats, &c->pol_caps, &c->h_acc, &c->h_acc_off, &c->h_ev_off,
                      &c->h_rt_off, &c->h_ev_info, &c->h_routed, &c->h_params, &c->h_reports, &c->h_latency,
                      &c->h_chain_reports, &c->h_hashes, &c->h_outcomes, &c->seg_snap, &c->seg_summ,
-                     &c->seg_out, &c->seg_codes, &c->nu_scratch};
+                     &c->seg_out, &c->seg_codes, &c->nu_scratch, &c->lecar_u, &c->lecar_f, &c->diag,
+                     &c->train_ws[0], &c->train_ws[1]};
     for (DevBuf *b : all) b->release();
+    if (c->cublas) cublasDestroy(c->cublas);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->side) cudaStreamDestroy(c->side);
 
@@ -405,6 +410,17 @@ extern "C" int mcb_score(mcb_ctx *c, const mcb_trace *t, const mcb_nets *nets, i
 // shared with the other translation units (mcb_diag.cu)
 DevTrace mcb_dev_trace(const mcb_trace *t) { return make_dev_trace(t); }
 int mcb_check_trace(const mcb_trace *t) { return check_trace(t); }
+int mcb_ctx_scratch_named(mcb_ctx *c, int slot, size_t bytes, void **p) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (int rc = c->train_ws[slot].ensure(bytes)) return rc;
+    *p = c->train_ws[slot].p;
+    return MCB_OK;
+}
+cublasHandle_t mcb_ctx_cublas(mcb_ctx *c) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!c->cublas && cublasCreate(&c->cublas) != CUBLAS_STATUS_SUCCESS) c->cublas = nullptr;
+    return c->cublas;
+}
 int mcb_ctx_scratch(mcb_ctx *c, size_t bytes, void **p) {
     std::lock_guard<std::mutex> lk(c->mu);
     if (int rc = c->diag.ensure(bytes)) return rc;

@@ -168,3 +168,13 @@ def test_lecar_random_stream_matches_python():
         r = random.Random(seed)
         want = np.array([r.random() for _ in range(2000)])
         assert np.array_equal(_lib.lecar_random(seed, 2000), want), seed
+
+
+def test_trainer_input_errors_without_gpu():
+    """EmptyDatasetError / ShapeMismatchError before any device work (net.py:214-221)."""
+    from paper_2601_17063_b200 import train
+    net = mcb.EvictionNet(4, hidden=8)
+    with pytest.raises(train.EmptyDatasetError):
+        train.train_eviction_net(net, np.zeros((0, 8)), np.zeros((0, 4)), np.zeros((0, 4), bool))
+    with pytest.raises(mcb.ShapeMismatchError):
+        train.train_eviction_net(net, np.zeros((3, 6)), np.zeros((3, 4)), np.zeros((3, 4), bool))
