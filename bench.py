@@ -36,6 +36,9 @@ WORKLOADS = {
     # configs[0]: Qwen3-30B-A3B-shaped, 2K tokens, C=32
     "c1": dict(name="c1-qwen3-30b-a3b-shaped", L=48, E=128, K=8, T=2048, d=2048, traces=1, caps=[32],
                scaling="weak"),
+    # configs[2]: OLMoE-1B-7B-shaped, 1M tokens, C in {16, 32} (ML vs Belady, LRU/LFU for context)
+    "c3": dict(name="c3-olmoe-1b-7b-shaped", L=16, E=64, K=8, T=1048576, d=2048, traces=1, caps=[16, 32],
+               scaling="weak"),
     # configs[3]: DeepSeek-V2-Lite-shaped, 4096 traces x 2048 tokens, C=16 (traces sharded over ranks)
     "c4": dict(name="c4-deepseek-v2-lite-shaped", L=27, E=64, K=6, T=2048, d=2048, traces=4096, caps=[16],
                scaling="strong"),

@@ -192,6 +192,9 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
 /* MCB_TUNE_SERIAL: 1 = run every stage on the caller's stream (no concurrent
  * side stream), so mcb_last_timings attributes time to each stage alone. */
 #define MCB_TUNE_SERIAL 5
+/* MCB_TUNE_K3_CTAS: scorer grid -- < 0 (default) = one CTA per 32-event tile;
+ * 0 = persistent, every CTA that fits; k > 0 = persistent, at most k per SM. */
+#define MCB_TUNE_K3_CTAS 6
 int mcb_set_tuning(mcb_ctx *ctx, int32_t knob, int64_t value);
 /* LeCaR parameters used by the MCB_LECAR cells of later mcb_replay calls on
  * this context (LeCaRPolicy.__init__, policies.py:333-349; defaults 0.45,

@@ -193,6 +193,10 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
         c->serial = value != 0;
         return MCB_OK;
     }
+    if (knob == MCB_TUNE_K3_CTAS) {
+        set_k3_ctas((int)value);
+        return MCB_OK;
+    }
     if (knob == MCB_TUNE_GROUP_LANES) {
         if (value != 0 && value != 8 && value != 16 && value != 32)
             return mcb_set_error(MCB_ERR_INVALID, "lane group must be 0, 8, 16 or 32");
@@ -240,6 +244,7 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     if (const char *env = getenv("MCB_SEG_NW")) c->seg_nw = atoll(env);
     if (const char *env = getenv("MCB_SEG_PASSES")) c->seg_passes = atoll(env);
     if (const char *env = getenv("MCB_GROUP_LANES")) c->group_lanes = atoll(env);
+    if (const char *env = getenv("MCB_K3_CTAS")) set_k3_ctas(atoi(env));
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);   // replay warps dispatch ahead of K3 blocks
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||

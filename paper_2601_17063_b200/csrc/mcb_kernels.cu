@@ -750,7 +750,8 @@ int launch_replay(const ReplayParams &p, cudaStream_t s) {
     // latency-bound, and a whole warp per instance has the shorter per-access
     // critical path (lane-parallel victim search, no divergence).
     const int64_t n_inst = (p.chain_hi - p.chain_lo) * p.n_pol_launch * p.n_cap;
-    const bool solo_ok = p.tr.total_acc < (1ll << 27) && n_inst >= p.solo_min_instances && p.window >= 0 &&
+    const int64_t chain_bound = p.tr.uniform ? p.tr.T * p.tr.K : p.tr.total_acc;   // longest chain (upper bound)
+    const bool solo_ok = chain_bound < (1ll << 27) && n_inst >= p.solo_min_instances && p.window >= 0 &&
                          p.window <= SOLO_WMAX;
     if (E <= 8 && solo_ok) { launch_solo_t<8>(p, s); return 1; }
     if (E <= 16 && solo_ok) { launch_solo_t<16>(p, s); return 1; }
@@ -1661,6 +1662,16 @@ int launch_score_prep(const DevTrace &tr, int include_prefill, int32_t *snaps, i
 
 // K3 part 2: score tiles [tile_lo, tile_hi) (persistent CTAs).  Uniform
 // traces number tiles chain-major, so a chain range maps to a tile range.
+// K3 grid: < 0 (default) = one CTA per 32-event tile; 0 = persistent, as
+// many CTAs as fit (4 per SM for the specialised shapes); k > 0 = persistent
+// with at most k CTAs per SM.  Measured on C2 (tools/k3_sweep.sh): one CTA
+// per tile is faster alone (4.12 vs 4.51 ms: better tail balance) and lets
+// the concurrent non-ML replay's blocks in as CTAs retire (persistent CTAs
+// hold the whole register file, so the replay waited for K3): 6.09 vs 6.55
+// ms per step.
+static int g_k3_ctas = -1;
+void set_k3_ctas(int v) { g_k3_ctas = v; }
+
 int launch_score_tiles(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill,
                        uint8_t *ranks, double *scores, const int32_t *snaps, const int64_t *tile_off,
                        int64_t tile_lo, int64_t tile_hi, unsigned long long *uncertain, cudaStream_t s) {
@@ -1671,7 +1682,9 @@ int launch_score_tiles(const DevTrace &tr, const double *wt, int H, int num_nets
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)fn, 256, smem);
-    const int64_t grid = std::min<int64_t>(tile_hi - tile_lo, (int64_t)n_sm * (per_sm > 0 ? per_sm : 1));
+    if (g_k3_ctas > 0 && g_k3_ctas < per_sm) per_sm = g_k3_ctas;
+    const int64_t grid = g_k3_ctas < 0 ? tile_hi - tile_lo
+                                       : std::min<int64_t>(tile_hi - tile_lo, (int64_t)n_sm * (per_sm > 0 ? per_sm : 1));
     fn<<<(unsigned)grid, 256, smem, s>>>(tr, wt, H, num_nets, include_prefill, tile_off, snaps, tile_lo, tile_hi,
                                          ranks, scores, uncertain);
     return 1;

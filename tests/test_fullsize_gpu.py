@@ -114,3 +114,36 @@ def test_full_size_state_dependent_policies(shape):
     for i, c in enumerate(sample):
         assert np.array_equal(cr[c].reshape(len(jobs), _lib.R_N)[:, :7], cnt[i]), c
         assert np.array_equal(res["hashes"][c].reshape(len(jobs)), hsh[i]), c
+
+
+def test_full_size_c3():
+    """C3 (BASELINE.json configs[2], OLMoE-shaped L=16, E=64, K=8, 1,048,576
+    tokens, C in {16, 32}): segmented and whole-chain replays identical on every
+    chain for all four policies; reference properties on every chain; the
+    first and last layers against the C oracle for LRU / LFU / Belady at full
+    length (8.4M accesses per chain)."""
+    L, E, K, T, d, caps = 16, 64, 8, 1 << 20, 2048, [16, 32]
+    ids = make_ids(L, E, K, T, d, seed=7)
+    packed = mcb.packed_from_decode_ids(ids, E)
+    nets = oracle.nets_from_spec({"kind": "per_layer_seed"}, L, E)
+    seg = replay(packed, caps, nets, True)
+    whole = replay(packed, caps, nets, False)
+    cr = seg["chain_reports"]
+    assert np.all(cr[..., _lib.R_STATUS] == 0)
+    assert np.array_equal(cr, whole["chain_reports"])
+    assert np.array_equal(seg["hashes"], whole["hashes"])
+    assert np.array_equal(seg["latency"], whole["latency"])
+    misses, hits = cr[..., _lib.R_DM], cr[..., _lib.R_DH]
+    assert np.array_equal(cr[..., _lib.R_EVICT], np.maximum(0, misses - np.array(caps)[None, None, :]))
+    assert np.all(np.diff(hits, axis=2) >= 0)
+    bel = hits[:, POLS.index("belady")]
+    for p in ("lru", "lfu"):
+        assert np.all(bel >= hits[:, POLS.index(p)]), p
+    sample = [0, L - 1]
+    sub = np.ascontiguousarray(ids[sample])
+    jobs = [(p, c) for p in ("lru", "lfu", "belady") for c in caps]
+    cnt, lat, hsh = oracle.replay_uniform(sub, len(sample), E, jobs, None, 5, None, hash_kind="poly")
+    for i, c in enumerate(sample):
+        got = cr[c, :3].reshape(len(jobs), _lib.R_N)[:, :7]
+        assert np.array_equal(got, cnt[i]), c
+        assert np.array_equal(seg["hashes"][c, :3].reshape(len(jobs)), hsh[i]), c
