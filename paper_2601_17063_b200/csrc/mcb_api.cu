@@ -75,6 +75,8 @@ struct DevBuf {
     }
 };
 
+#define MCB_MAX_ML_CHUNKS 8
+
 struct mcb_ctx {
     int device = 0;
     std::mutex mu;
@@ -88,6 +90,10 @@ struct mcb_ctx {
     bool timing = false;
     cudaStream_t side = nullptr;       // non-ML replay runs here concurrently with K3
     cudaEvent_t fork = nullptr, join = nullptr;
+    cudaStream_t side2 = nullptr;      // ML replay chunks, pipelined behind the K3 chunks
+    cudaEvent_t chunk_ev[MCB_MAX_ML_CHUNKS] = {};
+    cudaEvent_t join2 = nullptr;
+    int64_t ml_chunks = 1;             // K3 / ML replay pipeline depth (MCB_TUNE_ML_CHUNKS)
     int64_t solo_min_instances = 0;   // thread-per-instance whenever E <= 16 (MCB_SOLO_MIN overrides)
     int64_t seg_ev = 0;               // segmented replay: 0 auto, <0 off, >0 events per segment (MCB_SEG_EV)
     int64_t seg_nw = 0;               // warm-up events before each segment: 0 auto (MCB_SEG_NW)
@@ -193,6 +199,10 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
         c->serial = value != 0;
         return MCB_OK;
     }
+    if (knob == MCB_TUNE_ML_CHUNKS) {
+        c->ml_chunks = value;
+        return MCB_OK;
+    }
     if (knob == MCB_TUNE_K3_CTAS) {
         set_k3_ctas((int)value);
         return MCB_OK;
@@ -245,10 +255,18 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     if (const char *env = getenv("MCB_SEG_PASSES")) c->seg_passes = atoll(env);
     if (const char *env = getenv("MCB_GROUP_LANES")) c->group_lanes = atoll(env);
     if (const char *env = getenv("MCB_K3_CTAS")) set_k3_ctas(atoi(env));
+    if (const char *env = getenv("MCB_ML_CHUNKS")) c->ml_chunks = atoll(env);
+    for (auto &e : c->chunk_ev)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+            delete c;
+            return mcb_set_error(MCB_ERR_CUDA, "event creation failed");
+        }
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);   // replay warps dispatch ahead of K3 blocks
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c->side2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->join2, cudaEventDisableTiming) != cudaSuccess ||
 
         cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess) {
@@ -273,6 +291,10 @@ extern "C" int mcb_ctx_destroy(mcb_ctx *c) {
     if (c->cublas) cublasDestroy(c->cublas);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->side) cudaStreamDestroy(c->side);
+    if (c->side2) cudaStreamDestroy(c->side2);
+    if (c->join2) cudaEventDestroy(c->join2);
+    for (auto &e : c->chunk_ev)
+        if (e) cudaEventDestroy(e);
 
     if (c->fork) cudaEventDestroy(c->fork);
     if (c->join) cudaEventDestroy(c->join);
@@ -580,12 +602,48 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         mark(c, 5, sn);
         c->ran[2] = true;
     }
-    if (Pm.n_pol_launch > 0) {
+    // K3 / ML-replay pipeline: the chains are cut into ml_chunks ranges; K3
+    // scores them in order on s and the ML replay of a range starts on side2
+    // as soon as its ranks are written, overlapping K3 on the next range
+    // (uniform traces, one ML variant).  Off by default: measured on C2
+    // (tools/chunk_sweep.sh) 1 / 2 / 4 / 8 chunks = 6.09 / 6.12 / 6.34 / 8.28 ms
+    // per step -- a chunk's segmented ML replay is latency-bound (its finish
+    // walk is sequential over the segments), so it costs nearly as much as
+    // the whole replay and the overlap does not pay.
+    const int n_chunks = (Pm.n_pol_launch > 0 && d.uniform && !c->serial && !(need_ml[0] && need_ml[1]))
+                             ? (int)std::min<int64_t>(std::min<int64_t>(c->ml_chunks, MCB_MAX_ML_CHUNKS), d.n_chains)
+                             : 1;
+    if (Pm.n_pol_launch > 0 && n_chunks > 1) {
+        const int v = need_ml[0] ? 0 : 1;
+        if (int rc = check_nets(d, nets)) return rc;
+        mark(c, 2, s);
+        launched += launch_prepare_nets(nets->params, d.E, nets->hidden, nets->num_nets, (double *)c->wt.p, s);
+        const int64_t tiles = max_score_tiles(d);
+        launched += launch_score_prep(d, v == 0 ? 1 : 0, (int32_t *)c->snaps.p, (int64_t *)c->tile_off.p, tiles, s);
+        Pm.rank[v] = (const uint8_t *)c->ranks[v].p;
+        const int64_t tpc = (d.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
+        for (int k = 0; k < n_chunks; ++k) {
+            const int64_t lo = d.n_chains * k / n_chunks, hi = d.n_chains * (k + 1) / n_chunks;
+            launched += launch_score_tiles(d, (const double *)c->wt.p, nets->hidden, nets->num_nets, v == 0 ? 1 : 0,
+                                           (uint8_t *)c->ranks[v].p, nullptr, (const int32_t *)c->snaps.p,
+                                           (const int64_t *)c->tile_off.p, lo * tpc, hi * tpc,
+                                           (unsigned long long *)c->stats.p, s);
+            CUDA_TRY(cudaEventRecord(c->chunk_ev[k], s));
+            CUDA_TRY(cudaStreamWaitEvent(c->side2, c->chunk_ev[k], 0));
+            if (k == 0) mark(c, 6, c->side2);
+            ReplayParams Pk = Pm;
+            Pk.chain_lo = lo;
+            Pk.chain_hi = hi;
+            launched += seg_eligible(Pk) ? launch_replay_segmented(Pk, c->side2) : launch_replay(Pk, c->side2);
+        }
+        mark(c, 3, s);
+        mark(c, 7, c->side2);
+        CUDA_TRY(cudaEventRecord(c->join2, c->side2));
+        CUDA_TRY(cudaStreamWaitEvent(s, c->join2, 0));
+        c->ran[1] = true;
+        c->ran[3] = true;
+    } else if (Pm.n_pol_launch > 0) {
         // The ML replay needs K3's ranks; it follows K3 on the same stream.
-        // (Pipelining K3 chunks with per-chunk ML replays -- whole replays, or
-        // only the speculation with one finish walk -- was measured slower: the
-        // speculation and the walk are latency-bound per thread / instance, so
-        // every chunk pays their latency again.)
         mark(c, 2, s);
         for (int v = 0; v < 2; ++v) {
             if (!need_ml[v]) continue;
