@@ -46,3 +46,24 @@ for k, n in L.most_common(top):
 print("-- by stall samples")
 for k, n in W.most_common(top):
     print(f"{L[k] / tot * 100:5.1f}% inst {n / tw * 100:5.1f}% stall  {k}")
+
+# optional phase split: --ranges name:lo-hi,name:lo-hi (lines of the main file)
+if len(sys.argv) > 3:
+    spans = []
+    for part in sys.argv[3].split(","):
+        name, rng = part.split(":")
+        lo, hi = (int(x) for x in rng.split("-"))
+        spans.append((name, lo, hi))
+    agg_i, agg_w = collections.Counter(), collections.Counter()
+    for k in L:
+        name = "other"
+        if k and k[0] == "mcb_kernels.cu":
+            for nm, lo, hi in spans:
+                if lo <= k[1] <= hi:
+                    name = nm
+                    break
+        agg_i[name] += L[k]
+        agg_w[name] += W[k]
+    print("-- by phase")
+    for name in [s[0] for s in spans] + ["other"]:
+        print(f"{name:10s} {agg_i[name] / tot * 100:5.1f}% inst {agg_w[name] / tw * 100:5.1f}% stall")
