@@ -965,37 +965,40 @@ __global__ void __launch_bounds__(128) k_feat_snap(DevTrace tr, int include_pref
     }
 }
 
-// exp(x) for x <= 0 in float64, branch-free, table-driven: k = rint(32 x /
-// ln2), x = k ln2/32 + r with |r| <= ln2/64, exp(x) = 2^(k>>5) * T[k&31] *
-// exp(r) with T[j] = 2^(j/32) (shared-memory table) and exp(r) by its
-// degree-6 Taylor polynomial (truncation < 2^-58).  Within a few ulp of the
-// correctly rounded exp for x >= -708.
-__device__ double g_exp2_32[32] = {
-    1.0, 1.0218971486541166, 1.0442737824274138, 1.0671404006768237, 1.0905077326652577, 1.1143867425958924,
-    1.1387886347566916, 1.1637248587775775, 1.189207115002721, 1.215247359980469, 1.241857812073484,
-    1.2690509571917332, 1.2968395546510096, 1.3252366431597413, 1.3542555469368927, 1.383909881963832,
-    1.4142135623730951, 1.4451808069770467, 1.4768261459394993, 1.5091644275934228, 1.5422108254079407,
-    1.5759808451078865, 1.6104903319492543, 1.645755478153965, 1.681792830507429, 1.718619298122478,
-    1.7562521603732995, 1.7947090750031072, 1.8340080864093424, 1.8741676341103, 1.9152065613971474,
-    1.9571441241754002};
+// exp(x) for x <= 0 in float64, branch-free, table-driven: k = rint(64 x /
+// ln2), x = k ln2/64 + r with |r| <= ln2/128, exp(x) = 2^(k>>6) * T[k&63] *
+// exp(r) with T[j] = 2^(j/64) (shared-memory table, correctly rounded) and
+// exp(r) by its degree-5 Taylor polynomial (truncation < 2^-54).  Within a
+// few ulp of the correctly rounded exp for x >= -708.
+__device__ double g_exp2_64[64] = {
+    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284, 1.0442737824274138, 1.0556451783605572,
+    1.0671404006768237, 1.0787607977571199, 1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
+    1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812, 1.189207115002721, 1.202156731452703,
+    1.215247359980469, 1.22848053610687, 1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
+    1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303, 1.3542555469368927, 1.3690024229745905,
+    1.383909881963832, 1.3989796725383112, 1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
+    1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384, 1.5422108254079407, 1.559004400237837,
+    1.5759808451078865, 1.593142151342267, 1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
+    1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062, 1.7562521603732995, 1.7753764925265212,
+    1.7947090750031072, 1.8142521755003989, 1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
+    1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
 __device__ __forceinline__ double exp_nonpos(double x, const double *tab) {
     // literal coefficients: they become constant-bank operands of the DFMAs
     // (no separate uniform loads); x < -708 is clamped (its logistic is below
     // 1e-307, so the SiLU output differs from the reference's by < 1e-304
     // absolute, far below the ulp of any score)
     x = fmax(x, -708.0);
-    const double kd = rint(x * 46.16624130844683);                 // 32 / ln2
-    double r = fma(kd, -0.02166084939249829, x);                   // -(ln2/32) hi
-    r = fma(kd, -7.247021293269686e-19, r);                        // -(ln2/32) lo
-    double p = fma(1.0 / 720.0, r, 1.0 / 120.0);
-    p = fma(p, r, 1.0 / 24.0);
+    const double kd = rint(x * 92.33248261689366);                 // 64 / ln2
+    double r = fma(kd, -0.010830424696249145, x);                  // -(ln2/64) hi
+    r = fma(kd, -3.623510646634843e-19, r);                        // -(ln2/64) lo
+    double p = fma(1.0 / 120.0, r, 1.0 / 24.0);
     p = fma(p, r, 1.0 / 6.0);
     p = fma(p, r, 0.5);
     p = fma(p, r, 1.0);
     p = fma(p, r, 1.0);
     const int k = (int)kd;
-    const double m = __dmul_rn(tab[k & 31], p);
-    const int hi = __double2hiint(m) + ((k >> 5) << 20);
+    const double m = __dmul_rn(tab[k & 63], p);
+    const int hi = __double2hiint(m) + ((k >> 6) << 20);
     return __hiloint2double(hi, __double2loint(m));
 }
 
@@ -1465,8 +1468,8 @@ __global__ void __launch_bounds__(256, TE ? 4 : 1) k_score_tile(DevTrace tr, con
     uint8_t *s_rank = (uint8_t *)(bufB + ldB * MCB_TILE_EV);  // [TILE][E]
     int32_t *s_flag = (int32_t *)(s_rank + MCB_TILE_EV * MCB_MAX_EXPERTS);  // [TILE]
 
-    __shared__ double s_exp2[32];
-    if (threadIdx.x < 32) s_exp2[threadIdx.x] = g_exp2_32[threadIdx.x];   // visible after the first barrier
+    __shared__ double s_exp2[64];
+    if (threadIdx.x < 64) s_exp2[threadIdx.x] = g_exp2_64[threadIdx.x];   // visible after the first barrier
     // persistent: each CTA walks tiles blockIdx.x, blockIdx.x + gridDim.x, ...
     for (int64_t tile_it = tile_lo + blockIdx.x; tile_it < tile_hi; tile_it += gridDim.x) {
     int64_t tile = tile_it;
