@@ -1121,10 +1121,11 @@ __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double
                  : "d"(a), "d"(b));
 }
 
-template <int NTW>
-__device__ __forceinline__ void mma_layer(const double *A, int lda, int K, const double *__restrict__ Wt,
+template <int NTW, int KC = 0>
+__device__ __forceinline__ void mma_layer(const double *A, int lda, int K_rt, const double *__restrict__ Wt,
                                           const double *__restrict__ bias, int N, double *O, int ldo, bool act,
                                           const double *tab) {
+    const int K = KC ? KC : K_rt;   // compile-time depth: the k-loop unrolls fully, addresses fold
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, q = lane & 3;
     const int NT = N >> 3;
@@ -1150,7 +1151,7 @@ __device__ __forceinline__ void mma_layer(const double *A, int lda, int K, const
     for (int mt = 0; mt < 4; ++mt) a[mt] = arow[mt * 8 * lda];
 #pragma unroll
     for (int j = 0; j < NTW; ++j) b[j] = have[j] ? __ldg(wcol + col[j]) : 0.0;
-#pragma unroll 8
+#pragma unroll (KC ? 16 : 8)
     for (int k0 = 0; k0 < K; k0 += 4) {
         double an[4], bn[NTW];
         const int kn = k0 + 4 < K ? k0 + 4 : k0;
@@ -1190,9 +1191,11 @@ __device__ __forceinline__ void mma_layer(const double *A, int lda, int K, const
 // Narrow layer (N <= 16: the score layer for E <= 16): one 8x8 output tile
 // per warp (up to 8 tiles = 4 m-tiles x N/8), two accumulators over
 // alternating k-steps so consecutive DMMAs are independent.
-__device__ __forceinline__ void mma_layer_narrow(const double *A, int lda, int K, const double *__restrict__ Wt,
+template <int KC = 0>
+__device__ __forceinline__ void mma_layer_narrow(const double *A, int lda, int K_rt, const double *__restrict__ Wt,
                                                  const double *__restrict__ bias, int N, double *O, int ldo,
                                                  bool act, const double *tab) {
+    const int K = KC ? KC : K_rt;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, q = lane & 3;
     const int NT = N >> 3;
@@ -1201,7 +1204,7 @@ __device__ __forceinline__ void mma_layer_narrow(const double *A, int lda, int K
     const double *arow = A + (mt * 8 + g) * lda + q;
     const double *wcol = Wt + (int64_t)q * N + nt * 8 + g;
     double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
-#pragma unroll 8
+#pragma unroll (KC ? 32 : 8)
     for (int k0 = 0; k0 < K; k0 += 8) {
         const double a0 = arow[k0], b0 = __ldg(wcol + (int64_t)k0 * N);
         const bool two = k0 + 4 < K;
@@ -1225,6 +1228,17 @@ __device__ __forceinline__ void mma_layer_any(const double *A, int lda, int K, c
     else if (NT <= 8) mma_layer<1>(A, lda, K, Wt, bias, N, O, ldo, act, tab);
     else if (NT <= 16) mma_layer<2>(A, lda, K, Wt, bias, N, O, ldo, act, tab);
     else mma_layer<4>(A, lda, K, Wt, bias, N, O, ldo, act, tab);
+}
+
+// the same with the layer shape known at compile time (specialised scorers)
+template <int N, int KC>
+__device__ __forceinline__ void mma_layer_fixed(const double *A, int lda, const double *Wt, const double *bias,
+                                                double *O, int ldo, bool act, const double *tab) {
+    constexpr int NT = N >> 3;
+    if constexpr (NT <= 2) mma_layer_narrow<KC>(A, lda, KC, Wt, bias, N, O, ldo, act, tab);
+    else if constexpr (NT <= 8) mma_layer<1, KC>(A, lda, KC, Wt, bias, N, O, ldo, act, tab);
+    else if constexpr (NT <= 16) mma_layer<2, KC>(A, lda, KC, Wt, bias, N, O, ldo, act, tab);
+    else mma_layer<4, KC>(A, lda, KC, Wt, bias, N, O, ldo, act, tab);
 }
 
 __host__ __device__ __forceinline__ int mlp_ld(int cols) { return (cols + 15) / 16 * 16 + 4; }
@@ -1561,12 +1575,22 @@ __global__ void __launch_bounds__(256, TE ? 4 : 1) k_score_tile(DevTrace tr, con
     const double *wt = wt_all + (num_nets == 1 ? 0 : layer) * (int64_t)prepared_net_doubles(E, H);
     const double *Wt1 = wt, *b1 = Wt1 + (int64_t)Kp1 * Hp, *Wt2 = b1 + Hp, *b2 = Wt2 + (int64_t)Hp * Hp,
                  *Wt3 = b2 + Hp, *b3 = Wt3 + (int64_t)Hp * Ep;
-    mma_layer_any(bufA, ldA, Kp1, Wt1, b1, Hp, bufB, ldB, true, s_exp2);    // h1 -> B
-    __syncthreads();
-    mma_layer_any(bufB, ldB, Hp, Wt2, b2, Hp, bufB, ldB, true, s_exp2);     // h2 -> B (in place)
-    __syncthreads();
-    mma_layer_any(bufB, ldB, Hp, Wt3, b3, Ep, bufA, ldA, false, s_exp2);    // scores -> A
-    __syncthreads();
+    if constexpr (TE > 0 && TH > 0) {
+        constexpr int cHp = (TH + 7) / 8 * 8, cKp1 = (2 * TE + 3) / 4 * 4, cEp = (TE + 7) / 8 * 8;
+        mma_layer_fixed<cHp, cKp1>(bufA, ldA, Wt1, b1, bufB, ldB, true, s_exp2);    // h1 -> B
+        __syncthreads();
+        mma_layer_fixed<cHp, cHp>(bufB, ldB, Wt2, b2, bufB, ldB, true, s_exp2);     // h2 -> B (in place)
+        __syncthreads();
+        mma_layer_fixed<cEp, cHp>(bufB, ldB, Wt3, b3, bufA, ldA, false, s_exp2);    // scores -> A
+        __syncthreads();
+    } else {
+        mma_layer_any(bufA, ldA, Kp1, Wt1, b1, Hp, bufB, ldB, true, s_exp2);    // h1 -> B
+        __syncthreads();
+        mma_layer_any(bufB, ldB, Hp, Wt2, b2, Hp, bufB, ldB, true, s_exp2);     // h2 -> B (in place)
+        __syncthreads();
+        mma_layer_any(bufB, ldB, Hp, Wt3, b3, Ep, bufA, ldA, false, s_exp2);    // scores -> A
+        __syncthreads();
+    }
     for (int i = tid; i < MCB_TILE_EV; i += blockDim.x) s_flag[i] = 0;
     __syncthreads();
     if (E <= 16) {
