@@ -94,6 +94,7 @@ struct mcb_ctx {
     cudaEvent_t chunk_ev[MCB_MAX_ML_CHUNKS] = {};
     cudaEvent_t join2 = nullptr;
     int64_t ml_chunks = 1;             // K3 / ML replay pipeline depth (MCB_TUNE_ML_CHUNKS)
+    int k3_ctas = -1;                  // K3 grid mode (MCB_TUNE_K3_CTAS)
     int64_t solo_min_instances = 0;   // thread-per-instance whenever E <= 16 (MCB_SOLO_MIN overrides)
     int64_t seg_ev = 0;               // segmented replay: 0 auto, <0 off, >0 events per segment (MCB_SEG_EV)
     int64_t seg_nw = 0;               // warm-up events before each segment: 0 auto (MCB_SEG_NW)
@@ -204,7 +205,7 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
         return MCB_OK;
     }
     if (knob == MCB_TUNE_K3_CTAS) {
-        set_k3_ctas((int)value);
+        c->k3_ctas = (int)value;
         return MCB_OK;
     }
     if (knob == MCB_TUNE_GROUP_LANES) {
@@ -254,7 +255,7 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     if (const char *env = getenv("MCB_SEG_NW")) c->seg_nw = atoll(env);
     if (const char *env = getenv("MCB_SEG_PASSES")) c->seg_passes = atoll(env);
     if (const char *env = getenv("MCB_GROUP_LANES")) c->group_lanes = atoll(env);
-    if (const char *env = getenv("MCB_K3_CTAS")) set_k3_ctas(atoi(env));
+    if (const char *env = getenv("MCB_K3_CTAS")) c->k3_ctas = atoi(env);
     if (const char *env = getenv("MCB_ML_CHUNKS")) c->ml_chunks = atoll(env);
     for (auto &e : c->chunk_ev)
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
@@ -395,7 +396,7 @@ static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int in
     const int64_t tiles = max_score_tiles(d);
     const int n = launch_score(d, (const double *)c->wt.p, H, nets->num_nets, include_prefill, ranks, scores,
                                (int32_t *)c->snaps.p, (int64_t *)c->tile_off.p, tiles,
-                               (unsigned long long *)c->stats.p, s);
+                               (unsigned long long *)c->stats.p, c->k3_ctas, s);
     *launched += n;
     return MCB_OK;
 }
@@ -627,7 +628,7 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
             launched += launch_score_tiles(d, (const double *)c->wt.p, nets->hidden, nets->num_nets, v == 0 ? 1 : 0,
                                            (uint8_t *)c->ranks[v].p, nullptr, (const int32_t *)c->snaps.p,
                                            (const int64_t *)c->tile_off.p, lo * tpc, hi * tpc,
-                                           (unsigned long long *)c->stats.p, s);
+                                           (unsigned long long *)c->stats.p, c->k3_ctas, s);
             CUDA_TRY(cudaEventRecord(c->chunk_ev[k], s));
             CUDA_TRY(cudaStreamWaitEvent(c->side2, c->chunk_ev[k], 0));
             if (k == 0) mark(c, 6, c->side2);

@@ -1686,19 +1686,17 @@ int launch_score_prep(const DevTrace &tr, int include_prefill, int32_t *snaps, i
 
 // K3 part 2: score tiles [tile_lo, tile_hi) (persistent CTAs).  Uniform
 // traces number tiles chain-major, so a chain range maps to a tile range.
-// K3 grid: < 0 (default) = one CTA per 32-event tile; 0 = persistent, as
-// many CTAs as fit (4 per SM for the specialised shapes); k > 0 = persistent
-// with at most k CTAs per SM.  Measured on C2 (tools/k3_sweep.sh): one CTA
-// per tile is faster alone (4.12 vs 4.51 ms: better tail balance) and lets
-// the concurrent non-ML replay's blocks in as CTAs retire (persistent CTAs
-// hold the whole register file, so the replay waited for K3): 6.09 vs 6.55
-// ms per step.
-static int g_k3_ctas = -1;
-void set_k3_ctas(int v) { g_k3_ctas = v; }
-
+// K3 grid (k3_ctas): < 0 (default) = one CTA per 32-event tile; 0 =
+// persistent, as many CTAs as fit (4 per SM for the specialised shapes);
+// k > 0 = persistent with at most k CTAs per SM.  Measured on C2
+// (tools/k3_sweep.sh): one CTA per tile is faster alone (4.12 vs 4.51 ms:
+// better tail balance) and lets the concurrent non-ML replay's blocks in as
+// CTAs retire (persistent CTAs hold the whole register file, so the replay
+// waited for K3): 6.09 vs 6.55 ms per step.
 int launch_score_tiles(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill,
                        uint8_t *ranks, double *scores, const int32_t *snaps, const int64_t *tile_off,
-                       int64_t tile_lo, int64_t tile_hi, unsigned long long *uncertain, cudaStream_t s) {
+                       int64_t tile_lo, int64_t tile_hi, unsigned long long *uncertain, int k3_ctas,
+                       cudaStream_t s) {
     if (tile_hi <= tile_lo) return 0;
     const size_t smem = score_smem(tr.E, H);
     const score_fn fn = score_kernel(tr.E, H);
@@ -1706,8 +1704,8 @@ int launch_score_tiles(const DevTrace &tr, const double *wt, int H, int num_nets
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)fn, 256, smem);
-    if (g_k3_ctas > 0 && g_k3_ctas < per_sm) per_sm = g_k3_ctas;
-    const int64_t grid = g_k3_ctas < 0 ? tile_hi - tile_lo
+    if (k3_ctas > 0 && k3_ctas < per_sm) per_sm = k3_ctas;
+    const int64_t grid = k3_ctas < 0 ? tile_hi - tile_lo
                                        : std::min<int64_t>(tile_hi - tile_lo, (int64_t)n_sm * (per_sm > 0 ? per_sm : 1));
     fn<<<(unsigned)grid, 256, smem, s>>>(tr, wt, H, num_nets, include_prefill, tile_off, snaps, tile_lo, tile_hi,
                                          ranks, scores, uncertain);
@@ -1716,11 +1714,11 @@ int launch_score_tiles(const DevTrace &tr, const double *wt, int H, int num_nets
 
 int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill, uint8_t *ranks,
                  double *scores, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,
-                 unsigned long long *uncertain, cudaStream_t s) {
+                 unsigned long long *uncertain, int k3_ctas, cudaStream_t s) {
     if (tr.n_chains == 0) return 0;
     int launched = launch_score_prep(tr, include_prefill, snaps, tile_off, max_tiles, s);
     launched += launch_score_tiles(tr, wt, H, num_nets, include_prefill, ranks, scores, snaps, tile_off, 0,
-                                   max_tiles, uncertain, s);
+                                   max_tiles, uncertain, k3_ctas, s);
     return launched;
 }
 

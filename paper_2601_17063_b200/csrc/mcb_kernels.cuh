@@ -118,13 +118,13 @@ __host__ __device__ size_t net_param_doubles(int E, int H);
 // K3: snapshot scan + tile scorer. snaps scratch: n_tiles_total * (2E+1) int32; tile_off: n_chains+1 int64
 int launch_score_prep(const DevTrace &tr, int include_prefill, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,
                       cudaStream_t s);
-void set_k3_ctas(int v);
+// k3_ctas: grid mode of the tile scorer (mcb.h MCB_TUNE_K3_CTAS)
 int launch_score_tiles(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill,
                        uint8_t *ranks, double *scores, const int32_t *snaps, const int64_t *tile_off,
-                       int64_t tile_lo, int64_t tile_hi, unsigned long long *uncertain, cudaStream_t s);
+                       int64_t tile_lo, int64_t tile_hi, unsigned long long *uncertain, int k3_ctas, cudaStream_t s);
 int launch_train_features(const DevTrace &tr, const int32_t *snaps, int64_t max_tiles, double *features,
                           cudaStream_t s);
 int launch_train_targets(const DevTrace &tr, int distance_cap, double *targets, cudaStream_t s);
 int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill,
                  uint8_t *ranks, double *scores, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,
-                 unsigned long long *uncertain, cudaStream_t s);
+                 unsigned long long *uncertain, int k3_ctas, cudaStream_t s);
