@@ -23,7 +23,8 @@ from .engine import (
     sweep,
 )
 from .net import EvictionNet, NetError, ShapeMismatchError, load_net, save_net
-from .policies import NoEvictableError, PolicyDecision, PolicyError
+from .policies import NoEvictableError, PolicyDecision, PolicyError, lecar_update
+from .refgen import SyntheticWorkloadConfig, expert_popularity, generate_trace
 from .trace import (
     AccessEvent,
     HeaderMismatchError,
@@ -37,6 +38,7 @@ from .trace import (
     TraceParseError,
     pack_trace,
     packed_from_decode_ids,
+    prefill_coverage,
 )
 
 from .train import (
@@ -44,6 +46,7 @@ from .train import (
     NonFiniteLossError,
     TrainConfig,
     TrainResult,
+    masked_mse,
     train_eviction_net,
     train_eviction_nets,
 )

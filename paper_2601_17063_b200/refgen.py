@@ -54,6 +54,13 @@ class SyntheticWorkloadConfig:
             raise InvalidConfigError(f"w_hot must be >= 1, got {self.w_hot}")
 
 
+def expert_popularity(header: TraceHeader, cfg: SyntheticWorkloadConfig, layer: int) -> np.ndarray:
+    """The stationary per-expert routing probabilities of one layer (trace.py:205-209)."""
+    header.validate()
+    cfg.validate()
+    return layer_popularity(header, cfg)[layer]
+
+
 def layer_popularity(header: TraceHeader, cfg: SyntheticWorkloadConfig) -> np.ndarray:
     """float64 [L][E]: Zipf mass (r+1)^-s over a per-layer seeded permutation
     (the numpy draws of trace.py:186-202)."""

@@ -265,3 +265,29 @@ def packed_from_decode_ids(ids, num_experts: int) -> PackedTrace:
     return PackedTrace(num_layers=L, num_experts=num_experts, top_k=K, num_traces=n, uniform=True,
                        events_per_chain=T, acc=acc, total_acc=flat.size, total_events=n * L * T,
                        decode_steps=[T] * n)
+
+
+def prefill_coverage(trace, token_counts) -> list:
+    """Fraction of the expert pool touched by the first n prefill tokens
+    (trace.py:443-476): for each n (ascending), the mean over (sequence,
+    layer) of |distinct experts routed in the first n prefill events| / E."""
+    counts = list(token_counts)
+    if counts != sorted(counts) or any(n < 1 for n in counts):
+        raise InvalidConfigError("token_counts must be ascending positive integers")
+    groups: dict = {}
+    for ev in trace.events:
+        if ev.phase == Phase.PREFILL:
+            groups.setdefault((ev.seq_id, ev.layer), []).append(ev.experts)
+    if not groups:
+        raise InsufficientTokensError("trace contains no prefill events")
+    need = max(counts)
+    for (seq_id, layer), rows in groups.items():
+        if len(rows) < need:
+            raise InsufficientTokensError(f"sequence {seq_id} layer {layer} has only {len(rows)} prefill "
+                                          f"tokens, need {need}")
+    E = trace.header.num_experts
+    out = []
+    for n in counts:
+        fr = [len({x for row in rows[:n] for x in row}) / E for rows in groups.values()]
+        out.append((n, float(np.mean(fr))))
+    return out

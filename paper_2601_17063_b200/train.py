@@ -56,6 +56,15 @@ class TrainResult:
     stopped_epoch: int = 0
 
 
+def masked_mse(pred, target, mask) -> float:
+    """Mean squared error over the masked positions, 0.0 if none (net.py:141-147)."""
+    m = np.asarray(mask).astype(np.float64)
+    denom = m.sum()
+    if denom == 0:
+        return 0.0
+    return float((m * (np.asarray(pred) - np.asarray(target)) ** 2).sum() / denom)
+
+
 def _unflatten(net: EvictionNet, flat: np.ndarray) -> dict:
     out, o = {}, 0
     for name in PARAM_NAMES:
@@ -179,4 +188,4 @@ def _train_group(nets, data, cfg: TrainConfig, device: int):
 
 
 __all__ = ["TrainConfig", "TrainResult", "EmptyDatasetError", "NonFiniteLossError", "train_eviction_net",
-           "train_eviction_nets"]
+           "train_eviction_nets", "masked_mse"]
