@@ -236,12 +236,12 @@ __device__ __forceinline__ void keys_at(const ReplayParams &P, int64_t chain, in
 }
 
 // ------------------------------------------------------------------- spec --
-template <int EM, int POL>
+template <int EM, int POL, int KT, bool TRACK>
 __device__ __forceinline__ void seg_spec(const ReplayParams &P, int64_t chain, int seg, int pol_i, int cap_i,
                                          int ml_variant, uint16_t (*s_hist)[128], int pass) {
     constexpr int WMAX = SOLO_WMAX;
     const DevTrace &tr = P.tr;
-    const int E = tr.E, K = tr.K, W = P.window;
+    const int E = tr.E, K = KT ? KT : tr.K, W = P.window;   // KT: top_k known at compile time
     const int tid = threadIdx.x;
     const uint32_t C = (uint32_t)P.cap[cap_i];
     const int64_t inst = (chain * P.n_pol + pol_i) * P.n_cap + cap_i;
@@ -272,7 +272,6 @@ __device__ __forceinline__ void seg_spec(const ReplayParams &P, int64_t chain, i
     bool stuck = false;
     int32_t stuck_ev = -1;
     uint64_t h = 0;
-    const bool track = P.hashes != nullptr;
     for (int b = 0; b <= K; ++b) s_hist[b][tid] = 0;
 
     IdReader ids;
@@ -305,7 +304,8 @@ __device__ __forceinline__ void seg_spec(const ReplayParams &P, int64_t chain, i
         }
         uint32_t pin = 0, sm = 0;
         const int64_t A0 = a0 + ev * K;
-        for (int j = 0; j < K; ++j) {
+#pragma unroll
+        for (int j = 0; j < (KT ? KT : K); ++j) {
             const int64_t A = A0 + j;
             const uint32_t x = ids.get(A);
             const uint32_t bit = 1u << x;
@@ -317,7 +317,7 @@ __device__ __forceinline__ void seg_spec(const ReplayParams &P, int64_t chain, i
             comp += (miss && !(seen & bit)) ? 1u : 0u;
             seen |= bit;
             pin |= bit;
-            if (track && ev >= ev0) h = poly16(h, code);
+            if (TRACK && ev >= ev0) h = poly16(h, code);
         }
         if (ev >= ev0) {
             if (stuck && stuck_ev < 0) stuck_ev = (int32_t)ev;
@@ -343,6 +343,18 @@ __device__ __forceinline__ void seg_spec(const ReplayParams &P, int64_t chain, i
     for (int b = 0; b < MCB_SEG_BINS; ++b) o.hist[b] = b <= K ? s_hist[b][tid] : (uint16_t)0;
 }
 
+template <int EM, int KT, bool TRACK>
+__device__ __forceinline__ void seg_spec_pol(const ReplayParams &P, int64_t chain, int seg, int pol_i, int cap_i,
+                                             uint16_t (*s_hist)[128], int pass) {
+    switch (P.pol[pol_i]) {
+        case MCB_LRU: seg_spec<EM, POL_LRU, KT, TRACK>(P, chain, seg, pol_i, cap_i, 0, s_hist, pass); break;
+        case MCB_LFU: seg_spec<EM, POL_LFU, KT, TRACK>(P, chain, seg, pol_i, cap_i, 0, s_hist, pass); break;
+        case MCB_BELADY: seg_spec<EM, POL_BELADY, KT, TRACK>(P, chain, seg, pol_i, cap_i, 0, s_hist, pass); break;
+        case MCB_ML: seg_spec<EM, POL_ML, KT, TRACK>(P, chain, seg, pol_i, cap_i, 0, s_hist, pass); break;
+        default: seg_spec<EM, POL_ML, KT, TRACK>(P, chain, seg, pol_i, cap_i, 1, s_hist, pass); break;
+    }
+}
+
 template <int EM>
 __global__ void __launch_bounds__(128) k_seg_spec(const __grid_constant__ ReplayParams P, int pass) {
     __shared__ uint16_t s_hist[MCB_SEG_BINS][128];
@@ -355,12 +367,12 @@ __global__ void __launch_bounds__(128) k_seg_spec(const __grid_constant__ Replay
     const int64_t r = t / P.n_cap;
     const int seg = (int)(r % n_seg);
     const int64_t chain = P.chain_lo + r / n_seg;
-    switch (P.pol[pol_i]) {
-        case MCB_LRU: seg_spec<EM, POL_LRU>(P, chain, seg, pol_i, cap_i, 0, s_hist, pass); break;
-        case MCB_LFU: seg_spec<EM, POL_LFU>(P, chain, seg, pol_i, cap_i, 0, s_hist, pass); break;
-        case MCB_BELADY: seg_spec<EM, POL_BELADY>(P, chain, seg, pol_i, cap_i, 0, s_hist, pass); break;
-        case MCB_ML: seg_spec<EM, POL_ML>(P, chain, seg, pol_i, cap_i, 0, s_hist, pass); break;
-        default: seg_spec<EM, POL_ML>(P, chain, seg, pol_i, cap_i, 1, s_hist, pass); break;
+    if (P.tr.K == 2) {   // Mixtral-shaped top-2 (C2): fixed-length access loop
+        if (P.hashes) seg_spec_pol<EM, 2, true>(P, chain, seg, pol_i, cap_i, s_hist, pass);
+        else seg_spec_pol<EM, 2, false>(P, chain, seg, pol_i, cap_i, s_hist, pass);
+    } else {
+        if (P.hashes) seg_spec_pol<EM, 0, true>(P, chain, seg, pol_i, cap_i, s_hist, pass);
+        else seg_spec_pol<EM, 0, false>(P, chain, seg, pol_i, cap_i, s_hist, pass);
     }
 }
 

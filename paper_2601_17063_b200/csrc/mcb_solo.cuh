@@ -513,8 +513,27 @@ __device__ __forceinline__ void solo_ml_keys(uint32_t (&pk)[EM], uint32_t &valid
     }
 }
 
+// One event's rank row (E bytes).  Full rows (E == EM: rows are 8- / 16-byte
+// aligned in the engine's rank buffer) are one vector load.
 template <int EM>
 __device__ __forceinline__ void load_rank_row(uint32_t (&rrow)[EM], const uint8_t *row, int E) {
+    if (E == EM) {
+        uint32_t w[EM / 4];
+        if constexpr (EM == 8) {
+            const uint2 v = __ldcg((const uint2 *)row);
+            w[0] = v.x;
+            w[1] = v.y;
+        } else {
+            const uint4 v = __ldcg((const uint4 *)row);
+            w[0] = v.x;
+            w[1] = v.y;
+            w[2] = v.z;
+            w[3] = v.w;
+        }
+#pragma unroll
+        for (int s = 0; s < EM; ++s) rrow[s] = (w[s >> 2] >> (8 * (s & 3))) & 0xFFu;
+        return;
+    }
 #pragma unroll
     for (int s = 0; s < EM; ++s) rrow[s] = s < E ? (uint32_t)__ldcg(row + s) : 0u;
 }

@@ -4,11 +4,14 @@ import csv
 import subprocess
 import sys
 
+import os
+
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 15
-a = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+flt = os.environ.get("NCU_FILTER", "").split()   # e.g. "--kernel-name regex:k_seg_spec --launch-skip 1 --launch-count 1"
+a = subprocess.run(["ncu", "-i", rep, *flt, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                    capture_output=True, text=True).stdout.splitlines()
-b = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+b = subprocess.run(["ncu", "-i", rep, *flt, "--page", "source", "--csv", "--print-source", "sass"],
                    capture_output=True, text=True).stdout.splitlines()
 addr2line, cur, curfile = {}, None, None
 for r in csv.reader(a):
