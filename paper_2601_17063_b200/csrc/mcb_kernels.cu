@@ -1381,14 +1381,113 @@ int launch_train_targets(const DevTrace &tr, int distance_cap, double *targets, 
     return 1;
 }
 
-// Ranks of one event's E scores by a warp-wide bitonic sort of (score, id)
+// Order-preserving map of float64 to uint64 (-0.0 canonicalised to +0.0, so
+// equal doubles map to equal keys) and its inverse.
+__device__ __forceinline__ unsigned long long ordered_key(double x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x + 0.0);
+    return b ^ ((unsigned long long)((long long)b >> 63) | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_value(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k ^ 0x8000000000000000ull) : ~k));
+}
+
+// Ranks of one event's E scores by a warp-wide bitonic sort of the scores'
+// order-preserving integer keys (P elements per lane, N = 32 P >= E; padding
+// sorts last as +inf; equal scores need no tie-break because equal values get
+// equal ranks): rank = 1 + #{selectable j : s_j < s_e} = 1 + (first sorted
+// position of s_e's value) - #non-selectable, 0 for NaN / -inf (never
+// evicted, mlpolicy.py:15-26).  A near-tie (two distinct scores within 1e-12
+// relative) is always an adjacent sorted pair, which sets *flag.
+template <int P>
+__device__ __forceinline__ void rank_event_sorted(const double *srow, int E, uint8_t *rrow, int32_t *flag, int lane) {
+    constexpr int N = 32 * P;
+    const unsigned long long KNEG = ordered_key(-INFINITY), KPOS = ordered_key(INFINITY);
+    unsigned long long v[P];
+    int id[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const int n = lane * P + p;
+        id[p] = n;
+        if (n < E) {
+            const double x = srow[n];
+            v[p] = x > -INFINITY ? ordered_key(x) : KNEG;   // NaN -> -inf: never selectable
+        } else {
+            v[p] = KPOS;
+        }
+    }
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= P) {   // partner in lane ^ (j / P)
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const unsigned long long ov = __shfl_xor_sync(FULL_MASK, v[p], j / P);
+                    const int oid = __shfl_xor_sync(FULL_MASK, id[p], j / P);
+                    const int n = lane * P + p;
+                    const bool up = (n & k) == 0, lower = (n & j) == 0;
+                    // keep the smaller key in the lower slot of an ascending pair
+                    const bool take = lower == up ? ov < v[p] : ov > v[p];
+                    if (take) { v[p] = ov; id[p] = oid; }
+                }
+            } else {        // partner in the same lane: p ^ j
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    if (p & j) continue;
+                    const int q = p | j, n = lane * P + p;
+                    const bool up = (n & k) == 0;
+                    if (up ? v[q] < v[p] : v[q] > v[p]) {
+                        const unsigned long long tv = v[p]; v[p] = v[q]; v[q] = tv;
+                        const int ti = id[p]; id[p] = id[q]; id[q] = ti;
+                    }
+                }
+            }
+        }
+    }
+    // first sorted position of each value (inclusive max-scan of run starts)
+    const unsigned long long prev_last = __shfl_up_sync(FULL_MASK, v[P - 1], 1);
+    int start[P];
+    int nsel_local = 0, loc = -1;
+    bool near = false;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const int n = lane * P + p;
+        const unsigned long long pk = p > 0 ? v[p - 1] : prev_last;
+        const bool first = n == 0 || v[p] != pk;
+        loc = max(loc, first ? n : -1);
+        start[p] = loc;
+        nsel_local += (v[p] == KNEG) ? 1 : 0;
+        if (n > 0 && v[p] != pk && pk != KNEG && v[p] != KPOS) {
+            const double a = key_value(v[p]), b = key_value(pk);
+            if (fabs(a - b) <= 1e-12 * fmax(fabs(a), fabs(b))) near = true;
+        }
+    }
+    int carry = loc;   // warp inclusive max-scan of the lanes' last run start
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULL_MASK, carry, o);
+        if (lane >= o) carry = max(carry, t);
+    }
+    const int before = __shfl_up_sync(FULL_MASK, carry, 1);
+    const int nsel = __reduce_add_sync(FULL_MASK, nsel_local);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const int st = (lane > 0 && start[p] < 0) ? before : max(start[p], lane > 0 ? before : -1);
+        if (id[p] < E) rrow[id[p]] = v[p] != KNEG ? (uint8_t)(st - nsel + 1) : (uint8_t)0;
+    }
+    if (__any_sync(FULL_MASK, near) && lane == 0) *flag = 1;
+}
+
+// float64 variant of rank_event_sorted (the sort compares (score, id) pairs as
+// doubles): fewer live registers, used for E > 64 where the integer-key
+// version spills.  Ranks of one event's E scores by a warp-wide bitonic sort of (score, id)
 // (P elements per lane, N = 32 P >= E; padding sorts last as +inf):
 // rank = 1 + #{selectable j : s_j < s_e} = 1 + (first sorted position of
 // s_e's value) - #non-selectable, 0 for NaN / -inf (never evicted,
 // mlpolicy.py:15-26).  A near-tie (two distinct scores within 1e-12
 // relative) is always an adjacent sorted pair, which sets *flag.
 template <int P>
-__device__ __forceinline__ void rank_event_sorted(const double *srow, int E, uint8_t *rrow, int32_t *flag, int lane) {
+__device__ __forceinline__ void rank_event_sorted_f64(const double *srow, int E, uint8_t *rrow, int32_t *flag, int lane) {
     constexpr int N = 32 * P;
     double v[P];
     int id[P];
@@ -1622,7 +1721,7 @@ __global__ void __launch_bounds__(256, TE ? 4 : 1) k_score_tile(DevTrace tr, con
         for (int i = warp; i < nev; i += (int)(blockDim.x >> 5)) {
             if (E <= 32) rank_event_sorted<1>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
             else if (E <= 64) rank_event_sorted<2>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
-            else rank_event_sorted<4>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
+            else rank_event_sorted_f64<4>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
         }
     }
     if (scores)
