@@ -327,16 +327,18 @@ int mcb_router_topk(mcb_ctx *ctx, const void *hidden_bf16, const void *weight_bf
                     uint8_t *acc, float *logits, void *stream);
 
 /* ---- Belady-labelled training data ----
- * Replaces build_training_data (pkg/src/moecache/dataset.py:35-96) for
- * decode-only single-sequence traces (uniform layout): per chain and decode
- * step the float64 feature vector [1/r || f / max_f] (features.py:44-52),
- * float64 targets min(d, distance_cap) / distance_cap with d the steps until
- * the expert is next routed (replay.py:92-109; never -> 1.0), and the Belady
- * residency mask at `capacity` before the step's accesses.  Outputs
- * features[chain][T][2E], targets[chain][T][E], masks[chain][T][E] (bytes).
- * Device pointers, asynchronous on `stream`. */
+ * Replaces build_training_data (pkg/src/moecache/dataset.py:35-96) for any
+ * packed trace (prefill and several sequences included): for every event of
+ * every chain the float64 feature vector [1/r || f / max_f] after the
+ * event's tracker update (features.py:34-52; prefill events update it only
+ * with include_prefill), float64 targets min(d, distance_cap) / distance_cap
+ * with d the events until the expert is next routed (replay.py:92-109; never
+ * -> 1.0), and the Belady residency mask at `capacity` before the event's
+ * accesses.  Outputs features[event][2E], targets[event][E], masks[event][E]
+ * (bytes), events in mcb_trace order (chain-major); the reference's samples
+ * are the decode events.  Device pointers, asynchronous on `stream`. */
 int mcb_training_data(mcb_ctx *ctx, const mcb_trace *trace, int32_t capacity, int32_t distance_cap,
-                      double *features, double *targets, uint8_t *masks, void *stream);
+                      int32_t include_prefill, double *features, double *targets, uint8_t *masks, void *stream);
 
 /* ---- bit-exact reference generator ----
  * Replaces generate_trace / _draw_routed (pkg/src/moecache/trace.py:212-287):

@@ -147,7 +147,7 @@ def load_library():
             "mcb_next_use": ([P, P, P, P], ctypes.c_int),
             "mcb_score": ([P, P, P, i32, P, P, P], ctypes.c_int),
             "mcb_router_topk": ([P, P, P, i64, i32, i32, i32, i32, P, P, P], ctypes.c_int),
-            "mcb_training_data": ([P, P, i32, i32, P, P, P, P], ctypes.c_int),
+            "mcb_training_data": ([P, P, i32, i32, i32, P, P, P, P], ctypes.c_int),
             "mcb_set_lecar": ([P, ctypes.c_double, ctypes.c_double, i64], ctypes.c_int),
             "mcb_lecar_random": ([i64, i64, P], ctypes.c_int),
             "mcb_pack_decode_ids": ([P, P, i64, i64, i32, i32, i32, P, P, P], ctypes.c_int),

@@ -672,17 +672,16 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     return MCB_OK;
 }
 
-// Belady-labelled training data (dataset.py:35-96) for decode-only
-// single-sequence traces: features [chain][T][2E] (float64), targets
-// [chain][T][E] (float64) and masks [chain][T][E] (0/1 bytes).  Device
-// pointers, asynchronous on `stream`.
+// Belady-labelled training data (dataset.py:35-96): features [event][2E]
+// (float64), targets [event][E] (float64) and masks [event][E] (0/1 bytes)
+// for every event of every chain (chain-major, mcb_trace event order); the
+// reference's samples are the decode events.  Device pointers, asynchronous.
 extern "C" int mcb_training_data(mcb_ctx *c, const mcb_trace *t, int32_t capacity, int32_t distance_cap,
-                                 double *features, double *targets, uint8_t *masks, void *stream) {
+                                 int32_t include_prefill, double *features, double *targets, uint8_t *masks,
+                                 void *stream) {
     mcb_clear_error();
     if (!c) return mcb_set_error(MCB_ERR_INVALID, "ctx is NULL");
     if (int rc = check_trace(t)) return rc;
-    if (!t->uniform)
-        return mcb_set_error(MCB_ERR_UNSUPPORTED, "training data on the GPU needs a decode-only single-sequence trace");
     if (capacity < t->top_k) return mcb_set_error(MCB_ERR_CAPACITY, "capacity is below top_k");
     if (distance_cap < 1) return mcb_set_error(MCB_ERR_INVALID, "distance_cap must be >= 1");
     if (!features || !targets || !masks) return mcb_set_error(MCB_ERR_INVALID, "NULL output");
@@ -697,6 +696,7 @@ extern "C" int mcb_training_data(mcb_ctx *c, const mcb_trace *t, int32_t capacit
     if (int rc = c->next_pos.ensure((size_t)(d.total_acc + 64) * sizeof(uint32_t))) return rc;
     if (int rc = c->inst_out.ensure((size_t)(d.n_chains + 1) * MCB_R_N * sizeof(int64_t))) return rc;
     if (int rc = c->inst_lat.ensure((size_t)(d.n_chains + 1) * 2 * sizeof(double))) return rc;
+    if (int rc = c->tile_off.ensure((size_t)(d.n_chains + 1) * sizeof(int64_t))) return rc;
     const int64_t tiles = max_score_tiles(d);
     if (int rc = c->snaps.ensure((size_t)(tiles + 1) * (4 * d.E + 8) * sizeof(int32_t))) return rc;
     launch_next_use(d, (uint32_t *)c->next_pos.p, nu_sw ? (uint32_t *)c->nu_scratch.p : nullptr, s);
@@ -719,8 +719,9 @@ extern "C" int mcb_training_data(mcb_ctx *c, const mcb_trace *t, int32_t capacit
     P.res_masks = masks;
     launch_replay(P, s);
     // features and targets
-    launch_score_prep(d, 1, (int32_t *)c->snaps.p, (int64_t *)c->tile_off.p, tiles, s);
-    launch_train_features(d, (const int32_t *)c->snaps.p, tiles, features, s);
+    launch_score_prep(d, include_prefill ? 1 : 0, (int32_t *)c->snaps.p, (int64_t *)c->tile_off.p, tiles, s);
+    launch_train_features(d, (const int32_t *)c->snaps.p, (const int64_t *)c->tile_off.p, tiles,
+                          include_prefill ? 1 : 0, features, s);
     launch_train_targets(d, distance_cap, targets, s);
     CUDA_TRY(cudaGetLastError());
     return MCB_OK;

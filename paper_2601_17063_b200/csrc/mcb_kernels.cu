@@ -357,8 +357,8 @@ __device__ __forceinline__ void replay_instance(const ReplayParams &P, int64_t c
                                       : __ldg(tr.ev_info + e0 + ev);
         const uint32_t nacc = mcb_ev_nacc(info);
         const bool decode = mcb_ev_decode(info);
-        if (UNIFORM && P.res_masks) {   // resident set before the event (dataset.py:61-63)
-            uint8_t *m = P.res_masks + (chain * tr.T + ev) * E;
+        if (P.res_masks) {   // resident set before the event (dataset.py:61-63)
+            uint8_t *m = P.res_masks + (e0 + ev) * E;
 #pragma unroll
             for (int s = 0; s < EPL; ++s) {
                 const int e = glane * EPL + s;
@@ -628,8 +628,8 @@ __device__ __forceinline__ void solo_instance(const ReplayParams &P, int64_t cha
             for (int s = 0; s < EM; ++s) pk[s] = (uint32_t)s;   // start_sequence (policies.py:184-185)
         }
         if (POL == POL_LECAR && !UNIFORM && mcb_ev_newseq(info)) lecar_new_sequence<EM>(lec);
-        if (UNIFORM && P.res_masks) {   // resident set before the event (dataset.py:61-63)
-            uint8_t *m = P.res_masks + (chain * tr.T + ev) * E;
+        if (P.res_masks) {   // resident set before the event (dataset.py:61-63)
+            uint8_t *m = P.res_masks + (e0 + ev) * E;
             for (int e = 0; e < E; ++e) m[e] = (uint8_t)((S.res >> e) & 1u);
         }
         if (POL == POL_ML) {
@@ -1317,6 +1317,69 @@ __device__ __forceinline__ void tile_features_uniform(const DevTrace &tr, const 
 }
 
 // ---------------------------------------------------------------------------
+// Feature rows of the events [ev0, ev0 + nev) of chain c (general traces:
+// prefill, several sequences) from the tile's tracker snapshot, by one warp
+// walking the tile's events in order (features.py:34-52: reset at a new
+// sequence, update on decode events or on every event with include_prefill).
+// Rows go to bufA[i * ldA + ...]; all_rows also zero-fills rows i >= nev.
+__device__ __forceinline__ void tile_features_general(const DevTrace &tr, const int32_t *__restrict__ snaps,
+                                                      int64_t tile, int64_t c, int64_t e0, int64_t ev0, int nev,
+                                                      int E, int include_prefill, double *bufA, int ldA, int lane,
+                                                      bool all_rows) {
+    const int32_t *sp = snaps + tile * (2 * E + 4);
+    int32_t last[4], f[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int e = lane + 32 * j;
+        last[j] = e < E ? sp[e] : -1;
+        f[j] = e < E ? sp[E + e] : 0;
+    }
+    int32_t u = sp[2 * E];
+    int64_t rt = (int64_t)(uint32_t)sp[2 * E + 1] | ((int64_t)sp[2 * E + 2] << 32);
+    int32_t maxf = __reduce_max_sync(FULL_MASK, max(max(f[0], f[1]), max(f[2], f[3])));
+    const uint8_t *routed = tr.routed_ptr() + tr.rt_begin(c);
+    for (int i = 0; i < MCB_TILE_EV; ++i) {
+        if (i < nev) {
+            const uint32_t info = tr.info(c, e0 + ev0 + i);
+            const uint32_t nrt = mcb_ev_nrt(info);
+            if (mcb_ev_newseq(info)) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) { last[j] = -1; f[j] = 0; }
+                u = 0;
+                maxf = 0;
+            }
+            if (mcb_ev_decode(info) || include_prefill) {
+                ++u;
+                for (uint32_t r = 0; r < nrt; ++r) {
+                    const int x = __ldg(routed + rt + r);
+                    if ((x & 31) == lane) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            { const bool hit_j = (x >> 5) == j; last[j] = hit_j ? u : last[j]; f[j] += hit_j ? 1 : 0; }
+                    }
+                }
+                maxf = __reduce_max_sync(FULL_MASK, max(max(f[0], f[1]), max(f[2], f[3])));
+            }
+            rt += nrt;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int e = lane + 32 * j;
+            if (e < E) {
+                double rv = 0.0, fv = 0.0;
+                if (i < nev) {
+                    rv = last[j] < 0 ? 0.0 : 1.0 / (double)(u - last[j] + 1);
+                    fv = maxf > 0 ? (double)f[j] / (double)maxf : 0.0;
+                }
+                if (i < nev || all_rows) {
+                    bufA[i * ldA + e] = rv;
+                    bufA[i * ldA + E + e] = fv;
+                }
+            }
+        }
+    }
+}
+
 // Training data (dataset.py:35-96, decode-only single-sequence traces):
 // features of every decode step (the K3 feature rows) and capped next-use
 // distance targets; the Belady residency masks come from the replay kernels
@@ -1368,16 +1431,72 @@ __global__ void __launch_bounds__(128) k_train_targets(DevTrace tr, int cap, dou
     }
 }
 
-int launch_train_features(const DevTrace &tr, const int32_t *snaps, int64_t max_tiles, double *features,
-                          cudaStream_t s) {
+// General traces (prefill, several sequences): one warp per scorer tile
+// writes the feature rows of the tile's events (every event; the caller keeps
+// the decode rows, dataset.py:61-70).
+__global__ void __launch_bounds__(32) k_train_features_general(DevTrace tr, const int32_t *__restrict__ snaps,
+                                                               const int64_t *__restrict__ tile_off,
+                                                               int include_prefill, double *__restrict__ features) {
+    const int64_t tile = blockIdx.x;
+    if (tile >= tile_off[tr.n_chains]) return;
+    int64_t lo = 0, hi = tr.n_chains;   // largest c with tile_off[c] <= tile
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) / 2;
+        if (tile_off[mid] <= tile) lo = mid; else hi = mid;
+    }
+    const int64_t c = lo, e0 = tr.ev_begin(c);
+    const int64_t ev0 = (tile - tile_off[c]) * MCB_TILE_EV;
+    const int nev = (int)min((int64_t)MCB_TILE_EV, tr.ev_end(c) - e0 - ev0);
+    tile_features_general(tr, snaps, tile, c, e0, ev0, nev, tr.E, include_prefill,
+                          features + (e0 + ev0) * 2 * tr.E, 2 * tr.E, threadIdx.x & 31, false);
+}
+
+// Targets of general traces: StepNextUse (replay.py:92-109) counts event
+// ticks to the next event whose ROUTED list (not its accesses) holds e.
+__global__ void __launch_bounds__(128) k_train_targets_general(DevTrace tr, int cap, double *__restrict__ targets) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (c >= tr.n_chains) return;
+    const int E = tr.E;
+    int64_t next[4] = {-1, -1, -1, -1};
+    const double dcap = (double)cap;
+    const uint8_t *routed = tr.routed_ptr();
+    const int64_t e0 = tr.ev_begin(c);
+    int64_t rt = tr.rt_begin(c + 1);
+    for (int64_t t = tr.ev_end(c) - e0 - 1; t >= 0; --t) {
+        double *row = targets + (e0 + t) * E;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int e = lane + 32 * j;
+            if (e < E) {
+                const int64_t d = next[j] < 0 ? (int64_t)cap : min(next[j] - t, (int64_t)cap);
+                row[e] = __ddiv_rn((double)d, dcap);
+            }
+        }
+        const uint32_t nrt = mcb_ev_nrt(tr.info(c, e0 + t));
+        rt -= nrt;
+        for (uint32_t k = 0; k < nrt; ++k) {
+            const int x = __ldg(routed + rt + k);
+            if ((x & 31) == lane)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if ((x >> 5) == j) next[j] = t;
+        }
+    }
+}
+
+int launch_train_features(const DevTrace &tr, const int32_t *snaps, const int64_t *tile_off, int64_t max_tiles,
+                          int include_prefill, double *features, cudaStream_t s) {
     if (max_tiles <= 0) return 0;
-    k_train_features<<<(unsigned)max_tiles, 128, 0, s>>>(tr, snaps, features);
+    if (tr.uniform) k_train_features<<<(unsigned)max_tiles, 128, 0, s>>>(tr, snaps, features);
+    else k_train_features_general<<<(unsigned)max_tiles, 32, 0, s>>>(tr, snaps, tile_off, include_prefill, features);
     return 1;
 }
 
 int launch_train_targets(const DevTrace &tr, int distance_cap, double *targets, cudaStream_t s) {
     if (tr.n_chains == 0) return 0;
-    k_train_targets<<<(unsigned)((tr.n_chains + 3) / 4), 128, 0, s>>>(tr, distance_cap, targets);
+    if (tr.uniform) k_train_targets<<<(unsigned)((tr.n_chains + 3) / 4), 128, 0, s>>>(tr, distance_cap, targets);
+    else k_train_targets_general<<<(unsigned)((tr.n_chains + 3) / 4), 128, 0, s>>>(tr, distance_cap, targets);
     return 1;
 }
 
@@ -1616,56 +1735,7 @@ __global__ void __launch_bounds__(256, TE ? 4 : 1) k_score_tile(DevTrace tr, con
         tile_features_uniform(tr, snaps, tile, c, ev0, nev, E, (unsigned long long *)s_rank, s_flag, bufA, ldA,
                               true);
     } else if (tid < 32) {
-        const int32_t *sp = snaps + tile * (2 * E + 4);
-        int32_t last[4], f[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int e = lane + 32 * j;
-            last[j] = e < E ? sp[e] : -1;
-            f[j] = e < E ? sp[E + e] : 0;
-        }
-        int32_t u = sp[2 * E];
-        int64_t rt = (int64_t)(uint32_t)sp[2 * E + 1] | ((int64_t)sp[2 * E + 2] << 32);
-        int32_t maxf = __reduce_max_sync(FULL_MASK, max(max(f[0], f[1]), max(f[2], f[3])));
-        const uint8_t *routed = tr.routed_ptr() + tr.rt_begin(c);
-        for (int i = 0; i < MCB_TILE_EV; ++i) {
-            if (i < nev) {
-                const uint32_t info = tr.info(c, e0 + ev0 + i);
-                const uint32_t nrt = mcb_ev_nrt(info);
-                if (mcb_ev_newseq(info)) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) { last[j] = -1; f[j] = 0; }
-                    u = 0;
-                    maxf = 0;
-                }
-                if (mcb_ev_decode(info) || include_prefill) {
-                    ++u;
-                    for (uint32_t r = 0; r < nrt; ++r) {
-                        const int x = __ldg(routed + rt + r);
-                        if ((x & 31) == lane) {
-#pragma unroll
-                            for (int j = 0; j < 4; ++j)
-                                { const bool hit_j = (x >> 5) == j; last[j] = hit_j ? u : last[j]; f[j] += hit_j ? 1 : 0; }
-                        }
-                    }
-                    maxf = __reduce_max_sync(FULL_MASK, max(max(f[0], f[1]), max(f[2], f[3])));
-                }
-                rt += nrt;
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int e = lane + 32 * j;
-                if (e < E) {
-                    double rv = 0.0, fv = 0.0;
-                    if (i < nev) {
-                        rv = last[j] < 0 ? 0.0 : 1.0 / (double)(u - last[j] + 1);
-                        fv = maxf > 0 ? (double)f[j] / (double)maxf : 0.0;
-                    }
-                    bufA[i * ldA + e] = rv;
-                    bufA[i * ldA + E + e] = fv;
-                }
-            }
-        }
+        tile_features_general(tr, snaps, tile, c, e0, ev0, nev, E, include_prefill, bufA, ldA, lane, true);
     }
     for (int q = tid; q < MCB_TILE_EV * (Kp1 - D); q += blockDim.x)   // zero feature padding
         bufA[(q / (Kp1 - D)) * ldA + D + q % (Kp1 - D)] = 0.0;

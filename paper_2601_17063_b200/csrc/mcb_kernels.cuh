@@ -122,8 +122,8 @@ int launch_score_prep(const DevTrace &tr, int include_prefill, int32_t *snaps, i
 int launch_score_tiles(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill,
                        uint8_t *ranks, double *scores, const int32_t *snaps, const int64_t *tile_off,
                        int64_t tile_lo, int64_t tile_hi, unsigned long long *uncertain, int k3_ctas, cudaStream_t s);
-int launch_train_features(const DevTrace &tr, const int32_t *snaps, int64_t max_tiles, double *features,
-                          cudaStream_t s);
+int launch_train_features(const DevTrace &tr, const int32_t *snaps, const int64_t *tile_off, int64_t max_tiles,
+                          int include_prefill, double *features, cudaStream_t s);
 int launch_train_targets(const DevTrace &tr, int distance_cap, double *targets, cudaStream_t s);
 int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int include_prefill,
                  uint8_t *ranks, double *scores, int32_t *snaps, int64_t *tile_off, int64_t max_tiles,

@@ -1,12 +1,14 @@
 """Belady-labelled training data on the GPU.
 
 Drop-in for the reference's ``build_training_data`` (pkg/src/moecache/
-dataset.py:35-96) on decode-only single-sequence traces: per layer and
-decode step the float64 feature vector, the capped next-use-distance targets
-and the Belady residency mask at the label capacity, computed by
-``mcb_training_data`` (the K3 feature scan, a reverse next-routing scan and
-the Belady replay with per-event resident-set output).  Bit-identical to the
-reference (tests/test_dataset_gpu.py).
+dataset.py:35-96): per layer and decode step the float64 feature vector, the
+capped next-routing-distance targets and the Belady residency mask at the
+label capacity, computed by ``mcb_training_data`` for every event (the K3
+feature scan, a reverse next-routing scan and the Belady replay with
+per-event resident-set output) and reduced here to the decode events.  Any
+trace: prefill (``include_prefill`` decides whether prefill events update the
+feature tracker) and several sequences.  Bit-identical to the reference
+(tests/test_dataset_gpu.py).
 """
 from __future__ import annotations
 
@@ -34,36 +36,47 @@ class LayerDataset:
 
 
 def build_training_data_device(trace: DeviceTrace, capacity: int, distance_cap: int = DEFAULT_DISTANCE_CAP,
-                               device: int = 0):
-    """(features [chain][T][2E], targets [chain][T][E], masks [chain][T][E]) CUDA tensors."""
-    if not trace.uniform:
-        raise ValueError("GPU training data needs a decode-only single-sequence trace")
-    n, T, E = trace.num_chains, trace.events_per_chain, trace.num_experts
+                               include_prefill: bool = True, device: int = 0):
+    """(features [event][2E], targets [event][E], masks [event][E]) CUDA tensors
+    for every event of every chain (mcb_trace order)."""
+    n, E = trace.total_events, trace.num_experts
     dev = trace.acc.device
-    feats = torch.empty((n, T, 2 * E), dtype=torch.float64, device=dev)
-    targs = torch.empty((n, T, E), dtype=torch.float64, device=dev)
-    masks = torch.empty((n, T, E), dtype=torch.uint8, device=dev)
+    feats = torch.empty((max(n, 1), 2 * E), dtype=torch.float64, device=dev)
+    targs = torch.empty((max(n, 1), E), dtype=torch.float64, device=dev)
+    masks = torch.empty((max(n, 1), E), dtype=torch.uint8, device=dev)
     v = trace.view()
     s = torch.cuda.current_stream(dev)
     _lib.check(_lib.load_library().mcb_training_data(_lib.context(device), ctypes.byref(v), int(capacity),
-                                                     int(distance_cap), feats.data_ptr(), targs.data_ptr(),
-                                                     masks.data_ptr(), ctypes.c_void_p(s.cuda_stream)))
-    return feats, targs, masks
+                                                     int(distance_cap), int(bool(include_prefill)),
+                                                     feats.data_ptr(), targs.data_ptr(), masks.data_ptr(),
+                                                     ctypes.c_void_p(s.cuda_stream)))
+    return feats[:n], targs[:n], masks[:n]
 
 
 def build_training_data(trace, capacity: int, distance_cap: int = DEFAULT_DISTANCE_CAP,
                         include_prefill: bool = True, device: int = 0) -> dict:
-    """One LayerDataset per layer (dataset.py:35-96).  ``include_prefill`` has
-    no effect on decode-only traces, the only ones the GPU path accepts."""
-    if distance_cap < 1:
-        raise ValueError(f"distance_cap must be >= 1, got {distance_cap}")
+    """One LayerDataset per layer, samples = the layer's decode events (dataset.py:35-96)."""
     packed = trace if isinstance(trace, PackedTrace) else pack_trace(trace)
-    if packed.num_traces != 1:
-        raise ValueError("build_training_data takes one trace")
     if capacity < packed.top_k:
         raise ValueError(f"capacity {capacity} is below top_k {packed.top_k}")
+    if distance_cap < 1:
+        raise ValueError(f"distance_cap must be >= 1, got {distance_cap}")
+    if packed.num_traces != 1:
+        raise ValueError("build_training_data takes one trace")
     dt = DeviceTrace.from_packed(packed, device=torch.device("cuda", device))
-    f, t, m = build_training_data_device(dt, capacity, distance_cap, device)
+    f, t, m = build_training_data_device(dt, capacity, distance_cap, include_prefill, device)
     f, t, m = f.cpu().numpy(), t.cpu().numpy(), m.cpu().numpy().astype(bool)
-    return {layer: LayerDataset(features=f[layer], targets=t[layer], masks=m[layer])
-            for layer in range(packed.num_layers)}
+    E, L = packed.num_experts, packed.num_layers
+    out = {}
+    for layer in range(L):
+        if packed.uniform:
+            e0, e1 = layer * packed.events_per_chain, (layer + 1) * packed.events_per_chain
+            sel = np.arange(e0, e1)
+        else:
+            e0, e1 = int(packed.chain_ev_off[layer]), int(packed.chain_ev_off[layer + 1])
+            dec = ((packed.ev_info[e0:e1] >> 30) & 1).astype(bool)
+            sel = e0 + np.nonzero(dec)[0]
+        out[layer] = LayerDataset(features=f[sel] if len(sel) else np.zeros((0, 2 * E)),
+                                  targets=t[sel] if len(sel) else np.zeros((0, E)),
+                                  masks=m[sel] if len(sel) else np.zeros((0, E), dtype=bool))
+    return out
