@@ -55,3 +55,38 @@ def test_non_finite_loss_raises_like_reference():
     net = mcb.EvictionNet(c["E"], hidden=c["hidden"], seed=0)
     with pytest.raises(train.NonFiniteLossError, match=r"non-finite loss nan at epoch 1, batch offset \d+"):
         train.train_eviction_net(net, f, Z[c["name"] + "_t"], Z[c["name"] + "_m"], train.TrainConfig(epochs=2))
+
+
+def test_efficacy_net_retrained_on_gpu():
+    """End to end (test_acceptance.py:223-275): the efficacy net is retrained on
+    the GPU from GPU-generated traces and GPU training data, and compared with
+    the reference-trained checkpoint (tests/golden/efficacy_net.evnet) and its
+    held-out hit rates (ml 82.90 / lru 81.30 / lfu 79.78)."""
+    from golden_util import load
+    from paper_2601_17063_b200 import dataset, refgen
+    from paper_2601_17063_b200.trace import TraceHeader
+    header = TraceHeader("efficacy", 1, 64, 8)
+    feats, targs, masks = [], [], []
+    for s in (101, 102, 103):
+        cfg = refgen.SyntheticWorkloadConfig(num_seqs=8, decode_steps=2500, prefill_tokens=32, zipf_s=1.0,
+                                             recency_boost=0.3, w_hot=4, rng_seed=s, popularity_seed=7)
+        ds = dataset.build_training_data(refgen.generate_trace(header, cfg), 64, 64)[0]
+        feats.append(ds.features)
+        targs.append(ds.targets)
+        masks.append(ds.masks)
+    net = mcb.EvictionNet(64, seed=0)
+    res = train.train_eviction_net(net, np.concatenate(feats), np.concatenate(targs), np.concatenate(masks),
+                                   train.TrainConfig(seed=0))
+    ref = mcb.load_net(os.path.join(GOLDEN, "efficacy_net.evnet"))
+    np.testing.assert_allclose(flat(res.net), ref.flat_params(), rtol=1e-6, atol=1e-9)
+    import oracle
+    from golden_util import case_trace
+    rates = []
+    for case in load("efficacy_cases.json.gz")["cases"]:
+        header_, events = case_trace(case)
+        from paper_2601_17063_b200.trace import AccessEvent, Phase, RoutingTrace
+        L, E, K = header_
+        tr = RoutingTrace(TraceHeader("e", L, E, K),
+                          tuple(AccessEvent(s, Phase(p), t, l, tuple(x)) for s, p, t, l, x in events))
+        rates.append(mcb.simulate(tr, "ml", 32, nets=res.net).hit_rate)
+    assert round(100 * float(np.mean(rates)), 2) == 82.90
