@@ -95,6 +95,7 @@ struct mcb_ctx {
     cudaEvent_t join2 = nullptr;
     int64_t ml_chunks = 1;             // K3 / ML replay pipeline depth (MCB_TUNE_ML_CHUNKS)
     int k3_ctas = -1;                  // K3 grid mode (MCB_TUNE_K3_CTAS)
+    int overlap = 0;                   // non-ML replay: 0 after K3 (next to the ML replay), 1 during K3
     int64_t solo_min_instances = 0;   // thread-per-instance whenever E <= 16 (MCB_SOLO_MIN overrides)
     int64_t seg_ev = 0;               // segmented replay: 0 auto, <0 off, >0 events per segment (MCB_SEG_EV)
     int64_t seg_nw = 0;               // warm-up events before each segment: 0 auto (MCB_SEG_NW)
@@ -200,6 +201,10 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
         c->serial = value != 0;
         return MCB_OK;
     }
+    if (knob == MCB_TUNE_OVERLAP) {
+        c->overlap = (int)value;
+        return MCB_OK;
+    }
     if (knob == MCB_TUNE_ML_CHUNKS) {
         c->ml_chunks = value;
         return MCB_OK;
@@ -257,6 +262,7 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     if (const char *env = getenv("MCB_GROUP_LANES")) c->group_lanes = atoll(env);
     if (const char *env = getenv("MCB_K3_CTAS")) c->k3_ctas = atoi(env);
     if (const char *env = getenv("MCB_ML_CHUNKS")) c->ml_chunks = atoll(env);
+    if (const char *env = getenv("MCB_OVERLAP")) c->overlap = atoi(env);
     for (auto &e : c->chunk_ev)
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
             delete c;
@@ -590,19 +596,30 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         c->ran[0] = true;
     }
     if (P.seg.n_seg > 1) launched += launch_seg_snapshot(P, s);
-    if (split) {
-        CUDA_TRY(cudaEventRecord(c->fork, s));
-        CUDA_TRY(cudaStreamWaitEvent(c->side, c->fork, 0));
-    }
     for (int i = 0; i < Pn.n_pol_launch; ++i)
         if (pols[Pn.pol_map[i]] == MCB_FIFO || pols[Pn.pol_map[i]] == MCB_ARC || pols[Pn.pol_map[i]] == MCB_LECAR)
             Pn.seg.n_seg = 0;   // their eviction order depends on the cache state
-    if (Pn.n_pol_launch > 0) {
-        mark(c, 4, sn);
-        launched += seg_eligible(Pn) ? launch_replay_segmented(Pn, sn) : launch_replay(Pn, sn);
-        mark(c, 5, sn);
-        c->ran[2] = true;
-    }
+    // Where the non-ML replay overlaps: during K3 (it then competes with the
+    // scorer for issue slots), or after it, next to the ML replay (both are
+    // latency-bound and leave most of the GPU idle).  See MCB_TUNE_OVERLAP.
+    auto launch_non_ml = [&]() -> int {
+        if (split) {
+            CUDA_TRY(cudaEventRecord(c->fork, s));
+            CUDA_TRY(cudaStreamWaitEvent(c->side, c->fork, 0));
+        }
+        if (Pn.n_pol_launch > 0) {
+            mark(c, 4, sn);
+            launched += seg_eligible(Pn) ? launch_replay_segmented(Pn, sn) : launch_replay(Pn, sn);
+            mark(c, 5, sn);
+            c->ran[2] = true;
+        }
+        return MCB_OK;
+    };
+    const bool chunked = Pm.n_pol_launch > 0 && d.uniform && !c->serial && !(need_ml[0] && need_ml[1]) &&
+                         std::min<int64_t>(std::min<int64_t>(c->ml_chunks, MCB_MAX_ML_CHUNKS), d.n_chains) > 1;
+    const bool after_k3 = split && c->overlap == 0 && Pm.n_pol_launch > 0 && !chunked;
+    if (!after_k3)
+        if (int rc = launch_non_ml()) return rc;
     // K3 / ML-replay pipeline: the chains are cut into ml_chunks ranges; K3
     // scores them in order on s and the ML replay of a range starts on side2
     // as soon as its ranks are written, overlapping K3 on the next range
@@ -653,6 +670,8 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
             Pm.rank[v] = (const uint8_t *)c->ranks[v].p;
         }
         mark(c, 3, s);
+        if (after_k3)
+            if (int rc = launch_non_ml()) return rc;
         mark(c, 6, s);
         launched += seg_eligible(Pm) ? launch_replay_segmented(Pm, s) : launch_replay(Pm, s);
         mark(c, 7, s);
