@@ -93,6 +93,7 @@ struct mcb_ctx {
     cudaStream_t side2 = nullptr;      // ML replay chunks, pipelined behind the K3 chunks
     cudaEvent_t chunk_ev[MCB_MAX_ML_CHUNKS] = {};
     cudaEvent_t join2 = nullptr;
+    cudaEvent_t pre = nullptr;         // the side stream's replay preparation is done
     int64_t ml_chunks = 1;             // K3 / ML replay pipeline depth (MCB_TUNE_ML_CHUNKS)
     int k3_ctas = -1;                  // K3 grid mode (MCB_TUNE_K3_CTAS)
     int overlap = 0;                   // non-ML replay: 0 after K3 (next to the ML replay), 1 during K3
@@ -274,6 +275,7 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
         cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c->side2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join2, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->pre, cudaEventDisableTiming) != cudaSuccess ||
 
         cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess) {
@@ -300,6 +302,7 @@ extern "C" int mcb_ctx_destroy(mcb_ctx *c) {
     if (c->side) cudaStreamDestroy(c->side);
     if (c->side2) cudaStreamDestroy(c->side2);
     if (c->join2) cudaEventDestroy(c->join2);
+    if (c->pre) cudaEventDestroy(c->pre);
     for (auto &e : c->chunk_ev)
         if (e) cudaEventDestroy(e);
 
@@ -587,15 +590,26 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     const size_t nu_sw = need_next ? next_use_scratch_words(d) : 0;
     if (nu_sw)
         if (int rc = c->nu_scratch.ensure(nu_sw * sizeof(uint32_t))) return rc;
+    const bool chunked = Pm.n_pol_launch > 0 && d.uniform && !c->serial && !(need_ml[0] && need_ml[1]) &&
+                         std::min<int64_t>(std::min<int64_t>(c->ml_chunks, MCB_MAX_ML_CHUNKS), d.n_chains) > 1;
+    const bool after_k3 = split && c->overlap == 0 && Pm.n_pol_launch > 0 && !chunked;
+    // With the replays after K3, the replays' own preparation (K2 next-use scan,
+    // key snapshots) runs on the side stream under K3; the ML replay waits for it.
+    cudaStream_t sp = after_k3 ? c->side : s;
+    if (after_k3) {
+        CUDA_TRY(cudaEventRecord(c->fork, s));
+        CUDA_TRY(cudaStreamWaitEvent(c->side, c->fork, 0));
+    }
     if (need_next) {
         if (int rc = c->next_pos.ensure((size_t)(d.total_acc + 64) * sizeof(uint32_t))) return rc;
         Pn.next_pos = Pm.next_pos = (const uint32_t *)c->next_pos.p;
-        mark(c, 0, s);
-        launched += launch_next_use(d, (uint32_t *)c->next_pos.p, nu_sw ? (uint32_t *)c->nu_scratch.p : nullptr, s);
-        mark(c, 1, s);
+        mark(c, 0, sp);
+        launched += launch_next_use(d, (uint32_t *)c->next_pos.p, nu_sw ? (uint32_t *)c->nu_scratch.p : nullptr, sp);
+        mark(c, 1, sp);
         c->ran[0] = true;
     }
-    if (P.seg.n_seg > 1) launched += launch_seg_snapshot(P, s);
+    if (P.seg.n_seg > 1) launched += launch_seg_snapshot(P, sp);
+    if (after_k3) CUDA_TRY(cudaEventRecord(c->pre, c->side));
     for (int i = 0; i < Pn.n_pol_launch; ++i)
         if (pols[Pn.pol_map[i]] == MCB_FIFO || pols[Pn.pol_map[i]] == MCB_ARC || pols[Pn.pol_map[i]] == MCB_LECAR)
             Pn.seg.n_seg = 0;   // their eviction order depends on the cache state
@@ -615,9 +629,6 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         }
         return MCB_OK;
     };
-    const bool chunked = Pm.n_pol_launch > 0 && d.uniform && !c->serial && !(need_ml[0] && need_ml[1]) &&
-                         std::min<int64_t>(std::min<int64_t>(c->ml_chunks, MCB_MAX_ML_CHUNKS), d.n_chains) > 1;
-    const bool after_k3 = split && c->overlap == 0 && Pm.n_pol_launch > 0 && !chunked;
     if (!after_k3)
         if (int rc = launch_non_ml()) return rc;
     // K3 / ML-replay pipeline: the chains are cut into ml_chunks ranges; K3
@@ -670,8 +681,10 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
             Pm.rank[v] = (const uint8_t *)c->ranks[v].p;
         }
         mark(c, 3, s);
-        if (after_k3)
+        if (after_k3) {
             if (int rc = launch_non_ml()) return rc;
+            CUDA_TRY(cudaStreamWaitEvent(s, c->pre, 0));   // key snapshots / next-use for the ML replay
+        }
         mark(c, 6, s);
         launched += seg_eligible(Pm) ? launch_replay_segmented(Pm, s) : launch_replay(Pm, s);
         mark(c, 7, s);
