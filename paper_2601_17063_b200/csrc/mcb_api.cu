@@ -557,7 +557,9 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         ReplayParams probe = P;
         probe.seg.n_seg = 2;
         const bool solo_ok = n_launch >= c->solo_min_instances;
-        const int se = (c->seg_ev >= 0 && solo_ok && d.uniform) ? seg_events_per_segment(d.T, n_launch, c->seg_ev, d.E) : 0;
+        const bool paired = split && c->overlap == 0;   // ML and non-ML replays side by side after K3
+        const int se = (c->seg_ev >= 0 && solo_ok && d.uniform)
+                           ? seg_events_per_segment(d.T, n_launch, c->seg_ev, d.E, paired) : 0;
         if (se > 0 && seg_eligible(probe)) {
             P.seg.SE = se;
             P.seg.n_seg = (int)((d.T + se - 1) / se);

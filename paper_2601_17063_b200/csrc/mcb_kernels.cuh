@@ -100,7 +100,7 @@ void prepare_launch_attributes(const DevTrace &tr, int H);
 int preload_kernels();   // force module loading + smem attributes (call at context creation)
 // segmented replay (uniform traces, num_experts <= 16); seg_* are host helpers
 bool seg_eligible(const ReplayParams &p);
-int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se, int E);
+int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se, int E, bool paired);
 size_t seg_snap_bytes(int64_t n_chains, int n_snap, int E);
 int seg_snap_stride(int E);
 int preload_segment_warp_kernels();

@@ -59,15 +59,18 @@ bool seg_eligible(const ReplayParams &p) {
            p.tr.T * p.tr.K < (1ll << 27);   // chain-local positions pack into 27 bits
 }
 
-int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se, int E) {
+int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se, int E, bool paired) {
     // enough (instance, segment) workers to fill every SM several times over:
     // threads for the thread-per-instance replay (E <= 16), warps for the
     // warp-per-instance one.  Thread segments are at least 2 default warm-ups
-    // long (measured best on C2); warp segments at least 256 events (C1,
-    // E = 128: shorter segments coalesce too rarely and the fix-ups dominate).
+    // long, 4 when the ML and non-ML replays run side by side after the
+    // scorer (paired; measured on C2: 512 / 768 / 1024 / 1536 events = 5.31 /
+    // 5.26 / 5.21 / 5.52 ms per step, tools/seg_sweep2.sh); warp segments at
+    // least 256 events (C1, E = 128: shorter segments coalesce too rarely and
+    // the fix-ups dominate).
     const bool warp = E > SEG_MAX_E;
     const int64_t target = warp ? 148ll * 32 : 148ll * 1024;
-    const int64_t min_se = warp ? 8 * MCB_SNAP_EV : 2 * SEG_DEFAULT_NW;
+    const int64_t min_se = warp ? 8 * MCB_SNAP_EV : (paired ? 4 : 2) * SEG_DEFAULT_NW;
     int64_t se;
     if (override_se > 0) {
         se = override_se;
