@@ -105,7 +105,13 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region.
+
+    nvidia-smi takes ~100 ms to start, longer than a short timed region, so
+    the sampler is started (and its first line awaited) before the region;
+    a reader thread timestamps every line and only lines read between
+    begin() and stop() count.  A region shorter than the 50 ms sampling
+    period still gets the first sample taken after it began."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -114,21 +120,47 @@ class ClockSampler:
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+        self.lines = []
+        self.t0 = None
 
     def start(self):
+        import threading
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+            return
+        first = threading.Event()
+
+        def reader():
+            for line in self.proc.stdout:
+                self.lines.append((time.perf_counter(), line))
+                first.set()
+        threading.Thread(target=reader, daemon=True).start()
+        first.wait(timeout=10)
+
+    def begin(self):
+        self.t0 = time.perf_counter()
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t1 = time.perf_counter()
+        t0 = self.t0 if self.t0 is not None else t1
+        deadline = time.perf_counter() + 1.0
+        while not any(t >= t0 for t, _ in self.lines) and time.perf_counter() < deadline:
+            time.sleep(0.01)
         self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
-        rows = [r.split(",") for r in out.strip().splitlines() if r.strip()]
+        try:
+            self.proc.wait(timeout=10)
+        except Exception:
+            pass
+        inside = [ln for t, ln in self.lines if t0 <= t <= t1]
+        if not inside:   # region shorter than the sampling period: first sample after it began
+            inside = [ln for t, ln in self.lines if t >= t0][:1]
+        rows = [r.split(",") for r in inside if r.strip()]
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
@@ -330,6 +362,7 @@ def main():
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
+    clocks.start()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     stage = np.zeros(5)
@@ -337,7 +370,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.begin()
     for i in range(args.steps):
         flush.zero_()
         starts[i].record(stream)
