@@ -152,7 +152,15 @@ typedef struct {
 
 typedef struct mcb_ctx mcb_ctx;
 
-/* ---- lifecycle / errors ---- */
+/* ---- lifecycle / errors ----
+ * Threading model: a context owns device scratch buffers (next-use, ranks,
+ * segment records, duel and training workspaces) that its asynchronous
+ * entry points reuse, plus per-context settings (tuning knobs, LeCaR
+ * parameters).  Calls on one context are serialised by an internal mutex,
+ * but their device work is only ordered on the stream passed in: issue the
+ * asynchronous calls of one context on one stream (or synchronise between
+ * streams), and give each host thread that changes settings its own
+ * context.  mcb_last_error is thread-local. */
 int mcb_abi_version(void);
 int mcb_ctx_create(int device, mcb_ctx **out);
 int mcb_ctx_destroy(mcb_ctx *ctx);
