@@ -523,11 +523,14 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     if (need_lecar)
         if (int rc = lecar_prepare(c, d, caps, n_cap, P, s)) return rc;
 
-    // Orchestration.  K3 (ML scores) is only needed by ML instances, so when
-    // both kinds are present the non-ML replay runs on a high-priority side
-    // stream concurrently with K3, and the ML replay follows K3:
-    //     s:    K2 -- snapshot --+-- K3 -- K4(ml) --+-- K5
-    //     side:                  +-- K4(lru/lfu/belady) --+
+    // Orchestration.  K3 (ML scores) is only needed by ML instances.  When
+    // both kinds are present (default, MCB_TUNE_OVERLAP = 0) K3 runs alone
+    // while the side stream prepares the replays, then the two replays --
+    // both latency-bound -- run side by side:
+    //     s:    +-- K3 ---------------+-- (wait pre) K4(ml) --+-- K5
+    //     side: +-- K2 -- snapshot    +-- K4(lru/lfu/belady) -+
+    // With MCB_TUNE_OVERLAP = 1 the non-ML replay runs under K3 instead
+    // (measured slower: it competes with the scorer for issue slots).
     const int64_t n_inst = d.n_chains * n_pol * n_cap;
     if (out->chain_reports) {
         P.inst_out = out->chain_reports;
