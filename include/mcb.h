@@ -209,6 +209,10 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
 /* MCB_TUNE_OVERLAP: where the non-ML replay runs concurrently -- 0 (default)
  * after the scorer, next to the ML replay; 1 during the scorer. */
 #define MCB_TUNE_OVERLAP 8
+/* MCB_TUNE_WIDE_MIN: minimum instance count for the thread-per-instance
+ * replay of 16 < num_experts <= 64 (default 16384); below it one warp
+ * replays one instance. */
+#define MCB_TUNE_WIDE_MIN 9
 int mcb_set_tuning(mcb_ctx *ctx, int32_t knob, int64_t value);
 /* LeCaR parameters used by the MCB_LECAR cells of later mcb_replay calls on
  * this context (LeCaRPolicy.__init__, policies.py:333-349; defaults 0.45,

@@ -98,6 +98,7 @@ struct mcb_ctx {
     int k3_ctas = -1;                  // K3 grid mode (MCB_TUNE_K3_CTAS)
     int overlap = 0;                   // non-ML replay: 0 after K3 (next to the ML replay), 1 during K3
     int64_t solo_min_instances = 0;   // thread-per-instance whenever E <= 16 (MCB_SOLO_MIN overrides)
+    int64_t wide_min_instances = 16384;   // thread-per-instance for 16 < E <= 64 from this many (MCB_WIDE_MIN)
     int64_t seg_ev = 0;               // segmented replay: 0 auto, <0 off, >0 events per segment (MCB_SEG_EV)
     int64_t seg_nw = 0;               // warm-up events before each segment: 0 auto (MCB_SEG_NW)
     int64_t seg_passes = 0;           // speculation passes (MCB_SEG_PASSES): 0 auto, 1 or 2
@@ -202,6 +203,10 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
         c->serial = value != 0;
         return MCB_OK;
     }
+    if (knob == MCB_TUNE_WIDE_MIN) {
+        c->wide_min_instances = value;
+        return MCB_OK;
+    }
     if (knob == MCB_TUNE_OVERLAP) {
         c->overlap = (int)value;
         return MCB_OK;
@@ -250,13 +255,15 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     CUDA_TRY(cudaGetDeviceProperties(&prop, device));
     if (prop.major < 10)
         return mcb_set_error(MCB_ERR_UNSUPPORTED, "libmcb is built for sm_100a (B200); device is older");
-    if (preload_kernels() != 0 || preload_segment_kernels() != 0 || preload_segment_warp_kernels() != 0)
+    if (preload_kernels() != 0 || preload_segment_kernels() != 0 || preload_segment_warp_kernels() != 0 ||
+        preload_wide_kernels() != 0)
         return mcb_set_error(MCB_ERR_CUDA, "failed to load the replay kernels");
     if (int rc = mcb_router_preload()) return rc;
     auto *c = new (std::nothrow) mcb_ctx();
     if (!c) return mcb_set_error(MCB_ERR_NOMEM, "out of host memory");
     c->device = device;
     if (const char *env = getenv("MCB_SOLO_MIN")) c->solo_min_instances = atoll(env);
+    if (const char *env = getenv("MCB_WIDE_MIN")) c->wide_min_instances = atoll(env);
     if (const char *env = getenv("MCB_SEG_EV")) c->seg_ev = atoll(env);
     if (const char *env = getenv("MCB_SEG_NW")) c->seg_nw = atoll(env);
     if (const char *env = getenv("MCB_SEG_PASSES")) c->seg_passes = atoll(env);
@@ -516,6 +523,7 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     P.loads_serial = cost->loads_serial;
     P.window = cost->window;
     P.solo_min_instances = c->solo_min_instances;
+    P.wide_min_instances = c->wide_min_instances;
     P.stats = (unsigned long long *)c->stats.p;
     P.chain_lo = 0;
     P.chain_hi = d.n_chains;

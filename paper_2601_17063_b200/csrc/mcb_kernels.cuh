@@ -49,6 +49,7 @@ struct ReplayParams {
     uint64_t *hashes;                   // optional [chain][pol][cap]
     uint16_t *outcomes;                 // optional [pol][cap][total_acc]
     int64_t solo_min_instances;         // thread-per-instance kernel threshold (E <= 16)
+    int64_t wide_min_instances;         // thread-per-instance kernel threshold (16 < E <= 64)
     int64_t chain_lo, chain_hi;         // chains [lo, hi) replayed by this launch (outputs stay global)
     int group_lanes;                    // lane-group size of k_replay (0 = automatic)
     uint8_t *res_masks;                 // optional [chain][T][E]: resident set at each event start
@@ -96,6 +97,8 @@ struct SegOut {
 int launch_next_use(const DevTrace &tr, uint32_t *next_pos, uint32_t *scratch, cudaStream_t s);
 size_t next_use_scratch_words(const DevTrace &tr);   // scratch for the blocked walk (0: not used)
 int launch_replay(const ReplayParams &p, cudaStream_t s);
+int launch_replay_wide(const ReplayParams &p, cudaStream_t s);   // mcb_wide.cu; 0 = not applicable
+int preload_wide_kernels();
 void prepare_launch_attributes(const DevTrace &tr, int H);
 int preload_kernels();   // force module loading + smem attributes (call at context creation)
 // segmented replay (uniform traces, num_experts <= 16); seg_* are host helpers

@@ -1,0 +1,211 @@
+// K4-wide: one THREAD per cache instance for 16 < num_experts <= 64 (whole
+// chains; LRU, LFU, Belady, ML, FIFO).  The warp-per-instance replay
+// (k_replay) spends a warp's issue slot on every access; here one thread
+// carries the instance:
+//   * resident / pinned / seen / selectable sets and the refetch ring are
+//     64-bit masks in registers;
+//   * the per-expert packed keys (key << 6 | id) live in
+//     shared memory, column-major per thread (keys[s][thread]), so the
+//     per-access key write is one conflict-free store whatever the expert;
+//   * the victim is the minimum key over the candidate bits only (at most C
+//     loads), and only on an evicting miss.
+// Semantics are sstep()'s (mcb_solo.cuh) on 64-bit masks: policies.py:95-214,
+// mlpolicy.py:15-26, engine.py:229-257 (pinning), engine.py:266-297 (refetch).
+// Used when there are enough instances to fill the GPU (many traces, e.g. C4).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mcb_internal.h"
+#include "mcb_kernels.cuh"
+#include "mcb_solo.cuh"
+
+namespace wide {
+
+constexpr int BS = 128;     // threads per block
+constexpr int EMAX = 64;
+constexpr int SH = 6;       // id bits of a packed key
+constexpr uint32_t KMAX = (1u << (32 - SH)) - 1u;
+
+template <int POL, bool UNIFORM, int WMAX>
+__device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t chain, int pol_i, int cap_i,
+                                              int ml_variant, uint32_t *sk) {
+    const DevTrace &tr = P.tr;
+    const uint32_t C = (uint32_t)P.cap[cap_i];
+    const int E = tr.E;
+    const int W = P.window;
+    const int64_t inst = (chain * P.n_pol + pol_i) * P.n_cap + cap_i;
+    auto key = [&](int s) -> uint32_t & { return sk[s * BS]; };
+    for (int s = 0; s < E; ++s) key(s) = (uint32_t)s;
+
+    uint64_t res = 0, seen = 0, ring_or = 0;
+    uint64_t ring[WMAX + 1];
+#pragma unroll
+    for (int s = 0; s <= WMAX; ++s) ring[s] = 0;
+    const uint64_t all = E == 64 ? ~0ull : ((1ull << E) - 1ull);
+    uint64_t valid = all;
+    uint32_t ph = 0, pm = 0, dh = 0, dm = 0, comp = 0, nev = 0, refc = 0;
+    double dlat = 0.0, plat = 0.0;
+    uint64_t h = 0;
+    bool stuck = false;
+
+    const int64_t a0 = tr.acc_begin(chain);
+    const int64_t e0 = tr.ev_begin(chain);
+    const int64_t n_ev = tr.ev_end(chain) - e0;
+    const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
+    uint16_t *outc = P.outcomes ? P.outcomes + ((int64_t)pol_i * P.n_cap + cap_i) * tr.total_acc : nullptr;
+    const bool track = outc != nullptr || P.hashes != nullptr;
+
+    int64_t A = a0;
+    uint32_t pos = 0;
+    for (int64_t ev = 0; ev < n_ev; ++ev) {
+        const uint32_t info = UNIFORM ? mcb_ev_pack((uint32_t)tr.K, (uint32_t)tr.K, true, ev == 0)
+                                      : __ldg(tr.ev_info + e0 + ev);
+        const uint32_t nacc = mcb_ev_nacc(info);
+        const bool decode = UNIFORM ? true : mcb_ev_decode(info);
+        if (POL == POL_LFU && !UNIFORM && mcb_ev_newseq(info))
+            for (int s = 0; s < E; ++s) key(s) = (uint32_t)s;   // start_sequence (policies.py:184-185)
+        if (P.res_masks) {   // resident set before the event (dataset.py:61-63)
+            uint8_t *m = P.res_masks + (e0 + ev) * E;
+            for (int e = 0; e < E; ++e) m[e] = (uint8_t)((res >> e) & 1ull);
+        }
+        if (POL == POL_ML) {   // this event's rank row (mlpolicy.py:59-62): argmax score == argmin (256 - rank)
+            const uint8_t *row = rank + (e0 + ev) * E;
+            valid = 0;
+            for (int s = 0; s < E; ++s) {
+                const uint32_t r = __ldcg(row + s);
+                key(s) = ((256u - r) << SH) | (uint32_t)s;
+                valid |= (uint64_t)(r != 0u) << s;
+            }
+        }
+        uint64_t pin = 0;
+        uint32_t step_miss = 0;
+        for (uint32_t j = 0; j < nacc; ++j, ++pos, ++A) {
+            const uint32_t x = __ldg(tr.acc + A);
+            const uint64_t bit = 1ull << x;
+            // trace-determined key of x (applied before the victim search; x is never a candidate)
+            if (POL == POL_LRU) key(x) = (pos << SH) | x;
+            if (POL == POL_LFU) key(x) += 1u << SH;
+            if (POL == POL_BELADY) {
+                const uint32_t np = __ldg(P.next_pos + A);
+                key(x) = ((np == MCB_NEXT_INF ? 0u : KMAX - np) << SH) | x;
+            }
+            const bool hit = (res & bit) != 0ull;
+            uint32_t code = MCB_OUT_HIT;
+            if (!hit) {
+                uint64_t vbit = 0;
+                code = MCB_OUT_MISS;
+                if ((uint32_t)__popcll(res) >= C) {
+                    uint64_t cand = res & ~pin & valid;
+                    if (!cand) {
+                        stuck = true;
+                    } else {
+                        uint32_t best = ~0u;
+                        do {
+                            const int s = __ffsll((long long)cand) - 1;
+                            cand &= cand - 1ull;
+                            best = min(best, key(s));
+                        } while (cand);
+                        const uint32_t v = best & (uint32_t)(EMAX - 1);
+                        vbit = 1ull << v;
+                        code = v;
+                        ++nev;
+                    }
+                }
+                res = (res & ~vbit) | bit;
+                refc += (bit & ring_or) ? 1u : 0u;   // refetch of an earlier victim within the window
+                ring_or = (ring_or & ~bit) | vbit;
+#pragma unroll
+                for (int s = 0; s <= WMAX; ++s) ring[s] &= ~bit;
+                ring[0] |= vbit;
+                if (POL == POL_FIFO) key(x) = (pos << SH) | x;   // arrival (policies.py:159-161)
+                ++step_miss;
+                comp += (seen & bit) ? 0u : 1u;
+                if (decode) ++dm; else ++pm;
+            } else {
+                if (decode) ++dh; else ++ph;
+            }
+            seen |= bit;
+            if (decode) pin |= bit;
+            if (track) {
+                h = poly16(h, code);
+                if (outc) outc[A] = (uint16_t)code;
+            }
+        }
+        double lat;
+        if (step_miss > 0)
+            lat = __dmul_rn((double)(P.loads_serial ? step_miss : 1u), P.t_load);
+        else
+            lat = __dmul_rn((double)nacc, P.t_compute);
+        if (decode) {
+            dlat = __dadd_rn(dlat, __dadd_rn(lat, POL == POL_ML ? P.ml_cost : 0.0));
+#pragma unroll
+            for (int s = WMAX; s >= 1; --s) ring[s] = ring[s - 1];
+            ring[0] = 0;
+            uint64_t o = 0;
+#pragma unroll
+            for (int s = 0; s <= WMAX; ++s) o |= (s <= W) ? ring[s] : 0ull;
+            ring_or = o;
+        } else {
+            plat = __dadd_rn(plat, lat);
+        }
+    }
+    int64_t *o = P.inst_out + inst * MCB_R_N;
+    o[MCB_R_PREFILL_HITS] = ph;
+    o[MCB_R_PREFILL_MISSES] = pm;
+    o[MCB_R_DECODE_HITS] = dh;
+    o[MCB_R_DECODE_MISSES] = dm;
+    o[MCB_R_COMPULSORY] = comp;
+    o[MCB_R_EVICTIONS] = nev;
+    o[MCB_R_REFETCHED] = refc;
+    o[MCB_R_STATUS] = stuck ? MCB_ERR_NO_EVICTABLE : MCB_OK;
+    P.inst_lat[inst * 2 + 0] = dlat;
+    P.inst_lat[inst * 2 + 1] = plat;
+    if (P.hashes) P.hashes[inst] = h;
+}
+
+template <bool UNIFORM>
+__global__ void __launch_bounds__(BS) k_replay_wide(const __grid_constant__ ReplayParams P) {
+    extern __shared__ uint32_t s_keys[];   // [EMAX][BS]
+    const int pol_i = P.pol_map[blockIdx.y];
+    const int64_t t = (int64_t)blockIdx.x * BS + threadIdx.x;
+    if (t >= (P.chain_hi - P.chain_lo) * P.n_cap) return;
+    const int cap_i = (int)(t % P.n_cap);
+    const int64_t chain = P.chain_lo + t / P.n_cap;
+    uint32_t *sk = s_keys + threadIdx.x;
+    switch (P.pol[pol_i]) {
+        case MCB_LRU: wide_instance<POL_LRU, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0, sk); break;
+        case MCB_LFU: wide_instance<POL_LFU, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0, sk); break;
+        case MCB_BELADY: wide_instance<POL_BELADY, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0, sk); break;
+        case MCB_ML: wide_instance<POL_ML, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0, sk); break;
+        case MCB_FIFO: wide_instance<POL_FIFO, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0, sk); break;
+        default: wide_instance<POL_ML, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 1, sk); break;
+    }
+}
+
+}  // namespace wide
+
+// true when the launch was taken: 16 < E <= 64, only the policies above,
+// chains short enough for 26-bit positions, window <= SOLO_WMAX
+int launch_replay_wide(const ReplayParams &p, cudaStream_t s) {
+    const int E = p.tr.E;
+    if (E <= 16 || E > wide::EMAX || p.window < 0 || p.window > SOLO_WMAX) return 0;
+    const int64_t chain_bound = p.tr.uniform ? p.tr.T * p.tr.K : p.tr.total_acc;
+    if (chain_bound >= (1ll << 26)) return 0;
+    for (int i = 0; i < p.n_pol_launch; ++i) {
+        const int pol = p.pol[p.pol_map[i]];
+        if (pol == MCB_ARC || pol == MCB_LECAR) return 0;
+    }
+    const int64_t n = (p.chain_hi - p.chain_lo) * p.n_cap;
+    const dim3 grid((unsigned)((n + wide::BS - 1) / wide::BS), (unsigned)p.n_pol_launch);
+    const size_t smem = (size_t)wide::EMAX * wide::BS * sizeof(uint32_t);
+    if (p.tr.uniform) wide::k_replay_wide<true><<<grid, wide::BS, smem, s>>>(p);
+    else wide::k_replay_wide<false><<<grid, wide::BS, smem, s>>>(p);
+    return 1;
+}
+
+int preload_wide_kernels() {
+    cudaFuncAttributes a;
+    if (cudaFuncGetAttributes(&a, (const void *)wide::k_replay_wide<true>) != cudaSuccess) return -1;
+    if (cudaFuncGetAttributes(&a, (const void *)wide::k_replay_wide<false>) != cudaSuccess) return -1;
+    return 0;
+}

@@ -147,3 +147,45 @@ def test_full_size_c3():
         got = cr[c, :3].reshape(len(jobs), _lib.R_N)[:, :7]
         assert np.array_equal(got, cnt[i]), c
         assert np.array_equal(seg["hashes"][c, :3].reshape(len(jobs)), hsh[i]), c
+
+
+def zipf_ids(n, L, T, K, E, seed):
+    """[n][L][T][K] distinct-per-event Zipf-weighted ids (Gumbel top-K)."""
+    rng = np.random.default_rng(seed)
+    w = 1.0 / np.arange(1, E + 1)
+    perm = np.stack([rng.permutation(E) for _ in range(L)])          # per-layer popularity order
+    g = np.log(w)[None, None, None, :] - np.log(-np.log(rng.random((n, L, T, E))))
+    top = np.argsort(-g, axis=-1)[..., :K]
+    return np.take_along_axis(np.broadcast_to(perm[None, :, None, :], (n, L, T, E)), top, axis=-1).astype(np.uint8)
+
+
+def test_c4_shaped_wide_replay():
+    """C4-shaped batch (L=27, E=64, K=6, many traces): the thread-per-instance
+    replay for 16 < E <= 64 (k_replay_wide) against the warp-per-instance
+    kernel on every chain, and sampled chains against the oracle."""
+    n, L, E, K, T, caps = 64, 27, 64, 6, 512, [16, 24]
+    ids = zipf_ids(n, L, T, K, E, seed=4)
+    packed = mcb.packed_from_decode_ids(ids, E)
+    nets = oracle.nets_from_spec({"kind": "per_layer_seed"}, L, E)
+    codes = [_lib.MCB_LRU, _lib.MCB_LFU, _lib.MCB_BELADY, _lib.MCB_ML, _lib.MCB_FIFO]
+
+    def run(wide):
+        _lib.set_tuning(_lib.MCB_TUNE_WIDE_MIN, 0 if wide else 1 << 62)
+        try:
+            return engine.replay_host(packed, codes, caps, mcb.CostModel(), 5, nets, want_hashes=True,
+                                      want_chain=True)
+        finally:
+            _lib.set_tuning(_lib.MCB_TUNE_WIDE_MIN, 16384)
+
+    a, b = run(True), run(False)
+    assert np.all(a["chain_reports"][..., _lib.R_STATUS] == 0)
+    assert np.array_equal(a["chain_reports"], b["chain_reports"])
+    assert np.array_equal(a["hashes"], b["hashes"])
+    assert np.array_equal(a["latency"], b["latency"])
+    sub = np.ascontiguousarray(ids[0, :2])
+    jobs = [(p, c) for p in ("lru", "lfu", "belady", "fifo") for c in caps]
+    cnt, lat, hsh = oracle.replay_uniform(sub, 2, E, jobs, None, 5, None, hash_kind="poly")
+    for c in range(2):
+        got = a["chain_reports"][c][[0, 1, 2, 4]].reshape(len(jobs), _lib.R_N)[:, :7]
+        assert np.array_equal(got, cnt[c]), c
+        assert np.array_equal(a["hashes"][c][[0, 1, 2, 4]].reshape(len(jobs)), hsh[c]), c

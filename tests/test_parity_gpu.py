@@ -68,7 +68,7 @@ def check_case(case, decisions=True):
             assert got == run["decisions"], (case["name"], run["policy"])
 
 
-@pytest.fixture(params=["warp", "group8", "solo", "seg"])
+@pytest.fixture(params=["warp", "group8", "solo", "seg", "wide"])
 def kernel_variant(request):
     """Run each parity case through every replay kernel: one warp per
     instance, 8-lane groups (16 for num_experts > 64: 4 / 2 instances per
@@ -76,11 +76,13 @@ def kernel_variant(request):
     speculative replay (uniform traces, num_experts <= 16) with short
     segments so the stitching is exercised."""
     v = request.param
-    _lib.set_tuning(_lib.MCB_TUNE_SOLO_MIN, 1 << 62 if v in ("warp", "group8") else 0)
+    _lib.set_tuning(_lib.MCB_TUNE_SOLO_MIN, 1 << 62 if v in ("warp", "group8", "wide") else 0)
+    _lib.set_tuning(_lib.MCB_TUNE_WIDE_MIN, 0 if v == "wide" else 1 << 62)
     _lib.set_tuning(_lib.MCB_TUNE_GROUP_LANES, {"warp": 32, "group8": 8}.get(v, 0))
     _lib.set_tuning(_lib.MCB_TUNE_SEG_EV, 32 if v == "seg" else -1)
     yield v
     _lib.set_tuning(_lib.MCB_TUNE_SOLO_MIN, 0)
+    _lib.set_tuning(_lib.MCB_TUNE_WIDE_MIN, 16384)
     _lib.set_tuning(_lib.MCB_TUNE_GROUP_LANES, 0)
     _lib.set_tuning(_lib.MCB_TUNE_SEG_EV, 0)
 
