@@ -1,15 +1,15 @@
-// K4-wide: one THREAD per cache instance for 16 < num_experts <= 64 (whole
+// K4-wide: one THREAD per cache instance for 16 < num_experts <= 128 (whole
 // chains; LRU, LFU, Belady, ML, FIFO).  The warp-per-instance replay
 // (k_replay) spends a warp's issue slot on every access; here one thread
 // carries the instance:
 //   * resident / pinned / seen / selectable sets and the refetch ring are
-//     64-bit masks in registers;
-//   * the per-expert packed keys (key << 6 | id) live in
+//     64-bit (E <= 64) or 128-bit (two words) masks in registers;
+//   * the per-expert packed keys (key << 7 | id) live in
 //     shared memory, column-major per thread (keys[s][thread]), so the
 //     per-access key write is one conflict-free store whatever the expert;
 //   * the victim is the minimum key over the candidate bits only (at most C
 //     loads), and only on an evicting miss.
-// Semantics are sstep()'s (mcb_solo.cuh) on 64-bit masks: policies.py:95-214,
+// Semantics are sstep()'s (mcb_solo.cuh) on wide masks: policies.py:95-214,
 // mlpolicy.py:15-26, engine.py:229-257 (pinning), engine.py:266-297 (refetch).
 // Used when there are enough instances to fill the GPU (many traces, e.g. C4).
 #include <cuda_runtime.h>
@@ -22,11 +22,55 @@
 namespace wide {
 
 constexpr int BS = 128;     // threads per block
-constexpr int EMAX = 64;
-constexpr int SH = 6;       // id bits of a packed key
+constexpr int SH = 7;       // id bits of a packed key (E <= 128)
 constexpr uint32_t KMAX = (1u << (32 - SH)) - 1u;
 
-template <int POL, bool UNIFORM, int WMAX>
+// 128-bit expert mask as two words (EMAX = 128); EMAX = 64 uses one uint64_t
+struct M128 {
+    uint64_t lo, hi;
+};
+__device__ __forceinline__ M128 operator&(M128 a, M128 b) { return {a.lo & b.lo, a.hi & b.hi}; }
+__device__ __forceinline__ M128 operator|(M128 a, M128 b) { return {a.lo | b.lo, a.hi | b.hi}; }
+__device__ __forceinline__ M128 operator~(M128 a) { return {~a.lo, ~a.hi}; }
+__device__ __forceinline__ bool any(M128 a) { return (a.lo | a.hi) != 0ull; }
+__device__ __forceinline__ bool any(uint64_t a) { return a != 0ull; }
+__device__ __forceinline__ int popc(M128 a) { return __popcll(a.lo) + __popcll(a.hi); }
+__device__ __forceinline__ int popc(uint64_t a) { return __popcll(a); }
+template <typename M> __device__ __forceinline__ M zero();
+template <> __device__ __forceinline__ uint64_t zero<uint64_t>() { return 0ull; }
+template <> __device__ __forceinline__ M128 zero<M128>() { return {0ull, 0ull}; }
+template <typename M> __device__ __forceinline__ M bit_of(uint32_t x);
+template <> __device__ __forceinline__ uint64_t bit_of<uint64_t>(uint32_t x) { return 1ull << x; }
+template <> __device__ __forceinline__ M128 bit_of<M128>(uint32_t x) {
+    return x < 64 ? M128{1ull << x, 0ull} : M128{0ull, 1ull << (x - 64)};
+}
+template <typename M> __device__ __forceinline__ M first_n(int E);   // experts 0 .. E-1
+template <> __device__ __forceinline__ uint64_t first_n<uint64_t>(int E) { return E >= 64 ? ~0ull : ((1ull << E) - 1ull); }
+template <> __device__ __forceinline__ M128 first_n<M128>(int E) {
+    return E >= 128 ? M128{~0ull, ~0ull}
+                    : (E >= 64 ? M128{~0ull, E == 64 ? 0ull : ((1ull << (E - 64)) - 1ull)}
+                               : M128{(1ull << E) - 1ull, 0ull});
+}
+__device__ __forceinline__ bool test(uint64_t m, uint32_t x) { return (m >> x) & 1ull; }
+__device__ __forceinline__ bool test(M128 m, uint32_t x) { return x < 64 ? ((m.lo >> x) & 1ull) : ((m.hi >> (x - 64)) & 1ull); }
+// lowest set bit of a non-empty mask, removed
+__device__ __forceinline__ int pop_first(uint64_t &m) {
+    const int s = __ffsll((long long)m) - 1;
+    m &= m - 1ull;
+    return s;
+}
+__device__ __forceinline__ int pop_first(M128 &m) {
+    if (m.lo) {
+        const int s = __ffsll((long long)m.lo) - 1;
+        m.lo &= m.lo - 1ull;
+        return s;
+    }
+    const int s = __ffsll((long long)m.hi) - 1;
+    m.hi &= m.hi - 1ull;
+    return 64 + s;
+}
+
+template <int POL, bool UNIFORM, int WMAX, typename M>
 __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t chain, int pol_i, int cap_i,
                                               int ml_variant, uint32_t *sk) {
     const DevTrace &tr = P.tr;
@@ -37,12 +81,11 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
     auto key = [&](int s) -> uint32_t & { return sk[s * BS]; };
     for (int s = 0; s < E; ++s) key(s) = (uint32_t)s;
 
-    uint64_t res = 0, seen = 0, ring_or = 0;
-    uint64_t ring[WMAX + 1];
+    M res = zero<M>(), seen = zero<M>(), ring_or = zero<M>();
+    M ring[WMAX + 1];
 #pragma unroll
-    for (int s = 0; s <= WMAX; ++s) ring[s] = 0;
-    const uint64_t all = E == 64 ? ~0ull : ((1ull << E) - 1ull);
-    uint64_t valid = all;
+    for (int s = 0; s <= WMAX; ++s) ring[s] = zero<M>();
+    M valid = first_n<M>(E);
     uint32_t ph = 0, pm = 0, dh = 0, dm = 0, comp = 0, nev = 0, refc = 0;
     double dlat = 0.0, plat = 0.0;
     uint64_t h = 0;
@@ -66,22 +109,22 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
             for (int s = 0; s < E; ++s) key(s) = (uint32_t)s;   // start_sequence (policies.py:184-185)
         if (P.res_masks) {   // resident set before the event (dataset.py:61-63)
             uint8_t *m = P.res_masks + (e0 + ev) * E;
-            for (int e = 0; e < E; ++e) m[e] = (uint8_t)((res >> e) & 1ull);
+            for (int e = 0; e < E; ++e) m[e] = (uint8_t)test(res, (uint32_t)e);
         }
         if (POL == POL_ML) {   // this event's rank row (mlpolicy.py:59-62): argmax score == argmin (256 - rank)
             const uint8_t *row = rank + (e0 + ev) * E;
-            valid = 0;
+            valid = zero<M>();
             for (int s = 0; s < E; ++s) {
                 const uint32_t r = __ldcg(row + s);
                 key(s) = ((256u - r) << SH) | (uint32_t)s;
-                valid |= (uint64_t)(r != 0u) << s;
+                if (r != 0u) valid = valid | bit_of<M>((uint32_t)s);
             }
         }
-        uint64_t pin = 0;
+        M pin = zero<M>();
         uint32_t step_miss = 0;
         for (uint32_t j = 0; j < nacc; ++j, ++pos, ++A) {
             const uint32_t x = __ldg(tr.acc + A);
-            const uint64_t bit = 1ull << x;
+            const M bit = bit_of<M>(x);
             // trace-determined key of x (applied before the victim search; x is never a candidate)
             if (POL == POL_LRU) key(x) = (pos << SH) | x;
             if (POL == POL_LFU) key(x) += 1u << SH;
@@ -89,43 +132,41 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
                 const uint32_t np = __ldg(P.next_pos + A);
                 key(x) = ((np == MCB_NEXT_INF ? 0u : KMAX - np) << SH) | x;
             }
-            const bool hit = (res & bit) != 0ull;
+            const bool hit = test(res, x);
             uint32_t code = MCB_OUT_HIT;
             if (!hit) {
-                uint64_t vbit = 0;
+                M vbit = zero<M>();
                 code = MCB_OUT_MISS;
-                if ((uint32_t)__popcll(res) >= C) {
-                    uint64_t cand = res & ~pin & valid;
-                    if (!cand) {
+                if ((uint32_t)popc(res) >= C) {
+                    M cand = res & ~pin & valid;
+                    if (!any(cand)) {
                         stuck = true;
                     } else {
                         uint32_t best = ~0u;
                         do {
-                            const int s = __ffsll((long long)cand) - 1;
-                            cand &= cand - 1ull;
-                            best = min(best, key(s));
-                        } while (cand);
-                        const uint32_t v = best & (uint32_t)(EMAX - 1);
-                        vbit = 1ull << v;
+                            best = min(best, key(pop_first(cand)));
+                        } while (any(cand));
+                        const uint32_t v = best & ((1u << SH) - 1u);
+                        vbit = bit_of<M>(v);
                         code = v;
                         ++nev;
                     }
                 }
                 res = (res & ~vbit) | bit;
-                refc += (bit & ring_or) ? 1u : 0u;   // refetch of an earlier victim within the window
+                refc += test(ring_or, x) ? 1u : 0u;   // refetch of an earlier victim within the window
                 ring_or = (ring_or & ~bit) | vbit;
 #pragma unroll
-                for (int s = 0; s <= WMAX; ++s) ring[s] &= ~bit;
-                ring[0] |= vbit;
+                for (int s = 0; s <= WMAX; ++s) ring[s] = ring[s] & ~bit;
+                ring[0] = ring[0] | vbit;
                 if (POL == POL_FIFO) key(x) = (pos << SH) | x;   // arrival (policies.py:159-161)
                 ++step_miss;
-                comp += (seen & bit) ? 0u : 1u;
+                comp += test(seen, x) ? 0u : 1u;
                 if (decode) ++dm; else ++pm;
             } else {
                 if (decode) ++dh; else ++ph;
             }
-            seen |= bit;
-            if (decode) pin |= bit;
+            seen = seen | bit;
+            if (decode) pin = pin | bit;
             if (track) {
                 h = poly16(h, code);
                 if (outc) outc[A] = (uint16_t)code;
@@ -140,10 +181,11 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
             dlat = __dadd_rn(dlat, __dadd_rn(lat, POL == POL_ML ? P.ml_cost : 0.0));
 #pragma unroll
             for (int s = WMAX; s >= 1; --s) ring[s] = ring[s - 1];
-            ring[0] = 0;
-            uint64_t o = 0;
+            ring[0] = zero<M>();
+            M o = zero<M>();
 #pragma unroll
-            for (int s = 0; s <= WMAX; ++s) o |= (s <= W) ? ring[s] : 0ull;
+            for (int s = 0; s <= WMAX; ++s)
+                if (s <= W) o = o | ring[s];
             ring_or = o;
         } else {
             plat = __dadd_rn(plat, lat);
@@ -163,9 +205,9 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
     if (P.hashes) P.hashes[inst] = h;
 }
 
-template <bool UNIFORM>
+template <bool UNIFORM, typename M>
 __global__ void __launch_bounds__(BS) k_replay_wide(const __grid_constant__ ReplayParams P) {
-    extern __shared__ uint32_t s_keys[];   // [EMAX][BS]
+    extern __shared__ uint32_t s_keys[];   // [E][BS]
     const int pol_i = P.pol_map[blockIdx.y];
     const int64_t t = (int64_t)blockIdx.x * BS + threadIdx.x;
     if (t >= (P.chain_hi - P.chain_lo) * P.n_cap) return;
@@ -173,39 +215,51 @@ __global__ void __launch_bounds__(BS) k_replay_wide(const __grid_constant__ Repl
     const int64_t chain = P.chain_lo + t / P.n_cap;
     uint32_t *sk = s_keys + threadIdx.x;
     switch (P.pol[pol_i]) {
-        case MCB_LRU: wide_instance<POL_LRU, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0, sk); break;
-        case MCB_LFU: wide_instance<POL_LFU, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0, sk); break;
-        case MCB_BELADY: wide_instance<POL_BELADY, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0, sk); break;
-        case MCB_ML: wide_instance<POL_ML, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0, sk); break;
-        case MCB_FIFO: wide_instance<POL_FIFO, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 0, sk); break;
-        default: wide_instance<POL_ML, UNIFORM, SOLO_WMAX>(P, chain, pol_i, cap_i, 1, sk); break;
+        case MCB_LRU: wide_instance<POL_LRU, UNIFORM, SOLO_WMAX, M>(P, chain, pol_i, cap_i, 0, sk); break;
+        case MCB_LFU: wide_instance<POL_LFU, UNIFORM, SOLO_WMAX, M>(P, chain, pol_i, cap_i, 0, sk); break;
+        case MCB_BELADY: wide_instance<POL_BELADY, UNIFORM, SOLO_WMAX, M>(P, chain, pol_i, cap_i, 0, sk); break;
+        case MCB_ML: wide_instance<POL_ML, UNIFORM, SOLO_WMAX, M>(P, chain, pol_i, cap_i, 0, sk); break;
+        case MCB_FIFO: wide_instance<POL_FIFO, UNIFORM, SOLO_WMAX, M>(P, chain, pol_i, cap_i, 0, sk); break;
+        default: wide_instance<POL_ML, UNIFORM, SOLO_WMAX, M>(P, chain, pol_i, cap_i, 1, sk); break;
     }
 }
 
 }  // namespace wide
 
-// true when the launch was taken: 16 < E <= 64, only the policies above,
-// chains short enough for 26-bit positions, window <= SOLO_WMAX
+// true when the launch was taken: 16 < E <= 128, only the policies above,
+// chains short enough for 25-bit positions, window <= SOLO_WMAX
 int launch_replay_wide(const ReplayParams &p, cudaStream_t s) {
     const int E = p.tr.E;
-    if (E <= 16 || E > wide::EMAX || p.window < 0 || p.window > SOLO_WMAX) return 0;
+    if (E <= 16 || E > 128 || p.window < 0 || p.window > SOLO_WMAX) return 0;
     const int64_t chain_bound = p.tr.uniform ? p.tr.T * p.tr.K : p.tr.total_acc;
-    if (chain_bound >= (1ll << 26)) return 0;
+    if (chain_bound >= (1ll << (32 - wide::SH))) return 0;
     for (int i = 0; i < p.n_pol_launch; ++i) {
         const int pol = p.pol[p.pol_map[i]];
         if (pol == MCB_ARC || pol == MCB_LECAR) return 0;
     }
     const int64_t n = (p.chain_hi - p.chain_lo) * p.n_cap;
     const dim3 grid((unsigned)((n + wide::BS - 1) / wide::BS), (unsigned)p.n_pol_launch);
-    const size_t smem = (size_t)wide::EMAX * wide::BS * sizeof(uint32_t);
-    if (p.tr.uniform) wide::k_replay_wide<true><<<grid, wide::BS, smem, s>>>(p);
-    else wide::k_replay_wide<false><<<grid, wide::BS, smem, s>>>(p);
+    const size_t smem = (size_t)E * wide::BS * sizeof(uint32_t);
+    if (E <= 64) {
+        if (p.tr.uniform) wide::k_replay_wide<true, uint64_t><<<grid, wide::BS, smem, s>>>(p);
+        else wide::k_replay_wide<false, uint64_t><<<grid, wide::BS, smem, s>>>(p);
+    } else {
+        if (p.tr.uniform) wide::k_replay_wide<true, wide::M128><<<grid, wide::BS, smem, s>>>(p);
+        else wide::k_replay_wide<false, wide::M128><<<grid, wide::BS, smem, s>>>(p);
+    }
     return 1;
 }
 
 int preload_wide_kernels() {
-    cudaFuncAttributes a;
-    if (cudaFuncGetAttributes(&a, (const void *)wide::k_replay_wide<true>) != cudaSuccess) return -1;
-    if (cudaFuncGetAttributes(&a, (const void *)wide::k_replay_wide<false>) != cudaSuccess) return -1;
+    const void *fns[] = {(const void *)wide::k_replay_wide<true, uint64_t>,
+                         (const void *)wide::k_replay_wide<false, uint64_t>,
+                         (const void *)wide::k_replay_wide<true, wide::M128>,
+                         (const void *)wide::k_replay_wide<false, wide::M128>};
+    for (const void *f : fns) {
+        cudaFuncAttributes a;
+        if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
+        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * wide::BS * 4) != cudaSuccess)
+            return -1;
+    }
     return 0;
 }

@@ -159,11 +159,16 @@ def zipf_ids(n, L, T, K, E, seed):
     return np.take_along_axis(np.broadcast_to(perm[None, :, None, :], (n, L, T, E)), top, axis=-1).astype(np.uint8)
 
 
-def test_c4_shaped_wide_replay():
-    """C4-shaped batch (L=27, E=64, K=6, many traces): the thread-per-instance
-    replay for 16 < E <= 64 (k_replay_wide) against the warp-per-instance
-    kernel on every chain, and sampled chains against the oracle."""
-    n, L, E, K, T, caps = 64, 27, 64, 6, 512, [16, 24]
+@pytest.mark.parametrize("shape", ["c4", "c5"])
+def test_many_trace_wide_replay(shape):
+    """Many-trace batches, C4-shaped (L=27, E=64, K=6) and C5-shaped (L=48,
+    E=128, K=8): the thread-per-instance replay for 16 < E <= 128
+    (k_replay_wide, 64- / 128-bit masks) against the warp-per-instance kernel
+    on every chain, and sampled chains against the oracle."""
+    if shape == "c4":
+        n, L, E, K, T, caps = 64, 27, 64, 6, 512, [16, 24]
+    else:
+        n, L, E, K, T, caps = 24, 48, 128, 8, 384, [16, 40, 96]
     ids = zipf_ids(n, L, T, K, E, seed=4)
     packed = mcb.packed_from_decode_ids(ids, E)
     nets = oracle.nets_from_spec({"kind": "per_layer_seed"}, L, E)
