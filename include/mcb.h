@@ -213,6 +213,10 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
  * replay of 16 < num_experts <= 64 (default 16384); below it one warp
  * replays one instance. */
 #define MCB_TUNE_WIDE_MIN 9
+/* MCB_TUNE_SEG_TSPEC: speculation of the segmented replay for num_experts
+ * > 16 -- 0 automatic (one thread per (instance, segment) for chains of
+ * >= 65,536 events, else one warp), 1 thread, -1 warp. */
+#define MCB_TUNE_SEG_TSPEC 10
 int mcb_set_tuning(mcb_ctx *ctx, int32_t knob, int64_t value);
 /* LeCaR parameters used by the MCB_LECAR cells of later mcb_replay calls on
  * this context (LeCaRPolicy.__init__, policies.py:333-349; defaults 0.45,

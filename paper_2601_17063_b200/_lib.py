@@ -35,6 +35,7 @@ MCB_TUNE_K3_CTAS = 6
 MCB_TUNE_ML_CHUNKS = 7
 MCB_TUNE_OVERLAP = 8
 MCB_TUNE_WIDE_MIN = 9
+MCB_TUNE_SEG_TSPEC = 10
 R_PH, R_PM, R_DH, R_DM, R_COMP, R_EVICT, R_REFETCH, R_STATUS = range(8)
 R_N = 8
 OUT_HIT, OUT_MISS = 0xFFFF, 0xFFFE

@@ -102,6 +102,7 @@ struct mcb_ctx {
     int64_t seg_ev = 0;               // segmented replay: 0 auto, <0 off, >0 events per segment (MCB_SEG_EV)
     int64_t seg_nw = 0;               // warm-up events before each segment: 0 auto (MCB_SEG_NW)
     int64_t seg_passes = 0;           // speculation passes (MCB_SEG_PASSES): 0 auto, 1 or 2
+    int seg_tspec = 0;                // E > 16 speculation: 0 auto, 1 thread, -1 warp (MCB_SEG_TSPEC)
     int64_t group_lanes = 0;          // lanes per instance of the E > 16 replay: 0 auto, 8 / 16 / 32
     bool serial = false;              // one stream for every stage (per-stage attribution timing)
     DevBuf seg_snap, seg_summ, seg_out, seg_codes, nu_scratch;
@@ -203,6 +204,10 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
         c->serial = value != 0;
         return MCB_OK;
     }
+    if (knob == MCB_TUNE_SEG_TSPEC) {
+        c->seg_tspec = (int)value;
+        return MCB_OK;
+    }
     if (knob == MCB_TUNE_WIDE_MIN) {
         c->wide_min_instances = value;
         return MCB_OK;
@@ -267,6 +272,7 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     if (const char *env = getenv("MCB_SEG_EV")) c->seg_ev = atoll(env);
     if (const char *env = getenv("MCB_SEG_NW")) c->seg_nw = atoll(env);
     if (const char *env = getenv("MCB_SEG_PASSES")) c->seg_passes = atoll(env);
+    if (const char *env = getenv("MCB_SEG_TSPEC")) c->seg_tspec = atoi(env);
     if (const char *env = getenv("MCB_GROUP_LANES")) c->group_lanes = atoll(env);
     if (const char *env = getenv("MCB_K3_CTAS")) c->k3_ctas = atoi(env);
     if (const char *env = getenv("MCB_ML_CHUNKS")) c->ml_chunks = atoll(env);
@@ -569,14 +575,20 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         probe.seg.n_seg = 2;
         const bool solo_ok = n_launch >= c->solo_min_instances;
         const bool paired = split && c->overlap == 0;   // ML and non-ML replays side by side after K3
+        // E > 16: speculation by one thread per (instance, segment) for long
+        // chains (segments sized like the E <= 16 replay's), else one warp
+        const bool tspec = d.E > 16 && d.T * d.K < (1ll << 25) &&
+                           (c->seg_tspec > 0 || (c->seg_tspec == 0 && d.T >= 65536));
         const int se = (c->seg_ev >= 0 && solo_ok && d.uniform)
-                           ? seg_events_per_segment(d.T, n_launch, c->seg_ev, d.E, paired) : 0;
+                           ? seg_events_per_segment(d.T, n_launch, c->seg_ev, tspec ? 16 : d.E, paired) : 0;
         if (se > 0 && seg_eligible(probe)) {
             P.seg.SE = se;
             P.seg.n_seg = (int)((d.T + se - 1) / se);
             P.seg.NW = seg_warmup_events(se, c->seg_nw, d.E);
-            // one pass for the thread-per-instance replay (measured best on C2); two for
-            // the warp version, whose states (E > 16) coalesce more slowly
+            P.seg.thread_spec = tspec ? 1 : 0;
+            // one pass for E <= 16 (measured best on C2); two for E > 16, whose states
+            // coalesce more slowly (C3 with thread speculation: 1 / 2 passes = 333 / 141
+            // ms per step, the second pass removing almost all fix-up walking)
             P.seg.passes = c->seg_passes > 0 ? (int)c->seg_passes : (d.E <= 16 ? 1 : 2);
             P.seg.n_snap = (int)((d.T + MCB_SNAP_EV - 1) / MCB_SNAP_EV);
             P.seg.Tpad = (d.T + 15) / 16 * 16;

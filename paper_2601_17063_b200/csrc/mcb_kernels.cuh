@@ -65,6 +65,7 @@ struct ReplayParams {
         int passes;                     // speculation passes (1 or 2; LRU always 1)
         int n_snap;                     // snapshots per chain (every MCB_SNAP_EV events)
         int snap_e;                     // experts per snapshot record (16, or E rounded up to 32)
+        int thread_spec;                // E > 16: speculation by one thread per (instance, segment)
         int64_t Tpad;                   // row stride of codes (events, multiple of 16)
         int2 *snap;                     // [chain][n_snap][16] (last position before, count before)
         int2 *summ;                     // scratch [chain][n_snap][16]

@@ -1,0 +1,71 @@
+// Expert masks for up to 128 experts held by one thread: uint64_t for
+// num_experts <= 64, two words (M128) above.  Shared by the thread-per-
+// instance replay (mcb_wide.cu) and the thread speculation of the wide
+// segmented replay (mcb_segment_warp.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mm {
+
+struct M128 {
+    uint64_t lo, hi;
+};
+__device__ __forceinline__ M128 operator&(M128 a, M128 b) { return {a.lo & b.lo, a.hi & b.hi}; }
+__device__ __forceinline__ M128 operator|(M128 a, M128 b) { return {a.lo | b.lo, a.hi | b.hi}; }
+__device__ __forceinline__ M128 operator~(M128 a) { return {~a.lo, ~a.hi}; }
+__device__ __forceinline__ bool any(M128 a) { return (a.lo | a.hi) != 0ull; }
+__device__ __forceinline__ bool any(uint64_t a) { return a != 0ull; }
+__device__ __forceinline__ int popc(M128 a) { return __popcll(a.lo) + __popcll(a.hi); }
+__device__ __forceinline__ int popc(uint64_t a) { return __popcll(a); }
+template <typename M> __device__ __forceinline__ M zero();
+template <> __device__ __forceinline__ uint64_t zero<uint64_t>() { return 0ull; }
+template <> __device__ __forceinline__ M128 zero<M128>() { return {0ull, 0ull}; }
+template <typename M> __device__ __forceinline__ M bit_of(uint32_t x);
+template <> __device__ __forceinline__ uint64_t bit_of<uint64_t>(uint32_t x) { return 1ull << x; }
+template <> __device__ __forceinline__ M128 bit_of<M128>(uint32_t x) {
+    return x < 64 ? M128{1ull << x, 0ull} : M128{0ull, 1ull << (x - 64)};
+}
+template <typename M> __device__ __forceinline__ M first_n(int E);   // experts 0 .. E-1
+template <> __device__ __forceinline__ uint64_t first_n<uint64_t>(int E) { return E >= 64 ? ~0ull : ((1ull << E) - 1ull); }
+template <> __device__ __forceinline__ M128 first_n<M128>(int E) {
+    return E >= 128 ? M128{~0ull, ~0ull}
+                    : (E >= 64 ? M128{~0ull, E == 64 ? 0ull : ((1ull << (E - 64)) - 1ull)}
+                               : M128{(1ull << E) - 1ull, 0ull});
+}
+__device__ __forceinline__ bool test(uint64_t m, uint32_t x) { return (m >> x) & 1ull; }
+__device__ __forceinline__ bool test(M128 m, uint32_t x) { return x < 64 ? ((m.lo >> x) & 1ull) : ((m.hi >> (x - 64)) & 1ull); }
+// lowest set bit of a non-empty mask, removed
+__device__ __forceinline__ int pop_first(uint64_t &m) {
+    const int s = __ffsll((long long)m) - 1;
+    m &= m - 1ull;
+    return s;
+}
+__device__ __forceinline__ int pop_first(M128 &m) {
+    if (m.lo) {
+        const int s = __ffsll((long long)m.lo) - 1;
+        m.lo &= m.lo - 1ull;
+        return s;
+    }
+    const int s = __ffsll((long long)m.hi) - 1;
+    m.hi &= m.hi - 1ull;
+    return 64 + s;
+}
+
+// 4 x 32-bit words (bit e % 32 of word e / 32) <-> mask
+__device__ __forceinline__ void to_words(uint64_t m, uint32_t *w) {
+    w[0] = (uint32_t)m; w[1] = (uint32_t)(m >> 32); w[2] = 0u; w[3] = 0u;
+}
+__device__ __forceinline__ void to_words(M128 m, uint32_t *w) {
+    w[0] = (uint32_t)m.lo; w[1] = (uint32_t)(m.lo >> 32); w[2] = (uint32_t)m.hi; w[3] = (uint32_t)(m.hi >> 32);
+}
+template <typename M> __device__ __forceinline__ M from_words(const uint32_t *w);
+template <> __device__ __forceinline__ uint64_t from_words<uint64_t>(const uint32_t *w) {
+    return (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+}
+template <> __device__ __forceinline__ M128 from_words<M128>(const uint32_t *w) {
+    return {(uint64_t)w[0] | ((uint64_t)w[1] << 32), (uint64_t)w[2] | ((uint64_t)w[3] << 32)};
+}
+
+}  // namespace mm

@@ -18,6 +18,7 @@
 #include <stdint.h>
 
 #include "mcb_kernels.cuh"
+#include "mcb_mask.cuh"
 #include "mcb_solo.cuh"
 
 #define WKEY_SENT 0xFFFFFFFFu
@@ -402,6 +403,218 @@ __global__ void __launch_bounds__(128) k_wseg_spec(const __grid_constant__ Repla
     }
 }
 
+// ------------------------------------------------ thread speculation --
+// The same speculation with one THREAD per (instance, segment), for long
+// chains (many segments, e.g. C3's 1M-token trace): the state is a 64- or
+// 128-bit mask (mcb_mask.cuh), the packed keys (key << 7 | id) sit in shared
+// memory column-major per thread, and the victim is a minimum over the
+// candidate bits.  It writes the warp version's WSegOut records, so the warp
+// finish walk (which replays any segment whose recorded start state is not
+// the true one) is shared.
+namespace tspec {
+
+constexpr int BS = 128;
+constexpr int SH = 7;
+constexpr uint32_t KMAX = (1u << (32 - SH)) - 1u;
+
+template <int POL, typename M>
+__device__ __forceinline__ void tseg_spec(const ReplayParams &P, int64_t chain, int seg, int pol_i, int cap_i,
+                                          int ml_variant, uint32_t *sk, uint16_t *hist, int pass) {
+    using namespace mm;
+    const DevTrace &tr = P.tr;
+    const int E = tr.E, K = tr.K, W = P.window;
+    const uint32_t C = (uint32_t)P.cap[cap_i];
+    const int64_t inst = (chain * P.n_pol + pol_i) * P.n_cap + cap_i;
+    const int64_t ev0 = (int64_t)seg * P.seg.SE;
+    const int64_t ev1 = min(ev0 + P.seg.SE, tr.T);
+    const int64_t nw = POL == POL_LRU ? (P.seg.NW < MCB_SNAP_EV ? P.seg.NW : MCB_SNAP_EV) : P.seg.NW;
+    const int64_t ws = pass == 0 ? (ev0 > nw ? ev0 - nw : 0) : ev0;
+    const int64_t a0 = tr.acc_begin(chain);
+    const int64_t e0 = tr.ev_begin(chain);
+    const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
+    auto key = [&](int e) -> uint32_t & { return sk[e * BS]; };
+
+    // exact keys and seen set at ws (a snapshot point)
+    const int2 *sn = P.seg.snap + (chain * P.seg.n_snap + ws / MCB_SNAP_EV) * P.seg.snap_e;
+    M seen = zero<M>();
+    int n_seen = 0;
+    for (int e = 0; e < E; ++e) {
+        const int2 v = __ldg(sn + e);
+        uint32_t k = 0u;
+        if (POL == POL_LRU) k = v.x >= 0 ? (uint32_t)v.x : 0u;
+        if (POL == POL_LFU) k = (uint32_t)v.y;
+        if (POL == POL_BELADY) {
+            const uint32_t np = v.x >= 0 ? __ldg(P.next_pos + a0 + v.x) : MCB_NEXT_INF;
+            k = np == MCB_NEXT_INF ? 0u : KMAX - np;
+        }
+        if (POL == POL_ML) {
+            const uint32_t r = ws > 0 ? (uint32_t)__ldcg(rank + (e0 + ws - 1) * E + e) : 0u;
+            k = 256u - r;
+        }
+        key(e) = (k << SH) | (uint32_t)e;
+        if (v.x >= 0) {
+            seen = seen | bit_of<M>((uint32_t)e);
+            ++n_seen;
+        }
+    }
+    M res = zero<M>(), ring_or = zero<M>();
+    M ring[SOLO_WMAX + 1];
+#pragma unroll
+    for (int i = 0; i <= SOLO_WMAX; ++i) ring[i] = zero<M>();
+    if (pass == 1 && seg > 0) {   // pass 0's end state of the previous segment
+        const WSegOut &q = ((const WSegOut *)P.seg.out[0])[inst * P.seg.n_seg + seg - 1];
+        res = from_words<M>(q.res_end);
+#pragma unroll
+        for (int i = 0; i <= SOLO_WMAX; ++i) {
+            ring[i] = from_words<M>(q.ring_end[i]);
+            if (i <= W) ring_or = ring_or | ring[i];
+        }
+    } else {
+        // guess: the min(C, #seen) seen experts the policy would evict last
+        // (largest packed keys), by a bitwise search for the threshold key
+        const int n_res = min((int)C, n_seen);
+        if (n_res > 0) {
+            uint32_t tau = 0u;
+            for (int b = 31; b >= 0; --b) {
+                const uint32_t cand = tau | (1u << b);
+                int cnt = 0;
+                for (int e = 0; e < E; ++e) cnt += (test(seen, (uint32_t)e) && key(e) >= cand) ? 1 : 0;
+                if (cnt >= n_res) tau = cand;
+            }
+            for (int e = 0; e < E; ++e)
+                if (test(seen, (uint32_t)e) && key(e) >= tau) res = res | bit_of<M>((uint32_t)e);
+        }
+    }
+    M valid = first_n<M>(E);
+    uint32_t misses = 0, nev = 0, refc = 0, comp = 0;
+    int32_t stuck_ev = -1;
+    bool stuck = false;
+    uint64_t h = 0;
+    const bool track = P.hashes != nullptr;
+    for (int b = 0; b <= K; ++b) hist[b * BS] = 0;
+    WSegOut &o = ((WSegOut *)P.seg.out[pass])[inst * P.seg.n_seg + seg];
+    uint32_t *codes = (uint32_t *)(P.seg.codes + inst * P.seg.Tpad);
+    uint32_t word = 0;
+
+    for (int64_t ev = ws; ev < ev1; ++ev) {
+        if (ev == ev0) {
+            to_words(res, o.res_start);
+#pragma unroll
+            for (int i = 0; i <= SOLO_WMAX; ++i) to_words(ring[i], o.ring_start[i]);
+            misses = nev = refc = comp = 0u;
+            stuck = false;
+        }
+        if (POL == POL_ML) {   // this event's rank row (mlpolicy.py:59-62)
+            const uint8_t *row = rank + (e0 + ev) * E;
+            valid = zero<M>();
+            for (int e = 0; e < E; ++e) {
+                const uint32_t r = __ldcg(row + e);
+                key(e) = ((256u - r) << SH) | (uint32_t)e;
+                if (r != 0u) valid = valid | bit_of<M>((uint32_t)e);
+            }
+        }
+        M pin = zero<M>();
+        uint32_t sm = 0;
+        for (int j = 0; j < K; ++j) {
+            const int64_t A = a0 + ev * K + j;
+            const uint32_t x = __ldg(tr.acc + A);
+            const uint32_t pos = (uint32_t)(ev * K + j);
+            const M bit = bit_of<M>(x);
+            if (POL == POL_LRU) key(x) = (pos << SH) | x;
+            if (POL == POL_LFU) key(x) += 1u << SH;
+            if (POL == POL_BELADY) {
+                const uint32_t np = __ldg(P.next_pos + A);
+                key(x) = ((np == MCB_NEXT_INF ? 0u : KMAX - np) << SH) | x;
+            }
+            uint32_t code = MCB_OUT_HIT;
+            if (!test(res, x)) {
+                M vbit = zero<M>();
+                code = MCB_OUT_MISS;
+                if ((uint32_t)popc(res) >= C) {
+                    M cand = res & ~pin & valid;
+                    if (!any(cand)) {
+                        stuck = true;
+                    } else {
+                        uint32_t best = ~0u;
+                        do {
+                            best = min(best, key(pop_first(cand)));
+                        } while (any(cand));
+                        const uint32_t v = best & ((1u << SH) - 1u);
+                        vbit = bit_of<M>(v);
+                        code = v;
+                        ++nev;
+                    }
+                }
+                res = (res & ~vbit) | bit;
+                ++misses;
+                ++sm;
+                refc += test(ring_or, x) ? 1u : 0u;
+                ring_or = (ring_or & ~bit) | vbit;
+#pragma unroll
+                for (int i = 0; i <= SOLO_WMAX; ++i) ring[i] = ring[i] & ~bit;
+                ring[0] = ring[0] | vbit;
+                comp += test(seen, x) ? 0u : 1u;
+            }
+            seen = seen | bit;
+            pin = pin | bit;
+            if (track && ev >= ev0) h = poly16(h, code);
+        }
+        if (ev >= ev0) {
+            if (stuck && stuck_ev < 0) stuck_ev = (int32_t)ev;
+            hist[sm * BS] += 1;
+            word |= sm << (8 * (uint32_t)(ev & 3));
+            if ((ev & 3) == 3) {
+                codes[ev >> 2] = word;
+                word = 0;
+            }
+        }
+#pragma unroll
+        for (int i = SOLO_WMAX; i >= 1; --i) ring[i] = ring[i - 1];
+        ring[0] = zero<M>();
+        M orr = zero<M>();
+#pragma unroll
+        for (int i = 0; i <= SOLO_WMAX; ++i)
+            if (i <= W) orr = orr | ring[i];
+        ring_or = orr;
+    }
+    if (ev1 & 3) codes[ev1 >> 2] = word;   // a segment ends mid-word only at the chain end
+    to_words(res, o.res_end);
+#pragma unroll
+    for (int i = 0; i <= SOLO_WMAX; ++i) to_words(ring[i], o.ring_end[i]);
+    for (int b = 0; b < MCB_SEG_BINS; ++b) o.hist[b] = b <= K ? hist[b * BS] : (uint16_t)0;
+    o.misses = misses;
+    o.nev = nev;
+    o.refc = refc;
+    o.comp = comp;
+    o.stuck_ev = stuck_ev;
+    o.hash = h;
+}
+
+template <typename M>
+__global__ void __launch_bounds__(BS) k_tseg_spec(const __grid_constant__ ReplayParams P, int pass) {
+    extern __shared__ uint32_t s_tsk[];   // keys [E][BS], then uint16 histograms [MCB_SEG_BINS][BS]
+    const int pol_i = P.pol_map[blockIdx.y];
+    if (pass == 1 && P.pol[pol_i] == MCB_LRU) return;   // LRU's guess is exact
+    const int64_t t = (int64_t)blockIdx.x * BS + threadIdx.x;
+    const int n_seg = P.seg.n_seg;
+    if (t >= (P.chain_hi - P.chain_lo) * n_seg * P.n_cap) return;
+    const int cap_i = (int)(t % P.n_cap);
+    const int64_t r = t / P.n_cap;
+    const int seg = (int)(r % n_seg);
+    const int64_t chain = P.chain_lo + r / n_seg;
+    uint32_t *sk = s_tsk + threadIdx.x;
+    uint16_t *hist = (uint16_t *)(s_tsk + P.tr.E * BS) + threadIdx.x;
+    switch (P.pol[pol_i]) {
+        case MCB_LRU: tseg_spec<POL_LRU, M>(P, chain, seg, pol_i, cap_i, 0, sk, hist, pass); break;
+        case MCB_LFU: tseg_spec<POL_LFU, M>(P, chain, seg, pol_i, cap_i, 0, sk, hist, pass); break;
+        case MCB_BELADY: tseg_spec<POL_BELADY, M>(P, chain, seg, pol_i, cap_i, 0, sk, hist, pass); break;
+        case MCB_ML: tseg_spec<POL_ML, M>(P, chain, seg, pol_i, cap_i, 0, sk, hist, pass); break;
+        default: tseg_spec<POL_ML, M>(P, chain, seg, pol_i, cap_i, 1, sk, hist, pass); break;
+    }
+}
+
+}  // namespace tspec
+
 // ----------------------------------------------------------------- finish --
 
 template <int EPL, int POL>
@@ -559,7 +772,16 @@ __global__ void __launch_bounds__(32) k_wseg_finish(const __grid_constant__ Repl
 template <int EPL>
 static int launch_wseg_t(const ReplayParams &p, cudaStream_t s, int phase) {
     int n = 0;
-    if (phase != SEG_FINISH) {
+    if (phase != SEG_FINISH && p.seg.thread_spec) {
+        const int64_t n_spec = (p.chain_hi - p.chain_lo) * p.seg.n_seg * p.n_cap;   // threads
+        const dim3 g((unsigned)((n_spec + tspec::BS - 1) / tspec::BS), (unsigned)p.n_pol_launch);
+        const size_t smem = (size_t)p.tr.E * tspec::BS * 4 + (size_t)MCB_SEG_BINS * tspec::BS * 2;
+        for (int pass = 0; pass < p.seg.passes; ++pass) {
+            if (p.tr.E <= 64) tspec::k_tseg_spec<uint64_t><<<g, tspec::BS, smem, s>>>(p, pass);
+            else tspec::k_tseg_spec<mm::M128><<<g, tspec::BS, smem, s>>>(p, pass);
+            ++n;
+        }
+    } else if (phase != SEG_FINISH) {
         const int64_t n_spec = (p.chain_hi - p.chain_lo) * p.seg.n_seg * p.n_cap;   // warps
         const dim3 g((unsigned)((n_spec + 3) / 4), (unsigned)p.n_pol_launch);
         k_wseg_spec<EPL><<<g, 128, 0, s>>>(p, 0);
@@ -596,8 +818,13 @@ int preload_segment_warp_kernels() {
     cudaFuncAttributes a;
     const void *fns[] = {(const void *)k_wseg_summary, (const void *)k_wseg_spec<1>, (const void *)k_wseg_spec<2>,
                          (const void *)k_wseg_spec<4>, (const void *)k_wseg_finish<1>,
-                         (const void *)k_wseg_finish<2>, (const void *)k_wseg_finish<4>};
+                         (const void *)k_wseg_finish<2>, (const void *)k_wseg_finish<4>,
+                         (const void *)tspec::k_tseg_spec<uint64_t>, (const void *)tspec::k_tseg_spec<mm::M128>};
     for (const void *f : fns)
         if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
+    const int max_smem = 128 * tspec::BS * 4 + MCB_SEG_BINS * tspec::BS * 2;
+    if (cudaFuncSetAttribute((const void *)tspec::k_tseg_spec<mm::M128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             max_smem) != cudaSuccess)
+        return -1;
     return 0;
 }

@@ -17,58 +17,16 @@
 
 #include "mcb_internal.h"
 #include "mcb_kernels.cuh"
+#include "mcb_mask.cuh"
 #include "mcb_solo.cuh"
 
 namespace wide {
 
+using namespace mm;
+
 constexpr int BS = 128;     // threads per block
 constexpr int SH = 7;       // id bits of a packed key (E <= 128)
 constexpr uint32_t KMAX = (1u << (32 - SH)) - 1u;
-
-// 128-bit expert mask as two words (EMAX = 128); EMAX = 64 uses one uint64_t
-struct M128 {
-    uint64_t lo, hi;
-};
-__device__ __forceinline__ M128 operator&(M128 a, M128 b) { return {a.lo & b.lo, a.hi & b.hi}; }
-__device__ __forceinline__ M128 operator|(M128 a, M128 b) { return {a.lo | b.lo, a.hi | b.hi}; }
-__device__ __forceinline__ M128 operator~(M128 a) { return {~a.lo, ~a.hi}; }
-__device__ __forceinline__ bool any(M128 a) { return (a.lo | a.hi) != 0ull; }
-__device__ __forceinline__ bool any(uint64_t a) { return a != 0ull; }
-__device__ __forceinline__ int popc(M128 a) { return __popcll(a.lo) + __popcll(a.hi); }
-__device__ __forceinline__ int popc(uint64_t a) { return __popcll(a); }
-template <typename M> __device__ __forceinline__ M zero();
-template <> __device__ __forceinline__ uint64_t zero<uint64_t>() { return 0ull; }
-template <> __device__ __forceinline__ M128 zero<M128>() { return {0ull, 0ull}; }
-template <typename M> __device__ __forceinline__ M bit_of(uint32_t x);
-template <> __device__ __forceinline__ uint64_t bit_of<uint64_t>(uint32_t x) { return 1ull << x; }
-template <> __device__ __forceinline__ M128 bit_of<M128>(uint32_t x) {
-    return x < 64 ? M128{1ull << x, 0ull} : M128{0ull, 1ull << (x - 64)};
-}
-template <typename M> __device__ __forceinline__ M first_n(int E);   // experts 0 .. E-1
-template <> __device__ __forceinline__ uint64_t first_n<uint64_t>(int E) { return E >= 64 ? ~0ull : ((1ull << E) - 1ull); }
-template <> __device__ __forceinline__ M128 first_n<M128>(int E) {
-    return E >= 128 ? M128{~0ull, ~0ull}
-                    : (E >= 64 ? M128{~0ull, E == 64 ? 0ull : ((1ull << (E - 64)) - 1ull)}
-                               : M128{(1ull << E) - 1ull, 0ull});
-}
-__device__ __forceinline__ bool test(uint64_t m, uint32_t x) { return (m >> x) & 1ull; }
-__device__ __forceinline__ bool test(M128 m, uint32_t x) { return x < 64 ? ((m.lo >> x) & 1ull) : ((m.hi >> (x - 64)) & 1ull); }
-// lowest set bit of a non-empty mask, removed
-__device__ __forceinline__ int pop_first(uint64_t &m) {
-    const int s = __ffsll((long long)m) - 1;
-    m &= m - 1ull;
-    return s;
-}
-__device__ __forceinline__ int pop_first(M128 &m) {
-    if (m.lo) {
-        const int s = __ffsll((long long)m.lo) - 1;
-        m.lo &= m.lo - 1ull;
-        return s;
-    }
-    const int s = __ffsll((long long)m.hi) - 1;
-    m.hi &= m.hi - 1ull;
-    return 64 + s;
-}
 
 template <int POL, bool UNIFORM, int WMAX, typename M>
 __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t chain, int pol_i, int cap_i,
@@ -244,8 +202,8 @@ int launch_replay_wide(const ReplayParams &p, cudaStream_t s) {
         if (p.tr.uniform) wide::k_replay_wide<true, uint64_t><<<grid, wide::BS, smem, s>>>(p);
         else wide::k_replay_wide<false, uint64_t><<<grid, wide::BS, smem, s>>>(p);
     } else {
-        if (p.tr.uniform) wide::k_replay_wide<true, wide::M128><<<grid, wide::BS, smem, s>>>(p);
-        else wide::k_replay_wide<false, wide::M128><<<grid, wide::BS, smem, s>>>(p);
+        if (p.tr.uniform) wide::k_replay_wide<true, mm::M128><<<grid, wide::BS, smem, s>>>(p);
+        else wide::k_replay_wide<false, mm::M128><<<grid, wide::BS, smem, s>>>(p);
     }
     return 1;
 }
@@ -253,8 +211,8 @@ int launch_replay_wide(const ReplayParams &p, cudaStream_t s) {
 int preload_wide_kernels() {
     const void *fns[] = {(const void *)wide::k_replay_wide<true, uint64_t>,
                          (const void *)wide::k_replay_wide<false, uint64_t>,
-                         (const void *)wide::k_replay_wide<true, wide::M128>,
-                         (const void *)wide::k_replay_wide<false, wide::M128>};
+                         (const void *)wide::k_replay_wide<true, mm::M128>,
+                         (const void *)wide::k_replay_wide<false, mm::M128>};
     for (const void *f : fns) {
         cudaFuncAttributes a;
         if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;

@@ -86,14 +86,20 @@ def test_segmented_matches_oracle(E, K, caps, seg_ev, passes, nw):
 
 
 @pytest.mark.parametrize("E,K,caps", [(32, 4, [4, 10, 31]), (64, 6, [6, 16, 40]), (128, 8, [8, 32, 100]),
-                                      (48, 3, [3, 20])])
+                                      (48, 3, [3, 20]), (100, 5, [5, 64])])
 @pytest.mark.parametrize("seg_ev,nw,passes", [(32, 32, 1), (64, 32, 2), (0, 0, 0)])
-def test_warp_segmented_matches_oracle(E, K, caps, seg_ev, nw, passes):
-    """num_experts > 16: one warp per (instance, segment) (mcb_segment_warp.cu)."""
+@pytest.mark.parametrize("spec", ["warp", "thread"])
+def test_wide_segmented_matches_oracle(E, K, caps, seg_ev, nw, passes, spec):
+    """num_experts > 16 (mcb_segment_warp.cu): speculation by one warp or one
+    thread per (instance, segment), the warp finish walk."""
     rng = np.random.default_rng(E * 10 + K + seg_ev)
     L, T = 2, 640
     ids = random_ids(rng, 2 * L, T, E, K, locality=0.5)
-    run_case(ids, L, E, caps, 5, mcb.CostModel(), seg_ev, nw=nw, passes=passes)
+    _lib.set_tuning(_lib.MCB_TUNE_SEG_TSPEC, 1 if spec == "thread" else -1)
+    try:
+        run_case(ids, L, E, caps, 5, mcb.CostModel(), seg_ev, nw=nw, passes=passes)
+    finally:
+        _lib.set_tuning(_lib.MCB_TUNE_SEG_TSPEC, 0)
 
 
 @pytest.mark.parametrize("window", [0, 1, 7])
