@@ -68,4 +68,33 @@ template <> __device__ __forceinline__ M128 from_words<M128>(const uint32_t *w) 
     return {(uint64_t)w[0] | ((uint64_t)w[1] << 32), (uint64_t)w[2] | ((uint64_t)w[3] << 32)};
 }
 
+// ML keys of one event for a thread's column of shared-memory keys
+// (keys[e * 128]): key = (256 - rank) << 7 | e, selectable iff rank != 0
+// (mlpolicy.py:15-26).  Rows of a multiple of 16 experts are 16-byte aligned
+// and read 16 ranks per load, independent loads in flight together.
+template <typename M>
+__device__ __forceinline__ M ml_row_keys(const uint8_t *row, int E, uint32_t *sk) {
+    M valid = zero<M>();
+    if ((E & 15) == 0) {
+#pragma unroll 2
+        for (int s0 = 0; s0 < E; s0 += 16) {
+            const uint4 v = __ldcg((const uint4 *)(row + s0));
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const uint32_t r = (w[q >> 2] >> (8 * (q & 3))) & 0xFFu;
+                sk[(s0 + q) * 128] = ((256u - r) << 7) | (uint32_t)(s0 + q);
+                if (r != 0u) valid = valid | bit_of<M>((uint32_t)(s0 + q));
+            }
+        }
+        return valid;
+    }
+    for (int s = 0; s < E; ++s) {
+        const uint32_t r = __ldcg(row + s);
+        sk[s * 128] = ((256u - r) << 7) | (uint32_t)s;
+        if (r != 0u) valid = valid | bit_of<M>((uint32_t)s);
+    }
+    return valid;
+}
+
 }  // namespace mm

@@ -415,6 +415,7 @@ namespace tspec {
 
 constexpr int BS = 128;
 constexpr int SH = 7;
+static_assert(BS == 128 && SH == 7, "mm::ml_row_keys assumes 128-thread key columns and 7 id bits");
 constexpr uint32_t KMAX = (1u << (32 - SH)) - 1u;
 
 template <int POL, typename M>
@@ -506,12 +507,7 @@ __device__ __forceinline__ void tseg_spec(const ReplayParams &P, int64_t chain, 
         }
         if (POL == POL_ML) {   // this event's rank row (mlpolicy.py:59-62)
             const uint8_t *row = rank + (e0 + ev) * E;
-            valid = zero<M>();
-            for (int e = 0; e < E; ++e) {
-                const uint32_t r = __ldcg(row + e);
-                key(e) = ((256u - r) << SH) | (uint32_t)e;
-                if (r != 0u) valid = valid | bit_of<M>((uint32_t)e);
-            }
+            valid = ml_row_keys<M>(row, E, sk);
         }
         M pin = zero<M>();
         uint32_t sm = 0;

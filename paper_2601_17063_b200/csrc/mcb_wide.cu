@@ -26,6 +26,7 @@ using namespace mm;
 
 constexpr int BS = 128;     // threads per block
 constexpr int SH = 7;       // id bits of a packed key (E <= 128)
+static_assert(BS == 128 && SH == 7, "mm::ml_row_keys assumes 128-thread key columns and 7 id bits");
 constexpr uint32_t KMAX = (1u << (32 - SH)) - 1u;
 
 template <int POL, bool UNIFORM, int WMAX, typename M>
@@ -71,12 +72,7 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
         }
         if (POL == POL_ML) {   // this event's rank row (mlpolicy.py:59-62): argmax score == argmin (256 - rank)
             const uint8_t *row = rank + (e0 + ev) * E;
-            valid = zero<M>();
-            for (int s = 0; s < E; ++s) {
-                const uint32_t r = __ldcg(row + s);
-                key(s) = ((256u - r) << SH) | (uint32_t)s;
-                if (r != 0u) valid = valid | bit_of<M>((uint32_t)s);
-            }
+            valid = ml_row_keys<M>(row, E, sk);
         }
         M pin = zero<M>();
         uint32_t step_miss = 0;
