@@ -265,3 +265,39 @@ def test_scorer_matches_oracle_fp64():
         assert err.max() < 1e-12
         want_rank = 1 + (want[:, None, :] < want[:, :, None]).sum(axis=2)
         assert np.array_equal(rk[c], want_rank)
+
+
+@pytest.mark.parametrize("E,H", [(8, 128), (16, 128), (24, 16), (48, 32), (64, 128), (100, 12), (128, 128)])
+def test_scorer_ranks_match_scores(E, H):
+    """K3's integer ranks against its own float64 scores for every expert
+    count path (pairwise counts E <= 16, integer-key bitonic sort E <= 64,
+    float64 sort above): rank = 1 + #{j : s_j < s_e}; ties share a rank.
+    Nets with duplicated output rows force exact ties."""
+    import ctypes
+
+    import torch
+    rng = np.random.default_rng(E + H)
+    L, T, K = 2, 200, min(4, E)
+    ids = np.stack([np.stack([rng.choice(E, K, replace=False) for _ in range(T)]) for _ in range(L)])
+    packed = mcb.packed_from_decode_ids(ids.astype(np.uint8), E)
+    net = mcb.EvictionNet(E, hidden=H, seed=E)
+    net.params["w3"][E // 2] = net.params["w3"][0]      # expert E/2 always ties expert 0
+    net.params["b3"][E // 2] = net.params["b3"][0]
+    flat = net.flat_params()
+    lib = _lib.load_library()
+    dev_acc = torch.from_numpy(packed.acc).cuda()
+    v = packed.view()
+    v.acc = dev_acc.data_ptr()
+    dparams = torch.from_numpy(flat).cuda()
+    ns = _lib.MCBNets()
+    ns.num_experts, ns.hidden, ns.num_nets, ns.params = E, H, 1, dparams.data_ptr()
+    ranks = torch.zeros(packed.total_events * E + 64, dtype=torch.uint8, device="cuda")
+    scores = torch.zeros(packed.total_events * E, dtype=torch.float64, device="cuda")
+    _lib.check(lib.mcb_score(_lib.context(0), ctypes.byref(v), ctypes.byref(ns), 1, ranks.data_ptr(),
+                             scores.data_ptr(), None))
+    torch.cuda.synchronize()
+    s = scores.cpu().numpy().reshape(-1, E)
+    rk = ranks.cpu().numpy()[:packed.total_events * E].reshape(-1, E)
+    want = 1 + (s[:, None, :] < s[:, :, None]).sum(axis=2)
+    assert np.array_equal(rk, want)
+    assert np.all(rk[:, E // 2] == rk[:, 0])
