@@ -1599,6 +1599,89 @@ __device__ __forceinline__ void rank_event_sorted(const double *srow, int E, uin
     if (__any_sync(FULL_MASK, near) && lane == 0) *flag = 1;
 }
 
+// Faster variant for E <= 64: the sort moves one word per element -- the
+// order-preserving key with its low 7 bits replaced by the expert id -- so
+// there is no separate id to shuffle and no tie-break.  Two different
+// scores that agree in all but the low 7 key bits (or an exact tie) would
+// compare by id; such an event (adjacent equal truncated keys after the
+// sort, rare) is re-ranked exactly by rank_event_sorted.
+template <int P>
+__device__ __forceinline__ void rank_event_packed(const double *srow, int E, uint8_t *rrow, int32_t *flag, int lane) {
+    constexpr int N = 32 * P;
+    const unsigned long long KNEG = ordered_key(-INFINITY) & ~0x7Full, KPOS = ~0ull;
+    unsigned long long v[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const int n = lane * P + p;
+        if (n < E) {
+            const double x = srow[n];
+            v[p] = (x > -INFINITY ? (ordered_key(x) & ~0x7Full) : KNEG) | (unsigned long long)n;
+        } else {
+            v[p] = KPOS;
+        }
+    }
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= P) {
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const unsigned long long ov = __shfl_xor_sync(FULL_MASK, v[p], j / P);
+                    const int n = lane * P + p;
+                    const bool up = (n & k) == 0, lower = (n & j) == 0;
+                    v[p] = (lower == up) ? min(v[p], ov) : max(v[p], ov);
+                }
+            } else {
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    if (p & j) continue;
+                    const int q = p | j, n = lane * P + p;
+                    const bool up = (n & k) == 0;
+                    const unsigned long long lo = min(v[p], v[q]), hi = max(v[p], v[q]);
+                    v[p] = up ? lo : hi;
+                    v[q] = up ? hi : lo;
+                }
+            }
+        }
+    }
+    // adjacent equal truncated keys: the order between them is unknown
+    const unsigned long long prev_last = __shfl_up_sync(FULL_MASK, v[P - 1], 1);
+    bool collide = false;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const int n = lane * P + p;
+        const unsigned long long pk = p > 0 ? v[p - 1] : prev_last;
+        if (n > 0 && v[p] != KPOS && (v[p] >> 7) == (pk >> 7) && (v[p] >> 7) != (KNEG >> 7)) collide = true;
+    }
+    if (__any_sync(FULL_MASK, collide)) {
+        rank_event_sorted<P>(srow, E, rrow, flag, lane);
+        return;
+    }
+    // all selectable keys are distinct: rank = sorted position - #non-selectable + 1
+    int nsel_local = 0;
+    bool near = false;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const int n = lane * P + p;
+        const unsigned long long pk = p > 0 ? v[p - 1] : prev_last;
+        nsel_local += ((v[p] >> 7) == (KNEG >> 7) && v[p] != KPOS) ? 1 : 0;
+        if (n > 0 && v[p] != KPOS && (pk >> 7) != (KNEG >> 7)) {
+            const double a = srow[(int)(v[p] & 0x7Full)], b = srow[(int)(pk & 0x7Full)];
+            if (fabs(a - b) <= 1e-12 * fmax(fabs(a), fabs(b))) near = true;
+        }
+    }
+    const int nsel = __reduce_add_sync(FULL_MASK, nsel_local);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const int n = lane * P + p;
+        if (v[p] == KPOS) continue;
+        const int id = (int)(v[p] & 0x7Full);
+        rrow[id] = (v[p] >> 7) != (KNEG >> 7) ? (uint8_t)(n - nsel + 1) : (uint8_t)0;
+    }
+    if (__any_sync(FULL_MASK, near) && lane == 0) *flag = 1;
+}
+
 // float64 variant of rank_event_sorted (the sort compares (score, id) pairs as
 // doubles): fewer live registers, used for E > 64 where the integer-key
 // version spills.  Ranks of one event's E scores by a warp-wide bitonic sort of (score, id)
@@ -1791,8 +1874,8 @@ __global__ void __launch_bounds__(256, TE ? 4 : 1) k_score_tile(DevTrace tr, con
         // registers) -- O(E log^2 E) instead of O(E^2) per event
         const int warp = tid >> 5;
         for (int i = warp; i < nev; i += (int)(blockDim.x >> 5)) {
-            if (E <= 32) rank_event_sorted<1>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
-            else if (E <= 64) rank_event_sorted<2>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
+            if (E <= 32) rank_event_packed<1>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
+            else if (E <= 64) rank_event_packed<2>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
             else rank_event_sorted_f64<4>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
         }
     }
