@@ -1599,7 +1599,7 @@ __device__ __forceinline__ void rank_event_sorted(const double *srow, int E, uin
     if (__any_sync(FULL_MASK, near) && lane == 0) *flag = 1;
 }
 
-// Faster variant for E <= 64: the sort moves one word per element -- the
+// Faster variant (E <= 128): the sort moves one word per element -- the
 // order-preserving key with its low 7 bits replaced by the expert id -- so
 // there is no separate id to shuffle and no tie-break.  Two different
 // scores that agree in all but the low 7 key bits (or an exact tie) would
@@ -1678,92 +1678,6 @@ __device__ __forceinline__ void rank_event_packed(const double *srow, int E, uin
         if (v[p] == KPOS) continue;
         const int id = (int)(v[p] & 0x7Full);
         rrow[id] = (v[p] >> 7) != (KNEG >> 7) ? (uint8_t)(n - nsel + 1) : (uint8_t)0;
-    }
-    if (__any_sync(FULL_MASK, near) && lane == 0) *flag = 1;
-}
-
-// float64 variant of rank_event_sorted (the sort compares (score, id) pairs as
-// doubles): fewer live registers, used for E > 64 where the integer-key
-// version spills.  Ranks of one event's E scores by a warp-wide bitonic sort of (score, id)
-// (P elements per lane, N = 32 P >= E; padding sorts last as +inf):
-// rank = 1 + #{selectable j : s_j < s_e} = 1 + (first sorted position of
-// s_e's value) - #non-selectable, 0 for NaN / -inf (never evicted,
-// mlpolicy.py:15-26).  A near-tie (two distinct scores within 1e-12
-// relative) is always an adjacent sorted pair, which sets *flag.
-template <int P>
-__device__ __forceinline__ void rank_event_sorted_f64(const double *srow, int E, uint8_t *rrow, int32_t *flag, int lane) {
-    constexpr int N = 32 * P;
-    double v[P];
-    int id[P];
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-        const int n = lane * P + p;
-        id[p] = n;
-        if (n < E) {
-            const double x = srow[n];
-            v[p] = x > -INFINITY ? x : -INFINITY;   // NaN -> -inf: never selectable
-        } else {
-            v[p] = INFINITY;
-        }
-    }
-#pragma unroll
-    for (int k = 2; k <= N; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j >= P) {   // partner in lane ^ (j / P)
-#pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    const double ov = __shfl_xor_sync(FULL_MASK, v[p], j / P);
-                    const int oid = __shfl_xor_sync(FULL_MASK, id[p], j / P);
-                    const int n = lane * P + p;
-                    const bool up = (n & k) == 0, lower = (n & j) == 0;
-                    const bool mine_less = v[p] < ov || (v[p] == ov && id[p] < oid);
-                    if (mine_less != (lower == up)) { v[p] = ov; id[p] = oid; }
-                }
-            } else {        // partner in the same lane: p ^ j
-#pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    if (p & j) continue;
-                    const int q = p | j, n = lane * P + p;
-                    const bool up = (n & k) == 0;
-                    const bool q_less = v[q] < v[p] || (v[q] == v[p] && id[q] < id[p]);
-                    if (q_less == up) {
-                        const double tv = v[p]; v[p] = v[q]; v[q] = tv;
-                        const int ti = id[p]; id[p] = id[q]; id[q] = ti;
-                    }
-                }
-            }
-        }
-    }
-    // first sorted position of each value (inclusive max-scan of run starts)
-    const double prev_last = __shfl_up_sync(FULL_MASK, v[P - 1], 1);
-    int start[P];
-    int nsel_local = 0, loc = -1;
-    bool near = false;
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-        const int n = lane * P + p;
-        const double pv = p > 0 ? v[p - 1] : prev_last;
-        const bool first = n == 0 || v[p] != pv;
-        loc = max(loc, first ? n : -1);
-        start[p] = loc;
-        nsel_local += (v[p] == -INFINITY) ? 1 : 0;
-        if (n > 0 && v[p] != pv && pv > -INFINITY && v[p] < INFINITY &&
-            fabs(v[p] - pv) <= 1e-12 * fmax(fabs(v[p]), fabs(pv)))
-            near = true;
-    }
-    int carry = loc;   // warp inclusive max-scan of the lanes' last run start
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(FULL_MASK, carry, o);
-        if (lane >= o) carry = max(carry, t);
-    }
-    const int before = __shfl_up_sync(FULL_MASK, carry, 1);
-    const int nsel = __reduce_add_sync(FULL_MASK, nsel_local);
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-        const int st = (lane > 0 && start[p] < 0) ? before : max(start[p], lane > 0 ? before : -1);
-        if (id[p] < E) rrow[id[p]] = v[p] > -INFINITY ? (uint8_t)(st - nsel + 1) : (uint8_t)0;
     }
     if (__any_sync(FULL_MASK, near) && lane == 0) *flag = 1;
 }
@@ -1876,7 +1790,7 @@ __global__ void __launch_bounds__(256, TE ? 4 : 1) k_score_tile(DevTrace tr, con
         for (int i = warp; i < nev; i += (int)(blockDim.x >> 5)) {
             if (E <= 32) rank_event_packed<1>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
             else if (E <= 64) rank_event_packed<2>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
-            else rank_event_sorted_f64<4>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
+            else rank_event_packed<4>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
         }
     }
     if (scores)
