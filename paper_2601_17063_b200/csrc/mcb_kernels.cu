@@ -1770,15 +1770,20 @@ __global__ void __launch_bounds__(256, TE ? 4 : 1) k_score_tile(DevTrace tr, con
             uint32_t r = 0;
             bool near = false;
             if (s > -INFINITY) {
+                // rank = 1 + #{selectable j : s_j < s}; the near-tie test only needs the
+                // nearest smaller score (every adjacent pair of the sorted order is
+                // tested by its larger member)
                 r = 1;
+                double below = -INFINITY;
 #pragma unroll 8
                 for (int j = 0; j < E; ++j) {
                     const double sj = bufA[i * ldA + j];
-                    if (sj > -INFINITY) {
-                        if (sj < s) ++r;
-                        if (sj != s && fabs(sj - s) <= 1e-12 * fmax(fabs(s), fabs(sj))) near = true;
+                    if (sj > -INFINITY && sj < s) {
+                        ++r;
+                        below = fmax(below, sj);
                     }
                 }
+                near = below > -INFINITY && fabs(s - below) <= 1e-12 * fmax(fabs(s), fabs(below));
             }
             s_rank[i * E + e] = (uint8_t)r;
             if (near) s_flag[i] = 1;
