@@ -57,6 +57,11 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
     uint16_t *outc = P.outcomes ? P.outcomes + ((int64_t)pol_i * P.n_cap + cap_i) * tr.total_acc : nullptr;
     const bool track = outc != nullptr || P.hashes != nullptr;
 
+    const int64_t a_end = tr.acc_end(chain);
+    IdReader ids;   // 16 ids per vector load, the next vector in flight
+    ids.init(tr.acc, a0, a_end);
+    NextReader nx;
+    if (POL == POL_BELADY) nx.init(P.next_pos, a0, a_end);
     int64_t A = a0;
     uint32_t pos = 0;
     for (int64_t ev = 0; ev < n_ev; ++ev) {
@@ -77,13 +82,13 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
         M pin = zero<M>();
         uint32_t step_miss = 0;
         for (uint32_t j = 0; j < nacc; ++j, ++pos, ++A) {
-            const uint32_t x = __ldg(tr.acc + A);
+            const uint32_t x = ids.get(A);
             const M bit = bit_of<M>(x);
             // trace-determined key of x (applied before the victim search; x is never a candidate)
             if (POL == POL_LRU) key(x) = (pos << SH) | x;
             if (POL == POL_LFU) key(x) += 1u << SH;
             if (POL == POL_BELADY) {
-                const uint32_t np = __ldg(P.next_pos + A);
+                const uint32_t np = nx.get(A);
                 key(x) = ((np == MCB_NEXT_INF ? 0u : KMAX - np) << SH) | x;
             }
             const bool hit = test(res, x);
