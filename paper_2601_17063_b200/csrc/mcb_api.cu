@@ -94,6 +94,8 @@ struct mcb_ctx {
     cudaEvent_t chunk_ev[MCB_MAX_ML_CHUNKS] = {};
     cudaEvent_t join2 = nullptr;
     cudaEvent_t pre = nullptr;         // the side stream's replay preparation is done
+    cudaEvent_t nets_ev = nullptr;     // host path: the nets' upload (on side2) is done
+    bool nets_pending = false;         // the scorer must wait for nets_ev before using the nets
     int64_t ml_chunks = 1;             // K3 / ML replay pipeline depth (MCB_TUNE_ML_CHUNKS)
     int k3_ctas = -1;                  // K3 grid mode (MCB_TUNE_K3_CTAS)
     int overlap = 0;                   // non-ML replay: 0 after K3 (next to the ML replay), 1 during K3
@@ -289,6 +291,7 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
         cudaStreamCreateWithPriority(&c->side2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join2, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->pre, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->nets_ev, cudaEventDisableTiming) != cudaSuccess ||
 
         cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess) {
@@ -316,6 +319,7 @@ extern "C" int mcb_ctx_destroy(mcb_ctx *c) {
     if (c->side2) cudaStreamDestroy(c->side2);
     if (c->join2) cudaEventDestroy(c->join2);
     if (c->pre) cudaEventDestroy(c->pre);
+    if (c->nets_ev) cudaEventDestroy(c->nets_ev);
     for (auto &e : c->chunk_ev)
         if (e) cudaEventDestroy(e);
 
@@ -414,6 +418,7 @@ static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int in
     if (int rc = ensure_score_buffers(c, d, nets)) return rc;
     const size_t per = prepared_net_doubles(E, H);
     (void)per;
+    if (c->nets_pending) CUDA_TRY(cudaStreamWaitEvent(s, c->nets_ev, 0));   // host path: nets copied on side2
     *launched += launch_prepare_nets(nets->params, E, H, nets->num_nets, (double *)c->wt.p, s);
     const int64_t tiles = max_score_tiles(d);
     const int n = launch_score(d, (const double *)c->wt.p, H, nets->num_nets, include_prefill, ranks, scores,
@@ -671,6 +676,7 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         const int v = need_ml[0] ? 0 : 1;
         if (int rc = check_nets(d, nets)) return rc;
         mark(c, 2, s);
+        if (c->nets_pending) CUDA_TRY(cudaStreamWaitEvent(s, c->nets_ev, 0));
         launched += launch_prepare_nets(nets->params, d.E, nets->hidden, nets->num_nets, (double *)c->wt.p, s);
         const int64_t tiles = max_score_tiles(d);
         launched += launch_score_prep(d, v == 0 ? 1 : 0, (int32_t *)c->snaps.p, (int64_t *)c->tile_off.p, tiles, s);
@@ -830,9 +836,15 @@ extern "C" int mcb_replay_host(mcb_ctx *c, const mcb_trace *t, const int32_t *po
     mcb_nets dn;
     const mcb_nets *np = nullptr;
     if (nets && nets->params) {
+        // the nets' copy runs on side2 while the trace-only stages (K2, key and
+        // feature snapshots) start; the scorer waits for it (nets_ev)
         dn = *nets;
         const size_t cnt = net_param_doubles(nets->num_experts, nets->hidden) * (size_t)nets->num_nets;
-        if (int rc = upload(c->h_params, nets->params, cnt, 0, s, &dn.params)) return rc;
+        CUDA_TRY(cudaEventRecord(c->nets_ev, s));                 // after the previous call's use of h_params
+        CUDA_TRY(cudaStreamWaitEvent(c->side2, c->nets_ev, 0));
+        if (int rc = upload(c->h_params, nets->params, cnt, 0, c->side2, &dn.params)) return rc;
+        CUDA_TRY(cudaEventRecord(c->nets_ev, c->side2));
+        c->nets_pending = true;
         np = &dn;
     }
     const int64_t n_cells = (int64_t)t->num_traces * n_pol * n_cap;
@@ -855,9 +867,14 @@ extern "C" int mcb_replay_host(mcb_ctx *c, const mcb_trace *t, const int32_t *po
         if (int rc = c->h_outcomes.ensure((size_t)(n_pol * n_cap * d.total_acc + 1) * sizeof(uint16_t))) return rc;
         dout.outcomes = (uint16_t *)c->h_outcomes.p;
     }
-    if (int rc = replay_locked(c, &dt, pols, n_pol, caps, n_cap, cost, np, &dout, s)) {
+    const int rc_replay = replay_locked(c, &dt, pols, n_pol, caps, n_cap, cost, np, &dout, s);
+    if (c->nets_pending) {   // the stream must not outrun the copy even if no scorer ran
+        cudaStreamWaitEvent(s, c->nets_ev, 0);
+        c->nets_pending = false;
+    }
+    if (rc_replay) {
         cudaStreamSynchronize(s);
-        return rc;
+        return rc_replay;
     }
     CUDA_TRY(cudaMemcpyAsync(out->reports, dout.reports, (size_t)n_cells * MCB_R_N * sizeof(int64_t),
                              cudaMemcpyDeviceToHost, s));
