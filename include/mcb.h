@@ -20,8 +20,9 @@
  * context owns only its device scratch.
  *
  * Supported: num_experts <= 128, top_k <= num_experts, chains of < 2^32
- * accesses, policies LRU / LFU / Belady / ML (the north star's four), FIFO
- * and ARC.  LeCaR (policies.py:305-395) is rejected with
+ * accesses, policies LRU / LFU / Belady / ML (the north star's four) and the
+ * state-dependent FIFO, ARC and LeCaR (whole-chain kernels).  Anything else
+ * (custom per-access policy objects, > 128 experts) is rejected with
  * MCB_ERR_UNSUPPORTED rather than falling back to a CPU path.
  */
 #ifndef MCB_H_
@@ -139,8 +140,13 @@ typedef struct {
  * latency[trace][pol][cap][2] float64 (decode, prefill) are summed over
  * layers in layer order exactly like engine.py:330-343 (float64, no FMA).
  * Optional (NULL to skip): chain_reports[c][pol][cap][MCB_R_N],
- * hashes[c][pol][cap] (FNV-1a 64 over the u16 outcome codes of the chain),
- * outcomes[pol][cap][total_acc] u16 (record_decisions, small traces).
+ * hashes[c][pol][cap] (polynomial hash h = h * 0x100000001B3 + code + 1 mod
+ * 2^64 over the u16 outcome codes of the chain, in access order -- spliceable
+ * across the segmented replay's segments),
+ * outcomes[pol][cap][total_acc] u16 (record_decisions, small traces),
+ * chain_latency[c][pol][cap][2] float64 (the per-layer decode / prefill
+ * latency sums of _replay_layer, engine.py:258-263, before the layer fold --
+ * what a layer-sharded multi-GPU run gathers to fold in layer order).
  */
 typedef struct {
     int64_t *reports;
@@ -148,6 +154,7 @@ typedef struct {
     int64_t *chain_reports;
     uint64_t *hashes;
     uint16_t *outcomes;
+    double *chain_latency;
 } mcb_outputs;
 
 typedef struct mcb_ctx mcb_ctx;
@@ -217,6 +224,13 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
  * > 16 -- 0 automatic (one thread per (instance, segment) for chains of
  * >= 65,536 events, else one warp), 1 thread, -1 warp. */
 #define MCB_TUNE_SEG_TSPEC 10
+/* MCB_TUNE_SCRATCH_BYTES: device scratch budget of one mcb_replay call
+ * (next-use positions, ML rank rows, feature snapshots, per-instance
+ * outputs).  A uniform multi-trace batch whose scratch would exceed it is
+ * replayed in consecutive trace ranges that reuse the same scratch (results
+ * are identical; outcomes are not supported then).  0 (default) = 40% of
+ * the device memory free at the call. */
+#define MCB_TUNE_SCRATCH_BYTES 11
 int mcb_set_tuning(mcb_ctx *ctx, int32_t knob, int64_t value);
 /* LeCaR parameters used by the MCB_LECAR cells of later mcb_replay calls on
  * this context (LeCaRPolicy.__init__, policies.py:333-349; defaults 0.45,
@@ -371,6 +385,15 @@ int mcb_training_data(mcb_ctx *ctx, const mcb_trace *trace, int32_t capacity, in
 int mcb_gen_reference(mcb_ctx *ctx, int32_t num_layers, int32_t num_experts, int32_t top_k, int64_t num_seqs,
                       int64_t prefill_tokens, int64_t decode_steps, int32_t w_hot, double recency_boost,
                       const double *popularity, const uint64_t *pcg_state, uint8_t *experts, void *stream);
+/* Batch form for decode-only single-sequence traces (generate_trace with
+ * num_seqs = 1, prefill_tokens = 0, one rng_seed per trace and a shared
+ * popularity table, e.g. popularity_seed fixed): pcg_states is a DEVICE
+ * array [num_traces][4] (the initial state of default_rng([rng_seed_i, 1])),
+ * experts a device uint8 [trace][layer][token][K] -- the chain-major uniform
+ * layout of mcb_trace, ready to replay. */
+int mcb_gen_reference_batch(mcb_ctx *ctx, int32_t num_layers, int32_t num_experts, int32_t top_k,
+                            int64_t num_traces, int64_t decode_steps, int32_t w_hot, double recency_boost,
+                            const double *popularity, const uint64_t *pcg_states, uint8_t *experts, void *stream);
 
 #ifdef __cplusplus
 }

@@ -778,3 +778,145 @@ int orc_score_chain(const uint8_t *ids, int T, int K, int E, int H, const double
     free(rec); free(fr); free(x); free(h1); free(h2);
     return ORC_OK;
 }
+
+/* ------------------- the reference's synthetic generator ------------------ */
+
+/*
+ * generate_trace / _draw_routed (trace.py:212-287), restated for decode-only
+ * single-sequence traces (the bench workloads): per (token, layer) K draws
+ * without replacement from (1 - b) * pop + b * uniform(hot set of the last
+ * w_hot events of the layer), one numpy Generator.choice per draw.  numpy's
+ * own arithmetic, op by op: PCG64 (128-bit LCG, XSL-RR output) stepped once
+ * per choice, random() = (u64 >> 11) * 2^-53, p.sum() as numpy's pairwise
+ * sum (8 accumulators for 8 <= n <= 128), p /= total, cumsum, cdf /= cdf[-1],
+ * searchsorted(side='right').  The popularity table (trace.py:186-202) and
+ * the stream's initial state (default_rng([seed, 1]).bit_generator.state)
+ * come from numpy in the caller.  The stream is consumed token -> layer ->
+ * slot (trace.py:265-283), so layers are interleaved: this restatement walks
+ * the stream in that order, unlike the GPU kernel which jumps per chain.
+ */
+typedef unsigned __int128 orc_u128;
+
+static uint64_t orc_pcg_out(orc_u128 s) {
+    uint64_t x = (uint64_t)(s >> 64) ^ (uint64_t)s;
+    unsigned r = (unsigned)(s >> 122);
+    return (x >> r) | (x << ((64u - r) & 63u));
+}
+
+static double orc_np_sum(const double *a, int n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int i = 0; i < n; ++i) r += a[i];
+        return r;
+    }
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+        for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i];
+    return res;
+}
+
+/* One trace: out[T][L][K] (the reference's event order). */
+int orc_gen_decode(int L, int E, int K, int64_t T, int w_hot, double boost, const double *pop,
+                   const uint64_t *state /* hi, lo, inc_hi, inc_lo */, uint8_t *out) {
+    if (E > 128 || E < 1 || K < 1 || K > E || w_hot < 1 || w_hot > 64) return ORC_ERR_INVALID;
+    const orc_u128 mult = ((orc_u128)0x2360ED051FC65DA4ull << 64) | (orc_u128)0x4385DF649FCCF645ull;
+    const orc_u128 inc = ((orc_u128)state[2] << 64) | state[3];
+    orc_u128 st = ((orc_u128)state[0] << 64) | state[1];
+    uint8_t *ring = (uint8_t *)calloc((size_t)L * 64 * 128, 1);   /* [layer][w][E] routed flags */
+    int *n_recent = (int *)calloc((size_t)L, sizeof(int));
+    int *head = (int *)calloc((size_t)L, sizeof(int));
+    if (!ring || !n_recent || !head) { free(ring); free(n_recent); free(head); return ORC_ERR_NOMEM; }
+    const double omb = 1.0 - boost;
+    double p[128];
+    for (int64_t t = 0; t < T; ++t) {
+        for (int l = 0; l < L; ++l) {
+            uint8_t hot[128], chosen[128];
+            memset(hot, 0, sizeof hot);
+            memset(chosen, 0, sizeof chosen);
+            for (int i = 0; i < n_recent[l]; ++i)
+                for (int e = 0; e < E; ++e) hot[e] |= ring[((size_t)l * 64 + i) * 128 + e];
+            int nh = 0;
+            for (int e = 0; e < E; ++e) nh += hot[e];
+            const int mix = nh > 0 && boost > 0.0;
+            const double hm = mix ? 1.0 / (double)nh : 0.0;
+            uint8_t *o = out + ((size_t)t * L + l) * K;
+            for (int k = 0; k < K; ++k) {
+                for (int e = 0; e < E; ++e) {
+                    double v = pop[(size_t)l * E + e];
+                    if (mix) v = omb * v + boost * (hot[e] ? hm : 0.0);
+                    if (chosen[e]) v = 0.0;
+                    p[e] = v;
+                }
+                double total = orc_np_sum(p, E);
+                if (!(total > 0.0)) {
+                    for (int e = 0; e < E; ++e) p[e] = chosen[e] ? 0.0 : 1.0;
+                    total = orc_np_sum(p, E);
+                }
+                st = st * mult + inc;
+                const double u = (double)(orc_pcg_out(st) >> 11) * (1.0 / 9007199254740992.0);
+                double c = 0.0;
+                for (int e = 0; e < E; ++e) { c += p[e] / total; p[e] = c; }
+                const double last = p[E - 1];
+                int idx = 0;
+                for (int e = 0; e < E; ++e) idx += (p[e] / last <= u) ? 1 : 0;
+                chosen[idx] = 1;
+                o[k] = (uint8_t)idx;
+            }
+            uint8_t *slot = ring + ((size_t)l * 64 + head[l]) * 128;
+            memcpy(slot, chosen, 128);
+            head[l] = head[l] + 1 == w_hot ? 0 : head[l] + 1;
+            if (n_recent[l] < w_hot) n_recent[l]++;
+        }
+    }
+    free(ring); free(n_recent); free(head);
+    return ORC_OK;
+}
+
+typedef struct {
+    int L, E, K, w_hot;
+    int64_t T, n;
+    double boost;
+    const double *pop;
+    const uint64_t *states;
+    uint8_t *out;
+    int64_t next;
+    pthread_mutex_t mu;
+    int rc;
+} genb_t;
+
+static void *gen_worker(void *arg) {
+    genb_t *g = (genb_t *)arg;
+    for (;;) {
+        pthread_mutex_lock(&g->mu);
+        int64_t i = g->next++;
+        pthread_mutex_unlock(&g->mu);
+        if (i >= g->n) break;
+        int rc = orc_gen_decode(g->L, g->E, g->K, g->T, g->w_hot, g->boost, g->pop, g->states + 4 * i,
+                                g->out + (size_t)i * g->T * g->L * g->K);
+        if (rc) g->rc = rc;
+    }
+    return NULL;
+}
+
+/* n independent traces (one state each, one shared popularity table) on
+ * n_threads host threads: out[trace][T][L][K]. */
+int orc_gen_decode_batch(int L, int E, int K, int64_t T, int w_hot, double boost, const double *pop,
+                         int64_t n, const uint64_t *states, int n_threads, uint8_t *out) {
+    genb_t g;
+    memset(&g, 0, sizeof g);
+    g.L = L; g.E = E; g.K = K; g.w_hot = w_hot; g.T = T; g.n = n; g.boost = boost;
+    g.pop = pop; g.states = states; g.out = out;
+    pthread_mutex_init(&g.mu, NULL);
+    if (n_threads < 1) n_threads = 1;
+    pthread_t *th = (pthread_t *)malloc((size_t)n_threads * sizeof(pthread_t));
+    if (!th) return ORC_ERR_NOMEM;
+    for (int i = 0; i < n_threads; ++i) pthread_create(&th[i], NULL, gen_worker, &g);
+    for (int i = 0; i < n_threads; ++i) pthread_join(th[i], NULL);
+    free(th);
+    pthread_mutex_destroy(&g.mu);
+    return g.rc;
+}

@@ -22,6 +22,7 @@ from .engine import (
     step_latency_s,
     sweep,
 )
+from .distributed import replay_sharded, sweep_sharded
 from .net import EvictionNet, NetError, ShapeMismatchError, load_net, save_net
 from .policies import NoEvictableError, PolicyDecision, PolicyError, lecar_update
 from .refgen import SyntheticWorkloadConfig, expert_popularity, generate_trace

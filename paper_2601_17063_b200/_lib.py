@@ -36,6 +36,7 @@ MCB_TUNE_ML_CHUNKS = 7
 MCB_TUNE_OVERLAP = 8
 MCB_TUNE_WIDE_MIN = 9
 MCB_TUNE_SEG_TSPEC = 10
+MCB_TUNE_SCRATCH_BYTES = 11
 R_PH, R_PM, R_DH, R_DM, R_COMP, R_EVICT, R_REFETCH, R_STATUS = range(8)
 R_N = 8
 OUT_HIT, OUT_MISS = 0xFFFF, 0xFFFE
@@ -45,6 +46,7 @@ EXPORTED_SYMBOLS = (
     "mcb_set_timing", "mcb_last_timings", "mcb_set_tuning", "mcb_read_stats",
     "mcb_pack_trace", "mcb_packed_view", "mcb_packed_positions", "mcb_packed_free",
     "mcb_replay", "mcb_replay_host", "mcb_next_use", "mcb_score", "mcb_router_topk", "mcb_gen_reference",
+    "mcb_gen_reference_batch",
     "mcb_training_data", "mcb_set_lecar", "mcb_lecar_random", "mcb_pack_decode_ids",
     "mcb_eviction_duel", "mcb_train_epoch", "mcb_train_eval",
 )
@@ -113,6 +115,7 @@ class MCBOutputs(ctypes.Structure):
         ("chain_reports", ctypes.c_void_p),
         ("hashes", ctypes.c_void_p),
         ("outcomes", ctypes.c_void_p),
+        ("chain_latency", ctypes.c_void_p),
     ]
 
 
@@ -157,6 +160,7 @@ def load_library():
             "mcb_eviction_duel": ([P, P, P, P, P, P, P], ctypes.c_int),
             "mcb_train_epoch": ([P, P, P, P, P, P, i64, i64, P, P, P], ctypes.c_int),
             "mcb_train_eval": ([P, P, P, i64, i64, P, P], ctypes.c_int),
+            "mcb_gen_reference_batch": ([P, i32, i32, i32, i64, i64, i32, ctypes.c_double, P, P, P, P], i32),
             "mcb_gen_reference": ([P, i32, i32, i32, i64, i64, i64, i32, ctypes.c_double, P, P, P, P],
                                   ctypes.c_int),
         }

@@ -83,7 +83,7 @@ struct mcb_ctx {
     DevBuf next_pos, ranks[2], inst_out, inst_lat, wt, snaps, tile_off, stats, pol_caps;
     // host path staging
     DevBuf h_acc, h_acc_off, h_ev_off, h_rt_off, h_ev_info, h_routed, h_params, h_reports, h_latency,
-        h_chain_reports, h_hashes, h_outcomes;
+        h_chain_reports, h_hashes, h_outcomes, h_chain_latency;
     cudaStream_t stream = nullptr;
     int64_t last_kernels = 0;
     int64_t last_uncertain = 0;
@@ -106,6 +106,8 @@ struct mcb_ctx {
     int64_t seg_passes = 0;           // speculation passes (MCB_SEG_PASSES): 0 auto, 1 or 2
     int seg_tspec = 0;                // E > 16 speculation: 0 auto, 1 thread, -1 warp (MCB_SEG_TSPEC)
     int64_t group_lanes = 0;          // lanes per instance of the E > 16 replay: 0 auto, 8 / 16 / 32
+    int64_t scratch_bytes = 0;        // per-call scratch budget (MCB_TUNE_SCRATCH_BYTES): 0 = 40% of free
+    int64_t last_chunks = 1;          // trace ranges of the last mcb_replay
     bool serial = false;              // one stream for every stage (per-stage attribution timing)
     DevBuf seg_snap, seg_summ, seg_out, seg_codes, nu_scratch;
     // LeCaR (mcb_set_lecar): parameters, the shared random() stream (cached
@@ -218,6 +220,11 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
         c->overlap = (int)value;
         return MCB_OK;
     }
+    if (knob == MCB_TUNE_SCRATCH_BYTES) {
+        if (value < 0) return mcb_set_error(MCB_ERR_INVALID, "scratch budget must be >= 0");
+        c->scratch_bytes = value;
+        return MCB_OK;
+    }
     if (knob == MCB_TUNE_ML_CHUNKS) {
         c->ml_chunks = value;
         return MCB_OK;
@@ -279,6 +286,7 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     if (const char *env = getenv("MCB_K3_CTAS")) c->k3_ctas = atoi(env);
     if (const char *env = getenv("MCB_ML_CHUNKS")) c->ml_chunks = atoll(env);
     if (const char *env = getenv("MCB_OVERLAP")) c->overlap = atoi(env);
+    if (const char *env = getenv("MCB_SCRATCH_BYTES")) c->scratch_bytes = atoll(env);
     for (auto &e : c->chunk_ev)
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
             delete c;
@@ -309,7 +317,8 @@ extern "C" int mcb_ctx_destroy(mcb_ctx *c) {
     DevBuf *all[] = {&c->next_pos, &c->ranks[0], &c->ranks[1], &c->inst_out, &c->inst_lat, &c->wt, &c->snaps,
                      &c->tile_off, &c->stats, &c->pol_caps, &c->h_acc, &c->h_acc_off, &c->h_ev_off,
                      &c->h_rt_off, &c->h_ev_info, &c->h_routed, &c->h_params, &c->h_reports, &c->h_latency,
-                     &c->h_chain_reports, &c->h_hashes, &c->h_outcomes, &c->seg_snap, &c->seg_summ,
+                     &c->h_chain_reports, &c->h_hashes, &c->h_outcomes, &c->h_chain_latency, &c->seg_snap,
+                     &c->seg_summ,
                      &c->seg_out, &c->seg_codes, &c->nu_scratch, &c->lecar_u, &c->lecar_f, &c->diag,
                      &c->train_ws[0], &c->train_ws[1]};
     for (DevBuf *b : all) b->release();
@@ -485,7 +494,7 @@ int mcb_ctx_scratch(mcb_ctx *c, size_t bytes, void **p) {
 
 static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, int32_t n_pol, const int32_t *caps,
                          int32_t n_cap, const mcb_cost *cost, const mcb_nets *nets, const mcb_outputs *out,
-                         cudaStream_t s) {
+                         cudaStream_t s, bool reset_stats = true) {
     if (int rc = check_trace(t)) return rc;
     if (!pols || !caps || !cost || !out || !out->reports || !out->latency)
         return mcb_set_error(MCB_ERR_INVALID, "NULL policies / capacities / cost / outputs");
@@ -519,7 +528,7 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     const DevTrace d = make_dev_trace(t);
     int64_t launched = 0;
     if (int rc = c->stats.ensure(64)) return rc;
-    CUDA_TRY(cudaMemsetAsync(c->stats.p, 0, 64, s));
+    if (reset_stats) CUDA_TRY(cudaMemsetAsync(c->stats.p, 0, 64, s));
 
     ReplayParams P;
     memset(&P, 0, sizeof P);
@@ -728,6 +737,9 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     }
     mark(c, 8, s);
     launched += launch_fold(P, t->num_traces, out->reports, out->latency, s);
+    if (out->chain_latency && n_inst > 0)
+        CUDA_TRY(cudaMemcpyAsync(out->chain_latency, P.inst_lat, (size_t)n_inst * 2 * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, s));
     mark(c, 9, s);
     c->ran[4] = true;
     CUDA_TRY(cudaGetLastError());
@@ -790,6 +802,72 @@ extern "C" int mcb_training_data(mcb_ctx *c, const mcb_trace *t, int32_t capacit
     return MCB_OK;
 }
 
+// Device scratch of one replay of a uniform batch, per trace: K2 next-use
+// positions, the ML rank rows (one per ML variant), K3 feature snapshots,
+// per-instance outputs.  The segmented replay's records are only used when
+// the instances are too few to fill the GPU, i.e. never for large batches.
+static int64_t scratch_per_trace(const mcb_trace *t, const int32_t *pols, int n_pol, int n_cap) {
+    const int64_t ev = (int64_t)t->num_layers * t->events_per_chain;
+    bool ml[2] = {false, false}, nx = false;
+    for (int i = 0; i < n_pol; ++i) {
+        if (pols[i] == MCB_ML) ml[0] = true;
+        if (pols[i] == MCB_ML_NO_PREFILL) ml[1] = true;
+        if (pols[i] == MCB_BELADY) nx = true;
+    }
+    const int64_t E = t->num_experts;
+    int64_t b = (int64_t)t->num_layers * n_pol * n_cap * (MCB_R_N + 2) * 8;
+    if (nx) b += ev * t->top_k * 4;
+    if (ml[0] || ml[1]) b += ev * E * ((ml[0] ? 1 : 0) + (ml[1] ? 1 : 0)) + ev / MCB_TILE_EV * (4 * E + 8) * 4 + 64;
+    return b;
+}
+
+// Caller holds c->mu.
+static int replay_chunked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, int32_t n_pol, const int32_t *caps,
+                          int32_t n_cap, const mcb_cost *cost, const mcb_nets *nets, const mcb_outputs *out,
+                          void *stream) {
+    c->last_chunks = 1;
+    if (int rc = check_trace(t)) return rc;
+    if (!pols || n_pol < 1 || n_pol > MCB_MAX_POL || !caps || n_cap < 1 || n_cap > MCB_MAX_CAP || !out)
+        return replay_locked(c, t, pols, n_pol, caps, n_cap, cost, nets, out, (cudaStream_t)stream);
+    // Large uniform batches (e.g. C5: 4,096 Qwen3-shaped traces x 4,096 tokens,
+    // ~135 GB of rank rows and next-use positions at once) are replayed in
+    // consecutive trace ranges that share one bounded scratch.  Every chain
+    // is independent, so the results are those of one call.
+    int64_t per = t->uniform && t->num_traces > 1 ? scratch_per_trace(t, pols, n_pol, n_cap) : 0;
+    int64_t budget = c->scratch_bytes;
+    if (per > 0 && budget == 0) {
+        size_t fr = 0, tot = 0;
+        CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+        budget = (int64_t)(fr * 0.4);
+    }
+    const int64_t per_chunk = per > 0 ? std::max<int64_t>(1, budget / per) : t->num_traces;
+    if (per == 0 || per_chunk >= t->num_traces || out->outcomes)
+        return replay_locked(c, t, pols, n_pol, caps, n_cap, cost, nets, out, (cudaStream_t)stream);
+    const int64_t n_cells = (int64_t)n_pol * n_cap, L = t->num_layers;
+    const int64_t chain_acc = t->events_per_chain * t->top_k;
+    int64_t kernels = 0, chunks = 0;
+    for (int64_t t0 = 0; t0 < t->num_traces; t0 += per_chunk) {
+        const int64_t n = std::min<int64_t>(per_chunk, t->num_traces - t0);
+        mcb_trace sub = *t;
+        sub.num_traces = (int32_t)n;
+        sub.acc = t->acc + t0 * L * chain_acc;
+        mcb_outputs o = *out;
+        o.reports = out->reports + t0 * n_cells * MCB_R_N;
+        o.latency = out->latency + t0 * n_cells * 2;
+        if (out->chain_reports) o.chain_reports = out->chain_reports + t0 * L * n_cells * MCB_R_N;
+        if (out->hashes) o.hashes = out->hashes + t0 * L * n_cells;
+        if (out->chain_latency) o.chain_latency = out->chain_latency + t0 * L * n_cells * 2;
+        if (int rc = replay_locked(c, &sub, pols, n_pol, caps, n_cap, cost, nets, &o, (cudaStream_t)stream,
+                                   t0 == 0))
+            return rc;
+        kernels += c->last_kernels;
+        ++chunks;
+    }
+    c->last_kernels = kernels;
+    c->last_chunks = chunks;
+    return MCB_OK;
+}
+
 extern "C" int mcb_replay(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, int32_t n_pol, const int32_t *caps,
                           int32_t n_cap, const mcb_cost *cost, const mcb_nets *nets, const mcb_outputs *out,
                           void *stream) {
@@ -797,7 +875,7 @@ extern "C" int mcb_replay(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, i
     if (!c) return mcb_set_error(MCB_ERR_INVALID, "ctx is NULL");
     std::lock_guard<std::mutex> lk(c->mu);
     CUDA_TRY(cudaSetDevice(c->device));
-    return replay_locked(c, t, pols, n_pol, caps, n_cap, cost, nets, out, (cudaStream_t)stream);
+    return replay_chunked(c, t, pols, n_pol, caps, n_cap, cost, nets, out, stream);
 }
 
 template <typename T>
@@ -867,7 +945,11 @@ extern "C" int mcb_replay_host(mcb_ctx *c, const mcb_trace *t, const int32_t *po
         if (int rc = c->h_outcomes.ensure((size_t)(n_pol * n_cap * d.total_acc + 1) * sizeof(uint16_t))) return rc;
         dout.outcomes = (uint16_t *)c->h_outcomes.p;
     }
-    const int rc_replay = replay_locked(c, &dt, pols, n_pol, caps, n_cap, cost, np, &dout, s);
+    if (out->chain_latency) {
+        if (int rc = c->h_chain_latency.ensure((size_t)(n_inst + 1) * 2 * sizeof(double))) return rc;
+        dout.chain_latency = (double *)c->h_chain_latency.p;
+    }
+    const int rc_replay = replay_chunked(c, &dt, pols, n_pol, caps, n_cap, cost, np, &dout, s);
     if (c->nets_pending) {   // the stream must not outrun the copy even if no scorer ran
         cudaStreamWaitEvent(s, c->nets_ev, 0);
         c->nets_pending = false;
@@ -887,6 +969,9 @@ extern "C" int mcb_replay_host(mcb_ctx *c, const mcb_trace *t, const int32_t *po
         CUDA_TRY(cudaMemcpyAsync(out->hashes, dout.hashes, (size_t)n_inst * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     if (out->outcomes)
         CUDA_TRY(cudaMemcpyAsync(out->outcomes, dout.outcomes, (size_t)n_pol * n_cap * d.total_acc * sizeof(uint16_t),
+                                 cudaMemcpyDeviceToHost, s));
+    if (out->chain_latency)
+        CUDA_TRY(cudaMemcpyAsync(out->chain_latency, dout.chain_latency, (size_t)n_inst * 2 * sizeof(double),
                                  cudaMemcpyDeviceToHost, s));
     unsigned long long unc = 0;
     CUDA_TRY(cudaMemcpyAsync(&unc, c->stats.p, sizeof unc, cudaMemcpyDeviceToHost, s));

@@ -236,7 +236,8 @@ def replay_host(packed: PackedTrace, codes: Sequence[int], capacities: Sequence[
 
     Returns numpy arrays: reports [trace][pol][cap][8] int64, latency
     [trace][pol][cap][2] float64, and optionally chain_reports
-    [chain][pol][cap][8], hashes [chain][pol][cap], outcomes
+    [chain][pol][cap][8] + chain_latency [chain][pol][cap][2] (want_chain),
+    hashes [chain][pol][cap], outcomes
     [pol][cap][total_acc] uint16.
     """
     lib = _lib.load_library()
@@ -252,6 +253,8 @@ def replay_host(packed: PackedTrace, codes: Sequence[int], capacities: Sequence[
     if want_chain:
         res["chain_reports"] = np.zeros((packed.num_chains, n_pol, n_cap, _lib.R_N), dtype=np.int64)
         out.chain_reports = res["chain_reports"].ctypes.data
+        res["chain_latency"] = np.zeros((packed.num_chains, n_pol, n_cap, 2), dtype=np.float64)
+        out.chain_latency = res["chain_latency"].ctypes.data
     if want_hashes:
         res["hashes"] = np.zeros((packed.num_chains, n_pol, n_cap), dtype=np.uint64)
         out.hashes = res["hashes"].ctypes.data

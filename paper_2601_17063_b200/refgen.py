@@ -122,3 +122,30 @@ def generate_decode_ids(header: TraceHeader, cfg: SyntheticWorkloadConfig, devic
     if cfg.num_seqs != 1 or cfg.prefill_tokens != 0:
         raise InvalidConfigError("generate_decode_ids needs num_seqs == 1 and prefill_tokens == 0")
     return generate_experts(header, cfg, device)[0].permute(1, 0, 2).contiguous()
+
+
+def generate_decode_batch(header: TraceHeader, seeds, decode_steps: int, *, popularity_seed: int,
+                          zipf_s: float = 1.0, recency_boost: float = 0.0, w_hot: int = 4,
+                          device: int = 0) -> torch.Tensor:
+    """Many decode-only single-sequence traces in one launch: trace i is
+    ``generate_trace(header, SyntheticWorkloadConfig(num_seqs=1, decode_steps,
+    prefill_tokens=0, zipf_s, recency_boost, w_hot, rng_seed=seeds[i],
+    popularity_seed))`` -- uint8 CUDA tensor [n][L][T][K], chain-major."""
+    cfg0 = SyntheticWorkloadConfig(num_seqs=1, decode_steps=decode_steps, prefill_tokens=0, zipf_s=zipf_s,
+                                   recency_boost=recency_boost, w_hot=w_hot, rng_seed=0,
+                                   popularity_seed=popularity_seed)
+    header.validate()
+    cfg0.validate()
+    L, E, K = header.num_layers, header.num_experts, header.top_k
+    dev = torch.device("cuda", device)
+    pop = torch.from_numpy(layer_popularity(header, cfg0)).to(dev)
+    st = np.stack([stream_state(SyntheticWorkloadConfig(rng_seed=int(s))) for s in seeds]) if len(seeds) else \
+        np.zeros((0, 4), dtype=np.uint64)
+    dst = torch.from_numpy(np.ascontiguousarray(st).view(np.int64)).to(dev)
+    out = torch.empty((len(seeds), L, decode_steps, K), dtype=torch.uint8, device=dev)
+    s = torch.cuda.current_stream(dev)
+    lib = _lib.load_library()
+    _lib.check(lib.mcb_gen_reference_batch(_lib.context(device), L, E, K, len(seeds), decode_steps, w_hot,
+                                           float(recency_boost), pop.data_ptr(), dst.data_ptr(), out.data_ptr(),
+                                           ctypes.c_void_p(s.cuda_stream)))
+    return out

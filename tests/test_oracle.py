@@ -144,3 +144,32 @@ def test_oracle_duel_cases():
             got = oracle.eviction_duel(header, events, policy_name(d["a"]), policy_name(d["b"]), d["capacity"],
                                        nets, lecar_params(d["a"]), lecar_params(d["b"]))
             assert got == d["value"], (case["name"], d)
+
+
+def test_oracle_c_generator_matches_reference_fixtures():
+    """orc_gen_decode (C restatement of trace.py:186-287, used for the bench's
+    reference arm) against the decode-only reference-made traces: the small
+    decode-only fixtures and the full-size C1 (48 x 128 x 8, 2,048 tokens)
+    and Mixtral-shaped traces."""
+    import json
+    from golden_util import big_ids
+    z = np.load(os.path.join(GOLDEN, "gen_cases.npz"))
+    n = 0
+    for m in json.loads(str(z["meta"])):
+        c = m["config"]
+        if c.get("num_seqs", 1) != 1 or c.get("prefill_tokens", 32) != 0:
+            continue
+        got = oracle.generate_decode_batch(tuple(m["header"]), c["decode_steps"], [c.get("rng_seed", 0)],
+                                           c.get("popularity_seed"), c.get("zipf_s", 1.0),
+                                           c.get("recency_boost", 0.0), c.get("w_hot", 4))
+        assert np.array_equal(got[0], z[m["name"]][0]), m["name"]
+        n += 1
+    for case in load("big_cases.json.gz")["cases"][:2]:
+        ids, E = big_ids(case)
+        T, L, K = ids.shape
+        c = case["config"]
+        got = oracle.generate_decode_batch((L, E, K), T, [c["rng_seed"]], c.get("popularity_seed"), c["zipf_s"],
+                                           c["recency_boost"], c["w_hot"])
+        assert np.array_equal(got[0], ids)
+        n += 1
+    assert n >= 4

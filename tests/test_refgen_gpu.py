@@ -47,3 +47,20 @@ def test_generate_trace_api_matches_reference_events():
     tr = refgen.generate_trace(TraceHeader(m["name"], L, E, K), refgen.SyntheticWorkloadConfig(**m["config"]))
     ex = np.array([e.experts for e in tr.events], dtype=np.uint8).reshape(z[m["name"]].shape)
     assert np.array_equal(ex, z[m["name"]])
+
+
+def test_batch_generator_matches_single_and_oracle():
+    """mcb_gen_reference_batch (one stream per trace, shared popularity) equals
+    the per-trace generator and the oracle's C restatement, chain-major."""
+    import oracle
+    hdr = TraceHeader("b", 5, 64, 6)
+    seeds = [0, 1, 7, 1234567]
+    got = refgen.generate_decode_batch(hdr, seeds, 300, popularity_seed=7, recency_boost=0.3, w_hot=4)
+    got = got.cpu().numpy()
+    for i, s in enumerate(seeds):
+        cfg = refgen.SyntheticWorkloadConfig(num_seqs=1, decode_steps=300, prefill_tokens=0, recency_boost=0.3,
+                                             w_hot=4, rng_seed=s, popularity_seed=7)
+        one = refgen.generate_decode_ids(hdr, cfg).cpu().numpy()
+        assert np.array_equal(got[i], one), s
+    ref = oracle.generate_decode_batch((5, 64, 6), 300, seeds, 7, 1.0, 0.3, 4)   # [n][T][L][K]
+    assert np.array_equal(got, ref.transpose(0, 2, 1, 3))
