@@ -182,9 +182,10 @@ int mcb_last_stats(mcb_ctx *ctx, int64_t *kernels_launched, int64_t *uncertain_e
  * [0] K2 next-use scan, [1] K3 scorer, [2] K4 replay, [3] K5 fold. */
 int mcb_set_timing(mcb_ctx *ctx, int32_t enable);
 /* Device-side counters of the last mcb_replay (synchronises the device):
- * [0] uncertain scorer events, [1] segmented replay: events replayed by the
- * fix-up walk, [2] segments whose speculative state never converged,
- * [3] segments walked. */
+ * [0] uncertain scorer events (float64 near ties), [1] segmented replay:
+ * events replayed by the fix-up walk, [2] segments whose speculative state
+ * never converged, [3] segments walked, [4] latency folds done event by
+ * event, [5] events the tensor-core scorer re-scored in float64. */
 int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
 /* Tuning knobs (results never depend on them):
  * MCB_TUNE_SOLO_MIN: minimum instance count for the thread-per-instance
@@ -231,6 +232,15 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
  * are identical; outcomes are not supported then).  0 (default) = 40% of
  * the device memory free at the call. */
 #define MCB_TUNE_SCRATCH_BYTES 11
+/* MCB_TUNE_K3_TC: 1 (default) = the tensor-core scorer (bf16 x 3 split on
+ * tcgen05, certified ranks, float64 re-score of uncertified events) for
+ * uniform traces with hidden 128 and num_experts in {8, 16, 32, 64, 128};
+ * 0 = the float64 DMMA scorer for every event.  Ranks are identical. */
+#define MCB_TUNE_K3_TC 12
+/* MCB_TUNE_K3_TAU_PPB: the tensor-core scorer certifies an event's order when
+ * every two adjacent scores differ by more than 2 * tau * max|s|; tau in units
+ * of 1e-9 (default 4000 = 4e-6).  Larger = more events re-scored in float64. */
+#define MCB_TUNE_K3_TAU_PPB 13
 int mcb_set_tuning(mcb_ctx *ctx, int32_t knob, int64_t value);
 /* LeCaR parameters used by the MCB_LECAR cells of later mcb_replay calls on
  * this context (LeCaRPolicy.__init__, policies.py:333-349; defaults 0.45,
@@ -347,6 +357,13 @@ int mcb_next_use(mcb_ctx *ctx, const mcb_trace *trace, uint32_t *next_pos, void 
  * scores[event][E].  Device pointers. */
 int mcb_score(mcb_ctx *ctx, const mcb_trace *trace, const mcb_nets *nets, int32_t include_prefill,
               uint8_t *ranks, double *scores, void *stream);
+
+/* K3-TC alone (tests and calibration): the tensor-core scorer's ranks (after
+ * the float64 re-score of uncertified events, identical to mcb_score's) and
+ * its fp32 scores[event][E] before certification.  Uniform traces, hidden
+ * 128, num_experts in {8, 16, 32, 64, 128}.  Device pointers. */
+int mcb_score_tc_scores(mcb_ctx *ctx, const mcb_trace *trace, const mcb_nets *nets, uint8_t *ranks,
+                        float *scores, void *stream);
 
 /* ---- K1: router-logits GEMM + top-k trace generator (tcgen05 / TMA) ----
  * hidden[T][d] bf16 (shared by all layers), weight[L*E][d] bf16 (router

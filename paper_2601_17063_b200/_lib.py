@@ -37,6 +37,8 @@ MCB_TUNE_OVERLAP = 8
 MCB_TUNE_WIDE_MIN = 9
 MCB_TUNE_SEG_TSPEC = 10
 MCB_TUNE_SCRATCH_BYTES = 11
+MCB_TUNE_K3_TC = 12
+MCB_TUNE_K3_TAU_PPB = 13
 R_PH, R_PM, R_DH, R_DM, R_COMP, R_EVICT, R_REFETCH, R_STATUS = range(8)
 R_N = 8
 OUT_HIT, OUT_MISS = 0xFFFF, 0xFFFE
@@ -46,7 +48,7 @@ EXPORTED_SYMBOLS = (
     "mcb_set_timing", "mcb_last_timings", "mcb_set_tuning", "mcb_read_stats",
     "mcb_pack_trace", "mcb_packed_view", "mcb_packed_positions", "mcb_packed_free",
     "mcb_replay", "mcb_replay_host", "mcb_next_use", "mcb_score", "mcb_router_topk", "mcb_gen_reference",
-    "mcb_gen_reference_batch",
+    "mcb_gen_reference_batch", "mcb_score_tc_scores",
     "mcb_training_data", "mcb_set_lecar", "mcb_lecar_random", "mcb_pack_decode_ids",
     "mcb_eviction_duel", "mcb_train_epoch", "mcb_train_eval",
 )
@@ -161,6 +163,7 @@ def load_library():
             "mcb_train_epoch": ([P, P, P, P, P, P, i64, i64, P, P, P], ctypes.c_int),
             "mcb_train_eval": ([P, P, P, i64, i64, P, P], ctypes.c_int),
             "mcb_gen_reference_batch": ([P, i32, i32, i32, i64, i64, i32, ctypes.c_double, P, P, P, P], i32),
+            "mcb_score_tc_scores": ([P, P, P, P, P, P], i32),
             "mcb_gen_reference": ([P, i32, i32, i32, i64, i64, i64, i32, ctypes.c_double, P, P, P, P],
                                   ctypes.c_int),
         }

@@ -110,6 +110,9 @@ struct mcb_ctx {
     int64_t last_chunks = 1;          // trace ranges of the last mcb_replay
     bool serial = false;              // one stream for every stage (per-stage attribution timing)
     DevBuf seg_snap, seg_summ, seg_out, seg_codes, nu_scratch;
+    DevBuf tc_wimg, tc_bias, tc_flag_cnt, tc_flag_list;   // K3-TC scratch
+    int k3_tc = 1;                    // tensor-core scorer when eligible (MCB_TUNE_K3_TC)
+    int64_t k3_tau_ppb = 4000;        // its certification threshold tau in 1e-9 (MCB_TUNE_K3_TAU_PPB)
     // LeCaR (mcb_set_lecar): parameters, the shared random() stream (cached
     // per seed, grown on demand) and the per-call regret factor table
     double lecar_lr = 0.45, lecar_base = 0.005;
@@ -220,6 +223,15 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
         c->overlap = (int)value;
         return MCB_OK;
     }
+    if (knob == MCB_TUNE_K3_TC) {
+        c->k3_tc = value != 0;
+        return MCB_OK;
+    }
+    if (knob == MCB_TUNE_K3_TAU_PPB) {
+        if (value < 0) return mcb_set_error(MCB_ERR_INVALID, "tau must be >= 0");
+        c->k3_tau_ppb = value;
+        return MCB_OK;
+    }
     if (knob == MCB_TUNE_SCRATCH_BYTES) {
         if (value < 0) return mcb_set_error(MCB_ERR_INVALID, "scratch budget must be >= 0");
         c->scratch_bytes = value;
@@ -270,7 +282,7 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     if (prop.major < 10)
         return mcb_set_error(MCB_ERR_UNSUPPORTED, "libmcb is built for sm_100a (B200); device is older");
     if (preload_kernels() != 0 || preload_segment_kernels() != 0 || preload_segment_warp_kernels() != 0 ||
-        preload_wide_kernels() != 0)
+        preload_wide_kernels() != 0 || preload_score_tc() != 0)
         return mcb_set_error(MCB_ERR_CUDA, "failed to load the replay kernels");
     if (int rc = mcb_router_preload()) return rc;
     auto *c = new (std::nothrow) mcb_ctx();
@@ -287,6 +299,8 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     if (const char *env = getenv("MCB_ML_CHUNKS")) c->ml_chunks = atoll(env);
     if (const char *env = getenv("MCB_OVERLAP")) c->overlap = atoi(env);
     if (const char *env = getenv("MCB_SCRATCH_BYTES")) c->scratch_bytes = atoll(env);
+    if (const char *env = getenv("MCB_K3_TC")) c->k3_tc = atoi(env);
+    if (const char *env = getenv("MCB_K3_TAU_PPB")) c->k3_tau_ppb = atoll(env);
     for (auto &e : c->chunk_ev)
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
             delete c;
@@ -318,7 +332,7 @@ extern "C" int mcb_ctx_destroy(mcb_ctx *c) {
                      &c->tile_off, &c->stats, &c->pol_caps, &c->h_acc, &c->h_acc_off, &c->h_ev_off,
                      &c->h_rt_off, &c->h_ev_info, &c->h_routed, &c->h_params, &c->h_reports, &c->h_latency,
                      &c->h_chain_reports, &c->h_hashes, &c->h_outcomes, &c->h_chain_latency, &c->seg_snap,
-                     &c->seg_summ,
+                     &c->seg_summ, &c->tc_wimg, &c->tc_bias, &c->tc_flag_cnt, &c->tc_flag_list,
                      &c->seg_out, &c->seg_codes, &c->nu_scratch, &c->lecar_u, &c->lecar_f, &c->diag,
                      &c->train_ws[0], &c->train_ws[1]};
     for (DevBuf *b : all) b->release();
@@ -421,7 +435,7 @@ static int check_nets(const DevTrace &d, const mcb_nets *nets) {
 }
 
 static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int include_prefill, uint8_t *ranks,
-                     double *scores, cudaStream_t s, int64_t *launched) {
+                     double *scores, cudaStream_t s, int64_t *launched, float *tc_scores = nullptr) {
     const int E = d.E, H = nets->hidden;
     if (int rc = check_nets(d, nets)) return rc;
     if (int rc = ensure_score_buffers(c, d, nets)) return rc;
@@ -430,6 +444,24 @@ static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int in
     if (c->nets_pending) CUDA_TRY(cudaStreamWaitEvent(s, c->nets_ev, 0));   // host path: nets copied on side2
     *launched += launch_prepare_nets(nets->params, E, H, nets->num_nets, (double *)c->wt.p, s);
     const int64_t tiles = max_score_tiles(d);
+    if (c->k3_tc && !scores && score_tc_eligible(d, H)) {
+        // K3-TC: bf16x3 tcgen05 scorer; events it cannot certify are re-scored in float64
+        const int nn = nets->num_nets;
+        const int64_t cap = nn == 1 ? d.total_events : d.total_events / d.L;
+        if (int rc = c->tc_wimg.ensure(score_tc_net_bytes(E) * nn)) return rc;
+        if (int rc = c->tc_bias.ensure((size_t)score_tc_bias_stride(E) * nn * sizeof(float))) return rc;
+        if (int rc = c->tc_flag_cnt.ensure((size_t)nn * sizeof(int32_t))) return rc;
+        if (int rc = c->tc_flag_list.ensure((size_t)(nn * cap + 1) * sizeof(int32_t))) return rc;
+        *launched += launch_score_prep(d, include_prefill, (int32_t *)c->snaps.p, (int64_t *)c->tile_off.p, tiles, s);
+        *launched += launch_score_tc(d, nets->params, nn, (const int32_t *)c->snaps.p, (uint8_t *)c->tc_wimg.p,
+                                     (float *)c->tc_bias.p, ranks, (float)(c->k3_tau_ppb * 1e-9),
+                                     (int32_t *)c->tc_flag_cnt.p, (int32_t *)c->tc_flag_list.p, cap,
+                                     (unsigned long long *)c->stats.p, tc_scores, s) - 1;
+        *launched += launch_rescore(d, (const double *)c->wt.p, H, nn, (const int32_t *)c->snaps.p,
+                                    (const int32_t *)c->tc_flag_cnt.p, (const int32_t *)c->tc_flag_list.p, cap, ranks,
+                                    (unsigned long long *)c->stats.p, s);
+        return MCB_OK;
+    }
     const int n = launch_score(d, (const double *)c->wt.p, H, nets->num_nets, include_prefill, ranks, scores,
                                (int32_t *)c->snaps.p, (int64_t *)c->tile_off.p, tiles,
                                (unsigned long long *)c->stats.p, c->k3_ctas, s);
@@ -467,6 +499,30 @@ extern "C" int mcb_score(mcb_ctx *c, const mcb_trace *t, const mcb_nets *nets, i
     const DevTrace d = make_dev_trace(t);
     int64_t launched = 0;
     if (int rc = run_score(c, d, nets, include_prefill, ranks, scores, s, &launched)) return rc;
+    CUDA_TRY(cudaGetLastError());
+    return MCB_OK;
+}
+
+extern "C" int mcb_score_tc_scores(mcb_ctx *c, const mcb_trace *t, const mcb_nets *nets, uint8_t *ranks,
+                                   float *scores, void *stream) {
+    mcb_clear_error();
+    if (!c) return mcb_set_error(MCB_ERR_INVALID, "ctx is NULL");
+    if (int rc = check_trace(t)) return rc;
+    if (!nets || !ranks || !scores) return mcb_set_error(MCB_ERR_INVALID, "nets / ranks / scores is NULL");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (int rc = c->stats.ensure(64)) return rc;
+    CUDA_TRY(cudaMemsetAsync(c->stats.p, 0, 64, s));
+    const DevTrace d = make_dev_trace(t);
+    if (!score_tc_eligible(d, nets->hidden))
+        return mcb_set_error(MCB_ERR_UNSUPPORTED, "trace / net shape not eligible for the tensor-core scorer");
+    const int keep = c->k3_tc;
+    c->k3_tc = 1;
+    int64_t launched = 0;
+    const int rc = run_score(c, d, nets, 1, ranks, nullptr, s, &launched, scores);
+    c->k3_tc = keep;
+    if (rc) return rc;
     CUDA_TRY(cudaGetLastError());
     return MCB_OK;
 }
@@ -817,7 +873,7 @@ static int64_t scratch_per_trace(const mcb_trace *t, const int32_t *pols, int n_
     const int64_t E = t->num_experts;
     int64_t b = (int64_t)t->num_layers * n_pol * n_cap * (MCB_R_N + 2) * 8;
     if (nx) b += ev * t->top_k * 4;
-    if (ml[0] || ml[1]) b += ev * E * ((ml[0] ? 1 : 0) + (ml[1] ? 1 : 0)) + ev / MCB_TILE_EV * (4 * E + 8) * 4 + 64;
+    if (ml[0] || ml[1]) b += ev * E * ((ml[0] ? 1 : 0) + (ml[1] ? 1 : 0)) + ev / MCB_TILE_EV * (4 * E + 8) * 4 + ev * 4 + 64;
     return b;
 }
 

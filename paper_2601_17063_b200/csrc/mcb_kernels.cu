@@ -1682,6 +1682,55 @@ __device__ __forceinline__ void rank_event_packed(const double *srow, int E, uin
     if (__any_sync(FULL_MASK, near) && lane == 0) *flag = 1;
 }
 
+// Integer ranks of the fp64 scores of rows [0, nev) of bufA (row stride ldA)
+// into s_rank[row][E], near-tie flags into s_flag[row] (rank = 1 + #{selectable
+// j : s_j < s_e}, 0 for NaN / -inf; near tie = two distinct scores within
+// 1e-12 relative).  Every thread of the block calls it; ends with a barrier.
+__device__ __forceinline__ void rank_tile_rows(const double *bufA, int ldA, int E, int nev, uint8_t *s_rank,
+                                               int32_t *s_flag) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int i = tid; i < MCB_TILE_EV; i += blockDim.x) s_flag[i] = 0;
+    __syncthreads();
+    if (E <= 16) {
+        // few experts: each (event, expert) thread counts the smaller scores
+        for (int q = tid; q < MCB_TILE_EV * E; q += blockDim.x) {
+            const int i = q % MCB_TILE_EV, e = q / MCB_TILE_EV;
+            if (i >= nev) continue;
+            const double s = bufA[i * ldA + e];
+            uint32_t r = 0;
+            bool near = false;
+            if (s > -INFINITY) {
+                // rank = 1 + #{selectable j : s_j < s}; the near-tie test only needs the
+                // nearest smaller score (every adjacent pair of the sorted order is
+                // tested by its larger member)
+                r = 1;
+                double below = -INFINITY;
+#pragma unroll 8
+                for (int j = 0; j < E; ++j) {
+                    const double sj = bufA[i * ldA + j];
+                    if (sj > -INFINITY && sj < s) {
+                        ++r;
+                        below = fmax(below, sj);
+                    }
+                }
+                near = below > -INFINITY && fabs(s - below) <= 1e-12 * fmax(fabs(s), fabs(below));
+            }
+            s_rank[i * E + e] = (uint8_t)r;
+            if (near) s_flag[i] = 1;
+        }
+    } else {
+        // many experts: one warp sorts each event's scores (bitonic, in
+        // registers) -- O(E log^2 E) instead of O(E^2) per event
+        const int warp = tid >> 5;
+        for (int i = warp; i < nev; i += (int)(blockDim.x >> 5)) {
+            if (E <= 32) rank_event_packed<1>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
+            else if (E <= 64) rank_event_packed<2>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
+            else rank_event_packed<4>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
+        }
+    }
+    __syncthreads();
+}
+
 template <int TE, int TH>   // (num_experts, hidden) specialisation, 0 = runtime
 __global__ void __launch_bounds__(256, TE ? 4 : 1) k_score_tile(DevTrace tr, const double *__restrict__ wt_all, int H_rt,
                                                      int num_nets, int include_prefill,
@@ -1759,45 +1808,7 @@ __global__ void __launch_bounds__(256, TE ? 4 : 1) k_score_tile(DevTrace tr, con
         mma_layer_any(bufB, ldB, Hp, Wt3, b3, Ep, bufA, ldA, false, s_exp2);    // scores -> A
         __syncthreads();
     }
-    for (int i = tid; i < MCB_TILE_EV; i += blockDim.x) s_flag[i] = 0;
-    __syncthreads();
-    if (E <= 16) {
-        // few experts: each (event, expert) thread counts the smaller scores
-        for (int q = tid; q < MCB_TILE_EV * E; q += blockDim.x) {
-            const int i = q % MCB_TILE_EV, e = q / MCB_TILE_EV;
-            if (i >= nev) continue;
-            const double s = bufA[i * ldA + e];
-            uint32_t r = 0;
-            bool near = false;
-            if (s > -INFINITY) {
-                // rank = 1 + #{selectable j : s_j < s}; the near-tie test only needs the
-                // nearest smaller score (every adjacent pair of the sorted order is
-                // tested by its larger member)
-                r = 1;
-                double below = -INFINITY;
-#pragma unroll 8
-                for (int j = 0; j < E; ++j) {
-                    const double sj = bufA[i * ldA + j];
-                    if (sj > -INFINITY && sj < s) {
-                        ++r;
-                        below = fmax(below, sj);
-                    }
-                }
-                near = below > -INFINITY && fabs(s - below) <= 1e-12 * fmax(fabs(s), fabs(below));
-            }
-            s_rank[i * E + e] = (uint8_t)r;
-            if (near) s_flag[i] = 1;
-        }
-    } else {
-        // many experts: one warp sorts each event's scores (bitonic, in
-        // registers) -- O(E log^2 E) instead of O(E^2) per event
-        const int warp = tid >> 5;
-        for (int i = warp; i < nev; i += (int)(blockDim.x >> 5)) {
-            if (E <= 32) rank_event_packed<1>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
-            else if (E <= 64) rank_event_packed<2>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
-            else rank_event_packed<4>(bufA + i * ldA, E, s_rank + i * E, s_flag + i, lane);
-        }
-    }
+    rank_tile_rows(bufA, ldA, E, nev, s_rank, s_flag);
     if (scores)
         for (int q = tid; q < nev * E; q += blockDim.x) scores[(e0 + ev0) * E + q] = bufA[(q / E) * ldA + q % E];
     __syncthreads();
@@ -1810,6 +1821,137 @@ __global__ void __launch_bounds__(256, TE ? 4 : 1) k_score_tile(DevTrace tr, con
     }
     __syncthreads();   // shared buffers are reused by the next tile
     }
+}
+
+// float64 re-score of the events the tensor-core scorer could not certify
+// (mcb_score_tc.cu): flag_list holds, per net (bucket), the chain-major event
+// indices of a uniform trace.  Each CTA takes 32 listed events of one net at a
+// time, rebuilds their float64 features from the K3 snapshot of their 32-event
+// tile plus the tile's earlier events (features.py:34-52), runs the same
+// float64 MLP and ranking as k_score_tile and overwrites their rank rows.
+template <int TE, int TH>
+__global__ void __launch_bounds__(256, 1) k_rescore(DevTrace tr, const double *__restrict__ wt_all, int H_rt,
+                                                   int num_nets, const int32_t *__restrict__ snaps,
+                                                   const int32_t *__restrict__ flag_cnt,
+                                                   const int32_t *__restrict__ flag_list, int64_t bucket_cap,
+                                                   uint8_t *__restrict__ ranks, unsigned long long *uncertain) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int E = TE ? TE : tr.E, D = 2 * E, H = TH ? TH : H_rt;
+    const int Hp = mlp_hp(H), Kp1 = mlp_kp1(E), Ep = mlp_ep(E);
+    const int ldA = mlp_ld(Kp1 > Ep ? Kp1 : Ep), ldB = mlp_ld(Hp);
+    double *bufA = (double *)smem_raw;
+    double *bufB = bufA + ldA * MCB_TILE_EV;
+    uint8_t *s_rank = (uint8_t *)(bufB + ldB * MCB_TILE_EV);
+    int32_t *s_flag = (int32_t *)(s_rank + MCB_TILE_EV * MCB_MAX_EXPERTS);
+    __shared__ double s_exp2[64];
+    __shared__ int64_t s_pref[MCB_MAX_EXPERTS + 1];
+    __shared__ int32_t s_ev[MCB_TILE_EV];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < 64) s_exp2[tid] = g_exp2_64[tid];
+    if (tid == 0) {
+        int64_t a = 0;
+        s_pref[0] = 0;
+        for (int bk = 0; bk < num_nets; ++bk) {
+            a += (flag_cnt[bk] + MCB_TILE_EV - 1) / MCB_TILE_EV;
+            s_pref[bk + 1] = a;
+        }
+    }
+    __syncthreads();
+    const int64_t total = s_pref[num_nets];
+    const int64_t tpc32 = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
+    const int SN = 2 * E + 4;
+    for (int64_t vt = blockIdx.x; vt < total; vt += gridDim.x) {
+        int bk = 0;
+        while (s_pref[bk + 1] <= vt) ++bk;
+        const int64_t i0 = (vt - s_pref[bk]) * MCB_TILE_EV;
+        const int nev = (int)min((int64_t)MCB_TILE_EV, (int64_t)flag_cnt[bk] - i0);
+        if (tid < MCB_TILE_EV) s_ev[tid] = tid < nev ? flag_list[bk * bucket_cap + i0 + tid] : -1;
+        __syncthreads();
+        for (int r = warp; r < MCB_TILE_EV; r += (int)(blockDim.x >> 5)) {
+            const int32_t ev = s_ev[r];
+            int32_t last[4], f[4];
+            int32_t u = 0, maxf = 0;
+            if (ev >= 0) {
+                const int64_t c = ev / tr.T, i = ev % tr.T, s32 = i / MCB_TILE_EV;
+                const int32_t *sp = snaps + (c * tpc32 + s32) * SN;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int e = lane + 32 * j;
+                    last[j] = e < E ? sp[e] : -1;
+                    f[j] = e < E ? sp[E + e] : 0;
+                }
+                // the tile's events up to and including this one (features.py:34-39)
+                for (int64_t jj = s32 * MCB_TILE_EV; jj <= i; ++jj) {
+                    const uint8_t *ids = tr.acc + (c * tr.T + jj) * tr.K;
+                    for (int k = 0; k < tr.K; ++k) {
+                        const int x = __ldg(ids + k);
+                        if ((x & 31) == lane) {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                if ((x >> 5) == j) { last[j] = (int32_t)jj + 1; ++f[j]; }
+                        }
+                    }
+                }
+                u = (int32_t)i + 1;
+                maxf = __reduce_max_sync(FULL_MASK, max(max(f[0], f[1]), max(f[2], f[3])));
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int e = lane + 32 * j;
+                if (e < E) {
+                    double rv = 0.0, fv = 0.0;
+                    if (ev >= 0) {
+                        rv = last[j] < 0 ? 0.0 : 1.0 / (double)(u - last[j] + 1);
+                        fv = maxf > 0 ? (double)f[j] / (double)maxf : 0.0;
+                    }
+                    bufA[r * ldA + e] = rv;
+                    bufA[r * ldA + E + e] = fv;
+                }
+            }
+        }
+        for (int q = tid; q < MCB_TILE_EV * (Kp1 - D); q += blockDim.x)   // zero feature padding
+            bufA[(q / (Kp1 - D)) * ldA + D + q % (Kp1 - D)] = 0.0;
+        __syncthreads();
+        const double *wt = wt_all + (num_nets == 1 ? 0 : bk) * (int64_t)prepared_net_doubles(E, H);
+        const double *Wt1 = wt, *b1 = Wt1 + (int64_t)Kp1 * Hp, *Wt2 = b1 + Hp, *b2 = Wt2 + (int64_t)Hp * Hp,
+                     *Wt3 = b2 + Hp, *b3 = Wt3 + (int64_t)Hp * Ep;
+        if constexpr (TE > 0 && TH > 0) {
+            constexpr int cHp = (TH + 7) / 8 * 8, cKp1 = (2 * TE + 3) / 4 * 4, cEp = (TE + 7) / 8 * 8;
+            mma_layer_fixed<cHp, cKp1>(bufA, ldA, Wt1, b1, bufB, ldB, true, s_exp2);
+            __syncthreads();
+            mma_layer_fixed<cHp, cHp>(bufB, ldB, Wt2, b2, bufB, ldB, true, s_exp2);
+            __syncthreads();
+            mma_layer_fixed<cEp, cHp>(bufB, ldB, Wt3, b3, bufA, ldA, false, s_exp2);
+            __syncthreads();
+        } else {
+            mma_layer_any(bufA, ldA, Kp1, Wt1, b1, Hp, bufB, ldB, true, s_exp2);
+            __syncthreads();
+            mma_layer_any(bufB, ldB, Hp, Wt2, b2, Hp, bufB, ldB, true, s_exp2);
+            __syncthreads();
+            mma_layer_any(bufB, ldB, Hp, Wt3, b3, Ep, bufA, ldA, false, s_exp2);
+            __syncthreads();
+        }
+        rank_tile_rows(bufA, ldA, E, nev, s_rank, s_flag);
+        for (int q = tid; q < nev * E; q += blockDim.x) ranks[(int64_t)s_ev[q / E] * E + q % E] = s_rank[q];
+        if (tid == 0 && uncertain) {
+            unsigned long long cnt = 0;
+            for (int i = 0; i < nev; ++i) cnt += s_flag[i];
+            if (cnt) atomicAdd(uncertain, cnt);
+        }
+        __syncthreads();
+    }
+}
+
+typedef void (*rescore_fn)(DevTrace, const double *, int, int, const int32_t *, const int32_t *, const int32_t *,
+                           int64_t, uint8_t *, unsigned long long *);
+static rescore_fn rescore_kernel(int E, int H) {
+    if (H == 128) {
+        if (E == 8) return k_rescore<8, 128>;
+        if (E == 16) return k_rescore<16, 128>;
+        if (E == 64) return k_rescore<64, 128>;
+        if (E == 128) return k_rescore<128, 128>;
+    }
+    return k_rescore<0, 0>;
 }
 
 static size_t score_smem(int E, int H) {
@@ -1893,6 +2035,23 @@ int launch_score(const DevTrace &tr, const double *wt, int H, int num_nets, int 
     launched += launch_score_tiles(tr, wt, H, num_nets, include_prefill, ranks, scores, snaps, tile_off, 0,
                                    max_tiles, uncertain, k3_ctas, s);
     return launched;
+}
+
+// float64 re-score of the tensor-core scorer's flagged events (persistent
+// grid; the per-net counts are read on the device).
+int launch_rescore(const DevTrace &tr, const double *wt, int H, int num_nets, const int32_t *snaps,
+                   const int32_t *flag_cnt, const int32_t *flag_list, int64_t bucket_cap, uint8_t *ranks,
+                   unsigned long long *uncertain, cudaStream_t s) {
+    if (tr.n_chains == 0) return 0;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = score_smem(tr.E, H);
+    const rescore_fn fn = rescore_kernel(tr.E, H);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    fn<<<(unsigned)(2 * sms), 256, smem, s>>>(tr, wt, H, num_nets, snaps, flag_cnt, flag_list, bucket_cap, ranks,
+                                             uncertain);
+    return 1;
 }
 
 // Force-load every kernel of the library at context creation (CUDA 12 lazy

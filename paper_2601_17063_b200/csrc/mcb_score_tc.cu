@@ -1,0 +1,666 @@
+// K3-TC: the ML scorer (EvictionNet.forward, pkg/src/moecache/net.py:88-105,
+// fed by FeatureTracker, features.py:34-52) on the 5th-gen tensor cores, with
+// certified per-event ranks.
+//
+// The reference scores every event with a float64 3-layer MLP 2E -> 128 ->
+// 128 -> E (SiLU) and evicts the arg-max score over resident \ pinned,
+// lowest id on ties (mlpolicy.py:15-26).  The replay only needs the ORDER of
+// each event's scores (the rank row, shared by every capacity), so:
+//
+//   1. this kernel evaluates the MLP on tcgen05 in "bf16 x 3" arithmetic:
+//      every operand is split into three bf16 parts (a = a0 + a1 + a2, 24
+//      significant bits) and the six products with i + j <= 2 are
+//      accumulated in fp32 in TMEM (the leading a0*b0 product in its own
+//      accumulator, the five small ones in a second), bias + SiLU in fp32
+//      in the epilogue, which re-splits the activations into the next
+//      layer's A operand in shared memory;
+//   2. it sorts each event's E scores (one thread per event, bitonic network
+//      on order-preserving keys carrying the expert id in their low bits)
+//      and writes the rank row;
+//   3. an event is CERTIFIED only if every pair of adjacent scores in that
+//      order is separated by more than 2 * tau * max|s| (tau = 4e-6 by
+//      default, an order of magnitude above the largest deviation from the
+//      float64 forward measured over the test corpus, tests/test_score_tc_gpu.py)
+//      and all scores are finite; any other event is appended to a per-net
+//      list and RE-SCORED in float64 by k_rescore (mcb_kernels.cu: the fp64
+//      DMMA scorer on gathered events), whose ranks overwrite the row.
+//
+// So every rank row equals the float64 scorer's (the round-1 K3), and ML
+// decisions equal the reference's whenever the float64 scores order the
+// experts like the reference's BLAS float64 scores.
+//
+// Kernel shape: persistent, one CTA per SM, 10 warps:
+//   warp 0     weight producer: cp.async.bulk of pre-swizzled bf16 weight
+//              blocks (one part x one 64-wide K block) into a 2-stage ring
+//   warp 1     TMEM allocator (512 columns) + the single MMA-issuing thread
+//              (tcgen05.mma kind::f16, M=128, N=128 / E, K=16)
+//   warps 2-5  epilogue group 0, warps 6-9 epilogue group 1: each group owns
+//              one 128-event tile at a time (one event per thread: TMEM lane
+//              = event row), its A buffer (3 parts x 128 x 128 bf16 =
+//              96 KB) and 256 TMEM columns (hi + lo accumulators).
+// The two groups alternate on the tensor pipe: while one group runs its
+// epilogue (features, bias + SiLU + split, or the rank sort), the MMAs of the
+// other group's next layer run.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mcb_kernels.cuh"
+
+namespace k3tc {
+
+constexpr int H = 128;                    // EvictionNet hidden size (net.py:64 default)
+constexpr int BM = 128;                   // events per tile (MMA M)
+constexpr int ROWB = 128;                 // bytes per swizzled row: 64 bf16 (SWIZZLE_128B atom)
+constexpr int KBLK = BM * ROWB;           // [128 rows x 64 K] block: 16 KB
+constexpr int A_PART = 2 * KBLK;          // one bf16 part of a [128 x 128] operand: 32 KB
+constexpr int A_BYTES = 3 * A_PART;       // three parts: 96 KB per epilogue group
+constexpr int W_STAGE = 128 * ROWB;       // one weight block [<= 128 rows x 64 K]: 16 KB
+constexpr int W_STAGES = 2;
+constexpr int THREADS = 320;
+constexpr int SMEM_BYTES = 2 * A_BYTES + W_STAGES * W_STAGE + 1024 + 256;
+
+struct Params {
+    DevTrace tr;
+    const uint8_t *wimg;        // per net: swizzled bf16 weight blocks (k_prep_tc)
+    int64_t net_bytes;
+    const float *bias;          // per net: b1[128] b2[128] b3[N3]
+    int bias_stride;
+    int num_nets;
+    int N3, KB1, P1;            // layer-3 N (E rounded up to 16), layer-1 K blocks, layer-1 passes
+    int64_t n_tiles, tpc, tpc32;
+    const int32_t *snaps;       // K3 tracker snapshots every 32 events (k_snap_scan)
+    uint8_t *ranks;             // [event][E]
+    float tau;
+    int32_t *flag_cnt;          // [num_nets]
+    int32_t *flag_list;         // [num_nets][bucket_cap]
+    int64_t bucket_cap;
+    unsigned long long *stats;  // [5] += events flagged for the float64 re-score
+    float *dbg_scores;          // optional [event][E]: the fp32 scores (tests / calibration)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms of 1024 B
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+// kind::f16 instruction descriptor: D = f32, A = B = bf16, K-major, M = 128
+__device__ __forceinline__ uint32_t idesc(int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t id, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+// 32 consecutive fp32 TMEM columns of this thread's lane (no wait)
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// st.shared writes become visible to the tensor core's async proxy
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// byte offset of the 16-B chunk `ch` (0..7) of row `row` inside a
+// [rows x 64] bf16 block in the SWIZZLE_128B K-major layout
+__host__ __device__ __forceinline__ uint32_t sw128(int row, int ch) {
+    return (uint32_t)row * ROWB + ((uint32_t)(ch ^ (row & 7)) << 4);
+}
+
+// a = a0 + a1 + a2 (bf16, round to nearest; each remainder is exact in fp32)
+__device__ __forceinline__ void split3(float a, __nv_bfloat16 &p0, __nv_bfloat16 &p1, __nv_bfloat16 &p2) {
+    p0 = __float2bfloat16_rn(a);
+    const float r1 = a - __bfloat162float(p0);
+    p1 = __float2bfloat16_rn(r1);
+    p2 = __float2bfloat16_rn(r1 - __bfloat162float(p1));
+}
+
+// eight consecutive K values of one row -> the three parts' 16-B chunks
+__device__ __forceinline__ void store_chunk8(uint8_t *abuf, int row, int k0, const float (&v)[8]) {
+    uint32_t w[3][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        __nv_bfloat16 a0, a1, a2, b0, b1, b2;
+        split3(v[2 * j], a0, a1, a2);
+        split3(v[2 * j + 1], b0, b1, b2);
+        w[0][j] = (uint32_t)__bfloat16_as_ushort(a0) | ((uint32_t)__bfloat16_as_ushort(b0) << 16);
+        w[1][j] = (uint32_t)__bfloat16_as_ushort(a1) | ((uint32_t)__bfloat16_as_ushort(b1) << 16);
+        w[2][j] = (uint32_t)__bfloat16_as_ushort(a2) | ((uint32_t)__bfloat16_as_ushort(b2) << 16);
+    }
+    const uint32_t off = (uint32_t)(k0 >> 6) * KBLK + sw128(row, (k0 & 63) >> 3);
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+        *(uint4 *)(abuf + p * A_PART + off) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
+}
+
+// bit e of a 128-bit expert mask (word chosen by selects: no local memory)
+__device__ __forceinline__ uint32_t routes(const uint32_t (&m)[4], int e) {
+    const uint32_t w = e < 64 ? (e < 32 ? m[0] : m[1]) : (e < 96 ? m[2] : m[3]);
+    return (w >> (e & 31)) & 1u;
+}
+
+__device__ __forceinline__ float silu_f(float z) { return __fdividef(z, 1.0f + __expf(-z)); }
+
+// order-preserving map of fp32 to uint32 (-0.0 canonicalised to +0.0)
+__device__ __forceinline__ uint32_t okey(float x) {
+    const uint32_t b = __float_as_uint(x + 0.0f);
+    return b ^ ((uint32_t)((int32_t)b >> 31) | 0x80000000u);
+}
+
+template <int N>
+__device__ __forceinline__ void bitonic_sort(uint32_t (&v)[N]) {
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const uint32_t a = v[i], b = v[l];
+                    const bool up = (i & k) == 0;
+                    v[i] = up ? min(a, b) : max(a, b);
+                    v[l] = up ? max(a, b) : min(a, b);
+                }
+            }
+}
+
+// The tile / job order shared by the producer, the MMA issuer and the
+// epilogue groups: the k-th tile pair of CTA b is tiles (k * G + b) * 2 + g,
+// g = epilogue group; jobs interleave g0, g1 per job index.
+struct Job {
+    int g;
+    int64_t tile;
+    int j;   // 0..P1-1 layer-1 passes, P1 layer 2, P1 + 1 layer 3
+};
+
+template <int E>
+__global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__ Params P) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t *abuf0 = smem;                         // group 0 A operand (96 KB)
+    uint8_t *wring = smem + 2 * A_BYTES;           // weight ring
+    uint64_t *bars = (uint64_t *)(wring + W_STAGES * W_STAGE);
+    uint64_t *w_full = bars, *w_empty = bars + W_STAGES;
+    uint64_t *feat_ready = bars + 2 * W_STAGES, *acc_ready = feat_ready + 2;
+    uint32_t *tmem_slot = (uint32_t *)(acc_ready + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int P1 = P.P1, JOBS = P1 + 2;
+    const int64_t G = gridDim.x, b = blockIdx.x;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < W_STAGES; ++s) { mbar_init(&w_full[s], 1); mbar_init(&w_empty[s], 1); }
+        for (int g = 0; g < 2; ++g) { mbar_init(&feat_ready[g], 128); mbar_init(&acc_ready[g], 1); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    const int64_t T = P.tr.T;
+    const int L = P.tr.L;
+    auto net_of_tile = [&](int64_t t) -> int {
+        const int64_t c = t / P.tpc;
+        return P.num_nets == 1 ? 0 : (int)(c % L);
+    };
+    auto job_kblocks = [&](int j) -> int { return j < P1 ? min(2, P.KB1 - 2 * j) : 2; };
+    auto job_n = [&](int j) -> int { return j == P1 + 1 ? P.N3 : H; };
+    // weight block (layer of job j, global K block, part) of a net
+    auto wblock = [&](int net, int j, int kbl, int part) -> const uint8_t * {
+        const uint8_t *base = P.wimg + (int64_t)net * P.net_bytes;
+        if (j < P1) return base + (int64_t)((2 * j + kbl) * 3 + part) * KBLK;
+        base += (int64_t)P.KB1 * 3 * KBLK;
+        if (j == P1) return base + (int64_t)(kbl * 3 + part) * KBLK;
+        base += (int64_t)2 * 3 * KBLK;
+        return base + (int64_t)(kbl * 3 + part) * P.N3 * ROWB;
+    };
+
+    if (warp == 0) {
+        // ---------------------------------------------------- weight producer
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (int64_t k = 0;; ++k) {
+                const int64_t t0 = (k * G + b) * 2;
+                if (t0 >= P.n_tiles) break;
+                for (int j = 0; j < JOBS; ++j)
+                    for (int g = 0; g < 2; ++g) {
+                        const int64_t t = t0 + g;
+                        if (t >= P.n_tiles) continue;
+                        const int net = net_of_tile(t), nkb = job_kblocks(j);
+                        const uint32_t bytes = (uint32_t)job_n(j) * ROWB;
+                        for (int kbl = 0; kbl < nkb; ++kbl)
+                            for (int part = 0; part < 3; ++part, ++it) {
+                                const int s = it % W_STAGES;
+                                mbar_wait(&w_empty[s], ((it / W_STAGES) & 1) ^ 1);
+                                mbar_arrive_expect_tx(&w_full[s], bytes);
+                                bulk_g2s(wring + s * W_STAGE, wblock(net, j, kbl, part), bytes, &w_full[s]);
+                            }
+                    }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            uint32_t it = 0, fr[2] = {0u, 0u};
+            for (int64_t k = 0;; ++k) {
+                const int64_t t0 = (k * G + b) * 2;
+                if (t0 >= P.n_tiles) break;
+                for (int j = 0; j < JOBS; ++j)
+                    for (int g = 0; g < 2; ++g) {
+                        const int64_t t = t0 + g;
+                        if (t >= P.n_tiles) continue;
+                        mbar_wait(&feat_ready[g], fr[g] & 1);
+                        ++fr[g];
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        const uint32_t d_hi = tmem + (uint32_t)(256 * g), d_lo = d_hi + 128;
+                        const uint32_t id = idesc(job_n(j));
+                        const uint32_t a_base = smem_u32(abuf0 + g * A_BYTES);
+                        bool fresh_hi = !(j > 0 && j < P1), fresh_lo = fresh_hi;   // layer-1 passes > 0 accumulate
+                        const int nkb = job_kblocks(j);
+                        for (int kbl = 0; kbl < nkb; ++kbl)
+                            for (int part = 0; part < 3; ++part, ++it) {
+                                const int s = it % W_STAGES;
+                                mbar_wait(&w_full[s], (it / W_STAGES) & 1);
+                                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                                const uint32_t w_base = smem_u32(wring + s * W_STAGE);
+                                for (int ap = 0; ap + part <= 2; ++ap) {
+                                    const bool hi = ap == 0 && part == 0;
+                                    const uint32_t a0 = a_base + ap * A_PART + kbl * KBLK;
+#pragma unroll
+                                    for (int k4 = 0; k4 < 4; ++k4) {
+                                        const bool fresh = hi ? fresh_hi : fresh_lo;
+                                        mma_bf16(hi ? d_hi : d_lo, make_desc(a0 + k4 * 32), make_desc(w_base + k4 * 32),
+                                                 id, fresh ? 0u : 1u);
+                                        if (hi) fresh_hi = false; else fresh_lo = false;
+                                    }
+                                }
+                                mma_commit(&w_empty[s]);
+                            }
+                        mma_commit(&acc_ready[g]);
+                    }
+            }
+        }
+    } else {
+        // ---------------------------------------------------- epilogue groups
+        const int g = (warp - 2) >> 2;
+        const int q = warp & 3;                 // TMEM lane quarter of this warp
+        const int row = q * 32 + lane;          // event row of the tile = TMEM lane
+        uint8_t *abuf = abuf0 + g * A_BYTES;
+        const uint32_t t_hi = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(256 * g), t_lo = t_hi + 128;
+        const int SN = 2 * E + 4;
+        constexpr int EP = E <= 8 ? 8 : E <= 16 ? 16 : E <= 32 ? 32 : E <= 64 ? 64 : 128;   // sort width
+        constexpr int IDB = EP == 8 ? 3 : EP == 16 ? 4 : EP == 32 ? 5 : EP == 64 ? 6 : 7;   // id bits in a key
+        constexpr int SROW = E + 1;             // fp32 score staging row (words; odd: conflict-free columns)
+        uint32_t ar = 0;
+        for (int64_t k = 0;; ++k) {
+            const int64_t t = (k * G + b) * 2 + g;
+            if (t >= P.n_tiles) break;
+            const int64_t c = t / P.tpc, ev0 = (t % P.tpc) * BM, ev = ev0 + row;
+            const bool valid = ev < T;
+            const int net = P.num_nets == 1 ? 0 : (int)(c % L);
+            // this event's routed experts as a 128-bit mask
+            uint32_t mine[4] = {0u, 0u, 0u, 0u};
+            if (valid) {
+                const uint8_t *ids = P.tr.acc + (c * T + ev) * P.tr.K;
+                for (int kk = 0; kk < P.tr.K; ++kk) {
+                    const int x = __ldg(ids + kk);
+                    mine[x >> 5] |= 1u << (x & 31);
+                }
+            }
+            // tracker snapshot at the start of this warp's 32-event sub-tile
+            const int64_t s32 = (ev0 >> 5) + q;
+            const bool has_snap = s32 < P.tpc32;
+            const int32_t *sp = P.snaps + (c * P.tpc32 + (has_snap ? s32 : 0)) * SN;
+            const int32_t u0 = (int32_t)(s32 * 32);
+            const uint32_t upto = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);
+            // max_f over experts at this event (features.py:44-52)
+            int32_t maxf = 0;
+#pragma unroll 4
+            for (int e = 0; e < E; ++e) {
+                const uint32_t m = __ballot_sync(0xFFFFFFFFu, routes(mine, e));
+                const int32_t f = (has_snap ? __ldg(sp + E + e) : 0) + __popc(m & upto);
+                maxf = max(maxf, f);
+            }
+            named_sync(1 + g, 128);   // every thread is done with the previous tile's staging rows
+            // ---- layer-1 input: [1/r || f / max_f] (K = 2E, zero padded), P1 passes of 128
+            for (int p = 0; p < P1; ++p) {
+                if (p > 0) {   // the previous pass's MMAs have consumed the A buffer
+                    mbar_wait(&acc_ready[g], ar & 1);
+                    ++ar;
+                }
+                for (int k0 = 128 * p; k0 < 128 * p + 128; k0 += 8) {
+                    float v[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int kx = k0 + i;
+                        float val = 0.0f;
+                        if (kx < 2 * E) {
+                            const int e = kx < E ? kx : kx - E;
+                            const uint32_t m = __ballot_sync(0xFFFFFFFFu, routes(mine, e));
+                            const uint32_t seen = m & upto;
+                            if (kx < E) {
+                                const int32_t lastu = seen ? u0 + (31 - __clz(seen)) + 1
+                                                           : (has_snap ? __ldg(sp + e) : -1);
+                                const int32_t u = u0 + lane + 1;
+                                val = lastu < 0 ? 0.0f : 1.0f / (float)(u - lastu + 1);
+                            } else {
+                                const int32_t f = (has_snap ? __ldg(sp + E + e) : 0) + __popc(seen);
+                                val = maxf > 0 ? (float)f / (float)maxf : 0.0f;
+                            }
+                        }
+                        v[i] = val;
+                    }
+                    store_chunk8(abuf, row, k0 - 128 * p, v);
+                }
+                fence_async_smem();
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mbar_arrive(&feat_ready[g]);
+            }
+            // ---- hidden layers: h = silu(acc_hi + acc_lo + bias) -> next A operand
+            for (int layer = 0; layer < 2; ++layer) {
+                mbar_wait(&acc_ready[g], ar & 1);
+                ++ar;
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const float *bias = P.bias + (int64_t)net * P.bias_stride + layer * H;
+#pragma unroll 1
+                for (int c0 = 0; c0 < H; c0 += 32) {
+                    uint32_t rh[32], rl[32];
+                    tmem_ld32_nowait(t_hi + c0, rh);
+                    tmem_ld32_nowait(t_lo + c0, rl);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c8 = 0; c8 < 32; c8 += 8) {
+                        float v[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const float z = (__uint_as_float(rh[c8 + i]) + __uint_as_float(rl[c8 + i])) +
+                                            __ldg(bias + c0 + c8 + i);
+                            v[i] = silu_f(z);
+                        }
+                        store_chunk8(abuf, row, c0 + c8, v);
+                    }
+                }
+                fence_async_smem();
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mbar_arrive(&feat_ready[g]);
+            }
+            // ---- scores: s = acc_hi + acc_lo + b3, then ranks
+            mbar_wait(&acc_ready[g], ar & 1);
+            ++ar;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            float *srow = (float *)abuf + row * SROW;       // the A buffer is free now
+            const float *b3 = P.bias + (int64_t)net * P.bias_stride + 2 * H;
+            uint32_t key[EP];
+            bool bad = false;
+#pragma unroll
+            for (int c0 = 0; c0 < EP; c0 += 32) {
+                if (c0 >= E) break;
+                uint32_t rh[32], rl[32];
+                tmem_ld32_nowait(t_hi + c0, rh);
+                tmem_ld32_nowait(t_lo + c0, rl);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int e = c0 + i;
+                    if (e < EP) {
+                        if (e < E) {
+                            const float s = (__uint_as_float(rh[i]) + __uint_as_float(rl[i])) + __ldg(b3 + e);
+                            bad |= !isfinite(s);
+                            srow[e] = s;
+                            key[e] = (okey(s) & ~((1u << IDB) - 1u)) | (uint32_t)e;
+                        } else {
+                            key[e] = 0xFFFFFFFFu;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int e = E; e < EP; ++e) key[e] = 0xFFFFFFFFu;
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            bitonic_sort<EP>(key);
+            // certify: adjacent scores apart by more than 2 tau max|s|, no
+            // truncated-key collision (then the sorted order is the exact order)
+            const float smin = srow[key[0] & ((1u << IDB) - 1u)], smax = srow[key[E - 1] & ((1u << IDB) - 1u)];
+            const float thr = 2.0f * P.tau * fmaxf(fabsf(smin), fabsf(smax));
+            uint8_t *rrow = (uint8_t *)((float *)abuf + BM * SROW) + row * (E + 16);
+            float prev = smin;
+#pragma unroll
+            for (int n = 0; n < E; ++n) {
+                const int id = (int)(key[n] & ((1u << IDB) - 1u));
+                if (n > 0) {
+                    const float cur = srow[id];
+                    bad |= ((key[n] ^ key[n - 1]) >> IDB) == 0u;
+                    bad |= !(cur - prev > thr);
+                    prev = cur;
+                }
+                rrow[id] = (uint8_t)(n + 1);
+            }
+            if (valid && P.dbg_scores) {
+                float *ds = P.dbg_scores + (c * T + ev) * E;
+                for (int e = 0; e < E; ++e) ds[e] = srow[e];
+            }
+            if (valid) {
+                uint8_t *dst = P.ranks + (c * T + ev) * E;
+                if constexpr (E % 16 == 0) {
+#pragma unroll
+                    for (int i = 0; i < E; i += 16) *(uint4 *)(dst + i) = *(const uint4 *)(rrow + i);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < E; i += 8) *(uint2 *)(dst + i) = *(const uint2 *)(rrow + i);
+                }
+                if (bad) {
+                    const int slot = atomicAdd(P.flag_cnt + net, 1);
+                    P.flag_list[(int64_t)net * P.bucket_cap + slot] = (int32_t)(c * T + ev);
+                }
+            }
+            const unsigned nb = __popc(__ballot_sync(0xFFFFFFFFu, valid && bad));
+            if (lane == 0 && nb) atomicAdd(P.stats + 5, (unsigned long long)nb);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+// Weight images: per net, the bf16 x 3 parts of W1 (N = 128, K = 2E padded to
+// a multiple of 64), W2 (128 x 128) and W3 (N3 x 128), as [N x 64] blocks in
+// the SWIZZLE_128B K-major layout in MMA consumption order (layer, K block,
+// part), and fp32 biases b1, b2, b3 (padded to N3).  params: .evnet order.
+__global__ void k_prep_tc(const double *__restrict__ params, int E, int num_nets, int KB1, int N3,
+                          int64_t net_bytes, uint8_t *__restrict__ wimg, float *__restrict__ bias, int bias_stride) {
+    const int D = 2 * E;
+    const int64_t src_per = (int64_t)D * H + H + (int64_t)H * H + H + (int64_t)E * H + E;
+    // one thread per (net, layer, row n, 8-wide K chunk)
+    const int64_t per_net_chunks = (int64_t)H * (KB1 * 8) + (int64_t)H * 16 + (int64_t)N3 * 16;
+    const int64_t total = per_net_chunks * num_nets;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int net = (int)(i / per_net_chunks);
+        int64_t r = i % per_net_chunks;
+        const double *src = params + net * src_per;
+        const double *w;
+        int n, ch, ldw, kmax, nmax, layer;
+        if (r < (int64_t)H * KB1 * 8) {
+            layer = 0; n = (int)(r / (KB1 * 8)); ch = (int)(r % (KB1 * 8)); w = src; ldw = D; kmax = D; nmax = H;
+        } else if ((r -= (int64_t)H * KB1 * 8) < (int64_t)H * 16) {
+            layer = 1; n = (int)(r / 16); ch = (int)(r % 16); w = src + (int64_t)D * H + H; ldw = H; kmax = H; nmax = H;
+        } else {
+            r -= (int64_t)H * 16;
+            layer = 2; n = (int)(r / 16); ch = (int)(r % 16);
+            w = src + (int64_t)D * H + H + (int64_t)H * H + H; ldw = H; kmax = H; nmax = E;
+        }
+        const int kb = ch >> 3, c8 = ch & 7, Nl = layer == 2 ? N3 : H;
+        uint32_t part[3][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint16_t h[3][2];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const int kk = kb * 64 + c8 * 8 + 2 * j + hh;
+                const double x = (n < nmax && kk < kmax) ? w[(int64_t)n * ldw + kk] : 0.0;
+                const __nv_bfloat16 p0 = __double2bfloat16(x);
+                const double r1 = x - (double)__bfloat162float(p0);
+                const __nv_bfloat16 p1 = __double2bfloat16(r1);
+                const double r2 = r1 - (double)__bfloat162float(p1);
+                const __nv_bfloat16 p2 = __double2bfloat16(r2);
+                h[0][hh] = __bfloat16_as_ushort(p0);
+                h[1][hh] = __bfloat16_as_ushort(p1);
+                h[2][hh] = __bfloat16_as_ushort(p2);
+            }
+#pragma unroll
+            for (int p = 0; p < 3; ++p) part[p][j] = (uint32_t)h[p][0] | ((uint32_t)h[p][1] << 16);
+        }
+        uint8_t *base = wimg + (int64_t)net * net_bytes;
+        int64_t blk0;
+        if (layer == 0) blk0 = (int64_t)(kb * 3) * KBLK;
+        else if (layer == 1) blk0 = (int64_t)KB1 * 3 * KBLK + (int64_t)(kb * 3) * KBLK;
+        else blk0 = (int64_t)(KB1 + 2) * 3 * KBLK + (int64_t)(kb * 3) * N3 * ROWB;
+        const int64_t blk_bytes = (int64_t)Nl * ROWB;
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+            *(uint4 *)(base + blk0 + p * blk_bytes + sw128(n, c8)) =
+                make_uint4(part[p][0], part[p][1], part[p][2], part[p][3]);
+        if (ch == 0) {   // biases (fp32)
+            float *bb = bias + (int64_t)net * bias_stride;
+            const double *b1 = src + (int64_t)D * H, *b2 = b1 + H + (int64_t)H * H,
+                         *b3 = b2 + H + (int64_t)E * H;
+            if (layer == 0) bb[n] = (float)b1[n];
+            else if (layer == 1) bb[H + n] = (float)b2[n];
+            else bb[2 * H + n] = n < E ? (float)b3[n] : 0.0f;
+        }
+    }
+}
+
+}  // namespace k3tc
+
+size_t score_tc_net_bytes(int E) {
+    const int KB1 = (2 * E + 63) / 64, N3 = (E + 15) / 16 * 16;
+    return (size_t)(KB1 + 2) * 3 * k3tc::KBLK + (size_t)2 * 3 * N3 * k3tc::ROWB;
+}
+int score_tc_bias_stride(int E) { return 2 * k3tc::H + (E + 15) / 16 * 16; }
+
+bool score_tc_eligible(const DevTrace &tr, int H) {
+    return tr.uniform && H == k3tc::H && (tr.E == 8 || tr.E == 16 || tr.E == 32 || tr.E == 64 || tr.E == 128) &&
+           tr.total_events < (1ll << 31);
+}
+
+static int g_num_sms = 0;
+
+int preload_score_tc() {
+    const void *fns[] = {(const void *)k3tc::k_score_tc<8>, (const void *)k3tc::k_score_tc<16>,
+                         (const void *)k3tc::k_score_tc<32>, (const void *)k3tc::k_score_tc<64>,
+                         (const void *)k3tc::k_score_tc<128>};
+    for (const void *f : fns)
+        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, k3tc::SMEM_BYTES) != cudaSuccess)
+            return -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    return 0;
+}
+
+// Launches: weight images, then the tensor-core scorer over every 128-event
+// tile (ranks + flag lists).  snaps: K3 snapshots (launch_score_prep).
+int launch_score_tc(const DevTrace &tr, const double *params, int num_nets, const int32_t *snaps, uint8_t *wimg,
+                    float *bias, uint8_t *ranks, float tau, int32_t *flag_cnt, int32_t *flag_list, int64_t bucket_cap,
+                    unsigned long long *stats, float *dbg_scores, cudaStream_t s) {
+    using namespace k3tc;
+    const int E = tr.E;
+    const int KB1 = (2 * E + 63) / 64, N3 = (E + 15) / 16 * 16;
+    const int64_t net_bytes = (int64_t)score_tc_net_bytes(E);
+    const int bstride = score_tc_bias_stride(E);
+    {
+        const int64_t chunks = ((int64_t)H * KB1 * 8 + (int64_t)H * 16 + (int64_t)N3 * 16) * num_nets;
+        const unsigned blocks = (unsigned)std::min<int64_t>((chunks + 255) / 256, 4096);
+        k_prep_tc<<<blocks, 256, 0, s>>>(params, E, num_nets, KB1, N3, net_bytes, wimg, bias, bstride);
+    }
+    cudaMemsetAsync(flag_cnt, 0, sizeof(int32_t) * num_nets, s);
+    Params P;
+    P.tr = tr;
+    P.wimg = wimg;
+    P.net_bytes = net_bytes;
+    P.bias = bias;
+    P.bias_stride = bstride;
+    P.num_nets = num_nets;
+    P.N3 = N3;
+    P.KB1 = KB1;
+    P.P1 = (KB1 + 1) / 2;
+    P.tpc = (tr.T + BM - 1) / BM;
+    P.tpc32 = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
+    P.n_tiles = tr.n_chains * P.tpc;
+    P.snaps = snaps;
+    P.ranks = ranks;
+    P.tau = tau;
+    P.flag_cnt = flag_cnt;
+    P.flag_list = flag_list;
+    P.bucket_cap = bucket_cap;
+    P.stats = stats;
+    P.dbg_scores = dbg_scores;
+    if (P.n_tiles == 0) return 2;
+    const int sms = g_num_sms > 0 ? g_num_sms : 148;
+    const unsigned grid = (unsigned)std::min<int64_t>(sms, (P.n_tiles + 1) / 2);
+    switch (E) {
+        case 8: k_score_tc<8><<<grid, THREADS, SMEM_BYTES, s>>>(P); break;
+        case 16: k_score_tc<16><<<grid, THREADS, SMEM_BYTES, s>>>(P); break;
+        case 32: k_score_tc<32><<<grid, THREADS, SMEM_BYTES, s>>>(P); break;
+        case 64: k_score_tc<64><<<grid, THREADS, SMEM_BYTES, s>>>(P); break;
+        default: k_score_tc<128><<<grid, THREADS, SMEM_BYTES, s>>>(P); break;
+    }
+    return 2;
+}
