@@ -318,12 +318,18 @@ int mcb_pack_decode_ids(mcb_ctx *ctx, const uint8_t *ids, int64_t num_traces, in
  * 1 decode), step, layer, CSR experts.  Validates exactly what
  * RoutingTrace.validate() checks (MCB_ERR_INVALID + message on failure) and
  * produces an owned packed trace (uniform layout when the trace is
- * decode-only with one sequence). */
+ * decode-only with one sequence); num_experts > 128 is MCB_ERR_UNSUPPORTED
+ * (after validation). */
 typedef struct mcb_packed mcb_packed;
 int mcb_pack_trace(int32_t num_layers, int32_t num_experts, int32_t top_k, int64_t num_events,
                    const int64_t *seq_id, const uint8_t *phase, const int64_t *step,
                    const int32_t *layer, const int64_t *expert_off, const int32_t *experts,
                    mcb_packed **out);
+/* Validation only (RoutingTrace.validate, trace.py:115-137, with the
+ * reference's messages): no engine limits, nothing allocated. */
+int mcb_validate_trace(int32_t num_layers, int32_t num_experts, int32_t top_k, int64_t num_events,
+                       const int64_t *seq_id, const uint8_t *phase, const int64_t *step, const int32_t *layer,
+                       const int64_t *expert_off, const int32_t *experts);
 /* Host view of a packed trace, sizes, and num_decode_steps() (trace.py:139-141). */
 int mcb_packed_view(const mcb_packed *p, mcb_trace *view, int64_t *total_acc, int64_t *total_events,
                     int64_t *total_routed, int64_t *num_decode_steps);

@@ -46,7 +46,7 @@ OUT_HIT, OUT_MISS = 0xFFFF, 0xFFFE
 EXPORTED_SYMBOLS = (
     "mcb_abi_version", "mcb_ctx_create", "mcb_ctx_destroy", "mcb_last_error", "mcb_last_stats",
     "mcb_set_timing", "mcb_last_timings", "mcb_set_tuning", "mcb_read_stats",
-    "mcb_pack_trace", "mcb_packed_view", "mcb_packed_positions", "mcb_packed_free",
+    "mcb_pack_trace", "mcb_validate_trace", "mcb_packed_view", "mcb_packed_positions", "mcb_packed_free",
     "mcb_replay", "mcb_replay_host", "mcb_next_use", "mcb_score", "mcb_router_topk", "mcb_gen_reference",
     "mcb_gen_reference_batch", "mcb_score_tc_scores",
     "mcb_training_data", "mcb_set_lecar", "mcb_lecar_random", "mcb_pack_decode_ids",
@@ -143,6 +143,7 @@ def load_library():
             "mcb_last_error": ([ctypes.c_char_p, ctypes.c_size_t], ctypes.c_int),
             "mcb_last_stats": ([P, P, P], ctypes.c_int),
             "mcb_pack_trace": ([i32, i32, i32, i64, P, P, P, P, P, P, P], ctypes.c_int),
+            "mcb_validate_trace": ([i32, i32, i32, i64, P, P, P, P, P, P], ctypes.c_int),
             "mcb_packed_view": ([P, P, P, P, P, P], ctypes.c_int),
             "mcb_packed_positions": ([P, i64, P, P], ctypes.c_int),
             "mcb_packed_free": ([P], ctypes.c_int),

@@ -32,40 +32,38 @@ int fail(const std::string &msg) { return mcb_set_error(MCB_ERR_INVALID, msg.c_s
 
 }  // namespace
 
-extern "C" int mcb_pack_trace(int32_t L, int32_t E, int32_t K, int64_t n, const int64_t *seq,
-                              const uint8_t *phase, const int64_t *step, const int32_t *layer,
-                              const int64_t *off, const int32_t *experts, mcb_packed **out) {
-    mcb_clear_error();
-    if (!out) return mcb_set_error(MCB_ERR_INVALID, "out is NULL");
-    *out = nullptr;
-    // TraceHeader.validate (trace.py:57-66)
+// RoutingTrace.validate (trace.py:115-137) with TraceHeader.validate and
+// AccessEvent.validate (trace.py:57-107): the same checks, the same order of
+// reporting (every event's own checks and the ordering first, the
+// decode-step completeness last) and the same messages.  No engine limits
+// (num_experts may exceed 128 here).  Outputs the trace's shape.
+static int validate_events(int32_t L, int32_t E, int32_t K, int64_t n, const int64_t *seq, const uint8_t *phase,
+                           const int64_t *step, const int32_t *layer, const int64_t *off, const int32_t *experts,
+                           int64_t *decode_steps_out, bool *decode_only_out, bool *single_seq_out) {
     if (L < 1) return fail("num_layers must be >= 1, got " + std::to_string(L));
     if (E < 1) return fail("num_experts must be >= 1, got " + std::to_string(E));
     if (K < 1 || K > E)
         return fail("top_k must satisfy 1 <= top_k <= num_experts, got top_k=" + std::to_string(K) +
                     " with num_experts=" + std::to_string(E));
-    if (E > MCB_MAX_EXPERTS)
-        return mcb_set_error(MCB_ERR_UNSUPPORTED, "num_experts > 128 is not supported by the B200 engine");
     if (n > 0 && (!seq || !phase || !step || !layer || !off || !experts))
         return mcb_set_error(MCB_ERR_INVALID, "NULL event array");
-
     std::vector<uint8_t> mark(E, 0);
+    std::vector<uint8_t> present(L, 0);
     bool decode_only = true, single_seq = true;
-    int64_t grp_seq = -1, grp_step = -1;
-    int64_t grp_count = 0;
+    int64_t grp_seq = -1, grp_step = -1, grp_count = 0;
     bool in_grp = false;
-    auto close_group = [&]() -> int {
-        if (in_grp && grp_count != L) {
-            // layers strictly increase inside a (seq, step) decode group, so a
-            // short group means some layer is missing (trace.py:128-137)
-            return fail("decode step (seq " + std::to_string(grp_seq) + ", step " +
-                        std::to_string(grp_step) + ") missing events for some layers");
+    std::string missing_msg;   // the first incomplete decode step, reported after every event checked
+    auto close_group = [&]() {
+        if (in_grp && grp_count != L && missing_msg.empty()) {
+            std::string m;
+            for (int32_t l = 0; l < L; ++l)
+                if (!present[l]) m += (m.empty() ? "" : ", ") + std::to_string(l);
+            missing_msg = "decode step (seq " + std::to_string(grp_seq) + ", step " + std::to_string(grp_step) +
+                          ") missing events for layers [" + m + "]";
         }
-        return MCB_OK;
     };
     int64_t decode_steps = 0;
     for (int64_t i = 0; i < n; ++i) {
-        // AccessEvent.validate (trace.py:80-107)
         if (seq[i] < 0) return fail("seq_id must be >= 0, got " + std::to_string(seq[i]));
         if (step[i] < 0) return fail("step must be >= 0, got " + std::to_string(step[i]));
         if (layer[i] < 0 || layer[i] >= L)
@@ -73,19 +71,27 @@ extern "C" int mcb_pack_trace(int32_t L, int32_t E, int32_t K, int64_t n, const 
         if (phase[i] > 1) return fail("phase must be 0 (prefill) or 1 (decode)");
         const int64_t len = off[i + 1] - off[i];
         if (len < 0) return fail("negative expert count");
+        // duplicates (set(experts) smaller than the list), any value
         bool dup = false;
-        for (int64_t j = 0; j < len; ++j) {
+        for (int64_t j = 0; j < len && !dup; ++j) {
             const int32_t e = experts[off[i] + j];
             if (e >= 0 && e < E) {
                 if (mark[e]) dup = true;
                 mark[e] = 1;
+            } else {
+                for (int64_t jj = 0; jj < j; ++jj)
+                    if (experts[off[i] + jj] == e) dup = true;
             }
         }
         for (int64_t j = 0; j < len; ++j) {
             const int32_t e = experts[off[i] + j];
             if (e >= 0 && e < E) mark[e] = 0;
         }
-        if (dup) return fail("experts contain duplicates");
+        if (dup) {
+            std::string m;
+            for (int64_t j = 0; j < len; ++j) m += (j ? ", " : "") + std::to_string(experts[off[i] + j]);
+            return fail("experts contain duplicates: [" + m + "]");
+        }
         for (int64_t j = 0; j < len; ++j) {
             const int32_t e = experts[off[i] + j];
             if (e < 0 || e >= E)
@@ -99,8 +105,7 @@ extern "C" int mcb_pack_trace(int32_t L, int32_t E, int32_t K, int64_t n, const 
             return fail("prefill event must route between 1 and " + std::to_string(E) + " experts, got " +
                         std::to_string(len));
         }
-        // strict (seq, phase, step, layer) order (trace.py:121-127)
-        if (i > 0) {
+        if (i > 0) {   // strict (seq, phase, step, layer) order
             const int64_t a[4] = {seq[i - 1], phase[i - 1], step[i - 1], layer[i - 1]};
             const int64_t b[4] = {seq[i], phase[i], step[i], layer[i]};
             if (!std::lexicographical_compare(a, a + 4, b, b + 4))
@@ -110,20 +115,51 @@ extern "C" int mcb_pack_trace(int32_t L, int32_t E, int32_t K, int64_t n, const 
         }
         if (phase[i] == 1) {
             if (!in_grp || grp_seq != seq[i] || grp_step != step[i]) {
-                if (int rc = close_group()) return rc;
+                close_group();
                 in_grp = true;
                 grp_seq = seq[i];
                 grp_step = step[i];
                 grp_count = 0;
+                std::fill(present.begin(), present.end(), 0);
                 ++decode_steps;  // num_decode_steps (trace.py:139-141): distinct (seq, step)
             }
             ++grp_count;
+            present[layer[i]] = 1;
         } else {
             decode_only = false;
         }
         if (seq[i] != seq[0]) single_seq = false;
     }
-    if (int rc = close_group()) return rc;
+    close_group();
+    if (!missing_msg.empty()) return fail(missing_msg);
+    *decode_steps_out = decode_steps;
+    *decode_only_out = decode_only;
+    *single_seq_out = single_seq;
+    return MCB_OK;
+}
+
+extern "C" int mcb_validate_trace(int32_t L, int32_t E, int32_t K, int64_t n, const int64_t *seq,
+                                  const uint8_t *phase, const int64_t *step, const int32_t *layer,
+                                  const int64_t *off, const int32_t *experts) {
+    mcb_clear_error();
+    int64_t d;
+    bool a, b;
+    return validate_events(L, E, K, n, seq, phase, step, layer, off, experts, &d, &a, &b);
+}
+
+extern "C" int mcb_pack_trace(int32_t L, int32_t E, int32_t K, int64_t n, const int64_t *seq,
+                              const uint8_t *phase, const int64_t *step, const int32_t *layer,
+                              const int64_t *off, const int32_t *experts, mcb_packed **out) {
+    mcb_clear_error();
+    if (!out) return mcb_set_error(MCB_ERR_INVALID, "out is NULL");
+    *out = nullptr;
+    int64_t decode_steps = 0;
+    bool decode_only = true, single_seq = true;
+    if (int rc = validate_events(L, E, K, n, seq, phase, step, layer, off, experts, &decode_steps, &decode_only,
+                                 &single_seq))
+        return rc;
+    if (E > MCB_MAX_EXPERTS)
+        return mcb_set_error(MCB_ERR_UNSUPPORTED, "num_experts > 128 is not supported by the B200 engine");
 
     auto *p = new (std::nothrow) mcb_packed();
     if (!p) return mcb_set_error(MCB_ERR_NOMEM, "out of host memory");

@@ -78,6 +78,27 @@ class AccessEvent:
     def sort_key(self) -> tuple:
         return (self.seq_id, int(self.phase), self.step, self.layer)
 
+    def validate(self, header: TraceHeader) -> None:
+        """AccessEvent.validate (trace.py:80-106): the same checks, order and messages."""
+        if self.seq_id < 0:
+            raise InvalidConfigError(f"seq_id must be >= 0, got {self.seq_id}")
+        if self.step < 0:
+            raise InvalidConfigError(f"step must be >= 0, got {self.step}")
+        if not 0 <= self.layer < header.num_layers:
+            raise InvalidConfigError(f"layer {self.layer} out of range [0, {header.num_layers})")
+        if len(set(self.experts)) != len(self.experts):
+            raise InvalidConfigError(f"experts contain duplicates: {list(self.experts)}")
+        for e in self.experts:
+            if not 0 <= e < header.num_experts:
+                raise InvalidConfigError(f"expert {e} out of range [0, {header.num_experts})")
+        if self.phase == Phase.DECODE:
+            if len(self.experts) != header.top_k:
+                raise InvalidConfigError(f"decode event must route exactly top_k={header.top_k} experts, "
+                                         f"got {len(self.experts)}")
+        elif not 1 <= len(self.experts) <= header.num_experts:
+            raise InvalidConfigError(f"prefill event must route between 1 and {header.num_experts} "
+                                     f"experts, got {len(self.experts)}")
+
 
 @dataclass(frozen=True)
 class RoutingTrace:
@@ -85,8 +106,11 @@ class RoutingTrace:
     events: tuple
 
     def validate(self) -> None:
-        """RoutingTrace.validate (trace.py:115-137), executed natively."""
-        pack_trace(self).free()
+        """RoutingTrace.validate (trace.py:115-137), executed natively
+        (mcb_validate_trace): the reference's checks and messages, no engine
+        limits -- a 160-expert trace the reference accepts validates here too;
+        only replaying it is refused (num_experts > 128)."""
+        validate_trace(self)
 
     def num_decode_steps(self) -> int:
         return len({(ev.seq_id, ev.step) for ev in self.events if ev.phase == Phase.DECODE})
@@ -197,6 +221,16 @@ class PackedTrace:
             n = self.events_per_chain * self.top_k
             return self.acc[chain * n:(chain + 1) * n]
         return self.acc[int(self.chain_acc_off[chain]):int(self.chain_acc_off[chain + 1])]
+
+
+def validate_trace(trace) -> None:
+    """RoutingTrace.validate for ours or the reference's trace objects."""
+    h = trace.header
+    seq, phase, step, layer, off, experts = _flatten(trace)
+    rc = _lib.load_library().mcb_validate_trace(int(h.num_layers), int(h.num_experts), int(h.top_k), len(seq),
+                                                _ptr(seq), _ptr(phase), _ptr(step), _ptr(layer), _ptr(off),
+                                                _ptr(experts))
+    _lib.check(rc)
 
 
 def pack_trace(trace) -> PackedTrace:
