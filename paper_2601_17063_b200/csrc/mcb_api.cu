@@ -453,10 +453,12 @@ static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int in
         if (int rc = c->tc_flag_cnt.ensure((size_t)nn * sizeof(int32_t))) return rc;
         if (int rc = c->tc_flag_list.ensure((size_t)(nn * cap + 1) * sizeof(int32_t))) return rc;
         *launched += launch_score_prep(d, include_prefill, (int32_t *)c->snaps.p, (int64_t *)c->tile_off.p, tiles, s);
-        *launched += launch_score_tc(d, nets->params, nn, (const int32_t *)c->snaps.p, (uint8_t *)c->tc_wimg.p,
-                                     (float *)c->tc_bias.p, ranks, (float)(c->k3_tau_ppb * 1e-9),
-                                     (int32_t *)c->tc_flag_cnt.p, (int32_t *)c->tc_flag_list.p, cap,
-                                     (unsigned long long *)c->stats.p, tc_scores, s) - 1;
+        const int n_tc = launch_score_tc(d, nets->params, nn, (const int32_t *)c->snaps.p, (uint8_t *)c->tc_wimg.p,
+                                         (float *)c->tc_bias.p, ranks, (float)(c->k3_tau_ppb * 1e-9),
+                                         (int32_t *)c->tc_flag_cnt.p, (int32_t *)c->tc_flag_list.p, cap,
+                                         (unsigned long long *)c->stats.p, tc_scores, s);
+        if (n_tc < 0) return MCB_ERR_CUDA;
+        *launched += n_tc;
         *launched += launch_rescore(d, (const double *)c->wt.p, H, nn, (const int32_t *)c->snaps.p,
                                     (const int32_t *)c->tc_flag_cnt.p, (const int32_t *)c->tc_flag_list.p, cap, ranks,
                                     (unsigned long long *)c->stats.p, s);

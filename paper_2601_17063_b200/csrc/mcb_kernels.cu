@@ -1830,7 +1830,7 @@ __global__ void __launch_bounds__(256, TE ? 4 : 1) k_score_tile(DevTrace tr, con
 // tile plus the tile's earlier events (features.py:34-52), runs the same
 // float64 MLP and ranking as k_score_tile and overwrites their rank rows.
 template <int TE, int TH>
-__global__ void __launch_bounds__(256, 1) k_rescore(DevTrace tr, const double *__restrict__ wt_all, int H_rt,
+__global__ void __launch_bounds__(256, 3) k_rescore(DevTrace tr, const double *__restrict__ wt_all, int H_rt,
                                                    int num_nets, const int32_t *__restrict__ snaps,
                                                    const int32_t *__restrict__ flag_cnt,
                                                    const int32_t *__restrict__ flag_list, int64_t bucket_cap,
@@ -1880,15 +1880,26 @@ __global__ void __launch_bounds__(256, 1) k_rescore(DevTrace tr, const double *_
                     last[j] = e < E ? sp[e] : -1;
                     f[j] = e < E ? sp[E + e] : 0;
                 }
-                // the tile's events up to and including this one (features.py:34-39)
-                for (int64_t jj = s32 * MCB_TILE_EV; jj <= i; ++jj) {
-                    const uint8_t *ids = tr.acc + (c * tr.T + jj) * tr.K;
+                // the tile's events up to and including this one (features.py:34-39):
+                // lane j loads event s32*32 + j's ids, the walk broadcasts them
+                const int64_t j0 = s32 * MCB_TILE_EV;
+                const int nprefix = (int)(i - j0) + 1;
+                const uint8_t *ids = tr.acc + (c * tr.T + j0 + lane) * tr.K;
+                uint32_t mine[4] = {0u, 0u, 0u, 0u};   // ids of event j0 + lane, packed 4 per word
+                for (int k = 0; k < tr.K; ++k) {
+                    const uint32_t x = lane < nprefix ? (uint32_t)__ldg(ids + k) : 0u;
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) mine[w] |= (k >> 2) == w ? x << (8 * (k & 3)) : 0u;
+                }
+                for (int jj = 0; jj < nprefix; ++jj) {
                     for (int k = 0; k < tr.K; ++k) {
-                        const int x = __ldg(ids + k);
+                        const uint32_t wd = __shfl_sync(FULL_MASK, (k >> 2) == 0 ? mine[0] : (k >> 2) == 1 ? mine[1]
+                                                                     : (k >> 2) == 2 ? mine[2] : mine[3], jj);
+                        const int x = (int)((wd >> (8 * (k & 3))) & 0xFFu);
                         if ((x & 31) == lane) {
 #pragma unroll
                             for (int j = 0; j < 4; ++j)
-                                if ((x >> 5) == j) { last[j] = (int32_t)jj + 1; ++f[j]; }
+                                if ((x >> 5) == j) { last[j] = (int32_t)(j0 + jj) + 1; ++f[j]; }
                         }
                     }
                 }
@@ -2049,7 +2060,7 @@ int launch_rescore(const DevTrace &tr, const double *wt, int H, int num_nets, co
     const size_t smem = score_smem(tr.E, H);
     const rescore_fn fn = rescore_kernel(tr.E, H);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    fn<<<(unsigned)(2 * sms), 256, smem, s>>>(tr, wt, H, num_nets, snaps, flag_cnt, flag_list, bucket_cap, ranks,
+    fn<<<(unsigned)(8 * sms), 256, smem, s>>>(tr, wt, H, num_nets, snaps, flag_cnt, flag_list, bucket_cap, ranks,
                                              uncertain);
     return 1;
 }

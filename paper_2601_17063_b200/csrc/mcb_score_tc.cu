@@ -44,6 +44,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "mcb_kernels.cuh"
 
@@ -57,7 +58,7 @@ constexpr int A_PART = 2 * KBLK;          // one bf16 part of a [128 x 128] oper
 constexpr int A_BYTES = 3 * A_PART;       // three parts: 96 KB per epilogue group
 constexpr int W_STAGE = 128 * ROWB;       // one weight block [<= 128 rows x 64 K]: 16 KB
 constexpr int W_STAGES = 2;
-constexpr int THREADS = 320;
+constexpr int THREADS = 320;       // producer, MMA issuer, 2 epilogue groups x 4 warps
 constexpr int SMEM_BYTES = 2 * A_BYTES + W_STAGES * W_STAGE + 1024 + 256;
 
 struct Params {
@@ -92,6 +93,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
         "r"(parity)
+        : "memory");
+}
+// the same, letting the thread sleep until the phase completes (the producer
+// and the MMA issuer: their polling would steal issue slots from epilogue warps)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000u)
         : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -154,26 +166,25 @@ __host__ __device__ __forceinline__ uint32_t sw128(int row, int ch) {
     return (uint32_t)row * ROWB + ((uint32_t)(ch ^ (row & 7)) << 4);
 }
 
-// a = a0 + a1 + a2 (bf16, round to nearest; each remainder is exact in fp32)
-__device__ __forceinline__ void split3(float a, __nv_bfloat16 &p0, __nv_bfloat16 &p1, __nv_bfloat16 &p2) {
-    p0 = __float2bfloat16_rn(a);
-    const float r1 = a - __bfloat162float(p0);
-    p1 = __float2bfloat16_rn(r1);
-    p2 = __float2bfloat16_rn(r1 - __bfloat162float(p1));
+// (a, b) = (a0 + a1 + a2, b0 + b1 + b2), bf16 parts rounded to nearest, two
+// values per cvt.rn.bf16x2.f32 (each remainder is exact in fp32)
+__device__ __forceinline__ void split3x2(float a, float b, uint32_t &w0, uint32_t &w1, uint32_t &w2) {
+    const __nv_bfloat162 p0 = __floats2bfloat162_rn(a, b);
+    const float2 f0 = __bfloat1622float2(p0);
+    const float ra = a - f0.x, rb = b - f0.y;
+    const __nv_bfloat162 p1 = __floats2bfloat162_rn(ra, rb);
+    const float2 f1 = __bfloat1622float2(p1);
+    const __nv_bfloat162 p2 = __floats2bfloat162_rn(ra - f1.x, rb - f1.y);
+    w0 = *(const uint32_t *)&p0;
+    w1 = *(const uint32_t *)&p1;
+    w2 = *(const uint32_t *)&p2;
 }
 
 // eight consecutive K values of one row -> the three parts' 16-B chunks
 __device__ __forceinline__ void store_chunk8(uint8_t *abuf, int row, int k0, const float (&v)[8]) {
     uint32_t w[3][4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        __nv_bfloat16 a0, a1, a2, b0, b1, b2;
-        split3(v[2 * j], a0, a1, a2);
-        split3(v[2 * j + 1], b0, b1, b2);
-        w[0][j] = (uint32_t)__bfloat16_as_ushort(a0) | ((uint32_t)__bfloat16_as_ushort(b0) << 16);
-        w[1][j] = (uint32_t)__bfloat16_as_ushort(a1) | ((uint32_t)__bfloat16_as_ushort(b1) << 16);
-        w[2][j] = (uint32_t)__bfloat16_as_ushort(a2) | ((uint32_t)__bfloat16_as_ushort(b2) << 16);
-    }
+    for (int j = 0; j < 4; ++j) split3x2(v[2 * j], v[2 * j + 1], w[0][j], w[1][j], w[2][j]);
     const uint32_t off = (uint32_t)(k0 >> 6) * KBLK + sw128(row, (k0 & 63) >> 3);
 #pragma unroll
     for (int p = 0; p < 3; ++p)
@@ -184,6 +195,14 @@ __device__ __forceinline__ void store_chunk8(uint8_t *abuf, int row, int k0, con
 __device__ __forceinline__ uint32_t routes(const uint32_t (&m)[4], int e) {
     const uint32_t w = e < 64 ? (e < 32 ? m[0] : m[1]) : (e < 96 ? m[2] : m[3]);
     return (w >> (e & 31)) & 1u;
+}
+
+// a[w] without dynamic register indexing (w < N <= 4)
+template <int N>
+__device__ __forceinline__ int32_t sel(const int32_t (&a)[N], int w) {
+    if constexpr (N == 1) return a[0];
+    else if constexpr (N == 2) return w ? a[1] : a[0];
+    else return w < 2 ? (w ? a[1] : a[0]) : (w == 2 ? a[2] : a[3]);
 }
 
 __device__ __forceinline__ float silu_f(float z) { return __fdividef(z, 1.0f + __expf(-z)); }
@@ -285,7 +304,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
                         for (int kbl = 0; kbl < nkb; ++kbl)
                             for (int part = 0; part < 3; ++part, ++it) {
                                 const int s = it % W_STAGES;
-                                mbar_wait(&w_empty[s], ((it / W_STAGES) & 1) ^ 1);
+                                mbar_wait_sleep(&w_empty[s], ((it / W_STAGES) & 1) ^ 1);
                                 mbar_arrive_expect_tx(&w_full[s], bytes);
                                 bulk_g2s(wring + s * W_STAGE, wblock(net, j, kbl, part), bytes, &w_full[s]);
                             }
@@ -303,7 +322,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
                     for (int g = 0; g < 2; ++g) {
                         const int64_t t = t0 + g;
                         if (t >= P.n_tiles) continue;
-                        mbar_wait(&feat_ready[g], fr[g] & 1);
+                        mbar_wait_sleep(&feat_ready[g], fr[g] & 1);
                         ++fr[g];
                         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                         const uint32_t d_hi = tmem + (uint32_t)(256 * g), d_lo = d_hi + 128;
@@ -314,7 +333,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
                         for (int kbl = 0; kbl < nkb; ++kbl)
                             for (int part = 0; part < 3; ++part, ++it) {
                                 const int s = it % W_STAGES;
-                                mbar_wait(&w_full[s], (it / W_STAGES) & 1);
+                                mbar_wait_sleep(&w_full[s], (it / W_STAGES) & 1);
                                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                                 const uint32_t w_base = smem_u32(wring + s * W_STAGE);
                                 for (int ap = 0; ap + part <= 2; ++ap) {
@@ -336,15 +355,21 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
         }
     } else {
         // ---------------------------------------------------- epilogue groups
-        const int g = (warp - 2) >> 2;
+        // group g = 4 warps, one per TMEM lane quarter (32 event rows each)
+        const int g = (warp - 2) >> 2, h = 0;
         const int q = warp & 3;                 // TMEM lane quarter of this warp
         const int row = q * 32 + lane;          // event row of the tile = TMEM lane
         uint8_t *abuf = abuf0 + g * A_BYTES;
         const uint32_t t_hi = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(256 * g), t_lo = t_hi + 128;
         const int SN = 2 * E + 4;
-        constexpr int EP = E <= 8 ? 8 : E <= 16 ? 16 : E <= 32 ? 32 : E <= 64 ? 64 : 128;   // sort width
-        constexpr int IDB = EP == 8 ? 3 : EP == 16 ? 4 : EP == 32 ? 5 : EP == 64 ? 6 : 7;   // id bits in a key
-        constexpr int SROW = E + 1;             // fp32 score staging row (words; odd: conflict-free columns)
+        constexpr bool SPLIT = false;           // (one warp per lane quarter: no column split)
+        constexpr int EH = E;
+        constexpr int IDB = E <= 8 ? 3 : E <= 16 ? 4 : E <= 32 ? 5 : E <= 64 ? 6 : 7;   // id bits in a key
+        const bool feat_half = SPLIT || h == 0;   // halves that build layer-1 features
+        const int e_lo = SPLIT ? h * EH : 0;
+        // staging (the A buffer after the last layer's MMAs): fp32 scores
+        // [row][E + 1] (odd stride: conflict-free columns), then rank rows [row][E + 16]
+        float *sc = (float *)abuf;
         uint32_t ar = 0;
         for (int64_t k = 0;; ++k) {
             const int64_t t = (k * G + b) * 2 + g;
@@ -358,53 +383,68 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
                 const uint8_t *ids = P.tr.acc + (c * T + ev) * P.tr.K;
                 for (int kk = 0; kk < P.tr.K; ++kk) {
                     const int x = __ldg(ids + kk);
-                    mine[x >> 5] |= 1u << (x & 31);
+                    const uint32_t bit = 1u << (x & 31);
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) mine[w] |= (x >> 5) == w ? bit : 0u;
                 }
             }
-            // tracker snapshot at the start of this warp's 32-event sub-tile
+            // tracker snapshot at the start of this warp's 32-event sub-tile,
+            // distributed: lane l keeps last / f of experts l, l + 32, ...
             const int64_t s32 = (ev0 >> 5) + q;
             const bool has_snap = s32 < P.tpc32;
             const int32_t *sp = P.snaps + (c * P.tpc32 + (has_snap ? s32 : 0)) * SN;
+            constexpr int NW = (E + 31) / 32;
+            int32_t s_last[NW], s_f[NW];
+#pragma unroll
+            for (int j = 0; j < NW; ++j) {
+                const int e = lane + 32 * j;
+                s_last[j] = (has_snap && e < E) ? __ldg(sp + e) : -1;
+                s_f[j] = (has_snap && e < E) ? __ldg(sp + E + e) : 0;
+            }
             const int32_t u0 = (int32_t)(s32 * 32);
+            const int32_t u = u0 + lane + 1;   // this event's update index (1-based)
             const uint32_t upto = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);
             // max_f over experts at this event (features.py:44-52)
             int32_t maxf = 0;
-#pragma unroll 4
+#pragma unroll 8
             for (int e = 0; e < E; ++e) {
                 const uint32_t m = __ballot_sync(0xFFFFFFFFu, routes(mine, e));
-                const int32_t f = (has_snap ? __ldg(sp + E + e) : 0) + __popc(m & upto);
+                const int32_t f = __shfl_sync(0xFFFFFFFFu, sel(s_f, e >> 5), e & 31) + __popc(m & upto);
                 maxf = max(maxf, f);
             }
-            named_sync(1 + g, 128);   // every thread is done with the previous tile's staging rows
-            // ---- layer-1 input: [1/r || f / max_f] (K = 2E, zero padded), P1 passes of 128
+            const float rmaxf = maxf > 0 ? 1.0f / (float)maxf : 0.0f;
+            named_sync(1 + g, 128);   // every thread is done with the previous tile's staging
+            // ---- layer-1 input: [1/r || f / max_f] (K = 2E, zero padded to KB1 * 64).
+            // E <= 64: one pass holds both halves; E = 128: recency, then frequency.
             for (int p = 0; p < P1; ++p) {
                 if (p > 0) {   // the previous pass's MMAs have consumed the A buffer
                     mbar_wait(&acc_ready[g], ar & 1);
                     ++ar;
                 }
-                for (int k0 = 128 * p; k0 < 128 * p + 128; k0 += 8) {
-                    float v[8];
+                const bool want_r = 2 * E <= 128 || p == 0, want_f = 2 * E <= 128 || p == 1;
+                const int kr = 2 * E <= 128 ? 0 : -128 * p, kf = 2 * E <= 128 ? E : E - 128 * p;
+                if (feat_half) {
+#pragma unroll 1
+                    for (int e0 = e_lo; e0 < e_lo + EH; e0 += 8) {
+                        float rv[8], fv[8];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int kx = k0 + i;
-                        float val = 0.0f;
-                        if (kx < 2 * E) {
-                            const int e = kx < E ? kx : kx - E;
+                        for (int i = 0; i < 8; ++i) {
+                            const int e = e0 + i;
                             const uint32_t m = __ballot_sync(0xFFFFFFFFu, routes(mine, e));
                             const uint32_t seen = m & upto;
-                            if (kx < E) {
-                                const int32_t lastu = seen ? u0 + (31 - __clz(seen)) + 1
-                                                           : (has_snap ? __ldg(sp + e) : -1);
-                                const int32_t u = u0 + lane + 1;
-                                val = lastu < 0 ? 0.0f : 1.0f / (float)(u - lastu + 1);
-                            } else {
-                                const int32_t f = (has_snap ? __ldg(sp + E + e) : 0) + __popc(seen);
-                                val = maxf > 0 ? (float)f / (float)maxf : 0.0f;
-                            }
+                            const int32_t sl = __shfl_sync(0xFFFFFFFFu, sel(s_last, e >> 5), e & 31);
+                            const int32_t sf = __shfl_sync(0xFFFFFFFFu, sel(s_f, e >> 5), e & 31);
+                            const int32_t lastu = seen ? u0 + (31 - __clz(seen)) + 1 : sl;
+                            rv[i] = lastu < 0 ? 0.0f : __fdividef(1.0f, (float)(u - lastu + 1));
+                            fv[i] = (float)(sf + __popc(seen)) * rmaxf;
                         }
-                        v[i] = val;
+                        if (want_r) store_chunk8(abuf, row, kr + e0, rv);
+                        if (want_f) store_chunk8(abuf, row, kf + e0, fv);
                     }
-                    store_chunk8(abuf, row, k0 - 128 * p, v);
+                }
+                if (p == P1 - 1 && h == 0) {   // zero padding up to the K blocks the MMAs read
+                    const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                    for (int k0 = 2 * E - 128 * p; k0 < P.KB1 * 64 - 128 * p; k0 += 8) store_chunk8(abuf, row, k0, z);
                 }
                 fence_async_smem();
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -421,16 +461,19 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
                     uint32_t rh[32], rl[32];
                     tmem_ld32_nowait(t_hi + c0, rh);
                     tmem_ld32_nowait(t_lo + c0, rl);
+                    float4 b0 = __ldg((const float4 *)(bias + c0)), b1 = __ldg((const float4 *)(bias + c0) + 1);
                     tmem_wait_ld();
 #pragma unroll
                     for (int c8 = 0; c8 < 32; c8 += 8) {
+                        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                        if (c8 + 8 < 32) {
+                            b0 = __ldg((const float4 *)(bias + c0 + c8 + 8));
+                            b1 = __ldg((const float4 *)(bias + c0 + c8 + 8) + 1);
+                        }
                         float v[8];
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const float z = (__uint_as_float(rh[c8 + i]) + __uint_as_float(rl[c8 + i])) +
-                                            __ldg(bias + c0 + c8 + i);
-                            v[i] = silu_f(z);
-                        }
+                        for (int i = 0; i < 8; ++i)
+                            v[i] = silu_f((__uint_as_float(rh[c8 + i]) + __uint_as_float(rl[c8 + i])) + bb[i]);
                         store_chunk8(abuf, row, c0 + c8, v);
                     }
                 }
@@ -438,77 +481,78 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(&feat_ready[g]);
             }
-            // ---- scores: s = acc_hi + acc_lo + b3, then ranks
+            // ---- scores: s = acc_hi + acc_lo + b3, one thread per event sorts
+            // the E keys and certifies the order
             mbar_wait(&acc_ready[g], ar & 1);
             ++ar;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            float *srow = (float *)abuf + row * SROW;       // the A buffer is free now
-            const float *b3 = P.bias + (int64_t)net * P.bias_stride + 2 * H;
-            uint32_t key[EP];
             bool bad = false;
+            constexpr int EP = E;   // E is a power of two
+            constexpr uint32_t M = (1u << IDB) - 1u;
+            if (h == 0) {
+                const float *b3 = P.bias + (int64_t)net * P.bias_stride + 2 * H;
+                float *srow = sc + row * (E + 1);
+                uint8_t *rrow = (uint8_t *)(sc + BM * (E + 1)) + row * (E + 16);
+                uint32_t key[EP];
 #pragma unroll
-            for (int c0 = 0; c0 < EP; c0 += 32) {
-                if (c0 >= E) break;
-                uint32_t rh[32], rl[32];
-                tmem_ld32_nowait(t_hi + c0, rh);
-                tmem_ld32_nowait(t_lo + c0, rl);
-                tmem_wait_ld();
+                for (int c0 = 0; c0 < EP; c0 += 32) {
+                    uint32_t rh[32], rl[32];
+                    tmem_ld32_nowait(t_hi + c0, rh);
+                    tmem_ld32_nowait(t_lo + c0, rl);
+                    tmem_wait_ld();
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int e = c0 + i;
-                    if (e < EP) {
+                    for (int i = 0; i < 32; ++i) {
+                        const int e = c0 + i;
                         if (e < E) {
                             const float s = (__uint_as_float(rh[i]) + __uint_as_float(rl[i])) + __ldg(b3 + e);
                             bad |= !isfinite(s);
                             srow[e] = s;
-                            key[e] = (okey(s) & ~((1u << IDB) - 1u)) | (uint32_t)e;
-                        } else {
-                            key[e] = 0xFFFFFFFFu;
+                            key[e] = (okey(s) & ~M) | (uint32_t)e;
                         }
                     }
                 }
-            }
+                bitonic_sort<EP>(key);
+                // certify: adjacent scores apart by more than 2 tau max|s|, no
+                // truncated-key collision (then the sorted order is the exact order)
+                const float smin = srow[key[0] & M], smax = srow[key[E - 1] & M];
+                const float thr = 2.0f * P.tau * fmaxf(fabsf(smin), fabsf(smax));
+                float prev = smin;
 #pragma unroll
-            for (int e = E; e < EP; ++e) key[e] = 0xFFFFFFFFu;
+                for (int n = 0; n < E; ++n) {
+                    const int id = (int)(key[n] & M);
+                    if (n > 0) {
+                        const float cur = srow[id];
+                        bad |= ((key[n] ^ key[n - 1]) >> IDB) == 0u;
+                        bad |= !(cur - prev > thr);
+                        prev = cur;
+                    }
+                    rrow[id] = (uint8_t)(n + 1);
+                }
+                if (valid) {
+                    uint8_t *dst = P.ranks + (c * T + ev) * E;
+                    if constexpr (E % 16 == 0) {
+#pragma unroll
+                        for (int i = 0; i < E; i += 16) *(uint4 *)(dst + i) = *(const uint4 *)(rrow + i);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < E; i += 8) *(uint2 *)(dst + i) = *(const uint2 *)(rrow + i);
+                    }
+                    if (P.dbg_scores) {
+                        float *ds = P.dbg_scores + (c * T + ev) * E;
+                        for (int e = 0; e < E; ++e) ds[e] = srow[e];
+                    }
+                }
+            }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            bitonic_sort<EP>(key);
-            // certify: adjacent scores apart by more than 2 tau max|s|, no
-            // truncated-key collision (then the sorted order is the exact order)
-            const float smin = srow[key[0] & ((1u << IDB) - 1u)], smax = srow[key[E - 1] & ((1u << IDB) - 1u)];
-            const float thr = 2.0f * P.tau * fmaxf(fabsf(smin), fabsf(smax));
-            uint8_t *rrow = (uint8_t *)((float *)abuf + BM * SROW) + row * (E + 16);
-            float prev = smin;
-#pragma unroll
-            for (int n = 0; n < E; ++n) {
-                const int id = (int)(key[n] & ((1u << IDB) - 1u));
-                if (n > 0) {
-                    const float cur = srow[id];
-                    bad |= ((key[n] ^ key[n - 1]) >> IDB) == 0u;
-                    bad |= !(cur - prev > thr);
-                    prev = cur;
-                }
-                rrow[id] = (uint8_t)(n + 1);
-            }
-            if (valid && P.dbg_scores) {
-                float *ds = P.dbg_scores + (c * T + ev) * E;
-                for (int e = 0; e < E; ++e) ds[e] = srow[e];
-            }
-            if (valid) {
-                uint8_t *dst = P.ranks + (c * T + ev) * E;
-                if constexpr (E % 16 == 0) {
-#pragma unroll
-                    for (int i = 0; i < E; i += 16) *(uint4 *)(dst + i) = *(const uint4 *)(rrow + i);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < E; i += 8) *(uint2 *)(dst + i) = *(const uint2 *)(rrow + i);
-                }
-                if (bad) {
+            if (h == 0) {
+                const bool flagged = valid && bad;
+                if (flagged) {
                     const int slot = atomicAdd(P.flag_cnt + net, 1);
                     P.flag_list[(int64_t)net * P.bucket_cap + slot] = (int32_t)(c * T + ev);
                 }
+                const unsigned nb = __popc(__ballot_sync(0xFFFFFFFFu, flagged));
+                if (lane == 0 && nb) atomicAdd(P.stats + 5, (unsigned long long)nb);
             }
-            const unsigned nb = __popc(__ballot_sync(0xFFFFFFFFu, valid && bad));
-            if (lane == 0 && nb) atomicAdd(P.stats + 5, (unsigned long long)nb);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -597,7 +641,7 @@ int score_tc_bias_stride(int E) { return 2 * k3tc::H + (E + 15) / 16 * 16; }
 
 bool score_tc_eligible(const DevTrace &tr, int H) {
     return tr.uniform && H == k3tc::H && (tr.E == 8 || tr.E == 16 || tr.E == 32 || tr.E == 64 || tr.E == 128) &&
-           tr.total_events < (1ll << 31);
+           tr.K <= 16 && tr.total_events < (1ll << 31);
 }
 
 static int g_num_sms = 0;
@@ -661,6 +705,17 @@ int launch_score_tc(const DevTrace &tr, const double *params, int num_nets, cons
         case 32: k_score_tc<32><<<grid, THREADS, SMEM_BYTES, s>>>(P); break;
         case 64: k_score_tc<64><<<grid, THREADS, SMEM_BYTES, s>>>(P); break;
         default: k_score_tc<128><<<grid, THREADS, SMEM_BYTES, s>>>(P); break;
+    }
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        cudaFuncAttributes a;
+        cudaFuncGetAttributes(&a, (const void *)k_score_tc<64>);
+        char b[256];
+        snprintf(b, sizeof b, "k_score_tc launch: %s (maxThreadsPerBlock %d, regs %d, local %zu, static smem %zu, "
+                 "max dyn smem %d, requested %d threads x %d B)", cudaGetErrorString(e), a.maxThreadsPerBlock,
+                 a.numRegs, a.localSizeBytes, a.sharedSizeBytes, a.maxDynamicSharedSizeBytes, THREADS, SMEM_BYTES);
+        mcb_set_error(MCB_ERR_CUDA, b);
+        return -1;
     }
     return 2;
 }
