@@ -176,6 +176,9 @@ int mcb_last_error(char *buf, size_t n);
  * launched, and the uncertain-rank counter of the ML scorer (events whose
  * float64 scores had two values closer than 1e-12 relative). */
 int mcb_last_stats(mcb_ctx *ctx, int64_t *kernels_launched, int64_t *uncertain_events);
+/* Trace ranges the last mcb_replay / mcb_replay_host was split into to stay
+ * within the scratch budget (MCB_TUNE_SCRATCH_BYTES); 1 = one range. */
+int mcb_last_chunks(mcb_ctx *ctx, int64_t *chunks);
 /* Stage timing: when enabled, mcb_replay records CUDA events on its stream
  * around each stage; mcb_last_timings returns the stage durations in ms of
  * the last call (after the stream has been synchronised):

@@ -48,7 +48,7 @@ EXPORTED_SYMBOLS = (
     "mcb_set_timing", "mcb_last_timings", "mcb_set_tuning", "mcb_read_stats",
     "mcb_pack_trace", "mcb_validate_trace", "mcb_packed_view", "mcb_packed_positions", "mcb_packed_free",
     "mcb_replay", "mcb_replay_host", "mcb_next_use", "mcb_score", "mcb_router_topk", "mcb_gen_reference",
-    "mcb_gen_reference_batch", "mcb_score_tc_scores",
+    "mcb_gen_reference_batch", "mcb_score_tc_scores", "mcb_last_chunks",
     "mcb_training_data", "mcb_set_lecar", "mcb_lecar_random", "mcb_pack_decode_ids",
     "mcb_eviction_duel", "mcb_train_epoch", "mcb_train_eval",
 )
@@ -165,6 +165,7 @@ def load_library():
             "mcb_train_eval": ([P, P, P, i64, i64, P, P], ctypes.c_int),
             "mcb_gen_reference_batch": ([P, i32, i32, i32, i64, i64, i32, ctypes.c_double, P, P, P, P], i32),
             "mcb_score_tc_scores": ([P, P, P, P, P, P], i32),
+            "mcb_last_chunks": ([P, P], i32),
             "mcb_gen_reference": ([P, i32, i32, i32, i64, i64, i64, i32, ctypes.c_double, P, P, P, P],
                                   ctypes.c_int),
         }
@@ -226,6 +227,13 @@ def lecar_random(seed: int, n: int):
     out = np.zeros(max(int(n), 1), dtype=np.float64)
     check(load_library().mcb_lecar_random(int(seed), int(n), out.ctypes.data))
     return out[:n]
+
+
+def last_chunks(device: int = 0) -> int:
+    """Trace ranges the last replay on this device's context was split into."""
+    n = ctypes.c_int64()
+    check(load_library().mcb_last_chunks(context(device), ctypes.byref(n)))
+    return int(n.value)
 
 
 def set_tuning(knob: int, value: int, device: int = 0):

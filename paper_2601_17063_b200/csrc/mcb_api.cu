@@ -367,6 +367,12 @@ extern "C" int mcb_read_stats(mcb_ctx *c, int64_t *out, int32_t n) {
     return MCB_OK;
 }
 
+extern "C" int mcb_last_chunks(mcb_ctx *c, int64_t *chunks) {
+    if (!c || !chunks) return mcb_set_error(MCB_ERR_INVALID, "ctx / chunks is NULL");
+    *chunks = c->last_chunks;
+    return MCB_OK;
+}
+
 extern "C" int mcb_last_stats(mcb_ctx *c, int64_t *kernels, int64_t *uncertain) {
     if (!c) return mcb_set_error(MCB_ERR_INVALID, "ctx is NULL");
     if (kernels) *kernels = c->last_kernels;

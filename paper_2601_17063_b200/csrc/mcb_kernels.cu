@@ -1512,16 +1512,31 @@ __device__ __forceinline__ double key_value(unsigned long long k) {
     return __longlong_as_double((long long)((k >> 63) ? (k ^ 0x8000000000000000ull) : ~k));
 }
 
+// max_e |s_e| over the finite scores of one event row (warp-wide): the scale
+// of the float64 near-tie test, which is normwise so that two small scores
+// produced by cancellation of large terms are flagged too.
+__device__ __forceinline__ double row_scale(const double *srow, int E, int lane) {
+    double m = 0.0;
+    for (int e = lane; e < E; e += 32) {
+        const double x = fabs(srow[e]);
+        if (x < INFINITY) m = fmax(m, x);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL_MASK, m, o));
+    return m;
+}
+
 // Ranks of one event's E scores by a warp-wide bitonic sort of the scores'
 // order-preserving integer keys (P elements per lane, N = 32 P >= E; padding
 // sorts last as +inf; equal scores need no tie-break because equal values get
 // equal ranks): rank = 1 + #{selectable j : s_j < s_e} = 1 + (first sorted
 // position of s_e's value) - #non-selectable, 0 for NaN / -inf (never
-// evicted, mlpolicy.py:15-26).  A near-tie (two distinct scores within 1e-12
+// evicted, mlpolicy.py:15-26).  A near-tie (two distinct scores within 1e-12 * max|s|
 // relative) is always an adjacent sorted pair, which sets *flag.
 template <int P>
 __device__ __forceinline__ void rank_event_sorted(const double *srow, int E, uint8_t *rrow, int32_t *flag, int lane) {
     constexpr int N = 32 * P;
+    const double scale = row_scale(srow, E, lane);
     const unsigned long long KNEG = ordered_key(-INFINITY), KPOS = ordered_key(INFINITY);
     unsigned long long v[P];
     int id[P];
@@ -1580,7 +1595,7 @@ __device__ __forceinline__ void rank_event_sorted(const double *srow, int E, uin
         nsel_local += (v[p] == KNEG) ? 1 : 0;
         if (n > 0 && v[p] != pk && pk != KNEG && v[p] != KPOS) {
             const double a = key_value(v[p]), b = key_value(pk);
-            if (fabs(a - b) <= 1e-12 * fmax(fabs(a), fabs(b))) near = true;
+            if (fabs(a - b) <= 1e-12 * scale) near = true;
         }
     }
     int carry = loc;   // warp inclusive max-scan of the lanes' last run start
@@ -1608,6 +1623,7 @@ __device__ __forceinline__ void rank_event_sorted(const double *srow, int E, uin
 template <int P>
 __device__ __forceinline__ void rank_event_packed(const double *srow, int E, uint8_t *rrow, int32_t *flag, int lane) {
     constexpr int N = 32 * P;
+    const double scale = row_scale(srow, E, lane);
     const unsigned long long KNEG = ordered_key(-INFINITY) & ~0x7Full, KPOS = ~0ull;
     unsigned long long v[P];
 #pragma unroll
@@ -1668,7 +1684,7 @@ __device__ __forceinline__ void rank_event_packed(const double *srow, int E, uin
         nsel_local += ((v[p] >> 7) == (KNEG >> 7) && v[p] != KPOS) ? 1 : 0;
         if (n > 0 && v[p] != KPOS && (pk >> 7) != (KNEG >> 7)) {
             const double a = srow[(int)(v[p] & 0x7Full)], b = srow[(int)(pk & 0x7Full)];
-            if (fabs(a - b) <= 1e-12 * fmax(fabs(a), fabs(b))) near = true;
+            if (fabs(a - b) <= 1e-12 * scale) near = true;
         }
     }
     const int nsel = __reduce_add_sync(FULL_MASK, nsel_local);
@@ -1685,7 +1701,7 @@ __device__ __forceinline__ void rank_event_packed(const double *srow, int E, uin
 // Integer ranks of the fp64 scores of rows [0, nev) of bufA (row stride ldA)
 // into s_rank[row][E], near-tie flags into s_flag[row] (rank = 1 + #{selectable
 // j : s_j < s_e}, 0 for NaN / -inf; near tie = two distinct scores within
-// 1e-12 relative).  Every thread of the block calls it; ends with a barrier.
+// 1e-12 * max_e |s_e|, normwise).  Every thread of the block calls it; ends with a barrier.
 __device__ __forceinline__ void rank_tile_rows(const double *bufA, int ldA, int E, int nev, uint8_t *s_rank,
                                                int32_t *s_flag) {
     const int tid = threadIdx.x, lane = tid & 31;
@@ -1704,16 +1720,17 @@ __device__ __forceinline__ void rank_tile_rows(const double *bufA, int ldA, int 
                 // nearest smaller score (every adjacent pair of the sorted order is
                 // tested by its larger member)
                 r = 1;
-                double below = -INFINITY;
+                double below = -INFINITY, scale = 0.0;
 #pragma unroll 8
                 for (int j = 0; j < E; ++j) {
                     const double sj = bufA[i * ldA + j];
+                    if (fabs(sj) < INFINITY) scale = fmax(scale, fabs(sj));
                     if (sj > -INFINITY && sj < s) {
                         ++r;
                         below = fmax(below, sj);
                     }
                 }
-                near = below > -INFINITY && fabs(s - below) <= 1e-12 * fmax(fabs(s), fabs(below));
+                near = below > -INFINITY && fabs(s - below) <= 1e-12 * scale;
             }
             s_rank[i * E + e] = (uint8_t)r;
             if (near) s_flag[i] = 1;
@@ -1881,28 +1898,35 @@ __global__ void __launch_bounds__(256, 3) k_rescore(DevTrace tr, const double *_
                     f[j] = e < E ? sp[E + e] : 0;
                 }
                 // the tile's events up to and including this one (features.py:34-39):
-                // lane j loads event s32*32 + j's ids, the walk broadcasts them
+                // lane l holds the routed set of event j0 + l as a 128-bit mask; one
+                // ballot per expert gives that expert's occurrence mask over the prefix
                 const int64_t j0 = s32 * MCB_TILE_EV;
                 const int nprefix = (int)(i - j0) + 1;
-                const uint8_t *ids = tr.acc + (c * tr.T + j0 + lane) * tr.K;
-                uint32_t mine[4] = {0u, 0u, 0u, 0u};   // ids of event j0 + lane, packed 4 per word
-                for (int k = 0; k < tr.K; ++k) {
-                    const uint32_t x = lane < nprefix ? (uint32_t)__ldg(ids + k) : 0u;
-#pragma unroll
-                    for (int w = 0; w < 4; ++w) mine[w] |= (k >> 2) == w ? x << (8 * (k & 3)) : 0u;
-                }
-                for (int jj = 0; jj < nprefix; ++jj) {
+                uint32_t mine[4] = {0u, 0u, 0u, 0u};
+                if (lane < nprefix) {
+                    const uint8_t *ids = tr.acc + (c * tr.T + j0 + lane) * tr.K;
                     for (int k = 0; k < tr.K; ++k) {
-                        const uint32_t wd = __shfl_sync(FULL_MASK, (k >> 2) == 0 ? mine[0] : (k >> 2) == 1 ? mine[1]
-                                                                     : (k >> 2) == 2 ? mine[2] : mine[3], jj);
-                        const int x = (int)((wd >> (8 * (k & 3))) & 0xFFu);
-                        if ((x & 31) == lane) {
+                        const int x = __ldg(ids + k);
+                        const uint32_t bit = 1u << (x & 31);
 #pragma unroll
-                            for (int j = 0; j < 4; ++j)
-                                if ((x >> 5) == j) { last[j] = (int32_t)(j0 + jj) + 1; ++f[j]; }
-                        }
+                        for (int w = 0; w < 4; ++w) mine[w] |= (x >> 5) == w ? bit : 0u;
                     }
                 }
+                uint32_t occ[4] = {0u, 0u, 0u, 0u};   // lane l: occurrence masks of experts l + 32 w
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    if (32 * w >= E) break;
+                    for (int l = 0; l < 32; ++l) {
+                        const uint32_t m = __ballot_sync(FULL_MASK, (mine[w] >> l) & 1u);
+                        occ[w] = lane == l ? m : occ[w];
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (occ[j]) {
+                        last[j] = (int32_t)j0 + (31 - __clz(occ[j])) + 1;
+                        f[j] += __popc(occ[j]);
+                    }
                 u = (int32_t)i + 1;
                 maxf = __reduce_max_sync(FULL_MASK, max(max(f[0], f[1]), max(f[2], f[3])));
             }

@@ -13,6 +13,8 @@ exactly like engine.py:345-379.
 from __future__ import annotations
 
 import ctypes
+import threading
+import warnings
 import math
 from dataclasses import asdict, dataclass
 from typing import Optional, Sequence, Union
@@ -229,6 +231,32 @@ def _cost_struct(cost: CostModel, window: int) -> _lib.MCBCost:
     return c
 
 
+_REPLAY_LOCKS: dict = {}
+_REPLAY_LOCKS_GUARD = threading.Lock()
+
+
+def _replay_lock(device: int) -> threading.Lock:
+    with _REPLAY_LOCKS_GUARD:
+        return _REPLAY_LOCKS.setdefault(device, threading.Lock())
+
+
+class ScorerNearTieWarning(UserWarning):
+    """Some events' float64 scores had two values within 1e-12 relative: the
+    reference's own float64 BLAS order could rank them either way."""
+
+
+def _warn_uncertain(device: int):
+    """Surface float64 near ties of the last ML replay (mcb_last_stats): the
+    engine ranks them with its own float64 scores (lowest id on exact ties),
+    but a decision there is within the reference's rounding noise."""
+    k, u = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(_lib.load_library().mcb_last_stats(_lib.context(device), ctypes.byref(k), ctypes.byref(u)))
+    if u.value > 0:
+        warnings.warn(f"{u.value} event(s) had float64 scores within 1e-12 relative of each other; their ML "
+                      "decisions follow this engine's float64 scores and may differ from the reference's BLAS "
+                      "rounding", ScorerNearTieWarning, stacklevel=3)
+
+
 def replay_host(packed: PackedTrace, codes: Sequence[int], capacities: Sequence[int], cost: CostModel,
                 window: int, nets=None, *, want_outcomes=False, want_hashes=False, want_chain=False,
                 device: int = 0, stream=None, lecar=None) -> dict:
@@ -272,13 +300,19 @@ def replay_host(packed: PackedTrace, codes: Sequence[int], capacities: Sequence[
         ns.num_experts, ns.hidden, ns.num_nets = packed.num_experts, hidden, n_nets
         ns.params = keep.ctypes.data
         netsp = ctypes.byref(ns)
-    if _lib.MCB_LECAR in codes:
-        _lib.set_lecar(*(lecar or _LECAR_DEFAULTS), device=device)
     view = packed.view()
     cs = _cost_struct(cost, window)
-    rc = lib.mcb_replay_host(ctx, ctypes.byref(view), pols, n_pol, caps, n_cap, ctypes.byref(cs), netsp,
-                             ctypes.byref(out), stream)
-    _lib.check(rc)
+    # LeCaR parameters live on the per-device context: hold the device's lock
+    # from setting them through the replay so that concurrent callers with
+    # other parameters cannot interleave (each reference cell owns its policy)
+    with _replay_lock(device):
+        if _lib.MCB_LECAR in codes:
+            _lib.set_lecar(*(lecar or _LECAR_DEFAULTS), device=device)
+        rc = lib.mcb_replay_host(ctx, ctypes.byref(view), pols, n_pol, caps, n_cap, ctypes.byref(cs), netsp,
+                                 ctypes.byref(out), stream)
+        _lib.check(rc)
+        if any(c in _lib.ML_CODES for c in codes):
+            _warn_uncertain(device)
     del keep
     return res
 

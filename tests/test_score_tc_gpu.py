@@ -112,3 +112,33 @@ def test_tau_extremes():
     assert st0[5] < dt.total_events
     diff = int((rnone != r64).any(axis=1).sum())
     print(f"tau = 0: {st0[5]} re-scored, {diff} of {dt.total_events} rank rows differ from float64")
+
+
+def test_forced_near_ties_are_rescored_and_surfaced():
+    """Two experts whose float64 scores differ by ~1e-14 of max|s| (identical
+    W3 rows, b3 apart by a few ulp): not an exact tie, but inside any float64
+    evaluation order's rounding.  The tensor-core scorer cannot certify those
+    events (they go to the float64 re-score), the float64 ranking flags them
+    as near ties, and the public API warns instead of silently deciding."""
+    import warnings
+
+    import paper_2601_17063_b200 as mcb
+    from paper_2601_17063_b200.engine import ScorerNearTieWarning
+    L, E, K, T = 2, 64, 6, 1024
+    ids = _ids(L, E, K, T, 1)[0]                                          # [L][T][K]
+    net = mcb.EvictionNet(E, seed=3)
+    net.params["w3"][5] = net.params["w3"][9]
+    net.params["b3"][5] = np.nextafter(np.nextafter(net.params["b3"][9], 1.0), 1.0)
+    events = []
+    for t in range(T):
+        for layer in range(L):
+            events.append(mcb.AccessEvent(0, mcb.Phase.DECODE, t, layer, tuple(int(x) for x in ids[layer, t])))
+    tr = mcb.RoutingTrace(mcb.TraceHeader("near", L, E, K), tuple(events))
+    with warnings.catch_warnings(record=True) as got:
+        warnings.simplefilter("always")
+        rep = mcb.simulate(tr, "ml", 16, nets=net)
+    assert any(issubclass(w.category, ScorerNearTieWarning) for w in got)
+    assert rep.hits + rep.misses == L * T * K
+    st = _lib.read_stats()
+    assert st[0] > 0                       # float64 near ties counted
+    assert st[5] >= st[0]                  # every one of them went through the float64 re-score
