@@ -17,6 +17,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "mcb_internal.h"
 #include "mcb_kernels.cuh"
 
@@ -123,11 +125,20 @@ struct mcb_ctx {
     cublasHandle_t cublas = nullptr;   // K10 batched DGEMMs
     std::vector<double> lecar_host;
     cudaEvent_t ev[10] = {};          // start/stop per stage: K2, K3, K4 non-ML, K4 ML, K5
+    nvtxRangeId_t nvtx[5] = {};       // open NVTX range per stage
     bool ran[5] = {};
 };
 
+// Stage boundaries: CUDA events for mcb_last_timings (when timing is on) and
+// NVTX ranges around the enqueue of each stage (K2 next-use, K3 scorer, K4
+// non-ML / ML replay, K5 fold) for Nsight timelines; NVTX calls are no-ops
+// unless a tool is attached.
+static const char *const kStageNames[5] = {"mcb K2 next-use scan", "mcb K3 scorer", "mcb K4 replay (non-ML)",
+                                          "mcb K4 replay (ML)", "mcb K5 fold"};
 static void mark(mcb_ctx *c, int i, cudaStream_t s) {
     if (c->timing) cudaEventRecord(c->ev[i], s);
+    if (i % 2 == 0) c->nvtx[i / 2] = nvtxRangeStartA(kStageNames[i / 2]);
+    else nvtxRangeEnd(c->nvtx[i / 2]);
 }
 static const int N_STAGES = 5;
 
