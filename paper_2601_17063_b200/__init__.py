@@ -22,6 +22,7 @@ from .engine import (
     step_latency_s,
     sweep,
 )
+from .dataset import DEFAULT_DISTANCE_CAP, LayerDataset, build_training_data
 from .distributed import replay_sharded, sweep_sharded
 from .net import EvictionNet, NetError, ShapeMismatchError, load_net, save_net
 from .policies import NoEvictableError, PolicyDecision, PolicyError, lecar_update

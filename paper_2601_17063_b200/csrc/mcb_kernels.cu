@@ -1201,19 +1201,25 @@ __device__ __forceinline__ void mma_layer_narrow(const double *A, int lda, int K
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, q = lane & 3;
     const int NT = N >> 3;
-    if (warp >= 4 * NT) return;
-    const int mt = warp / NT, nt = warp % NT;
+    const bool idle = warp >= 4 * NT;
+    const int mt = idle ? 0 : warp / NT, nt = idle ? 0 : warp % NT;
     const double *arow = A + (mt * 8 + g) * lda + q;
     const double *wcol = Wt + (int64_t)q * N + nt * 8 + g;
     double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+    if (!idle) {
 #pragma unroll (KC ? 32 : 8)
-    for (int k0 = 0; k0 < K; k0 += 8) {
-        const double a0 = arow[k0], b0 = __ldg(wcol + (int64_t)k0 * N);
-        const bool two = k0 + 4 < K;
-        const double a1 = two ? arow[k0 + 4] : 0.0, b1 = two ? __ldg(wcol + (int64_t)(k0 + 4) * N) : 0.0;
-        dmma884(c0, c1, a0, b0);
-        dmma884(d0, d1, a1, b1);
+        for (int k0 = 0; k0 < K; k0 += 8) {
+            const double a0 = arow[k0], b0 = __ldg(wcol + (int64_t)k0 * N);
+            const bool two = k0 + 4 < K;
+            const double a1 = two ? arow[k0 + 4] : 0.0, b1 = two ? __ldg(wcol + (int64_t)(k0 + 4) * N) : 0.0;
+            dmma884(c0, c1, a0, b0);
+            dmma884(d0, d1, a1, b1);
+        }
     }
+    // every warp has consumed A before anyone overwrites it (O may alias A:
+    // the in-place hidden layer of a net with hidden <= 16)
+    __syncthreads();
+    if (idle) return;
     const int cc = nt * 8 + 2 * q;
     const double z0 = __dadd_rn(__dadd_rn(c0, d0), __ldg(bias + cc));
     const double z1 = __dadd_rn(__dadd_rn(c1, d1), __ldg(bias + cc + 1));
