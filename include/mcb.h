@@ -235,7 +235,7 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
  * are identical; outcomes are not supported then).  0 (default) = 40% of
  * the device memory free at the call. */
 #define MCB_TUNE_SCRATCH_BYTES 11
-/* MCB_TUNE_K3_TC: 1 (default) = the tensor-core scorer (bf16 x 3 split on
+/* MCB_TUNE_K3_TC: 1 (default) = the tensor-core scorer (fp16 x 2 split on
  * tcgen05, certified ranks, float64 re-score of uncertified events) for
  * uniform traces with hidden 128 and num_experts in {8, 16, 32, 64, 128};
  * 0 = the float64 DMMA scorer for every event.  Ranks are identical. */
@@ -244,6 +244,10 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
  * every two adjacent scores differ by more than 2 * tau * max|s|; tau in units
  * of 1e-9 (default 4000 = 4e-6).  Larger = more events re-scored in float64. */
 #define MCB_TUNE_K3_TAU_PPB 13
+/* MCB_TUNE_K3_GROUPS: epilogue groups (128-event tiles in flight per SM) of
+ * the tensor-core scorer for num_experts <= 64: 3 (default) or 2.
+ * num_experts = 128 always runs 2.  Ranks are identical. */
+#define MCB_TUNE_K3_GROUPS 14
 int mcb_set_tuning(mcb_ctx *ctx, int32_t knob, int64_t value);
 /* LeCaR parameters used by the MCB_LECAR cells of later mcb_replay calls on
  * this context (LeCaRPolicy.__init__, policies.py:333-349; defaults 0.45,

@@ -115,6 +115,7 @@ struct mcb_ctx {
     DevBuf tc_wimg, tc_bias, tc_flag_cnt, tc_flag_list;   // K3-TC scratch
     int k3_tc = 1;                    // tensor-core scorer when eligible (MCB_TUNE_K3_TC)
     int64_t k3_tau_ppb = 4000;        // its certification threshold tau in 1e-9 (MCB_TUNE_K3_TAU_PPB)
+    int k3_groups = 3;                // its epilogue groups for E <= 64 (MCB_TUNE_K3_GROUPS)
     // LeCaR (mcb_set_lecar): parameters, the shared random() stream (cached
     // per seed, grown on demand) and the per-call regret factor table
     double lecar_lr = 0.45, lecar_base = 0.005;
@@ -243,6 +244,11 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
         c->k3_tau_ppb = value;
         return MCB_OK;
     }
+    if (knob == MCB_TUNE_K3_GROUPS) {
+        if (value != 2 && value != 3) return mcb_set_error(MCB_ERR_INVALID, "K3 groups must be 2 or 3");
+        c->k3_groups = (int)value;
+        return MCB_OK;
+    }
     if (knob == MCB_TUNE_SCRATCH_BYTES) {
         if (value < 0) return mcb_set_error(MCB_ERR_INVALID, "scratch budget must be >= 0");
         c->scratch_bytes = value;
@@ -312,6 +318,7 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     if (const char *env = getenv("MCB_SCRATCH_BYTES")) c->scratch_bytes = atoll(env);
     if (const char *env = getenv("MCB_K3_TC")) c->k3_tc = atoi(env);
     if (const char *env = getenv("MCB_K3_TAU_PPB")) c->k3_tau_ppb = atoll(env);
+    if (const char *env = getenv("MCB_K3_GROUPS")) c->k3_groups = atoi(env) == 2 ? 2 : 3;
     for (auto &e : c->chunk_ev)
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
             delete c;
@@ -473,7 +480,7 @@ static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int in
         const int n_tc = launch_score_tc(d, nets->params, nn, (const int32_t *)c->snaps.p, (uint8_t *)c->tc_wimg.p,
                                          (float *)c->tc_bias.p, ranks, (float)(c->k3_tau_ppb * 1e-9),
                                          (int32_t *)c->tc_flag_cnt.p, (int32_t *)c->tc_flag_list.p, cap,
-                                         (unsigned long long *)c->stats.p, tc_scores, s);
+                                         (unsigned long long *)c->stats.p, tc_scores, c->k3_groups, s);
         if (n_tc < 0) return MCB_ERR_CUDA;
         *launched += n_tc;
         *launched += launch_rescore(d, (const double *)c->wt.p, H, nn, (const int32_t *)c->snaps.p,

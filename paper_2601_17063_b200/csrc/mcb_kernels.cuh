@@ -129,7 +129,7 @@ int launch_score_tiles(const DevTrace &tr, const double *wt, int H, int num_nets
 int launch_train_features(const DevTrace &tr, const int32_t *snaps, const int64_t *tile_off, int64_t max_tiles,
                           int include_prefill, double *features, cudaStream_t s);
 int launch_train_targets(const DevTrace &tr, int distance_cap, double *targets, cudaStream_t s);
-// K3-TC (mcb_score_tc.cu): bf16x3 tcgen05 scorer with certified ranks; flagged
+// K3-TC (mcb_score_tc.cu): fp16x2 tcgen05 scorer with certified ranks; flagged
 // events go to per-net lists that launch_rescore re-scores in float64.
 bool score_tc_eligible(const DevTrace &tr, int H);
 size_t score_tc_net_bytes(int E);
@@ -137,7 +137,7 @@ int score_tc_bias_stride(int E);
 int preload_score_tc();
 int launch_score_tc(const DevTrace &tr, const double *params, int num_nets, const int32_t *snaps, uint8_t *wimg,
                     float *bias, uint8_t *ranks, float tau, int32_t *flag_cnt, int32_t *flag_list, int64_t bucket_cap,
-                    unsigned long long *stats, float *dbg_scores, cudaStream_t s);
+                    unsigned long long *stats, float *dbg_scores, int groups, cudaStream_t s);
 int launch_rescore(const DevTrace &tr, const double *wt, int H, int num_nets, const int32_t *snaps,
                    const int32_t *flag_cnt, const int32_t *flag_list, int64_t bucket_cap, uint8_t *ranks,
                    unsigned long long *uncertain, cudaStream_t s);

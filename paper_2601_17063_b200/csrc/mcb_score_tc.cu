@@ -7,13 +7,17 @@
 // lowest id on ties (mlpolicy.py:15-26).  The replay only needs the ORDER of
 // each event's scores (the rank row, shared by every capacity), so:
 //
-//   1. this kernel evaluates the MLP on tcgen05 in "bf16 x 3" arithmetic:
-//      every operand is split into three bf16 parts (a = a0 + a1 + a2, 24
-//      significant bits) and the six products with i + j <= 2 are
-//      accumulated in fp32 in TMEM (the leading a0*b0 product in its own
-//      accumulator, the five small ones in a second), bias + SiLU in fp32
-//      in the epilogue, which re-splits the activations into the next
-//      layer's A operand in shared memory;
+//   1. this kernel evaluates the MLP on tcgen05 in "fp16 x 2" arithmetic:
+//      every operand is split into two fp16 parts, a = a0 + a1 with
+//      a0 = rn(a), a1 = rn(a - a0) (11 + 1 + 11 + 1 = 24 significant bits,
+//      |a - a0 - a1| <= 2^-24 |a|), and the three products a0*w0 + a1*w0 +
+//      a0*w1 are accumulated in fp32 in TMEM (the dropped a1*w1 is below
+//      2^-22 of a product).  fp16's range is handled with exact powers of
+//      two: each layer's weights are scaled per net so that max|w| lies in
+//      [2^13, 2^14), layer-1 features (in [0, 1]) by 2^14 and the hidden
+//      activations by 2^8; the epilogue folds the inverse scale into one
+//      FFMA with the bias.  An activation that would overflow (|h| > 255)
+//      marks its event uncertified;
 //   2. it sorts each event's E scores (one thread per event, bitonic network
 //      on order-preserving keys carrying the expert id in their low bits)
 //      and writes the rank row;
@@ -29,19 +33,20 @@
 // decisions equal the reference's whenever the float64 scores order the
 // experts like the reference's BLAS float64 scores.
 //
-// Kernel shape: persistent, one CTA per SM, 10 warps:
-//   warp 0     weight producer: cp.async.bulk of pre-swizzled bf16 weight
-//              blocks (one part x one 64-wide K block) into a 2-stage ring
-//   warp 1     TMEM allocator (512 columns) + the single MMA-issuing thread
-//              (tcgen05.mma kind::f16, M=128, N=128 / E, K=16)
-//   warps 2-5  epilogue group 0, warps 6-9 epilogue group 1: each group owns
-//              one 128-event tile at a time (one event per thread: TMEM lane
-//              = event row), its A buffer (3 parts x 128 x 128 bf16 =
-//              96 KB) and 256 TMEM columns (hi + lo accumulators).
-// The two groups alternate on the tensor pipe: while one group runs its
+// Kernel shape: persistent, one CTA per SM, 2 + 4 * GROUPS warps:
+//   warp 0     weight producer: cp.async.bulk of pre-swizzled fp16 weight
+//              blocks (one part x one 64-wide K block) into a ring
+//   warp 1     TMEM allocator + the single MMA-issuing thread
+//              (tcgen05.mma kind::f16 with fp16 operands, M=128, N=128 / E, K=16)
+//   warps 2..  GROUPS epilogue groups of 4 warps: each group owns one
+//              128-event tile at a time (one event per thread: TMEM lane =
+//              event row), its A buffer (2 parts x 128 x 128 fp16 = 64 KB,
+//              plus the score staging) and 128 TMEM columns.
+// The groups take turns on the tensor pipe: while one group runs its
 // epilogue (features, bias + SiLU + split, or the rank sort), the MMAs of the
-// other group's next layer run.
-#include <cuda_bf16.h>
+// others' layers run.  E <= 64 runs 3 groups (2 weight stages), E = 128 two
+// groups (its score staging needs 84 KB; 3 weight stages).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -52,20 +57,29 @@ namespace k3tc {
 
 constexpr int H = 128;                    // EvictionNet hidden size (net.py:64 default)
 constexpr int BM = 128;                   // events per tile (MMA M)
-constexpr int ROWB = 128;                 // bytes per swizzled row: 64 bf16 (SWIZZLE_128B atom)
+constexpr int ROWB = 128;                 // bytes per swizzled row: 64 fp16 (SWIZZLE_128B atom)
 constexpr int KBLK = BM * ROWB;           // [128 rows x 64 K] block: 16 KB
-constexpr int A_PART = 2 * KBLK;          // one bf16 part of a [128 x 128] operand: 32 KB
-constexpr int A_BYTES = 3 * A_PART;       // three parts: 96 KB per epilogue group
+constexpr int A_PART = 2 * KBLK;          // one fp16 part of a [128 x 128] operand: 32 KB
+constexpr int NPART = 2;                  // fp16 parts per operand
 constexpr int W_STAGE = 128 * ROWB;       // one weight block [<= 128 rows x 64 K]: 16 KB
-constexpr int W_STAGES = 2;
-constexpr int THREADS = 320;       // producer, MMA issuer, 2 epilogue groups x 4 warps
-constexpr int SMEM_BYTES = 2 * A_BYTES + W_STAGES * W_STAGE + 1024 + 256;
+constexpr float FEAT_SCALE = 16384.0f;    // layer-1 features in [0, 1] -> [0, 2^14]
+constexpr float ACT_SCALE = 256.0f;       // hidden activations -> x 2^8 (|h| <= 255 certified)
+constexpr int NSCALE = 8;                 // per net: 2^s of layers 1..3, then their epilogue multipliers
+
+template <int GROUPS>
+struct Shape {
+    static constexpr int REGION = GROUPS == 3 ? 64 * 1024 : 88 * 1024;   // A parts + score staging
+    static constexpr int W_STAGES = GROUPS == 3 ? 2 : 3;
+    static constexpr int THREADS = 64 + 128 * GROUPS;
+    static constexpr int SMEM = GROUPS * REGION + W_STAGES * W_STAGE + 1024 + 256;
+    static constexpr int TMEM_COLS = GROUPS * 128 > 256 ? 512 : 256;
+};
 
 struct Params {
     DevTrace tr;
-    const uint8_t *wimg;        // per net: swizzled bf16 weight blocks (k_prep_tc)
+    const uint8_t *wimg;        // per net: swizzled fp16 weight blocks (k_prep_tc)
     int64_t net_bytes;
-    const float *bias;          // per net: b1[128] b2[128] b3[N3]
+    const float *bias;          // per net: b1[128] b2[128] b3[N3] scales[NSCALE]
     int bias_stride;
     int num_nets;
     int N3, KB1, P1;            // layer-3 N (E rounded up to 16), layer-1 K blocks, layer-1 passes
@@ -128,11 +142,12 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
     d |= (uint64_t)2 << 61;
     return d;
 }
-// kind::f16 instruction descriptor: D = f32, A = B = bf16, K-major, M = 128
+// kind::f16 instruction descriptor: D = f32 (bit 4), A = B = f16 (format 0),
+// K-major, N >> 3 at bit 17, M >> 4 at bit 24
 __device__ __forceinline__ uint32_t idesc(int n) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+    return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t id, uint32_t acc) {
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t id, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
@@ -161,33 +176,29 @@ __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sy
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // byte offset of the 16-B chunk `ch` (0..7) of row `row` inside a
-// [rows x 64] bf16 block in the SWIZZLE_128B K-major layout
+// [rows x 64] fp16 block in the SWIZZLE_128B K-major layout
 __host__ __device__ __forceinline__ uint32_t sw128(int row, int ch) {
     return (uint32_t)row * ROWB + ((uint32_t)(ch ^ (row & 7)) << 4);
 }
 
-// (a, b) = (a0 + a1 + a2, b0 + b1 + b2), bf16 parts rounded to nearest, two
-// values per cvt.rn.bf16x2.f32 (each remainder is exact in fp32)
-__device__ __forceinline__ void split3x2(float a, float b, uint32_t &w0, uint32_t &w1, uint32_t &w2) {
-    const __nv_bfloat162 p0 = __floats2bfloat162_rn(a, b);
-    const float2 f0 = __bfloat1622float2(p0);
-    const float ra = a - f0.x, rb = b - f0.y;
-    const __nv_bfloat162 p1 = __floats2bfloat162_rn(ra, rb);
-    const float2 f1 = __bfloat1622float2(p1);
-    const __nv_bfloat162 p2 = __floats2bfloat162_rn(ra - f1.x, rb - f1.y);
+// (a, b) = (a0 + a1, b0 + b1), fp16 parts rounded to nearest, two values per
+// cvt.rn.f16x2.f32 (the remainders a - a0 are exact in fp32)
+__device__ __forceinline__ void split2x2(float a, float b, uint32_t &w0, uint32_t &w1) {
+    const __half2 p0 = __floats2half2_rn(a, b);
+    const float2 f0 = __half22float2(p0);
+    const __half2 p1 = __floats2half2_rn(a - f0.x, b - f0.y);
     w0 = *(const uint32_t *)&p0;
     w1 = *(const uint32_t *)&p1;
-    w2 = *(const uint32_t *)&p2;
 }
 
-// eight consecutive K values of one row -> the three parts' 16-B chunks
+// eight consecutive K values of one row -> the two parts' 16-B chunks
 __device__ __forceinline__ void store_chunk8(uint8_t *abuf, int row, int k0, const float (&v)[8]) {
-    uint32_t w[3][4];
+    uint32_t w[NPART][4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) split3x2(v[2 * j], v[2 * j + 1], w[0][j], w[1][j], w[2][j]);
+    for (int j = 0; j < 4; ++j) split2x2(v[2 * j], v[2 * j + 1], w[0][j], w[1][j]);
     const uint32_t off = (uint32_t)(k0 >> 6) * KBLK + sw128(row, (k0 & 63) >> 3);
 #pragma unroll
-    for (int p = 0; p < 3; ++p)
+    for (int p = 0; p < NPART; ++p)
         *(uint4 *)(abuf + p * A_PART + off) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
 }
 
@@ -231,38 +242,34 @@ __device__ __forceinline__ void bitonic_sort(uint32_t (&v)[N]) {
             }
 }
 
-// The tile / job order shared by the producer, the MMA issuer and the
-// epilogue groups: the k-th tile pair of CTA b is tiles (k * G + b) * 2 + g,
-// g = epilogue group; jobs interleave g0, g1 per job index.
-struct Job {
-    int g;
-    int64_t tile;
-    int j;   // 0..P1-1 layer-1 passes, P1 layer 2, P1 + 1 layer 3
-};
-
-template <int E>
-__global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__ Params P) {
+// Tile order shared by the producer, the MMA issuer and the epilogue groups:
+// the k-th tile set of CTA b is tiles (k * G + b) * GROUPS + g, g = epilogue
+// group; per tile set the jobs (layer-1 passes, layer 2, layer 3) run in
+// order, the groups interleaved within each job.
+template <int E, int GROUPS>
+__global__ void __launch_bounds__(Shape<GROUPS>::THREADS, 1) k_score_tc(const __grid_constant__ Params P) {
+    using S = Shape<GROUPS>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t *abuf0 = smem;                         // group 0 A operand (96 KB)
-    uint8_t *wring = smem + 2 * A_BYTES;           // weight ring
-    uint64_t *bars = (uint64_t *)(wring + W_STAGES * W_STAGE);
-    uint64_t *w_full = bars, *w_empty = bars + W_STAGES;
-    uint64_t *feat_ready = bars + 2 * W_STAGES, *acc_ready = feat_ready + 2;
-    uint32_t *tmem_slot = (uint32_t *)(acc_ready + 2);
+    uint8_t *abuf0 = smem;                         // group regions (A operand + score staging)
+    uint8_t *wring = smem + GROUPS * S::REGION;    // weight ring
+    uint64_t *bars = (uint64_t *)(wring + S::W_STAGES * W_STAGE);
+    uint64_t *w_full = bars, *w_empty = bars + S::W_STAGES;
+    uint64_t *feat_ready = bars + 2 * S::W_STAGES, *acc_ready = feat_ready + GROUPS;
+    uint32_t *tmem_slot = (uint32_t *)(acc_ready + GROUPS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int P1 = P.P1, JOBS = P1 + 2;
     const int64_t G = gridDim.x, b = blockIdx.x;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < W_STAGES; ++s) { mbar_init(&w_full[s], 1); mbar_init(&w_empty[s], 1); }
-        for (int g = 0; g < 2; ++g) { mbar_init(&feat_ready[g], 128); mbar_init(&acc_ready[g], 1); }
+        for (int s = 0; s < S::W_STAGES; ++s) { mbar_init(&w_full[s], 1); mbar_init(&w_empty[s], 1); }
+        for (int g = 0; g < GROUPS; ++g) { mbar_init(&feat_ready[g], 128); mbar_init(&acc_ready[g], 1); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(512));
+                     "r"(S::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -281,11 +288,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
     // weight block (layer of job j, global K block, part) of a net
     auto wblock = [&](int net, int j, int kbl, int part) -> const uint8_t * {
         const uint8_t *base = P.wimg + (int64_t)net * P.net_bytes;
-        if (j < P1) return base + (int64_t)((2 * j + kbl) * 3 + part) * KBLK;
-        base += (int64_t)P.KB1 * 3 * KBLK;
-        if (j == P1) return base + (int64_t)(kbl * 3 + part) * KBLK;
-        base += (int64_t)2 * 3 * KBLK;
-        return base + (int64_t)(kbl * 3 + part) * P.N3 * ROWB;
+        if (j < P1) return base + (int64_t)((2 * j + kbl) * NPART + part) * KBLK;
+        base += (int64_t)P.KB1 * NPART * KBLK;
+        if (j == P1) return base + (int64_t)(kbl * NPART + part) * KBLK;
+        base += (int64_t)2 * NPART * KBLK;
+        return base + (int64_t)(kbl * NPART + part) * P.N3 * ROWB;
     };
 
     if (warp == 0) {
@@ -293,18 +300,19 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
         if (lane == 0) {
             uint32_t it = 0;
             for (int64_t k = 0;; ++k) {
-                const int64_t t0 = (k * G + b) * 2;
+                const int64_t t0 = (k * G + b) * GROUPS;
                 if (t0 >= P.n_tiles) break;
                 for (int j = 0; j < JOBS; ++j)
-                    for (int g = 0; g < 2; ++g) {
+                    for (int g = 0; g < GROUPS; ++g) {
                         const int64_t t = t0 + g;
                         if (t >= P.n_tiles) continue;
                         const int net = net_of_tile(t), nkb = job_kblocks(j);
                         const uint32_t bytes = (uint32_t)job_n(j) * ROWB;
-                        for (int kbl = 0; kbl < nkb; ++kbl)
-                            for (int part = 0; part < 3; ++part, ++it) {
-                                const int s = it % W_STAGES;
-                                mbar_wait_sleep(&w_empty[s], ((it / W_STAGES) & 1) ^ 1);
+                        // the job's weight blocks: part 1 of every K block, then part 0
+                        for (int part = NPART - 1; part >= 0; --part)
+                            for (int kbl = 0; kbl < nkb; ++kbl, ++it) {
+                                const int s = it % S::W_STAGES;
+                                mbar_wait_sleep(&w_empty[s], ((it / S::W_STAGES) & 1) ^ 1);
                                 mbar_arrive_expect_tx(&w_full[s], bytes);
                                 bulk_g2s(wring + s * W_STAGE, wblock(net, j, kbl, part), bytes, &w_full[s]);
                             }
@@ -314,41 +322,58 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
     } else if (warp == 1) {
         // ------------------------------------------------------- MMA issuer
         if (lane == 0) {
-            uint32_t it = 0, fr[2] = {0u, 0u};
+            uint32_t it = 0, fr[GROUPS];
+#pragma unroll
+            for (int g = 0; g < GROUPS; ++g) fr[g] = 0u;
             for (int64_t k = 0;; ++k) {
-                const int64_t t0 = (k * G + b) * 2;
+                const int64_t t0 = (k * G + b) * GROUPS;
                 if (t0 >= P.n_tiles) break;
                 for (int j = 0; j < JOBS; ++j)
-                    for (int g = 0; g < 2; ++g) {
+#pragma unroll
+                    for (int g = 0; g < GROUPS; ++g) {
                         const int64_t t = t0 + g;
                         if (t >= P.n_tiles) continue;
                         mbar_wait_sleep(&feat_ready[g], fr[g] & 1);
                         ++fr[g];
                         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                        const uint32_t d_hi = tmem + (uint32_t)(256 * g), d_lo = d_hi + 128;
+                        const uint32_t d = tmem + (uint32_t)(128 * g);
                         const uint32_t id = idesc(job_n(j));
-                        const uint32_t a_base = smem_u32(abuf0 + g * A_BYTES);
-                        bool fresh_hi = !(j > 0 && j < P1), fresh_lo = fresh_hi;   // layer-1 passes > 0 accumulate
+                        const uint32_t a_base = smem_u32(abuf0 + g * S::REGION);
+                        bool fresh = !(j > 0 && j < P1);   // layer-1 passes > 0 accumulate
                         const int nkb = job_kblocks(j);
-                        for (int kbl = 0; kbl < nkb; ++kbl)
-                            for (int part = 0; part < 3; ++part, ++it) {
-                                const int s = it % W_STAGES;
-                                mbar_wait_sleep(&w_full[s], (it / W_STAGES) & 1);
-                                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                                const uint32_t w_base = smem_u32(wring + s * W_STAGE);
-                                for (int ap = 0; ap + part <= 2; ++ap) {
-                                    const bool hi = ap == 0 && part == 0;
-                                    const uint32_t a0 = a_base + ap * A_PART + kbl * KBLK;
+                        // Small products first, the leading a0*w0 last: the cross terms
+                        // a0*w1 (weight part 1) and a1*w0 are summed while the accumulator
+                        // is still small, so the accumulator's alignment to its running
+                        // magnitude costs them nothing; then a0*w0 over the same K blocks.
+                        // The ring holds the job's <= 2 part-0 blocks at once (W_STAGES >= 2).
+                        auto issue = [&](uint32_t a_part, uint32_t w_base, int kbl) {
+                            const uint32_t a0 = a_base + a_part * A_PART + kbl * KBLK;
 #pragma unroll
-                                    for (int k4 = 0; k4 < 4; ++k4) {
-                                        const bool fresh = hi ? fresh_hi : fresh_lo;
-                                        mma_bf16(hi ? d_hi : d_lo, make_desc(a0 + k4 * 32), make_desc(w_base + k4 * 32),
-                                                 id, fresh ? 0u : 1u);
-                                        if (hi) fresh_hi = false; else fresh_lo = false;
-                                    }
-                                }
-                                mma_commit(&w_empty[s]);
+                            for (int k4 = 0; k4 < 4; ++k4) {
+                                mma_f16(d, make_desc(a0 + k4 * 32), make_desc(w_base + k4 * 32), id, fresh ? 0u : 1u);
+                                fresh = false;
                             }
+                        };
+                        for (int kbl = 0; kbl < nkb; ++kbl, ++it) {   // part 1: a0 * w1
+                            const int s = it % S::W_STAGES;
+                            mbar_wait_sleep(&w_full[s], (it / S::W_STAGES) & 1);
+                            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                            issue(0, smem_u32(wring + s * W_STAGE), kbl);
+                            mma_commit(&w_empty[s]);
+                        }
+                        const uint32_t it0 = it;
+                        for (int kbl = 0; kbl < nkb; ++kbl) {          // part 0: a1 * w0
+                            const uint32_t i2 = it0 + kbl;
+                            const int s = i2 % S::W_STAGES;
+                            mbar_wait_sleep(&w_full[s], (i2 / S::W_STAGES) & 1);
+                            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                            issue(1, smem_u32(wring + s * W_STAGE), kbl);
+                        }
+                        for (int kbl = 0; kbl < nkb; ++kbl, ++it) {   // part 0: a0 * w0
+                            const int s = it % S::W_STAGES;
+                            issue(0, smem_u32(wring + s * W_STAGE), kbl);
+                            mma_commit(&w_empty[s]);
+                        }
                         mma_commit(&acc_ready[g]);
                     }
             }
@@ -356,27 +381,27 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
     } else {
         // ---------------------------------------------------- epilogue groups
         // group g = 4 warps, one per TMEM lane quarter (32 event rows each)
-        const int g = (warp - 2) >> 2, h = 0;
+        const int g = (warp - 2) >> 2;
         const int q = warp & 3;                 // TMEM lane quarter of this warp
         const int row = q * 32 + lane;          // event row of the tile = TMEM lane
-        uint8_t *abuf = abuf0 + g * A_BYTES;
-        const uint32_t t_hi = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(256 * g), t_lo = t_hi + 128;
+        uint8_t *abuf = abuf0 + g * S::REGION;
+        const uint32_t t_acc = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(128 * g);
         const int SN = 2 * E + 4;
-        constexpr bool SPLIT = false;           // (one warp per lane quarter: no column split)
-        constexpr int EH = E;
         constexpr int IDB = E <= 8 ? 3 : E <= 16 ? 4 : E <= 32 ? 5 : E <= 64 ? 6 : 7;   // id bits in a key
-        const bool feat_half = SPLIT || h == 0;   // halves that build layer-1 features
-        const int e_lo = SPLIT ? h * EH : 0;
-        // staging (the A buffer after the last layer's MMAs): fp32 scores
+        // staging (the region after the last layer's MMAs): fp32 scores
         // [row][E + 1] (odd stride: conflict-free columns), then rank rows [row][E + 16]
+        static_assert(BM * (E + 1) * 4 + BM * (E + 16) <= Shape<GROUPS>::REGION, "score staging");
         float *sc = (float *)abuf;
         uint32_t ar = 0;
         for (int64_t k = 0;; ++k) {
-            const int64_t t = (k * G + b) * 2 + g;
+            const int64_t t = (k * G + b) * GROUPS + g;
             if (t >= P.n_tiles) break;
             const int64_t c = t / P.tpc, ev0 = (t % P.tpc) * BM, ev = ev0 + row;
             const bool valid = ev < T;
             const int net = P.num_nets == 1 ? 0 : (int)(c % L);
+            const float *nb = P.bias + (int64_t)net * P.bias_stride;
+            const float *mult = nb + 2 * H + P.N3 + 3;   // epilogue multipliers of layers 1..3
+            bool bad = false;
             // this event's routed experts as a 128-bit mask
             uint32_t mine[4] = {0u, 0u, 0u, 0u};
             if (valid) {
@@ -412,9 +437,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
                 const int32_t f = __shfl_sync(0xFFFFFFFFu, sel(s_f, e >> 5), e & 31) + __popc(m & upto);
                 maxf = max(maxf, f);
             }
-            const float rmaxf = maxf > 0 ? 1.0f / (float)maxf : 0.0f;
+            // f / max_f, pre-scaled by 2^14 for fp16
+            const float rmaxf = maxf > 0 ? FEAT_SCALE / (float)maxf : 0.0f;
             named_sync(1 + g, 128);   // every thread is done with the previous tile's staging
-            // ---- layer-1 input: [1/r || f / max_f] (K = 2E, zero padded to KB1 * 64).
+            // ---- layer-1 input: [1/r || f / max_f] x 2^14 (K = 2E, zero padded to KB1 * 64).
             // E <= 64: one pass holds both halves; E = 128: recency, then frequency.
             for (int p = 0; p < P1; ++p) {
                 if (p > 0) {   // the previous pass's MMAs have consumed the A buffer
@@ -423,26 +449,24 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
                 }
                 const bool want_r = 2 * E <= 128 || p == 0, want_f = 2 * E <= 128 || p == 1;
                 const int kr = 2 * E <= 128 ? 0 : -128 * p, kf = 2 * E <= 128 ? E : E - 128 * p;
-                if (feat_half) {
 #pragma unroll 1
-                    for (int e0 = e_lo; e0 < e_lo + EH; e0 += 8) {
-                        float rv[8], fv[8];
+                for (int e0 = 0; e0 < E; e0 += 8) {
+                    float rv[8], fv[8];
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const int e = e0 + i;
-                            const uint32_t m = __ballot_sync(0xFFFFFFFFu, routes(mine, e));
-                            const uint32_t seen = m & upto;
-                            const int32_t sl = __shfl_sync(0xFFFFFFFFu, sel(s_last, e >> 5), e & 31);
-                            const int32_t sf = __shfl_sync(0xFFFFFFFFu, sel(s_f, e >> 5), e & 31);
-                            const int32_t lastu = seen ? u0 + (31 - __clz(seen)) + 1 : sl;
-                            rv[i] = lastu < 0 ? 0.0f : __fdividef(1.0f, (float)(u - lastu + 1));
-                            fv[i] = (float)(sf + __popc(seen)) * rmaxf;
-                        }
-                        if (want_r) store_chunk8(abuf, row, kr + e0, rv);
-                        if (want_f) store_chunk8(abuf, row, kf + e0, fv);
+                    for (int i = 0; i < 8; ++i) {
+                        const int e = e0 + i;
+                        const uint32_t m = __ballot_sync(0xFFFFFFFFu, routes(mine, e));
+                        const uint32_t seen = m & upto;
+                        const int32_t sl = __shfl_sync(0xFFFFFFFFu, sel(s_last, e >> 5), e & 31);
+                        const int32_t sf = __shfl_sync(0xFFFFFFFFu, sel(s_f, e >> 5), e & 31);
+                        const int32_t lastu = seen ? u0 + (31 - __clz(seen)) + 1 : sl;
+                        rv[i] = lastu < 0 ? 0.0f : __fdividef(FEAT_SCALE, (float)(u - lastu + 1));
+                        fv[i] = (float)(sf + __popc(seen)) * rmaxf;
                     }
+                    if (want_r) store_chunk8(abuf, row, kr + e0, rv);
+                    if (want_f) store_chunk8(abuf, row, kf + e0, fv);
                 }
-                if (p == P1 - 1 && h == 0) {   // zero padding up to the K blocks the MMAs read
+                if (p == P1 - 1) {   // zero padding up to the K blocks the MMAs read
                     const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                     for (int k0 = 2 * E - 128 * p; k0 < P.KB1 * 64 - 128 * p; k0 += 8) store_chunk8(abuf, row, k0, z);
                 }
@@ -450,17 +474,18 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(&feat_ready[g]);
             }
-            // ---- hidden layers: h = silu(acc_hi + acc_lo + bias) -> next A operand
+            // ---- hidden layers: h = silu(acc * 2^-s + bias) -> next A operand (x 2^8)
             for (int layer = 0; layer < 2; ++layer) {
                 mbar_wait(&acc_ready[g], ar & 1);
                 ++ar;
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const float *bias = P.bias + (int64_t)net * P.bias_stride + layer * H;
+                const float *bias = nb + layer * H;
+                const float mul = __ldg(mult + layer);
+                float hmax = 0.0f;
 #pragma unroll 1
                 for (int c0 = 0; c0 < H; c0 += 32) {
-                    uint32_t rh[32], rl[32];
-                    tmem_ld32_nowait(t_hi + c0, rh);
-                    tmem_ld32_nowait(t_lo + c0, rl);
+                    uint32_t ra[32];
+                    tmem_ld32_nowait(t_acc + c0, ra);
                     float4 b0 = __ldg((const float4 *)(bias + c0)), b1 = __ldg((const float4 *)(bias + c0) + 1);
                     tmem_wait_ld();
 #pragma unroll
@@ -472,39 +497,43 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
                         }
                         float v[8];
 #pragma unroll
-                        for (int i = 0; i < 8; ++i)
-                            v[i] = silu_f((__uint_as_float(rh[c8 + i]) + __uint_as_float(rl[c8 + i])) + bb[i]);
+                        for (int i = 0; i < 8; ++i) {
+                            const float z = fmaf(__uint_as_float(ra[c8 + i]), mul, bb[i]);
+                            const float h = __fdividef(z, 1.0f + __expf(-z));
+                            hmax = fmaxf(hmax, fabsf(h));
+                            v[i] = h * ACT_SCALE;
+                        }
                         store_chunk8(abuf, row, c0 + c8, v);
                     }
                 }
+                bad |= !(hmax <= 255.0f);   // fp16 range of the scaled activations (and NaN)
                 fence_async_smem();
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(&feat_ready[g]);
             }
-            // ---- scores: s = acc_hi + acc_lo + b3, one thread per event sorts
+            // ---- scores: s = acc * 2^-s + b3, one thread per event sorts
             // the E keys and certifies the order
             mbar_wait(&acc_ready[g], ar & 1);
             ++ar;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            bool bad = false;
             constexpr int EP = E;   // E is a power of two
             constexpr uint32_t M = (1u << IDB) - 1u;
-            if (h == 0) {
-                const float *b3 = P.bias + (int64_t)net * P.bias_stride + 2 * H;
+            {
+                const float *b3 = nb + 2 * H;
+                const float mul = __ldg(mult + 2);
                 float *srow = sc + row * (E + 1);
                 uint8_t *rrow = (uint8_t *)(sc + BM * (E + 1)) + row * (E + 16);
                 uint32_t key[EP];
 #pragma unroll
                 for (int c0 = 0; c0 < EP; c0 += 32) {
-                    uint32_t rh[32], rl[32];
-                    tmem_ld32_nowait(t_hi + c0, rh);
-                    tmem_ld32_nowait(t_lo + c0, rl);
+                    uint32_t ra[32];
+                    tmem_ld32_nowait(t_acc + c0, ra);
                     tmem_wait_ld();
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const int e = c0 + i;
                         if (e < E) {
-                            const float s = (__uint_as_float(rh[i]) + __uint_as_float(rl[i])) + __ldg(b3 + e);
+                            const float s = fmaf(__uint_as_float(ra[i]), mul, __ldg(b3 + e));
                             bad |= !isfinite(s);
                             srow[e] = s;
                             key[e] = (okey(s) & ~M) | (uint32_t)e;
@@ -544,14 +573,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            if (h == 0) {
+            {
                 const bool flagged = valid && bad;
                 if (flagged) {
                     const int slot = atomicAdd(P.flag_cnt + net, 1);
                     P.flag_list[(int64_t)net * P.bucket_cap + slot] = (int32_t)(c * T + ev);
                 }
-                const unsigned nb = __popc(__ballot_sync(0xFFFFFFFFu, flagged));
-                if (lane == 0 && nb) atomicAdd(P.stats + 5, (unsigned long long)nb);
+                const unsigned nbad = __popc(__ballot_sync(0xFFFFFFFFu, flagged));
+                if (lane == 0 && nbad) atomicAdd(P.stats + 5, (unsigned long long)nbad);
             }
         }
     }
@@ -559,14 +588,46 @@ __global__ void __launch_bounds__(THREADS, 1) k_score_tc(const __grid_constant__
     __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(S::TMEM_COLS));
     }
 }
 
-// Weight images: per net, the bf16 x 3 parts of W1 (N = 128, K = 2E padded to
-// a multiple of 64), W2 (128 x 128) and W3 (N3 x 128), as [N x 64] blocks in
-// the SWIZZLE_128B K-major layout in MMA consumption order (layer, K block,
-// part), and fp32 biases b1, b2, b3 (padded to N3).  params: .evnet order.
+// Per (net, layer): the power of two 2^s with max|w| * 2^s in [2^13, 2^14)
+// (fp16 range with headroom for the split; s clamped to +-100), and the
+// epilogue multiplier 2^-(s + activation scale).  One block per (net, layer).
+__global__ void k_wscale(const double *__restrict__ params, int E, int N3, float *__restrict__ bias, int bias_stride) {
+    const int net = blockIdx.x / 3, layer = blockIdx.x % 3;
+    const int D = 2 * E;
+    const int64_t src_per = (int64_t)D * H + H + (int64_t)H * H + H + (int64_t)E * H + E;
+    const double *src = params + net * src_per;
+    const double *w = layer == 0 ? src : layer == 1 ? src + (int64_t)D * H + H : src + (int64_t)D * H + H + (int64_t)H * H + H;
+    const int n = layer == 0 ? D * H : layer == 1 ? H * H : E * H;
+    double m = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, fabs(w[i]));
+    __shared__ double red[256];
+    red[threadIdx.x] = m;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        m = red[0];
+        int s = 0;
+        if (m > 0.0 && isfinite(m)) s = 13 - ilogb(m);
+        s = max(-100, min(100, s));
+        const int act = layer == 0 ? 14 : 8;   // FEAT_SCALE, ACT_SCALE
+        float *sc = bias + (int64_t)net * bias_stride + 2 * H + N3;
+        sc[layer] = ldexpf(1.0f, s);
+        sc[3 + layer] = ldexpf(1.0f, -(s + act));
+    }
+}
+
+// Weight images: per net, the fp16 x 2 parts of 2^s * W1 (N = 128, K = 2E
+// padded to a multiple of 64), 2^s * W2 (128 x 128) and 2^s * W3 (N3 x 128),
+// as [N x 64] blocks in the SWIZZLE_128B K-major layout in MMA consumption
+// order (layer, K block, part), and fp32 biases b1, b2, b3 (padded to N3).
+// params: .evnet order.  Runs after k_wscale.
 __global__ void k_prep_tc(const double *__restrict__ params, int E, int num_nets, int KB1, int N3,
                           int64_t net_bytes, uint8_t *__restrict__ wimg, float *__restrict__ bias, int bias_stride) {
     const int D = 2 * E;
@@ -589,35 +650,32 @@ __global__ void k_prep_tc(const double *__restrict__ params, int E, int num_nets
             layer = 2; n = (int)(r / 16); ch = (int)(r % 16);
             w = src + (int64_t)D * H + H + (int64_t)H * H + H; ldw = H; kmax = H; nmax = E;
         }
+        const double scale = (double)bias[(int64_t)net * bias_stride + 2 * H + N3 + layer];
         const int kb = ch >> 3, c8 = ch & 7, Nl = layer == 2 ? N3 : H;
-        uint32_t part[3][4];
+        uint32_t part[NPART][4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            uint16_t h[3][2];
+            uint16_t h[NPART][2];
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
                 const int kk = kb * 64 + c8 * 8 + 2 * j + hh;
-                const double x = (n < nmax && kk < kmax) ? w[(int64_t)n * ldw + kk] : 0.0;
-                const __nv_bfloat16 p0 = __double2bfloat16(x);
-                const double r1 = x - (double)__bfloat162float(p0);
-                const __nv_bfloat16 p1 = __double2bfloat16(r1);
-                const double r2 = r1 - (double)__bfloat162float(p1);
-                const __nv_bfloat16 p2 = __double2bfloat16(r2);
-                h[0][hh] = __bfloat16_as_ushort(p0);
-                h[1][hh] = __bfloat16_as_ushort(p1);
-                h[2][hh] = __bfloat16_as_ushort(p2);
+                const double x = (n < nmax && kk < kmax) ? w[(int64_t)n * ldw + kk] * scale : 0.0;
+                const __half p0 = __double2half(x);
+                const __half p1 = __double2half(x - (double)__half2float(p0));
+                h[0][hh] = __half_as_ushort(p0);
+                h[1][hh] = __half_as_ushort(p1);
             }
 #pragma unroll
-            for (int p = 0; p < 3; ++p) part[p][j] = (uint32_t)h[p][0] | ((uint32_t)h[p][1] << 16);
+            for (int p = 0; p < NPART; ++p) part[p][j] = (uint32_t)h[p][0] | ((uint32_t)h[p][1] << 16);
         }
         uint8_t *base = wimg + (int64_t)net * net_bytes;
         int64_t blk0;
-        if (layer == 0) blk0 = (int64_t)(kb * 3) * KBLK;
-        else if (layer == 1) blk0 = (int64_t)KB1 * 3 * KBLK + (int64_t)(kb * 3) * KBLK;
-        else blk0 = (int64_t)(KB1 + 2) * 3 * KBLK + (int64_t)(kb * 3) * N3 * ROWB;
+        if (layer == 0) blk0 = (int64_t)(kb * NPART) * KBLK;
+        else if (layer == 1) blk0 = (int64_t)KB1 * NPART * KBLK + (int64_t)(kb * NPART) * KBLK;
+        else blk0 = (int64_t)(KB1 + 2) * NPART * KBLK + (int64_t)(kb * NPART) * N3 * ROWB;
         const int64_t blk_bytes = (int64_t)Nl * ROWB;
 #pragma unroll
-        for (int p = 0; p < 3; ++p)
+        for (int p = 0; p < NPART; ++p)
             *(uint4 *)(base + blk0 + p * blk_bytes + sw128(n, c8)) =
                 make_uint4(part[p][0], part[p][1], part[p][2], part[p][3]);
         if (ch == 0) {   // biases (fp32)
@@ -635,9 +693,9 @@ __global__ void k_prep_tc(const double *__restrict__ params, int E, int num_nets
 
 size_t score_tc_net_bytes(int E) {
     const int KB1 = (2 * E + 63) / 64, N3 = (E + 15) / 16 * 16;
-    return (size_t)(KB1 + 2) * 3 * k3tc::KBLK + (size_t)2 * 3 * N3 * k3tc::ROWB;
+    return (size_t)(KB1 + 2) * k3tc::NPART * k3tc::KBLK + (size_t)2 * k3tc::NPART * N3 * k3tc::ROWB;
 }
-int score_tc_bias_stride(int E) { return 2 * k3tc::H + (E + 15) / 16 * 16; }
+int score_tc_bias_stride(int E) { return 2 * k3tc::H + (E + 15) / 16 * 16 + k3tc::NSCALE; }
 
 bool score_tc_eligible(const DevTrace &tr, int H) {
     return tr.uniform && H == k3tc::H && (tr.E == 8 || tr.E == 16 || tr.E == 32 || tr.E == 64 || tr.E == 128) &&
@@ -646,29 +704,42 @@ bool score_tc_eligible(const DevTrace &tr, int H) {
 
 static int g_num_sms = 0;
 
+template <int E, int GROUPS>
+static int set_smem() {
+    return cudaFuncSetAttribute(k3tc::k_score_tc<E, GROUPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                k3tc::Shape<GROUPS>::SMEM) == cudaSuccess ? 0 : -1;
+}
+
 int preload_score_tc() {
-    const void *fns[] = {(const void *)k3tc::k_score_tc<8>, (const void *)k3tc::k_score_tc<16>,
-                         (const void *)k3tc::k_score_tc<32>, (const void *)k3tc::k_score_tc<64>,
-                         (const void *)k3tc::k_score_tc<128>};
-    for (const void *f : fns)
-        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, k3tc::SMEM_BYTES) != cudaSuccess)
-            return -1;
+    if (set_smem<8, 3>() || set_smem<16, 3>() || set_smem<32, 3>() || set_smem<64, 3>() || set_smem<8, 2>() ||
+        set_smem<16, 2>() || set_smem<32, 2>() || set_smem<64, 2>() || set_smem<128, 2>())
+        return -1;
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     return 0;
 }
 
-// Launches: weight images, then the tensor-core scorer over every 128-event
-// tile (ranks + flag lists).  snaps: K3 snapshots (launch_score_prep).
+template <int E, int GROUPS>
+static void launch_tc(const k3tc::Params &P, cudaStream_t s) {
+    using S = k3tc::Shape<GROUPS>;
+    const int sms = g_num_sms > 0 ? g_num_sms : 148;
+    const unsigned grid = (unsigned)std::min<int64_t>(sms, (P.n_tiles + GROUPS - 1) / GROUPS);
+    k3tc::k_score_tc<E, GROUPS><<<grid, S::THREADS, S::SMEM, s>>>(P);
+}
+
+// Launches: weight scales + images, then the tensor-core scorer over every
+// 128-event tile (ranks + flag lists).  snaps: K3 snapshots (launch_score_prep).
+// groups: epilogue groups (3 or 2; E = 128 always runs 2).
 int launch_score_tc(const DevTrace &tr, const double *params, int num_nets, const int32_t *snaps, uint8_t *wimg,
                     float *bias, uint8_t *ranks, float tau, int32_t *flag_cnt, int32_t *flag_list, int64_t bucket_cap,
-                    unsigned long long *stats, float *dbg_scores, cudaStream_t s) {
+                    unsigned long long *stats, float *dbg_scores, int groups, cudaStream_t s) {
     using namespace k3tc;
     const int E = tr.E;
     const int KB1 = (2 * E + 63) / 64, N3 = (E + 15) / 16 * 16;
     const int64_t net_bytes = (int64_t)score_tc_net_bytes(E);
     const int bstride = score_tc_bias_stride(E);
+    k_wscale<<<num_nets * 3, 256, 0, s>>>(params, E, N3, bias, bstride);
     {
         const int64_t chunks = ((int64_t)H * KB1 * 8 + (int64_t)H * 16 + (int64_t)N3 * 16) * num_nets;
         const unsigned blocks = (unsigned)std::min<int64_t>((chunks + 255) / 256, 4096);
@@ -696,26 +767,22 @@ int launch_score_tc(const DevTrace &tr, const double *params, int num_nets, cons
     P.bucket_cap = bucket_cap;
     P.stats = stats;
     P.dbg_scores = dbg_scores;
-    if (P.n_tiles == 0) return 2;
-    const int sms = g_num_sms > 0 ? g_num_sms : 148;
-    const unsigned grid = (unsigned)std::min<int64_t>(sms, (P.n_tiles + 1) / 2);
+    if (P.n_tiles == 0) return 3;
+    const bool three = groups != 2;
     switch (E) {
-        case 8: k_score_tc<8><<<grid, THREADS, SMEM_BYTES, s>>>(P); break;
-        case 16: k_score_tc<16><<<grid, THREADS, SMEM_BYTES, s>>>(P); break;
-        case 32: k_score_tc<32><<<grid, THREADS, SMEM_BYTES, s>>>(P); break;
-        case 64: k_score_tc<64><<<grid, THREADS, SMEM_BYTES, s>>>(P); break;
-        default: k_score_tc<128><<<grid, THREADS, SMEM_BYTES, s>>>(P); break;
+        case 8: three ? launch_tc<8, 3>(P, s) : launch_tc<8, 2>(P, s); break;
+        case 16: three ? launch_tc<16, 3>(P, s) : launch_tc<16, 2>(P, s); break;
+        case 32: three ? launch_tc<32, 3>(P, s) : launch_tc<32, 2>(P, s); break;
+        case 64: three ? launch_tc<64, 3>(P, s) : launch_tc<64, 2>(P, s); break;
+        default: launch_tc<128, 2>(P, s); break;
     }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
-        cudaFuncAttributes a;
-        cudaFuncGetAttributes(&a, (const void *)k_score_tc<64>);
-        char b[256];
-        snprintf(b, sizeof b, "k_score_tc launch: %s (maxThreadsPerBlock %d, regs %d, local %zu, static smem %zu, "
-                 "max dyn smem %d, requested %d threads x %d B)", cudaGetErrorString(e), a.maxThreadsPerBlock,
-                 a.numRegs, a.localSizeBytes, a.sharedSizeBytes, a.maxDynamicSharedSizeBytes, THREADS, SMEM_BYTES);
+        char b[160];
+        snprintf(b, sizeof b, "k_score_tc launch (E = %d, %d groups): %s", E, E == 128 ? 2 : (three ? 3 : 2),
+                 cudaGetErrorString(e));
         mcb_set_error(MCB_ERR_CUDA, b);
         return -1;
     }
-    return 2;
+    return 3;
 }

@@ -6,7 +6,8 @@ seeded uniform(+-1/sqrt(fan_in)) initialisation so ``EvictionNet(E, seed=s)``
 is bit-identical to the reference's, and the same checkpoint bytes.  The B200
 engine consumes the parameters (converted once per call to the transposed
 device layout of K3); it never calls ``forward`` -- that host helper exists
-only for API compatibility.  Training stays out of scope.
+only for API compatibility.  Training (net.py:107-279) is train.py's GPU
+implementation (K10).
 """
 from __future__ import annotations
 

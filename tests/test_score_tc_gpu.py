@@ -5,7 +5,7 @@ scorer and the oracle.
   on every event, for every specialised expert count -- the certification
   plus the float64 re-score of the uncertified events make the fast path
   exact, not approximate.
-* The fp32 (bf16 x 3) scores deviate from the oracle's float64 forward by far
+* The fp32 (fp16 x 2 split) scores deviate from the oracle's float64 forward by far
   less than the certification threshold tau: the calibration that makes the
   certificate meaningful (the measured maximum is printed).
 * tau = 1 (every event re-scored) and tau = 0 (only collisions re-scored)
@@ -47,10 +47,11 @@ def _setup(L, E, K, T, n):
     return ids, dt, dn, (hidden, n_nets, flat)
 
 
-def _ranks(dt, dn, tc: bool, tau_ppb: int = 4000):
+def _ranks(dt, dn, tc: bool, tau_ppb: int = 4000, groups: int = 3):
     lib = _lib.load_library()
     _lib.set_tuning(_lib.MCB_TUNE_K3_TC, int(tc))
     _lib.set_tuning(_lib.MCB_TUNE_K3_TAU_PPB, tau_ppb)
+    _lib.set_tuning(_lib.MCB_TUNE_K3_GROUPS, groups)
     try:
         out = torch.zeros(dt.total_events * dt.num_experts + 64, dtype=torch.uint8, device="cuda")
         v, ns = dt.view(), dn.struct()
@@ -61,24 +62,26 @@ def _ranks(dt, dn, tc: bool, tau_ppb: int = 4000):
     finally:
         _lib.set_tuning(_lib.MCB_TUNE_K3_TC, 1)
         _lib.set_tuning(_lib.MCB_TUNE_K3_TAU_PPB, 4000)
+        _lib.set_tuning(_lib.MCB_TUNE_K3_GROUPS, 3)
     return out[:dt.total_events * dt.num_experts].cpu().numpy().reshape(-1, dt.num_experts), stats
 
 
+@pytest.mark.parametrize("groups", [3, 2])
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"E{s[1]}")
-def test_tc_ranks_equal_float64_ranks(shape):
+def test_tc_ranks_equal_float64_ranks(shape, groups):
     L, E, K, T, n = shape
     _, dt, dn, _ = _setup(L, E, K, T, n)
     r64, _ = _ranks(dt, dn, tc=False)
-    rtc, st = _ranks(dt, dn, tc=True)
+    rtc, st = _ranks(dt, dn, tc=True, groups=groups)
     rescored = st[5]
-    print(f"E={E}: {rescored} of {dt.total_events} events re-scored in float64 ({rescored / dt.total_events:.4%})")
+    print(f"E={E}, {groups} groups: {rescored} of {dt.total_events} events re-scored in float64 ({rescored / dt.total_events:.4%})")
     assert np.array_equal(rtc, r64)
     assert rescored < dt.total_events      # the fast path certified most events
 
 
 @pytest.mark.parametrize("shape", SHAPES[:3], ids=lambda s: f"E{s[1]}")
 def test_tc_scores_within_calibrated_error(shape):
-    """Normwise deviation of the bf16x3 / fp32 scores from the float64
+    """Normwise deviation of the fp16x2 / fp32 scores from the float64
     oracle, per event: max_e |s_tc - s_64| / max_e |s_64| << tau."""
     L, E, K, T, n = shape
     ids, dt, dn, nets = _setup(L, E, K, T, n)
@@ -142,3 +145,21 @@ def test_forced_near_ties_are_rescored_and_surfaced():
     st = _lib.read_stats()
     assert st[0] > 0                       # float64 near ties counted
     assert st[5] >= st[0]                  # every one of them went through the float64 re-score
+
+
+@pytest.mark.parametrize("wscale", [1e-3, 40.0])
+def test_scaled_weights_ranks_equal_float64(wscale):
+    """fp16's range: every layer's weights scaled by a large or a small
+    factor.  The per-layer power-of-two scaling keeps the split exact; with
+    large weights the hidden activations exceed the fp16-safe bound, those
+    events are flagged and re-scored in float64.  Ranks stay identical."""
+    L, E, K, T, n = 2, 64, 6, 1024, 2
+    ids = _ids(L, E, K, T, n)
+    dt = DeviceTrace.from_decode_ids(torch.from_numpy(ids).cuda(), E)
+    hidden, n_nets, flat = oracle.nets_from_spec({"kind": "per_layer_seed"}, L, E)
+    flat = flat * wscale
+    dn = DeviceNets(hidden, n_nets, flat, E)
+    r64, _ = _ranks(dt, dn, tc=False)
+    rtc, st = _ranks(dt, dn, tc=True)
+    print(f"weights x {wscale}: {st[5]} of {dt.total_events} events re-scored")
+    assert np.array_equal(rtc, r64)
