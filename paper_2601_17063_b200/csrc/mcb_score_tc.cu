@@ -79,7 +79,7 @@ struct Params {
     DevTrace tr;
     const uint8_t *wimg;        // per net: swizzled fp16 weight blocks (k_prep_tc)
     int64_t net_bytes;
-    const float *bias;          // per net: b1[128] b2[128] b3[N3] scales[NSCALE]
+    const float *bias;          // per net: b1[128] b2[128] b3[N3] scales[NSCALE] -log2(e)*b1[128] -log2(e)*b2[128]
     int bias_stride;
     int num_nets;
     int N3, KB1, P1;            // layer-3 N (E rounded up to 16), layer-1 K blocks, layer-1 passes
@@ -175,6 +175,18 @@ __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sy
 // st.shared writes become visible to the tensor core's async proxy
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+constexpr float LOG2E = 1.4426950408889634f;
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // byte offset of the 16-B chunk `ch` (0..7) of row `row` inside a
 // [rows x 64] fp16 block in the SWIZZLE_128B K-major layout
 __host__ __device__ __forceinline__ uint32_t sw128(int row, int ch) {
@@ -201,22 +213,6 @@ __device__ __forceinline__ void store_chunk8(uint8_t *abuf, int row, int k0, con
     for (int p = 0; p < NPART; ++p)
         *(uint4 *)(abuf + p * A_PART + off) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
 }
-
-// bit e of a 128-bit expert mask (word chosen by selects: no local memory)
-__device__ __forceinline__ uint32_t routes(const uint32_t (&m)[4], int e) {
-    const uint32_t w = e < 64 ? (e < 32 ? m[0] : m[1]) : (e < 96 ? m[2] : m[3]);
-    return (w >> (e & 31)) & 1u;
-}
-
-// a[w] without dynamic register indexing (w < N <= 4)
-template <int N>
-__device__ __forceinline__ int32_t sel(const int32_t (&a)[N], int w) {
-    if constexpr (N == 1) return a[0];
-    else if constexpr (N == 2) return w ? a[1] : a[0];
-    else return w < 2 ? (w ? a[1] : a[0]) : (w == 2 ? a[2] : a[3]);
-}
-
-__device__ __forceinline__ float silu_f(float z) { return __fdividef(z, 1.0f + __expf(-z)); }
 
 // order-preserving map of fp32 to uint32 (-0.0 canonicalised to +0.0)
 __device__ __forceinline__ uint32_t okey(float x) {
@@ -419,6 +415,7 @@ __global__ void __launch_bounds__(Shape<GROUPS>::THREADS, 1) k_score_tc(const __
             const bool has_snap = s32 < P.tpc32;
             const int32_t *sp = P.snaps + (c * P.tpc32 + (has_snap ? s32 : 0)) * SN;
             constexpr int NW = (E + 31) / 32;
+            constexpr int EW = E < 32 ? E : 32;   // experts per mask word
             int32_t s_last[NW], s_f[NW];
 #pragma unroll
             for (int j = 0; j < NW; ++j) {
@@ -431,11 +428,14 @@ __global__ void __launch_bounds__(Shape<GROUPS>::THREADS, 1) k_score_tc(const __
             const uint32_t upto = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);
             // max_f over experts at this event (features.py:44-52)
             int32_t maxf = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {   // 32-expert words: the word index is static
 #pragma unroll 8
-            for (int e = 0; e < E; ++e) {
-                const uint32_t m = __ballot_sync(0xFFFFFFFFu, routes(mine, e));
-                const int32_t f = __shfl_sync(0xFFFFFFFFu, sel(s_f, e >> 5), e & 31) + __popc(m & upto);
-                maxf = max(maxf, f);
+                for (int el = 0; el < EW; ++el) {
+                    const uint32_t m = __ballot_sync(0xFFFFFFFFu, (mine[w] >> el) & 1u);
+                    const int32_t f = __shfl_sync(0xFFFFFFFFu, s_f[w], el) + __popc(m & upto);
+                    maxf = max(maxf, f);
+                }
             }
             // f / max_f, pre-scaled by 2^14 for fp16
             const float rmaxf = maxf > 0 ? FEAT_SCALE / (float)maxf : 0.0f;
@@ -444,27 +444,31 @@ __global__ void __launch_bounds__(Shape<GROUPS>::THREADS, 1) k_score_tc(const __
             // E <= 64: one pass holds both halves; E = 128: recency, then frequency.
             for (int p = 0; p < P1; ++p) {
                 if (p > 0) {   // the previous pass's MMAs have consumed the A buffer
-                    mbar_wait(&acc_ready[g], ar & 1);
+                    mbar_wait_sleep(&acc_ready[g], ar & 1);
                     ++ar;
                 }
                 const bool want_r = 2 * E <= 128 || p == 0, want_f = 2 * E <= 128 || p == 1;
                 const int kr = 2 * E <= 128 ? 0 : -128 * p, kf = 2 * E <= 128 ? E : E - 128 * p;
-#pragma unroll 1
-                for (int e0 = 0; e0 < E; e0 += 8) {
-                    float rv[8], fv[8];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int e = e0 + i;
-                        const uint32_t m = __ballot_sync(0xFFFFFFFFu, routes(mine, e));
-                        const uint32_t seen = m & upto;
-                        const int32_t sl = __shfl_sync(0xFFFFFFFFu, sel(s_last, e >> 5), e & 31);
-                        const int32_t sf = __shfl_sync(0xFFFFFFFFu, sel(s_f, e >> 5), e & 31);
-                        const int32_t lastu = seen ? u0 + (31 - __clz(seen)) + 1 : sl;
-                        rv[i] = lastu < 0 ? 0.0f : __fdividef(FEAT_SCALE, (float)(u - lastu + 1));
-                        fv[i] = (float)(sf + __popc(seen)) * rmaxf;
+                for (int w = 0; w < NW; ++w) {
+#pragma unroll 1
+                    for (int e8 = 0; e8 < EW; e8 += 8) {
+                        float rv[8], fv[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int el = e8 + i;
+                            const uint32_t m = __ballot_sync(0xFFFFFFFFu, (mine[w] >> el) & 1u);
+                            const uint32_t seen = m & upto;
+                            const int32_t sl = __shfl_sync(0xFFFFFFFFu, s_last[w], el);
+                            const int32_t sf = __shfl_sync(0xFFFFFFFFu, s_f[w], el);
+                            const int32_t lastu = seen ? u0 + 32 - __clz(seen) : sl;
+                            rv[i] = lastu < 0 ? 0.0f : FEAT_SCALE * rcp_ftz((float)(u - lastu + 1));
+                            fv[i] = (float)(sf + __popc(seen)) * rmaxf;
+                        }
+                        const int e0 = 32 * w + e8;
+                        if (want_r) store_chunk8(abuf, row, kr + e0, rv);
+                        if (want_f) store_chunk8(abuf, row, kf + e0, fv);
                     }
-                    if (want_r) store_chunk8(abuf, row, kr + e0, rv);
-                    if (want_f) store_chunk8(abuf, row, kf + e0, fv);
                 }
                 if (p == P1 - 1) {   // zero padding up to the K blocks the MMAs read
                     const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -476,44 +480,46 @@ __global__ void __launch_bounds__(Shape<GROUPS>::THREADS, 1) k_score_tc(const __
             }
             // ---- hidden layers: h = silu(acc * 2^-s + bias) -> next A operand (x 2^8)
             for (int layer = 0; layer < 2; ++layer) {
-                mbar_wait(&acc_ready[g], ar & 1);
+                mbar_wait_sleep(&acc_ready[g], ar & 1);
                 ++ar;
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const float *bias = nb + layer * H;
-                const float mul = __ldg(mult + layer);
+                // u = -log2(e) * z in one FFMA (prescaled multiplier and bias),
+                // h * 2^8 = u * (-2^8 / log2(e)) * 1 / (1 + 2^u)
+                const float *nbias = nb + 2 * H + P.N3 + NSCALE + layer * H;
+                const float mul = __ldg(mult + layer) * -LOG2E;
                 float hmax = 0.0f;
 #pragma unroll 1
                 for (int c0 = 0; c0 < H; c0 += 32) {
                     uint32_t ra[32];
                     tmem_ld32_nowait(t_acc + c0, ra);
-                    float4 b0 = __ldg((const float4 *)(bias + c0)), b1 = __ldg((const float4 *)(bias + c0) + 1);
+                    float4 b0 = __ldg((const float4 *)(nbias + c0)), b1 = __ldg((const float4 *)(nbias + c0) + 1);
                     tmem_wait_ld();
 #pragma unroll
                     for (int c8 = 0; c8 < 32; c8 += 8) {
                         const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
                         if (c8 + 8 < 32) {
-                            b0 = __ldg((const float4 *)(bias + c0 + c8 + 8));
-                            b1 = __ldg((const float4 *)(bias + c0 + c8 + 8) + 1);
+                            b0 = __ldg((const float4 *)(nbias + c0 + c8 + 8));
+                            b1 = __ldg((const float4 *)(nbias + c0 + c8 + 8) + 1);
                         }
                         float v[8];
 #pragma unroll
                         for (int i = 0; i < 8; ++i) {
-                            const float z = fmaf(__uint_as_float(ra[c8 + i]), mul, bb[i]);
-                            const float h = __fdividef(z, 1.0f + __expf(-z));
-                            hmax = fmaxf(hmax, fabsf(h));
-                            v[i] = h * ACT_SCALE;
+                            const float uu = fmaf(__uint_as_float(ra[c8 + i]), mul, bb[i]);
+                            const float r = rcp_ftz(1.0f + ex2_ftz(uu));
+                            v[i] = (uu * (-ACT_SCALE / LOG2E)) * r;
+                            hmax = fmaxf(hmax, fabsf(v[i]));
                         }
                         store_chunk8(abuf, row, c0 + c8, v);
                     }
                 }
-                bad |= !(hmax <= 255.0f);   // fp16 range of the scaled activations (and NaN)
+                bad |= !(hmax <= 255.0f * ACT_SCALE);   // fp16 range of the scaled activations (and NaN)
                 fence_async_smem();
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(&feat_ready[g]);
             }
             // ---- scores: s = acc * 2^-s + b3, one thread per event sorts
             // the E keys and certifies the order
-            mbar_wait(&acc_ready[g], ar & 1);
+            mbar_wait_sleep(&acc_ready[g], ar & 1);
             ++ar;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             constexpr int EP = E;   // E is a power of two
@@ -682,8 +688,9 @@ __global__ void k_prep_tc(const double *__restrict__ params, int E, int num_nets
             float *bb = bias + (int64_t)net * bias_stride;
             const double *b1 = src + (int64_t)D * H, *b2 = b1 + H + (int64_t)H * H,
                          *b3 = b2 + H + (int64_t)E * H;
-            if (layer == 0) bb[n] = (float)b1[n];
-            else if (layer == 1) bb[H + n] = (float)b2[n];
+            float *nbb = bb + 2 * H + N3 + NSCALE;   // the hidden layers' biases times -log2(e)
+            if (layer == 0) { bb[n] = (float)b1[n]; nbb[n] = (float)(b1[n] * -1.4426950408889634); }
+            else if (layer == 1) { bb[H + n] = (float)b2[n]; nbb[H + n] = (float)(b2[n] * -1.4426950408889634); }
             else bb[2 * H + n] = n < E ? (float)b3[n] : 0.0f;
         }
     }
@@ -695,7 +702,7 @@ size_t score_tc_net_bytes(int E) {
     const int KB1 = (2 * E + 63) / 64, N3 = (E + 15) / 16 * 16;
     return (size_t)(KB1 + 2) * k3tc::NPART * k3tc::KBLK + (size_t)2 * k3tc::NPART * N3 * k3tc::ROWB;
 }
-int score_tc_bias_stride(int E) { return 2 * k3tc::H + (E + 15) / 16 * 16 + k3tc::NSCALE; }
+int score_tc_bias_stride(int E) { return 4 * k3tc::H + (E + 15) / 16 * 16 + k3tc::NSCALE; }
 
 bool score_tc_eligible(const DevTrace &tr, int H) {
     return tr.uniform && H == k3tc::H && (tr.E == 8 || tr.E == 16 || tr.E == 32 || tr.E == 64 || tr.E == 128) &&

@@ -29,6 +29,33 @@ constexpr int SH = 7;       // id bits of a packed key (E <= 128)
 static_assert(BS == 128 && SH == 7, "mm::ml_row_keys assumes 128-thread key columns and 7 id bits");
 constexpr uint32_t KMAX = (1u << (32 - SH)) - 1u;
 
+// Minimum packed key over the experts of a candidate mask: 32-bit words,
+// highest set bit first (one FLO per candidate), two candidates per trip so
+// two key loads are in flight.
+__device__ __forceinline__ uint32_t min_key_word(uint32_t w, uint32_t best, const uint32_t *sk) {
+    while (w) {
+        const int i = 31 - __clz(w);
+        w ^= 1u << i;
+        uint32_t k = sk[i * BS];
+        if (w) {
+            const int i2 = 31 - __clz(w);
+            w ^= 1u << i2;
+            k = min(k, sk[i2 * BS]);
+        }
+        best = min(best, k);
+    }
+    return best;
+}
+__device__ __forceinline__ uint32_t min_key(uint64_t cand, const uint32_t *sk) {
+    return min_key_word((uint32_t)(cand >> 32), min_key_word((uint32_t)cand, ~0u, sk), sk + 32 * BS);
+}
+__device__ __forceinline__ uint32_t min_key(M128 cand, const uint32_t *sk) {
+    uint32_t b = min_key_word((uint32_t)cand.lo, ~0u, sk);
+    b = min_key_word((uint32_t)(cand.lo >> 32), b, sk + 32 * BS);
+    b = min_key_word((uint32_t)cand.hi, b, sk + 64 * BS);
+    return min_key_word((uint32_t)(cand.hi >> 32), b, sk + 96 * BS);
+}
+
 template <int POL, bool UNIFORM, int WMAX, typename M>
 __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t chain, int pol_i, int cap_i,
                                               int ml_variant, uint32_t *sk) {
@@ -101,10 +128,7 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
                     if (!any(cand)) {
                         stuck = true;
                     } else {
-                        uint32_t best = ~0u;
-                        do {
-                            best = min(best, key(pop_first(cand)));
-                        } while (any(cand));
+                        const uint32_t best = min_key(cand, sk);
                         const uint32_t v = best & ((1u << SH) - 1u);
                         vbit = bit_of<M>(v);
                         code = v;
