@@ -66,13 +66,15 @@ constexpr float FEAT_SCALE = 16384.0f;    // layer-1 features in [0, 1] -> [0, 2
 constexpr float ACT_SCALE = 256.0f;       // hidden activations -> x 2^8 (|h| <= 255 certified)
 constexpr int NSCALE = 8;                 // per net: 2^s of layers 1..3, then their epilogue multipliers
 
-template <int GROUPS>
+template <int GROUPS, int E>
 struct Shape {
-    static constexpr int REGION = GROUPS == 3 ? 64 * 1024 : 88 * 1024;   // A parts + score staging
-    static constexpr int W_STAGES = GROUPS == 3 ? 2 : 3;
+    static constexpr int REGION = E == 128 ? 88 * 1024 : 64 * 1024;   // A parts + score staging
+    static constexpr int SMEM_MAX = 232448;                             // opt-in shared memory per block
+    static constexpr int W_STAGES = (SMEM_MAX - GROUPS * REGION - 1024 - 256) / W_STAGE;
     static constexpr int THREADS = 64 + 128 * GROUPS;
     static constexpr int SMEM = GROUPS * REGION + W_STAGES * W_STAGE + 1024 + 256;
     static constexpr int TMEM_COLS = GROUPS * 128 > 256 ? 512 : 256;
+    static_assert(W_STAGES >= 2, "the MMA order needs two weight stages");
 };
 
 struct Params {
@@ -220,6 +222,41 @@ __device__ __forceinline__ uint32_t okey(float x) {
     return b ^ ((uint32_t)((int32_t)b >> 31) | 0x80000000u);
 }
 
+// ascending sort network: Batcher's odd-even merge sort (543 comparators for
+// 64 keys against the bitonic network's 672), recursive templates so every
+// index is a compile-time constant (the keys stay in registers)
+template <int N>
+__device__ __forceinline__ void cswap(uint32_t (&v)[N], int a, int b) {
+    const uint32_t x = v[a], y = v[b];
+    v[a] = min(x, y);
+    v[b] = max(x, y);
+}
+template <int LO, int N, int R, int NV>
+__device__ __forceinline__ void oem_merge(uint32_t (&v)[NV]) {
+    constexpr int M = R * 2;
+    if constexpr (M < N) {
+        oem_merge<LO, N, M, NV>(v);
+        oem_merge<LO + R, N, M, NV>(v);
+#pragma unroll
+        for (int i = LO + R; i + R < LO + N; i += M) cswap(v, i, i + R);
+    } else {
+        cswap(v, LO, LO + R);
+    }
+}
+template <int LO, int N, int NV>
+__device__ __forceinline__ void oem_sort_range(uint32_t (&v)[NV]) {
+    if constexpr (N > 1) {
+        constexpr int M = N / 2;
+        oem_sort_range<LO, M, NV>(v);
+        oem_sort_range<LO + M, M, NV>(v);
+        oem_merge<LO, N, 1, NV>(v);
+    }
+}
+template <int N>
+__device__ __forceinline__ void oem_sort(uint32_t (&v)[N]) {
+    oem_sort_range<0, N, N>(v);
+}
+// bitonic network (E = 128: the odd-even network's live ranges spill there)
 template <int N>
 __device__ __forceinline__ void bitonic_sort(uint32_t (&v)[N]) {
 #pragma unroll
@@ -243,8 +280,8 @@ __device__ __forceinline__ void bitonic_sort(uint32_t (&v)[N]) {
 // group; per tile set the jobs (layer-1 passes, layer 2, layer 3) run in
 // order, the groups interleaved within each job.
 template <int E, int GROUPS>
-__global__ void __launch_bounds__(Shape<GROUPS>::THREADS, 1) k_score_tc(const __grid_constant__ Params P) {
-    using S = Shape<GROUPS>;
+__global__ void __launch_bounds__(Shape<GROUPS, E>::THREADS, 1) k_score_tc(const __grid_constant__ Params P) {
+    using S = Shape<GROUPS, E>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *abuf0 = smem;                         // group regions (A operand + score staging)
@@ -386,7 +423,7 @@ __global__ void __launch_bounds__(Shape<GROUPS>::THREADS, 1) k_score_tc(const __
         constexpr int IDB = E <= 8 ? 3 : E <= 16 ? 4 : E <= 32 ? 5 : E <= 64 ? 6 : 7;   // id bits in a key
         // staging (the region after the last layer's MMAs): fp32 scores
         // [row][E + 1] (odd stride: conflict-free columns), then rank rows [row][E + 16]
-        static_assert(BM * (E + 1) * 4 + BM * (E + 16) <= Shape<GROUPS>::REGION, "score staging");
+        static_assert(BM * (E + 1) * 4 + BM * (E + 16) <= S::REGION, "score staging");
         float *sc = (float *)abuf;
         uint32_t ar = 0;
         for (int64_t k = 0;; ++k) {
@@ -442,12 +479,14 @@ __global__ void __launch_bounds__(Shape<GROUPS>::THREADS, 1) k_score_tc(const __
             named_sync(1 + g, 128);   // every thread is done with the previous tile's staging
             // ---- layer-1 input: [1/r || f / max_f] x 2^14 (K = 2E, zero padded to KB1 * 64).
             // E <= 64: one pass holds both halves; E = 128: recency, then frequency.
-            for (int p = 0; p < P1; ++p) {
+            constexpr int P1C = 2 * E <= 128 ? 1 : 2;   // == P.P1
+#pragma unroll
+            for (int p = 0; p < P1C; ++p) {
                 if (p > 0) {   // the previous pass's MMAs have consumed the A buffer
-                    mbar_wait_sleep(&acc_ready[g], ar & 1);
+                    mbar_wait(&acc_ready[g], ar & 1);
                     ++ar;
                 }
-                const bool want_r = 2 * E <= 128 || p == 0, want_f = 2 * E <= 128 || p == 1;
+                const bool want_r = P1C == 1 || p == 0, want_f = P1C == 1 || p == 1;   // static per pass
                 const int kr = 2 * E <= 128 ? 0 : -128 * p, kf = 2 * E <= 128 ? E : E - 128 * p;
 #pragma unroll
                 for (int w = 0; w < NW; ++w) {
@@ -470,7 +509,7 @@ __global__ void __launch_bounds__(Shape<GROUPS>::THREADS, 1) k_score_tc(const __
                         if (want_f) store_chunk8(abuf, row, kf + e0, fv);
                     }
                 }
-                if (p == P1 - 1) {   // zero padding up to the K blocks the MMAs read
+                if (p == P1C - 1) {   // zero padding up to the K blocks the MMAs read
                     const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                     for (int k0 = 2 * E - 128 * p; k0 < P.KB1 * 64 - 128 * p; k0 += 8) store_chunk8(abuf, row, k0, z);
                 }
@@ -480,7 +519,7 @@ __global__ void __launch_bounds__(Shape<GROUPS>::THREADS, 1) k_score_tc(const __
             }
             // ---- hidden layers: h = silu(acc * 2^-s + bias) -> next A operand (x 2^8)
             for (int layer = 0; layer < 2; ++layer) {
-                mbar_wait_sleep(&acc_ready[g], ar & 1);
+                mbar_wait(&acc_ready[g], ar & 1);
                 ++ar;
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 // u = -log2(e) * z in one FFMA (prescaled multiplier and bias),
@@ -519,7 +558,7 @@ __global__ void __launch_bounds__(Shape<GROUPS>::THREADS, 1) k_score_tc(const __
             }
             // ---- scores: s = acc * 2^-s + b3, one thread per event sorts
             // the E keys and certifies the order
-            mbar_wait_sleep(&acc_ready[g], ar & 1);
+            mbar_wait(&acc_ready[g], ar & 1);
             ++ar;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             constexpr int EP = E;   // E is a power of two
@@ -546,7 +585,7 @@ __global__ void __launch_bounds__(Shape<GROUPS>::THREADS, 1) k_score_tc(const __
                         }
                     }
                 }
-                bitonic_sort<EP>(key);
+                if constexpr (E == 128) bitonic_sort<EP>(key); else oem_sort<EP>(key);
                 // certify: adjacent scores apart by more than 2 tau max|s|, no
                 // truncated-key collision (then the sorted order is the exact order)
                 const float smin = srow[key[0] & M], smax = srow[key[E - 1] & M];
@@ -714,7 +753,7 @@ static int g_num_sms = 0;
 template <int E, int GROUPS>
 static int set_smem() {
     return cudaFuncSetAttribute(k3tc::k_score_tc<E, GROUPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                k3tc::Shape<GROUPS>::SMEM) == cudaSuccess ? 0 : -1;
+                                k3tc::Shape<GROUPS, E>::SMEM) == cudaSuccess ? 0 : -1;
 }
 
 int preload_score_tc() {
@@ -729,7 +768,7 @@ int preload_score_tc() {
 
 template <int E, int GROUPS>
 static void launch_tc(const k3tc::Params &P, cudaStream_t s) {
-    using S = k3tc::Shape<GROUPS>;
+    using S = k3tc::Shape<GROUPS, E>;
     const int sms = g_num_sms > 0 ? g_num_sms : 148;
     const unsigned grid = (unsigned)std::min<int64_t>(sms, (P.n_tiles + GROUPS - 1) / GROUPS);
     k3tc::k_score_tc<E, GROUPS><<<grid, S::THREADS, S::SMEM, s>>>(P);
