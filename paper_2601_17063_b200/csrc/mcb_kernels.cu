@@ -756,7 +756,8 @@ int launch_replay(const ReplayParams &p, cudaStream_t s) {
     if (E <= 8 && solo_ok) { launch_solo_t<8>(p, s); return 1; }
     if (E <= 16 && solo_ok) { launch_solo_t<16>(p, s); return 1; }
     // many instances of 16 < E <= 128 (e.g. C4's 4,096 traces): one thread per instance
-    if (n_inst >= p.wide_min_instances && launch_replay_wide(p, s)) return 1;
+    if (n_inst >= p.wide_min_instances)
+        if (const int n_wide = launch_replay_wide(p, s)) return n_wide;   // one launch per policy
     // Lane-group size: one whole warp per instance by default.  Groups of 8 /
     // 16 lanes (4 / 2 instances per warp) are available through
     // MCB_TUNE_GROUP_LANES but measured slower even with many instances

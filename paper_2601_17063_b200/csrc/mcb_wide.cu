@@ -8,7 +8,15 @@
 //     shared memory, column-major per thread (keys[s][thread]), so the
 //     per-access key write is one conflict-free store whatever the expert;
 //   * the victim is the minimum key over the candidate bits only (at most C
-//     loads), and only on an evicting miss.
+//     loads), and only on an evicting miss;
+//   * LRU keeps no keys: a doubly linked recency list of the resident
+//     experts (byte links in shared memory) gives the victim in O(1) -- the
+//     tail is the minimum last-access position, and it is never pinned
+//     unless every resident expert is (pinned experts were accessed in the
+//     current event, after every other resident one);
+//   * ML keeps the event's rank row as bytes (one row per thread, four
+//     16-byte copies per event) and takes the maximum rank over the
+//     candidates (rank 0 = NaN / -inf score, never selectable).
 // Semantics are sstep()'s (mcb_solo.cuh) on wide masks: policies.py:95-214,
 // mlpolicy.py:15-26, engine.py:229-257 (pinning), engine.py:266-297 (refetch).
 // Used when there are enough instances to fill the GPU (many traces, e.g. C4).
@@ -26,7 +34,7 @@ using namespace mm;
 
 constexpr int BS = 128;     // threads per block
 constexpr int SH = 7;       // id bits of a packed key (E <= 128)
-static_assert(BS == 128 && SH == 7, "mm::ml_row_keys assumes 128-thread key columns and 7 id bits");
+static_assert(SH == 7, "packed keys carry 7 id bits (E <= 128)");
 constexpr uint32_t KMAX = (1u << (32 - SH)) - 1u;
 
 // Minimum packed key over the experts of a candidate mask: 32-bit words,
@@ -56,6 +64,35 @@ __device__ __forceinline__ uint32_t min_key(M128 cand, const uint32_t *sk) {
     return min_key_word((uint32_t)(cand.hi >> 32), b, sk + 96 * BS);
 }
 
+// Maximum (rank << 8 | expert) over the experts of a candidate mask, rank
+// bytes of this thread's row (mlpolicy.py:15-26: arg-max score; ranks are
+// distinct, 0 = not selectable).
+__device__ __forceinline__ uint32_t max_rank_word(uint32_t w, uint32_t best, const uint8_t *row, int e0) {
+    while (w) {
+        const int i = 31 - __clz(w);
+        w ^= 1u << i;
+        uint32_t k = ((uint32_t)row[i] << 8) | (uint32_t)(e0 + i);
+        if (w) {
+            const int i2 = 31 - __clz(w);
+            w ^= 1u << i2;
+            k = max(k, ((uint32_t)row[i2] << 8) | (uint32_t)(e0 + i2));
+        }
+        best = max(best, k);
+    }
+    return best;
+}
+__device__ __forceinline__ uint32_t max_rank(uint64_t cand, const uint8_t *row) {
+    return max_rank_word((uint32_t)(cand >> 32), max_rank_word((uint32_t)cand, 0u, row, 0), row + 32, 32);
+}
+__device__ __forceinline__ uint32_t max_rank(M128 cand, const uint8_t *row) {
+    uint32_t b = max_rank_word((uint32_t)cand.lo, 0u, row, 0);
+    b = max_rank_word((uint32_t)(cand.lo >> 32), b, row + 32, 32);
+    b = max_rank_word((uint32_t)cand.hi, b, row + 64, 64);
+    return max_rank_word((uint32_t)(cand.hi >> 32), b, row + 96, 96);
+}
+
+constexpr uint32_t NIL = 0xFFu;   // end of the LRU list
+
 template <int POL, bool UNIFORM, int WMAX, typename M>
 __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t chain, int pol_i, int cap_i,
                                               int ml_variant, uint32_t *sk) {
@@ -65,7 +102,14 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
     const int W = P.window;
     const int64_t inst = (chain * P.n_pol + pol_i) * P.n_cap + cap_i;
     auto key = [&](int s) -> uint32_t & { return sk[s * BS]; };
-    for (int s = 0; s < E; ++s) key(s) = (uint32_t)s;
+    if (POL != POL_LRU && POL != POL_ML)
+        for (int s = 0; s < E; ++s) key(s) = (uint32_t)s;
+    // LRU: next / prev links [2][E][BS] bytes; ML: this thread's rank row
+    uint8_t *const lb = (uint8_t *)(sk - threadIdx.x) + threadIdx.x;
+    auto nxt = [&](uint32_t e) -> uint8_t & { return lb[e * BS]; };
+    auto prv = [&](uint32_t e) -> uint8_t & { return lb[(E + e) * BS]; };
+    uint32_t head = NIL, tail = NIL;
+    uint8_t *const mrow = (uint8_t *)(sk - threadIdx.x) + threadIdx.x * (E + 16);
 
     M res = zero<M>(), seen = zero<M>(), ring_or = zero<M>();
     M ring[WMAX + 1];
@@ -102,9 +146,10 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
             uint8_t *m = P.res_masks + (e0 + ev) * E;
             for (int e = 0; e < E; ++e) m[e] = (uint8_t)test(res, (uint32_t)e);
         }
-        if (POL == POL_ML) {   // this event's rank row (mlpolicy.py:59-62): argmax score == argmin (256 - rank)
-            const uint8_t *row = rank + (e0 + ev) * E;
-            valid = ml_row_keys<M>(row, E, sk);
+        if (POL == POL_ML) {   // this event's rank row (mlpolicy.py:59-62), 16 bytes per copy
+            const uint4 *row = (const uint4 *)(rank + (e0 + ev) * E);
+#pragma unroll 2
+            for (int q = 0; q < E / 16; ++q) *(uint4 *)(mrow + 16 * q) = __ldcg(row + q);
         }
         M pin = zero<M>();
         uint32_t step_miss = 0;
@@ -112,7 +157,16 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
             const uint32_t x = ids.get(A);
             const M bit = bit_of<M>(x);
             // trace-determined key of x (applied before the victim search; x is never a candidate)
-            if (POL == POL_LRU) key(x) = (pos << SH) | x;
+            if (POL == POL_LRU && test(res, x) && x != head) {   // hit: move x to the front
+                const uint32_t p = prv(x), n = nxt(x);
+                nxt(p) = (uint8_t)n;
+                if (x == tail) tail = p;
+                else prv(n) = (uint8_t)p;
+                nxt(x) = (uint8_t)head;
+                prv(x) = (uint8_t)NIL;
+                prv(head) = (uint8_t)x;
+                head = x;
+            }
             if (POL == POL_LFU) key(x) += 1u << SH;
             if (POL == POL_BELADY) {
                 const uint32_t np = nx.get(A);
@@ -124,16 +178,47 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
                 M vbit = zero<M>();
                 code = MCB_OUT_MISS;
                 if ((uint32_t)popc(res) >= C) {
-                    M cand = res & ~pin & valid;
-                    if (!any(cand)) {
-                        stuck = true;
+                    if (POL == POL_LRU) {
+                        if (tail == NIL || test(pin, tail)) {   // every resident expert is pinned
+                            stuck = true;
+                        } else {
+                            const uint32_t v = tail;
+                            tail = prv(v);
+                            if (tail == NIL) head = NIL;
+                            else nxt(tail) = (uint8_t)NIL;
+                            vbit = bit_of<M>(v);
+                            code = v;
+                            ++nev;
+                        }
+                    } else if (POL == POL_ML) {
+                        const uint32_t best = max_rank(res & ~pin, mrow);
+                        if ((best >> 8) == 0u) {   // no candidate with a selectable score
+                            stuck = true;
+                        } else {
+                            const uint32_t v = best & 0xFFu;
+                            vbit = bit_of<M>(v);
+                            code = v;
+                            ++nev;
+                        }
                     } else {
-                        const uint32_t best = min_key(cand, sk);
-                        const uint32_t v = best & ((1u << SH) - 1u);
-                        vbit = bit_of<M>(v);
-                        code = v;
-                        ++nev;
+                        M cand = res & ~pin & valid;
+                        if (!any(cand)) {
+                            stuck = true;
+                        } else {
+                            const uint32_t best = min_key(cand, sk);
+                            const uint32_t v = best & ((1u << SH) - 1u);
+                            vbit = bit_of<M>(v);
+                            code = v;
+                            ++nev;
+                        }
                     }
+                }
+                if (POL == POL_LRU) {   // insert x at the front
+                    nxt(x) = (uint8_t)head;
+                    prv(x) = (uint8_t)NIL;
+                    if (head == NIL) tail = x;
+                    else prv(head) = (uint8_t)x;
+                    head = x;
                 }
                 res = (res & ~vbit) | bit;
                 refc += test(ring_or, x) ? 1u : 0u;   // refetch of an earlier victim within the window
@@ -188,9 +273,12 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
     if (P.hashes) P.hashes[inst] = h;
 }
 
+// All policies of the call in one launch (blockIdx.y = policy), so the
+// instances of every policy share the waves; blockIdx.x * BS + threadIdx.x =
+// (chain, capacity) instance.
 template <bool UNIFORM, typename M>
-__global__ void __launch_bounds__(BS) k_replay_wide(const __grid_constant__ ReplayParams P) {
-    extern __shared__ uint32_t s_keys[];   // [E][BS]
+__global__ void __launch_bounds__(BS, sizeof(M) == 8 ? 5 : 4) k_replay_wide(const __grid_constant__ ReplayParams P) {
+    extern __shared__ uint32_t s_keys[];   // [E][BS] keys, LRU links or ML rank rows
     const int pol_i = P.pol_map[blockIdx.y];
     const int64_t t = (int64_t)blockIdx.x * BS + threadIdx.x;
     if (t >= (P.chain_hi - P.chain_lo) * P.n_cap) return;
@@ -205,6 +293,14 @@ __global__ void __launch_bounds__(BS) k_replay_wide(const __grid_constant__ Repl
         case MCB_FIFO: wide_instance<POL_FIFO, UNIFORM, SOLO_WMAX, M>(P, chain, pol_i, cap_i, 0, sk); break;
         default: wide_instance<POL_ML, UNIFORM, SOLO_WMAX, M>(P, chain, pol_i, cap_i, 1, sk); break;
     }
+}
+
+template <bool UNIFORM, typename M>
+int set_wide_smem(size_t smem) {
+    const void *f = (const void *)k_replay_wide<UNIFORM, M>;
+    cudaFuncAttributes a;
+    if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
+    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess ? 0 : -1;
 }
 
 }  // namespace wide
@@ -234,15 +330,9 @@ int launch_replay_wide(const ReplayParams &p, cudaStream_t s) {
 }
 
 int preload_wide_kernels() {
-    const void *fns[] = {(const void *)wide::k_replay_wide<true, uint64_t>,
-                         (const void *)wide::k_replay_wide<false, uint64_t>,
-                         (const void *)wide::k_replay_wide<true, mm::M128>,
-                         (const void *)wide::k_replay_wide<false, mm::M128>};
-    for (const void *f : fns) {
-        cudaFuncAttributes a;
-        if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
-        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * wide::BS * 4) != cudaSuccess)
-            return -1;
-    }
+    const size_t smem = 128 * wide::BS * 4;
+    if (wide::set_wide_smem<true, uint64_t>(smem) || wide::set_wide_smem<false, uint64_t>(smem) ||
+        wide::set_wide_smem<true, mm::M128>(smem) || wide::set_wide_smem<false, mm::M128>(smem))
+        return -1;
     return 0;
 }
