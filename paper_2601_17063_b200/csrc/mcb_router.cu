@@ -11,19 +11,35 @@
 // The reference has no GEMM generator: parity is against
 // torch (tests/test_router_gpu.py).
 //
-// One CTA per 128-token x 256-column output tile:
-//   warp 0      TMA producer: 128x64 hidden tile + 256x64 weight tile per
-//               stage (SWIZZLE_128B, K-major), 4-stage mbarrier ring
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//               (M=128, N=256, K=16 per instruction, fp32 accumulator in
-//               256 TMEM columns), tcgen05.commit frees smem stages
-//   warps 2..5  epilogue: tcgen05.ld 32 columns at a time, running top-k per
-//               layer segment in registers, uint8 ids to HBM
+// Persistent kernel, one CTA per SM, 256-token x 128-column tiles:
+//   warp 0      TMA producer: 256x64 hidden tile + 128x64 weight tile per
+//               stage (SWIZZLE_128B, K-major), 4-stage mbarrier ring (48 KB
+//               per stage; the weight tile is shared by both token halves)
+//   warp 1      TMEM allocator (512 columns) + the single tcgen05.mma issuer:
+//               per K step, M=128 N=128 K=16 for each 128-token half into
+//               its own 128-column fp32 accumulator; two accumulator sets
+//               (2 x 256 columns) so the MMAs of tile i+1 run while the
+//               epilogue drains tile i
+//   warps 2..9  epilogue (warp w: TMEM lane quarter w % 4, token half
+//               (w - 2) / 4): tcgen05.ld 32 columns at a time; every logit
+//               becomes a 32-bit key (order-preserving float bits, low 7
+//               bits = 127 - expert) and is inserted branch-free into the
+//               running top-K of its layer segment (max/min exchange chain:
+//               no divergence between the lanes' tokens); uint8 ids to HBM.
+// Tiles are taken round-robin (tile = k * grid + blockIdx.x), n fastest, so
+// the ~150 tiles in flight share a few hidden m-blocks and the whole gate
+// matrix in L2.
+//
+// Keys keep the top 25 bits of the order-preserving logit (2^-16 relative):
+// logits closer than that are ordered by expert id.  That is far below the
+// difference between this kernel's fp32 summation order and torch's (the
+// near-tie bound of tests/test_router_gpu.py is 4e-3 absolute).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 
@@ -31,10 +47,13 @@
 
 namespace k1 {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int BM = 256, BN = 128, BK = 64, STAGES = 4;   // BM = two M=128 MMA halves
 constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int HALF_A = 128 * BK * 2;   // 16 KB: rows 128..255 of the A tile
 constexpr int KMAX = 8;             // top-k capacity of the epilogue (K <= 8)
-constexpr int THREADS = 192;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
+constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -52,6 +71,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
@@ -77,8 +100,8 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
     return d;
 }
 
-// instruction descriptor, kind::f16: D=f32, A=B=bf16, both K-major, M=128, N=256
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// instruction descriptor, kind::f16: D=f32, A=B=bf16, both K-major, M=128, N=BN
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 
 __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
     asm volatile(
@@ -109,54 +132,57 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// order-preserving map of fp32 to uint32 (-0.0 canonicalised to +0.0)
+__device__ __forceinline__ uint32_t okey(float x) {
+    const uint32_t b = __float_as_uint(x + 0.0f);
+    return b ^ ((uint32_t)((int32_t)b >> 31) | 0x80000000u);
+}
+
+// Running top-K of packed keys, descending; insertion is a max/min exchange
+// chain (the same instructions whatever the lane's data).
 struct TopK {
-    float v[KMAX];
-    int i[KMAX];
+    uint32_t v[KMAX];
     __device__ __forceinline__ void reset() {
 #pragma unroll
-        for (int k = 0; k < KMAX; ++k) { v[k] = -INFINITY; i[k] = 0x7FFFFFFF; }
+        for (int k = 0; k < KMAX; ++k) v[k] = 0u;
     }
-    // columns arrive in ascending id order: strict '>' keeps the lower id on ties
-    __device__ __forceinline__ void push(float x, int id) {
-        if (x > v[KMAX - 1]) {
-            v[KMAX - 1] = x;
-            i[KMAX - 1] = id;
+    __device__ __forceinline__ void push(uint32_t x) {
 #pragma unroll
-            for (int k = KMAX - 1; k > 0; --k) {
-                if (v[k] > v[k - 1]) {
-                    const float tv = v[k]; v[k] = v[k - 1]; v[k - 1] = tv;
-                    const int ti = i[k]; i[k] = i[k - 1]; i[k - 1] = ti;
-                }
-            }
+        for (int k = 0; k < KMAX; ++k) {
+            const uint32_t hi = max(x, v[k]);
+            x = min(x, v[k]);
+            v[k] = hi;
         }
     }
 };
 
 __global__ void __launch_bounds__(THREADS, 1)
 router_topk_kernel(const __grid_constant__ CUtensorMap map_h, const __grid_constant__ CUtensorMap map_w, int T, int Dp,
-                   int L, int E, int Ep, int K, uint8_t *__restrict__ acc, float *__restrict__ logits, int N_total) {
+                   int L, int E, int lgEp, int K, uint8_t *__restrict__ acc, float *__restrict__ logits, int N_total) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for the swizzle atoms
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t *full = (uint64_t *)(smem + STAGES * STAGE_BYTES);
     uint64_t *empty = full + STAGES;
-    uint64_t *tmem_full = empty + STAGES;
-    uint32_t *tmem_slot = (uint32_t *)(tmem_full + 1);
+    uint64_t *tfull = empty + STAGES;     // [2] accumulator set ready
+    uint64_t *tempty = tfull + 2;         // [2] accumulator set drained (EPI_WARPS arrivals)
+    uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
     const int nk = Dp / BK;
+    const int tiles_n = (N_total + BN - 1) / BN;
+    const int64_t n_tiles = (int64_t)((T + BM - 1) / BM) * tiles_n;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        mbar_init(tmem_full, 1);
+        for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], EPI_WARPS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_h)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_w)) : "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(BN));
+                     "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -166,69 +192,93 @@ router_topk_kernel(const __grid_constant__ CUtensorMap map_h, const __grid_const
 
     if (warp == 0) {
         if (lane == 0) {
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
-                mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-                uint8_t *sa = smem + s * STAGE_BYTES;
-                tma_load_2d(sa, &map_h, &full[s], kb * BK, m0);
-                tma_load_2d(sa + A_BYTES, &map_w, &full[s], kb * BK, n0);
+            uint32_t it = 0;
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+                const int m0 = (int)(t / tiles_n) * BM, n0 = (int)(t % tiles_n) * BN;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+                    uint8_t *sa = smem + s * STAGE_BYTES;
+                    tma_load_2d(sa, &map_h, &full[s], kb * BK, m0);
+                    tma_load_2d(sa + A_BYTES, &map_w, &full[s], kb * BK, n0);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                mbar_wait(&full[s], (kb / STAGES) & 1);
+            uint32_t it = 0, ti = 0;
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++ti) {
+                const uint32_t buf = ti & 1, d = tmem + 256 * buf;
+                mbar_wait(&tempty[buf], ((ti >> 1) & 1) ^ 1);   // the epilogue drained this set
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
-                const uint32_t sb = sa + A_BYTES;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&full[s], (it / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
+                    const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-                    // advance 16 bf16 = 32 B along K inside the swizzled rows
-                    mma_bf16(tmem, make_desc(sa + k * 32), make_desc(sb + k * 32), (kb > 0 || k > 0) ? 1u : 0u);
+                    for (int k = 0; k < BK / 16; ++k) {
+                        // advance 16 bf16 = 32 B along K inside the swizzled rows
+                        const uint64_t db = make_desc(sb + k * 32);
+                        const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+                        mma_bf16(d, make_desc(sa + k * 32), db, accum);
+                        mma_bf16(d + 128, make_desc(sa + HALF_A + k * 32), db, accum);
+                    }
+                    mma_commit(&empty[s]);
                 }
-                mma_commit(&empty[s]);
+                mma_commit(&tfull[buf]);
             }
-            mma_commit(tmem_full);
         }
     } else {
-        // epilogue: warp (2..5) owns TMEM lanes 32*(warp%4) .. +31 = tokens of the tile
-        const int q = warp & 3;
-        const int row = q * 32 + lane;
-        const int t = m0 + row;
-        mbar_wait(tmem_full, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        TopK tk;
-        tk.reset();
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-            float v[32];
-            tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
-            if (logits != nullptr && t < T) {
+        const int q = warp & 3, h = (warp - 2) >> 2;   // TMEM lane quarter, token half
+        const uint32_t Ep1 = (1u << lgEp) - 1u;
+        uint32_t ti = 0;
+        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++ti) {
+            const uint32_t buf = ti & 1;
+            const int m0 = (int)(t / tiles_n) * BM, n0 = (int)(t % tiles_n) * BN;
+            const int tok = m0 + h * 128 + q * 32 + lane;
+            mbar_wait(&tfull[buf], (ti >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            TopK tk;
+            tk.reset();
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                float v[32];
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + 256 * buf + 128 * h + (uint32_t)c0, v);
+                if (logits != nullptr && tok < T) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (n0 + c0 + j < N_total) logits[(int64_t)t * N_total + n0 + c0 + j] = v[j];
-            }
+                    for (int j = 0; j < 32; ++j)
+                        if (n0 + c0 + j < N_total) logits[(int64_t)tok * N_total + n0 + c0 + j] = v[j];
+                }
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const int n = n0 + c0 + j;
-                const int layer = n / Ep, e = n - layer * Ep;
-                if (e < E && layer < L) tk.push(v[j], e);
-                if (e == Ep - 1) {
-                    if (layer < L && t < T) {
-                        uint8_t *dst = acc + ((int64_t)layer * T + t) * K;
-                        for (int k = 0; k < K; ++k) dst[k] = (uint8_t)tk.i[k];
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t n = (uint32_t)(n0 + c0 + j);
+                    const uint32_t e = n & Ep1;
+                    if ((int)e < E) tk.push((okey(v[j]) & ~127u) | (127u - e));
+                    if (e == Ep1) {   // end of a layer segment
+                        const int layer = (int)(n >> lgEp);
+                        if (layer < L && tok < T) {
+                            uint8_t *dst = acc + ((int64_t)layer * T + tok) * K;
+#pragma unroll
+                            for (int k = 0; k < KMAX; ++k)   // static indices: tk stays in registers
+                                if (k < K) dst[k] = (uint8_t)(127u - (tk.v[k] & 127u));
+                        }
+                        tk.reset();
                     }
-                    tk.reset();
                 }
             }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
     }
 }
 
@@ -264,12 +314,16 @@ int make_map(CUtensorMap *map, const void *base, uint64_t rows, uint64_t cols, u
 
 }  // namespace k1
 
+static int k1_num_sms = 0;
+
 int mcb_router_preload() {
     cudaFuncAttributes a;
     if (cudaFuncGetAttributes(&a, (const void *)k1::router_topk_kernel) != cudaSuccess)
         return mcb_set_error(MCB_ERR_CUDA, "failed to load the router kernel");
-    const size_t smem = (size_t)k1::STAGES * k1::STAGE_BYTES + 1024 + 256;
-    cudaFuncSetAttribute(k1::router_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k1::router_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, k1::SMEM);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&k1_num_sms, cudaDevAttrMultiProcessorCount, dev);
     return MCB_OK;
 }
 
@@ -284,17 +338,17 @@ extern "C" int mcb_router_topk(mcb_ctx *ctx, const void *hidden, const void *wei
     if (d < k1::BK || d % k1::BK) return mcb_set_error(MCB_ERR_INVALID, "hidden dim must be a multiple of 64");
     if (L < 1 || E < 1 || E > MCB_MAX_EXPERTS || K < 1 || K > E || K > k1::KMAX)
         return mcb_set_error(MCB_ERR_INVALID, "need 1 <= K <= min(E, 8), E <= 128");
-    int Ep = 8;
-    while (Ep < E) Ep *= 2;  // power of two, divides 256
+    int Ep = 8, lgEp = 3;
+    while (Ep < E) { Ep *= 2; ++lgEp; }  // power of two, divides the 128-column tile
     const int64_t N = (int64_t)L * Ep;
     CUtensorMap mh, mw;
-    if (int rc = k1::make_map(&mh, hidden, (uint64_t)T, (uint64_t)d, k1::BM)) return rc;
-    if (int rc = k1::make_map(&mw, weight, (uint64_t)N, (uint64_t)d, k1::BN)) return rc;
-    const size_t smem = (size_t)k1::STAGES * k1::STAGE_BYTES + 1024 + 256;
-    cudaFuncSetAttribute(k1::router_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 grid((unsigned)((T + k1::BM - 1) / k1::BM), (unsigned)((N + k1::BN - 1) / k1::BN));
-    k1::router_topk_kernel<<<grid, k1::THREADS, smem, (cudaStream_t)stream>>>(mh, mw, (int)T, d, L, E, Ep, K, acc, logits,
-                                                                               (int)N);
+    if (int rc = k1::make_map(&mh, hidden, (uint64_t)T, (uint64_t)d, k1::BM)) return rc;   // 256-row boxes
+    if (int rc = k1::make_map(&mw, weight, (uint64_t)N, (uint64_t)d, k1::BN)) return rc;   // 128-row boxes
+    const int64_t tiles = ((T + k1::BM - 1) / k1::BM) * ((N + k1::BN - 1) / k1::BN);
+    const int sms = k1_num_sms > 0 ? k1_num_sms : 148;
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+    k1::router_topk_kernel<<<grid, k1::THREADS, k1::SMEM, (cudaStream_t)stream>>>(mh, mw, (int)T, d, L, E, lgEp, K, acc,
+                                                                                  logits, (int)N);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return mcb_set_error(MCB_ERR_CUDA, cudaGetErrorString(e));
     return MCB_OK;
