@@ -244,9 +244,11 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
  * every two adjacent scores differ by more than 2 * tau * max|s|; tau in units
  * of 1e-9 (default 4000 = 4e-6).  Larger = more events re-scored in float64. */
 #define MCB_TUNE_K3_TAU_PPB 13
-/* MCB_TUNE_K3_GROUPS: epilogue groups (128-event tiles in flight per SM) of
- * the tensor-core scorer for num_experts <= 64: 3 (default) or 2.
- * num_experts = 128 always runs 2.  Ranks are identical. */
+/* MCB_TUNE_K3_GROUPS: layout of the tensor-core scorer for num_experts <= 64:
+ * 3 (default) or 2 epilogue groups (128-event tiles in flight per SM) with
+ * the MMA operands in shared memory, or 1 = two groups with the operands in
+ * TMEM and a deep weight ring.  num_experts = 128 always runs 2 groups with
+ * shared-memory operands.  Ranks are identical. */
 #define MCB_TUNE_K3_GROUPS 14
 int mcb_set_tuning(mcb_ctx *ctx, int32_t knob, int64_t value);
 /* LeCaR parameters used by the MCB_LECAR cells of later mcb_replay calls on

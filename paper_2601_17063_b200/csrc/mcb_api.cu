@@ -245,7 +245,7 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
         return MCB_OK;
     }
     if (knob == MCB_TUNE_K3_GROUPS) {
-        if (value != 2 && value != 3) return mcb_set_error(MCB_ERR_INVALID, "K3 groups must be 2 or 3");
+        if (value < 1 || value > 3) return mcb_set_error(MCB_ERR_INVALID, "K3 variant must be 1, 2 or 3");
         c->k3_groups = (int)value;
         return MCB_OK;
     }
@@ -318,7 +318,7 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     if (const char *env = getenv("MCB_SCRATCH_BYTES")) c->scratch_bytes = atoll(env);
     if (const char *env = getenv("MCB_K3_TC")) c->k3_tc = atoi(env);
     if (const char *env = getenv("MCB_K3_TAU_PPB")) c->k3_tau_ppb = atoll(env);
-    if (const char *env = getenv("MCB_K3_GROUPS")) c->k3_groups = atoi(env) == 2 ? 2 : 3;
+    if (const char *env = getenv("MCB_K3_GROUPS")) c->k3_groups = std::max(1, std::min(3, atoi(env)));
     for (auto &e : c->chunk_ev)
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
             delete c;

@@ -49,6 +49,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <type_traits>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -67,15 +69,22 @@ constexpr float FEAT_SCALE = 16384.0f;    // layer-1 features in [0, 1] -> [0, 2
 constexpr float ACT_SCALE = 256.0f;       // hidden activations -> x 2^8 (|h| <= 255 certified)
 constexpr int NSCALE = 8;                 // per net: 2^s of layers 1..3, then their epilogue multipliers
 
-template <int GROUPS, int E>
+// TA = activations (the MMA's A operand) in TMEM instead of shared memory:
+// 2 groups x (128 accumulator + 128 operand columns), and the shared memory
+// left to the score staging goes to a deep weight ring.
+template <int GROUPS, int E, bool TA = false>
 struct Shape {
-    static constexpr int REGION = E == 128 ? 88 * 1024 : 64 * 1024;   // A parts + score staging
+    static constexpr int STAGING = ((BM * (E + 1) * 4 + BM * (E + 16)) + 1023) / 1024 * 1024;
+    static constexpr int REGION = TA ? STAGING : (E == 128 ? 88 * 1024 : 64 * 1024);   // [A parts +] staging
     static constexpr int SMEM_MAX = 232448;                             // opt-in shared memory per block
-    static constexpr int W_STAGES = (SMEM_MAX - GROUPS * REGION - 1024 - 256) / W_STAGE;
+    static constexpr int W_STAGES_FIT = (SMEM_MAX - GROUPS * REGION - 1024 - 256) / W_STAGE;
+    static constexpr int W_STAGES = W_STAGES_FIT > 8 ? 8 : W_STAGES_FIT;
     static constexpr int THREADS = 64 + 128 * GROUPS;
     static constexpr int SMEM = GROUPS * REGION + W_STAGES * W_STAGE + 1024 + 256;
-    static constexpr int TMEM_COLS = GROUPS * 128 > 256 ? 512 : 256;
-    static_assert(W_STAGES >= 2, "the MMA order needs two weight stages");
+    static constexpr int TMEM_COLS = (TA ? 256 : 128) * GROUPS > 256 ? 512 : 256;
+    static constexpr int D_STRIDE = TA ? 256 : 128;                     // TMEM columns per group
+    static_assert(W_STAGES >= (TA ? 4 : 2), "the MMA order holds a job's blocks (TA: all four)");
+    static_assert(!TA || GROUPS * 256 <= 512, "TMEM: 256 columns per group");
 };
 
 struct Params {
@@ -157,6 +166,30 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t d
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(da), "l"(db), "r"(id), "r"(acc));
 }
+// A operand from TMEM (tcgen05.mma ... [d], [a], b_desc): M=128 rows = lanes,
+// two fp16 K values per 32-bit column (lower K in the low half)
+__device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t id, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(db), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&r)[4]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
+                 "r"(r[2]), "r"(r[3])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -280,9 +313,9 @@ __device__ __forceinline__ void bitonic_sort(uint32_t (&v)[N]) {
 // the k-th tile set of CTA b is tiles (k * G + b) * GROUPS + g, g = epilogue
 // group; per tile set the jobs (layer-1 passes, layer 2, layer 3) run in
 // order, the groups interleaved within each job.
-template <int E, int GROUPS>
-__global__ void __launch_bounds__(Shape<GROUPS, E>::THREADS, 1) k_score_tc(const __grid_constant__ Params P) {
-    using S = Shape<GROUPS, E>;
+template <int E, int GROUPS, bool TA>
+__global__ void __launch_bounds__(Shape<GROUPS, E, TA>::THREADS, 1) k_score_tc(const __grid_constant__ Params P) {
+    using S = Shape<GROUPS, E, TA>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *abuf0 = smem;                         // group regions (A operand + score staging)
@@ -355,6 +388,8 @@ __global__ void __launch_bounds__(Shape<GROUPS, E>::THREADS, 1) k_score_tc(const
         }
     } else if (warp == 1) {
         // ------------------------------------------------------- MMA issuer
+        // (lane 0 alone: the whole warp polling the barriers costs the epilogue
+        // warps more issue slots than uniform operand arithmetic saves)
         if (lane == 0) {
             uint32_t it = 0, fr[GROUPS];
 #pragma unroll
@@ -370,9 +405,10 @@ __global__ void __launch_bounds__(Shape<GROUPS, E>::THREADS, 1) k_score_tc(const
                         mbar_wait_sleep(&feat_ready[g], fr[g] & 1);
                         ++fr[g];
                         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                        const uint32_t d = tmem + (uint32_t)(128 * g);
+                        const uint32_t d = tmem + (uint32_t)(S::D_STRIDE * g);
                         const uint32_t id = idesc(job_n(j));
                         const uint32_t a_base = smem_u32(abuf0 + g * S::REGION);
+                        const uint32_t a_tm = d + 128;   // TA: the group's operand columns
                         bool fresh = !(j > 0 && j < P1);   // layer-1 passes > 0 accumulate
                         const int nkb = job_kblocks(j);
                         // Small products first, the leading a0*w0 last: the cross terms
@@ -380,13 +416,31 @@ __global__ void __launch_bounds__(Shape<GROUPS, E>::THREADS, 1) k_score_tc(const
                         // is still small, so the accumulator's alignment to its running
                         // magnitude costs them nothing; then a0*w0 over the same K blocks.
                         // The ring holds the job's <= 2 part-0 blocks at once (W_STAGES >= 2).
-                        auto issue = [&](uint32_t a_part, uint32_t w_base, int kbl) {
-                            const uint32_t a0 = a_base + a_part * A_PART + kbl * KBLK;
+                        // layer-1 K steps stop at 2E (E = 8, 16: the rest of the block is padding)
+                        constexpr int NS1 = 2 * E < 64 ? 2 * E / 16 : 4;
+                        const bool short_k = NS1 < 4 && j < P1;
+                        auto issue_n = [&](auto ns_c, uint32_t a_part, uint32_t w_base, int kbl) {
+                            constexpr int NS = decltype(ns_c)::value;
+                            if constexpr (TA) {
+                                const uint32_t a0 = a_tm + a_part * 64 + kbl * 32;
 #pragma unroll
-                            for (int k4 = 0; k4 < 4; ++k4) {
-                                mma_f16(d, make_desc(a0 + k4 * 32), make_desc(w_base + k4 * 32), id, fresh ? 0u : 1u);
-                                fresh = false;
+                                for (int k4 = 0; k4 < NS; ++k4) {
+                                    mma_f16_ts(d, a0 + k4 * 8, make_desc(w_base + k4 * 32), id, fresh ? 0u : 1u);
+                                    fresh = false;
+                                }
+                            } else {
+                                const uint32_t a0 = a_base + a_part * A_PART + kbl * KBLK;
+#pragma unroll
+                                for (int k4 = 0; k4 < NS; ++k4) {
+                                    mma_f16(d, make_desc(a0 + k4 * 32), make_desc(w_base + k4 * 32), id,
+                                            fresh ? 0u : 1u);
+                                    fresh = false;
+                                }
                             }
+                        };
+                        auto issue = [&](uint32_t a_part, uint32_t w_base, int kbl) {
+                            if (short_k) issue_n(std::integral_constant<int, NS1>{}, a_part, w_base, kbl);
+                            else issue_n(std::integral_constant<int, 4>{}, a_part, w_base, kbl);
                         };
                         for (int kbl = 0; kbl < nkb; ++kbl, ++it) {   // part 1: a0 * w1
                             const int s = it % S::W_STAGES;
@@ -419,7 +473,27 @@ __global__ void __launch_bounds__(Shape<GROUPS, E>::THREADS, 1) k_score_tc(const
         const int q = warp & 3;                 // TMEM lane quarter of this warp
         const int row = q * 32 + lane;          // event row of the tile = TMEM lane
         uint8_t *abuf = abuf0 + g * S::REGION;
-        const uint32_t t_acc = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(128 * g);
+        const uint32_t t_acc = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(S::D_STRIDE * g);
+        const uint32_t t_a = t_acc + 128;   // TA: this lane quarter's operand columns (part p at + 64 p)
+        // eight consecutive K values of this thread's row -> both fp16 parts of the A operand
+        auto put8 = [&](int k0, const float (&v)[8]) {
+            if constexpr (TA) {
+                uint32_t w0[4], w1[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) split2x2(v[2 * j], v[2 * j + 1], w0[j], w1[j]);
+                tmem_st4(t_a + (uint32_t)(k0 >> 1), w0);
+                tmem_st4(t_a + 64 + (uint32_t)(k0 >> 1), w1);
+            } else {
+                store_chunk8(abuf, row, k0, v);
+            }
+        };
+        // the A operand of the next MMA job is complete
+        auto publish = [&]() {
+            if constexpr (TA) tmem_wait_st();
+            else fence_async_smem();
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(&feat_ready[g]);
+        };
         const int SN = 2 * E + 4;
         constexpr int IDB = E <= 8 ? 3 : E <= 16 ? 4 : E <= 32 ? 5 : E <= 64 ? 6 : 7;   // id bits in a key
         // staging (the region after the last layer's MMAs): fp32 scores
@@ -506,17 +580,11 @@ __global__ void __launch_bounds__(Shape<GROUPS, E>::THREADS, 1) k_score_tc(const
                             fv[i] = (float)(sf + __popc(seen)) * rmaxf;
                         }
                         const int e0 = 32 * w + e8;
-                        if (want_r) store_chunk8(abuf, row, kr + e0, rv);
-                        if (want_f) store_chunk8(abuf, row, kf + e0, fv);
+                        if (want_r) put8(kr + e0, rv);
+                        if (want_f) put8(kf + e0, fv);
                     }
                 }
-                if (p == P1C - 1) {   // zero padding up to the K blocks the MMAs read
-                    const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                    for (int k0 = 2 * E - 128 * p; k0 < P.KB1 * 64 - 128 * p; k0 += 8) store_chunk8(abuf, row, k0, z);
-                }
-                fence_async_smem();
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                mbar_arrive(&feat_ready[g]);
+                publish();   // (the MMAs read layer-1 K steps up to 2E only: no padding)
             }
             // ---- hidden layers: h = silu(acc * 2^-s + bias) -> next A operand (x 2^8)
             for (int layer = 0; layer < 2; ++layer) {
@@ -549,13 +617,11 @@ __global__ void __launch_bounds__(Shape<GROUPS, E>::THREADS, 1) k_score_tc(const
                             v[i] = (uu * (-ACT_SCALE / LOG2E)) * r;
                             hmax = fmaxf(hmax, fabsf(v[i]));
                         }
-                        store_chunk8(abuf, row, c0 + c8, v);
+                        put8(c0 + c8, v);
                     }
                 }
                 bad |= !(hmax <= 255.0f * ACT_SCALE);   // fp16 range of the scaled activations (and NaN)
-                fence_async_smem();
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                mbar_arrive(&feat_ready[g]);
+                publish();
             }
             // ---- scores: s = acc * 2^-s + b3, one thread per event sorts
             // the E keys and certifies the order
@@ -751,15 +817,16 @@ bool score_tc_eligible(const DevTrace &tr, int H) {
 
 static int g_num_sms = 0;
 
-template <int E, int GROUPS>
+template <int E, int GROUPS, bool TA = false>
 static int set_smem() {
-    return cudaFuncSetAttribute(k3tc::k_score_tc<E, GROUPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                k3tc::Shape<GROUPS, E>::SMEM) == cudaSuccess ? 0 : -1;
+    return cudaFuncSetAttribute(k3tc::k_score_tc<E, GROUPS, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                k3tc::Shape<GROUPS, E, TA>::SMEM) == cudaSuccess ? 0 : -1;
 }
 
 int preload_score_tc() {
     if (set_smem<8, 3>() || set_smem<16, 3>() || set_smem<32, 3>() || set_smem<64, 3>() || set_smem<8, 2>() ||
-        set_smem<16, 2>() || set_smem<32, 2>() || set_smem<64, 2>() || set_smem<128, 2>())
+        set_smem<16, 2>() || set_smem<32, 2>() || set_smem<64, 2>() || set_smem<128, 2>() ||
+        set_smem<8, 2, true>() || set_smem<16, 2, true>() || set_smem<32, 2, true>() || set_smem<64, 2, true>())
         return -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -767,17 +834,26 @@ int preload_score_tc() {
     return 0;
 }
 
-template <int E, int GROUPS>
+template <int E, int GROUPS, bool TA = false>
 static void launch_tc(const k3tc::Params &P, cudaStream_t s) {
-    using S = k3tc::Shape<GROUPS, E>;
+    using S = k3tc::Shape<GROUPS, E, TA>;
     const int sms = g_num_sms > 0 ? g_num_sms : 148;
     const unsigned grid = (unsigned)std::min<int64_t>(sms, (P.n_tiles + GROUPS - 1) / GROUPS);
-    k3tc::k_score_tc<E, GROUPS><<<grid, S::THREADS, S::SMEM, s>>>(P);
+    k3tc::k_score_tc<E, GROUPS, TA><<<grid, S::THREADS, S::SMEM, s>>>(P);
+}
+
+template <int E>
+static void launch_variant(const k3tc::Params &P, int variant, cudaStream_t s) {
+    if (variant == 1) launch_tc<E, 2, true>(P, s);
+    else if (variant == 2) launch_tc<E, 2>(P, s);
+    else launch_tc<E, 3>(P, s);
 }
 
 // Launches: weight scales + images, then the tensor-core scorer over every
 // 128-event tile (ranks + flag lists).  snaps: K3 snapshots (launch_score_prep).
-// groups: epilogue groups (3 or 2; E = 128 always runs 2).
+// groups (MCB_TUNE_K3_GROUPS): 3 or 2 epilogue groups with the operands in
+// shared memory, 1 = two groups with the operands in TMEM; E = 128 always
+// runs 2 groups with shared-memory operands.
 int launch_score_tc(const DevTrace &tr, const double *params, int num_nets, const int32_t *snaps, uint8_t *wimg,
                     float *bias, uint8_t *ranks, float tau, int32_t *flag_cnt, int32_t *flag_list, int64_t bucket_cap,
                     unsigned long long *stats, float *dbg_scores, int groups, cudaStream_t s) {
@@ -815,19 +891,17 @@ int launch_score_tc(const DevTrace &tr, const double *params, int num_nets, cons
     P.stats = stats;
     P.dbg_scores = dbg_scores;
     if (P.n_tiles == 0) return 3;
-    const bool three = groups != 2;
     switch (E) {
-        case 8: three ? launch_tc<8, 3>(P, s) : launch_tc<8, 2>(P, s); break;
-        case 16: three ? launch_tc<16, 3>(P, s) : launch_tc<16, 2>(P, s); break;
-        case 32: three ? launch_tc<32, 3>(P, s) : launch_tc<32, 2>(P, s); break;
-        case 64: three ? launch_tc<64, 3>(P, s) : launch_tc<64, 2>(P, s); break;
-        default: launch_tc<128, 2>(P, s); break;
+        case 8: launch_variant<8>(P, groups, s); break;
+        case 16: launch_variant<16>(P, groups, s); break;
+        case 32: launch_variant<32>(P, groups, s); break;
+        case 64: launch_variant<64>(P, groups, s); break;
+        default: launch_tc<128, 2>(P, s); break;   // (its score staging leaves no room for a TMEM-operand ring)
     }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         char b[160];
-        snprintf(b, sizeof b, "k_score_tc launch (E = %d, %d groups): %s", E, E == 128 ? 2 : (three ? 3 : 2),
-                 cudaGetErrorString(e));
+        snprintf(b, sizeof b, "k_score_tc launch (E = %d, variant %d): %s", E, groups, cudaGetErrorString(e));
         mcb_set_error(MCB_ERR_CUDA, b);
         return -1;
     }

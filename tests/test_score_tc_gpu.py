@@ -66,7 +66,7 @@ def _ranks(dt, dn, tc: bool, tau_ppb: int = 4000, groups: int = 3):
     return out[:dt.total_events * dt.num_experts].cpu().numpy().reshape(-1, dt.num_experts), stats
 
 
-@pytest.mark.parametrize("groups", [3, 2])
+@pytest.mark.parametrize("groups", [3, 2, 1])
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"E{s[1]}")
 def test_tc_ranks_equal_float64_ranks(shape, groups):
     L, E, K, T, n = shape
