@@ -190,6 +190,18 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// one lane of the (converged) warp -- the same lane every time, so the
+// tcgen05.commit that tracks a job's MMAs is issued by the thread that issued them
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -388,12 +400,16 @@ __global__ void __launch_bounds__(Shape<GROUPS, E, TA>::THREADS, 1) k_score_tc(c
         }
     } else if (warp == 1) {
         // ------------------------------------------------------- MMA issuer
-        // (lane 0 alone: the whole warp polling the barriers costs the epilogue
-        // warps more issue slots than uniform operand arithmetic saves)
-        if (lane == 0) {
+        // The whole warp walks the schedule, so every operand (TMEM address,
+        // smem descriptors, instruction descriptor) is warp-uniform and lives in
+        // uniform registers; one elected lane issues each block's MMAs and
+        // commits.  The issue rate matters: a group's job is 24 MMAs.
+        {
             uint32_t it = 0, fr[GROUPS];
 #pragma unroll
             for (int g = 0; g < GROUPS; ++g) fr[g] = 0u;
+            const uint64_t wdesc0 = make_desc(smem_u32(wring));   // + (slot offset >> 4)
+            const uint64_t adesc0 = make_desc(smem_u32(abuf0));   // + (A offset >> 4)
             for (int64_t k = 0;; ++k) {
                 const int64_t t0 = (k * G + b) * GROUPS;
                 if (t0 >= P.n_tiles) break;
@@ -404,10 +420,11 @@ __global__ void __launch_bounds__(Shape<GROUPS, E, TA>::THREADS, 1) k_score_tc(c
                         if (t >= P.n_tiles) continue;
                         mbar_wait_sleep(&feat_ready[g], fr[g] & 1);
                         ++fr[g];
+                        __syncwarp();
                         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                         const uint32_t d = tmem + (uint32_t)(S::D_STRIDE * g);
                         const uint32_t id = idesc(job_n(j));
-                        const uint32_t a_base = smem_u32(abuf0 + g * S::REGION);
+                        const uint64_t ag = adesc0 + (uint64_t)((g * S::REGION) >> 4);
                         const uint32_t a_tm = d + 128;   // TA: the group's operand columns
                         bool fresh = !(j > 0 && j < P1);   // layer-1 passes > 0 accumulate
                         const int nkb = job_kblocks(j);
@@ -419,50 +436,63 @@ __global__ void __launch_bounds__(Shape<GROUPS, E, TA>::THREADS, 1) k_score_tc(c
                         // layer-1 K steps stop at 2E (E = 8, 16: the rest of the block is padding)
                         constexpr int NS1 = 2 * E < 64 ? 2 * E / 16 : 4;
                         const bool short_k = NS1 < 4 && j < P1;
-                        auto issue_n = [&](auto ns_c, uint32_t a_part, uint32_t w_base, int kbl) {
+                        // (descriptor start addresses advance by 32 B = 2 units per K step)
+                        auto issue_n = [&](auto ns_c, uint32_t a_part, int s, int kbl) {
                             constexpr int NS = decltype(ns_c)::value;
+                            const uint64_t wd = wdesc0 + (uint64_t)((s * W_STAGE) >> 4);
                             if constexpr (TA) {
                                 const uint32_t a0 = a_tm + a_part * 64 + kbl * 32;
 #pragma unroll
                                 for (int k4 = 0; k4 < NS; ++k4) {
-                                    mma_f16_ts(d, a0 + k4 * 8, make_desc(w_base + k4 * 32), id, fresh ? 0u : 1u);
+                                    mma_f16_ts(d, a0 + k4 * 8, wd + 2 * k4, id, fresh ? 0u : 1u);
                                     fresh = false;
                                 }
                             } else {
-                                const uint32_t a0 = a_base + a_part * A_PART + kbl * KBLK;
+                                const uint64_t ad = ag + (uint64_t)((a_part * A_PART + kbl * KBLK) >> 4);
 #pragma unroll
                                 for (int k4 = 0; k4 < NS; ++k4) {
-                                    mma_f16(d, make_desc(a0 + k4 * 32), make_desc(w_base + k4 * 32), id,
-                                            fresh ? 0u : 1u);
+                                    mma_f16(d, ad + 2 * k4, wd + 2 * k4, id, fresh ? 0u : 1u);
                                     fresh = false;
                                 }
                             }
                         };
-                        auto issue = [&](uint32_t a_part, uint32_t w_base, int kbl) {
-                            if (short_k) issue_n(std::integral_constant<int, NS1>{}, a_part, w_base, kbl);
-                            else issue_n(std::integral_constant<int, 4>{}, a_part, w_base, kbl);
+                        auto issue = [&](uint32_t a_part, int s, int kbl) {
+                            if (short_k) issue_n(std::integral_constant<int, NS1>{}, a_part, s, kbl);
+                            else issue_n(std::integral_constant<int, 4>{}, a_part, s, kbl);
                         };
                         for (int kbl = 0; kbl < nkb; ++kbl, ++it) {   // part 1: a0 * w1
                             const int s = it % S::W_STAGES;
                             mbar_wait_sleep(&w_full[s], (it / S::W_STAGES) & 1);
+                            __syncwarp();
                             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                            issue(0, smem_u32(wring + s * W_STAGE), kbl);
-                            mma_commit(&w_empty[s]);
+                            if (elect_one()) {
+                                issue(0, s, kbl);
+                                mma_commit(&w_empty[s]);
+                            }
+                            __syncwarp();
+                            fresh = false;
                         }
                         const uint32_t it0 = it;
                         for (int kbl = 0; kbl < nkb; ++kbl) {          // part 0: a1 * w0
                             const uint32_t i2 = it0 + kbl;
                             const int s = i2 % S::W_STAGES;
                             mbar_wait_sleep(&w_full[s], (i2 / S::W_STAGES) & 1);
+                            __syncwarp();
                             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                            issue(1, smem_u32(wring + s * W_STAGE), kbl);
+                            if (elect_one()) issue(1, s, kbl);
+                            __syncwarp();
+                            fresh = false;
                         }
                         for (int kbl = 0; kbl < nkb; ++kbl, ++it) {   // part 0: a0 * w0
                             const int s = it % S::W_STAGES;
-                            issue(0, smem_u32(wring + s * W_STAGE), kbl);
-                            mma_commit(&w_empty[s]);
+                            if (elect_one()) {
+                                issue(0, s, kbl);
+                                mma_commit(&w_empty[s]);
+                            }
+                            __syncwarp();
                         }
-                        mma_commit(&acc_ready[g]);
+                        if (elect_one()) mma_commit(&acc_ready[g]);
+                        __syncwarp();
                     }
             }
         }
