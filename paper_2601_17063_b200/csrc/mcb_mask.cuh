@@ -68,6 +68,76 @@ template <> __device__ __forceinline__ M128 from_words<M128>(const uint32_t *w) 
     return {(uint64_t)w[0] | ((uint64_t)w[1] << 32), (uint64_t)w[2] | ((uint64_t)w[3] << 32)};
 }
 
+// Minimum packed key over the experts of a candidate mask (keys column-major
+// per thread, stride BS): 32-bit words,
+// highest set bit first (one FLO per candidate), two candidates per trip so
+// two key loads are in flight.
+template <int BS>
+__device__ __forceinline__ uint32_t min_key_word(uint32_t w, uint32_t best, const uint32_t *sk) {
+    while (w) {
+        const int i = 31 - __clz(w);
+        w ^= 1u << i;
+        uint32_t k = sk[i * BS];
+        if (w) {
+            const int i2 = 31 - __clz(w);
+            w ^= 1u << i2;
+            k = min(k, sk[i2 * BS]);
+        }
+        best = min(best, k);
+    }
+    return best;
+}
+template <int BS>
+__device__ __forceinline__ uint32_t min_key(uint64_t cand, const uint32_t *sk) {
+    return min_key_word<BS>((uint32_t)(cand >> 32), min_key_word<BS>((uint32_t)cand, ~0u, sk), sk + 32 * BS);
+}
+template <int BS>
+__device__ __forceinline__ uint32_t min_key(M128 cand, const uint32_t *sk) {
+    uint32_t b = min_key_word<BS>((uint32_t)cand.lo, ~0u, sk);
+    b = min_key_word<BS>((uint32_t)(cand.lo >> 32), b, sk + 32 * BS);
+    b = min_key_word<BS>((uint32_t)cand.hi, b, sk + 64 * BS);
+    return min_key_word<BS>((uint32_t)(cand.hi >> 32), b, sk + 96 * BS);
+}
+
+// Maximum (rank << 8 | expert) over the experts of a candidate mask, rank
+// bytes of this thread's row (mlpolicy.py:15-26: arg-max score; ranks are
+// distinct, 0 = not selectable).
+__device__ __forceinline__ uint32_t max_rank_word(uint32_t w, uint32_t best, const uint8_t *row, int e0) {
+    while (w) {
+        const int i = 31 - __clz(w);
+        w ^= 1u << i;
+        uint32_t k = ((uint32_t)row[i] << 8) | (uint32_t)(e0 + i);
+        if (w) {
+            const int i2 = 31 - __clz(w);
+            w ^= 1u << i2;
+            k = max(k, ((uint32_t)row[i2] << 8) | (uint32_t)(e0 + i2));
+        }
+        best = max(best, k);
+    }
+    return best;
+}
+__device__ __forceinline__ uint32_t max_rank(uint64_t cand, const uint8_t *row) {
+    return max_rank_word((uint32_t)(cand >> 32), max_rank_word((uint32_t)cand, 0u, row, 0), row + 32, 32);
+}
+__device__ __forceinline__ uint32_t max_rank(M128 cand, const uint8_t *row) {
+    uint32_t b = max_rank_word((uint32_t)cand.lo, 0u, row, 0);
+    b = max_rank_word((uint32_t)(cand.lo >> 32), b, row + 32, 32);
+    b = max_rank_word((uint32_t)cand.hi, b, row + 64, 64);
+    return max_rank_word((uint32_t)(cand.hi >> 32), b, row + 96, 96);
+}
+
+// One event's rank row into a thread's shared-memory row (row stride
+// mrow_stride(E), 16-byte aligned): four 16-byte copies for E % 16 == 0, bytes otherwise.
+__host__ __device__ __forceinline__ int mrow_stride(int E) { return (E + 31) & ~15; }
+__device__ __forceinline__ void copy_rank_row(const uint8_t *src, uint8_t *dst, int E) {
+    if ((E & 15) == 0) {
+#pragma unroll 2
+        for (int q = 0; q < E / 16; ++q) *(uint4 *)(dst + 16 * q) = __ldcg((const uint4 *)src + q);
+    } else {
+        for (int e = 0; e < E; ++e) dst[e] = __ldcg(src + e);
+    }
+}
+
 // ML keys of one event for a thread's column of shared-memory keys
 // (keys[e * 128]): key = (256 - rank) << 7 | e, selectable iff rank != 0
 // (mlpolicy.py:15-26).  Rows of a multiple of 16 experts are 16-byte aligned

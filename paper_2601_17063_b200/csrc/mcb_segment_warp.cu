@@ -415,7 +415,7 @@ namespace tspec {
 
 constexpr int BS = 128;
 constexpr int SH = 7;
-static_assert(BS == 128 && SH == 7, "mm::ml_row_keys assumes 128-thread key columns and 7 id bits");
+static_assert(SH == 7, "packed keys carry 7 id bits (E <= 128)");
 constexpr uint32_t KMAX = (1u << (32 - SH)) - 1u;
 
 template <int POL, typename M>
@@ -434,6 +434,8 @@ __device__ __forceinline__ void tseg_spec(const ReplayParams &P, int64_t chain, 
     const int64_t e0 = tr.ev_begin(chain);
     const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
     auto key = [&](int e) -> uint32_t & { return sk[e * BS]; };
+    // ML: the event's rank row as bytes, [thread][mrow_stride(E)] inside the key area
+    uint8_t *const mrow = (uint8_t *)(sk - threadIdx.x) + threadIdx.x * mrow_stride(E);
 
     // exact keys and seen set at ws (a snapshot point)
     const int2 *sn = P.seg.snap + (chain * P.seg.n_snap + ws / MCB_SNAP_EV) * P.seg.snap_e;
@@ -448,11 +450,8 @@ __device__ __forceinline__ void tseg_spec(const ReplayParams &P, int64_t chain, 
             const uint32_t np = v.x >= 0 ? __ldg(P.next_pos + a0 + v.x) : MCB_NEXT_INF;
             k = np == MCB_NEXT_INF ? 0u : KMAX - np;
         }
-        if (POL == POL_ML) {
-            const uint32_t r = ws > 0 ? (uint32_t)__ldcg(rank + (e0 + ws - 1) * E + e) : 0u;
-            k = 256u - r;
-        }
-        key(e) = (k << SH) | (uint32_t)e;
+        if (POL == POL_ML) mrow[e] = ws > 0 ? __ldcg(rank + (e0 + ws - 1) * E + e) : (uint8_t)0;
+        else key(e) = (k << SH) | (uint32_t)e;
         if (v.x >= 0) {
             seen = seen | bit_of<M>((uint32_t)e);
             ++n_seen;
@@ -473,20 +472,22 @@ __device__ __forceinline__ void tseg_spec(const ReplayParams &P, int64_t chain, 
     } else {
         // guess: the min(C, #seen) seen experts the policy would evict last
         // (largest packed keys), by a bitwise search for the threshold key
+        auto gkey = [&](int e) -> uint32_t {
+            return POL == POL_ML ? (((256u - mrow[e]) << SH) | (uint32_t)e) : key(e);
+        };
         const int n_res = min((int)C, n_seen);
         if (n_res > 0) {
             uint32_t tau = 0u;
             for (int b = 31; b >= 0; --b) {
                 const uint32_t cand = tau | (1u << b);
                 int cnt = 0;
-                for (int e = 0; e < E; ++e) cnt += (test(seen, (uint32_t)e) && key(e) >= cand) ? 1 : 0;
+                for (int e = 0; e < E; ++e) cnt += (test(seen, (uint32_t)e) && gkey(e) >= cand) ? 1 : 0;
                 if (cnt >= n_res) tau = cand;
             }
             for (int e = 0; e < E; ++e)
-                if (test(seen, (uint32_t)e) && key(e) >= tau) res = res | bit_of<M>((uint32_t)e);
+                if (test(seen, (uint32_t)e) && gkey(e) >= tau) res = res | bit_of<M>((uint32_t)e);
         }
     }
-    M valid = first_n<M>(E);
     uint32_t misses = 0, nev = 0, refc = 0, comp = 0;
     int32_t stuck_ev = -1;
     bool stuck = false;
@@ -505,10 +506,8 @@ __device__ __forceinline__ void tseg_spec(const ReplayParams &P, int64_t chain, 
             misses = nev = refc = comp = 0u;
             stuck = false;
         }
-        if (POL == POL_ML) {   // this event's rank row (mlpolicy.py:59-62)
-            const uint8_t *row = rank + (e0 + ev) * E;
-            valid = ml_row_keys<M>(row, E, sk);
-        }
+        if (POL == POL_ML)   // this event's rank row (mlpolicy.py:59-62) as bytes (rank 0 = not selectable)
+            copy_rank_row(rank + (e0 + ev) * E, mrow, E);
         M pin = zero<M>();
         uint32_t sm = 0;
         for (int j = 0; j < K; ++j) {
@@ -527,15 +526,14 @@ __device__ __forceinline__ void tseg_spec(const ReplayParams &P, int64_t chain, 
                 M vbit = zero<M>();
                 code = MCB_OUT_MISS;
                 if ((uint32_t)popc(res) >= C) {
-                    M cand = res & ~pin & valid;
-                    if (!any(cand)) {
+                    const M cand = res & ~pin;
+                    // ML: arg-max rank over the candidates; rank 0 (no candidate selectable) = stuck
+                    const uint32_t best = !any(cand) ? 0u
+                                          : (POL == POL_ML ? max_rank(cand, mrow) : min_key<BS>(cand, sk));
+                    if (!any(cand) || (POL == POL_ML && (best >> 8) == 0u)) {
                         stuck = true;
                     } else {
-                        uint32_t best = ~0u;
-                        do {
-                            best = min(best, key(pop_first(cand)));
-                        } while (any(cand));
-                        const uint32_t v = best & ((1u << SH) - 1u);
+                        const uint32_t v = POL == POL_ML ? (best & 0xFFu) : (best & ((1u << SH) - 1u));
                         vbit = bit_of<M>(v);
                         code = v;
                         ++nev;

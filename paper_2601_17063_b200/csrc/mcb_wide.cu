@@ -37,60 +37,6 @@ constexpr int SH = 7;       // id bits of a packed key (E <= 128)
 static_assert(SH == 7, "packed keys carry 7 id bits (E <= 128)");
 constexpr uint32_t KMAX = (1u << (32 - SH)) - 1u;
 
-// Minimum packed key over the experts of a candidate mask: 32-bit words,
-// highest set bit first (one FLO per candidate), two candidates per trip so
-// two key loads are in flight.
-__device__ __forceinline__ uint32_t min_key_word(uint32_t w, uint32_t best, const uint32_t *sk) {
-    while (w) {
-        const int i = 31 - __clz(w);
-        w ^= 1u << i;
-        uint32_t k = sk[i * BS];
-        if (w) {
-            const int i2 = 31 - __clz(w);
-            w ^= 1u << i2;
-            k = min(k, sk[i2 * BS]);
-        }
-        best = min(best, k);
-    }
-    return best;
-}
-__device__ __forceinline__ uint32_t min_key(uint64_t cand, const uint32_t *sk) {
-    return min_key_word((uint32_t)(cand >> 32), min_key_word((uint32_t)cand, ~0u, sk), sk + 32 * BS);
-}
-__device__ __forceinline__ uint32_t min_key(M128 cand, const uint32_t *sk) {
-    uint32_t b = min_key_word((uint32_t)cand.lo, ~0u, sk);
-    b = min_key_word((uint32_t)(cand.lo >> 32), b, sk + 32 * BS);
-    b = min_key_word((uint32_t)cand.hi, b, sk + 64 * BS);
-    return min_key_word((uint32_t)(cand.hi >> 32), b, sk + 96 * BS);
-}
-
-// Maximum (rank << 8 | expert) over the experts of a candidate mask, rank
-// bytes of this thread's row (mlpolicy.py:15-26: arg-max score; ranks are
-// distinct, 0 = not selectable).
-__device__ __forceinline__ uint32_t max_rank_word(uint32_t w, uint32_t best, const uint8_t *row, int e0) {
-    while (w) {
-        const int i = 31 - __clz(w);
-        w ^= 1u << i;
-        uint32_t k = ((uint32_t)row[i] << 8) | (uint32_t)(e0 + i);
-        if (w) {
-            const int i2 = 31 - __clz(w);
-            w ^= 1u << i2;
-            k = max(k, ((uint32_t)row[i2] << 8) | (uint32_t)(e0 + i2));
-        }
-        best = max(best, k);
-    }
-    return best;
-}
-__device__ __forceinline__ uint32_t max_rank(uint64_t cand, const uint8_t *row) {
-    return max_rank_word((uint32_t)(cand >> 32), max_rank_word((uint32_t)cand, 0u, row, 0), row + 32, 32);
-}
-__device__ __forceinline__ uint32_t max_rank(M128 cand, const uint8_t *row) {
-    uint32_t b = max_rank_word((uint32_t)cand.lo, 0u, row, 0);
-    b = max_rank_word((uint32_t)(cand.lo >> 32), b, row + 32, 32);
-    b = max_rank_word((uint32_t)cand.hi, b, row + 64, 64);
-    return max_rank_word((uint32_t)(cand.hi >> 32), b, row + 96, 96);
-}
-
 constexpr uint32_t NIL = 0xFFu;   // end of the LRU list
 
 template <int POL, bool UNIFORM, int WMAX, typename M>
@@ -109,7 +55,7 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
     auto nxt = [&](uint32_t e) -> uint8_t & { return lb[e * BS]; };
     auto prv = [&](uint32_t e) -> uint8_t & { return lb[(E + e) * BS]; };
     uint32_t head = NIL, tail = NIL;
-    uint8_t *const mrow = (uint8_t *)(sk - threadIdx.x) + threadIdx.x * (E + 16);
+    uint8_t *const mrow = (uint8_t *)(sk - threadIdx.x) + threadIdx.x * mrow_stride(E);
 
     M res = zero<M>(), seen = zero<M>(), ring_or = zero<M>();
     M ring[WMAX + 1];
@@ -146,11 +92,8 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
             uint8_t *m = P.res_masks + (e0 + ev) * E;
             for (int e = 0; e < E; ++e) m[e] = (uint8_t)test(res, (uint32_t)e);
         }
-        if (POL == POL_ML) {   // this event's rank row (mlpolicy.py:59-62), 16 bytes per copy
-            const uint4 *row = (const uint4 *)(rank + (e0 + ev) * E);
-#pragma unroll 2
-            for (int q = 0; q < E / 16; ++q) *(uint4 *)(mrow + 16 * q) = __ldcg(row + q);
-        }
+        if (POL == POL_ML)   // this event's rank row (mlpolicy.py:59-62)
+            copy_rank_row(rank + (e0 + ev) * E, mrow, E);
         M pin = zero<M>();
         uint32_t step_miss = 0;
         for (uint32_t j = 0; j < nacc; ++j, ++pos, ++A) {
@@ -205,7 +148,7 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
                         if (!any(cand)) {
                             stuck = true;
                         } else {
-                            const uint32_t best = min_key(cand, sk);
+                            const uint32_t best = min_key<BS>(cand, sk);
                             const uint32_t v = best & ((1u << SH) - 1u);
                             vbit = bit_of<M>(v);
                             code = v;
