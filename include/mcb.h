@@ -202,8 +202,8 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
  * (0 = automatic). */
 #define MCB_TUNE_SEG_NW 2
 /* MCB_TUNE_SEG_PASSES: speculation passes of the segmented replay (0 = auto,
- * 1 or 2; the second restarts every segment from the first pass's end state
- * of its predecessor). */
+ * else 1..8; pass p > 0 restarts every segment from pass p-1's end state of
+ * its predecessor; num_experts <= 16 uses at most 2). */
 #define MCB_TUNE_SEG_PASSES 3
 /* MCB_TUNE_GROUP_LANES: lanes per cache instance of the num_experts > 16
  * replay (0 = automatic, 8, 16 or 32). */

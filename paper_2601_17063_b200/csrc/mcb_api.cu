@@ -269,7 +269,7 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
         return MCB_OK;
     }
     if (knob == MCB_TUNE_SEG_PASSES) {
-        if (value < 0 || value > 2) return mcb_set_error(MCB_ERR_INVALID, "speculation passes must be 0 (auto), 1 or 2");
+        if (value < 0 || value > 8) return mcb_set_error(MCB_ERR_INVALID, "speculation passes must be 0 (auto) .. 8");
         c->seg_passes = value;
         return MCB_OK;
     }
@@ -686,6 +686,7 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
             // coalesce more slowly (C3 with thread speculation: 1 / 2 passes = 333 / 141
             // ms per step, the second pass removing almost all fix-up walking)
             P.seg.passes = c->seg_passes > 0 ? (int)c->seg_passes : (d.E <= 16 ? 1 : 2);
+            if (d.E <= 16) P.seg.passes = std::min(P.seg.passes, 2);   // (mcb_segment.cu: two record buffers, two passes)
             P.seg.n_snap = (int)((d.T + MCB_SNAP_EV - 1) / MCB_SNAP_EV);
             P.seg.Tpad = (d.T + 15) / 16 * 16;
             P.seg.snap_e = seg_snap_stride(d.E);

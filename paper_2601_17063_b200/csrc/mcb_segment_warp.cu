@@ -310,8 +310,8 @@ __device__ __forceinline__ void wseg_spec(const ReplayParams &P, int64_t chain, 
     wkeys_at<EPL, POL>(P, chain, ws, lane, ml_variant, key, seen);
     WState<EPL> S;
     wstate_clear(S);
-    if (pass == 1 && seg > 0) {
-        const WSegOut &q = ((const WSegOut *)P.seg.out[0])[inst * P.seg.n_seg + seg - 1];
+    if (pass >= 1 && seg > 0) {   // the previous pass's end state of the previous segment
+        const WSegOut &q = ((const WSegOut *)P.seg.out[(pass - 1) & 1])[inst * P.seg.n_seg + seg - 1];
         load_state<EPL>(S, q.res_end, q.ring_end, lane, W);
     } else {
         S.res = wguess<EPL>(key, seen, C, lane);
@@ -326,7 +326,7 @@ __device__ __forceinline__ void wseg_spec(const ReplayParams &P, int64_t chain, 
     int32_t stuck_ev = -1;
     uint64_t h = 0;
     const bool track = P.hashes != nullptr;
-    WSegOut &o = ((WSegOut *)P.seg.out[pass])[inst * P.seg.n_seg + seg];
+    WSegOut &o = ((WSegOut *)P.seg.out[pass & 1])[inst * P.seg.n_seg + seg];   // passes alternate buffers
     uint32_t *codes = (uint32_t *)(P.seg.codes + inst * P.seg.Tpad);
     uint32_t word = 0;
     WReplay<EPL, POL> rp;
@@ -385,7 +385,7 @@ __device__ __forceinline__ void wseg_spec(const ReplayParams &P, int64_t chain, 
 template <int EPL>
 __global__ void __launch_bounds__(128) k_wseg_spec(const __grid_constant__ ReplayParams P, int pass) {
     const int pol_i = P.pol_map[blockIdx.y];
-    if (pass == 1 && P.pol[pol_i] == MCB_LRU) return;   // LRU's guess is exact
+    if (pass >= 1 && P.pol[pol_i] == MCB_LRU) return;   // LRU's guess is exact
     const int lane = threadIdx.x & 31;
     const int64_t w = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
     const int n_seg = P.seg.n_seg;
@@ -461,8 +461,8 @@ __device__ __forceinline__ void tseg_spec(const ReplayParams &P, int64_t chain, 
     M ring[SOLO_WMAX + 1];
 #pragma unroll
     for (int i = 0; i <= SOLO_WMAX; ++i) ring[i] = zero<M>();
-    if (pass == 1 && seg > 0) {   // pass 0's end state of the previous segment
-        const WSegOut &q = ((const WSegOut *)P.seg.out[0])[inst * P.seg.n_seg + seg - 1];
+    if (pass >= 1 && seg > 0) {   // the previous pass's end state of the previous segment
+        const WSegOut &q = ((const WSegOut *)P.seg.out[(pass - 1) & 1])[inst * P.seg.n_seg + seg - 1];
         res = from_words<M>(q.res_end);
 #pragma unroll
         for (int i = 0; i <= SOLO_WMAX; ++i) {
@@ -494,7 +494,7 @@ __device__ __forceinline__ void tseg_spec(const ReplayParams &P, int64_t chain, 
     uint64_t h = 0;
     const bool track = P.hashes != nullptr;
     for (int b = 0; b <= K; ++b) hist[b * BS] = 0;
-    WSegOut &o = ((WSegOut *)P.seg.out[pass])[inst * P.seg.n_seg + seg];
+    WSegOut &o = ((WSegOut *)P.seg.out[pass & 1])[inst * P.seg.n_seg + seg];   // passes alternate buffers
     uint32_t *codes = (uint32_t *)(P.seg.codes + inst * P.seg.Tpad);
     uint32_t word = 0;
 
@@ -588,7 +588,7 @@ template <typename M>
 __global__ void __launch_bounds__(BS) k_tseg_spec(const __grid_constant__ ReplayParams P, int pass) {
     extern __shared__ uint32_t s_tsk[];   // keys [E][BS], then uint16 histograms [MCB_SEG_BINS][BS]
     const int pol_i = P.pol_map[blockIdx.y];
-    if (pass == 1 && P.pol[pol_i] == MCB_LRU) return;   // LRU's guess is exact
+    if (pass >= 1 && P.pol[pol_i] == MCB_LRU) return;   // LRU's guess is exact
     const int64_t t = (int64_t)blockIdx.x * BS + threadIdx.x;
     const int n_seg = P.seg.n_seg;
     if (t >= (P.chain_hi - P.chain_lo) * n_seg * P.n_cap) return;
@@ -623,7 +623,7 @@ __device__ __forceinline__ void wseg_finish(const ReplayParams &P, int64_t chain
     const int64_t e0 = tr.ev_begin(chain);
     const uint8_t *rank = (POL == POL_ML) ? P.rank[ml_variant] : nullptr;
     const uint8_t *codes = P.seg.codes + inst * P.seg.Tpad;
-    const WSegOut *so = (const WSegOut *)P.seg.out[(POL == POL_LRU || P.seg.passes < 2) ? 0 : 1] + inst * n_seg;
+    const WSegOut *so = (const WSegOut *)P.seg.out[POL == POL_LRU ? 0 : ((P.seg.passes - 1) & 1)] + inst * n_seg;
     const bool track = P.hashes != nullptr;
 
     WState<EPL> A;                         // the true state, carried across segments
