@@ -391,6 +391,13 @@ int mcb_router_topk(mcb_ctx *ctx, const void *hidden_bf16, const void *weight_bf
                     int32_t d, int32_t num_layers, int32_t num_experts, int32_t top_k,
                     uint8_t *acc, float *logits, void *stream);
 
+/* K1's input: AR(1) hidden states over tokens, out[T][d_pad] bf16 with
+ * h[0] ~ N(0, 1), h[t] = rho h[t-1] + sqrt(1 - rho^2) n(t) per column j < d
+ * (n: a counter-based normal of (seed, t, j)), column d = 1 (the bias input
+ * of the gate rows), columns > d = 0.  Device pointer. */
+int mcb_ar1_hidden(mcb_ctx *ctx, int64_t T, int32_t d, int32_t d_pad, double rho, uint64_t seed, void *out_bf16,
+                   void *stream);
+
 /* ---- Belady-labelled training data ----
  * Replaces build_training_data (pkg/src/moecache/dataset.py:35-96) for any
  * packed trace (prefill and several sequences included): for every event of

@@ -37,9 +37,11 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <cuda_bf16.h>
 #include <stdint.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 
@@ -350,6 +352,92 @@ extern "C" int mcb_router_topk(mcb_ctx *ctx, const void *hidden, const void *wei
     k1::router_topk_kernel<<<grid, k1::THREADS, k1::SMEM, (cudaStream_t)stream>>>(mh, mw, (int)T, d, L, E, lgEp, K, acc,
                                                                                   logits, (int)N);
     cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return mcb_set_error(MCB_ERR_CUDA, cudaGetErrorString(e));
+    return MCB_OK;
+}
+
+// ---- K1 input synthesis: AR(1) hidden states over tokens (bf16) ------------
+// h[0][j] = n(0, j), h[t][j] = rho h[t-1][j] + sqrt(1 - rho^2) n(t, j), with
+// n a counter-based standard normal (splitmix64 hash of (seed, t, j) -> two
+// uniforms -> Box-Muller), so any token chunk can be generated independently:
+// pass 1 runs each 512-token chunk from zero, pass 2 carries the chunk ends
+// across chunks (h_end[c] = g_end[c] + rho^len h_end[c-1]), pass 3 reruns
+// each chunk from its carry and writes bf16 rows [T][d_pad] (column d = 1,
+// the bias input of the gate rows; columns > d = 0).
+namespace ar1 {
+
+constexpr int CHUNK = 512;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ float normal(uint64_t seed, int64_t t, int j) {
+    const uint64_t r = mix64(seed ^ mix64(((uint64_t)t << 20) ^ (uint64_t)j));
+    const float u1 = ((float)(uint32_t)(r >> 40) + 0.5f) * (1.0f / 16777216.0f);   // (0, 1)
+    const float u2 = (float)(uint32_t)(r & 0xFFFFFFu) * (1.0f / 16777216.0f);
+    return sqrtf(-2.0f * logf(u1)) * __cosf(6.283185307179586f * u2);
+}
+
+// pass 1 (write_out == false): chunk-end values from a zero start;
+// pass 3 (write_out == true): the chunk again from its carry, bf16 rows out
+template <bool WRITE>
+__global__ void k_ar1_chunk(int64_t T, int d, int d_pad, float rho, float c, uint64_t seed, const float *carry_in,
+                            float *chunk_end, __nv_bfloat16 *out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t ch = blockIdx.y;
+    const int64_t t0 = ch * CHUNK, t1 = min(T, t0 + CHUNK);
+    if (j >= d_pad) return;
+    if (j >= d) {   // bias column and padding
+        if (WRITE)
+            for (int64_t t = t0; t < t1; ++t) out[t * d_pad + j] = __float2bfloat16(j == d ? 1.0f : 0.0f);
+        return;
+    }
+    float h = WRITE ? carry_in[ch * d + j] : 0.0f;
+    for (int64_t t = t0; t < t1; ++t) {
+        const float n = normal(seed, t, j);
+        h = t == 0 ? n : fmaf(rho, h, c * n);   // stationary start: h_0 ~ N(0, 1)
+        if (WRITE) out[t * d_pad + j] = __float2bfloat16(h);
+    }
+    if (!WRITE) chunk_end[ch * d + j] = h;
+}
+
+// pass 2: carry_in[c] = the true h before chunk c (one thread per column)
+__global__ void k_ar1_carry(int64_t T, int d, float rho, const float *chunk_end, float *carry_in) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= d) return;
+    const int64_t n_ch = (T + CHUNK - 1) / CHUNK;
+    const float rho_full = powf(rho, (float)CHUNK);
+    float carry = 0.0f;
+    for (int64_t ch = 0; ch < n_ch; ++ch) {
+        carry_in[ch * d + j] = carry;
+        carry = chunk_end[ch * d + j] + (ch == 0 ? 0.0f : rho_full * carry);   // chunk 0 starts at h_0
+    }
+}
+
+}  // namespace ar1
+
+extern "C" int mcb_ar1_hidden(mcb_ctx *ctx, int64_t T, int32_t d, int32_t d_pad, double rho, uint64_t seed,
+                              void *out_bf16, void *stream) {
+    mcb_clear_error();
+    if (!ctx || !out_bf16) return mcb_set_error(MCB_ERR_INVALID, "NULL argument");
+    if (T < 1 || d < 1 || d_pad < d + 1 || !(rho >= 0.0 && rho < 1.0))
+        return mcb_set_error(MCB_ERR_INVALID, "need T >= 1, d >= 1, d_pad > d, 0 <= rho < 1");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n_ch = (T + ar1::CHUNK - 1) / ar1::CHUNK;
+    float *scratch = nullptr;
+    if (cudaMallocAsync((void **)&scratch, sizeof(float) * 2 * (size_t)n_ch * d, s) != cudaSuccess)
+        return mcb_set_error(MCB_ERR_NOMEM, "ar1 scratch");
+    float *chunk_end = scratch, *carry_in = scratch + (size_t)n_ch * d;
+    const float fr = (float)rho, fc = (float)std::sqrt(1.0 - rho * rho);
+    const dim3 g1((unsigned)((d + 127) / 128), (unsigned)n_ch), g3((unsigned)((d_pad + 127) / 128), (unsigned)n_ch);
+    ar1::k_ar1_chunk<false><<<g1, 128, 0, s>>>(T, d, d_pad, fr, fc, seed, nullptr, chunk_end, nullptr);
+    ar1::k_ar1_carry<<<(d + 127) / 128, 128, 0, s>>>(T, d, fr, chunk_end, carry_in);
+    ar1::k_ar1_chunk<true><<<g3, 128, 0, s>>>(T, d, d_pad, fr, fc, seed, carry_in, nullptr, (__nv_bfloat16 *)out_bf16);
+    cudaFreeAsync(scratch, s);
+    const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return mcb_set_error(MCB_ERR_CUDA, cudaGetErrorString(e));
     return MCB_OK;
 }

@@ -51,9 +51,19 @@ def _gen(seed: int, device) -> torch.Generator:
 def ar1_hidden(tokens: int, d: int, rho: float, seed: int, device="cuda", chunk: int = 8192) -> torch.Tensor:
     """bf16 [T, d_pad] hidden states; column d is the constant 1 of the bias trick.
 
-    AR(1) over tokens computed chunk by chunk with a log-depth doubling scan
-    inside each chunk (h_t = rho h_{t-1} + c eps_t)."""
+    On a CUDA device: the engine's kernel (mcb_ar1_hidden: counter-based
+    normals, chunked AR(1) scan with carries).  On the CPU (the reference
+    arm's regeneration only): torch's AR(1) over tokens, chunk by chunk with a
+    log-depth doubling scan inside each chunk (h_t = rho h_{t-1} + c eps_t) --
+    a different random stream."""
     d_pad = (d + 1 + 63) // 64 * 64
+    if torch.device(device).type == "cuda":
+        out = torch.empty((tokens, d_pad), dtype=torch.bfloat16, device=device)
+        lib = _lib.load_library()
+        dev = out.device.index or 0
+        _lib.check(lib.mcb_ar1_hidden(_lib.context(dev), tokens, d, d_pad, float(rho), int(seed) & (2 ** 64 - 1),
+                                      out.data_ptr(), ctypes.c_void_p(torch.cuda.current_stream(out.device).cuda_stream)))
+        return out
     out = torch.zeros((tokens, d_pad), dtype=torch.bfloat16, device=device)
     g = _gen(seed, device)
     c = math.sqrt(max(1.0 - rho * rho, 0.0))

@@ -48,3 +48,25 @@ def _check(T, d, L, E, K, seed=0):
 def test_router_topk_matches_torch(T, d, L, E, K):
     frac, _ = _check(T, d, L, E, K)
     assert frac < 0.01
+
+
+def test_ar1_hidden_kernel_statistics():
+    """K1's input kernel (mcb_ar1_hidden): stationary N(0, 1) columns with
+    lag-1 correlation rho, continuous across the 512-token chunk boundaries
+    (the residual h_t - rho h_{t-1} has variance 1 - rho^2 everywhere),
+    bias column = 1, padding = 0, deterministic per seed."""
+    T, d, rho = 3000, 256, 0.9
+    H = generator.ar1_hidden(T, d, rho, 7)
+    assert H.shape == (T, (d + 1 + 63) // 64 * 64) and H.dtype == torch.bfloat16
+    assert torch.equal(H, generator.ar1_hidden(T, d, rho, 7))
+    assert not torch.equal(H, generator.ar1_hidden(T, d, rho, 8))
+    h = H[:, :d].float()
+    assert torch.all(H[:, d] == 1) and torch.all(H[:, d + 1:] == 0)
+    assert abs(float(h.mean())) < 0.05 and abs(float(h.var()) - 1.0) < 0.1
+    r = h[1:] - rho * h[:-1]
+    c2 = 1 - rho * rho
+    assert abs(float(r.var()) - c2) < 0.03
+    at_boundary = r[[t - 1 for t in range(512, T, 512)]]      # rows t = 512, 1024, ...
+    assert abs(float(at_boundary.var()) - c2) < 0.06
+    lag1 = float((h[1:] * h[:-1]).mean() / h.var())
+    assert abs(lag1 - rho) < 0.02
