@@ -250,6 +250,11 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
  * TMEM and a deep weight ring.  num_experts = 128 always runs 2 groups with
  * shared-memory operands.  Ranks are identical. */
 #define MCB_TUNE_K3_GROUPS 14
+/* MCB_TUNE_UPLOAD_PIECES: mcb_replay_host copies a uniform batch of >= 16
+ * traces in this many trace-range pieces (default 8, at most 16; 0/1 = one
+ * copy) and starts the trace-only stages (K2, K3) of each piece as soon as
+ * it has landed, so the host-to-device copy overlaps the scorer. */
+#define MCB_TUNE_UPLOAD_PIECES 16
 int mcb_set_tuning(mcb_ctx *ctx, int32_t knob, int64_t value);
 /* LeCaR parameters used by the MCB_LECAR cells of later mcb_replay calls on
  * this context (LeCaRPolicy.__init__, policies.py:333-349; defaults 0.45,

@@ -40,6 +40,7 @@ MCB_TUNE_SCRATCH_BYTES = 11
 MCB_TUNE_K3_TC = 12
 MCB_TUNE_K3_TAU_PPB = 13
 MCB_TUNE_K3_GROUPS = 14
+MCB_TUNE_UPLOAD_PIECES = 16
 R_PH, R_PM, R_DH, R_DM, R_COMP, R_EVICT, R_REFETCH, R_STATUS = range(8)
 R_N = 8
 OUT_HIT, OUT_MISS = 0xFFFF, 0xFFFE

@@ -20,6 +20,8 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include "mcb_internal.h"
+
+#define MCB_MAX_UPLOAD_PIECES 16
 #include "mcb_kernels.cuh"
 
 // ---------------------------------------------------------------- errors ---
@@ -97,6 +99,16 @@ struct mcb_ctx {
     cudaEvent_t join2 = nullptr;
     cudaEvent_t pre = nullptr;         // the side stream's replay preparation is done
     cudaEvent_t nets_ev = nullptr;     // host path: the nets' upload (on side2) is done
+    // host path, uniform batches: the trace arrives in trace-range pieces on
+    // copy_stream (up_ev[k] = piece k landed) and the trace-only stages (K2,
+    // snapshots, K3) of piece k start as soon as it is there
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t up_ev[MCB_MAX_UPLOAD_PIECES] = {};
+    int n_pieces = 0;                  // > 0 only inside one mcb_replay_host call
+    int64_t piece_chain[MCB_MAX_UPLOAD_PIECES + 1] = {};
+    int64_t upload_pieces = 8;         // MCB_TUNE_UPLOAD_PIECES
+    bool pieces_next = false;          // the pieced K3 loop also runs K2 per piece
+    size_t pieces_nu_sw = 0;
     bool nets_pending = false;         // the scorer must wait for nets_ev before using the nets
     int64_t ml_chunks = 1;             // K3 / ML replay pipeline depth (MCB_TUNE_ML_CHUNKS)
     int k3_ctas = -1;                  // K3 grid mode (MCB_TUNE_K3_CTAS)
@@ -244,6 +256,12 @@ extern "C" int mcb_set_tuning(mcb_ctx *c, int32_t knob, int64_t value) {
         c->k3_tau_ppb = value;
         return MCB_OK;
     }
+    if (knob == MCB_TUNE_UPLOAD_PIECES) {
+        if (value < 0 || value > MCB_MAX_UPLOAD_PIECES)
+            return mcb_set_error(MCB_ERR_INVALID, "upload pieces must be 0 .. 16");
+        c->upload_pieces = value;
+        return MCB_OK;
+    }
     if (knob == MCB_TUNE_K3_GROUPS) {
         if (value < 1 || value > 3) return mcb_set_error(MCB_ERR_INVALID, "K3 variant must be 1, 2 or 3");
         c->k3_groups = (int)value;
@@ -318,7 +336,14 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     if (const char *env = getenv("MCB_SCRATCH_BYTES")) c->scratch_bytes = atoll(env);
     if (const char *env = getenv("MCB_K3_TC")) c->k3_tc = atoi(env);
     if (const char *env = getenv("MCB_K3_TAU_PPB")) c->k3_tau_ppb = atoll(env);
+    if (const char *env = getenv("MCB_UPLOAD_PIECES"))
+        c->upload_pieces = std::max<int64_t>(0, std::min<int64_t>(MCB_MAX_UPLOAD_PIECES, atoll(env)));
     if (const char *env = getenv("MCB_K3_GROUPS")) c->k3_groups = std::max(1, std::min(3, atoi(env)));
+    for (auto &e : c->up_ev)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+            delete c;
+            return mcb_set_error(MCB_ERR_CUDA, "event creation failed");
+        }
     for (auto &e : c->chunk_ev)
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
             delete c;
@@ -329,6 +354,7 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c->side2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join2, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->pre, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->nets_ev, cudaEventDisableTiming) != cudaSuccess ||
@@ -358,6 +384,9 @@ extern "C" int mcb_ctx_destroy(mcb_ctx *c) {
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->side2) cudaStreamDestroy(c->side2);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    for (auto &e : c->up_ev)
+        if (e) cudaEventDestroy(e);
     if (c->join2) cudaEventDestroy(c->join2);
     if (c->pre) cudaEventDestroy(c->pre);
     if (c->nets_ev) cudaEventDestroy(c->nets_ev);
@@ -432,6 +461,17 @@ static DevTrace make_dev_trace(const mcb_trace *t) {
     return d;
 }
 
+// A uniform trace's chains [lo, hi) as a trace of their own (chain-major
+// layout: every per-chain output is offset by lo times its per-chain size)
+static DevTrace sub_trace(const DevTrace &d, int64_t lo, int64_t hi) {
+    DevTrace s = d;
+    s.acc = d.acc + lo * d.T * d.K;
+    s.n_chains = hi - lo;
+    s.total_acc = s.n_chains * d.T * d.K;
+    s.total_events = s.n_chains * d.T;
+    return s;
+}
+
 static int64_t max_score_tiles(const DevTrace &d) {
     if (d.uniform) return d.n_chains * ((d.T + MCB_TILE_EV - 1) / MCB_TILE_EV);
     return d.total_events / MCB_TILE_EV + d.n_chains;  // upper bound of sum(ceil(n_c / TILE))
@@ -476,16 +516,37 @@ static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int in
         if (int rc = c->tc_bias.ensure((size_t)score_tc_bias_stride(E) * nn * sizeof(float))) return rc;
         if (int rc = c->tc_flag_cnt.ensure((size_t)nn * sizeof(int32_t))) return rc;
         if (int rc = c->tc_flag_list.ensure((size_t)(nn * cap + 1) * sizeof(int32_t))) return rc;
-        *launched += launch_score_prep(d, include_prefill, (int32_t *)c->snaps.p, (int64_t *)c->tile_off.p, tiles, s);
-        const int n_tc = launch_score_tc(d, nets->params, nn, (const int32_t *)c->snaps.p, (uint8_t *)c->tc_wimg.p,
-                                         (float *)c->tc_bias.p, ranks, (float)(c->k3_tau_ppb * 1e-9),
-                                         (int32_t *)c->tc_flag_cnt.p, (int32_t *)c->tc_flag_list.p, cap,
-                                         (unsigned long long *)c->stats.p, tc_scores, c->k3_groups, s);
-        if (n_tc < 0) return MCB_ERR_CUDA;
-        *launched += n_tc;
+        // one pass, or one per uploaded piece (trace ranges; each waits for its
+        // bytes): K2 (when the call needs it) + snapshots + the scorer per
+        // piece on this stream, the float64 re-score once over all pieces
+        const int np = c->n_pieces > 0 ? c->n_pieces : 1;
+        const int64_t tpc32 = (d.T + MCB_TILE_EV - 1) / MCB_TILE_EV, SN = 2 * E + 4;
+        for (int k = 0; k < np; ++k) {
+            const int64_t lo = c->n_pieces > 0 ? c->piece_chain[k] : 0;
+            const int64_t hi = c->n_pieces > 0 ? c->piece_chain[k + 1] : d.n_chains;
+            const DevTrace dk = c->n_pieces > 0 ? sub_trace(d, lo, hi) : d;
+            if (c->n_pieces > 0) {
+                CUDA_TRY(cudaStreamWaitEvent(s, c->up_ev[k], 0));
+                if (c->pieces_next)
+                    *launched += launch_next_use(dk, (uint32_t *)c->next_pos.p + lo * d.T * d.K,
+                                                 c->pieces_nu_sw ? (uint32_t *)c->nu_scratch.p : nullptr, s);
+            }
+            int32_t *snk = (int32_t *)c->snaps.p + lo * tpc32 * SN;
+            *launched += launch_score_prep(dk, include_prefill, snk, (int64_t *)c->tile_off.p, max_score_tiles(dk), s);
+            const int n_tc = launch_score_tc(dk, nets->params, nn, snk, (uint8_t *)c->tc_wimg.p, (float *)c->tc_bias.p,
+                                             ranks + lo * d.T * E, (float)(c->k3_tau_ppb * 1e-9),
+                                             (int32_t *)c->tc_flag_cnt.p, (int32_t *)c->tc_flag_list.p, cap,
+                                             (unsigned long long *)c->stats.p,
+                                             tc_scores ? tc_scores + lo * d.T * E : nullptr, c->k3_groups, s, k == 0,
+                                             lo * d.T);
+            if (n_tc < 0) return MCB_ERR_CUDA;
+            *launched += n_tc;
+        }
         *launched += launch_rescore(d, (const double *)c->wt.p, H, nn, (const int32_t *)c->snaps.p,
                                     (const int32_t *)c->tc_flag_cnt.p, (const int32_t *)c->tc_flag_list.p, cap, ranks,
                                     (unsigned long long *)c->stats.p, s);
+        (void)tiles;
+        (void)cap;
         return MCB_OK;
     }
     const int n = launch_score(d, (const double *)c->wt.p, H, nets->num_nets, include_prefill, ranks, scores,
@@ -715,6 +776,16 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     const bool chunked = Pm.n_pol_launch > 0 && d.uniform && !c->serial && !(need_ml[0] && need_ml[1]) &&
                          std::min<int64_t>(std::min<int64_t>(c->ml_chunks, MCB_MAX_ML_CHUNKS), d.n_chains) > 1;
     const bool after_k3 = split && c->overlap == 0 && Pm.n_pol_launch > 0 && !chunked;
+    // Piecewise upload (mcb_replay_host): the pieced schedule needs K3-TC on a
+    // uniform trace with the replays after it; otherwise wait for the whole trace.
+    if (c->n_pieces > 0) {
+        const bool pieced = after_k3 && d.uniform && P.seg.n_seg <= 1 && !(need_ml[0] && need_ml[1]) && nets &&
+                            c->k3_tc && score_tc_eligible(d, nets->hidden);
+        if (!pieced) {
+            for (int k = 0; k < c->n_pieces; ++k) CUDA_TRY(cudaStreamWaitEvent(s, c->up_ev[k], 0));
+            c->n_pieces = 0;
+        }
+    }
     // With the replays after K3, the replays' own preparation (K2 next-use scan,
     // key snapshots) runs on the side stream under K3; the ML replay waits for it.
     cudaStream_t sp = after_k3 ? c->side : s;
@@ -726,7 +797,13 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         if (int rc = c->next_pos.ensure((size_t)(d.total_acc + 64) * sizeof(uint32_t))) return rc;
         Pn.next_pos = Pm.next_pos = (const uint32_t *)c->next_pos.p;
         mark(c, 0, sp);
-        launched += launch_next_use(d, (uint32_t *)c->next_pos.p, nu_sw ? (uint32_t *)c->nu_scratch.p : nullptr, sp);
+        if (c->n_pieces > 0) {   // piece by piece in the scorer's loop (run_score), as the trace arrives
+            c->pieces_next = true;
+            c->pieces_nu_sw = nu_sw;
+        } else {
+            launched += launch_next_use(d, (uint32_t *)c->next_pos.p, nu_sw ? (uint32_t *)c->nu_scratch.p : nullptr,
+                                        sp);
+        }
         mark(c, 1, sp);
         c->ran[0] = true;
     }
@@ -926,6 +1003,9 @@ static int replay_chunked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, i
     const int64_t per_chunk = per > 0 ? std::max<int64_t>(1, budget / per) : t->num_traces;
     if (per == 0 || per_chunk >= t->num_traces || out->outcomes)
         return replay_locked(c, t, pols, n_pol, caps, n_cap, cost, nets, out, (cudaStream_t)stream);
+    for (int k = 0; k < c->n_pieces; ++k)   // trace ranges of their own: the whole upload first
+        CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, c->up_ev[k], 0));
+    c->n_pieces = 0;
     const int64_t n_cells = (int64_t)n_pol * n_cap, L = t->num_layers;
     const int64_t chain_acc = t->events_per_chain * t->top_k;
     int64_t kernels = 0, chunks = 0;
@@ -984,7 +1064,47 @@ extern "C" int mcb_replay_host(mcb_ctx *c, const mcb_trace *t, const int32_t *po
     mcb_trace dt = *t;
     const DevTrace d = make_dev_trace(t);
     const int64_t n_chains = d.n_chains;
-    if (int rc = upload(c->h_acc, t->acc, (size_t)d.total_acc, 256, s, &dt.acc)) return rc;
+    mcb_nets dn;
+    const mcb_nets *npn = nullptr;
+    if (nets && nets->params) {
+        // the nets' copy runs on side2 while the trace-only stages (K2, key and
+        // feature snapshots) start; the scorer waits for it (nets_ev).  It is
+        // submitted before the trace: copies in one direction share the copy
+        // engine in submission order, and the scorer must not wait for the trace.
+        dn = *nets;
+        const size_t cnt = net_param_doubles(nets->num_experts, nets->hidden) * (size_t)nets->num_nets;
+        CUDA_TRY(cudaEventRecord(c->nets_ev, s));                 // after the previous call's use of h_params
+        CUDA_TRY(cudaStreamWaitEvent(c->side2, c->nets_ev, 0));
+        if (int rc = upload(c->h_params, nets->params, cnt, 0, c->side2, &dn.params)) return rc;
+        CUDA_TRY(cudaEventRecord(c->nets_ev, c->side2));
+        c->nets_pending = true;
+        npn = &dn;
+    }
+    // Uniform batches of many traces: upload in trace-range pieces on the copy
+    // stream so that the trace-only stages of piece k overlap the copy of k+1
+    // (whole traces per piece: a piece's first chain is layer 0).  Batches that
+    // will be replayed in scratch-bounded trace ranges take the plain upload.
+    c->n_pieces = 0;
+    const int np = t->uniform ? (int)std::min<int64_t>(c->upload_pieces, t->num_traces / 8) : 0;
+    if (np >= 2) {
+        if (int rc = c->h_acc.ensure((size_t)d.total_acc + 256)) return rc;
+        uint8_t *dst = (uint8_t *)c->h_acc.p;
+        const int64_t per_trace = (int64_t)t->num_layers * t->events_per_chain * t->top_k;
+        CUDA_TRY(cudaEventRecord(c->fork, s));   // after the previous call's use of the buffer
+        CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->fork, 0));
+        CUDA_TRY(cudaMemsetAsync(dst + d.total_acc, 0, 256, c->copy_stream));
+        for (int k = 0; k <= np; ++k) c->piece_chain[k] = (int64_t)t->num_traces * k / np * t->num_layers;
+        for (int k = 0; k < np; ++k) {
+            const int64_t b0 = c->piece_chain[k] / t->num_layers * per_trace;
+            const int64_t b1 = c->piece_chain[k + 1] / t->num_layers * per_trace;
+            CUDA_TRY(cudaMemcpyAsync(dst + b0, t->acc + b0, (size_t)(b1 - b0), cudaMemcpyHostToDevice, c->copy_stream));
+            CUDA_TRY(cudaEventRecord(c->up_ev[k], c->copy_stream));
+        }
+        dt.acc = dst;
+        c->n_pieces = np;
+    } else if (int rc = upload(c->h_acc, t->acc, (size_t)d.total_acc, 256, s, &dt.acc)) {
+        return rc;
+    }
     if (!t->uniform) {
         int64_t total_rt = 0;
         if (n_chains > 0) total_rt = t->chain_rt_off[n_chains];
@@ -993,20 +1113,6 @@ extern "C" int mcb_replay_host(mcb_ctx *c, const mcb_trace *t, const int32_t *po
         if (int rc = upload(c->h_rt_off, t->chain_rt_off, (size_t)n_chains + 1, 0, s, &dt.chain_rt_off)) return rc;
         if (int rc = upload(c->h_ev_info, t->ev_info, (size_t)d.total_events, 64, s, &dt.ev_info)) return rc;
         if (int rc = upload(c->h_routed, t->routed, (size_t)total_rt, 64, s, &dt.routed)) return rc;
-    }
-    mcb_nets dn;
-    const mcb_nets *np = nullptr;
-    if (nets && nets->params) {
-        // the nets' copy runs on side2 while the trace-only stages (K2, key and
-        // feature snapshots) start; the scorer waits for it (nets_ev)
-        dn = *nets;
-        const size_t cnt = net_param_doubles(nets->num_experts, nets->hidden) * (size_t)nets->num_nets;
-        CUDA_TRY(cudaEventRecord(c->nets_ev, s));                 // after the previous call's use of h_params
-        CUDA_TRY(cudaStreamWaitEvent(c->side2, c->nets_ev, 0));
-        if (int rc = upload(c->h_params, nets->params, cnt, 0, c->side2, &dn.params)) return rc;
-        CUDA_TRY(cudaEventRecord(c->nets_ev, c->side2));
-        c->nets_pending = true;
-        np = &dn;
     }
     const int64_t n_cells = (int64_t)t->num_traces * n_pol * n_cap;
     const int64_t n_inst = n_chains * n_pol * n_cap;
@@ -1032,7 +1138,10 @@ extern "C" int mcb_replay_host(mcb_ctx *c, const mcb_trace *t, const int32_t *po
         if (int rc = c->h_chain_latency.ensure((size_t)(n_inst + 1) * 2 * sizeof(double))) return rc;
         dout.chain_latency = (double *)c->h_chain_latency.p;
     }
-    const int rc_replay = replay_chunked(c, &dt, pols, n_pol, caps, n_cap, cost, np, &dout, s);
+    const int rc_replay = replay_chunked(c, &dt, pols, n_pol, caps, n_cap, cost, npn, &dout, s);
+    for (int k = 0; k < c->n_pieces; ++k) cudaStreamWaitEvent(s, c->up_ev[k], 0);   // (a path that did not wait)
+    c->n_pieces = 0;
+    c->pieces_next = false;
     if (c->nets_pending) {   // the stream must not outrun the copy even if no scorer ran
         cudaStreamWaitEvent(s, c->nets_ev, 0);
         c->nets_pending = false;

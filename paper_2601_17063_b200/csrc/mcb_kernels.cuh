@@ -137,7 +137,8 @@ int score_tc_bias_stride(int E);
 int preload_score_tc();
 int launch_score_tc(const DevTrace &tr, const double *params, int num_nets, const int32_t *snaps, uint8_t *wimg,
                     float *bias, uint8_t *ranks, float tau, int32_t *flag_cnt, int32_t *flag_list, int64_t bucket_cap,
-                    unsigned long long *stats, float *dbg_scores, int groups, cudaStream_t s);
+                    unsigned long long *stats, float *dbg_scores, int groups, cudaStream_t s, bool prep = true,
+                    int64_t ev_base = 0);
 int launch_rescore(const DevTrace &tr, const double *wt, int H, int num_nets, const int32_t *snaps,
                    const int32_t *flag_cnt, const int32_t *flag_list, int64_t bucket_cap, uint8_t *ranks,
                    unsigned long long *uncertain, cudaStream_t s);

@@ -96,6 +96,7 @@ struct Params {
     int num_nets;
     int N3, KB1, P1;            // layer-3 N (E rounded up to 16), layer-1 K blocks, layer-1 passes
     int64_t n_tiles, tpc, tpc32;
+    int64_t ev_base;            // event index of this launch's first chain in the flag lists (trace pieces)
     const int32_t *snaps;       // K3 tracker snapshots every 32 events (k_snap_scan)
     uint8_t *ranks;             // [event][E]
     float tau;
@@ -719,7 +720,7 @@ __global__ void __launch_bounds__(Shape<GROUPS, E, TA>::THREADS, 1) k_score_tc(c
                 const bool flagged = valid && bad;
                 if (flagged) {
                     const int slot = atomicAdd(P.flag_cnt + net, 1);
-                    P.flag_list[(int64_t)net * P.bucket_cap + slot] = (int32_t)(c * T + ev);
+                    P.flag_list[(int64_t)net * P.bucket_cap + slot] = (int32_t)(P.ev_base + c * T + ev);
                 }
                 const unsigned nbad = __popc(__ballot_sync(0xFFFFFFFFu, flagged));
                 if (lane == 0 && nbad) atomicAdd(P.stats + 5, (unsigned long long)nbad);
@@ -886,19 +887,20 @@ static void launch_variant(const k3tc::Params &P, int variant, cudaStream_t s) {
 // runs 2 groups with shared-memory operands.
 int launch_score_tc(const DevTrace &tr, const double *params, int num_nets, const int32_t *snaps, uint8_t *wimg,
                     float *bias, uint8_t *ranks, float tau, int32_t *flag_cnt, int32_t *flag_list, int64_t bucket_cap,
-                    unsigned long long *stats, float *dbg_scores, int groups, cudaStream_t s) {
+                    unsigned long long *stats, float *dbg_scores, int groups, cudaStream_t s, bool prep,
+                    int64_t ev_base) {
     using namespace k3tc;
     const int E = tr.E;
     const int KB1 = (2 * E + 63) / 64, N3 = (E + 15) / 16 * 16;
     const int64_t net_bytes = (int64_t)score_tc_net_bytes(E);
     const int bstride = score_tc_bias_stride(E);
-    k_wscale<<<num_nets * 3, 256, 0, s>>>(params, E, N3, bias, bstride);
-    {
+    if (prep) {   // weight images + flag lists (once per call; trace pieces reuse them)
+        k_wscale<<<num_nets * 3, 256, 0, s>>>(params, E, N3, bias, bstride);
         const int64_t chunks = ((int64_t)H * KB1 * 8 + (int64_t)H * 16 + (int64_t)N3 * 16) * num_nets;
         const unsigned blocks = (unsigned)std::min<int64_t>((chunks + 255) / 256, 4096);
         k_prep_tc<<<blocks, 256, 0, s>>>(params, E, num_nets, KB1, N3, net_bytes, wimg, bias, bstride);
+        cudaMemsetAsync(flag_cnt, 0, sizeof(int32_t) * num_nets, s);
     }
-    cudaMemsetAsync(flag_cnt, 0, sizeof(int32_t) * num_nets, s);
     Params P;
     P.tr = tr;
     P.wimg = wimg;
@@ -920,6 +922,7 @@ int launch_score_tc(const DevTrace &tr, const double *params, int num_nets, cons
     P.bucket_cap = bucket_cap;
     P.stats = stats;
     P.dbg_scores = dbg_scores;
+    P.ev_base = ev_base;
     if (P.n_tiles == 0) return 3;
     switch (E) {
         case 8: launch_variant<8>(P, groups, s); break;
