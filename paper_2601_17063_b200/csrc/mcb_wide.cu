@@ -219,8 +219,8 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
 // All policies of the call in one launch (blockIdx.y = policy), so the
 // instances of every policy share the waves; blockIdx.x * BS + threadIdx.x =
 // (chain, capacity) instance.
-template <bool UNIFORM, typename M>
-__global__ void __launch_bounds__(BS, sizeof(M) == 8 ? 5 : 4) k_replay_wide(const __grid_constant__ ReplayParams P) {
+template <bool UNIFORM, typename M, int WMAX>
+__global__ void __launch_bounds__(BS, sizeof(M) == 8 ? 6 : 4) k_replay_wide(const __grid_constant__ ReplayParams P) {
     extern __shared__ uint32_t s_keys[];   // [E][BS] keys, LRU links or ML rank rows
     const int pol_i = P.pol_map[blockIdx.y];
     const int64_t t = (int64_t)blockIdx.x * BS + threadIdx.x;
@@ -229,21 +229,32 @@ __global__ void __launch_bounds__(BS, sizeof(M) == 8 ? 5 : 4) k_replay_wide(cons
     const int64_t chain = P.chain_lo + t / P.n_cap;
     uint32_t *sk = s_keys + threadIdx.x;
     switch (P.pol[pol_i]) {
-        case MCB_LRU: wide_instance<POL_LRU, UNIFORM, SOLO_WMAX, M>(P, chain, pol_i, cap_i, 0, sk); break;
-        case MCB_LFU: wide_instance<POL_LFU, UNIFORM, SOLO_WMAX, M>(P, chain, pol_i, cap_i, 0, sk); break;
-        case MCB_BELADY: wide_instance<POL_BELADY, UNIFORM, SOLO_WMAX, M>(P, chain, pol_i, cap_i, 0, sk); break;
-        case MCB_ML: wide_instance<POL_ML, UNIFORM, SOLO_WMAX, M>(P, chain, pol_i, cap_i, 0, sk); break;
-        case MCB_FIFO: wide_instance<POL_FIFO, UNIFORM, SOLO_WMAX, M>(P, chain, pol_i, cap_i, 0, sk); break;
-        default: wide_instance<POL_ML, UNIFORM, SOLO_WMAX, M>(P, chain, pol_i, cap_i, 1, sk); break;
+        case MCB_LRU: wide_instance<POL_LRU, UNIFORM, WMAX, M>(P, chain, pol_i, cap_i, 0, sk); break;
+        case MCB_LFU: wide_instance<POL_LFU, UNIFORM, WMAX, M>(P, chain, pol_i, cap_i, 0, sk); break;
+        case MCB_BELADY: wide_instance<POL_BELADY, UNIFORM, WMAX, M>(P, chain, pol_i, cap_i, 0, sk); break;
+        case MCB_ML: wide_instance<POL_ML, UNIFORM, WMAX, M>(P, chain, pol_i, cap_i, 0, sk); break;
+        case MCB_FIFO: wide_instance<POL_FIFO, UNIFORM, WMAX, M>(P, chain, pol_i, cap_i, 0, sk); break;
+        default: wide_instance<POL_ML, UNIFORM, WMAX, M>(P, chain, pol_i, cap_i, 1, sk); break;
     }
 }
 
 template <bool UNIFORM, typename M>
 int set_wide_smem(size_t smem) {
-    const void *f = (const void *)k_replay_wide<UNIFORM, M>;
-    cudaFuncAttributes a;
-    if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
-    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess ? 0 : -1;
+    const void *fs[] = {(const void *)k_replay_wide<UNIFORM, M, 5>, (const void *)k_replay_wide<UNIFORM, M, SOLO_WMAX>};
+    for (const void *f : fs) {
+        cudaFuncAttributes a;
+        if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
+        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
+    }
+    return 0;
+}
+
+// the refetch ring sized for the call's window: 6 slots for the default
+// window 5 (fewer registers, fewer mask updates per miss), else SOLO_WMAX + 1
+template <bool UNIFORM, typename M>
+void launch_wide_w(const ReplayParams &p, dim3 grid, size_t smem, cudaStream_t s) {
+    if (p.window <= 5) k_replay_wide<UNIFORM, M, 5><<<grid, BS, smem, s>>>(p);
+    else k_replay_wide<UNIFORM, M, SOLO_WMAX><<<grid, BS, smem, s>>>(p);
 }
 
 }  // namespace wide
@@ -263,11 +274,11 @@ int launch_replay_wide(const ReplayParams &p, cudaStream_t s) {
     const dim3 grid((unsigned)((n + wide::BS - 1) / wide::BS), (unsigned)p.n_pol_launch);
     const size_t smem = (size_t)E * wide::BS * sizeof(uint32_t);
     if (E <= 64) {
-        if (p.tr.uniform) wide::k_replay_wide<true, uint64_t><<<grid, wide::BS, smem, s>>>(p);
-        else wide::k_replay_wide<false, uint64_t><<<grid, wide::BS, smem, s>>>(p);
+        if (p.tr.uniform) wide::launch_wide_w<true, uint64_t>(p, grid, smem, s);
+        else wide::launch_wide_w<false, uint64_t>(p, grid, smem, s);
     } else {
-        if (p.tr.uniform) wide::k_replay_wide<true, mm::M128><<<grid, wide::BS, smem, s>>>(p);
-        else wide::k_replay_wide<false, mm::M128><<<grid, wide::BS, smem, s>>>(p);
+        if (p.tr.uniform) wide::launch_wide_w<true, mm::M128>(p, grid, smem, s);
+        else wide::launch_wide_w<false, mm::M128>(p, grid, smem, s);
     }
     return 1;
 }
