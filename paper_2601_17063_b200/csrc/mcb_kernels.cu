@@ -1031,7 +1031,7 @@ __device__ __forceinline__ double sigmoid_ref(double z, const double *tab) {
 // passes instead of one sequential walk per chain:
 //   k_tile_summary  one warp per tile: per-expert routing count in the tile
 //                   and the 1-based index of its last routing in the tile
-//   k_snap_scan     one warp per chain: exclusive scan over its tiles ->
+//   k_snap_scan     one warp per (chain, 32 experts): walk over its tiles ->
 //                   snapshot (last update index, count, u) at every tile start
 __global__ void __launch_bounds__(128) k_tile_summary(DevTrace tr, int32_t *__restrict__ summ) {
     // one warp per 32-event tile: lane i marks bit i of occ[e] for each
@@ -1062,50 +1062,41 @@ __global__ void __launch_bounds__(128) k_tile_summary(DevTrace tr, int32_t *__re
     }
 }
 
-// One warp per (chain, expert): 32 tiles at a time, lane j = tile t0 + j,
-// warp-wide exclusive prefix sum of the routing counts and prefix max of the
-// last-routing update index (u at a tile start is t * TILE for decode-only
-// single-sequence chains), carried across chunks.
+// One warp per (chain, 32 experts), lane = expert: a sequential walk over
+// the chain's tiles carrying (count, last routing) -- every load and store is
+// one coalesced row segment (the tile-per-lane scan read and wrote one 4-byte
+// word per 512-byte row).  u at a tile start is t * TILE for decode-only
+// single-sequence chains; later tiles have later update indices, so the last
+// routing before tile t is the latest non-empty tile's.
 __global__ void __launch_bounds__(128) k_snap_scan(DevTrace tr, const int32_t *__restrict__ summ,
                                                    int32_t *__restrict__ snaps) {
     const int lane = threadIdx.x & 31;
     const int64_t wid = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-    const int E = tr.E, SN = 2 * E + 4;
-    const int64_t c = wid / E;
-    const int e = (int)(wid % E);
+    const int E = tr.E, SN = 2 * E + 4, EB = (E + 31) / 32;
+    const int64_t c = wid / EB;
+    const int e = (int)(wid % EB) * 32 + lane;
     if (c >= tr.n_chains) return;
     const int64_t tpc = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
+    const bool on = e < E;
+    const int32_t *sm = summ + c * tpc * 2 * E;
+    int32_t *sp = snaps + c * tpc * SN;
     int32_t carry_f = 0, carry_last = -1;
-    for (int64_t t0 = 0; t0 < tpc; t0 += 32) {
-        const int64_t t = t0 + lane;
-        const bool ok = t < tpc;
-        const int32_t *sm = summ + (c * tpc + (ok ? t : 0)) * 2 * E;
-        const int32_t cnt = ok ? __ldg(sm + e) : 0;
-        const int32_t l = ok ? __ldg(sm + E + e) : 0;
-        const int32_t la = l > 0 ? (int32_t)(t * MCB_TILE_EV) + l : -1;
-        int32_t incl_f = cnt, incl_l = la;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int32_t vf = __shfl_up_sync(FULL_MASK, incl_f, o);
-            const int32_t vl = __shfl_up_sync(FULL_MASK, incl_l, o);
-            if (lane >= o) { incl_f += vf; incl_l = max(incl_l, vl); }
+#pragma unroll 4
+    for (int64_t t = 0; t < tpc; ++t) {
+        const int32_t cnt = on ? __ldg(sm + t * 2 * E + e) : 0;
+        const int32_t l = on ? __ldg(sm + t * 2 * E + E + e) : 0;
+        if (on) {
+            sp[t * SN + e] = carry_last;
+            sp[t * SN + E + e] = carry_f;
         }
-        const int32_t ex_f = __shfl_up_sync(FULL_MASK, incl_f, 1), ex_l = __shfl_up_sync(FULL_MASK, incl_l, 1);
-        const int32_t f_before = carry_f + (lane ? ex_f : 0);
-        const int32_t l_before = max(carry_last, lane ? ex_l : -1);
-        if (ok) {
-            int32_t *sp = snaps + (c * tpc + t) * SN;
-            sp[e] = l_before;
-            sp[E + e] = f_before;
-            if (e == 0) {
-                const int64_t rt = t * MCB_TILE_EV * (int64_t)tr.K;
-                sp[2 * E] = (int32_t)(t * MCB_TILE_EV);
-                sp[2 * E + 1] = (int32_t)(rt & 0xFFFFFFFF);
-                sp[2 * E + 2] = (int32_t)(rt >> 32);
-            }
+        if (e == 0) {
+            const int64_t rt = t * MCB_TILE_EV * (int64_t)tr.K;
+            sp[t * SN + 2 * E] = (int32_t)(t * MCB_TILE_EV);
+            sp[t * SN + 2 * E + 1] = (int32_t)(rt & 0xFFFFFFFF);
+            sp[t * SN + 2 * E + 2] = (int32_t)(rt >> 32);
         }
-        carry_f += __shfl_sync(FULL_MASK, incl_f, 31);
-        carry_last = max(carry_last, __shfl_sync(FULL_MASK, incl_l, 31));
+        carry_f += cnt;
+        carry_last = l > 0 ? (int32_t)(t * MCB_TILE_EV) + l : carry_last;
     }
 }
 
@@ -2033,7 +2024,7 @@ int launch_score_prep(const DevTrace &tr, int include_prefill, int32_t *snaps, i
         // snaps scratch holds [summaries | snapshots]
         int32_t *summ = snaps + max_tiles * (2 * tr.E + 4);
         k_tile_summary<<<(unsigned)((max_tiles + 3) / 4), 128, 0, s>>>(tr, summ);
-        k_snap_scan<<<(unsigned)((tr.n_chains * tr.E + 3) / 4), 128, 0, s>>>(tr, summ, snaps);
+        k_snap_scan<<<(unsigned)((tr.n_chains * ((tr.E + 31) / 32) + 3) / 4), 128, 0, s>>>(tr, summ, snaps);
     } else {
         k_tile_offsets<<<1, 1024, 0, s>>>(tr, tile_off);
         k_feat_snap<<<(unsigned)((tr.n_chains + 3) / 4), 128, 0, s>>>(tr, include_prefill, tile_off, snaps);
