@@ -1062,6 +1062,54 @@ __global__ void __launch_bounds__(128) k_tile_summary(DevTrace tr, int32_t *__re
     }
 }
 
+// Few long chains (C3: 16 chains of 32K tiles): one warp per (chain, expert),
+// 32 tiles at a time, lane j = tile t0 + j,
+// warp-wide exclusive prefix sum of the routing counts and prefix max of the
+// last-routing update index (u at a tile start is t * TILE for decode-only
+// single-sequence chains), carried across chunks.
+__global__ void __launch_bounds__(128) k_snap_scan_tiles(DevTrace tr, const int32_t *__restrict__ summ,
+                                                   int32_t *__restrict__ snaps) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int E = tr.E, SN = 2 * E + 4;
+    const int64_t c = wid / E;
+    const int e = (int)(wid % E);
+    if (c >= tr.n_chains) return;
+    const int64_t tpc = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
+    int32_t carry_f = 0, carry_last = -1;
+    for (int64_t t0 = 0; t0 < tpc; t0 += 32) {
+        const int64_t t = t0 + lane;
+        const bool ok = t < tpc;
+        const int32_t *sm = summ + (c * tpc + (ok ? t : 0)) * 2 * E;
+        const int32_t cnt = ok ? __ldg(sm + e) : 0;
+        const int32_t l = ok ? __ldg(sm + E + e) : 0;
+        const int32_t la = l > 0 ? (int32_t)(t * MCB_TILE_EV) + l : -1;
+        int32_t incl_f = cnt, incl_l = la;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t vf = __shfl_up_sync(FULL_MASK, incl_f, o);
+            const int32_t vl = __shfl_up_sync(FULL_MASK, incl_l, o);
+            if (lane >= o) { incl_f += vf; incl_l = max(incl_l, vl); }
+        }
+        const int32_t ex_f = __shfl_up_sync(FULL_MASK, incl_f, 1), ex_l = __shfl_up_sync(FULL_MASK, incl_l, 1);
+        const int32_t f_before = carry_f + (lane ? ex_f : 0);
+        const int32_t l_before = max(carry_last, lane ? ex_l : -1);
+        if (ok) {
+            int32_t *sp = snaps + (c * tpc + t) * SN;
+            sp[e] = l_before;
+            sp[E + e] = f_before;
+            if (e == 0) {
+                const int64_t rt = t * MCB_TILE_EV * (int64_t)tr.K;
+                sp[2 * E] = (int32_t)(t * MCB_TILE_EV);
+                sp[2 * E + 1] = (int32_t)(rt & 0xFFFFFFFF);
+                sp[2 * E + 2] = (int32_t)(rt >> 32);
+            }
+        }
+        carry_f += __shfl_sync(FULL_MASK, incl_f, 31);
+        carry_last = max(carry_last, __shfl_sync(FULL_MASK, incl_l, 31));
+    }
+}
+
 // One warp per (chain, 32 experts), lane = expert: a sequential walk over
 // the chain's tiles carrying (count, last routing) -- every load and store is
 // one coalesced row segment (the tile-per-lane scan read and wrote one 4-byte
@@ -2024,7 +2072,14 @@ int launch_score_prep(const DevTrace &tr, int include_prefill, int32_t *snaps, i
         // snaps scratch holds [summaries | snapshots]
         int32_t *summ = snaps + max_tiles * (2 * tr.E + 4);
         k_tile_summary<<<(unsigned)((max_tiles + 3) / 4), 128, 0, s>>>(tr, summ);
-        k_snap_scan<<<(unsigned)((tr.n_chains * ((tr.E + 31) / 32) + 3) / 4), 128, 0, s>>>(tr, summ, snaps);
+        // many chains: lane = expert, coalesced walk over the tiles; few long
+        // chains (not enough warps to fill the GPU): lane = tile, warp scans
+        const int64_t tpc = (tr.T + MCB_TILE_EV - 1) / MCB_TILE_EV;
+        const int64_t walkers = tr.n_chains * ((tr.E + 31) / 32);
+        if (walkers >= 4096 || tpc <= 64)
+            k_snap_scan<<<(unsigned)((walkers + 3) / 4), 128, 0, s>>>(tr, summ, snaps);
+        else
+            k_snap_scan_tiles<<<(unsigned)((tr.n_chains * tr.E + 3) / 4), 128, 0, s>>>(tr, summ, snaps);
     } else {
         k_tile_offsets<<<1, 1024, 0, s>>>(tr, tile_off);
         k_feat_snap<<<(unsigned)((tr.n_chains + 3) / 4), 128, 0, s>>>(tr, include_prefill, tile_off, snaps);
@@ -2096,6 +2151,7 @@ int preload_kernels() {
         (const void *)k_next_use<true>, (const void *)k_next_use<false>, (const void *)k_next_use_blocks,
         (const void *)k_fold, (const void *)k_train_features, (const void *)k_train_targets, (const void *)k_prepare_nets, (const void *)k_tile_offsets,
         (const void *)k_feat_snap, (const void *)k_tile_summary, (const void *)k_snap_scan,
+        (const void *)k_snap_scan_tiles,
         (const void *)k_score_tile<0, 0>, (const void *)k_score_tile<8, 128>, (const void *)k_score_tile<16, 128>,
         (const void *)k_score_tile<64, 128>, (const void *)k_score_tile<128, 128>,
         (const void *)k_replay<32, 1, true>, (const void *)k_replay<32, 1, false>,
