@@ -161,6 +161,58 @@ __device__ __forceinline__ void load_state(WState<EPL> &S, const uint32_t *res4,
     S.count = __reduce_add_sync(FULL_MASK_W, (uint32_t)__popc(S.res));
 }
 
+// A segment record held across the warp: lane l owns 32-bit words l, l + 32
+// and l + 64 of the 384-byte WSegOut (one coalesced load per word block), so
+// the finish walk can prefetch the next segment's record while it splices the
+// current one.  Field words: counters 0-4, hash 6-7, res_start 8-11, res_end
+// 12-15, ring_start 16 + 4 s, ring_end 48 + 4 s, hist 80-84 (16-bit pairs).
+struct WRec {
+    uint32_t w[3];
+};
+static_assert(sizeof(WSegOut) == 3 * 32 * 4, "WRec covers WSegOut");
+__device__ __forceinline__ void wrec_load(WRec &r, const WSegOut *o, int lane) {
+    const uint32_t *p = (const uint32_t *)o;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) r.w[i] = __ldg(p + 32 * i + lane);
+}
+// word I of the record, on every lane (I compile-time)
+template <int I>
+__device__ __forceinline__ uint32_t wrec_word(const WRec &r) {
+    return __shfl_sync(FULL_MASK_W, r.w[I / 32], I % 32);
+}
+// word BASE + w (w = this lane's word of a 4-word expert mask, 0..3)
+template <int BASE>
+__device__ __forceinline__ uint32_t wrec_mask_word(const WRec &r, int w) {
+    static_assert(BASE % 32 + 3 < 32, "a mask's four words share one block");
+    return __shfl_sync(FULL_MASK_W, r.w[BASE / 32], BASE % 32 + w);
+}
+template <int EPL, int RES, int RING>
+__device__ __forceinline__ void load_state_rec(WState<EPL> &S, const WRec &r, int lane, int W) {
+    const int e0 = lane * EPL, w = e0 >> 5, sh = e0 & 31;
+    const uint32_t m = (1u << EPL) - 1u;
+    S.res = (wrec_mask_word<RES>(r, w) >> sh) & m;
+    uint32_t o = 0u;
+#pragma unroll
+    for (int sl = 0; sl <= SOLO_WMAX; ++sl) {
+        uint32_t v;
+        switch (sl) {   // (compile-time word index per slot)
+            case 0: v = wrec_mask_word<RING + 0>(r, w); break;
+            case 1: v = wrec_mask_word<RING + 4>(r, w); break;
+            case 2: v = wrec_mask_word<RING + 8>(r, w); break;
+            case 3: v = wrec_mask_word<RING + 12>(r, w); break;
+            case 4: v = wrec_mask_word<RING + 16>(r, w); break;
+            case 5: v = wrec_mask_word<RING + 20>(r, w); break;
+            case 6: v = wrec_mask_word<RING + 24>(r, w); break;
+            default: v = wrec_mask_word<RING + 28>(r, w); break;
+        }
+        S.ring[sl] = (v >> sh) & m;
+        o |= (sl <= W) ? S.ring[sl] : 0u;
+    }
+    S.ring_or = o;
+    S.count = __reduce_add_sync(FULL_MASK_W, (uint32_t)__popc(S.res));
+}
+static_assert(SOLO_WMAX == 7, "load_state_rec unrolls 8 ring slots");
+
 // ------------------------------------------------------------------ snapshot --
 // one warp per (chain, block of MCB_SNAP_EV events), lanes over experts
 __global__ void __launch_bounds__(128) k_wseg_summary(const __grid_constant__ ReplayParams P) {
@@ -636,12 +688,15 @@ __device__ __forceinline__ void wseg_finish(const ReplayParams &P, int64_t chain
 #pragma unroll
     for (int s = 0; s < EPL; ++s) valid0 |= (lane * EPL + s < E ? 1u : 0u) << s;
 
+    WRec rn;                               // the next segment's record, in flight
+    if (n_seg > 0) wrec_load(rn, so, lane);
     for (int seg = 0; seg < n_seg; ++seg) {
         const int64_t ev0 = (int64_t)seg * SE;
         const int64_t ev1 = min(ev0 + (int64_t)SE, tr.T);
-        const WSegOut &o = so[seg];
+        const WRec o = rn;
+        if (seg + 1 < n_seg) wrec_load(rn, so + seg + 1, lane);
         WState<EPL> B;
-        load_state<EPL>(B, o.res_start, o.ring_start, lane, W);
+        load_state_rec<EPL, 8, 16>(B, o, lane, W);
         bool conv = wstate_equal<EPL>(A, B, W);
         int64_t ev = ev0;
         SCount ca = {0u, 0u, 0u}, cb = {0u, 0u, 0u};
@@ -686,17 +741,23 @@ __device__ __forceinline__ void wseg_finish(const ReplayParams &P, int64_t chain
         const uint32_t refb = __reduce_add_sync(FULL_MASK_W, cb.refc);
         uint64_t hseg;
         if (conv) {
-            misses += ca.misses + o.misses - cb.misses;
-            nev += ca.nev + o.nev - cb.nev;
-            refc += refa + o.refc - refb;
-            stuck = stuck || stuck_a || (o.stuck_ev >= 0 && o.stuck_ev >= ev);
-            hseg = track ? o.hash + (ha - hb) * pow_mul((uint64_t)(ev1 - ev) * K) : 0ull;
-            load_state<EPL>(A, o.res_end, o.ring_end, lane, W);
+            const int32_t o_stuck = (int32_t)wrec_word<4>(o);
+            misses += ca.misses + wrec_word<0>(o) - cb.misses;
+            nev += ca.nev + wrec_word<1>(o) - cb.nev;
+            refc += refa + wrec_word<2>(o) - refb;
+            stuck = stuck || stuck_a || (o_stuck >= 0 && o_stuck >= ev);
+            const uint64_t o_hash = (uint64_t)wrec_word<6>(o) | ((uint64_t)wrec_word<7>(o) << 32);
+            hseg = track ? o_hash + (ha - hb) * pow_mul((uint64_t)(ev1 - ev) * K) : 0ull;
+            load_state_rec<EPL, 12, 48>(A, o, lane, W);
+            // hist[b] = 16-bit half (b & 1) of word 80 + b / 2: lane 16 + b / 2 of block 2
+            const uint32_t hw = __shfl_sync(FULL_MASK_W, o.w[2], 16 + ((lane >> 1) & 15));
+            const uint32_t h_lane = (lane & 1) ? (hw >> 16) : (hw & 0xFFFFu);   // lane b holds hist[b]
             uint32_t cnt[MCB_SEG_BINS];
 #pragma unroll
             for (int b = 0; b < MCB_SEG_BINS; ++b) {
                 const uint32_t hbv = __shfl_sync(FULL_MASK_W, hb_lane, b);
-                cnt[b] = b <= K ? (uint32_t)o.hist[b] - hbv : 0u;
+                const uint32_t hv = __shfl_sync(FULL_MASK_W, h_lane, b);
+                cnt[b] = b <= K ? hv - hbv : 0u;
             }
             if (!fold_hist_fast(dlat, cnt, K + 1, lut)) {
                 dlat = fold_codes(dlat, codes, ev, ev1, lut);
@@ -710,7 +771,7 @@ __device__ __forceinline__ void wseg_finish(const ReplayParams &P, int64_t chain
             hseg = ha;
             ++unconverged;
         }
-        comp += o.comp;
+        comp += wrec_word<3>(o);
         if (track) h = h * pow_mul((uint64_t)(ev1 - ev0) * K) + hseg;
     }
     if (lane != 0) return;
