@@ -503,13 +503,11 @@ static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int in
     const int E = d.E, H = nets->hidden;
     if (int rc = check_nets(d, nets)) return rc;
     if (int rc = ensure_score_buffers(c, d, nets)) return rc;
-    const size_t per = prepared_net_doubles(E, H);
-    (void)per;
     if (c->nets_pending) CUDA_TRY(cudaStreamWaitEvent(s, c->nets_ev, 0));   // host path: nets copied on side2
     *launched += launch_prepare_nets(nets->params, E, H, nets->num_nets, (double *)c->wt.p, s);
     const int64_t tiles = max_score_tiles(d);
     if (c->k3_tc && !scores && score_tc_eligible(d, H)) {
-        // K3-TC: bf16x3 tcgen05 scorer; events it cannot certify are re-scored in float64
+        // K3-TC: fp16x2 tcgen05 scorer; events it cannot certify are re-scored in float64
         const int nn = nets->num_nets;
         const int64_t cap = nn == 1 ? d.total_events : d.total_events / d.L;
         if (int rc = c->tc_wimg.ensure(score_tc_net_bytes(E) * nn)) return rc;
@@ -545,8 +543,6 @@ static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int in
         *launched += launch_rescore(d, (const double *)c->wt.p, H, nn, (const int32_t *)c->snaps.p,
                                     (const int32_t *)c->tc_flag_cnt.p, (const int32_t *)c->tc_flag_list.p, cap, ranks,
                                     (unsigned long long *)c->stats.p, s);
-        (void)tiles;
-        (void)cap;
         return MCB_OK;
     }
     const int n = launch_score(d, (const double *)c->wt.p, H, nets->num_nets, include_prefill, ranks, scores,
