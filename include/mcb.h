@@ -247,8 +247,8 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
 /* MCB_TUNE_K3_GROUPS: layout of the tensor-core scorer for num_experts <= 64:
  * 3 (default) or 2 epilogue groups (128-event tiles in flight per SM) with
  * the MMA operands in shared memory, or 1 = two groups with the operands in
- * TMEM and a deep weight ring.  num_experts = 128 always runs 2 groups with
- * shared-memory operands.  Ranks are identical. */
+ * TMEM and a deep weight ring.  num_experts = 128 always runs 2 groups, with
+ * the operands in TMEM unless the knob is 2.  Ranks are identical. */
 #define MCB_TUNE_K3_GROUPS 14
 /* MCB_TUNE_UPLOAD_PIECES: mcb_replay_host copies a uniform batch of >= 16
  * traces in this many trace-range pieces (default 8, at most 16; 0/1 = one

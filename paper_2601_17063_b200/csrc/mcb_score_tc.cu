@@ -45,7 +45,8 @@
 // The groups take turns on the tensor pipe: while one group runs its
 // epilogue (features, bias + SiLU + split, or the rank sort), the MMAs of the
 // others' layers run.  E <= 64 runs 3 groups (2 weight stages), E = 128 two
-// groups (its score staging needs 84 KB; 3 weight stages).
+// groups (its score staging needs 84 KB) with the activations as the MMA's A
+// operand in TMEM (tcgen05.st by the epilogue; 3 weight stages).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -83,7 +84,7 @@ struct Shape {
     static constexpr int SMEM = GROUPS * REGION + W_STAGES * W_STAGE + 1024 + 256;
     static constexpr int TMEM_COLS = (TA ? 256 : 128) * GROUPS > 256 ? 512 : 256;
     static constexpr int D_STRIDE = TA ? 256 : 128;                     // TMEM columns per group
-    static_assert(W_STAGES >= (TA ? 4 : 2), "the MMA order holds a job's blocks (TA: all four)");
+    static_assert(W_STAGES >= 2, "the MMA order holds a job's two part-0 blocks at once");
     static_assert(!TA || GROUPS * 256 <= 512, "TMEM: 256 columns per group");
 };
 
@@ -857,7 +858,8 @@ static int set_smem() {
 int preload_score_tc() {
     if (set_smem<8, 3>() || set_smem<16, 3>() || set_smem<32, 3>() || set_smem<64, 3>() || set_smem<8, 2>() ||
         set_smem<16, 2>() || set_smem<32, 2>() || set_smem<64, 2>() || set_smem<128, 2>() ||
-        set_smem<8, 2, true>() || set_smem<16, 2, true>() || set_smem<32, 2, true>() || set_smem<64, 2, true>())
+        set_smem<8, 2, true>() || set_smem<16, 2, true>() || set_smem<32, 2, true>() || set_smem<64, 2, true>() ||
+        set_smem<128, 2, true>())
         return -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -884,7 +886,7 @@ static void launch_variant(const k3tc::Params &P, int variant, cudaStream_t s) {
 // 128-event tile (ranks + flag lists).  snaps: K3 snapshots (launch_score_prep).
 // groups (MCB_TUNE_K3_GROUPS): 3 or 2 epilogue groups with the operands in
 // shared memory, 1 = two groups with the operands in TMEM; E = 128 always
-// runs 2 groups with shared-memory operands.
+// runs 2 groups, with the operands in TMEM unless groups == 2.
 int launch_score_tc(const DevTrace &tr, const double *params, int num_nets, const int32_t *snaps, uint8_t *wimg,
                     float *bias, uint8_t *ranks, float tau, int32_t *flag_cnt, int32_t *flag_list, int64_t bucket_cap,
                     unsigned long long *stats, float *dbg_scores, int groups, cudaStream_t s, bool prep,
@@ -929,7 +931,10 @@ int launch_score_tc(const DevTrace &tr, const double *params, int num_nets, cons
         case 16: launch_variant<16>(P, groups, s); break;
         case 32: launch_variant<32>(P, groups, s); break;
         case 64: launch_variant<64>(P, groups, s); break;
-        default: launch_tc<128, 2>(P, s); break;   // (its score staging leaves no room for a TMEM-operand ring)
+        default:   // two groups (84 KB of score staging each): operands in TMEM (6 % faster), or smem
+            if (groups == 2) launch_tc<128, 2>(P, s);
+            else launch_tc<128, 2, true>(P, s);
+            break;
     }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {

@@ -117,3 +117,24 @@ def test_c5_16_traces_8_budgets_chunked():
     chains = ids.reshape(n * L, T, K)
     check(res, chains, L, E, ["lru", "lfu", "belady"], caps, list(range(n * L)), None)
     check(res, chains[:4 * L], L, E, ["ml"], caps, list(range(4 * L)), nets)
+
+
+def test_piecewise_upload_equals_single_copy():
+    """mcb_replay_host's piecewise upload (trace-range pieces; K2, snapshots and
+    K3-TC per piece as it lands, one float64 re-score) gives the same reports,
+    float64 latencies and per-chain decision hashes as one copy."""
+    L, E, K, T, n = 6, 64, 6, 512, 64
+    ids = refgen.generate_decode_batch(TraceHeader("pieces", L, E, K), list(range(n)), T, popularity_seed=7,
+                                       recency_boost=0.3, w_hot=4).cpu().numpy()
+    pols, caps = ["lru", "lfu", "belady", "ml"], [8, 16]
+    nets = nets_for(L, E)
+    packed = mcb.packed_from_decode_ids(ids, E)
+    out = {}
+    for pieces in (8, 0):
+        _lib.set_tuning(_lib.MCB_TUNE_UPLOAD_PIECES, pieces)
+        try:
+            out[pieces] = run(packed, pols, caps, nets)
+        finally:
+            _lib.set_tuning(_lib.MCB_TUNE_UPLOAD_PIECES, 8)
+    for key in ("reports", "latency", "hashes"):
+        assert np.array_equal(out[8][key], out[0][key]), key
