@@ -171,6 +171,23 @@ typedef struct mcb_ctx mcb_ctx;
 int mcb_abi_version(void);
 int mcb_ctx_create(int device, mcb_ctx **out);
 int mcb_ctx_destroy(mcb_ctx *ctx);
+
+/* ---- Multi-GPU: the context's NCCL communicator ----
+ * The sharded engine (one process per GPU, traces or layers per rank) needs
+ * one collective: an in-place int64 sum of the per-(trace, policy, capacity)
+ * counters and float64 latency bit patterns, every slot written by exactly
+ * one rank (paper_2601_17063_b200/distributed.py).  These entry points give a
+ * non-Python caller that collective; the reference's counterpart is the
+ * thread pool of sweep(jobs) (engine.py:456-464).  NCCL is loaded at run
+ * time (MCB_ERR_UNSUPPORTED without it).
+ * mcb_comm_unique_id: rank 0 creates the 128-byte id and shares it;
+ * mcb_comm_init: every rank joins with it (the context then owns the
+ * communicator until mcb_comm_destroy / mcb_ctx_destroy);
+ * mcb_comm_allreduce_i64: in-place sum of count int64 on a device buffer. */
+int mcb_comm_unique_id(uint8_t *out, int32_t n);
+int mcb_comm_init(mcb_ctx *ctx, int32_t nranks, int32_t rank, const uint8_t *unique_id);
+int mcb_comm_allreduce_i64(mcb_ctx *ctx, int64_t *buf, int64_t count, void *stream);
+int mcb_comm_destroy(mcb_ctx *ctx);
 int mcb_last_error(char *buf, size_t n);
 /* Launch statistics of the last mcb_replay on this context: number of kernels
  * launched, and the uncertain-rank counter of the ML scorer (events whose

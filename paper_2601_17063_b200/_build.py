@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
           "--expt-relaxed-constexpr", "-Xptxas", "-v", f"-I{os.path.join(HERE, '..', 'include')}"]
-SOURCES = ["mcb_pack.cpp", "mcb_api.cu", "mcb_kernels.cu", "mcb_segment.cu", "mcb_segment_warp.cu", "mcb_router.cu", "mcb_refgen.cu", "mcb_lecar.cpp", "mcb_tracepack.cu", "mcb_diag.cu", "mcb_train.cu", "mcb_wide.cu", "mcb_score_tc.cu"]
+SOURCES = ["mcb_pack.cpp", "mcb_api.cu", "mcb_kernels.cu", "mcb_segment.cu", "mcb_segment_warp.cu", "mcb_router.cu", "mcb_refgen.cu", "mcb_lecar.cpp", "mcb_tracepack.cu", "mcb_diag.cu", "mcb_train.cu", "mcb_wide.cu", "mcb_score_tc.cu", "mcb_comm.cpp"]
 HEADERS = ["mcb_internal.h", "mcb_kernels.cuh", "mcb_solo.cuh", "mcb_mask.cuh"]
 
 
@@ -57,7 +57,7 @@ def build(verbose: bool = False) -> str:
             if log:
                 sys.stderr.write(log)
     if not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lcublas"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lcublas", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -50,6 +50,7 @@ EXPORTED_SYMBOLS = (
     "mcb_set_timing", "mcb_last_timings", "mcb_set_tuning", "mcb_read_stats",
     "mcb_pack_trace", "mcb_validate_trace", "mcb_packed_view", "mcb_packed_positions", "mcb_packed_free",
     "mcb_replay", "mcb_replay_host", "mcb_next_use", "mcb_score", "mcb_router_topk", "mcb_ar1_hidden", "mcb_gen_reference",
+    "mcb_comm_unique_id", "mcb_comm_init", "mcb_comm_allreduce_i64", "mcb_comm_destroy",
     "mcb_gen_reference_batch", "mcb_score_tc_scores", "mcb_last_chunks",
     "mcb_training_data", "mcb_set_lecar", "mcb_lecar_random", "mcb_pack_decode_ids",
     "mcb_eviction_duel", "mcb_train_epoch", "mcb_train_eval",
@@ -159,6 +160,10 @@ def load_library():
             "mcb_score": ([P, P, P, i32, P, P, P], ctypes.c_int),
             "mcb_router_topk": ([P, P, P, i64, i32, i32, i32, i32, P, P, P], ctypes.c_int),
             "mcb_ar1_hidden": ([P, i64, i32, i32, ctypes.c_double, ctypes.c_uint64, P, P], ctypes.c_int),
+            "mcb_comm_unique_id": ([P, i32], ctypes.c_int),
+            "mcb_comm_init": ([P, i32, i32, P], ctypes.c_int),
+            "mcb_comm_allreduce_i64": ([P, P, i64, P], ctypes.c_int),
+            "mcb_comm_destroy": ([P], ctypes.c_int),
             "mcb_training_data": ([P, P, i32, i32, i32, P, P, P, P], ctypes.c_int),
             "mcb_set_lecar": ([P, ctypes.c_double, ctypes.c_double, i64], ctypes.c_int),
             "mcb_lecar_random": ([i64, i64, P], ctypes.c_int),

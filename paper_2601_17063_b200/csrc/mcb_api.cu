@@ -81,7 +81,12 @@ struct DevBuf {
 
 #define MCB_MAX_ML_CHUNKS 8
 
+#include <nccl.h>
+
+int mcb_comm_release(ncclComm_t *slot);   // mcb_comm.cpp
+
 struct mcb_ctx {
+    ncclComm_t comm = nullptr;         // sharded engine's communicator (mcb_comm_init), owned
     int device = 0;
     std::mutex mu;
     DevBuf next_pos, ranks[2], inst_out, inst_lat, wt, snaps, tile_off, stats, pol_caps;
@@ -369,9 +374,13 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     return MCB_OK;
 }
 
+ncclComm_t *mcb_ctx_comm(mcb_ctx *c) { return &c->comm; }
+int mcb_ctx_device(mcb_ctx *c) { return c->device; }
+
 extern "C" int mcb_ctx_destroy(mcb_ctx *c) {
     if (!c) return MCB_OK;
     cudaSetDevice(c->device);
+    mcb_comm_release(&c->comm);
     DevBuf *all[] = {&c->next_pos, &c->ranks[0], &c->ranks[1], &c->inst_out, &c->inst_lat, &c->wt, &c->snaps,
                      &c->tile_off, &c->stats, &c->pol_caps, &c->h_acc, &c->h_acc_off, &c->h_ev_off,
                      &c->h_rt_off, &c->h_ev_info, &c->h_routed, &c->h_params, &c->h_reports, &c->h_latency,

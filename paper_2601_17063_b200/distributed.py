@@ -261,3 +261,36 @@ def max_over_ranks(x: float, device) -> float:
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+class NativeCommunicator:
+    """The C ABI's own NCCL communicator (mcb_comm_*): the context of one GPU
+    joins an NCCL clique and sums the sharded engine's int64 buffer in place,
+    without torch.distributed -- the path a non-Python caller of libmcb.so
+    uses.  Rank 0 creates the id (``unique_id()``) and shares it out of band."""
+
+    def __init__(self, nranks: int, rank: int, unique_id: bytes, device: int = 0):
+        import ctypes
+        self._lib = _lib.load_library()
+        self._ctx = _lib.context(device)
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(unique_id)
+        _lib.check(self._lib.mcb_comm_init(self._ctx, nranks, rank, buf))
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes
+        lib = _lib.load_library()
+        out = (ctypes.c_uint8 * 128)()
+        _lib.check(lib.mcb_comm_unique_id(out, 128))
+        return bytes(out)
+
+    def all_reduce_(self, t: torch.Tensor) -> torch.Tensor:
+        """In-place sum of a contiguous int64 CUDA tensor over the clique."""
+        import ctypes
+        assert t.is_cuda and t.dtype == torch.int64 and t.is_contiguous()
+        _lib.check(self._lib.mcb_comm_allreduce_i64(self._ctx, t.data_ptr(), t.numel(),
+                                                    ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)))
+        return t
+
+    def close(self):
+        _lib.check(self._lib.mcb_comm_destroy(self._ctx))

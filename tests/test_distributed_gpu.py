@@ -114,3 +114,29 @@ def test_two_rank_shards_equal_one_gpu_run():
         assert kind == "layers"
         assert np.array_equal(rep, want_l["reports"]) and np.array_equal(lat, want_l["latency"])
         assert out["sweep"] == want_s
+
+
+def test_native_communicator_single_rank():
+    """The C ABI's NCCL communicator (mcb_comm_*) on one GPU: a one-rank clique
+    sums in place (the identity), the context refuses a second communicator,
+    and it can be re-created after mcb_comm_destroy."""
+    import torch
+
+    from paper_2601_17063_b200 import _lib
+    from paper_2601_17063_b200.distributed import NativeCommunicator
+    uid = NativeCommunicator.unique_id()
+    assert len(uid) == 128
+    comm = NativeCommunicator(1, 0, uid)
+    try:
+        x = torch.arange(-5, 1000, dtype=torch.int64, device="cuda") * 3
+        want = x.clone()
+        comm.all_reduce_(x)
+        torch.cuda.synchronize()
+        assert torch.equal(x, want)
+        with pytest.raises(Exception):
+            NativeCommunicator(1, 0, NativeCommunicator.unique_id())
+    finally:
+        comm.close()
+    comm = NativeCommunicator(1, 0, NativeCommunicator.unique_id())
+    comm.close()
+    _ = _lib
