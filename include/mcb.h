@@ -237,9 +237,10 @@ int mcb_read_stats(mcb_ctx *ctx, int64_t *out, int32_t n);
 /* MCB_TUNE_OVERLAP: where the non-ML replay runs concurrently -- 0 (default)
  * after the scorer, next to the ML replay; 1 during the scorer. */
 #define MCB_TUNE_OVERLAP 8
-/* MCB_TUNE_WIDE_MIN: minimum instance count for the thread-per-instance
- * replay of 16 < num_experts <= 64 (default 16384); below it one warp
- * replays one instance. */
+/* MCB_TUNE_WIDE_MIN: minimum instance count (per launch) for the
+ * thread-per-instance replay of 16 < num_experts <= 128 (default 8192: e.g.
+ * C4's ML replay at 8 GPUs, 13,824 instances per rank, 26 -> 20 ms); below it
+ * one warp replays one instance. */
 #define MCB_TUNE_WIDE_MIN 9
 /* MCB_TUNE_SEG_TSPEC: speculation of the segmented replay for num_experts
  * > 16 -- 0 automatic (one thread per (instance, segment) for chains of

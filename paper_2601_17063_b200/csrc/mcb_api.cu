@@ -119,7 +119,7 @@ struct mcb_ctx {
     int k3_ctas = -1;                  // K3 grid mode (MCB_TUNE_K3_CTAS)
     int overlap = 0;                   // non-ML replay: 0 after K3 (next to the ML replay), 1 during K3
     int64_t solo_min_instances = 0;   // thread-per-instance whenever E <= 16 (MCB_SOLO_MIN overrides)
-    int64_t wide_min_instances = 16384;   // thread-per-instance for 16 < E <= 64 from this many (MCB_WIDE_MIN)
+    int64_t wide_min_instances = 8192;    // thread-per-instance for 16 < E <= 128 from this many (MCB_WIDE_MIN)
     int64_t seg_ev = 0;               // segmented replay: 0 auto, <0 off, >0 events per segment (MCB_SEG_EV)
     int64_t seg_nw = 0;               // warm-up events before each segment: 0 auto (MCB_SEG_NW)
     int64_t seg_passes = 0;           // speculation passes (MCB_SEG_PASSES): 0 auto, 1 or 2

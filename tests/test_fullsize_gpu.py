@@ -180,7 +180,7 @@ def test_many_trace_wide_replay(shape):
             return engine.replay_host(packed, codes, caps, mcb.CostModel(), 5, nets, want_hashes=True,
                                       want_chain=True)
         finally:
-            _lib.set_tuning(_lib.MCB_TUNE_WIDE_MIN, 16384)
+            _lib.set_tuning(_lib.MCB_TUNE_WIDE_MIN, 8192)
 
     a, b = run(True), run(False)
     assert np.all(a["chain_reports"][..., _lib.R_STATUS] == 0)

@@ -82,7 +82,7 @@ def kernel_variant(request):
     _lib.set_tuning(_lib.MCB_TUNE_SEG_EV, 32 if v == "seg" else -1)
     yield v
     _lib.set_tuning(_lib.MCB_TUNE_SOLO_MIN, 0)
-    _lib.set_tuning(_lib.MCB_TUNE_WIDE_MIN, 16384)
+    _lib.set_tuning(_lib.MCB_TUNE_WIDE_MIN, 8192)
     _lib.set_tuning(_lib.MCB_TUNE_GROUP_LANES, 0)
     _lib.set_tuning(_lib.MCB_TUNE_SEG_EV, 0)
 
