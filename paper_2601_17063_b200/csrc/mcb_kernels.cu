@@ -86,6 +86,39 @@ __global__ void __launch_bounds__(128) k_next_use(DevTrace tr, int64_t blk_acc, 
         for (int e = lane; e < E; e += 32) tab_out[id * E + e] = tbl[e];
 }
 
+// Many chains (C4, C5, their per-rank shares): one THREAD per chain walks it
+// backwards with its own table [E][thread] in shared memory (last position
+// seen per expert) -- no warp MATCH (the warp walk is MIO-throttled), 16 ids
+// per vector load with the next one in flight, 16 results per four 16-byte
+// stores.  Uniform traces with T*K a multiple of 16.
+__global__ void __launch_bounds__(128) k_next_use_thread(DevTrace tr, uint32_t *__restrict__ next_pos) {
+    extern __shared__ uint32_t s_nu[];   // [E][128]
+    const int64_t c = (int64_t)blockIdx.x * 128 + threadIdx.x;
+    if (c >= tr.n_chains) return;
+    const int E = tr.E;
+    uint32_t *tab = s_nu + threadIdx.x;
+    for (int e = 0; e < E; ++e) tab[e * 128] = MCB_NEXT_INF;
+    const int64_t len = tr.T * tr.K;
+    const uint4 *src = (const uint4 *)(tr.acc + c * len);
+    uint4 *dst = (uint4 *)(next_pos + c * len);
+    const int64_t nb = len / 16;
+    uint4 nxt = nb > 0 ? __ldg(src + nb - 1) : make_uint4(0, 0, 0, 0);
+    for (int64_t b = nb - 1; b >= 0; --b) {
+        const uint4 v = nxt;
+        if (b > 0) nxt = __ldg(src + b - 1);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        uint32_t r[16];
+#pragma unroll
+        for (int i = 15; i >= 0; --i) {
+            const uint32_t x = (w[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+            r[i] = tab[x * 128];
+            tab[x * 128] = (uint32_t)(b * 16 + i);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[b * 4 + q] = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+    }
+}
+
 // firsts[c][b][e] (first occurrence in block b) -> after[c][b][e] (first
 // occurrence in any later block), one thread per (chain, expert)
 __global__ void k_next_use_blocks(int64_t n_chains, int E, int64_t n_blk, const uint32_t *__restrict__ firsts,
@@ -121,6 +154,11 @@ size_t next_use_scratch_words(const DevTrace &tr) {
 
 int launch_next_use(const DevTrace &tr, uint32_t *next_pos, uint32_t *scratch, cudaStream_t s) {
     if (tr.n_chains == 0) return 0;
+    if (tr.uniform && tr.n_chains >= 8192 && (tr.T * tr.K) % 16 == 0 && tr.E <= MCB_MAX_EXPERTS) {
+        k_next_use_thread<<<(unsigned)((tr.n_chains + 127) / 128), 128, (size_t)tr.E * 128 * sizeof(uint32_t), s>>>(
+            tr, next_pos);
+        return 1;
+    }
     const int64_t nb = scratch ? next_use_blocks(tr) : 1;
     if (nb <= 1) {
         const int64_t blocks = (tr.n_chains + 3) / 4;
@@ -2149,7 +2187,7 @@ int preload_kernels() {
     cudaFuncAttributes a;
     const void *fns[] = {
         (const void *)k_next_use<true>, (const void *)k_next_use<false>, (const void *)k_next_use_blocks,
-        (const void *)k_fold, (const void *)k_train_features, (const void *)k_train_targets, (const void *)k_prepare_nets, (const void *)k_tile_offsets,
+        (const void *)k_next_use_thread, (const void *)k_fold, (const void *)k_train_features, (const void *)k_train_targets, (const void *)k_prepare_nets, (const void *)k_tile_offsets,
         (const void *)k_feat_snap, (const void *)k_tile_summary, (const void *)k_snap_scan,
         (const void *)k_snap_scan_tiles,
         (const void *)k_score_tile<0, 0>, (const void *)k_score_tile<8, 128>, (const void *)k_score_tile<16, 128>,
@@ -2165,6 +2203,9 @@ int preload_kernels() {
         (const void *)k_replay_solo<8, true>, (const void *)k_replay_solo<8, false>,
         (const void *)k_replay_solo<16, true>, (const void *)k_replay_solo<16, false>,
     };
+    if (cudaFuncSetAttribute(k_next_use_thread, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             MCB_MAX_EXPERTS * 128 * (int)sizeof(uint32_t)) != cudaSuccess)
+        return -1;
     for (const void *f : fns)
         if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -1;
     cudaFuncSetAttribute(k_replay_solo<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);

@@ -301,3 +301,33 @@ def test_scorer_ranks_match_scores(E, H):
     want = 1 + (s[:, None, :] < s[:, :, None]).sum(axis=2)
     assert np.array_equal(rk, want)
     assert np.all(rk[:, E // 2] == rk[:, 0])
+
+
+@pytest.mark.parametrize("E,K,T", [(64, 6, 64), (128, 8, 32), (32, 4, 100)])
+def test_next_use_thread_walk_matches_numpy(E, K, T):
+    """K2 for many chains (>= 8,192: one thread per chain, shared-memory table,
+    vector loads / stores) against a vectorised numpy reference; T*K = 100*4
+    is a multiple of 16, 64*6 = 384 and 32*8 = 256 too."""
+    import ctypes
+
+    import torch
+    rng = np.random.default_rng(E + K)
+    n_chains = 8300
+    ids = np.argsort(rng.random((n_chains, T, E)), axis=2)[:, :, :K].astype(np.uint8)   # distinct per event
+    packed = mcb.packed_from_decode_ids(ids[None], E)
+    dev_acc = torch.from_numpy(packed.acc).cuda()
+    v = packed.view()
+    v.acc = dev_acc.data_ptr()
+    out = torch.zeros(packed.total_acc + 64, dtype=torch.int32, device="cuda")
+    lib = _lib.load_library()
+    _lib.check(lib.mcb_next_use(_lib.context(0), ctypes.byref(v), out.data_ptr(), None))
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().view(np.uint32)[:packed.total_acc].reshape(n_chains, T * K).astype(np.int64)
+    s = ids.reshape(n_chains, T * K).astype(np.int64)
+    want = np.full(s.shape, 0xFFFFFFFF, dtype=np.int64)
+    last = np.full((n_chains, E), 0xFFFFFFFF, dtype=np.int64)
+    rows = np.arange(n_chains)
+    for p in range(T * K - 1, -1, -1):
+        want[:, p] = last[rows, s[:, p]]
+        last[rows, s[:, p]] = p
+    assert np.array_equal(got, want)
