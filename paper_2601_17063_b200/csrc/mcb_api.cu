@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 
 #include <cstdio>
 #include <cstdlib>
@@ -99,7 +100,9 @@ struct mcb_ctx {
     bool timing = false;
     cudaStream_t side = nullptr;       // non-ML replay runs here concurrently with K3
     cudaEvent_t fork = nullptr, join = nullptr;
-    cudaStream_t side2 = nullptr;      // ML replay chunks, pipelined behind the K3 chunks
+    cudaStream_t side2 = nullptr;      // ML replay chunks, pipelined behind the K3 chunks; the ML replay after K3
+    cudaStream_t side_lo = nullptr;    // the non-ML replay after K3 (least priority: the ML replay's blocks go first)
+    cudaEvent_t join_lo = nullptr;
     cudaEvent_t chunk_ev[MCB_MAX_ML_CHUNKS] = {};
     cudaEvent_t join2 = nullptr;
     cudaEvent_t pre = nullptr;         // the side stream's replay preparation is done
@@ -113,6 +116,7 @@ struct mcb_ctx {
     int64_t piece_chain[MCB_MAX_UPLOAD_PIECES + 1] = {};
     int64_t upload_pieces = 8;         // MCB_TUNE_UPLOAD_PIECES
     bool pieces_next = false;          // the pieced K3 loop also runs K2 per piece
+    std::function<int()> before_rescore;   // replay_locked: start the non-ML replay under the re-score
     size_t pieces_nu_sw = 0;
     bool nets_pending = false;         // the scorer must wait for nets_ev before using the nets
     int64_t ml_chunks = 1;             // K3 / ML replay pipeline depth (MCB_TUNE_ML_CHUNKS)
@@ -126,6 +130,8 @@ struct mcb_ctx {
     int seg_tspec = 0;                // E > 16 speculation: 0 auto, 1 thread, -1 warp (MCB_SEG_TSPEC)
     int64_t group_lanes = 0;          // lanes per instance of the E > 16 replay: 0 auto, 8 / 16 / 32
     int64_t scratch_bytes = 0;        // per-call scratch budget (MCB_TUNE_SCRATCH_BYTES): 0 = 40% of free
+    int64_t fit_need = 0;             // largest scratch estimate replayed in one range (its buffers are held)
+    int64_t mem_total = 0;            // device memory (cudaDeviceProp::totalGlobalMem)
     int64_t last_chunks = 1;          // trace ranges of the last mcb_replay
     bool serial = false;              // one stream for every stage (per-stage attribution timing)
     DevBuf seg_snap, seg_summ, seg_out, seg_codes, nu_scratch;
@@ -328,6 +334,7 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     auto *c = new (std::nothrow) mcb_ctx();
     if (!c) return mcb_set_error(MCB_ERR_NOMEM, "out of host memory");
     c->device = device;
+    c->mem_total = (int64_t)prop.totalGlobalMem;
     if (const char *env = getenv("MCB_SOLO_MIN")) c->solo_min_instances = atoll(env);
     if (const char *env = getenv("MCB_WIDE_MIN")) c->wide_min_instances = atoll(env);
     if (const char *env = getenv("MCB_SEG_EV")) c->seg_ev = atoll(env);
@@ -359,6 +366,8 @@ extern "C" int mcb_ctx_create(int device, mcb_ctx **out) {
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c->side2, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c->side_lo, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->join_lo, cudaEventDisableTiming) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join2, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->pre, cudaEventDisableTiming) != cudaSuccess ||
@@ -393,6 +402,8 @@ extern "C" int mcb_ctx_destroy(mcb_ctx *c) {
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->side2) cudaStreamDestroy(c->side2);
+    if (c->side_lo) cudaStreamDestroy(c->side_lo);
+    if (c->join_lo) cudaEventDestroy(c->join_lo);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     for (auto &e : c->up_ev)
         if (e) cudaEventDestroy(e);
@@ -548,6 +559,10 @@ static int run_score(mcb_ctx *c, const DevTrace &d, const mcb_nets *nets, int in
                                              lo * d.T);
             if (n_tc < 0) return MCB_ERR_CUDA;
             *launched += n_tc;
+        }
+        if (c->before_rescore) {   // (the float64 re-score leaves most of the GPU to the non-ML replay)
+            if (int rc = c->before_rescore()) return rc;
+            c->before_rescore = nullptr;
         }
         *launched += launch_rescore(d, (const double *)c->wt.p, H, nn, (const int32_t *)c->snaps.p,
                                     (const int32_t *)c->tc_flag_cnt.p, (const int32_t *)c->tc_flag_list.p, cap, ranks,
@@ -820,17 +835,25 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
     // Where the non-ML replay overlaps: during K3 (it then competes with the
     // scorer for issue slots), or after it, next to the ML replay (both are
     // latency-bound and leave most of the GPU idle).  See MCB_TUNE_OVERLAP.
+    // After K3 the two replays run side by side for the rest of the step; the
+    // ML replay (side2, highest priority) is the longer chain of the two, so its
+    // blocks are dispatched ahead of the non-ML replay's (side_lo, least
+    // priority) -- at equal priority the launch order decides, and a non-ML
+    // grid queued first delayed the ML replay by up to 80 ms on C4.
     auto launch_non_ml = [&]() -> int {
+        cudaStream_t sx = after_k3 ? c->side_lo : sn;
         if (split) {
             CUDA_TRY(cudaEventRecord(c->fork, s));
-            CUDA_TRY(cudaStreamWaitEvent(c->side, c->fork, 0));
+            CUDA_TRY(cudaStreamWaitEvent(sx, c->fork, 0));
+            if (after_k3) CUDA_TRY(cudaStreamWaitEvent(sx, c->pre, 0));
         }
         if (Pn.n_pol_launch > 0) {
-            mark(c, 4, sn);
-            launched += seg_eligible(Pn) ? launch_replay_segmented(Pn, sn) : launch_replay(Pn, sn);
-            mark(c, 5, sn);
+            mark(c, 4, sx);
+            launched += seg_eligible(Pn) ? launch_replay_segmented(Pn, sx) : launch_replay(Pn, sx);
+            mark(c, 5, sx);
             c->ran[2] = true;
         }
+        if (after_k3) CUDA_TRY(cudaEventRecord(c->join_lo, sx));
         return MCB_OK;
     };
     if (!after_k3)
@@ -878,21 +901,43 @@ static int replay_locked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, in
         c->ran[3] = true;
     } else if (Pm.n_pol_launch > 0) {
         // The ML replay needs K3's ranks; it follows K3 on the same stream.
+        // With the replays after K3, the non-ML replay starts between the
+        // tensor-core scorer and its float64 re-score (run_score's hook).
         mark(c, 2, s);
+        bool non_ml_started = false;
+        if (after_k3)
+            c->before_rescore = [&]() -> int {
+                non_ml_started = true;
+                return launch_non_ml();
+            };
         for (int v = 0; v < 2; ++v) {
             if (!need_ml[v]) continue;
-            if (int rc = run_score(c, d, nets, v == 0 ? 1 : 0, (uint8_t *)c->ranks[v].p, nullptr, s, &launched))
+            const int rc = run_score(c, d, nets, v == 0 ? 1 : 0, (uint8_t *)c->ranks[v].p, nullptr, s, &launched);
+            if (rc) {
+                c->before_rescore = nullptr;
                 return rc;
+            }
             Pm.rank[v] = (const uint8_t *)c->ranks[v].p;
         }
+        c->before_rescore = nullptr;
         mark(c, 3, s);
+        cudaStream_t sm = s;
         if (after_k3) {
-            if (int rc = launch_non_ml()) return rc;
-            CUDA_TRY(cudaStreamWaitEvent(s, c->pre, 0));   // key snapshots / next-use for the ML replay
+            if (!non_ml_started)
+                if (int rc = launch_non_ml()) return rc;
+            sm = c->side2;
+            CUDA_TRY(cudaEventRecord(c->fork, s));
+            CUDA_TRY(cudaStreamWaitEvent(sm, c->fork, 0));
+            CUDA_TRY(cudaStreamWaitEvent(sm, c->pre, 0));   // key snapshots / next-use for the ML replay
         }
-        mark(c, 6, s);
-        launched += seg_eligible(Pm) ? launch_replay_segmented(Pm, s) : launch_replay(Pm, s);
-        mark(c, 7, s);
+        mark(c, 6, sm);
+        launched += seg_eligible(Pm) ? launch_replay_segmented(Pm, sm) : launch_replay(Pm, sm);
+        mark(c, 7, sm);
+        if (after_k3) {
+            CUDA_TRY(cudaEventRecord(c->join2, sm));
+            CUDA_TRY(cudaStreamWaitEvent(s, c->join2, 0));
+            CUDA_TRY(cudaStreamWaitEvent(s, c->join_lo, 0));
+        }
         c->ran[1] = true;
         c->ran[3] = true;
     }
@@ -1000,14 +1045,26 @@ static int replay_chunked(mcb_ctx *c, const mcb_trace *t, const int32_t *pols, i
     // is independent, so the results are those of one call.
     int64_t per = t->uniform && t->num_traces > 1 ? scratch_per_trace(t, pols, n_pol, n_cap) : 0;
     int64_t budget = c->scratch_bytes;
+    // cudaMemGetInfo is a driver round trip that took 3-76 ms on the GPU box
+    // (measured, tools/var_probe.py): a call whose whole scratch is below 10%
+    // of the device does not ask for the free memory.
+    if (per > 0 && budget == 0 && per * t->num_traces <= c->mem_total / 10) budget = per * t->num_traces;
+    // cudaMemGetInfo is a driver round trip that took 3-80 ms on the GPU box
+    // (tools/var_probe.py, host-side stalls of the whole step); a call whose
+    // scratch fits the buffers an earlier one-range call left does not ask.
+    const int64_t need = per * t->num_traces;
+    if (per > 0 && budget == 0 && need <= c->fit_need) budget = need;
     if (per > 0 && budget == 0) {
         size_t fr = 0, tot = 0;
         CUDA_TRY(cudaMemGetInfo(&fr, &tot));
         budget = (int64_t)(fr * 0.4);
     }
     const int64_t per_chunk = per > 0 ? std::max<int64_t>(1, budget / per) : t->num_traces;
-    if (per == 0 || per_chunk >= t->num_traces || out->outcomes)
-        return replay_locked(c, t, pols, n_pol, caps, n_cap, cost, nets, out, (cudaStream_t)stream);
+    if (per == 0 || per_chunk >= t->num_traces || out->outcomes) {
+        const int rc = replay_locked(c, t, pols, n_pol, caps, n_cap, cost, nets, out, (cudaStream_t)stream);
+        if (rc == MCB_OK && per > 0 && c->scratch_bytes == 0) c->fit_need = std::max(c->fit_need, need);
+        return rc;
+    }
     for (int k = 0; k < c->n_pieces; ++k)   // trace ranges of their own: the whole upload first
         CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, c->up_ev[k], 0));
     c->n_pieces = 0;

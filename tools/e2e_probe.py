@@ -54,7 +54,7 @@ print("H2D copy of the trace", timed(lambda: dst.copy_(acc_pinned, non_blocking=
 import ctypes  # noqa: E402
 lib = _lib.load_library()
 _lib.check(lib.mcb_set_timing(_lib.context(0), 1))
-for u in (4, 8, 4, 3, 1):
+for u in (8, 1, 8):
     _lib.set_tuning(_lib.MCB_TUNE_UPLOAD_PIECES, u)
     print(f"replay_host pieces={u}", timed(lambda: replay_host(packed, codes, wl["caps"], CostModel(), 5, nets_host,
                                                              stream=st.cuda_stream)))
