@@ -329,17 +329,54 @@ __device__ __forceinline__ void wkey_update(uint32_t (&key)[EPL], bool mine, int
     }
 }
 
+// This lane's EPL bytes of an event's rank row, packed (byte s = expert
+// lane * EPL + s); one 32- / 16-bit load when the row splits evenly.
 template <int EPL>
-__device__ __forceinline__ void wml_keys(uint32_t (&key)[EPL], uint32_t &valid, const uint8_t *row, int lane, int E) {
-    valid = 0u;
+__device__ __forceinline__ uint32_t wrow_load(const uint8_t *row, int lane, int E) {
+    const int e = lane * EPL;
+    if (EPL == 4 && (E & 3) == 0) return e < E ? __ldcg((const uint32_t *)row + lane) : 0u;
+    if (EPL == 2 && (E & 1) == 0) return e < E ? (uint32_t)__ldcg((const uint16_t *)row + lane) : 0u;
+    uint32_t v = 0u;
 #pragma unroll
-    for (int s = 0; s < EPL; ++s) {
-        const int e = lane * EPL + s;
-        const uint32_t r = e < E ? (uint32_t)__ldcg(row + e) : 0u;
-        key[s] = r ? 256u - r : WKEY_SENT;
-        valid |= (r ? 1u : 0u) << s;
-    }
+    for (int s = 0; s < EPL; ++s)
+        if (e + s < E) v |= (uint32_t)__ldcg(row + e + s) << (8 * s);
+    return v;
 }
+
+// The per-event rank rows of a run of events, two events in flight ahead of
+// the one being replayed (a row load is an L2 / HBM round trip; one event of
+// K accesses is shorter than that on a warp that issues alone).
+template <int EPL>
+struct WRows {
+    const uint8_t *row;   // the next row to load
+    int64_t left;         // rows left to load
+    int E;
+    uint32_t r0, r1;
+    __device__ __forceinline__ void init(const uint8_t *first, int64_t n, int E_, int lane) {
+        row = first;
+        left = n;
+        E = E_;
+        r0 = left > 0 ? wrow_load<EPL>(row, lane, E) : 0u;
+        r1 = left > 1 ? wrow_load<EPL>(row + E, lane, E) : 0u;
+        row += 2 * (int64_t)E;
+        left -= 2;
+    }
+    // this event's keys and selectable mask; starts the load two events ahead
+    __device__ __forceinline__ void next(uint32_t (&key)[EPL], uint32_t &valid, int lane) {
+        const uint32_t r = r0;
+        r0 = r1;
+        r1 = left > 0 ? wrow_load<EPL>(row, lane, E) : 0u;
+        row += E;
+        --left;
+        valid = 0u;
+#pragma unroll
+        for (int s = 0; s < EPL; ++s) {
+            const uint32_t b = (r >> (8 * s)) & 0xFFu;
+            key[s] = b ? 256u - b : WKEY_SENT;
+            valid |= (b ? 1u : 0u) << s;
+        }
+    }
+};
 
 template <int EPL, int POL>
 __device__ __forceinline__ void wseg_spec(const ReplayParams &P, int64_t chain, int seg, int pol_i, int cap_i,
@@ -383,6 +420,8 @@ __device__ __forceinline__ void wseg_spec(const ReplayParams &P, int64_t chain, 
     uint32_t word = 0;
     WReplay<EPL, POL> rp;
     rp.init(P, a0 + ws * K, lane);
+    WRows<EPL> rows;
+    if (POL == POL_ML) rows.init(rank + (e0 + ws) * E, ev1 - ws, E, lane);
 
     for (int64_t ev = ws; ev < ev1; ++ev) {
         if (ev == ev0) {
@@ -391,7 +430,7 @@ __device__ __forceinline__ void wseg_spec(const ReplayParams &P, int64_t chain, 
             comp = 0u;
             stuck = false;
         }
-        if (POL == POL_ML) wml_keys<EPL>(key, valid, rank + (e0 + ev) * E, lane, E);
+        if (POL == POL_ML) rows.next(key, valid, lane);
         uint32_t pin = 0, sm = 0;
         for (int j = 0; j < K; ++j) {
             const int64_t A = a0 + ev * K + j;
@@ -709,8 +748,10 @@ __device__ __forceinline__ void wseg_finish(const ReplayParams &P, int64_t chain
             uint32_t valid = valid0;
             WReplay<EPL, POL> rp;
             rp.init(P, a0 + ev0 * K, lane);
+            WRows<EPL> rows;
+            if (POL == POL_ML) rows.init(rank + (e0 + ev0) * E, ev1 - ev0, E, lane);
             while (!conv && ev < ev1) {
-                if (POL == POL_ML) wml_keys<EPL>(key, valid, rank + (e0 + ev) * E, lane, E);
+                if (POL == POL_ML) rows.next(key, valid, lane);
                 uint32_t pin = 0, sma = 0, smb = 0;
                 for (int j = 0; j < K; ++j) {
                     const int64_t Aa = a0 + ev * K + j;
