@@ -56,7 +56,8 @@
 bool seg_eligible(const ReplayParams &p) {
     return p.seg.n_seg > 1 && p.tr.uniform && p.tr.E <= MCB_MAX_EXPERTS && p.tr.K + 1 <= MCB_SEG_BINS &&
            p.outcomes == nullptr && p.window >= 0 && p.window <= SOLO_WMAX &&
-           p.tr.T * p.tr.K < (1ll << 27);   // chain-local positions pack into 27 bits
+           p.tr.T * p.tr.K < (1ll << 27) &&   // chain-local positions pack into 27 bits
+           (p.tr.E <= SEG_MAX_E || p.tr.T * p.tr.K < (1ll << 25));   // 25 bits in the warp version's keys
 }
 
 int seg_events_per_segment(int64_t T, int64_t n_inst_launch, int64_t override_se, int E, bool paired) {

@@ -22,6 +22,12 @@
 #include "mcb_solo.cuh"
 
 #define WKEY_SENT 0xFFFFFFFFu
+// Warp replay keys are packed (key << WKEY_SH | expert) so that the warp-wide
+// minimum names the victim (ties to the smallest id, as before the packing);
+// chain-local positions must stay below 2^25 (seg_eligible).
+#define WKEY_SH 7
+#define WKEY_ID 0x7Fu
+#define WKEY_KMAX ((1u << (32 - WKEY_SH)) - 1u)
 
 template <int EPL>
 struct WState {
@@ -53,22 +59,20 @@ __device__ __forceinline__ uint32_t wstep(WState<EPL> &S, const uint32_t (&key)[
     if (hit) return MCB_OUT_HIT;
     uint32_t code = MCB_OUT_MISS, vbit = 0u;
     if (S.count >= C) {
+        // keys are packed (key << 7 | expert): the warp minimum is the victim,
+        // ties to the smallest id
         const uint32_t cand = S.res & ~pin & valid;
         uint32_t lk = WKEY_SENT;
-        int ls = 0;
 #pragma unroll
-        for (int s = 0; s < EPL; ++s)
-            if (((cand >> s) & 1u) && key[s] < lk) { lk = key[s]; ls = s; }
+        for (int s = 0; s < EPL; ++s) lk = min(lk, ((cand >> s) & 1u) ? key[s] : WKEY_SENT);
         const uint32_t m = __reduce_min_sync(FULL_MASK_W, lk);
         stuck |= m == WKEY_SENT;
-        const unsigned b = __ballot_sync(FULL_MASK_W, lk == m);
-        const int wl = __ffs(b) - 1;
-        const int vs = __shfl_sync(FULL_MASK_W, ls, wl);
-        if (lane == wl) {
-            vbit = 1u << vs;
+        const uint32_t v = m & WKEY_ID;
+        if (lane == (int)(v / EPL)) {
+            vbit = 1u << (v % EPL);
             S.res &= ~vbit;
         }
-        code = (uint32_t)(wl * EPL + vs);
+        code = v;
         ++n.nev;
     } else {
         ++S.count;
@@ -268,12 +272,15 @@ __device__ __forceinline__ void wkeys_at(const ReplayParams &P, int64_t chain, i
         uint32_t k = 0u;
         if (POL == POL_LRU) k = v.x >= 0 ? (uint32_t)v.x : 0u;
         if (POL == POL_LFU) k = (uint32_t)v.y;
-        if (POL == POL_BELADY) k = ~(v.x >= 0 ? __ldg(P.next_pos + a0 + v.x) : MCB_NEXT_INF);
+        if (POL == POL_BELADY) {
+            const uint32_t np = v.x >= 0 ? __ldg(P.next_pos + a0 + v.x) : MCB_NEXT_INF;
+            k = np == MCB_NEXT_INF ? 0u : WKEY_KMAX - np;
+        }
+        key[s] = (k << WKEY_SH) | (uint32_t)e;
         if (POL == POL_ML) {
             const uint32_t r = (ev > 0 && e < E) ? (uint32_t)__ldcg(P.rank[ml_variant] + (tr.ev_begin(chain) + ev - 1) * E + e) : 0u;
-            k = r ? 256u - r : WKEY_SENT;
+            key[s] = r ? ((256u - r) << WKEY_SH) | (uint32_t)e : WKEY_SENT;
         }
-        key[s] = k;
     }
 }
 
@@ -284,48 +291,79 @@ __device__ __forceinline__ uint32_t wguess(const uint32_t (&key)[EPL], uint32_t 
     uint32_t chosen = 0u;
     for (uint32_t r = 0; r < n_res; ++r) {
         // largest key among the unchosen seen experts, ties to the largest id
+        // (packed: (key + 1) << 7 | id, a non-selectable ML score as the bare
+        // id, below every other key; a lane without candidates offers 0, and
+        // a candidate always remains, so a maximum of 0 is expert 0)
         uint32_t lk = 0u;
-        int ls = -1;
 #pragma unroll
         for (int s = 0; s < EPL; ++s)
-            if (((seen & ~chosen) >> s) & 1u) {
-                const uint32_t k = key[s] == WKEY_SENT ? 0u : key[s] + 1u;
-                if (ls < 0 || k >= lk) { lk = k; ls = s; }
-            }
-        const uint32_t m = __reduce_max_sync(FULL_MASK_W, ls >= 0 ? lk : 0u);
-        const unsigned b = __ballot_sync(FULL_MASK_W, ls >= 0 && lk == m);
-        const int wl = 31 - __clz(b);
-        if (lane == wl) chosen |= 1u << ls;
+            if (((seen & ~chosen) >> s) & 1u)
+                lk = max(lk, key[s] == WKEY_SENT ? (uint32_t)(lane * EPL + s) : key[s] + (1u << WKEY_SH));
+        const uint32_t m = __reduce_max_sync(FULL_MASK_W, lk);
+        const uint32_t v = m & WKEY_ID;
+        if (lane == (int)(v / EPL)) chosen |= 1u << (v % EPL);
     }
     return chosen;
 }
 
 // ---------------------------------------------------------------- replay --
-template <int EPL, int POL>
-struct WReplay {
-    // access stream of one chain from access index a
-    U32Stream<32> ids;
-    U32Stream<32> nx;
-    __device__ __forceinline__ void init(const ReplayParams &P, int64_t a, int lane) {
-        ids.init(P.tr.acc, (P.tr.total_acc + 3) >> 2, a >> 2, lane);
-        if (POL == POL_BELADY) nx.init(P.next_pos, P.tr.total_acc, a, lane);
+// Sequential reader of a word stream by the whole warp: 32-word chunks, one
+// word per lane, the next chunk in flight; `off` counts items (of 32 / PER
+// bits) consumed in the current chunk, so an item costs one shuffle.
+template <int PER>   // items per word: 4 (uint8 ids) or 1 (uint32 next-use positions)
+struct WCursor {
+    const uint32_t *p;     // the next chunk to load (this lane's word)
+    const uint32_t *end;   // one past the last readable word
+    uint32_t cur, nxt, off;
+    __device__ __forceinline__ uint32_t load(const uint32_t *q) const { return q < end ? __ldg(q) : 0u; }
+    __device__ __forceinline__ void init(const void *base, int64_t words, int64_t first_item, int lane) {
+        const int64_t w0 = (first_item / PER) & ~(int64_t)31;   // the chunk holding the first item
+        end = (const uint32_t *)base + words;
+        p = (const uint32_t *)base + w0 + lane;
+        cur = load(p);
+        nxt = load(p + 32);
+        p += 64;
+        off = (uint32_t)(first_item - w0 * PER);
     }
-    __device__ __forceinline__ uint32_t id(int64_t A, int lane) {
-        const uint32_t word = ids.get(A >> 2, lane, 0, FULL_MASK_W);
-        return (word >> (8 * (uint32_t)(A & 3))) & 0xFFu;
+    __device__ __forceinline__ uint32_t get() {
+        if (off == 32u * PER) {
+            cur = nxt;
+            nxt = load(p);
+            p += 32;
+            off = 0u;
+        }
+        const uint32_t w = __shfl_sync(FULL_MASK_W, cur, (int)(off / PER));
+        const uint32_t v = PER == 4 ? (w >> (8u * (off & 3u))) & 0xFFu : w;
+        ++off;
+        return v;
     }
-    __device__ __forceinline__ uint32_t next(int64_t A, int lane) { return nx.get(A, lane, 0, FULL_MASK_W); }
 };
 
 template <int EPL, int POL>
-__device__ __forceinline__ void wkey_update(uint32_t (&key)[EPL], bool mine, int slot, uint32_t pos, uint32_t np) {
+struct WReplay {
+    // access stream of one chain from access index a, read in order
+    WCursor<4> ids;
+    WCursor<1> nx;
+    __device__ __forceinline__ void init(const ReplayParams &P, int64_t a, int lane) {
+        ids.init(P.tr.acc, (P.tr.total_acc + 3) >> 2, a, lane);
+        if (POL == POL_BELADY) nx.init(P.next_pos, P.tr.total_acc, a, lane);
+    }
+    __device__ __forceinline__ uint32_t id() { return ids.get(); }
+    __device__ __forceinline__ uint32_t next() { return nx.get(); }
+};
+
+template <int EPL, int POL>
+__device__ __forceinline__ void wkey_update(uint32_t (&key)[EPL], bool mine, int slot, uint32_t x, uint32_t pos,
+                                            uint32_t np) {
     if (!mine) return;
+    uint32_t k = 0u;
+    if (POL == POL_LRU) k = (pos << WKEY_SH) | x;
+    if (POL == POL_BELADY) k = ((np == MCB_NEXT_INF ? 0u : WKEY_KMAX - np) << WKEY_SH) | x;
 #pragma unroll
     for (int s = 0; s < EPL; ++s) {
         if (s != slot) continue;
-        if (POL == POL_LRU) key[s] = pos;
-        if (POL == POL_LFU) key[s] += 1u;
-        if (POL == POL_BELADY) key[s] = ~np;
+        if (POL == POL_LFU) key[s] += 1u << WKEY_SH;
+        else if (POL == POL_LRU || POL == POL_BELADY) key[s] = k;
     }
 }
 
@@ -363,6 +401,7 @@ struct WRows {
     }
     // this event's keys and selectable mask; starts the load two events ahead
     __device__ __forceinline__ void next(uint32_t (&key)[EPL], uint32_t &valid, int lane) {
+        const uint32_t e0 = (uint32_t)(lane * EPL);
         const uint32_t r = r0;
         r0 = r1;
         r1 = left > 0 ? wrow_load<EPL>(row, lane, E) : 0u;
@@ -372,7 +411,7 @@ struct WRows {
 #pragma unroll
         for (int s = 0; s < EPL; ++s) {
             const uint32_t b = (r >> (8 * s)) & 0xFFu;
-            key[s] = b ? 256u - b : WKEY_SENT;
+            key[s] = b ? ((256u - b) << WKEY_SH) | (e0 + s) : WKEY_SENT;
             valid |= (b ? 1u : 0u) << s;
         }
     }
@@ -422,6 +461,7 @@ __device__ __forceinline__ void wseg_spec(const ReplayParams &P, int64_t chain, 
     rp.init(P, a0 + ws * K, lane);
     WRows<EPL> rows;
     if (POL == POL_ML) rows.init(rank + (e0 + ws) * E, ev1 - ws, E, lane);
+    uint32_t pos = (uint32_t)(ws * K);   // chain-local access position
 
     for (int64_t ev = ws; ev < ev1; ++ev) {
         if (ev == ev0) {
@@ -432,14 +472,13 @@ __device__ __forceinline__ void wseg_spec(const ReplayParams &P, int64_t chain, 
         }
         if (POL == POL_ML) rows.next(key, valid, lane);
         uint32_t pin = 0, sm = 0;
-        for (int j = 0; j < K; ++j) {
-            const int64_t A = a0 + ev * K + j;
-            const uint32_t x = rp.id(A, lane);
+        for (int j = 0; j < K; ++j, ++pos) {
+            const uint32_t x = rp.id();
             const int owner = (int)(x / EPL), slot = (int)(x % EPL);
             const uint32_t bit = 1u << slot;
             const bool mine = lane == owner;
-            const uint32_t np = POL == POL_BELADY ? rp.next(A, lane) : 0u;
-            wkey_update<EPL, POL>(key, mine, slot, (uint32_t)(ev * K + j), np);
+            const uint32_t np = POL == POL_BELADY ? rp.next() : 0u;
+            wkey_update<EPL, POL>(key, mine, slot, x, pos, np);
             uint32_t miss;
             const uint32_t code = wstep<EPL>(S, key, owner, bit, pin, valid, C, lane, n, stuck, miss);
             sm += miss;
@@ -750,17 +789,17 @@ __device__ __forceinline__ void wseg_finish(const ReplayParams &P, int64_t chain
             rp.init(P, a0 + ev0 * K, lane);
             WRows<EPL> rows;
             if (POL == POL_ML) rows.init(rank + (e0 + ev0) * E, ev1 - ev0, E, lane);
+            uint32_t pos = (uint32_t)(ev0 * K);
             while (!conv && ev < ev1) {
                 if (POL == POL_ML) rows.next(key, valid, lane);
                 uint32_t pin = 0, sma = 0, smb = 0;
-                for (int j = 0; j < K; ++j) {
-                    const int64_t Aa = a0 + ev * K + j;
-                    const uint32_t x = rp.id(Aa, lane);
+                for (int j = 0; j < K; ++j, ++pos) {
+                    const uint32_t x = rp.id();
                     const int owner = (int)(x / EPL), slot = (int)(x % EPL);
                     const uint32_t bit = 1u << slot;
                     const bool mine = lane == owner;
-                    const uint32_t np = POL == POL_BELADY ? rp.next(Aa, lane) : 0u;
-                    wkey_update<EPL, POL>(key, mine, slot, (uint32_t)(ev * K + j), np);
+                    const uint32_t np = POL == POL_BELADY ? rp.next() : 0u;
+                    wkey_update<EPL, POL>(key, mine, slot, x, pos, np);
                     uint32_t ma, mb;
                     const uint32_t codea = wstep<EPL>(A, key, owner, bit, pin, valid, C, lane, ca, stuck_a, ma);
                     const uint32_t codeb = wstep<EPL>(B, key, owner, bit, pin, valid, C, lane, cb, stuck_b, mb);
