@@ -99,31 +99,54 @@ __device__ __forceinline__ uint32_t min_key(M128 cand, const uint32_t *sk) {
     return min_key_word<BS>((uint32_t)(cand.hi >> 32), b, sk + 96 * BS);
 }
 
-// Maximum (rank << 8 | expert) over the experts of a candidate mask, rank
-// bytes of this thread's row (mlpolicy.py:15-26: arg-max score; ranks are
-// distinct, 0 = not selectable).
-__device__ __forceinline__ uint32_t max_rank_word(uint32_t w, uint32_t best, const uint8_t *row, int e0) {
+// Highest set bit of a non-empty mask.
+__device__ __forceinline__ uint32_t top_bit(uint64_t m) { return 63u - (uint32_t)__clzll((long long)m); }
+__device__ __forceinline__ uint32_t top_bit(M128 m) {
+    return m.hi ? 127u - (uint32_t)__clzll((long long)m.hi) : 63u - (uint32_t)__clzll((long long)m.lo);
+}
+
+// A candidate set in RANK space for one event: bit r - 1 for every candidate
+// of rank r >= 1 (rank-0 experts are never selectable), and ord[r - 1] = that
+// expert.  Ranks of one event are distinct, so the ML victim (arg-max score,
+// mlpolicy.py:15-26) of any subset is ord[top_bit(subset)] -- one FLO per
+// evicting miss instead of a scan of the candidates' ranks.
+template <typename M>
+__device__ __forceinline__ void rank_space_word(uint32_t w, int e0, const uint8_t *row, uint8_t *ord, M &out) {
     while (w) {
         const int i = 31 - __clz(w);
         w ^= 1u << i;
-        uint32_t k = ((uint32_t)row[i] << 8) | (uint32_t)(e0 + i);
+        const uint32_t r = row[e0 + i];
         if (w) {
             const int i2 = 31 - __clz(w);
             w ^= 1u << i2;
-            k = max(k, ((uint32_t)row[i2] << 8) | (uint32_t)(e0 + i2));
+            const uint32_t r2 = row[e0 + i2];
+            if (r2) {
+                out = out | bit_of<M>(r2 - 1u);
+                ord[r2 - 1u] = (uint8_t)(e0 + i2);
+            }
         }
-        best = max(best, k);
+        if (r) {
+            out = out | bit_of<M>(r - 1u);
+            ord[r - 1u] = (uint8_t)(e0 + i);
+        }
     }
-    return best;
 }
-__device__ __forceinline__ uint32_t max_rank(uint64_t cand, const uint8_t *row) {
-    return max_rank_word((uint32_t)(cand >> 32), max_rank_word((uint32_t)cand, 0u, row, 0), row + 32, 32);
+template <typename M>
+__device__ __forceinline__ M rank_space(M cand, const uint8_t *row, uint8_t *ord) {
+    uint32_t w[4];
+    to_words(cand, w);
+    M out = zero<M>();
+    rank_space_word(w[0], 0, row, ord, out);
+    rank_space_word(w[1], 32, row, ord, out);
+    if (sizeof(M) > 8) {
+        rank_space_word(w[2], 64, row, ord, out);
+        rank_space_word(w[3], 96, row, ord, out);
+    }
+    return out;
 }
-__device__ __forceinline__ uint32_t max_rank(M128 cand, const uint8_t *row) {
-    uint32_t b = max_rank_word((uint32_t)cand.lo, 0u, row, 0);
-    b = max_rank_word((uint32_t)(cand.lo >> 32), b, row + 32, 32);
-    b = max_rank_word((uint32_t)cand.hi, b, row + 64, 64);
-    return max_rank_word((uint32_t)(cand.hi >> 32), b, row + 96, 96);
+template <typename M>
+__device__ __forceinline__ M rank_bit(uint32_t r) {   // rank r >= 1 -> its bit, rank 0 -> none
+    return r ? bit_of<M>(r - 1u) : zero<M>();
 }
 
 // One event's rank row into a thread's shared-memory row (row stride

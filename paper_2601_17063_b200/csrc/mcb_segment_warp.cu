@@ -538,7 +538,8 @@ __global__ void __launch_bounds__(128) k_wseg_spec(const __grid_constant__ Repla
 // chains (many segments, e.g. C3's 1M-token trace): the state is a 64- or
 // 128-bit mask (mcb_mask.cuh), the packed keys (key << 7 | id) sit in shared
 // memory column-major per thread, and the victim is a minimum over the
-// candidate bits.  It writes the warp version's WSegOut records, so the warp
+// candidate bits (ML: the top bit of the event's rank-space candidate mask,
+// mcb_mask.cuh rank_space).  It writes the warp version's WSegOut records, so the warp
 // finish walk (which replays any segment whose recorded start state is not
 // the true one) is shared.
 namespace tspec {
@@ -566,6 +567,8 @@ __device__ __forceinline__ void tseg_spec(const ReplayParams &P, int64_t chain, 
     auto key = [&](int e) -> uint32_t & { return sk[e * BS]; };
     // ML: the event's rank row as bytes, [thread][mrow_stride(E)] inside the key area
     uint8_t *const mrow = (uint8_t *)(sk - threadIdx.x) + threadIdx.x * mrow_stride(E);
+    // ML: rank -> expert of the event's candidates (rank_space), [thread][E] after the rank rows
+    uint8_t *const mord = (uint8_t *)(sk - threadIdx.x) + BS * mrow_stride(E) + threadIdx.x * E;
 
     // exact keys and seen set at ws (a snapshot point)
     const int2 *sn = P.seg.snap + (chain * P.seg.n_snap + ws / MCB_SNAP_EV) * P.seg.snap_e;
@@ -636,8 +639,11 @@ __device__ __forceinline__ void tseg_spec(const ReplayParams &P, int64_t chain, 
             misses = nev = refc = comp = 0u;
             stuck = false;
         }
-        if (POL == POL_ML)   // this event's rank row (mlpolicy.py:59-62) as bytes (rank 0 = not selectable)
+        M cr = zero<M>();   // ML: resident \ pinned in rank space, kept in step with every access
+        if (POL == POL_ML) {   // this event's rank row (mlpolicy.py:59-62) as bytes (rank 0 = not selectable)
             copy_rank_row(rank + (e0 + ev) * E, mrow, E);
+            cr = rank_space(res, mrow, mord);
+        }
         M pin = zero<M>();
         uint32_t sm = 0;
         for (int j = 0; j < K; ++j) {
@@ -657,13 +663,15 @@ __device__ __forceinline__ void tseg_spec(const ReplayParams &P, int64_t chain, 
                 code = MCB_OUT_MISS;
                 if ((uint32_t)popc(res) >= C) {
                     const M cand = res & ~pin;
-                    // ML: arg-max rank over the candidates; rank 0 (no candidate selectable) = stuck
-                    const uint32_t best = !any(cand) ? 0u
-                                          : (POL == POL_ML ? max_rank(cand, mrow) : min_key<BS>(cand, sk));
-                    if (!any(cand) || (POL == POL_ML && (best >> 8) == 0u)) {
+                    // ML: the highest-ranked candidate; none with rank >= 1 (no candidate selectable) = stuck
+                    const bool none = POL == POL_ML ? !any(cr) : !any(cand);
+                    const uint32_t best = none ? 0u
+                                          : (POL == POL_ML ? (uint32_t)mord[top_bit(cr)] : min_key<BS>(cand, sk));
+                    if (none) {
                         stuck = true;
                     } else {
-                        const uint32_t v = POL == POL_ML ? (best & 0xFFu) : (best & ((1u << SH) - 1u));
+                        if (POL == POL_ML) cr = cr & ~bit_of<M>(top_bit(cr));
+                        const uint32_t v = POL == POL_ML ? best : (best & ((1u << SH) - 1u));
                         vbit = bit_of<M>(v);
                         code = v;
                         ++nev;
@@ -679,6 +687,7 @@ __device__ __forceinline__ void tseg_spec(const ReplayParams &P, int64_t chain, 
                 ring[0] = ring[0] | vbit;
                 comp += test(seen, x) ? 0u : 1u;
             }
+            if (POL == POL_ML) cr = cr & ~rank_bit<M>(mrow[x]);   // x is pinned for the rest of the event
             seen = seen | bit;
             pin = pin | bit;
             if (track && ev >= ev0) h = poly16(h, code);

@@ -15,8 +15,13 @@
 //     unless every resident expert is (pinned experts were accessed in the
 //     current event, after every other resident one);
 //   * ML keeps the event's rank row as bytes (one row per thread, four
-//     16-byte copies per event) and takes the maximum rank over the
-//     candidates (rank 0 = NaN / -inf score, never selectable).
+//     16-byte copies per event), turns resident \ pinned into a rank-space
+//     mask once per event (rank_space: bit r - 1 per candidate of rank r,
+//     plus rank -> expert bytes) and keeps it in step with every access, so
+//     each evicting miss takes the highest-ranked candidate with one FLO
+//     (rank 0 = NaN / -inf score, never selectable).  The per-miss rank scan
+//     it replaces ran once per miss under SIMT divergence (70 % of the ML
+//     launch's instructions on C4).
 // Semantics are sstep()'s (mcb_solo.cuh) on wide masks: policies.py:95-214,
 // mlpolicy.py:15-26, engine.py:229-257 (pinning), engine.py:266-297 (refetch).
 // Used when there are enough instances to fill the GPU (many traces, e.g. C4).
@@ -56,6 +61,8 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
     auto prv = [&](uint32_t e) -> uint8_t & { return lb[(E + e) * BS]; };
     uint32_t head = NIL, tail = NIL;
     uint8_t *const mrow = (uint8_t *)(sk - threadIdx.x) + threadIdx.x * mrow_stride(E);
+    // ML: rank -> expert of the event's candidates, [thread][E] after the rank rows
+    uint8_t *const mord = (uint8_t *)(sk - threadIdx.x) + BS * mrow_stride(E) + threadIdx.x * E;
 
     M res = zero<M>(), seen = zero<M>(), ring_or = zero<M>();
     M ring[WMAX + 1];
@@ -92,8 +99,11 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
             uint8_t *m = P.res_masks + (e0 + ev) * E;
             for (int e = 0; e < E; ++e) m[e] = (uint8_t)test(res, (uint32_t)e);
         }
-        if (POL == POL_ML)   // this event's rank row (mlpolicy.py:59-62)
+        M cr = zero<M>();   // ML: resident \ pinned in rank space (rank_space), kept in step below
+        if (POL == POL_ML) {   // this event's rank row (mlpolicy.py:59-62)
             copy_rank_row(rank + (e0 + ev) * E, mrow, E);
+            cr = rank_space(res, mrow, mord);
+        }
         M pin = zero<M>();
         uint32_t step_miss = 0;
         for (uint32_t j = 0; j < nacc; ++j, ++pos, ++A) {
@@ -134,11 +144,12 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
                             ++nev;
                         }
                     } else if (POL == POL_ML) {
-                        const uint32_t best = max_rank(res & ~pin, mrow);
-                        if ((best >> 8) == 0u) {   // no candidate with a selectable score
+                        if (!any(cr)) {   // no candidate with a selectable score
                             stuck = true;
                         } else {
-                            const uint32_t v = best & 0xFFu;
+                            const uint32_t r = top_bit(cr);   // the highest-ranked candidate
+                            const uint32_t v = mord[r];
+                            cr = cr & ~bit_of<M>(r);
                             vbit = bit_of<M>(v);
                             code = v;
                             ++nev;
@@ -175,6 +186,15 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
                 if (decode) ++dm; else ++pm;
             } else {
                 if (decode) ++dh; else ++ph;
+            }
+            if (POL == POL_ML) {
+                const uint32_t rx = mrow[x];
+                if (decode) {
+                    cr = cr & ~rank_bit<M>(rx);   // x is pinned for the rest of the event
+                } else if (!hit && rx != 0u) {   // a prefill insertion is a candidate
+                    cr = cr | bit_of<M>(rx - 1u);
+                    mord[rx - 1u] = (uint8_t)x;
+                }
             }
             seen = seen | bit;
             if (decode) pin = pin | bit;
