@@ -99,6 +99,43 @@ __device__ __forceinline__ uint32_t min_key(M128 cand, const uint32_t *sk) {
     return min_key_word<BS>((uint32_t)(cand.hi >> 32), b, sk + 96 * BS);
 }
 
+// The N smallest packed keys over the experts of a candidate mask, ascending
+// in low[] (~0u where there are fewer candidates): one insertion network step
+// (2N - 1 min / max) per candidate, two key loads in flight.
+template <int N>
+__device__ __forceinline__ void insert_low(uint32_t k, uint32_t (&low)[N]) {
+#pragma unroll
+    for (int q = N - 1; q >= 1; --q) low[q] = min(low[q], max(low[q - 1], k));
+    low[0] = min(low[0], k);
+}
+template <int BS, int N>
+__device__ __forceinline__ void lowest_keys_word(uint32_t w, const uint32_t *sk, uint32_t (&low)[N]) {
+    while (w) {
+        const int i = 31 - __clz(w);
+        w ^= 1u << i;
+        const uint32_t k = sk[i * BS];
+        if (w) {
+            const int i2 = 31 - __clz(w);
+            w ^= 1u << i2;
+            insert_low<N>(sk[i2 * BS], low);
+        }
+        insert_low<N>(k, low);
+    }
+}
+template <int BS, int N, typename M>
+__device__ __forceinline__ void lowest_keys(M cand, const uint32_t *sk, uint32_t (&low)[N]) {
+    uint32_t w[4];
+    to_words(cand, w);
+#pragma unroll
+    for (int q = 0; q < N; ++q) low[q] = ~0u;
+    lowest_keys_word<BS, N>(w[0], sk, low);
+    lowest_keys_word<BS, N>(w[1], sk + 32 * BS, low);
+    if (sizeof(M) > 8) {
+        lowest_keys_word<BS, N>(w[2], sk + 64 * BS, low);
+        lowest_keys_word<BS, N>(w[3], sk + 96 * BS, low);
+    }
+}
+
 // Highest set bit of a non-empty mask.
 __device__ __forceinline__ uint32_t top_bit(uint64_t m) { return 63u - (uint32_t)__clzll((long long)m); }
 __device__ __forceinline__ uint32_t top_bit(M128 m) {

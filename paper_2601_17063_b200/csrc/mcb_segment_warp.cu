@@ -548,6 +548,8 @@ constexpr int BS = 128;
 constexpr int SH = 7;
 static_assert(SH == 7, "packed keys carry 7 id bits (E <= 128)");
 constexpr uint32_t KMAX = (1u << (32 - SH)) - 1u;
+constexpr int NLOW = 4;   // smallest keys kept per event (LRU / LFU / Belady) ...
+constexpr uint32_t NLOW_MAXC = 32;   // ... for capacities up to this (as K4-wide)
 
 template <int POL, typename M>
 __device__ __forceinline__ void tseg_spec(const ReplayParams &P, int64_t chain, int seg, int pol_i, int cap_i,
@@ -644,6 +646,14 @@ __device__ __forceinline__ void tseg_spec(const ReplayParams &P, int64_t chain, 
             copy_rank_row(rank + (e0 + ev) * E, mrow, E);
             cr = rank_space(res, mrow, mord);
         }
+        // LRU / LFU / Belady: the event's victims in key order from the NLOW
+        // smallest keys of the resident set at its start (see K4-wide, mcb_wide.cu)
+        constexpr bool KEYED = POL != POL_ML;
+        uint32_t low[NLOW], lp = NLOW;
+        if (KEYED && C <= NLOW_MAXC && (uint32_t)popc(res) + (uint32_t)K > C) {
+            lowest_keys<BS, NLOW>(res, sk, low);
+            lp = 0;
+        }
         M pin = zero<M>();
         uint32_t sm = 0;
         for (int j = 0; j < K; ++j) {
@@ -664,9 +674,23 @@ __device__ __forceinline__ void tseg_spec(const ReplayParams &P, int64_t chain, 
                 if ((uint32_t)popc(res) >= C) {
                     const M cand = res & ~pin;
                     // ML: the highest-ranked candidate; none with rank >= 1 (no candidate selectable) = stuck
+                    uint32_t lk = ~0u;
+                    while (KEYED && lp < NLOW) {
+                        uint32_t k = low[0];
+#pragma unroll
+                        for (int q = 1; q < NLOW; ++q) k = lp == (uint32_t)q ? low[q] : k;
+                        ++lp;
+                        if (k == ~0u) {   // the start-of-event resident set is used up
+                            lp = NLOW;
+                        } else if (!test(pin, k & ((1u << SH) - 1u))) {
+                            lk = k;
+                            break;
+                        }
+                    }
                     const bool none = POL == POL_ML ? !any(cr) : !any(cand);
                     const uint32_t best = none ? 0u
-                                          : (POL == POL_ML ? (uint32_t)mord[top_bit(cr)] : min_key<BS>(cand, sk));
+                                          : (POL == POL_ML ? (uint32_t)mord[top_bit(cr)]
+                                                           : (lk != ~0u ? lk : min_key<BS>(cand, sk)));
                     if (none) {
                         stuck = true;
                     } else {

@@ -43,6 +43,9 @@ static_assert(SH == 7, "packed keys carry 7 id bits (E <= 128)");
 constexpr uint32_t KMAX = (1u << (32 - SH)) - 1u;
 
 constexpr uint32_t NIL = 0xFFu;   // end of the LRU list
+constexpr int NLOW = 4;           // smallest keys kept per event (LFU / Belady / FIFO)
+constexpr uint32_t NLOW_MAXC = 32;   // ... for capacities up to this (a larger resident set costs more to
+                                     // select from per event than the few evicting misses it serves: C5)
 
 template <int POL, bool UNIFORM, int WMAX, typename M>
 __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t chain, int pol_i, int cap_i,
@@ -104,6 +107,20 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
             copy_rank_row(rank + (e0 + ev) * E, mrow, E);
             cr = rank_space(res, mrow, mord);
         }
+        // LFU / Belady / FIFO in a decode event: a candidate's key cannot change
+        // within the event (only accessed experts' keys change, and an accessed
+        // expert is pinned from then on), so the event's victims come in key
+        // order from the NLOW smallest keys of the resident set at its start,
+        // skipping experts pinned since -- one uniform pass per event instead of
+        // a candidate scan per evicting miss (which SIMT divergence paid at
+        // almost every access).  More victims than that, or a prefill event,
+        // take the scan.
+        constexpr bool KEYED = POL == POL_LFU || POL == POL_BELADY || POL == POL_FIFO;
+        uint32_t low[NLOW], lp = NLOW;
+        if (KEYED && decode && C <= NLOW_MAXC && (uint32_t)popc(res) + nacc > C) {
+            lowest_keys<BS, NLOW>(res, sk, low);
+            lp = 0;
+        }
         M pin = zero<M>();
         uint32_t step_miss = 0;
         for (uint32_t j = 0; j < nacc; ++j, ++pos, ++A) {
@@ -155,11 +172,24 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
                             ++nev;
                         }
                     } else {
+                        uint32_t best = ~0u;
+                        while (KEYED && lp < NLOW) {
+                            uint32_t k = low[0];
+#pragma unroll
+                            for (int q = 1; q < NLOW; ++q) k = lp == (uint32_t)q ? low[q] : k;
+                            ++lp;
+                            if (k == ~0u) {   // the start-of-event resident set is used up
+                                lp = NLOW;
+                            } else if (!test(pin, k & ((1u << SH) - 1u))) {
+                                best = k;
+                                break;
+                            }
+                        }
                         M cand = res & ~pin & valid;
-                        if (!any(cand)) {
+                        if (best == ~0u && any(cand)) best = min_key<BS>(cand, sk);
+                        if (best == ~0u) {
                             stuck = true;
                         } else {
-                            const uint32_t best = min_key<BS>(cand, sk);
                             const uint32_t v = best & ((1u << SH) - 1u);
                             vbit = bit_of<M>(v);
                             code = v;
