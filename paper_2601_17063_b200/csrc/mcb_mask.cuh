@@ -198,6 +198,17 @@ __device__ __forceinline__ void copy_rank_row(const uint8_t *src, uint8_t *dst, 
     }
 }
 
+// The same copy issued asynchronously (cp.async.cg, 16 bytes per op, no
+// registers), so the next event's row is in flight while this one is used;
+// E % 16 == 0 only.  rank_row_wait() before reading the row.
+__device__ __forceinline__ void rank_row_async(const uint8_t *src, uint8_t *dst, int E) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    for (int q = 0; q < E / 16; ++q)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d + 16 * q), "l"(src + 16 * q) : "memory");
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void rank_row_wait() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 // ML keys of one event for a thread's column of shared-memory keys
 // (keys[e * 128]): key = (256 - rank) << 7 | e, selectable iff rank != 0
 // (mlpolicy.py:15-26).  Rows of a multiple of 16 experts are 16-byte aligned

@@ -63,9 +63,15 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
     auto nxt = [&](uint32_t e) -> uint8_t & { return lb[e * BS]; };
     auto prv = [&](uint32_t e) -> uint8_t & { return lb[(E + e) * BS]; };
     uint32_t head = NIL, tail = NIL;
-    uint8_t *const mrow = (uint8_t *)(sk - threadIdx.x) + threadIdx.x * mrow_stride(E);
+    uint8_t *const mrow0 = (uint8_t *)(sk - threadIdx.x) + threadIdx.x * mrow_stride(E);
     // ML: rank -> expert of the event's candidates, [thread][E] after the rank rows
     uint8_t *const mord = (uint8_t *)(sk - threadIdx.x) + BS * mrow_stride(E) + threadIdx.x * E;
+    // ML with E % 16 == 0 (and E >= 32, so it fits the key area): two rank-row
+    // buffers after the rank -> expert bytes, the next event's row copied
+    // asynchronously while this one is used (its load latency is otherwise
+    // exposed once per event when few instances share an SM)
+    const bool ml_async = POL == POL_ML && (E & 15) == 0 && E >= 32;
+    uint8_t *const mrow1 = (uint8_t *)(sk - threadIdx.x) + BS * (mrow_stride(E) + E) + threadIdx.x * mrow_stride(E);
 
     M res = zero<M>(), seen = zero<M>(), ring_or = zero<M>();
     M ring[WMAX + 1];
@@ -91,6 +97,7 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
     if (POL == POL_BELADY) nx.init(P.next_pos, a0, a_end);
     int64_t A = a0;
     uint32_t pos = 0;
+    if (ml_async && n_ev > 0) rank_row_async(rank + e0 * E, mrow0, E);
     for (int64_t ev = 0; ev < n_ev; ++ev) {
         const uint32_t info = UNIFORM ? mcb_ev_pack((uint32_t)tr.K, (uint32_t)tr.K, true, ev == 0)
                                       : __ldg(tr.ev_info + e0 + ev);
@@ -103,8 +110,14 @@ __device__ __forceinline__ void wide_instance(const ReplayParams &P, int64_t cha
             for (int e = 0; e < E; ++e) m[e] = (uint8_t)test(res, (uint32_t)e);
         }
         M cr = zero<M>();   // ML: resident \ pinned in rank space (rank_space), kept in step below
+        uint8_t *const mrow = (ml_async && (ev & 1)) ? mrow1 : mrow0;
         if (POL == POL_ML) {   // this event's rank row (mlpolicy.py:59-62)
-            copy_rank_row(rank + (e0 + ev) * E, mrow, E);
+            if (ml_async) {
+                rank_row_wait();
+                if (ev + 1 < n_ev) rank_row_async(rank + (e0 + ev + 1) * E, (ev & 1) ? mrow0 : mrow1, E);
+            } else {
+                copy_rank_row(rank + (e0 + ev) * E, mrow, E);
+            }
             cr = rank_space(res, mrow, mord);
         }
         // LFU / Belady / FIFO in a decode event: a candidate's key cannot change
