@@ -1982,29 +1982,25 @@ __global__ void __launch_bounds__(256, 3) k_rescore(DevTrace tr, const double *_
                     f[j] = e < E ? sp[E + e] : 0;
                 }
                 // the tile's events up to and including this one (features.py:34-39):
-                // lane l holds the routed set of event j0 + l as a 128-bit mask; one
-                // ballot per expert gives that expert's occurrence mask over the prefix
+                // lane l ORs bit l into the occurrence word of each expert event
+                // j0 + l routes (shared-memory atomics into this warp's 128 words of
+                // the rank staging, free until the ranking), then lane l reads the
+                // occurrence masks of experts l + 32 w
                 const int64_t j0 = s32 * MCB_TILE_EV;
                 const int nprefix = (int)(i - j0) + 1;
-                uint32_t mine[4] = {0u, 0u, 0u, 0u};
+                uint32_t *so = (uint32_t *)s_rank + warp * MCB_MAX_EXPERTS;
+#pragma unroll
+                for (int w = 0; w < 4; ++w) so[lane + 32 * w] = 0u;
+                __syncwarp();
                 if (lane < nprefix) {
                     const uint8_t *ids = tr.acc + (c * tr.T + j0 + lane) * tr.K;
-                    for (int k = 0; k < tr.K; ++k) {
-                        const int x = __ldg(ids + k);
-                        const uint32_t bit = 1u << (x & 31);
-#pragma unroll
-                        for (int w = 0; w < 4; ++w) mine[w] |= (x >> 5) == w ? bit : 0u;
-                    }
+                    for (int k = 0; k < tr.K; ++k) atomicOr(so + __ldg(ids + k), 1u << lane);
                 }
-                uint32_t occ[4] = {0u, 0u, 0u, 0u};   // lane l: occurrence masks of experts l + 32 w
+                __syncwarp();
+                uint32_t occ[4];   // lane l: occurrence masks of experts l + 32 w
 #pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                    if (32 * w >= E) break;
-                    for (int l = 0; l < 32; ++l) {
-                        const uint32_t m = __ballot_sync(FULL_MASK, (mine[w] >> l) & 1u);
-                        occ[w] = lane == l ? m : occ[w];
-                    }
-                }
+                for (int w = 0; w < 4; ++w) occ[w] = so[lane + 32 * w];
+                __syncwarp();   // read before the warp's next event clears the words
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
                     if (occ[j]) {
