@@ -159,16 +159,27 @@ def zipf_ids(n, L, T, K, E, seed):
     return np.take_along_axis(np.broadcast_to(perm[None, :, None, :], (n, L, T, E)), top, axis=-1).astype(np.uint8)
 
 
-@pytest.mark.parametrize("shape", ["c4", "c5"])
+@pytest.mark.parametrize("shape", ["c4", "c5", "stress32", "stress40", "stress48"])
 def test_many_trace_wide_replay(shape):
     """Many-trace batches, C4-shaped (L=27, E=64, K=6) and C5-shaped (L=48,
     E=128, K=8): the thread-per-instance replay for 16 < E <= 128
     (k_replay_wide, 64- / 128-bit masks) against the warp-per-instance kernel
-    on every chain, and sampled chains against the oracle."""
+    on every chain, and sampled chains against the oracle.  The stress shapes
+    put up to K = 8 evicting misses in one event at C = K (more victims than
+    the 4 start-of-event keys K4-wide keeps, so the scan fallback and the
+    pinned-expert skips run constantly), straddle the C <= 32 gate of that
+    selection, and cover rank rows copied asynchronously (E % 16 == 0) and
+    byte-wise (E = 40)."""
     if shape == "c4":
         n, L, E, K, T, caps = 64, 27, 64, 6, 512, [16, 24]
-    else:
+    elif shape == "c5":
         n, L, E, K, T, caps = 24, 48, 128, 8, 384, [16, 40, 96]
+    elif shape == "stress32":
+        n, L, E, K, T, caps = 48, 4, 32, 8, 256, [8, 9, 12, 32]
+    elif shape == "stress40":
+        n, L, E, K, T, caps = 48, 4, 40, 8, 256, [8, 20, 33]
+    else:
+        n, L, E, K, T, caps = 48, 4, 48, 8, 256, [8, 31, 33]
     ids = zipf_ids(n, L, T, K, E, seed=4)
     packed = mcb.packed_from_decode_ids(ids, E)
     nets = oracle.nets_from_spec({"kind": "per_layer_seed"}, L, E)
